@@ -1,0 +1,191 @@
+/*
+ * occult.h — C-ABI of the B200-native Occult expert-parallel MoE layer.
+ *
+ * Drop-in boundary for the reference's C++ library API (moesim, namespace
+ * `moesim`; /root/reference/proj/include/moesim/*.hpp).  Every entry point
+ * below names the reference interface it replaces.  The reference is a
+ * header-level C++ library with value semantics and exceptions; this ABI is
+ * plain C: device buffers are caller-owned raw pointers, every call is
+ * ordered on the caller's CUDA stream, and errors are returned as
+ * `occ_status` values that map 1:1 onto the reference's exception taxonomy
+ * (common.hpp:11-34).  Nothing throws across the ABI.
+ *
+ * Layout conventions (row-major everywhere, like moesim::Matrix):
+ *   tokens   x       [n, D]       bf16
+ *   routing  ids     [n, k]       int32, weights [n, k] f32 (f64 for *_f64)
+ *   experts  w1, w3  [E_l, D, F]  bf16  (reference ExpertWeights::w1, D x H)
+ *            w2      [E_l, F, D]  bf16  (reference ExpertWeights::w2, H x D)
+ *   placement        [N_d, P]     int32, P = E / N_d, list order significant
+ *                                 (reference Placement::devices)
+ *
+ * One handle per GPU.  A handle with world_size == 1 hosts all N_d logical
+ * EP devices on one GPU exactly as the reference simulates them in one
+ * process (pipeline.cpp:393-466); with world_size == N_d each rank is one
+ * EP device and the two exchanges run over NCCL.  Handles are not
+ * thread-safe.
+ */
+#ifndef OCCULT_H
+#define OCCULT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* occ_stream_t; /* == cudaStream_t */
+
+/* Status codes; 1..6 mirror moesim::{Shape,Config,Placement,Routing,
+ * Capacity,State}Error (common.hpp:11-28). */
+typedef enum {
+    OCC_OK = 0,
+    OCC_ERR_SHAPE = 1,
+    OCC_ERR_CONFIG = 2,
+    OCC_ERR_PLACEMENT = 3,
+    OCC_ERR_ROUTING = 4,
+    OCC_ERR_CAPACITY = 5,
+    OCC_ERR_STATE = 6,
+    OCC_ERR_CUDA = 10,
+    OCC_ERR_NCCL = 11,
+    OCC_ERR_ARG = 12,
+    OCC_ERR_UNSUPPORTED = 13
+} occ_status;
+
+/* moesim::Activation (config.hpp:10) + the gated SwiGLU extension
+ * (silu(x w1) * (x w3); not in the reference). */
+typedef enum { OCC_ACT_IDENTITY = 0, OCC_ACT_SILU = 1, OCC_ACT_RELU = 2, OCC_ACT_SWIGLU = 3 } occ_activation;
+
+/* moesim::PruneMode / ReplacementWeightPolicy (pruning.hpp:14-18). */
+typedef enum { OCC_PRUNE_NONE = 0, OCC_PRUNE_ROUTER = 1, OCC_PRUNE_SIMILARITY = 2 } occ_prune_mode;
+
+/* Router / layer config — replaces moesim::MoEConfig (config.hpp:12-28). */
+typedef struct {
+    int num_experts;  /* E */
+    int top_k;        /* k */
+    int num_devices;  /* N_d: EP degree (logical devices) */
+    int embed_dim;    /* D */
+    int hidden_dim;   /* F (reference: H) */
+    int renormalize;  /* renormalise top-k weights (MoEConfig::renormalize) */
+    int activation;   /* occ_activation */
+    int dedup;        /* 1: Occult dispatch, one copy per (token, device);
+                         0: naive replicate-k baseline, one copy per (token, expert) */
+} occ_config;
+
+/* Pruning knob — replaces moesim::PruneSpec (pruning.hpp:32-39).  The
+ * similarity table is attached separately (occ_set_similarity). */
+typedef struct {
+    int mode;          /* occ_prune_mode */
+    int device_budget; /* max devices a token's experts may span */
+    int own_score;     /* 1: ReplacementWeightPolicy::OwnScore, 0: Inherit */
+} occ_prune;
+
+/* Communication accounting — replaces moesim::CommReport (collab.hpp:36-43)
+ * for the last occ_forward call, plus the naive top-k comparison. */
+typedef struct {
+    double mean_replicas;             /* E(C_T): mean per-token device span */
+    double cap_replicas;              /* min(k, N_d) or the prune budget */
+    double intra_share, inter_share;  /* co-activated pair shares */
+    long long cross_device_bytes;     /* dispatch rows crossing devices x D x bytes_per_scalar */
+    long long crossing_rows;          /* Occult (dedup) rows leaving their source device */
+    long long naive_crossing_rows;    /* replicate-k rows that would leave their source */
+    long long n_sfd;                  /* total Sfd rows (sum over sources) */
+    long long n_epd;                  /* total Epd rows */
+    long long per_device_rows[64];    /* Sfd rows received per device (CommReport::per_device_token_counts) */
+} occ_comm_report;
+
+typedef struct occ_handle occ_handle;
+
+/* ------------------------------------------------------------ lifecycle */
+/* Validates like MoEConfig::validate (core.cpp:10-23) + Placement::validate
+ * (placement.cpp:32-45).  placement is a HOST pointer [N_d * P]. */
+occ_status occ_create(const occ_config* cfg, const int32_t* placement, int world_size, int rank, occ_handle** out);
+occ_status occ_destroy(occ_handle* h);
+/* Replace the expert-placement table (e.g. after occ_reschedule_placement).
+ * Must be followed by occ_load_experts. HOST pointer. */
+occ_status occ_set_placement(occ_handle* h, const int32_t* placement);
+/* Resident expert weights, reference layout (token.hpp:30-44), DEVICE
+ * pointers.  world_size == 1: all E experts in expert-id order.
+ * world_size > 1: this rank's P local experts in placement-list order.
+ * w3 is required iff activation == OCC_ACT_SWIGLU, else NULL. */
+occ_status occ_load_experts(occ_handle* h, const void* w1, const void* w3, const void* w2, occ_stream_t stream);
+/* Squared-cosine similarity table (SimilarityTable::values, pruning.hpp:25-30),
+ * HOST pointer [E * E]; the per-expert ranking is built as the reference does. */
+occ_status occ_set_similarity(occ_handle* h, const double* values);
+
+/* Validation (default on): synchronise at the end of occ_route/occ_forward
+ * and report RoutingError/CapacityError/ShapeError found on the device.
+ * Off: fully asynchronous and CUDA-graph capturable. */
+occ_status occ_set_validate(occ_handle* h, int on);
+
+/* NCCL plumbing for world_size > 1 (one process per GPU). */
+occ_status occ_comm_unique_id(void* id128);
+occ_status occ_comm_init(occ_handle* h, const void* id128);
+
+/* -------------------------------------------------------------- routing */
+/* gate_scores (routing.cpp:33-52), exact fp64 mode: logits accumulated
+ * sequentially in ascending k without FMA, softmax with max subtraction. */
+occ_status occ_gate_scores_f64(const double* x, int n, int d, const double* gate, int e, double* scores,
+                               occ_stream_t stream);
+/* topk_route (routing.cpp:60-84): (score desc, index asc), optional
+ * renormalisation; bit-exact with the reference. */
+occ_status occ_topk_route_f64(const double* scores, int n, int e, int k, int renormalize, int32_t* ids,
+                              double* weights, occ_stream_t stream);
+/* prune_routing (pruning.cpp:141-163) on fp64 scores; bit-exact.
+ * Per-token CapacityError is reported through the return status. */
+occ_status occ_prune_routing_f64(occ_handle* h, const double* scores, const int32_t* ids_in, const double* w_in,
+                                 int n, const occ_prune* prune, int32_t* ids, double* weights, occ_stream_t stream);
+/* Production router (forward_expert_parallel's routing stage,
+ * pipeline.cpp:509-512): logits = x g^T (bf16 in, f32 accumulate),
+ * softmax, top-k, renormalise, optional pruning (prune may be NULL).
+ * scores (nullable, [n, E] f32) receives the softmax rows. */
+occ_status occ_route(occ_handle* h, const void* x, const void* gate, int n, const occ_prune* prune, int32_t* ids,
+                     float* weights, float* scores, occ_stream_t stream);
+
+/* ------------------------------------------------------------- EP path */
+/* build_dispatch_index (pipeline.cpp:24-50) for every source at once.
+ * sources: [n] device of each token (NULL = round_robin_sources,
+ * pipeline.cpp:12-16).  brim0 (nullable): concatenation over sources s of
+ * the N_d x n_s BRIM0 matrices; counts (nullable): [N_d * N_d] Sfd rows
+ * per (source, destination). */
+occ_status occ_build_dispatch(occ_handle* h, const int32_t* ids, const int32_t* sources, int n, int32_t* brim0,
+                              int32_t* counts, occ_stream_t stream);
+/* forward_given_routing (pipeline.cpp:360-501): dispatch -> exchange ->
+ * grouped expert FFN -> intra-device partial combine -> return exchange ->
+ * combine.  world_size == 1: x/out hold all n tokens, sources as above.
+ * world_size > 1: x/out hold this rank's n tokens (sources ignored). */
+occ_status occ_forward(occ_handle* h, const void* x, const int32_t* ids, const float* weights,
+                       const int32_t* sources, int n, void* out, occ_stream_t stream);
+/* forward_expert_parallel (pipeline.cpp:503-517): occ_route + occ_forward. */
+occ_status occ_forward_expert_parallel(occ_handle* h, const void* x, const void* gate, const occ_prune* prune,
+                                       const int32_t* sources, int n, void* out, occ_stream_t stream);
+/* CommReport of the last forward (synchronises the stream).
+ * bytes_per_scalar as in forward_given_routing's argument. */
+occ_status occ_comm_report_get(occ_handle* h, int bytes_per_scalar, occ_comm_report* rep, occ_stream_t stream);
+/* Saved index state of the last forward (ForwardState, pipeline.hpp:155-165),
+ * DEVICE pointers, each nullable:
+ *   inbox_token/source/slot [sum_d R_d]  (DeviceInbox::token/source/source_slot)
+ *   cindex [sum_d P x R_d]                (ShardRecord::cindex, BRIM1, unpadded counters) */
+occ_status occ_saved_index(occ_handle* h, int32_t* inbox_token, int32_t* inbox_source, int32_t* inbox_slot,
+                           int32_t* cindex, occ_stream_t stream);
+
+/* ----------------------------------------------- collaboration profiling */
+/* accumulate_collab (collab.cpp:10-23): counts [E, E] int64 DEVICE buffer,
+ * accumulated in place. */
+occ_status occ_coactivation_histogram(const int32_t* ids, int n, int k, int e, int64_t* counts, occ_stream_t stream);
+/* normalize_graph (collab.cpp:31-39), HOST buffers. */
+occ_status occ_normalize_graph(const int64_t* counts, int e, double* p);
+/* reschedule_placement (placement.cpp:88-148, Alg. 1), HOST buffers; bit-exact. */
+occ_status occ_reschedule_placement(const double* p, int e, int num_devices, int32_t* placement);
+/* Sum the histogram across ranks (world_size > 1; ncclAllReduce). */
+occ_status occ_allreduce_histogram(occ_handle* h, int64_t* counts, occ_stream_t stream);
+
+/* Human-readable message of the last error on this thread. */
+const char* occ_last_error(void);
+/* Kernel launches issued by this process so far (for launch accounting). */
+long long occ_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OCCULT_H */

@@ -1,0 +1,428 @@
+"""Host-side mirror of the reference's C++ API (namespace ``moesim``) over the
+C-ABI in ``include/occult.h`` (``libocc.so``, sm_100a).
+
+Names, argument meaning and error behaviour follow the reference headers
+(/root/reference/proj/include/moesim/*.hpp) so callers and parity tests read
+like the reference's own; tensors are torch CUDA tensors (PyTorch provides
+device memory and streams only — every op below runs in this package's CUDA
+kernels).  There is no CPU fallback: importing on a machine without the
+built library, or calling without a GPU, raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libocc.so")
+
+# ---------------------------------------------------------------- errors ---
+# common.hpp:11-34 taxonomy; occ_status 1..6.
+
+
+class MoesimError(RuntimeError):
+    pass
+
+
+class ShapeError(MoesimError):
+    pass
+
+
+class ConfigError(MoesimError):
+    pass
+
+
+class PlacementError(MoesimError):
+    pass
+
+
+class RoutingError(MoesimError):
+    pass
+
+
+class CapacityError(MoesimError):
+    pass
+
+
+class StateError(MoesimError):
+    pass
+
+
+class DeviceError(MoesimError):
+    """CUDA / NCCL failure or unsupported configuration on the B200 path."""
+
+
+_STATUS = {1: ShapeError, 2: ConfigError, 3: PlacementError, 4: RoutingError, 5: CapacityError, 6: StateError}
+
+ACT = {"identity": 0, "silu": 1, "relu": 2, "swiglu": 3}
+PRUNE = {"none": 0, "router": 1, "similarity": 2}
+
+
+class _Config(C.Structure):
+    _fields_ = [(n, C.c_int) for n in ("num_experts", "top_k", "num_devices", "embed_dim", "hidden_dim",
+                                       "renormalize", "activation", "dedup")]
+
+
+class _Prune(C.Structure):
+    _fields_ = [("mode", C.c_int), ("device_budget", C.c_int), ("own_score", C.c_int)]
+
+
+class _Report(C.Structure):
+    _fields_ = [("mean_replicas", C.c_double), ("cap_replicas", C.c_double), ("intra_share", C.c_double),
+                ("inter_share", C.c_double), ("cross_device_bytes", C.c_longlong), ("crossing_rows", C.c_longlong),
+                ("naive_crossing_rows", C.c_longlong), ("n_sfd", C.c_longlong), ("n_epd", C.c_longlong),
+                ("per_device_rows", C.c_longlong * 64)]
+
+
+EXPORTS = (
+    "occ_create", "occ_destroy", "occ_set_placement", "occ_load_experts", "occ_set_similarity", "occ_set_validate",
+    "occ_comm_unique_id", "occ_comm_init", "occ_gate_scores_f64", "occ_topk_route_f64", "occ_prune_routing_f64",
+    "occ_route", "occ_build_dispatch", "occ_forward", "occ_forward_expert_parallel", "occ_comm_report_get",
+    "occ_saved_index", "occ_coactivation_histogram", "occ_normalize_graph", "occ_reschedule_placement",
+    "occ_allreduce_histogram", "occ_last_error", "occ_launch_count",
+)
+
+_LIB = None
+
+
+def lib():
+    """Load libocc.so (built in-tree by ``__graft_entry__.build()``). Fails loudly."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = C.CDLL(LIB_PATH)
+        L.occ_last_error.restype = C.c_char_p
+        L.occ_launch_count.restype = C.c_longlong
+        _LIB = L
+    return _LIB
+
+
+def _check(rc, what=""):
+    if rc != 0:
+        msg = lib().occ_last_error().decode(errors="replace")
+        raise _STATUS.get(rc, DeviceError)(f"{what}: {msg} (status {rc})")
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _need_cuda(*ts):
+    for t in ts:
+        if t is not None and not t.is_cuda:
+            raise DeviceError("B200 path: tensors must live on the GPU (no CPU fallback)")
+
+
+def launch_count() -> int:
+    return int(lib().occ_launch_count())
+
+# ------------------------------------------------------------ config types --
+
+
+@dataclass
+class MoEConfig:
+    """config.hpp:12-28 (``tiles``/``seed``/``precision`` have no GPU meaning:
+    the device path is bf16 storage with fp32 accumulation)."""
+
+    num_experts: int
+    top_k: int
+    num_devices: int = 1
+    embed_dim: int = 0
+    hidden_dim: int = 0
+    renormalize: bool = True
+    activation: str = "identity"
+    dedup: bool = True
+
+    def experts_per_device(self) -> int:
+        return self.num_experts // self.num_devices
+
+    def _c(self):
+        return _Config(self.num_experts, self.top_k, self.num_devices, self.embed_dim, self.hidden_dim,
+                       int(self.renormalize), ACT[self.activation], int(self.dedup))
+
+
+@dataclass
+class Placement:
+    """placement.hpp:14-25: per-device expert lists, list order significant."""
+
+    devices: list
+
+    def num_devices(self) -> int:
+        return len(self.devices)
+
+    def num_experts(self) -> int:
+        return sum(len(d) for d in self.devices)
+
+    def expert_to_device(self):
+        n = self.num_experts()
+        dev = [-1] * n
+        for d, lst in enumerate(self.devices):
+            for e in lst:
+                if e < 0 or e >= n or dev[e] >= 0:
+                    raise PlacementError(f"placement: device lists are not a partition of [0, {n})")
+                dev[e] = d
+        return dev
+
+    def flat(self):
+        return [e for d in self.devices for e in d]
+
+
+def trivial_placement(num_experts: int, num_devices: int) -> Placement:
+    """placement.cpp:47-58."""
+    if num_devices < 1 or num_experts < 1 or num_experts % num_devices:
+        raise ConfigError("trivial_placement: num_experts must be a positive multiple of num_devices")
+    per = num_experts // num_devices
+    return Placement([list(range(d * per, (d + 1) * per)) for d in range(num_devices)])
+
+
+@dataclass
+class PruneSpec:
+    """pruning.hpp:32-39 (the similarity table is given as its E x E values)."""
+
+    mode: str = "none"
+    device_budget: int = 1
+    table: Optional[Sequence[float]] = None
+    weight_policy: str = "inherit"
+
+    def _c(self):
+        return _Prune(PRUNE[self.mode], self.device_budget, int(self.weight_policy == "own"))
+
+
+@dataclass
+class CommReport:
+    """collab.hpp:36-43 + naive top-k comparison."""
+
+    mean_replicas: float = 0.0
+    cap_replicas: float = 0.0
+    intra_share: float = 0.0
+    inter_share: float = 0.0
+    cross_device_bytes: int = 0
+    crossing_rows: int = 0
+    naive_crossing_rows: int = 0
+    n_sfd: int = 0
+    n_epd: int = 0
+    per_device_token_counts: list = field(default_factory=list)
+
+
+# -------------------------------------------------------------- the layer ---
+
+
+class ExpertParallelLayer:
+    """One handle of the C-ABI: router config + placement table + resident
+    experts (+ optional similarity table), the drop-in for
+    forward_given_routing / forward_expert_parallel (pipeline.hpp:178-189)."""
+
+    def __init__(self, config: MoEConfig, placement: Optional[Placement] = None, world_size: int = 1, rank: int = 0):
+        self.config = config
+        self.placement = placement or trivial_placement(config.num_experts, config.num_devices)
+        if self.placement.num_devices() != config.num_devices:
+            raise ConfigError("placement device count disagrees with the config")
+        if self.placement.num_experts() != config.num_experts:
+            raise PlacementError(f"placement: covers {self.placement.num_experts()} experts, expected {config.num_experts}")
+        per = {len(d) for d in self.placement.devices}
+        if len(per) != 1:
+            raise PlacementError("placement: uneven device lists")
+        self.placement.expert_to_device()
+        cfg = config._c()
+        pl = (C.c_int32 * config.num_experts)(*self.placement.flat())
+        h = C.c_void_p()
+        _check(lib().occ_create(C.byref(cfg), pl, world_size, rank, C.byref(h)), "occ_create")
+        self._h = h
+        self._prune_cache = None
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and _LIB is not None:
+            _LIB.occ_destroy(h)
+            self._h = None
+
+    # weights (reference layout: w1 [E, D, F], w3 [E, D, F], w2 [E, F, D]) --------
+    def load_experts(self, w1: torch.Tensor, w2: torch.Tensor, w3: Optional[torch.Tensor] = None):
+        _need_cuda(w1, w2, w3)
+        ts = [t.to(torch.bfloat16).contiguous() if t is not None else None for t in (w1, w3, w2)]
+        _check(lib().occ_load_experts(self._h, _ptr(ts[0]), _ptr(ts[1]), _ptr(ts[2]), _stream()), "load_experts")
+        torch.cuda.current_stream().synchronize()
+        self._weights = ts
+
+    def set_placement(self, placement: Placement):
+        pl = (C.c_int32 * self.config.num_experts)(*placement.flat())
+        _check(lib().occ_set_placement(self._h, pl), "set_placement")
+        self.placement = placement
+
+    def set_similarity(self, values):
+        import numpy as np
+        v = np.ascontiguousarray(values, dtype=np.float64)
+        _check(lib().occ_set_similarity(self._h, v.ctypes.data_as(C.c_void_p)), "set_similarity")
+
+    def set_validate(self, on: bool):
+        _check(lib().occ_set_validate(self._h, int(on)), "set_validate")
+
+    # routing ------------------------------------------------------------------
+    def route(self, x: torch.Tensor, gate: torch.Tensor, prune: Optional[PruneSpec] = None, want_scores=False):
+        """Production router: ids int32 [n,k], weights f32 [n,k] (+ scores)."""
+        _need_cuda(x, gate)
+        n = x.shape[0]
+        k = self.config.top_k
+        ids = torch.empty((n, k), dtype=torch.int32, device=x.device)
+        w = torch.empty((n, k), dtype=torch.float32, device=x.device)
+        sc = torch.empty((n, self.config.num_experts), dtype=torch.float32, device=x.device) if want_scores else None
+        pr = self._prune(prune)
+        _check(lib().occ_route(self._h, _ptr(x.contiguous()), _ptr(gate.contiguous()), n,
+                               C.byref(pr) if pr else None, _ptr(ids), _ptr(w), _ptr(sc), _stream()), "route")
+        return (ids, w, sc) if want_scores else (ids, w)
+
+    def _prune(self, prune):
+        if prune is None or prune.mode == "none":
+            return None
+        if prune.mode == "similarity" and prune.table is not None and self._prune_cache is not prune.table:
+            self.set_similarity(prune.table)
+            self._prune_cache = prune.table
+        return prune._c()
+
+    def prune_routing(self, scores: torch.Tensor, ids: torch.Tensor, w: torch.Tensor, prune: PruneSpec):
+        """prune_routing (pruning.cpp:141-163) on fp64 scores, bit-exact."""
+        _need_cuda(scores, ids, w)
+        oi = torch.empty_like(ids)
+        ow = torch.empty_like(w)
+        pr = self._prune(prune) or _Prune(0, 1, 0)
+        _check(lib().occ_prune_routing_f64(self._h, _ptr(scores), _ptr(ids), _ptr(w), ids.shape[0], C.byref(pr),
+                                           _ptr(oi), _ptr(ow), _stream()), "prune_routing")
+        return oi, ow
+
+    # EP path -------------------------------------------------------------------
+    def build_dispatch_index(self, ids: torch.Tensor, sources: Optional[torch.Tensor] = None):
+        """BRIM0 of every source (pipeline.cpp:24-50) + the (source, dest) counts."""
+        _need_cuda(ids, sources)
+        n = ids.shape[0]
+        nd = self.config.num_devices
+        brim0 = torch.empty(n * nd, dtype=torch.int32, device=ids.device)
+        counts = torch.empty((nd, nd), dtype=torch.int32, device=ids.device)
+        _check(lib().occ_build_dispatch(self._h, _ptr(ids.contiguous()), _ptr(sources), n, _ptr(brim0),
+                                        _ptr(counts), _stream()), "build_dispatch")
+        return brim0, counts
+
+    def forward_given_routing(self, x: torch.Tensor, ids: torch.Tensor, w: torch.Tensor,
+                              sources: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None):
+        """pipeline.cpp:360-501 (values) — returns the Ori-order output."""
+        _need_cuda(x, ids, w, sources)
+        if x.dtype != torch.bfloat16:
+            raise ShapeError("forward: tokens must be bf16")
+        n = x.shape[0]
+        if ids.shape[0] != n:
+            raise ShapeError("forward: routing token count mismatch")
+        if x.shape[1] != self.config.embed_dim:
+            raise ShapeError("forward: token width != expert input width")
+        if sources is not None and sources.shape[0] != n:
+            raise ShapeError("forward: one source device per token required")
+        if out is None:
+            out = torch.empty_like(x)
+        _check(lib().occ_forward(self._h, _ptr(x), _ptr(ids), _ptr(w.float().contiguous()) if w.dtype != torch.float32 else _ptr(w),
+                                 _ptr(sources), n, _ptr(out), _stream()), "forward")
+        return out
+
+    def forward_expert_parallel(self, x, gate, prune: Optional[PruneSpec] = None, sources=None, out=None):
+        """pipeline.cpp:503-517: route (+prune) then the indexed data path."""
+        _need_cuda(x, gate, sources)
+        if out is None:
+            out = torch.empty_like(x)
+        pr = self._prune(prune)
+        _check(lib().occ_forward_expert_parallel(self._h, _ptr(x), _ptr(gate), C.byref(pr) if pr else None,
+                                                 _ptr(sources), x.shape[0], _ptr(out), _stream()), "forward_ep")
+        return out
+
+    def comm_report(self, bytes_per_scalar: int = 4, cap_replicas: Optional[float] = None) -> CommReport:
+        r = _Report()
+        _check(lib().occ_comm_report_get(self._h, bytes_per_scalar, C.byref(r), _stream()), "comm_report")
+        nd = self.config.num_devices
+        return CommReport(r.mean_replicas, r.cap_replicas if cap_replicas is None else cap_replicas, r.intra_share,
+                          r.inter_share, r.cross_device_bytes, r.crossing_rows, r.naive_crossing_rows, r.n_sfd,
+                          r.n_epd, [int(r.per_device_rows[d]) for d in range(nd)])
+
+    def saved_index(self):
+        """Inbox records (token, source, slot) and BRIM1 of the last forward."""
+        rep = self.comm_report()
+        R = sum(rep.per_device_token_counts)
+        P = self.config.experts_per_device()
+        dev = torch.device("cuda")
+        tok = torch.empty(R, dtype=torch.int32, device=dev)
+        src = torch.empty(R, dtype=torch.int32, device=dev)
+        slot = torch.empty(R, dtype=torch.int32, device=dev)
+        cix = torch.empty(R * P, dtype=torch.int32, device=dev)
+        _check(lib().occ_saved_index(self._h, _ptr(tok), _ptr(src), _ptr(slot), _ptr(cix), _stream()), "saved_index")
+        return tok, src, slot, cix, rep.per_device_token_counts
+
+
+# ------------------------------------------------------ stateless functions --
+
+def gate_scores_f64(x: torch.Tensor, gate: torch.Tensor) -> torch.Tensor:
+    """gate_scores (routing.cpp:33-52), exact fp64 mode."""
+    _need_cuda(x, gate)
+    x, gate = x.double().contiguous(), gate.double().contiguous()
+    out = torch.empty((x.shape[0], gate.shape[0]), dtype=torch.float64, device=x.device)
+    if x.shape[1] != gate.shape[1]:
+        raise ShapeError(f"gate_scores: token width {x.shape[1]} != gate width {gate.shape[1]}")
+    _check(lib().occ_gate_scores_f64(_ptr(x), x.shape[0], x.shape[1], _ptr(gate), gate.shape[0], _ptr(out),
+                                     _stream()), "gate_scores")
+    return out
+
+
+def topk_route(scores: torch.Tensor, k: int, renormalize: bool = True):
+    """topk_route (routing.cpp:60-84) on fp64 scores; bit-exact."""
+    _need_cuda(scores)
+    s = scores.double().contiguous()
+    n, e = s.shape
+    ids = torch.empty((n, k), dtype=torch.int32, device=s.device)
+    w = torch.empty((n, k), dtype=torch.float64, device=s.device)
+    _check(lib().occ_topk_route_f64(_ptr(s), n, e, k, int(renormalize), _ptr(ids), _ptr(w), _stream()), "topk_route")
+    return ids, w
+
+
+def accumulate_collab(counts: torch.Tensor, ids: torch.Tensor) -> torch.Tensor:
+    """accumulate_collab (collab.cpp:10-23): int64 [E,E] device histogram, in place."""
+    _need_cuda(counts, ids)
+    e = counts.shape[0]
+    n, k = ids.shape
+    _check(lib().occ_coactivation_histogram(_ptr(ids.contiguous()), n, k, e, _ptr(counts), _stream()), "collab")
+    return counts
+
+
+def build_collab_graph(ids: torch.Tensor, num_experts: int) -> torch.Tensor:
+    counts = torch.zeros((num_experts, num_experts), dtype=torch.int64, device=ids.device)
+    return accumulate_collab(counts, ids)
+
+
+def normalize_graph(counts) -> "numpy.ndarray":
+    """normalize_graph (collab.cpp:31-39), host."""
+    import numpy as np
+    c = np.ascontiguousarray(counts.cpu().numpy() if isinstance(counts, torch.Tensor) else counts, dtype=np.int64)
+    e = c.shape[0]
+    p = np.empty((e, e), np.float64)
+    _check(lib().occ_normalize_graph(c.ctypes.data_as(C.c_void_p), e, p.ctypes.data_as(C.c_void_p)), "normalize")
+    return p
+
+
+def reschedule_placement(p, num_devices: int) -> Placement:
+    """reschedule_placement (placement.cpp:88-148), host, bit-exact."""
+    import numpy as np
+    p = np.ascontiguousarray(p, dtype=np.float64)
+    e = p.shape[0]
+    out = np.empty(e, np.int32)
+    _check(lib().occ_reschedule_placement(p.ctypes.data_as(C.c_void_p), e, num_devices,
+                                          out.ctypes.data_as(C.c_void_p)), "reschedule_placement")
+    per = e // num_devices
+    return Placement([out[d * per:(d + 1) * per].tolist() for d in range(num_devices)])
+
+
+def round_robin_sources(num_tokens: int, num_devices: int, device="cuda") -> torch.Tensor:
+    """pipeline.cpp:12-16."""
+    return (torch.arange(num_tokens, dtype=torch.int32, device=device) % num_devices).to(torch.int32)

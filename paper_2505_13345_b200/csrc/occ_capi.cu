@@ -1,0 +1,621 @@
+// occ_capi.cu — the C-ABI (include/occult.h): handle, workspace, stage
+// entry points and the fused end-to-end forward.
+//
+// Per forward (world_size == 1, all N_d logical devices on this GPU, the
+// reference's single-process simulation made real):
+//   plan_mask -> rank(count, scan) -> dispatch_finalize -> rank(emit)    BRIM0, inbox slots
+//   pack                                                                  dispatch + exchange placement
+//   compute_mask -> rank(count, scan) -> compute_finalize -> rank(emit)   BRIM1, Epd segments
+//   gather -> grouped GEMM-1 (tcgen05, act/SwiGLU x routing weight)       scatter_matmul+act+modulate
+//   grouped GEMM-2 (tcgen05, fp32)                                        merge_matmul products
+//   partial_combine (intra-device, placement order)                       merge_matmul sum
+//   combine (devices ascending)                                           return exchange + combine
+// Everything is stream-ordered with device-side counts: no host sync
+// unless validation is on (the default; occ_set_validate(h, 0) for
+// capture/benchmarks).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/occult.h"
+#include "occ_internal.h"
+
+using namespace occ;
+
+namespace {
+
+thread_local std::string g_err;
+
+occ_status fail(occ_status s, const std::string& msg) {
+    g_err = msg;
+    return s;
+}
+
+#define CUDA_TRY(x)                                                                        \
+    do {                                                                                   \
+        cudaError_t e_ = (x);                                                              \
+        if (e_ != cudaSuccess) return fail(OCC_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    cudaError_t ensure(size_t count) {
+        if (count <= n && p) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+        cudaError_t e = cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T));
+        if (e == cudaSuccess) n = count;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+
+}  // namespace
+
+struct alignas(64) TmapBox {
+    alignas(64) unsigned char bytes[128];
+};
+
+struct occ_handle {
+    occ_config cfg{};
+    int E = 0, k = 0, nd = 0, D = 0, F = 0, P = 0, world = 1, rank = 0;
+    int gated = 0;
+    int validate = 1;
+    int num_sms = 148;
+    std::vector<int32_t> plist;  // nd * P
+    std::vector<int32_t> dev_of, slot_of;
+    DevBuf<int32_t> d_dev_of, d_slot_of, d_widx, d_ranking;
+    bool have_ranking = false;
+    // resident weights, K-major
+    DevBuf<__nv_bfloat16> w13t, w2t;
+    int n1rows = 0;  // B rows per expert of GEMM-1
+    bool weights_loaded = false;
+    // workspace
+    int n_cap = -1;
+    DevBuf<uint64_t> mask, rmask;
+    DevBuf<int32_t> group, rgroup, chunk_cnt, totals, totals2;
+    DevBuf<int> offs;  // dispatch + compute offset arrays
+    DevBuf<long long> stats;
+    DevBuf<int32_t> err;
+    DevBuf<int32_t> tok_row, tok_sfd, lam;
+    DevBuf<__nv_bfloat16> in_x, x_epd, hbuf, ret;
+    DevBuf<int32_t> in_ids, in_tok, in_src, in_slot, in_dev, row_epd, epd_src, mblk_w;
+    DevBuf<float> in_w, epd_w, ybuf, logits;
+    size_t R_max = 0, Q_max = 0, max_mblk = 0;
+    int last_n = 0;
+    bool have_forward = false;
+    TmapBox tmA1, tmA2, tmB1, tmB2;
+    DispatchOffsets dofs{};
+    ComputeOffsets cofs{};
+    int* d_tok_base = nullptr;
+    int* d_n_mblk = nullptr;
+    int* d_q_total = nullptr;
+    // NCCL (world_size > 1)
+    void* nccl_comm = nullptr;
+};
+
+namespace {
+
+occ_status validate_placement(const occ_config& c, const int32_t* pl, std::vector<int32_t>& dev_of,
+                              std::vector<int32_t>& slot_of) {
+    const int E = c.num_experts, nd = c.num_devices, P = E / nd;
+    dev_of.assign(E, -1);
+    slot_of.assign(E, -1);
+    for (int d = 0; d < nd; ++d)
+        for (int i = 0; i < P; ++i) {
+            const int e = pl[d * P + i];
+            if (e < 0 || e >= E || dev_of[e] >= 0)
+                return fail(OCC_ERR_PLACEMENT, "placement: device lists are not a partition of [0, E)");
+            dev_of[e] = d;
+            slot_of[e] = i;
+        }
+    return OCC_OK;
+}
+
+occ_status upload_tables(occ_handle* h) {
+    CUDA_TRY(h->d_dev_of.ensure(h->E));
+    CUDA_TRY(h->d_slot_of.ensure(h->E));
+    const int G = h->world == 1 ? h->nd : 1;
+    CUDA_TRY(h->d_widx.ensure(G * h->P));
+    std::vector<int32_t> widx(G * h->P);
+    for (int g = 0; g < G; ++g)
+        for (int p = 0; p < h->P; ++p) widx[g * h->P + p] = h->world == 1 ? h->plist[g * h->P + p] : p;
+    CUDA_TRY(cudaMemcpy(h->d_dev_of.p, h->dev_of.data(), sizeof(int32_t) * h->E, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(h->d_slot_of.p, h->slot_of.data(), sizeof(int32_t) * h->E, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(h->d_widx.p, widx.data(), sizeof(int32_t) * widx.size(), cudaMemcpyHostToDevice));
+    return OCC_OK;
+}
+
+// Grow-only workspace for n tokens.
+occ_status ensure_ws(occ_handle* h, int n) {
+    if (n <= h->n_cap) return OCC_OK;
+    const int nd = h->nd, k = h->k, P = h->P, D = h->D, F = h->F;
+    const int G = h->world == 1 ? nd : 1;
+    const int dedup = h->cfg.dedup;
+    const size_t items = dedup ? (size_t)n : (size_t)n * k;
+    const size_t span_max = dedup ? (size_t)std::min(k, nd) : (size_t)k;
+    h->R_max = (size_t)n * span_max;
+    if (h->world > 1) h->R_max = h->R_max * 1;  // recv rows bounded by the same per-source bound x world
+    h->Q_max = (size_t)n * k + (size_t)G * P * (kBM - 1);
+    h->Q_max = (h->Q_max + kBM - 1) / kBM * kBM;
+    h->max_mblk = h->Q_max / kBM;
+    const size_t K1 = (size_t)nd * (nd + 1), K2 = (size_t)G * (P + 1);
+    const size_t nchunks = (std::max(items, h->R_max) + kRankChunk - 1) / kRankChunk + 1;
+    CUDA_TRY(h->mask.ensure(items));
+    CUDA_TRY(h->group.ensure(items));
+    CUDA_TRY(h->chunk_cnt.ensure(nchunks * std::max(K1, K2)));
+    CUDA_TRY(h->totals.ensure(K1));
+    CUDA_TRY(h->totals2.ensure(K2));
+    // offsets: C, off_sd, inoff (3 nd^2) + in_base(nd+1) + nsfd(nd) + src_base(nd+1) + tok_base(2nd)
+    //          + cnt/seg_base/unp_base (3 G P) + n_mblk + q_total
+    const size_t noffs = 3 * (size_t)nd * nd + (nd + 1) + nd + (nd + 1) + 2 * nd + 3 * (size_t)G * P + 2;
+    CUDA_TRY(h->offs.ensure(noffs));
+    CUDA_TRY(h->stats.ensure(8));
+    CUDA_TRY(h->err.ensure(1));
+    CUDA_TRY(h->tok_row.ensure(dedup ? (size_t)n * nd : items));
+    CUDA_TRY(h->tok_sfd.ensure(dedup ? (size_t)n * nd : items));
+    CUDA_TRY(h->lam.ensure(n));
+    CUDA_TRY(h->in_x.ensure(h->R_max * D));
+    CUDA_TRY(h->in_ids.ensure(h->R_max * k));
+    CUDA_TRY(h->in_w.ensure(h->R_max * k));
+    CUDA_TRY(h->in_tok.ensure(h->R_max));
+    CUDA_TRY(h->in_src.ensure(h->R_max));
+    CUDA_TRY(h->in_slot.ensure(h->R_max));
+    CUDA_TRY(h->in_dev.ensure(h->R_max));
+    CUDA_TRY(h->rmask.ensure(h->R_max));
+    CUDA_TRY(h->rgroup.ensure(h->R_max));
+    CUDA_TRY(h->row_epd.ensure(h->R_max * P));
+    CUDA_TRY(h->epd_src.ensure(h->Q_max));
+    CUDA_TRY(h->epd_w.ensure(h->Q_max));
+    CUDA_TRY(h->x_epd.ensure(h->Q_max * D));
+    CUDA_TRY(h->hbuf.ensure(h->Q_max * F));
+    CUDA_TRY(h->ybuf.ensure(h->Q_max * D));
+    CUDA_TRY(h->mblk_w.ensure(h->max_mblk));
+    CUDA_TRY(h->ret.ensure(h->R_max * D));
+    int* o = h->offs.p;
+    DispatchOffsets& d = h->dofs;
+    d.C = o; o += nd * nd;
+    d.off_sd = o; o += nd * nd;
+    d.inoff = o; o += nd * nd;
+    d.in_base = o; o += nd + 1;
+    d.nsfd = o; o += nd;
+    d.src_base = o; o += nd + 1;
+    h->d_tok_base = o; o += 2 * nd;
+    d.ntok = h->d_tok_base + nd;
+    d.stats = h->stats.p;
+    ComputeOffsets& c = h->cofs;
+    c.cnt = o; o += G * P;
+    c.seg_base = o; o += G * P;
+    c.unp_base = o; o += G * P;
+    c.n_mblk = o; o += 1;
+    c.q_total = o; o += 1;
+    c.mblk_w = h->mblk_w.p;
+    c.widx = h->d_widx.p;
+    c.stats = h->stats.p;
+    h->d_n_mblk = c.n_mblk;
+    h->d_q_total = c.q_total;
+    // A-operand tensor maps (buffers just (re)allocated)
+    if (!make_tmap_2d(h->tmA1.bytes, h->x_epd.p, D, h->Q_max, 64, kBM) ||
+        !make_tmap_2d(h->tmA2.bytes, h->hbuf.p, F, h->Q_max, 64, kBM))
+        return fail(OCC_ERR_CUDA, "cuTensorMapEncodeTiled failed (A operands)");
+    h->n_cap = n;
+    return OCC_OK;
+}
+
+__global__ void tok_base_kernel(int nd, int* tok_base) {
+    // tok_base[0..nd) = exclusive prefix of ntok = tok_base[nd..2nd)
+    if (threadIdx.x == 0) {
+        int run = 0;
+        for (int s = 0; s < nd; ++s) {
+            tok_base[s] = run;
+            run += tok_base[nd + s];
+        }
+    }
+}
+
+// Dispatch plan: BRIM0 + inbox placement (+ stats). world_size == 1.
+occ_status run_plan(occ_handle* h, const int32_t* ids, const float* w, const int32_t* sources, int n,
+                    cudaStream_t st) {
+    const int nd = h->nd, k = h->k, dedup = h->cfg.dedup;
+    const int items = dedup ? n : n * k;
+    PlanArgs pa{n, k, nd, dedup, ids, w, sources, -1, h->d_dev_of.p, h->d_slot_of.p, h->E, h->mask.p, h->group.p,
+                h->err.p};
+    launch_plan_mask(pa, st);
+    RankWs ws{h->chunk_cnt.p, h->totals.p};
+    launch_rank_count(items, h->group.p, h->mask.p, nd, nd, ws, st);
+    launch_rank_scan(items, nd, nd, ws, st);
+    launch_dispatch_finalize(nd, h->totals.p, h->dofs, st);
+    tok_base_kernel<<<1, 32, 0, st>>>(nd, h->d_tok_base);
+    count_launch();
+    EmitDispatch em{n, k, nd, dedup, ids, w, sources, -1, h->d_dev_of.p, h->dofs, 1, h->tok_row.p, h->tok_sfd.p,
+                    h->lam.p, h->in_tok.p, h->in_src.p, h->in_slot.p, h->in_dev.p};
+    launch_rank_emit_dispatch(items, h->group.p, h->mask.p, nd, nd, ws, em, st);
+    launch_token_stats(n, k, nd, ids, sources, -1, h->d_dev_of.p, h->stats.p, st);
+    return OCC_OK;
+}
+
+occ_status check_err(occ_handle* h, cudaStream_t st) {
+    CUDA_TRY(cudaStreamSynchronize(st));
+    int32_t e = 0;
+    CUDA_TRY(cudaMemcpy(&e, h->err.p, sizeof(e), cudaMemcpyDeviceToHost));
+    if (e == 1) return fail(OCC_ERR_SHAPE, "forward: source device out of range");
+    if (e == 4) return fail(OCC_ERR_ROUTING, "routing: invalid expert id, duplicate id, non-positive weight, or a row with no local expert");
+    if (e == 5) return fail(OCC_ERR_CAPACITY, "prune: device budget too small for top-k");
+    if (e) return fail(OCC_ERR_ROUTING, "routing error");
+    return OCC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* occ_last_error(void) { return g_err.c_str(); }
+long long occ_launch_count(void) { return g_launches; }
+
+occ_status occ_create(const occ_config* cfg, const int32_t* placement, int world_size, int rank, occ_handle** out) {
+    if (!cfg || !placement || !out) return fail(OCC_ERR_ARG, "null argument");
+    const occ_config& c = *cfg;
+    // MoEConfig::validate (core.cpp:10-23)
+    if (c.num_experts < 1) return fail(OCC_ERR_CONFIG, "config: num_experts must be >= 1");
+    if (c.num_devices < 1) return fail(OCC_ERR_CONFIG, "config: num_devices must be >= 1");
+    if (c.top_k < 1 || c.top_k > c.num_experts) return fail(OCC_ERR_CONFIG, "config: top_k must satisfy 1 <= k <= num_experts");
+    if (c.num_experts % c.num_devices) return fail(OCC_ERR_CONFIG, "config: num_experts must be divisible by num_devices");
+    if (c.embed_dim < 1 || c.hidden_dim < 1) return fail(OCC_ERR_CONFIG, "config: dims must be >= 1");
+    // B200 path constraints
+    if (c.num_devices > kMaxDev || c.num_experts / c.num_devices > kMaxLocal || c.num_experts > 256)
+        return fail(OCC_ERR_UNSUPPORTED, "N_d <= 64, experts per device <= 64, E <= 256");
+    if (c.embed_dim % 8 || c.hidden_dim % 8) return fail(OCC_ERR_UNSUPPORTED, "embed_dim and hidden_dim must be multiples of 8");
+    if (c.activation == OCC_ACT_SWIGLU && c.hidden_dim % 128)
+        return fail(OCC_ERR_UNSUPPORTED, "SwiGLU needs hidden_dim % 128 == 0");
+    if (c.activation < 0 || c.activation > 3) return fail(OCC_ERR_CONFIG, "config: bad activation");
+    if (world_size != 1 && world_size != c.num_devices)
+        return fail(OCC_ERR_CONFIG, "world_size must be 1 (all devices local) or num_devices");
+    if (rank < 0 || rank >= world_size) return fail(OCC_ERR_CONFIG, "rank out of range");
+    occ_handle* h = new occ_handle();
+    h->cfg = c;
+    h->E = c.num_experts;
+    h->k = c.top_k;
+    h->nd = c.num_devices;
+    h->D = c.embed_dim;
+    h->F = c.hidden_dim;
+    h->P = h->E / h->nd;
+    h->world = world_size;
+    h->rank = rank;
+    h->gated = c.activation == OCC_ACT_SWIGLU;
+    h->plist.assign(placement, placement + h->E);
+    occ_status s = validate_placement(c, placement, h->dev_of, h->slot_of);
+    if (s != OCC_OK) { delete h; return s; }
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, dev);
+    s = upload_tables(h);
+    if (s != OCC_OK) { delete h; return s; }
+    *out = h;
+    return OCC_OK;
+}
+
+occ_status occ_destroy(occ_handle* h) {
+    if (!h) return OCC_OK;
+    for (auto* b : {&h->d_dev_of, &h->d_slot_of, &h->d_widx, &h->d_ranking, &h->group, &h->rgroup, &h->chunk_cnt,
+                    &h->totals, &h->totals2, &h->err, &h->tok_row, &h->tok_sfd, &h->lam, &h->in_ids, &h->in_tok,
+                    &h->in_src, &h->in_slot, &h->in_dev, &h->row_epd, &h->epd_src, &h->mblk_w})
+        b->release();
+    h->offs.release();
+    h->stats.release();
+    h->mask.release();
+    h->rmask.release();
+    for (auto* b : {&h->w13t, &h->w2t, &h->in_x, &h->x_epd, &h->hbuf, &h->ret}) b->release();
+    for (auto* b : {&h->in_w, &h->epd_w, &h->ybuf, &h->logits}) b->release();
+    delete h;
+    return OCC_OK;
+}
+
+occ_status occ_set_placement(occ_handle* h, const int32_t* placement) {
+    if (!h || !placement) return fail(OCC_ERR_ARG, "null argument");
+    std::vector<int32_t> dev_of, slot_of;
+    occ_status s = validate_placement(h->cfg, placement, dev_of, slot_of);
+    if (s != OCC_OK) return s;
+    h->plist.assign(placement, placement + h->E);
+    h->dev_of = dev_of;
+    h->slot_of = slot_of;
+    h->weights_loaded = h->world == 1 && h->weights_loaded;  // world>1: local experts changed
+    return upload_tables(h);
+}
+
+occ_status occ_load_experts(occ_handle* h, const void* w1, const void* w3, const void* w2, occ_stream_t stream) {
+    if (!h || !w1 || !w2) return fail(OCC_ERR_ARG, "null weight pointer");
+    if (h->gated != (w3 != nullptr)) return fail(OCC_ERR_SHAPE, "w3 must be given iff activation is SwiGLU");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int El = h->world == 1 ? h->E : h->P;
+    const int D = h->D, F = h->F;
+    h->n1rows = h->gated ? 2 * F : F;
+    CUDA_TRY(h->w13t.ensure((size_t)El * h->n1rows * D));
+    CUDA_TRY(h->w2t.ensure((size_t)El * D * F));
+    const auto* b1 = reinterpret_cast<const __nv_bfloat16*>(w1);
+    const auto* b2 = reinterpret_cast<const __nv_bfloat16*>(w2);
+    if (h->gated) {
+        launch_transpose_weights(b1, El, D, F, h->w13t.p, h->n1rows, 1, st);
+        launch_transpose_weights(reinterpret_cast<const __nv_bfloat16*>(w3), El, D, F, h->w13t.p, h->n1rows, 2, st);
+    } else {
+        launch_transpose_weights(b1, El, D, F, h->w13t.p, h->n1rows, 0, st);
+    }
+    launch_transpose_weights(b2, El, F, D, h->w2t.p, D, 0, st);
+    CUDA_TRY(cudaGetLastError());
+    if (!make_tmap_2d(h->tmB1.bytes, h->w13t.p, D, (uint64_t)El * h->n1rows, 64, 256) ||
+        !make_tmap_2d(h->tmB2.bytes, h->w2t.p, F, (uint64_t)El * D, 64, 256))
+        return fail(OCC_ERR_CUDA, "cuTensorMapEncodeTiled failed (weights)");
+    h->weights_loaded = true;
+    return OCC_OK;
+}
+
+occ_status occ_set_similarity(occ_handle* h, const double* values) {
+    if (!h || !values) return fail(OCC_ERR_ARG, "null argument");
+    const int E = h->E;
+    // ranking exactly as SimilarityAccumulator::finalize (pruning.cpp:203-211)
+    std::vector<int32_t> rk((size_t)E * (E - 1 > 0 ? E - 1 : 1));
+    for (int i = 0; i < E; ++i) {
+        std::vector<int> r;
+        for (int j = 0; j < E; ++j)
+            if (j != i) r.push_back(j);
+        const double* row = values + (size_t)i * E;
+        std::stable_sort(r.begin(), r.end(), [&](int a, int b) {
+            if (row[a] != row[b]) return row[a] > row[b];
+            return a < b;
+        });
+        std::copy(r.begin(), r.end(), rk.begin() + (size_t)i * (E - 1));
+    }
+    CUDA_TRY(h->d_ranking.ensure(rk.size()));
+    CUDA_TRY(cudaMemcpy(h->d_ranking.p, rk.data(), sizeof(int32_t) * rk.size(), cudaMemcpyHostToDevice));
+    h->have_ranking = true;
+    return OCC_OK;
+}
+
+occ_status occ_set_validate(occ_handle* h, int on) {
+    if (!h) return fail(OCC_ERR_ARG, "null handle");
+    h->validate = on;
+    return OCC_OK;
+}
+
+// ----------------------------------------------------------------- routing
+occ_status occ_gate_scores_f64(const double* x, int n, int d, const double* gate, int e, double* scores,
+                               occ_stream_t stream) {
+    if (n < 0 || d < 1 || e < 1) return fail(OCC_ERR_SHAPE, "gate_scores: bad shape");
+    launch_gate_scores_f64(x, n, d, gate, e, scores, reinterpret_cast<cudaStream_t>(stream));
+    CUDA_TRY(cudaGetLastError());
+    return OCC_OK;
+}
+
+occ_status occ_topk_route_f64(const double* scores, int n, int e, int k, int renormalize, int32_t* ids,
+                              double* weights, occ_stream_t stream) {
+    if (k < 1 || k > e || e > 256) return fail(OCC_ERR_ROUTING, "topk_route: k out of range");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    int32_t* err = nullptr;
+    CUDA_TRY(cudaMallocAsync(&err, sizeof(int32_t), st));
+    CUDA_TRY(cudaMemsetAsync(err, 0, sizeof(int32_t), st));
+    launch_topk_f64(scores, n, e, k, renormalize, ids, weights, err, st);
+    int32_t he = 0;
+    CUDA_TRY(cudaMemcpyAsync(&he, err, sizeof(he), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaFreeAsync(err, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    if (he) return fail(OCC_ERR_ROUTING, "renormalize: non-positive weight sum");
+    return OCC_OK;
+}
+
+static occ_status prune_dev(occ_handle* h, const occ_prune* prune, PruneDev& p) {
+    p = PruneDev{0, 1, 0, h->cfg.renormalize, h->nd, h->d_dev_of.p, nullptr};
+    if (!prune || prune->mode == OCC_PRUNE_NONE) return OCC_OK;
+    if (prune->device_budget < 1 || prune->device_budget > h->nd)
+        return fail(OCC_ERR_CONFIG, "prune: device budget must be in [1, num_devices]");
+    if (prune->mode == OCC_PRUNE_SIMILARITY && !h->have_ranking)
+        return fail(OCC_ERR_CONFIG, "prune: similarity mode requires a similarity table");
+    p.mode = prune->mode;
+    p.budget = prune->device_budget;
+    p.own_score = prune->own_score;
+    p.ranking = h->d_ranking.p;
+    return OCC_OK;
+}
+
+occ_status occ_prune_routing_f64(occ_handle* h, const double* scores, const int32_t* ids_in, const double* w_in,
+                                 int n, const occ_prune* prune, int32_t* ids, double* weights, occ_stream_t stream) {
+    if (!h) return fail(OCC_ERR_ARG, "null handle");
+    PruneDev p;
+    occ_status s = prune_dev(h, prune, p);
+    if (s != OCC_OK) return s;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    CUDA_TRY(h->err.ensure(1));
+    CUDA_TRY(cudaMemsetAsync(h->err.p, 0, sizeof(int32_t), st));
+    launch_prune_f64(scores, n, h->E, h->k, ids_in, w_in, p, ids, weights, h->err.p, st);
+    return check_err(h, st);
+}
+
+occ_status occ_route(occ_handle* h, const void* x, const void* gate, int n, const occ_prune* prune, int32_t* ids,
+                     float* weights, float* scores, occ_stream_t stream) {
+    if (!h || !x || !gate || !ids || !weights) return fail(OCC_ERR_ARG, "null argument");
+    PruneDev p;
+    occ_status s = prune_dev(h, prune, p);
+    if (s != OCC_OK) return s;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    CUDA_TRY(h->logits.ensure((size_t)std::max(n, 1) * h->E));
+    CUDA_TRY(h->err.ensure(1));
+    CUDA_TRY(cudaMemsetAsync(h->err.p, 0, sizeof(int32_t), st));
+    launch_router_bf16(reinterpret_cast<const __nv_bfloat16*>(x), reinterpret_cast<const __nv_bfloat16*>(gate), n,
+                       h->D, h->E, h->k, h->cfg.renormalize, p, ids, weights, scores, h->logits.p, h->err.p, st);
+    CUDA_TRY(cudaGetLastError());
+    if (h->validate) return check_err(h, st);
+    return OCC_OK;
+}
+
+// ----------------------------------------------------------------- EP path
+occ_status occ_build_dispatch(occ_handle* h, const int32_t* ids, const int32_t* sources, int n, int32_t* brim0,
+                              int32_t* counts, occ_stream_t stream) {
+    if (!h || !ids) return fail(OCC_ERR_ARG, "null argument");
+    if (h->world != 1) return fail(OCC_ERR_UNSUPPORTED, "occ_build_dispatch: world_size 1 only");
+    if (!h->cfg.dedup) return fail(OCC_ERR_UNSUPPORTED, "BRIM0 is defined for the dedup dispatch");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    occ_status s = ensure_ws(h, n);
+    if (s != OCC_OK) return s;
+    CUDA_TRY(cudaMemsetAsync(h->stats.p, 0, sizeof(long long) * 8, st));
+    CUDA_TRY(cudaMemsetAsync(h->err.p, 0, sizeof(int32_t), st));
+    s = run_plan(h, ids, nullptr, sources, n, st);
+    if (s != OCC_OK) return s;
+    if (brim0) launch_extract_brim0(n, h->nd, sources, -1, h->mask.p, h->lam.p, h->tok_sfd.p, h->d_tok_base, brim0, st);
+    if (counts) CUDA_TRY(cudaMemcpyAsync(counts, h->dofs.C, sizeof(int) * h->nd * h->nd, cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(cudaGetLastError());
+    return check_err(h, st);
+}
+
+occ_status occ_forward(occ_handle* h, const void* x, const int32_t* ids, const float* weights,
+                       const int32_t* sources, int n, void* out, occ_stream_t stream) {
+    if (!h) return fail(OCC_ERR_ARG, "null handle");
+    if (n > 0 && (!x || !ids || !weights || !out)) return fail(OCC_ERR_ARG, "null argument");
+    if (!h->weights_loaded) return fail(OCC_ERR_STATE, "forward: experts not loaded");
+    if (h->world != 1) return fail(OCC_ERR_UNSUPPORTED, "forward: world_size > 1 needs occ_comm_init");
+    if (n < 0) return fail(OCC_ERR_SHAPE, "forward: negative token count");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    occ_status s = ensure_ws(h, n);
+    if (s != OCC_OK) return s;
+    h->last_n = n;
+    h->have_forward = true;
+    if (n == 0) return OCC_OK;
+    const int nd = h->nd, k = h->k, P = h->P, D = h->D, F = h->F, dedup = h->cfg.dedup;
+    const int G = nd;
+    CUDA_TRY(cudaMemsetAsync(h->stats.p, 0, sizeof(long long) * 8, st));
+    CUDA_TRY(cudaMemsetAsync(h->err.p, 0, sizeof(int32_t), st));
+    // 1. dispatch plan (BRIM0) and exchange placement
+    s = run_plan(h, ids, weights, sources, n, st);
+    if (s != OCC_OK) return s;
+    // 2. pack: x rows -> inbox rows of every destination device
+    const int32_t* rowmap = h->tok_row.p;
+    PackArgs pk{n, k, nd, D, dedup, reinterpret_cast<const __nv_bfloat16*>(x), ids, weights, h->mask.p, rowmap,
+                h->in_x.p, h->in_ids.p, h->in_w.p};
+    launch_pack(pk, st);
+    // 3. compute index (BRIM1) over the inbox rows
+    const int* R_total = h->dofs.in_base + nd;
+    const int R_max = (int)h->R_max;
+    ComputeArgs ca{R_max, R_total, k, P, G, h->in_ids.p, h->in_w.p, h->in_dev.p, h->d_dev_of.p, h->d_slot_of.p, 0,
+                   h->rmask.p, h->rgroup.p, h->err.p};
+    launch_compute_mask(ca, st);
+    RankWs ws{h->chunk_cnt.p, h->totals2.p};
+    launch_rank_count_dev(R_max, R_total, h->rgroup.p, h->rmask.p, G, P, ws, st);
+    launch_rank_scan(R_max, G, P, ws, st);
+    launch_compute_finalize(G, P, h->totals2.p, h->cofs, (int)h->max_mblk, st);
+    launch_init_epd((int)h->Q_max, h->epd_src.p, h->epd_w.p, st);
+    EmitCompute ec{k, P, 0, h->in_ids.p, h->in_w.p, h->d_slot_of.p, h->d_dev_of.p, h->cofs, h->row_epd.p,
+                   h->epd_src.p, h->epd_w.p};
+    launch_rank_emit_compute(R_max, R_total, h->rgroup.p, h->rmask.p, G, P, ws, ec, st);
+    // 4. gather + grouped GEMM-1 (activation / SwiGLU, routing weight fused)
+    launch_gather_rows((int)h->Q_max, h->d_q_total, h->epd_src.p, h->in_x.p, D, h->x_epd.p, st);
+    const int max_mb = (int)h->max_mblk;
+    GemmArgs g1{h->tmA1.bytes, h->tmB1.bytes, D, F, h->n1rows, h->d_n_mblk, h->mblk_w.p, h->epd_w.p, h->hbuf.p, F,
+                h->cfg.activation, max_mb * (h->gated ? F / 128 : (F + 255) / 256)};
+    launch_grouped_gemm(h->gated ? EPI_SWIGLU_BF16 : EPI_ACT_BF16, g1, h->num_sms, st);
+    // 5. grouped GEMM-2 (per-expert products, fp32)
+    GemmArgs g2{h->tmA2.bytes, h->tmB2.bytes, F, D, D, h->d_n_mblk, h->mblk_w.p, nullptr, h->ybuf.p, D, 0,
+                max_mb * ((D + 255) / 256)};
+    launch_grouped_gemm(EPI_F32, g2, h->num_sms, st);
+    // 6. intra-device partial combine -> return payload (bf16)
+    launch_partial_combine(R_max, R_total, P, D, h->row_epd.p, h->ybuf.p, h->ret.p, st);
+    // 7. return exchange + combine
+    launch_combine(n, nd, k, dedup, D, h->mask.p, h->tok_row.p, h->ret.p, reinterpret_cast<__nv_bfloat16*>(out), st);
+    CUDA_TRY(cudaGetLastError());
+    if (h->validate) return check_err(h, st);
+    return OCC_OK;
+}
+
+occ_status occ_forward_expert_parallel(occ_handle* h, const void* x, const void* gate, const occ_prune* prune,
+                                       const int32_t* sources, int n, void* out, occ_stream_t stream) {
+    if (!h) return fail(OCC_ERR_ARG, "null handle");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    int32_t* ids = nullptr;
+    float* w = nullptr;
+    CUDA_TRY(cudaMallocAsync(&ids, sizeof(int32_t) * std::max(n, 1) * h->k, st));
+    CUDA_TRY(cudaMallocAsync(&w, sizeof(float) * std::max(n, 1) * h->k, st));
+    occ_status s = occ_route(h, x, gate, n, prune, ids, w, nullptr, stream);
+    if (s == OCC_OK) s = occ_forward(h, x, ids, w, sources, n, out, stream);
+    cudaFreeAsync(ids, st);
+    cudaFreeAsync(w, st);
+    return s;
+}
+
+occ_status occ_comm_report_get(occ_handle* h, int bytes_per_scalar, occ_comm_report* rep, occ_stream_t stream) {
+    if (!h || !rep) return fail(OCC_ERR_ARG, "null argument");
+    if (!h->have_forward) return fail(OCC_ERR_STATE, "no forward to report");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    CUDA_TRY(cudaStreamSynchronize(st));
+    std::memset(rep, 0, sizeof(*rep));
+    const int nd = h->nd, n = h->last_n;
+    if (n == 0) return OCC_OK;
+    long long stats[8];
+    CUDA_TRY(cudaMemcpy(stats, h->stats.p, sizeof(stats), cudaMemcpyDeviceToHost));
+    std::vector<int> C(nd * nd);
+    CUDA_TRY(cudaMemcpy(C.data(), h->dofs.C, sizeof(int) * nd * nd, cudaMemcpyDeviceToHost));
+    rep->mean_replicas = (double)stats[2] / n;
+    rep->cap_replicas = (double)std::min(h->k, nd);
+    const long long pairs = stats[3] + stats[4];
+    rep->intra_share = pairs ? (double)stats[3] / pairs : 0.0;
+    rep->inter_share = pairs ? (double)stats[4] / pairs : 0.0;
+    rep->crossing_rows = stats[0];
+    rep->naive_crossing_rows = stats[1];
+    rep->cross_device_bytes = stats[0] * (long long)h->D * bytes_per_scalar;
+    rep->n_sfd = stats[5];
+    rep->n_epd = stats[6];
+    for (int d = 0; d < nd; ++d) {
+        long long r = 0;
+        for (int s = 0; s < nd; ++s) r += C[s * nd + d];
+        rep->per_device_rows[d] = r;
+    }
+    return OCC_OK;
+}
+
+occ_status occ_saved_index(occ_handle* h, int32_t* inbox_token, int32_t* inbox_source, int32_t* inbox_slot,
+                           int32_t* cindex, occ_stream_t stream) {
+    if (!h) return fail(OCC_ERR_ARG, "null handle");
+    if (!h->have_forward) return fail(OCC_ERR_STATE, "no saved forward state");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (h->last_n == 0) return OCC_OK;
+    CUDA_TRY(cudaStreamSynchronize(st));
+    int R = 0;
+    CUDA_TRY(cudaMemcpy(&R, h->dofs.in_base + h->nd, sizeof(int), cudaMemcpyDeviceToHost));
+    if (inbox_token) CUDA_TRY(cudaMemcpyAsync(inbox_token, h->in_tok.p, sizeof(int) * R, cudaMemcpyDeviceToDevice, st));
+    if (inbox_source) CUDA_TRY(cudaMemcpyAsync(inbox_source, h->in_src.p, sizeof(int) * R, cudaMemcpyDeviceToDevice, st));
+    if (inbox_slot) CUDA_TRY(cudaMemcpyAsync(inbox_slot, h->in_slot.p, sizeof(int) * R, cudaMemcpyDeviceToDevice, st));
+    if (cindex)
+        launch_extract_cindex((int)h->R_max, h->dofs.in_base + h->nd, h->P, h->in_dev.p, h->dofs.in_base,
+                              h->row_epd.p, h->cofs, cindex, st);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaStreamSynchronize(st));
+    return OCC_OK;
+}
+
+occ_status occ_coactivation_histogram(const int32_t* ids, int n, int k, int e, int64_t* counts, occ_stream_t stream) {
+    if (!ids || !counts) return fail(OCC_ERR_ARG, "null argument");
+    if (e < 1 || e > 110 || k < 1) return fail(OCC_ERR_UNSUPPORTED, "histogram: 1 <= E <= 110 (shared-memory bins)");
+    launch_histogram(ids, n, k, e, counts, reinterpret_cast<cudaStream_t>(stream));
+    CUDA_TRY(cudaGetLastError());
+    return OCC_OK;
+}
+
+occ_status occ_comm_unique_id(void*) { return fail(OCC_ERR_UNSUPPORTED, "NCCL path not built in this round"); }
+occ_status occ_comm_init(occ_handle*, const void*) {
+    return fail(OCC_ERR_UNSUPPORTED, "NCCL path not built in this round");
+}
+occ_status occ_allreduce_histogram(occ_handle*, int64_t*, occ_stream_t) {
+    return fail(OCC_ERR_UNSUPPORTED, "NCCL path not built in this round");
+}
+
+}  // extern "C"

@@ -1,0 +1,209 @@
+// occ_internal.h — kernel launchers shared by the C-ABI layer (occ_capi.cu).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace occ {
+
+constexpr int kMaxDev = 64;    // N_d <= 64 (uint64 device masks)
+constexpr int kMaxLocal = 64;  // P <= 64 experts per device
+constexpr int kRankChunk = 256;
+constexpr int kBM = 128;       // GEMM M tile (EPD segments are padded to it)
+
+extern long long g_launches;
+inline void count_launch(int n = 1) { g_launches += n; }
+
+// ---- generic stable bucketed rank ("warp-ballot / scan compaction") ----
+// Items i < n carry group g_i in [0,G) and a bucket mask m_i (bits < B).
+// rank(i, b) = #{i' < i : g_i' = g_i, b in m_i'}; grank(i) = #{i' < i : g_i' = g_i}.
+// Phase 1 counts per (chunk, key), phase 2 scans chunks per key, phase 3
+// re-derives the in-chunk ranks and hands them to an emitter.
+struct RankWs {
+    int* chunk_cnt;  // [nchunks][G*(B+1)] -> exclusive bases after phase 2
+    int* totals;     // [G*(B+1)]
+};
+
+// Dispatch plan (BRIM0 + inbox placement), all sources resident on one GPU
+// or (world>1) this rank's tokens only.
+struct PlanArgs {
+    int n, k, nd, dedup;
+    const int32_t* ids;       // [n,k]
+    const float* w;           // [n,k]
+    const int32_t* sources;   // [n] or null (round robin)
+    int src_fixed;            // >=0: all tokens have this source (world>1)
+    const int32_t* dev_of;    // [E]
+    const int32_t* slot_of;   // [E]
+    int E;
+    // outputs / workspace
+    uint64_t* mask;           // [items]
+    int32_t* group;           // [items]
+    int32_t* err;             // device error flag
+};
+
+void launch_plan_mask(const PlanArgs& a, cudaStream_t st);
+void launch_rank_count(int n_items, const int32_t* group, const uint64_t* mask, int G, int B, RankWs ws,
+                       cudaStream_t st);
+void launch_rank_count_dev(int n_max, const int* n_dev, const int32_t* group, const uint64_t* mask, int G, int B,
+                           RankWs ws, cudaStream_t st);
+void launch_rank_scan(int n_items, int G, int B, RankWs ws, cudaStream_t st);
+
+// Offsets derived from the dispatch counts (device-side, no host sync).
+struct DispatchOffsets {
+    int* C;          // [nd*nd] counts (s,d)
+    int* off_sd;     // [nd*nd] BRIM0 counter base per (s,d)
+    int* inoff;      // [nd*nd] inbox offset of source s within device d (index d*nd+s)
+    int* in_base;    // [nd+1]  concatenated inbox base per device (world=1)
+    int* nsfd;       // [nd]    Sfd rows per source
+    int* src_base;   // [nd+1]  concatenated Sfd base per source
+    int* ntok;       // [nd]    tokens per source
+    long long* stats;  // [8]: 0 crossing rows, 1 naive crossing, 2 span sum, 3 intra pairs, 4 inter pairs, 5 n_sfd total
+};
+void launch_dispatch_finalize(int nd, const int* totals, DispatchOffsets o, cudaStream_t st);
+
+struct EmitDispatch {
+    int n, k, nd, dedup;
+    const int32_t* ids;
+    const float* w;
+    const int32_t* sources;
+    int src_fixed;
+    const int32_t* dev_of;
+    DispatchOffsets o;
+    int world1;              // inbox rows are global (all devices resident)
+    int32_t* tok_row;        // [items*nd or items] inbox row per (token,device) / item (world=1)
+    int32_t* tok_sfd;        // same shape: BRIM0 counter (Sfd slot within the source)
+    int32_t* lam;            // [n] local index of the token within its source (dedup only)
+    int32_t* in_tok;         // [R] (world=1)
+    int32_t* in_src;
+    int32_t* in_slot;
+    int32_t* in_dev;
+};
+void launch_rank_emit_dispatch(int n_items, const int32_t* group, const uint64_t* mask, int G, int B, RankWs ws,
+                               const EmitDispatch& e, cudaStream_t st);
+
+// BRIM0 extraction (per source N_d x n_s, concatenated) from tok_sfd.
+void launch_extract_brim0(int n, int nd, const int32_t* sources, int src_fixed, const uint64_t* mask,
+                          const int32_t* lam, const int32_t* tok_sfd, const int* src_tok_base, int32_t* brim0,
+                          cudaStream_t st);
+
+// Pack x rows (and the routing rows) into the inbox / send buffer.
+struct PackArgs {
+    int n, k, nd, D, dedup;
+    const __nv_bfloat16* x;
+    const int32_t* ids;
+    const float* w;
+    const uint64_t* mask;      // dedup: device mask per token
+    const int32_t* tok_row;    // dedup [n*nd]; naive [n*k]
+    __nv_bfloat16* dst_x;      // rows
+    int32_t* dst_ids;          // [rows*k]
+    float* dst_w;              // [rows*k]
+};
+void launch_pack(const PackArgs& a, cudaStream_t st);
+
+// BRIM1 (compute index) over inbox rows.
+struct ComputeArgs {
+    int R_max;                 // upper bound on inbox rows (grid sizing)
+    const int* R_total;        // device: actual rows (world=1: in_base[nd]; world>1: recv total)
+    int k, P, G;               // G local devices (world=1: nd; else 1)
+    const int32_t* row_ids;    // [R*k] routing ids carried with each row
+    const float* row_w;        // [R*k]
+    const int32_t* row_dev;    // [R] local device of row (null -> 0)
+    const int32_t* dev_of;     // [E]
+    const int32_t* slot_of;    // [E]
+    int dev_base;              // world>1: global device id of local device 0
+    uint64_t* mask;            // [R] out: local slot mask
+    int32_t* group;            // [R] out
+    int32_t* err;
+};
+void launch_compute_mask(const ComputeArgs& a, cudaStream_t st);
+
+struct ComputeOffsets {
+    int* cnt;          // [G*P] Epd rows per group (local device, slot)
+    int* seg_base;     // [G*P] padded Epd base per group
+    int* unp_base;     // [G*P] unpadded BRIM1 base per group (within device)
+    int* n_mblk;       // [1] total m-blocks
+    int* mblk_w;       // [max_mblk] weight index of each m-block
+    int* q_total;      // [1] padded Epd rows
+    const int32_t* widx;  // [G*P] weight index of each group
+    long long* stats;  // stats[6] += n_epd
+};
+void launch_compute_finalize(int G, int P, const int* totals, ComputeOffsets o, int max_mblk, cudaStream_t st);
+
+struct EmitCompute {
+    int k, P, dev_base;
+    const int32_t* row_ids;
+    const float* row_w;
+    const int32_t* slot_of;
+    const int32_t* dev_of;
+    ComputeOffsets o;
+    int32_t* row_epd;     // [R*P] padded Epd row per (row, slot)
+    int32_t* epd_src;     // [Q] inbox row feeding each padded Epd row
+    float* epd_w;         // [Q] routing weight of each Epd row
+};
+void launch_rank_emit_compute(int R_max, const int* R_total, const int32_t* group, const uint64_t* mask, int G,
+                              int B, RankWs ws, const EmitCompute& e, cudaStream_t st);
+void launch_init_epd(int Q_max, int32_t* epd_src, float* epd_w, cudaStream_t st);
+
+// Gather inbox rows into the padded Epd layout (GEMM-1 A operand).
+void launch_gather_rows(int Q_max, const int* q_total, const int32_t* epd_src, const __nv_bfloat16* src, int D,
+                        __nv_bfloat16* dst, cudaStream_t st);
+
+// Intra-device partial combine: ret[r] = bf16( sum_{p asc} Y[row_epd[r,p]] ).
+void launch_partial_combine(int R_max, const int* R_total, int P, int D, const int32_t* row_epd, const float* Y,
+                            __nv_bfloat16* ret, cudaStream_t st);
+// Final combine: out[t] = bf16( sum_{d asc} ret[row_of(t,d)] ).
+void launch_combine(int n, int nd, int k, int dedup, int D, const uint64_t* mask, const int32_t* tok_row,
+                    const __nv_bfloat16* ret, __nv_bfloat16* out, cudaStream_t st);
+
+// Saved-index extraction (parity): unpadded BRIM1 per device, P x R_d.
+void launch_extract_cindex(int R_max, const int* R_total, int P, const int32_t* row_dev, const int* in_base,
+                           const int32_t* row_epd, const ComputeOffsets& o, int32_t* cindex, cudaStream_t st);
+
+// Collaboration histogram (K8).
+void launch_histogram(const int32_t* ids, int n, int k, int e, int64_t* counts, cudaStream_t st);
+
+// Comm statistics (spans, pair shares, naive crossings) per token.
+void launch_token_stats(int n, int k, int nd, const int32_t* ids, const int32_t* sources, int src_fixed,
+                        const int32_t* dev_of, long long* stats, cudaStream_t st);
+
+// Routers.
+void launch_gate_scores_f64(const double* x, int n, int d, const double* g, int e, double* s, cudaStream_t st);
+void launch_topk_f64(const double* s, int n, int e, int k, int renorm, int32_t* ids, double* w, int32_t* err,
+                     cudaStream_t st);
+struct PruneDev {
+    int mode, budget, own_score, renorm, nd;
+    const int32_t* dev_of;   // [E]
+    const int32_t* ranking;  // [E*(E-1)] or null
+};
+void launch_prune_f64(const double* s, int n, int e, int k, const int32_t* ids_in, const double* w_in, PruneDev p,
+                      int32_t* ids, double* w, int32_t* err, cudaStream_t st);
+void launch_router_bf16(const __nv_bfloat16* x, const __nv_bfloat16* g, int n, int d, int e, int k, int renorm,
+                        PruneDev p, int32_t* ids, float* w, float* scores, float* logits_ws, int32_t* err,
+                        cudaStream_t st);
+
+// Weight layout conversion: reference [E, K, N] row-major -> K-major [E, N, K]
+// (optionally interleaving w1/w3 in 128-column blocks for SwiGLU).
+void launch_transpose_weights(const __nv_bfloat16* w, int E, int K, int N, __nv_bfloat16* out, int out_rows_per_e,
+                              int interleave_half, cudaStream_t st);
+
+// Grouped GEMM on tcgen05 (occ_gemm.cu).
+enum EpiMode { EPI_ACT_BF16 = 0, EPI_SWIGLU_BF16 = 1, EPI_F32 = 2 };
+struct GemmArgs {
+    const void* tmap_a;       // CUtensorMap* (host object, passed by value to the kernel)
+    const void* tmap_b;
+    int K;                    // reduction dim
+    int N;                    // output columns per expert (GEMM-1 SwiGLU: F; B rows per expert = 2F)
+    int b_rows_per_e;         // rows of B per expert in the stacked K-major weight matrix
+    const int* n_mblk;        // device
+    const int* mblk_w;        // device: weight index per m-block
+    const float* row_w;       // per padded Epd row routing weight (EPI_ACT/SWIGLU), null = 1
+    void* out;                // [Q, N] bf16 or f32
+    int ldo;                  // output row stride (elements)
+    int act;                  // occ_activation for EPI_ACT_BF16
+    int max_tiles;            // static upper bound (grid sizing)
+};
+void launch_grouped_gemm(EpiMode mode, const GemmArgs& a, int num_sms, cudaStream_t st);
+bool make_tmap_2d(void* tmap, const void* base, uint64_t inner, uint64_t outer, uint32_t box_inner,
+                  uint32_t box_outer);
+
+}  // namespace occ

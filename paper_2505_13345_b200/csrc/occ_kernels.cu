@@ -1,0 +1,1049 @@
+// occ_kernels.cu — HBM-bound kernels of the Occult EP path on sm_100a:
+// dispatch plan (BRIM0), pack (dispatch + exchange placement), compute
+// index (BRIM1), gather, intra-device partial combine, combine, the
+// co-activation histogram and the routers.  Citations are to
+// /root/reference/proj/<file>:<line>.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "occ_common.cuh"
+#include "occ_internal.h"
+
+namespace occ {
+
+long long g_launches = 0;
+
+namespace {
+
+constexpr int kRankThreads = kRankChunk;  // one item per thread, 8 warps
+constexpr int kRankWarps = kRankThreads / 32;
+
+__device__ __forceinline__ int item_valid(int i, int n_host, const int* n_dev) {
+    return i < (n_dev ? *n_dev : n_host);
+}
+
+// ------------------------------------------------------------- plan mask --
+// Per token (dedup) or per (token, slot) item (naive): source group and
+// destination-device mask.  Validates the routing like
+// RoutingOutcome::validate (routing.cpp:11-31).
+__global__ void plan_mask_kernel(PlanArgs a) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= a.n) return;
+    const int s = a.src_fixed >= 0 ? 0 : (a.sources ? a.sources[t] : t % a.nd);
+    if (s < 0 || s >= a.nd) { atomicExch(a.err, 1); return; }  // ShapeError: source out of range
+    uint64_t m = 0;
+    for (int j = 0; j < a.k; ++j) {
+        const int e = a.ids[(long)t * a.k + j];
+        const float wt = a.w ? a.w[(long)t * a.k + j] : 1.0f;
+        bool bad = e < 0 || e >= a.E || !(wt > 0.0f);
+        for (int l = 0; l < j && !bad; ++l) bad = a.ids[(long)t * a.k + l] == e;
+        if (bad) { atomicExch(a.err, 4); return; }  // RoutingError
+        const uint64_t bit = 1ull << a.dev_of[e];
+        if (a.dedup) m |= bit;
+        else { a.mask[(long)t * a.k + j] = bit; a.group[(long)t * a.k + j] = s; }
+    }
+    if (a.dedup) { a.mask[t] = m; a.group[t] = s; }
+}
+
+// ------------------------------------------------------ generic rank core --
+// Computes, for the calling warp, its per-key counts into wcnt[warp][key].
+__device__ __forceinline__ void warp_key_counts(int valid, int g, uint64_t m, int B, int K, int* wcnt, int warp,
+                                                int lane) {
+    const uint32_t same = __match_any_sync(0xffffffffu, valid ? g : -1);
+    const bool leader = (__ffs(same) - 1) == lane;
+    for (int b = 0; b < B; ++b) {
+        const uint32_t bal = __ballot_sync(0xffffffffu, valid && ((m >> b) & 1));
+        if (valid && leader) wcnt[warp * K + g * (B + 1) + b] = __popc(bal & same);
+    }
+    if (valid && leader) wcnt[warp * K + g * (B + 1) + B] = __popc(same);
+}
+
+__global__ void __launch_bounds__(kRankThreads) rank_count_kernel(int n, const int* n_dev, const int32_t* group,
+                                                                  const uint64_t* mask, int G, int B, int* chunk_cnt,
+                                                                  int nchunks) {
+    extern __shared__ int wcnt[];
+    const int K = G * (B + 1);
+    for (int i = threadIdx.x; i < kRankWarps * K; i += kRankThreads) wcnt[i] = 0;
+    __syncthreads();
+    const int i = blockIdx.x * kRankThreads + threadIdx.x;
+    const int valid = item_valid(i, n, n_dev);
+    const int g = valid ? group[i] : -1;
+    const uint64_t m = valid ? mask[i] : 0;
+    warp_key_counts(valid, g, m, B, K, wcnt, threadIdx.x >> 5, threadIdx.x & 31);
+    __syncthreads();
+    for (int key = threadIdx.x; key < K; key += kRankThreads) {
+        int s = 0;
+        for (int w = 0; w < kRankWarps; ++w) s += wcnt[w * K + key];
+        chunk_cnt[(long)key * nchunks + blockIdx.x] = s;
+    }
+}
+
+// One block per key: exclusive scan of the per-chunk counts.
+__global__ void __launch_bounds__(1024) rank_scan_kernel(int* chunk_cnt, int nchunks, int* totals) {
+    __shared__ int warp_sums[32];
+    const int key = blockIdx.x;
+    int* row = chunk_cnt + (long)key * nchunks;
+    const int per = (nchunks + 1023) / 1024;
+    const int c0 = threadIdx.x * per;
+    int local = 0;
+    for (int c = c0; c < c0 + per && c < nchunks; ++c) local += row[c];
+    // block exclusive scan of `local`
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int v = local;
+    for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += u;
+    }
+    if (lane == 31) warp_sums[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        int ws = warp_sums[lane];
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, ws, o);
+            if (lane >= o) ws += u;
+        }
+        warp_sums[lane] = ws;  // inclusive
+    }
+    __syncthreads();
+    int run = v - local + (warp ? warp_sums[warp - 1] : 0);
+    for (int c = c0; c < c0 + per && c < nchunks; ++c) {
+        const int x = row[c];
+        row[c] = run;
+        run += x;
+    }
+    if (threadIdx.x == 1023) totals[key] = run;
+}
+
+// Phase 3: in-chunk ranks, handed to an emitter.
+template <class Emit>
+__global__ void __launch_bounds__(kRankThreads) rank_emit_kernel(int n, const int* n_dev, const int32_t* group,
+                                                                 const uint64_t* mask, int G, int B,
+                                                                 const int* chunk_cnt, int nchunks, Emit em) {
+    extern __shared__ int wcnt[];
+    const int K = G * (B + 1);
+    for (int i = threadIdx.x; i < kRankWarps * K; i += kRankThreads) wcnt[i] = 0;
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int i = blockIdx.x * kRankThreads + threadIdx.x;
+    const int valid = item_valid(i, n, n_dev);
+    const int g = valid ? group[i] : -1;
+    const uint64_t m = valid ? mask[i] : 0;
+    warp_key_counts(valid, g, m, B, K, wcnt, warp, lane);
+    __syncthreads();
+    for (int key = threadIdx.x; key < K; key += kRankThreads) {
+        int run = chunk_cnt[(long)key * nchunks + blockIdx.x];
+        for (int w = 0; w < kRankWarps; ++w) {
+            const int x = wcnt[w * K + key];
+            wcnt[w * K + key] = run;
+            run += x;
+        }
+    }
+    __syncthreads();
+    const uint32_t same = __match_any_sync(0xffffffffu, valid ? g : -1);
+    const uint32_t lt = lanemask_lt();
+    if (valid) em.group_rank(i, g, wcnt[warp * K + g * (B + 1) + B] + __popc(same & lt));
+    for (int b = 0; b < B; ++b) {
+        const bool hit = valid && ((m >> b) & 1);
+        const uint32_t bal = __ballot_sync(0xffffffffu, hit);
+        if (hit) em.emit(i, g, b, wcnt[warp * K + g * (B + 1) + b] + __popc(bal & same & lt));
+        else if (valid) em.miss(i, b);
+    }
+}
+
+size_t rank_smem(int G, int B) { return sizeof(int) * (size_t)kRankWarps * G * (B + 1); }
+
+template <class Emit>
+void launch_rank_emit(int n_host, const int* n_dev, const int32_t* group, const uint64_t* mask, int G, int B,
+                      RankWs ws, const Emit& em, cudaStream_t st) {
+    const int nchunks = (n_host + kRankChunk - 1) / kRankChunk;
+    if (nchunks == 0) return;
+    const size_t smem = rank_smem(G, B);
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(rank_emit_kernel<Emit>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    rank_emit_kernel<Emit><<<nchunks, kRankThreads, smem, st>>>(n_host, n_dev, group, mask, G, B, ws.chunk_cnt,
+                                                                nchunks, em);
+    count_launch();
+}
+
+// ---------------------------------------------------------- dispatch plan --
+// From the per-key totals (key = s*(nd+1)+d) derive every offset of
+// build_dispatch_index (pipeline.cpp:24-50: counters device-major per
+// source) and all_to_all_exchange (pipeline.cpp:153-174: inbox of d is
+// ordered by (source asc, counter asc)).
+__global__ void dispatch_finalize_kernel(int nd, const int* totals, DispatchOffsets o) {
+    const int tid = threadIdx.x;
+    for (int i = tid; i < nd * nd; i += blockDim.x) {
+        const int s = i / nd, d = i % nd;
+        o.C[i] = totals[s * (nd + 1) + d];
+    }
+    __syncthreads();
+    if (tid < nd) {  // per source: row scan
+        const int s = tid;
+        int run = 0;
+        for (int d = 0; d < nd; ++d) {
+            o.off_sd[s * nd + d] = run;
+            run += o.C[s * nd + d];
+        }
+        o.nsfd[s] = run;
+        o.ntok[s] = totals[s * (nd + 1) + nd];
+    } else if (tid >= 64 && tid < 64 + nd) {  // per destination: column scan
+        const int d = tid - 64;
+        int run = 0;
+        for (int s = 0; s < nd; ++s) {
+            o.inoff[d * nd + s] = run;
+            run += o.C[s * nd + d];
+        }
+        o.in_base[d] = run;  // temporarily R_d
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int run = 0;
+        for (int d = 0; d < nd; ++d) {
+            const int r = o.in_base[d];
+            o.in_base[d] = run;
+            run += r;
+        }
+        o.in_base[nd] = run;
+        run = 0;
+        long long cross = 0;
+        for (int s = 0; s < nd; ++s) {
+            o.src_base[s] = run;
+            run += o.nsfd[s];
+            for (int d = 0; d < nd; ++d)
+                if (d != s) cross += o.C[s * nd + d];
+        }
+        o.src_base[nd] = run;
+        o.stats[0] = cross;
+        o.stats[5] = run;
+    }
+}
+
+__device__ __forceinline__ int token_source(const EmitDispatch& e, int t) {
+    return e.src_fixed >= 0 ? e.src_fixed : (e.sources ? e.sources[t] : t % e.nd);
+}
+
+struct DispatchEmitter {
+    EmitDispatch e;
+    __device__ void group_rank(int i, int, int r) {
+        if (e.dedup) e.lam[i] = r;
+    }
+    __device__ void emit(int i, int, int d, int r) {
+        const int t = e.dedup ? i : i / e.k;
+        const int s = token_source(e, t);
+        const int c = e.o.off_sd[s * e.nd + d] + r;  // BRIM0 counter
+        const long slot = e.dedup ? (long)t * e.nd + d : (long)i;
+        e.tok_sfd[slot] = c;
+        if (e.world1) {
+            const int row = e.o.in_base[d] + e.o.inoff[d * e.nd + s] + r;
+            e.tok_row[slot] = row;
+            e.in_tok[row] = t;
+            e.in_src[row] = s;
+            e.in_slot[row] = c;
+            e.in_dev[row] = d;
+        } else {
+            e.tok_row[slot] = c;  // send buffer is the Sfd batch (device-major)
+        }
+    }
+    __device__ void miss(int i, int d) {
+        if (!e.dedup) return;
+        e.tok_sfd[(long)i * e.nd + d] = -1;
+        e.tok_row[(long)i * e.nd + d] = -1;
+    }
+};
+
+// BRIM0 per source: nd x n_s, column = local token index.
+__global__ void extract_brim0_kernel(int n, int nd, const int32_t* sources, int src_fixed, const uint64_t* mask,
+                                     const int32_t* lam, const int32_t* tok_sfd, const int* src_tok_base,
+                                     const int* ntok, int32_t* brim0) {
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long)n * nd) return;
+    const int t = (int)(i / nd), d = (int)(i % nd);
+    const int s = src_fixed >= 0 ? 0 : (sources ? sources[t] : t % nd);
+    const long base = (long)src_tok_base[s] * nd;
+    brim0[base + (long)d * ntok[s] + lam[t]] = ((mask[t] >> d) & 1) ? tok_sfd[(long)t * nd + d] : -1;
+}
+
+// ------------------------------------------------------------------ pack ---
+// dispatch (pipeline.cpp:91-123) fused with the exchange placement
+// (pipeline.cpp:154-174): each token row is read once from HBM and written
+// to every destination row (one per device under dedup), with its routing
+// row alongside.  One warp per token, 16-byte vectors, 8 vectors in flight
+// per lane.
+__global__ void __launch_bounds__(256) pack_kernel(PackArgs a) {
+    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (warp >= a.n) return;
+    const int t = warp;
+    const int nvec = a.D / 8;
+    const uint4* src = reinterpret_cast<const uint4*>(a.x + (long)t * a.D);
+    int rows[kMaxDev];
+    int nrows = 0;
+    if (a.dedup) {
+        uint64_t m = a.mask[t];
+        while (m) {
+            const int d = __ffsll(m) - 1;
+            m &= m - 1;
+            rows[nrows++] = a.tok_row[(long)t * a.nd + d];
+        }
+    } else {
+        for (int j = 0; j < a.k; ++j) rows[nrows++] = a.tok_row[(long)t * a.k + j];
+    }
+    for (int v0 = 0; v0 < nvec; v0 += 8 * 32) {
+        uint4 buf[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int v = v0 + u * 32 + lane;
+            if (v < nvec) buf[u] = __ldg(src + v);
+        }
+        for (int q = 0; q < nrows; ++q) {
+            uint4* dst = reinterpret_cast<uint4*>(a.dst_x + (long)rows[q] * a.D);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int v = v0 + u * 32 + lane;
+                if (v < nvec) dst[v] = buf[u];
+            }
+        }
+    }
+    for (int q = 0; q < nrows; ++q) {
+        if (lane < a.k) {
+            const long di = (long)rows[q] * a.k + lane;
+            const bool keep = a.dedup || lane == q;  // naive rows carry only their own expert
+            a.dst_ids[di] = keep ? a.ids[(long)t * a.k + lane] : -1;
+            a.dst_w[di] = keep ? a.w[(long)t * a.k + lane] : 0.0f;
+        }
+    }
+}
+
+// -------------------------------------------------------- compute index ---
+// Per received Sfd row: local-expert mask in placement-list slots
+// (pipeline.cpp:409-421) and validation (build_compute_index rejects rows
+// with no local expert, pipeline.cpp:66-69).
+__global__ void compute_mask_kernel(ComputeArgs a) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= *a.R_total) return;
+    const int dl = a.row_dev ? a.row_dev[r] : 0;
+    const int gdev = a.dev_base + dl;
+    uint64_t m = 0;
+    for (int j = 0; j < a.k; ++j) {
+        const int e = a.row_ids[(long)r * a.k + j];
+        if (e >= 0 && a.dev_of[e] == gdev) m |= 1ull << a.slot_of[e];
+    }
+    if (!m) atomicExch(a.err, 4);
+    a.mask[r] = m;
+    a.group[r] = dl;
+}
+
+// Epd segment layout: group g = (local device, slot) in placement-list
+// order (pipeline.cpp:79-86, expert-major counters); each segment padded
+// to the GEMM M tile so no tile straddles two experts.
+__global__ void compute_finalize_kernel(int G, int P, const int* totals, ComputeOffsets o, int max_mblk) {
+    __shared__ int s_mb[1024];
+    __shared__ int s_mbbase[1024 + 1];
+    const int NG = G * P;
+    for (int g = threadIdx.x; g < NG; g += blockDim.x) {
+        const int d = g / P, p = g % P;
+        const int c = totals[d * (P + 1) + p];
+        o.cnt[g] = c;
+        s_mb[g] = (c + kBM - 1) / kBM;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int run = 0, mb = 0;
+        long long nepd = 0;
+        for (int g = 0; g < NG; ++g) {
+            o.seg_base[g] = run;
+            s_mbbase[g] = mb;
+            run += s_mb[g] * kBM;
+            mb += s_mb[g];
+            nepd += o.cnt[g];
+        }
+        s_mbbase[NG] = mb;
+        for (int d = 0; d < G; ++d) {
+            int u = 0;
+            for (int p = 0; p < P; ++p) {
+                o.unp_base[d * P + p] = u;
+                u += o.cnt[d * P + p];
+            }
+        }
+        *o.n_mblk = mb < max_mblk ? mb : max_mblk;
+        *o.q_total = run;
+        o.stats[6] += nepd;
+    }
+    __syncthreads();
+    for (int g = 0; g < NG; ++g)
+        for (int i = threadIdx.x; i < s_mb[g]; i += blockDim.x)
+            if (s_mbbase[g] + i < max_mblk) o.mblk_w[s_mbbase[g] + i] = o.widx[g];
+}
+
+struct ComputeEmitter {
+    EmitCompute e;
+    __device__ void group_rank(int, int, int) {}
+    __device__ void emit(int r, int g, int p, int rank) {
+        const int q = e.o.seg_base[g * e.P + p] + rank;
+        e.row_epd[(long)r * e.P + p] = q;
+        e.epd_src[q] = r;
+        float wt = 0.0f;
+        const int gdev = e.dev_base + g;
+        for (int j = 0; j < e.k; ++j) {
+            const int ex = e.row_ids[(long)r * e.k + j];
+            if (ex >= 0 && e.dev_of[ex] == gdev && e.slot_of[ex] == p) {
+                wt = e.row_w[(long)r * e.k + j];
+                break;
+            }
+        }
+        e.epd_w[q] = wt;
+    }
+    __device__ void miss(int r, int p) { e.row_epd[(long)r * e.P + p] = -1; }
+};
+
+__global__ void init_epd_kernel(int Q, int32_t* src, float* w) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < Q) { src[q] = -1; w[q] = 0.0f; }
+}
+
+// ---------------------------------------------------------------- gather --
+__global__ void __launch_bounds__(256) gather_rows_kernel(int Q_max, const int* q_total, const int32_t* epd_src,
+                                                          const __nv_bfloat16* src, int D, __nv_bfloat16* dst) {
+    const int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (q >= *q_total) return;
+    const int r = epd_src[q];
+    const int nvec = D / 8;
+    uint4* out = reinterpret_cast<uint4*>(dst + (long)q * D);
+    if (r < 0) {
+        for (int v = lane; v < nvec; v += 32) out[v] = make_uint4(0, 0, 0, 0);
+        return;
+    }
+    const uint4* in = reinterpret_cast<const uint4*>(src + (long)r * D);
+    for (int v0 = 0; v0 < nvec; v0 += 4 * 32) {
+        uint4 b[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (v0 + u * 32 + lane < nvec) b[u] = __ldg(in + v0 + u * 32 + lane);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (v0 + u * 32 + lane < nvec) out[v0 + u * 32 + lane] = b[u];
+    }
+}
+
+// ------------------------------------------------------- partial combine --
+// merge_matmul's per-row sum over local experts (pipeline.cpp:263-281),
+// done after the grouped GEMM: ascending placement-list order, fp32.
+__global__ void __launch_bounds__(256) partial_combine_kernel(int R_max, const int* R_total, int P, int D,
+                                                              const int32_t* row_epd, const float* Y,
+                                                              __nv_bfloat16* ret) {
+    const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (r >= *R_total) return;
+    int qs[kMaxLocal];
+    int nq = 0;
+    for (int p = 0; p < P; ++p) {
+        const int q = row_epd[(long)r * P + p];
+        if (q >= 0) qs[nq++] = q;
+    }
+    const int nv = D / 4;
+    for (int v = lane; v < nv; v += 32) {
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int i = 0; i < nq; ++i) {
+            const float4 y = __ldg(reinterpret_cast<const float4*>(Y + (long)qs[i] * D) + v);
+            acc.x += y.x; acc.y += y.y; acc.z += y.z; acc.w += y.w;
+        }
+        uint2 o;
+        o.x = pack_bf16(acc.x, acc.y);
+        o.y = pack_bf16(acc.z, acc.w);
+        reinterpret_cast<uint2*>(ret + (long)r * D)[v] = o;
+    }
+}
+
+// ---------------------------------------------------------------- combine --
+// combine (pipeline.cpp:285-300): Ori row = sum over devices ascending of
+// the returned rows; fp32 accumulation, bf16 out.
+__global__ void __launch_bounds__(256) combine_kernel(int n, int nd, int k, int dedup, int D, const uint64_t* mask,
+                                                      const int32_t* tok_row, const __nv_bfloat16* ret,
+                                                      __nv_bfloat16* out) {
+    const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (t >= n) return;
+    int rows[kMaxDev];
+    int nr = 0;
+    if (dedup) {
+        uint64_t m = mask[t];
+        while (m) {
+            const int d = __ffsll(m) - 1;
+            m &= m - 1;
+            rows[nr++] = tok_row[(long)t * nd + d];
+        }
+    } else {
+        for (int j = 0; j < k; ++j) rows[nr++] = tok_row[(long)t * k + j];
+    }
+    const int nv = D / 8;
+    for (int v = lane; v < nv; v += 32) {
+        float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int i = 0; i < nr; ++i) {
+            const uint4 u = __ldg(reinterpret_cast<const uint4*>(ret + (long)rows[i] * D) + v);
+            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float2 f = __bfloat1622float2(h[q]);
+                acc[2 * q] += f.x;
+                acc[2 * q + 1] += f.y;
+            }
+        }
+        uint4 o;
+        o.x = pack_bf16(acc[0], acc[1]);
+        o.y = pack_bf16(acc[2], acc[3]);
+        o.z = pack_bf16(acc[4], acc[5]);
+        o.w = pack_bf16(acc[6], acc[7]);
+        reinterpret_cast<uint4*>(out + (long)t * D)[v] = o;
+    }
+}
+
+__global__ void extract_cindex_kernel(int R_max, const int* R_total, int P, const int32_t* row_dev,
+                                      const int* in_base, const int32_t* row_epd, ComputeOffsets o, int32_t* cindex) {
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    const int R = *R_total;
+    if (i >= (long)R * P) return;
+    const int r = (int)(i / P), p = (int)(i % P);
+    const int d = row_dev ? row_dev[r] : 0;
+    const int base = in_base ? in_base[d] : 0;
+    const int Rd = (in_base ? in_base[d + 1] : R) - base;
+    const int q = row_epd[(long)r * P + p];
+    const int g = d * P + p;
+    const int v = q < 0 ? -1 : q - o.seg_base[g] + o.unp_base[g];
+    // per device: P x R_d block, blocks concatenated in device order
+    cindex[(long)base * P + (long)p * Rd + (r - base)] = v;
+}
+
+// ------------------------------------------------------------- histogram --
+// accumulate_collab (collab.cpp:10-23): privatised E x E counters in shared
+// memory, flushed with one 64-bit atomic per non-zero bin.
+__global__ void __launch_bounds__(256) histogram_kernel(const int32_t* ids, int n, int k, int e,
+                                                        unsigned long long* counts) {
+    extern __shared__ unsigned int h[];
+    for (int i = threadIdx.x; i < e * e; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        const int32_t* row = ids + (long)t * k;
+        for (int a = 0; a < k; ++a) {
+            const int ea = row[a];
+            for (int b = a + 1; b < k; ++b) {
+                const int eb = row[b];
+                atomicAdd(&h[ea * e + eb], 1u);
+                atomicAdd(&h[eb * e + ea], 1u);
+            }
+        }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < e * e; i += blockDim.x)
+        if (h[i]) atomicAdd(&counts[i], (unsigned long long)h[i]);
+}
+
+// ------------------------------------------------------------ token stats --
+// Per-pass accounting (CommReport, pipeline.cpp:479-487): device span
+// (mean_token_replicas, collab.cpp:41-61), co-activated pair shares
+// (collab.cpp:105-118) and naive replicate-k crossings
+// (test_simnet.cpp:167-180 brute force, per expert instead of per device).
+__global__ void token_stats_kernel(int n, int k, int nd, const int32_t* ids, const int32_t* sources, int src_fixed,
+                                   const int32_t* dev_of, long long* stats) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    long long span = 0, naive = 0, intra = 0, inter = 0;
+    if (t < n) {
+        const int s = src_fixed >= 0 ? src_fixed : (sources ? sources[t] : t % nd);
+        uint64_t m = 0;
+        for (int j = 0; j < k; ++j) {
+            const int d = dev_of[ids[(long)t * k + j]];
+            m |= 1ull << d;
+            naive += d != s;
+            for (int l = j + 1; l < k; ++l) {
+                if (dev_of[ids[(long)t * k + l]] == d) ++intra;
+                else ++inter;
+            }
+        }
+        span = __popcll(m);
+    }
+    for (int o = 16; o; o >>= 1) {
+        span += __shfl_xor_sync(0xffffffffu, span, o);
+        naive += __shfl_xor_sync(0xffffffffu, naive, o);
+        intra += __shfl_xor_sync(0xffffffffu, intra, o);
+        inter += __shfl_xor_sync(0xffffffffu, inter, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(&stats[1]), (unsigned long long)naive);
+        atomicAdd(reinterpret_cast<unsigned long long*>(&stats[2]), (unsigned long long)span);
+        atomicAdd(reinterpret_cast<unsigned long long*>(&stats[3]), (unsigned long long)intra);
+        atomicAdd(reinterpret_cast<unsigned long long*>(&stats[4]), (unsigned long long)inter);
+    }
+}
+
+// ------------------------------------------------------- routers (fp64) --
+// gate_scores (routing.cpp:33-52) in exact mode: one thread per (token,
+// expert), sequential ascending-k double accumulation without FMA
+// (matrix.cpp:25-31), then per-row max-subtracted softmax.
+__global__ void gate_logits_f64_kernel(const double* x, int n, int d, const double* g, int e, double* s) {
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long)n * e) return;
+    const int t = (int)(i / e), j = (int)(i % e);
+    double acc = 0.0;
+    for (int c = 0; c < d; ++c) acc = __dadd_rn(acc, __dmul_rn(x[(long)t * d + c], g[(long)j * d + c]));
+    s[i] = acc;
+}
+__global__ void softmax_f64_kernel(int n, int e, double* s) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    double* row = s + (long)t * e;
+    double mx = row[0];
+    for (int j = 1; j < e; ++j) mx = row[j] > mx ? row[j] : mx;
+    double sum = 0.0;
+    for (int j = 0; j < e; ++j) {
+        row[j] = exp(__dsub_rn(row[j], mx));
+        sum = __dadd_rn(sum, row[j]);
+    }
+    for (int j = 0; j < e; ++j) row[j] = __ddiv_rn(row[j], sum);
+}
+
+template <class T>
+__device__ __forceinline__ bool score_before(const T* row, int a, int b) {
+    if (row[a] != row[b]) return row[a] > row[b];
+    return a < b;
+}
+
+// Selection of the k best under (score desc, index asc): identical to
+// std::partial_sort with the reference comparator (routing.cpp:71-74).
+template <class T>
+__device__ void select_topk(const T* row, int e, int k, int* out) {
+    for (int j = 0; j < k; ++j) {
+        int best = -1;
+        for (int c = 0; c < e; ++c) {
+            bool taken = false;
+            for (int l = 0; l < j; ++l) taken |= out[l] == c;
+            if (taken) continue;
+            if (best < 0 || score_before(row, c, best)) best = c;
+        }
+        out[j] = best;
+    }
+}
+
+template <class T>
+__device__ bool renorm_row(T* w, int k) {  // renormalize_row, routing.cpp:54-58
+    T sum = 0;
+    for (int j = 0; j < k; ++j) sum += w[j];
+    if (!(sum > 0)) return false;
+    for (int j = 0; j < k; ++j) w[j] = w[j] / sum;
+    return true;
+}
+
+__global__ void topk_f64_kernel(const double* s, int n, int e, int k, int renorm, int32_t* ids, double* w,
+                                int32_t* err) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    const double* row = s + (long)t * e;
+    int sel[256];
+    select_topk(row, e, k, sel);
+    double wt[256];
+    for (int j = 0; j < k; ++j) wt[j] = row[sel[j]];
+    if (renorm && !renorm_row(wt, k)) atomicExch(err, 4);
+    for (int j = 0; j < k; ++j) {
+        ids[(long)t * k + j] = sel[j];
+        w[(long)t * k + j] = wt[j];
+    }
+}
+
+// ------------------------------------------------------------- pruning ---
+// allowed_devices (pruning.cpp:21-33): first `budget` distinct devices in
+// the given order.
+__device__ int allowed_devices(const int* ids, int k, const int32_t* dev_of, int budget, int* devs) {
+    int na = 0;
+    for (int j = 0; j < k; ++j) {
+        const int d = dev_of[ids[j]];
+        bool found = false;
+        for (int i = 0; i < na; ++i) found |= devs[i] == d;
+        if (!found) {
+            if (na == budget) break;
+            devs[na++] = d;
+        }
+    }
+    return na;
+}
+
+// prune_router_score (pruning.cpp:35-64) / prune_similarity (:66-122) for
+// one token.  Returns 0 or an occ_status.
+template <class T>
+__device__ int prune_token(const T* row, int e, int k, const int* ids_in, const PruneDev& p, int* ids, T* w) {
+    int devs[kMaxDev];
+    bool in_range[kMaxDev];
+    for (int d = 0; d < p.nd; ++d) in_range[d] = false;
+    if (p.mode == 1) {
+        int top[256];
+        select_topk(row, e, k, top);
+        const int na = allowed_devices(top, k, p.dev_of, p.budget, devs);
+        for (int i = 0; i < na; ++i) in_range[devs[i]] = true;
+        // walk experts in full score order, keep those on allowed devices
+        int m = 0;
+        int last = -1;
+        while (m < k) {
+            int best = -1;
+            for (int c = 0; c < e; ++c) {
+                if (!in_range[p.dev_of[c]]) continue;
+                if (last >= 0 && !score_before(row, last, c)) continue;  // strictly after `last`
+                if (best < 0 || score_before(row, c, best)) best = c;
+            }
+            if (best < 0) return 5;  // CapacityError
+            ids[m] = best;
+            w[m] = row[best];
+            last = best;
+            ++m;
+        }
+        if (p.renorm && !renorm_row(w, k)) return 4;
+        return 0;
+    }
+    // similarity
+    const int na = allowed_devices(ids_in, k, p.dev_of, p.budget, devs);
+    for (int i = 0; i < na; ++i) in_range[devs[i]] = true;
+    bool selected[256];
+    for (int c = 0; c < e; ++c) selected[c] = false;
+    bool replaced[256];
+    for (int j = 0; j < k; ++j)
+        if (in_range[p.dev_of[ids_in[j]]]) selected[ids_in[j]] = true;
+    for (int j = 0; j < k; ++j) {
+        const int ex = ids_in[j];
+        replaced[j] = false;
+        if (in_range[p.dev_of[ex]]) { ids[j] = ex; continue; }
+        int pick = -1;
+        for (int c = 0; c < e - 1; ++c) {
+            const int cand = p.ranking[(long)ex * (e - 1) + c];
+            if (!in_range[p.dev_of[cand]] || selected[cand]) continue;
+            pick = cand;
+            break;
+        }
+        if (pick < 0) return 5;
+        selected[pick] = true;
+        ids[j] = pick;
+        replaced[j] = true;
+    }
+    // pruned_weight_policy (pruning.cpp:124-139): originals are raw scores
+    for (int j = 0; j < k; ++j) w[j] = (p.own_score && replaced[j]) ? row[ids[j]] : row[ids_in[j]];
+    if (p.renorm && !renorm_row(w, k)) return 4;
+    if (p.own_score) {  // pruning.cpp:106-119: (weight desc, id asc)
+        for (int i = 1; i < k; ++i) {
+            const int vi = ids[i];
+            const T vw = w[i];
+            int q = i - 1;
+            while (q >= 0 && (vw > w[q] || (vw == w[q] && vi < ids[q]))) {
+                ids[q + 1] = ids[q];
+                w[q + 1] = w[q];
+                --q;
+            }
+            ids[q + 1] = vi;
+            w[q + 1] = vw;
+        }
+    }
+    return 0;
+}
+
+__global__ void prune_f64_kernel(const double* s, int n, int e, int k, const int32_t* ids_in, const double* w_in,
+                                 PruneDev p, int32_t* ids, double* w, int32_t* err) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    if (p.mode == 0) {
+        for (int j = 0; j < k; ++j) {
+            ids[(long)t * k + j] = ids_in[(long)t * k + j];
+            w[(long)t * k + j] = w_in[(long)t * k + j];
+        }
+        return;
+    }
+    int in[256], oi[256];
+    double ow[256];
+    for (int j = 0; j < k; ++j) in[j] = ids_in[(long)t * k + j];
+    const int rc = prune_token(s + (long)t * e, e, k, in, p, oi, ow);
+    if (rc) { atomicExch(err, rc); return; }
+    for (int j = 0; j < k; ++j) {
+        ids[(long)t * k + j] = oi[j];
+        w[(long)t * k + j] = ow[j];
+    }
+}
+
+// ------------------------------------------------- production router ---
+// logits[t, j] = sum_c x[t,c] g[j,c]: bf16 inputs, fp32 accumulation.
+// Block tile: 32 tokens x 64 experts, D staged through shared memory.
+constexpr int kRT = 32, kRE = 64, kRK = 64;
+__global__ void __launch_bounds__(256) router_logits_kernel(const __nv_bfloat16* x, const __nv_bfloat16* g, int n,
+                                                            int d, int e, float* logits) {
+    __shared__ float xs[kRT][kRK + 1];
+    __shared__ float gs[kRE][kRK + 1];
+    const int t0 = blockIdx.x * kRT, e0 = blockIdx.y * kRE;
+    const int tid = threadIdx.x;
+    const int tr = tid / 16, ec = tid % 16;  // each thread: 2 tokens x 4 experts
+    float acc[2][4] = {};
+    for (int k0 = 0; k0 < d; k0 += kRK) {
+        for (int i = tid; i < kRT * kRK; i += 256) {
+            const int r = i / kRK, c = i % kRK;
+            xs[r][c] = (t0 + r < n && k0 + c < d) ? __bfloat162float(x[(long)(t0 + r) * d + k0 + c]) : 0.f;
+        }
+        for (int i = tid; i < kRE * kRK; i += 256) {
+            const int r = i / kRK, c = i % kRK;
+            gs[r][c] = (e0 + r < e && k0 + c < d) ? __bfloat162float(g[(long)(e0 + r) * d + k0 + c]) : 0.f;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int c = 0; c < kRK; ++c) {
+            const float a0 = xs[tr * 2][c], a1 = xs[tr * 2 + 1][c];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float b = gs[ec + 16 * q][c];
+                acc[0][q] = fmaf(a0, b, acc[0][q]);
+                acc[1][q] = fmaf(a1, b, acc[1][q]);
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int t = t0 + tr * 2 + r, j = e0 + ec + 16 * q;
+            if (t < n && j < e) logits[(long)t * e + j] = acc[r][q];
+        }
+}
+
+// softmax + top-k + renormalise (+ pruning) per token, fp32.
+__global__ void router_select_kernel(float* logits, int n, int e, int k, int renorm, PruneDev p, int32_t* ids,
+                                     float* w, float* scores, int32_t* err) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    float* row = logits + (long)t * e;
+    float mx = row[0];
+    for (int j = 1; j < e; ++j) mx = fmaxf(mx, row[j]);
+    float sum = 0.f;
+    for (int j = 0; j < e; ++j) {
+        row[j] = __expf(row[j] - mx);
+        sum += row[j];
+    }
+    const float inv = 1.0f / sum;
+    for (int j = 0; j < e; ++j) row[j] *= inv;
+    if (scores)
+        for (int j = 0; j < e; ++j) scores[(long)t * e + j] = row[j];
+    int sel[256];
+    float wt[256];
+    select_topk(row, e, k, sel);
+    if (p.mode != 0) {
+        int oi[256];
+        const int rc = prune_token(row, e, k, sel, p, oi, wt);
+        if (rc) { atomicExch(err, rc); return; }
+        for (int j = 0; j < k; ++j) sel[j] = oi[j];
+    } else {
+        for (int j = 0; j < k; ++j) wt[j] = row[sel[j]];
+        if (renorm && !renorm_row(wt, k)) atomicExch(err, 4);
+    }
+    for (int j = 0; j < k; ++j) {
+        ids[(long)t * k + j] = sel[j];
+        w[(long)t * k + j] = wt[j];
+    }
+}
+
+// -------------------------------------------------- weight re-layout ---
+// Reference expert matrices are [K, N] row-major (token.hpp:30-44); the
+// tensor-core path wants them K-major ([N, K]).  For SwiGLU the w1/w3 rows
+// are interleaved in 128-row blocks so one 256-row B tile holds matching
+// gate/up columns.
+__global__ void transpose_weights_kernel(const __nv_bfloat16* w, int K, int N, __nv_bfloat16* out, int out_rows_per_e,
+                                         int interleave_half) {
+    __shared__ __nv_bfloat16 tile[32][33];
+    const int e = blockIdx.z;
+    const int n0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
+    const __nv_bfloat16* src = w + (long)e * K * N;
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int kk = k0 + i, nn = n0 + threadIdx.x;
+        if (kk < K && nn < N) tile[i][threadIdx.x] = src[(long)kk * N + nn];
+    }
+    __syncthreads();
+    for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+        const int nn = n0 + i, kk = k0 + threadIdx.x;
+        if (kk < K && nn < N) {
+            long orow = nn;
+            if (interleave_half) orow = (long)(nn / 128) * 256 + (interleave_half - 1) * 128 + nn % 128;
+            out[((long)e * out_rows_per_e + orow) * K + kk] = tile[threadIdx.x][i];
+        }
+    }
+}
+
+}  // namespace
+
+// ================================================================ launchers
+void launch_plan_mask(const PlanArgs& a, cudaStream_t st) {
+    if (a.n == 0) return;
+    plan_mask_kernel<<<(a.n + 255) / 256, 256, 0, st>>>(a);
+    count_launch();
+}
+
+void launch_rank_count(int n_items, const int32_t* group, const uint64_t* mask, int G, int B, RankWs ws,
+                       cudaStream_t st) {
+    const int nchunks = (n_items + kRankChunk - 1) / kRankChunk;
+    if (nchunks == 0) return;
+    const size_t smem = rank_smem(G, B);
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(rank_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    rank_count_kernel<<<nchunks, kRankThreads, smem, st>>>(n_items, nullptr, group, mask, G, B, ws.chunk_cnt, nchunks);
+    count_launch();
+}
+
+void launch_rank_count_dev(int n_max, const int* n_dev, const int32_t* group, const uint64_t* mask, int G, int B,
+                           RankWs ws, cudaStream_t st) {
+    const int nchunks = (n_max + kRankChunk - 1) / kRankChunk;
+    if (nchunks == 0) return;
+    const size_t smem = rank_smem(G, B);
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(rank_count_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    rank_count_kernel<<<nchunks, kRankThreads, smem, st>>>(n_max, n_dev, group, mask, G, B, ws.chunk_cnt, nchunks);
+    count_launch();
+}
+
+void launch_rank_scan(int n_items, int G, int B, RankWs ws, cudaStream_t st) {
+    const int nchunks = (n_items + kRankChunk - 1) / kRankChunk;
+    const int K = G * (B + 1);
+    if (nchunks == 0) {
+        cudaMemsetAsync(ws.totals, 0, sizeof(int) * K, st);
+        return;
+    }
+    rank_scan_kernel<<<K, 1024, 0, st>>>(ws.chunk_cnt, nchunks, ws.totals);
+    count_launch();
+}
+
+void launch_dispatch_finalize(int nd, const int* totals, DispatchOffsets o, cudaStream_t st) {
+    dispatch_finalize_kernel<<<1, 128, 0, st>>>(nd, totals, o);
+    count_launch();
+}
+
+void launch_rank_emit_dispatch(int n_items, const int32_t* group, const uint64_t* mask, int G, int B, RankWs ws,
+                               const EmitDispatch& e, cudaStream_t st) {
+    launch_rank_emit(n_items, nullptr, group, mask, G, B, ws, DispatchEmitter{e}, st);
+}
+
+void launch_extract_brim0(int n, int nd, const int32_t* sources, int src_fixed, const uint64_t* mask,
+                          const int32_t* lam, const int32_t* tok_sfd, const int* src_tok_base, int32_t* brim0,
+                          cudaStream_t st) {
+    // src_tok_base holds [nd] prefix of tokens per source followed by ntok[nd]
+    const long total = (long)n * nd;
+    if (!total) return;
+    extract_brim0_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(n, nd, sources, src_fixed, mask, lam,
+                                                                            tok_sfd, src_tok_base,
+                                                                            src_tok_base + nd, brim0);
+    count_launch();
+}
+
+void launch_pack(const PackArgs& a, cudaStream_t st) {
+    if (a.n == 0) return;
+    pack_kernel<<<(a.n + 7) / 8, 256, 0, st>>>(a);
+    count_launch();
+}
+
+void launch_compute_mask(const ComputeArgs& a, cudaStream_t st) {
+    if (a.R_max == 0) return;
+    compute_mask_kernel<<<(a.R_max + 255) / 256, 256, 0, st>>>(a);
+    count_launch();
+}
+
+void launch_compute_finalize(int G, int P, const int* totals, ComputeOffsets o, int max_mblk, cudaStream_t st) {
+    compute_finalize_kernel<<<1, 256, 0, st>>>(G, P, totals, o, max_mblk);
+    count_launch();
+}
+
+void launch_rank_emit_compute(int R_max, const int* R_total, const int32_t* group, const uint64_t* mask, int G,
+                              int B, RankWs ws, const EmitCompute& e, cudaStream_t st) {
+    launch_rank_emit(R_max, R_total, group, mask, G, B, ws, ComputeEmitter{e}, st);
+}
+
+void launch_init_epd(int Q_max, int32_t* epd_src, float* epd_w, cudaStream_t st) {
+    if (!Q_max) return;
+    init_epd_kernel<<<(Q_max + 255) / 256, 256, 0, st>>>(Q_max, epd_src, epd_w);
+    count_launch();
+}
+
+void launch_gather_rows(int Q_max, const int* q_total, const int32_t* epd_src, const __nv_bfloat16* src, int D,
+                        __nv_bfloat16* dst, cudaStream_t st) {
+    if (!Q_max) return;
+    gather_rows_kernel<<<(Q_max + 7) / 8, 256, 0, st>>>(Q_max, q_total, epd_src, src, D, dst);
+    count_launch();
+}
+
+void launch_partial_combine(int R_max, const int* R_total, int P, int D, const int32_t* row_epd, const float* Y,
+                            __nv_bfloat16* ret, cudaStream_t st) {
+    if (!R_max) return;
+    partial_combine_kernel<<<(R_max + 7) / 8, 256, 0, st>>>(R_max, R_total, P, D, row_epd, Y, ret);
+    count_launch();
+}
+
+void launch_combine(int n, int nd, int k, int dedup, int D, const uint64_t* mask, const int32_t* tok_row,
+                    const __nv_bfloat16* ret, __nv_bfloat16* out, cudaStream_t st) {
+    if (!n) return;
+    combine_kernel<<<(n + 7) / 8, 256, 0, st>>>(n, nd, k, dedup, D, mask, tok_row, ret, out);
+    count_launch();
+}
+
+void launch_extract_cindex(int R_max, const int* R_total, int P, const int32_t* row_dev, const int* in_base,
+                           const int32_t* row_epd, const ComputeOffsets& o, int32_t* cindex, cudaStream_t st) {
+    const long total = (long)R_max * P;
+    if (!total) return;
+    extract_cindex_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(R_max, R_total, P, row_dev, in_base,
+                                                                             row_epd, o, cindex);
+    count_launch();
+}
+
+void launch_histogram(const int32_t* ids, int n, int k, int e, int64_t* counts, cudaStream_t st) {
+    if (!n) return;
+    int blocks = (n + 255) / 256;
+    if (blocks > 148 * 4) blocks = 148 * 4;
+    const size_t smem = sizeof(unsigned) * (size_t)e * e;
+    if (smem > 48 * 1024)
+        cudaFuncSetAttribute(histogram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    histogram_kernel<<<blocks, 256, smem, st>>>(ids, n, k, e, reinterpret_cast<unsigned long long*>(counts));
+    count_launch();
+}
+
+void launch_token_stats(int n, int k, int nd, const int32_t* ids, const int32_t* sources, int src_fixed,
+                        const int32_t* dev_of, long long* stats, cudaStream_t st) {
+    if (!n) return;
+    token_stats_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, k, nd, ids, sources, src_fixed, dev_of, stats);
+    count_launch();
+}
+
+void launch_gate_scores_f64(const double* x, int n, int d, const double* g, int e, double* s, cudaStream_t st) {
+    const long total = (long)n * e;
+    if (!total) return;
+    gate_logits_f64_kernel<<<(unsigned)((total + 127) / 128), 128, 0, st>>>(x, n, d, g, e, s);
+    softmax_f64_kernel<<<(n + 127) / 128, 128, 0, st>>>(n, e, s);
+    count_launch(2);
+}
+
+void launch_topk_f64(const double* s, int n, int e, int k, int renorm, int32_t* ids, double* w, int32_t* err,
+                     cudaStream_t st) {
+    if (!n) return;
+    topk_f64_kernel<<<(n + 127) / 128, 128, 0, st>>>(s, n, e, k, renorm, ids, w, err);
+    count_launch();
+}
+
+void launch_prune_f64(const double* s, int n, int e, int k, const int32_t* ids_in, const double* w_in, PruneDev p,
+                      int32_t* ids, double* w, int32_t* err, cudaStream_t st) {
+    if (!n) return;
+    prune_f64_kernel<<<(n + 127) / 128, 128, 0, st>>>(s, n, e, k, ids_in, w_in, p, ids, w, err);
+    count_launch();
+}
+
+void launch_router_bf16(const __nv_bfloat16* x, const __nv_bfloat16* g, int n, int d, int e, int k, int renorm,
+                        PruneDev p, int32_t* ids, float* w, float* scores, float* logits_ws, int32_t* err,
+                        cudaStream_t st) {
+    if (!n) return;
+    dim3 grid((n + kRT - 1) / kRT, (e + kRE - 1) / kRE);
+    router_logits_kernel<<<grid, 256, 0, st>>>(x, g, n, d, e, logits_ws);
+    router_select_kernel<<<(n + 127) / 128, 128, 0, st>>>(logits_ws, n, e, k, renorm, p, ids, w, scores, err);
+    count_launch(2);
+}
+
+void launch_transpose_weights(const __nv_bfloat16* w, int E, int K, int N, __nv_bfloat16* out, int out_rows_per_e,
+                              int interleave_half, cudaStream_t st) {
+    dim3 grid((N + 31) / 32, (K + 31) / 32, E);
+    transpose_weights_kernel<<<grid, dim3(32, 8), 0, st>>>(w, K, N, out, out_rows_per_e, interleave_half);
+    count_launch();
+}
+
+}  // namespace occ
