@@ -1,0 +1,391 @@
+#!/usr/bin/env python3
+"""Benchmark of the Occult expert-parallel MoE layer on B200.
+
+Metric (BASELINE.json): MoE layer tokens/s at 1/2/4/8 B200; all-to-all
+bytes/token vs naive top-k.  Workload: the Mixtral-8x7B MoE layer
+(BASELINE configs[1]: 8 experts top-2, d=4096, ffn=14336, SwiGLU) prefilling
+16,384 tokens; EP degree = number of GPUs; synthetic tokens and random-init
+experts of that shape.  One step = route (gate GEMV, softmax, top-2) +
+dispatch plan + pack/exchange + grouped SwiGLU FFN + intra-device partial
+combine + return + combine, over one 16k-token batch.
+
+Arms:
+  default            this package's sm_100a path (C-ABI via the Python mirror)
+  --impl reference   the reference's own CPU implementation (oracle/_ref,
+                     compiled from /root/reference sources) on the host cores
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MoE layer tokens/s at 1/2/4/8 B200; all-to-all bytes/token vs naive top-k"
+E, K_TOP, D, F = 8, 2, 4096, 14336
+TOKENS = 16384
+WORKLOAD = "Mixtral-8x7B MoE layer (8 experts top-2, d=4096, ffn=14336, SwiGLU) prefill 16384 tokens, EP=#GPUs"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.15)
+        self.proc.terminate()
+        self.proc.wait()
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        with open(self.path) as f:
+            for line in f:
+                c = [x.strip() for x in line.split(",")]
+                if len(c) < 9:
+                    continue
+                try:
+                    sm.append(float(c[1]))
+                    mx = max(mx, float(c[2]))
+                except ValueError:
+                    continue
+                for nm, v in zip(names, c[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        os.unlink(self.path)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "samples": len(sm), "reasons": sorted(reasons)}
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ----------------------------------------------------------- reference arm --
+def reference_sample(threads, tokens_per_thread, seed=1):
+    """Mixtral-shaped layer on the reference CPU path.  The reference has no
+    gated experts, so its closest layer is the 2-matrix SiLU
+    expert at the same shape (2/3 of the SwiGLU FLOPs)."""
+    import numpy as np
+    from oracle import oracle as O
+    rng = np.random.default_rng(seed)
+    n = threads * tokens_per_thread
+    x = rng.uniform(-1, 1, (n, D))
+    g = rng.uniform(-1, 1, (E, D)) * (3.0 / np.sqrt(D))
+    w1 = rng.uniform(-1, 1, (E, D, F)) / np.sqrt(D)
+    w2 = rng.uniform(-1, 1, (E, F, D)) / np.sqrt(F)
+    return O, x, g, w1, w2
+
+
+def run_reference_arm(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import ctypes as C
+
+    import numpy as np
+    threads = os.cpu_count() or 1
+    tpt = args.ref_tokens_per_thread
+    O, x, g, w1, w2 = reference_sample(threads, tpt)
+    L = O.ref_lib()
+    n = x.shape[0]
+    out = np.empty_like(x)
+    P = lambda a: a.ctypes.data_as(C.c_void_p)
+
+    def step():
+        t0 = time.perf_counter()
+        rc = L.ref_forward_expert_parallel_mt(P(x), n, D, P(g), E, K_TOP, P(w1), P(w2), F, 8, 1, 1, threads, P(out))
+        if rc < 0:
+            raise RuntimeError(f"reference failed: status {-rc}")
+        return time.perf_counter() - t0
+
+    for _ in range(args.warmup):
+        step()
+    times = [step() for _ in range(args.steps)]
+    tot = sum(times)
+    value = n * args.steps / tot
+    sample = (f"{n} tokens/step ({tpt} per thread x {threads} threads) through gate_scores + topk_route + "
+              f"forward_given_routing (reference sources, g++ -O2), 2-matrix SiLU experts at d=4096, ffn=14336, "
+              f"EP=8 simulated (reference has no gated experts)")
+    line = {"metric": METRIC, "impl": "reference", "value": value, "unit": "tokens/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "experts": E, "top_k": K_TOP, "d_model": D, "d_ff": F,
+                       "tokens_per_step": n},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads, "kind": "reference",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_port_baseline(seconds_target=15.0):
+    """The oracle restatement (SwiGLU-capable, the reference's loops) on all
+    host cores: same workload shape, bounded token sample."""
+    import ctypes as C
+
+    import numpy as np
+    from oracle import oracle as O
+    threads = os.cpu_count() or 1
+    rng = np.random.default_rng(7)
+    w1 = rng.uniform(-1, 1, (E, D, F)) / np.sqrt(D)
+    w3 = rng.uniform(-1, 1, (E, D, F)) / np.sqrt(D)
+    w2 = rng.uniform(-1, 1, (E, F, D)) / np.sqrt(F)
+    lib = O.port_lib()
+    plist = np.arange(E, dtype=np.int32).reshape(1, E)
+    P = lambda a: None if a is None else a.ctypes.data_as(C.c_void_p)
+
+    def chunk(tokens, out_times, idx):
+        x = rng.uniform(-1, 1, (tokens, D))
+        ids = np.stack([np.random.default_rng(idx * 1000 + t).permutation(E)[:K_TOP] for t in range(tokens)])
+        ids = ids.astype(np.int32)
+        w = np.full((tokens, K_TOP), 0.5)
+        src = np.zeros(tokens, np.int32)
+        y = np.empty_like(x)
+        rep = O.Report()
+        t0 = time.perf_counter()
+        lib.orc_forward_given_routing(P(x), tokens, D, P(ids), P(w), K_TOP, P(w1), P(w2), P(w3), E, F, P(plist), 1,
+                                      P(src), 1, 1, 2, -1.0, P(y), C.byref(rep), None, None, None, None, None)
+        out_times[idx] = time.perf_counter() - t0
+
+    # calibrate on one token, then size the sample to ~seconds_target
+    t = [0.0]
+    chunk(1, t, 0)
+    per_tok = max(t[0], 1e-3)
+    tpt = max(1, int(seconds_target / per_tok))
+    times = [0.0] * threads
+    ths = [threading.Thread(target=chunk, args=(tpt, times, i)) for i in range(threads)]
+    t0 = time.perf_counter()
+    for th in ths:
+        th.start()
+    for th in ths:
+        th.join()
+    wall = time.perf_counter() - t0
+    n = tpt * threads
+    return {"value": n / wall, "unit": "tokens/s", "cores": threads, "kind": "port",
+            "sample": f"{n} tokens ({tpt} per thread x {threads} threads) of the SwiGLU layer at d=4096, ffn=14336, "
+                      f"top-2 of 8, EP=1, oracle/occ_oracle.c (fp64, the reference's loop order), wall {wall:.1f} s"}
+
+
+# ----------------------------------------------------------------- our arm --
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import paper_2505_13345_b200 as occ
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    peaks, peaks_src = load_peaks()
+    n_local = args.tokens // world
+    torch.manual_seed(1234 + rank)
+
+    cfg = occ.MoEConfig(E, K_TOP, world, D, F, activation="swiglu")
+    layer = occ.ExpertParallelLayer(cfg, world_size=world, rank=rank)
+    if world > 1:
+        layer.comm_init()
+    e_local = E if world == 1 else E // world
+    w1 = torch.empty((e_local, D, F), dtype=torch.bfloat16, device=dev).uniform_(-1, 1).mul_(D ** -0.5)
+    w3 = torch.empty((e_local, D, F), dtype=torch.bfloat16, device=dev).uniform_(-1, 1).mul_(D ** -0.5)
+    w2 = torch.empty((e_local, F, D), dtype=torch.bfloat16, device=dev).uniform_(-1, 1).mul_(F ** -0.5)
+    layer.load_experts(w1, w2, w3)
+    del w1, w2, w3
+    torch.cuda.empty_cache()
+    gate = torch.empty((E, D), dtype=torch.bfloat16, device=dev).uniform_(-1, 1).mul_(3.0 / D ** 0.5)
+    x = torch.empty((n_local, D), dtype=torch.bfloat16, device=dev).uniform_(-1, 1)
+    out = torch.empty_like(x)
+    layer.set_validate(False)
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def step():
+        layer.forward_expert_parallel(x, gate, out=out)
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    clocks.start()
+    l0 = occ.launch_count()
+    barrier()
+    for i in range(args.steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    barrier()
+    launches = occ.launch_count() - l0
+    clk = clocks.stop()
+    step_ms = [a.elapsed_time(b) for a, b in ev]
+    tot_ms = sum(step_ms)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([tot_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+    value = args.tokens * args.steps / (tot_ms / 1e3)
+
+    # --- end to end through the public API with host buffers -------------
+    xh = torch.empty_like(x, device="cpu").pin_memory()
+    xh.copy_(x)
+    oh = torch.empty_like(xh).pin_memory()
+    for _ in range(2):
+        x.copy_(xh, non_blocking=True)
+        step()
+        oh.copy_(out, non_blocking=True)
+    barrier()
+    ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    for i in range(args.steps):
+        flush.zero_()
+        ev2[i][0].record(stream)
+        x.copy_(xh, non_blocking=True)
+        step()
+        oh.copy_(out, non_blocking=True)
+        ev2[i][1].record(stream)
+    barrier()
+    e2e_ms = sum(a.elapsed_time(b) for a, b in ev2)
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e = {"value": args.tokens * args.steps / (e2e_ms / 1e3), "unit": "tokens/s",
+           "h2d_bytes_per_step": x.numel() * x.element_size(), "d2h_bytes_per_step": out.numel() * out.element_size()}
+
+    # --- stage profile (CUDA events on the launching stream) --------------
+    layer.set_profiling(True)
+    acc = {}
+    for i in range(args.steps):
+        flush.zero_()
+        step()
+        for kk, v in layer.stage_ms().items():
+            acc.setdefault(kk, []).append(v)
+    layer.set_profiling(False)
+    stages = {kk: statistics.mean(v) for kk, v in acc.items()}
+    rep = layer.comm_report(bytes_per_scalar=2)
+    n_epd = rep.n_epd
+    flops1 = 2.0 * n_epd * D * (2 * F)
+    flops2 = 2.0 * n_epd * F * D
+    tflops1 = flops1 / (stages["gemm1"] / 1e3) / 1e12
+    tflops2 = flops2 / (stages["gemm2"] / 1e3) / 1e12
+    # burst peak (cuBLAS timed alone): our timed loop is ~0.1 s, far shorter than
+    # the 4 s sustained measurement, so burst is the conservative denominator
+    peak = peaks.get("bf16_tflops")
+    peak_sus = peaks.get("bf16_tflops_sustained", peak)
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "gemm1_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get("bytes_per_launch")
+    roofline = {"kernel": "grouped_gemm_kernel<SWIGLU> (GEMM-1: x @ [w1|w3], silu*up*gate-weight epilogue)",
+                "bound": "tensor", "achieved": tflops1, "peak": peak, "unit": "TFLOP/s", "frac": tflops1 / peak,
+                "peak_source": f"{peaks_src} bf16_tflops (burst)", "frac_of_sustained": tflops1 / peak_sus,
+                "traffic": traffic,
+                "flops_per_launch": flops1, "launch_ms": stages["gemm1"],
+                "gemm2": {"achieved": tflops2, "frac": tflops2 / peak, "launch_ms": stages["gemm2"]},
+                "layer_frac": (flops1 + flops2) / (sum(stages.values()) / 1e3) / 1e12 / peak}
+
+    # --- all-to-all bytes/token: dedup vs naive top-k at the config's EP=8 ---
+    ids, w = layer.route(x, gate)
+    plan8 = occ.ExpertParallelLayer(occ.MoEConfig(E, K_TOP, 8, D, F, activation="swiglu"))
+    plan8.build_dispatch_index(ids)
+    r8 = plan8.comm_report(bytes_per_scalar=2)
+    a2a = {"ep": 8, "payload": "bf16", "dedup_bytes_per_token": r8.crossing_rows * D * 2 / n_local,
+           "naive_bytes_per_token": r8.naive_crossing_rows * D * 2 / n_local,
+           "ratio": (r8.crossing_rows / r8.naive_crossing_rows) if r8.naive_crossing_rows else None,
+           "mean_replicas": r8.mean_replicas, "note": "Mixtral at EP=8 hosts one expert per GPU: dedup == naive"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cpu = cpu_port_baseline(args.cpu_seconds)
+        except Exception as exc:  # report, never fake
+            cpu = {"value": None, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
+                   "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+                "data": "synthetic (uniform tokens, random-init experts and gate of the Mixtral layer shape)",
+                "config": {"workload": WORKLOAD, "experts": E, "top_k": K_TOP, "d_model": D, "d_ff": F,
+                           "ffn": "SwiGLU", "tokens_per_step": args.tokens, "ep": world,
+                           "l2": "flushed between steps (512 MiB write); weights 2.8 GB >> L2",
+                           "step": "route + plan + pack + grouped GEMM-1/2 + partial combine + combine"},
+                "e2e": e2e, "gpu_launches": launches, "clocks": clk, "roofline": roofline,
+                "stages_ms": stages, "a2a": a2a, "cpu_baseline": cpu,
+                "comm_report": {"mean_replicas": rep.mean_replicas, "n_sfd": rep.n_sfd, "n_epd": rep.n_epd}}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--tokens", type=int, default=TOKENS)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-tokens-per-thread", type=int, default=2)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -180,6 +180,13 @@ occ_status occ_reschedule_placement(const double* p, int e, int num_devices, int
 /* Sum the histogram across ranks (world_size > 1; ncclAllReduce). */
 occ_status occ_allreduce_histogram(occ_handle* h, int64_t* counts, occ_stream_t stream);
 
+/* Stage profiling with CUDA events on the launching stream (default off).
+ * occ_stage_ms fills ms[0..8) for the last occ_forward_expert_parallel /
+ * occ_forward: route, plan, pack, compute_index, gather, gemm1, gemm2,
+ * partial_combine, combine (ms < 0: stage not recorded); returns the count. */
+occ_status occ_set_profiling(occ_handle* h, int on);
+int occ_stage_ms(occ_handle* h, float* ms, int max_stages);
+
 /* Human-readable message of the last error on this thread. */
 const char* occ_last_error(void);
 /* Kernel launches issued by this process so far (for launch accounting). */

@@ -83,8 +83,10 @@ EXPORTS = (
     "occ_comm_unique_id", "occ_comm_init", "occ_gate_scores_f64", "occ_topk_route_f64", "occ_prune_routing_f64",
     "occ_route", "occ_build_dispatch", "occ_forward", "occ_forward_expert_parallel", "occ_comm_report_get",
     "occ_saved_index", "occ_coactivation_histogram", "occ_normalize_graph", "occ_reschedule_placement",
-    "occ_allreduce_histogram", "occ_last_error", "occ_launch_count",
+    "occ_allreduce_histogram", "occ_last_error", "occ_launch_count", "occ_set_profiling", "occ_stage_ms",
 )
+
+STAGES = ("route", "plan", "pack", "compute_index", "gather", "gemm1", "gemm2", "partial_combine", "combine")
 
 _LIB = None
 
@@ -266,6 +268,15 @@ class ExpertParallelLayer:
 
     def set_validate(self, on: bool):
         _check(lib().occ_set_validate(self._h, int(on)), "set_validate")
+
+    def set_profiling(self, on: bool):
+        _check(lib().occ_set_profiling(self._h, int(on)), "set_profiling")
+
+    def stage_ms(self) -> dict:
+        """CUDA-event time of each stage of the last forward (profiling on)."""
+        buf = (C.c_float * len(STAGES))()
+        n = lib().occ_stage_ms(self._h, buf, len(STAGES))
+        return {STAGES[i]: float(buf[i]) for i in range(max(n, 0)) if buf[i] >= 0}
 
     # routing ------------------------------------------------------------------
     def route(self, x: torch.Tensor, gate: torch.Tensor, prune: Optional[PruneSpec] = None, want_scores=False):

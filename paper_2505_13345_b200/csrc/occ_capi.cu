@@ -67,6 +67,9 @@ struct DevBuf {
 
 }  // namespace
 
+// Stage boundaries recorded by occ_forward_expert_parallel / occ_forward.
+enum Stage { ST_ROUTE = 0, ST_PLAN, ST_PACK, ST_CINDEX, ST_GATHER, ST_GEMM1, ST_GEMM2, ST_PCOMBINE, ST_COMBINE, kStages };
+
 struct alignas(64) TmapBox {
     alignas(64) unsigned char bytes[128];
 };
@@ -95,7 +98,8 @@ struct occ_handle {
     DevBuf<int32_t> tok_row, tok_sfd, lam;
     DevBuf<__nv_bfloat16> in_x, x_epd, hbuf, ret;
     DevBuf<int32_t> in_ids, in_tok, in_src, in_slot, in_dev, row_epd, epd_src, mblk_w;
-    DevBuf<float> in_w, epd_w, ybuf, logits;
+    DevBuf<float> in_w, epd_w, ybuf, logits, rt_w;
+    DevBuf<int32_t> rt_ids;  // routing of occ_forward_expert_parallel
     size_t R_max = 0, Q_max = 0, max_mblk = 0;
     int last_n = 0;
     bool have_forward = false;
@@ -107,6 +111,11 @@ struct occ_handle {
     int* d_q_total = nullptr;
     // NCCL (world_size > 1)
     void* nccl_comm = nullptr;
+    // stage profiling (CUDA events on the launching stream)
+    int profiling = 0;
+    cudaEvent_t ev[kStages + 1] = {};
+    int ev_recorded = 0;
+    int in_ep = 0;
 };
 
 namespace {
@@ -249,6 +258,13 @@ occ_status run_plan(occ_handle* h, const int32_t* ids, const float* w, const int
     return OCC_OK;
 }
 
+void mark(occ_handle* h, int i, cudaStream_t st) {
+    if (!h->profiling) return;
+    if (!h->ev[i]) cudaEventCreate(&h->ev[i]);
+    cudaEventRecord(h->ev[i], st);
+    h->ev_recorded |= 1 << i;
+}
+
 occ_status check_err(occ_handle* h, cudaStream_t st) {
     CUDA_TRY(cudaStreamSynchronize(st));
     int32_t e = 0;
@@ -320,7 +336,10 @@ occ_status occ_destroy(occ_handle* h) {
     h->mask.release();
     h->rmask.release();
     for (auto* b : {&h->w13t, &h->w2t, &h->in_x, &h->x_epd, &h->hbuf, &h->ret}) b->release();
-    for (auto* b : {&h->in_w, &h->epd_w, &h->ybuf, &h->logits}) b->release();
+    for (auto* b : {&h->in_w, &h->epd_w, &h->ybuf, &h->logits, &h->rt_w}) b->release();
+    h->rt_ids.release();
+    for (auto& e : h->ev)
+        if (e) cudaEventDestroy(e);
     delete h;
     return OCC_OK;
 }
@@ -475,6 +494,8 @@ occ_status occ_build_dispatch(occ_handle* h, const int32_t* ids, const int32_t* 
     if (s != OCC_OK) return s;
     if (brim0) launch_extract_brim0(n, h->nd, sources, -1, h->mask.p, h->lam.p, h->tok_sfd.p, h->d_tok_base, brim0, st);
     if (counts) CUDA_TRY(cudaMemcpyAsync(counts, h->dofs.C, sizeof(int) * h->nd * h->nd, cudaMemcpyDeviceToDevice, st));
+    h->last_n = n;
+    h->have_forward = true;  // the CommReport of the plan is available
     CUDA_TRY(cudaGetLastError());
     return check_err(h, st);
 }
@@ -496,14 +517,18 @@ occ_status occ_forward(occ_handle* h, const void* x, const int32_t* ids, const f
     const int G = nd;
     CUDA_TRY(cudaMemsetAsync(h->stats.p, 0, sizeof(long long) * 8, st));
     CUDA_TRY(cudaMemsetAsync(h->err.p, 0, sizeof(int32_t), st));
+    if (!h->in_ep) h->ev_recorded = 0;
+    mark(h, ST_PLAN, st);
     // 1. dispatch plan (BRIM0) and exchange placement
     s = run_plan(h, ids, weights, sources, n, st);
     if (s != OCC_OK) return s;
+    mark(h, ST_PACK, st);
     // 2. pack: x rows -> inbox rows of every destination device
     const int32_t* rowmap = h->tok_row.p;
     PackArgs pk{n, k, nd, D, dedup, reinterpret_cast<const __nv_bfloat16*>(x), ids, weights, h->mask.p, rowmap,
                 h->in_x.p, h->in_ids.p, h->in_w.p};
     launch_pack(pk, st);
+    mark(h, ST_CINDEX, st);
     // 3. compute index (BRIM1) over the inbox rows
     const int* R_total = h->dofs.in_base + nd;
     const int R_max = (int)h->R_max;
@@ -519,19 +544,25 @@ occ_status occ_forward(occ_handle* h, const void* x, const int32_t* ids, const f
                    h->epd_src.p, h->epd_w.p};
     launch_rank_emit_compute(R_max, R_total, h->rgroup.p, h->rmask.p, G, P, ws, ec, st);
     // 4. gather + grouped GEMM-1 (activation / SwiGLU, routing weight fused)
+    mark(h, ST_GATHER, st);
     launch_gather_rows((int)h->Q_max, h->d_q_total, h->epd_src.p, h->in_x.p, D, h->x_epd.p, st);
+    mark(h, ST_GEMM1, st);
     const int max_mb = (int)h->max_mblk;
     GemmArgs g1{h->tmA1.bytes, h->tmB1.bytes, D, F, h->n1rows, h->d_n_mblk, h->mblk_w.p, h->epd_w.p, h->hbuf.p, F,
                 h->cfg.activation, max_mb * (h->gated ? F / 128 : (F + 255) / 256)};
     launch_grouped_gemm(h->gated ? EPI_SWIGLU_BF16 : EPI_ACT_BF16, g1, h->num_sms, st);
+    mark(h, ST_GEMM2, st);
     // 5. grouped GEMM-2 (per-expert products, fp32)
     GemmArgs g2{h->tmA2.bytes, h->tmB2.bytes, F, D, D, h->d_n_mblk, h->mblk_w.p, nullptr, h->ybuf.p, D, 0,
                 max_mb * ((D + 255) / 256)};
     launch_grouped_gemm(EPI_F32, g2, h->num_sms, st);
+    mark(h, ST_PCOMBINE, st);
     // 6. intra-device partial combine -> return payload (bf16)
     launch_partial_combine(R_max, R_total, P, D, h->row_epd.p, h->ybuf.p, h->ret.p, st);
+    mark(h, ST_COMBINE, st);
     // 7. return exchange + combine
     launch_combine(n, nd, k, dedup, D, h->mask.p, h->tok_row.p, h->ret.p, reinterpret_cast<__nv_bfloat16*>(out), st);
+    mark(h, kStages, st);
     CUDA_TRY(cudaGetLastError());
     if (h->validate) return check_err(h, st);
     return OCC_OK;
@@ -541,15 +572,37 @@ occ_status occ_forward_expert_parallel(occ_handle* h, const void* x, const void*
                                        const int32_t* sources, int n, void* out, occ_stream_t stream) {
     if (!h) return fail(OCC_ERR_ARG, "null handle");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    int32_t* ids = nullptr;
-    float* w = nullptr;
-    CUDA_TRY(cudaMallocAsync(&ids, sizeof(int32_t) * std::max(n, 1) * h->k, st));
-    CUDA_TRY(cudaMallocAsync(&w, sizeof(float) * std::max(n, 1) * h->k, st));
+    CUDA_TRY(h->rt_ids.ensure((size_t)std::max(n, 1) * h->k));
+    CUDA_TRY(h->rt_w.ensure((size_t)std::max(n, 1) * h->k));
+    int32_t* ids = h->rt_ids.p;
+    float* w = h->rt_w.p;
+    h->ev_recorded = 0;
+    mark(h, ST_ROUTE, st);
     occ_status s = occ_route(h, x, gate, n, prune, ids, w, nullptr, stream);
+    h->in_ep = 1;
     if (s == OCC_OK) s = occ_forward(h, x, ids, w, sources, n, out, stream);
-    cudaFreeAsync(ids, st);
-    cudaFreeAsync(w, st);
+    h->in_ep = 0;
     return s;
+}
+
+occ_status occ_set_profiling(occ_handle* h, int on) {
+    if (!h) return fail(OCC_ERR_ARG, "null handle");
+    h->profiling = on;
+    return OCC_OK;
+}
+
+int occ_stage_ms(occ_handle* h, float* ms, int max_stages) {
+    // Elapsed time of each recorded stage of the last forward (ms[i] < 0: not recorded).
+    if (!h || !ms) return -1;
+    int n = 0;
+    for (int i = 0; i < kStages && i < max_stages; ++i, ++n) {
+        ms[i] = -1.0f;
+        if ((h->ev_recorded >> i & 1) && (h->ev_recorded >> (i + 1) & 1)) {
+            cudaEventSynchronize(h->ev[i + 1]);
+            cudaEventElapsedTime(&ms[i], h->ev[i], h->ev[i + 1]);
+        }
+    }
+    return n;
 }
 
 occ_status occ_comm_report_get(occ_handle* h, int bytes_per_scalar, occ_comm_report* rep, occ_stream_t stream) {
