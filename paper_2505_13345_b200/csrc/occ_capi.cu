@@ -97,7 +97,7 @@ struct occ_handle {
     DevBuf<int32_t> err;
     DevBuf<int32_t> tok_row, tok_sfd, lam;
     DevBuf<__nv_bfloat16> in_x, x_epd, hbuf, ret;
-    DevBuf<int32_t> in_ids, in_tok, in_src, in_slot, in_dev, row_epd, epd_src, mblk_w;
+    DevBuf<int32_t> in_ids, in_tok, in_src, in_slot, in_dev, row_epd, epd_src;
     DevBuf<float> in_w, epd_w, ybuf, logits, rt_w;
     DevBuf<int32_t> rt_ids;  // routing of occ_forward_expert_parallel
     size_t R_max = 0, Q_max = 0, max_mblk = 0;
@@ -171,8 +171,8 @@ occ_status ensure_ws(occ_handle* h, int n) {
     CUDA_TRY(h->totals.ensure(K1));
     CUDA_TRY(h->totals2.ensure(K2));
     // offsets: C, off_sd, inoff (3 nd^2) + in_base(nd+1) + nsfd(nd) + src_base(nd+1) + tok_base(2nd)
-    //          + cnt/seg_base/unp_base (3 G P) + n_mblk + q_total
-    const size_t noffs = 3 * (size_t)nd * nd + (nd + 1) + nd + (nd + 1) + 2 * nd + 3 * (size_t)G * P + 2;
+    //          + cnt/seg_base/unp_base (3 G P) + grp_mb (G P + 1) + n_mblk + q_total
+    const size_t noffs = 3 * (size_t)nd * nd + (nd + 1) + nd + (nd + 1) + 2 * nd + 4 * (size_t)G * P + 3;
     CUDA_TRY(h->offs.ensure(noffs));
     CUDA_TRY(h->stats.ensure(8));
     CUDA_TRY(h->err.ensure(1));
@@ -194,7 +194,6 @@ occ_status ensure_ws(occ_handle* h, int n) {
     CUDA_TRY(h->x_epd.ensure(h->Q_max * D));
     CUDA_TRY(h->hbuf.ensure(h->Q_max * F));
     CUDA_TRY(h->ybuf.ensure(h->Q_max * D));
-    CUDA_TRY(h->mblk_w.ensure(h->max_mblk));
     CUDA_TRY(h->ret.ensure(h->R_max * D));
     int* o = h->offs.p;
     DispatchOffsets& d = h->dofs;
@@ -211,16 +210,16 @@ occ_status ensure_ws(occ_handle* h, int n) {
     c.cnt = o; o += G * P;
     c.seg_base = o; o += G * P;
     c.unp_base = o; o += G * P;
+    c.grp_mb = o; o += G * P + 1;
     c.n_mblk = o; o += 1;
     c.q_total = o; o += 1;
-    c.mblk_w = h->mblk_w.p;
     c.widx = h->d_widx.p;
     c.stats = h->stats.p;
     h->d_n_mblk = c.n_mblk;
     h->d_q_total = c.q_total;
     // A-operand tensor maps (buffers just (re)allocated)
-    if (!make_tmap_2d(h->tmA1.bytes, h->x_epd.p, D, h->Q_max, 64, kBM) ||
-        !make_tmap_2d(h->tmA2.bytes, h->hbuf.p, F, h->Q_max, 64, kBM))
+    if (!make_tmap_2d(h->tmA1.bytes, h->x_epd.p, D, h->Q_max, 64, kBM / 2) ||
+        !make_tmap_2d(h->tmA2.bytes, h->hbuf.p, F, h->Q_max, 64, kBM / 2))
         return fail(OCC_ERR_CUDA, "cuTensorMapEncodeTiled failed (A operands)");
     h->n_cap = n;
     return OCC_OK;
@@ -290,6 +289,7 @@ occ_status occ_create(const occ_config* cfg, const int32_t* placement, int world
     if (c.num_experts < 1) return fail(OCC_ERR_CONFIG, "config: num_experts must be >= 1");
     if (c.num_devices < 1) return fail(OCC_ERR_CONFIG, "config: num_devices must be >= 1");
     if (c.top_k < 1 || c.top_k > c.num_experts) return fail(OCC_ERR_CONFIG, "config: top_k must satisfy 1 <= k <= num_experts");
+    if (c.top_k > 64) return fail(OCC_ERR_UNSUPPORTED, "top_k <= 64 on the device path");
     if (c.num_experts % c.num_devices) return fail(OCC_ERR_CONFIG, "config: num_experts must be divisible by num_devices");
     if (c.embed_dim < 1 || c.hidden_dim < 1) return fail(OCC_ERR_CONFIG, "config: dims must be >= 1");
     // B200 path constraints
@@ -329,7 +329,7 @@ occ_status occ_destroy(occ_handle* h) {
     if (!h) return OCC_OK;
     for (auto* b : {&h->d_dev_of, &h->d_slot_of, &h->d_widx, &h->d_ranking, &h->group, &h->rgroup, &h->chunk_cnt,
                     &h->totals, &h->totals2, &h->err, &h->tok_row, &h->tok_sfd, &h->lam, &h->in_ids, &h->in_tok,
-                    &h->in_src, &h->in_slot, &h->in_dev, &h->row_epd, &h->epd_src, &h->mblk_w})
+                    &h->in_src, &h->in_slot, &h->in_dev, &h->row_epd, &h->epd_src})
         b->release();
     h->offs.release();
     h->stats.release();
@@ -375,8 +375,8 @@ occ_status occ_load_experts(occ_handle* h, const void* w1, const void* w3, const
     }
     launch_transpose_weights(b2, El, F, D, h->w2t.p, D, 0, st);
     CUDA_TRY(cudaGetLastError());
-    if (!make_tmap_2d(h->tmB1.bytes, h->w13t.p, D, (uint64_t)El * h->n1rows, 64, 256) ||
-        !make_tmap_2d(h->tmB2.bytes, h->w2t.p, F, (uint64_t)El * D, 64, 256))
+    if (!make_tmap_2d(h->tmB1.bytes, h->w13t.p, D, (uint64_t)El * h->n1rows, 64, 128) ||
+        !make_tmap_2d(h->tmB2.bytes, h->w2t.p, F, (uint64_t)El * D, 64, 128))
         return fail(OCC_ERR_CUDA, "cuTensorMapEncodeTiled failed (weights)");
     h->weights_loaded = true;
     return OCC_OK;
@@ -538,7 +538,7 @@ occ_status occ_forward(occ_handle* h, const void* x, const int32_t* ids, const f
     RankWs ws{h->chunk_cnt.p, h->totals2.p};
     launch_rank_count_dev(R_max, R_total, h->rgroup.p, h->rmask.p, G, P, ws, st);
     launch_rank_scan(R_max, G, P, ws, st);
-    launch_compute_finalize(G, P, h->totals2.p, h->cofs, (int)h->max_mblk, st);
+    launch_compute_finalize(G, P, h->totals2.p, h->cofs, st);
     launch_init_epd((int)h->Q_max, h->epd_src.p, h->epd_w.p, st);
     EmitCompute ec{k, P, 0, h->in_ids.p, h->in_w.p, h->d_slot_of.p, h->d_dev_of.p, h->cofs, h->row_epd.p,
                    h->epd_src.p, h->epd_w.p};
@@ -548,20 +548,19 @@ occ_status occ_forward(occ_handle* h, const void* x, const int32_t* ids, const f
     launch_gather_rows((int)h->Q_max, h->d_q_total, h->epd_src.p, h->in_x.p, D, h->x_epd.p, st);
     mark(h, ST_GEMM1, st);
     const int max_mb = (int)h->max_mblk;
-    GemmArgs g1{h->tmA1.bytes, h->tmB1.bytes, D, F, h->n1rows, h->d_n_mblk, h->mblk_w.p, h->epd_w.p, h->hbuf.p, F,
-                h->cfg.activation, max_mb * (h->gated ? F / 128 : (F + 255) / 256)};
+    GemmArgs g1{h->tmA1.bytes, h->tmB1.bytes, D, F, h->n1rows, h->cofs.grp_mb, h->d_widx.p, G * P, 1 << 20,
+                h->epd_w.p, h->hbuf.p, F, h->cfg.activation, max_mb * (h->gated ? F / 128 : (F + 255) / 256)};
     launch_grouped_gemm(h->gated ? EPI_SWIGLU_BF16 : EPI_ACT_BF16, g1, h->num_sms, st);
     mark(h, ST_GEMM2, st);
     // 5. grouped GEMM-2 (per-expert products, fp32)
-    GemmArgs g2{h->tmA2.bytes, h->tmB2.bytes, F, D, D, h->d_n_mblk, h->mblk_w.p, nullptr, h->ybuf.p, D, 0,
-                max_mb * ((D + 255) / 256)};
+    GemmArgs g2{h->tmA2.bytes, h->tmB2.bytes, F, D, D, h->cofs.grp_mb, h->d_widx.p, G * P, 8, nullptr, h->ybuf.p,
+                D, 0, max_mb * ((D + 255) / 256)};
     launch_grouped_gemm(EPI_F32, g2, h->num_sms, st);
-    mark(h, ST_PCOMBINE, st);
-    // 6. intra-device partial combine -> return payload (bf16)
-    launch_partial_combine(R_max, R_total, P, D, h->row_epd.p, h->ybuf.p, h->ret.p, st);
+    // 6+7. intra-device partial combine (placement order) -> bf16 return
+    // payload -> combine over devices ascending, fused on one GPU
     mark(h, ST_COMBINE, st);
-    // 7. return exchange + combine
-    launch_combine(n, nd, k, dedup, D, h->mask.p, h->tok_row.p, h->ret.p, reinterpret_cast<__nv_bfloat16*>(out), st);
+    launch_combine_fused(n, nd, k, P, dedup, D, h->mask.p, h->tok_row.p, h->row_epd.p, h->ybuf.p,
+                         reinterpret_cast<__nv_bfloat16*>(out), st);
     mark(h, kStages, st);
     CUDA_TRY(cudaGetLastError());
     if (h->validate) return check_err(h, st);
@@ -597,10 +596,12 @@ int occ_stage_ms(occ_handle* h, float* ms, int max_stages) {
     int n = 0;
     for (int i = 0; i < kStages && i < max_stages; ++i, ++n) {
         ms[i] = -1.0f;
-        if ((h->ev_recorded >> i & 1) && (h->ev_recorded >> (i + 1) & 1)) {
-            cudaEventSynchronize(h->ev[i + 1]);
-            cudaEventElapsedTime(&ms[i], h->ev[i], h->ev[i + 1]);
-        }
+        if (!(h->ev_recorded >> i & 1)) continue;
+        int j = i + 1;
+        while (j <= kStages && !(h->ev_recorded >> j & 1)) ++j;
+        if (j > kStages) continue;
+        cudaEventSynchronize(h->ev[j]);
+        cudaEventElapsedTime(&ms[i], h->ev[i], h->ev[j]);
     }
     return n;
 }

@@ -9,13 +9,16 @@
 // compute_finalize_kernel), so each tile belongs to exactly one expert and
 // the B operand is that expert's resident K-major weight slice.
 //
-// Persistent, warp-specialised, one CTA per SM:
-//   warp 0      TMA producer (A 128x64 + B 256x64 bf16 per stage, 4 stages)
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
-//               (M=128, N=256, K=16 per instruction, fp32 accumulate)
-//   warps 2..5  epilogue: tcgen05.ld -> activation / SwiGLU / routing
-//               weight -> global stores; double-buffered TMEM accumulators
-//               (2 x 256 columns) overlap the epilogue with the next tile.
+// Persistent, warp-specialised, CTA pairs (cluster 2x1x1, cta_group::2):
+// one 256x256 output tile per pair and K-step, each CTA staging its 128 A
+// rows and its half (128 rows) of the B tile, so per-SM operand traffic is
+// 32 KB per 64-deep K block (6 stages in 192 KB of shared memory).
+//   warp 0      TMA producer in both CTAs (completion on the leader's barrier)
+//   warp 1      TMEM allocator (both CTAs) + single-thread tcgen05.mma issuer
+//               in the leader CTA (M=256, N=256, K=16, fp32 accumulate)
+//   warps 2..5  epilogue in both CTAs: tcgen05.ld -> activation / SwiGLU /
+//               routing weight -> global stores; double-buffered TMEM
+//               accumulators (2 x 256 columns) overlap the next tile.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -27,30 +30,43 @@
 namespace occ {
 namespace {
 
-constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int BM = 128;               // rows per CTA (pair tile: 256)
+constexpr int BN = 256, BK = 64, STAGES = 6;
 constexpr int A_BYTES = BM * BK * 2;   // 16 KB
-constexpr int B_BYTES = BN * BK * 2;   // 32 KB
+constexpr int B_BYTES = (BN / 2) * BK * 2;  // 16 KB: this CTA's half of the B tile
 constexpr int SMEM_BYTES = STAGES * (A_BYTES + B_BYTES) + 256;
 constexpr int THREADS = 192;
-constexpr int BAND = 16;  // m-blocks per raster band (L2 reuse of B)
-constexpr uint32_t IDESC = idesc_bf16_f32(BM, BN);
+constexpr int MAX_GROUPS = 256;
+constexpr uint32_t IDESC = idesc_bf16_f32(2 * BM, BN);
+static_assert(kBM == 2 * BM, "Epd segments are padded to the pair tile");
 
 struct Params {
     int K, N, b_rows_per_e, act;
-    const int* n_mblk;
-    const int* mblk_w;
+    const int* grp_mb;
+    const int* grp_w;
+    int ngroups, band;
     const float* row_w;
     void* out;
     int ldo;
 };
 
-__device__ __forceinline__ void tile_coords(int tile, int MB, int NB, int& mb, int& nb) {
-    const int band = tile / (BAND * NB);
-    const int rem = tile - band * BAND * NB;
-    int bm = MB - band * BAND;
-    bm = bm < BAND ? bm : BAND;
+// Tile -> (m-block, n-block, weight slice).  Tiles are enumerated expert
+// group by expert group, and inside a group in bands of `band` m-blocks
+// walked n-block-major, so concurrently resident CTAs share B (weight)
+// n-blocks and a band's A rows stay in L2; no band straddles two experts.
+__device__ __forceinline__ void tile_coords(int tile, const int* gmb, const int* gw, int ng, int NB, int band,
+                                            int& mb, int& nb, int& w) {
+    int g = 0;
+    while (g < ng - 1 && gmb[g + 1] * NB <= tile) ++g;
+    const int lt = tile - gmb[g] * NB;
+    const int cnt = gmb[g + 1] - gmb[g];
+    const int b = lt / (band * NB);
+    const int rem = lt - b * band * NB;
+    int bm = cnt - b * band;
+    bm = bm < band ? bm : band;
     nb = rem / bm;
-    mb = band * BAND + rem % bm;
+    mb = gmb[g] + b * band + rem % bm;
+    w = gw[g];
 }
 
 __device__ __forceinline__ float act_f(float v, int act) {
@@ -60,7 +76,7 @@ __device__ __forceinline__ float act_f(float v, int act) {
 }
 
 template <int EPI>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Params p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -71,91 +87,100 @@ __global__ void __launch_bounds__(THREADS, 1)
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    __shared__ int s_gmb[MAX_GROUPS + 1];
+    __shared__ int s_gw[MAX_GROUPS];
+    for (int i = threadIdx.x; i <= p.ngroups; i += blockDim.x) s_gmb[i] = p.grp_mb[i];
+    for (int i = threadIdx.x; i < p.ngroups; i += blockDim.x) s_gw[i] = p.grp_w[i];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
         for (int s = 0; s < STAGES; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&full[s], 1);   // leader: one expect_tx arrival + both CTAs' bytes
+            mbar_init(&empty[s], 1);  // one multicast commit per phase
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 4);
+            mbar_init(&tempty[a], 8);  // leader: 4 epilogue warps x 2 CTAs
         }
         fence_barrier_init();
     }
-    if (warp == 1) tmem_alloc<512>(tmem_slot);
+    if (warp == 1) tmem_alloc_cg2<512>(tmem_slot);
     tc_fence_before();
-    __syncthreads();
+    cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    const int MB = *p.n_mblk;
+    const int MB = s_gmb[p.ngroups];  // pair tiles of 256 rows
     const int NB = EPI == EPI_SWIGLU_BF16 ? (p.N + 127) / 128 : (p.N + BN - 1) / BN;
     const int num_tiles = MB * NB;
     const int KB = (p.K + BK - 1) / BK;
+    const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
 
     if (warp == 0) {
         // ------------------------------------------------ TMA producer
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-                int mb, nb;
-                tile_coords(tile, MB, NB, mb, nb);
-                const int arow = mb * BM;
-                const int brow = p.mblk_w[mb] * p.b_rows_per_e + nb * BN;
+            for (int tile = cid; tile < num_tiles; tile += ncl) {
+                int mb, nb, wi;
+                tile_coords(tile, s_gmb, s_gw, p.ngroups, NB, p.band, mb, nb, wi);
+                const int arow = mb * 2 * BM + rank * BM;
+                const int brow = wi * p.b_rows_per_e + nb * BN + rank * (BN / 2);
                 for (int kb = 0; kb < KB; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_arrive_expect_tx(&full[stage], A_BYTES + B_BYTES);
-                    tma_load_2d(sA + stage * A_BYTES, &tmA, &full[stage], kb * BK, arow);
-                    tma_load_2d(sB + stage * B_BYTES, &tmB, &full[stage], kb * BK, brow);
+                    const uint32_t lbar = smem_u32(&full[stage]) & kPeerBitMask;
+                    if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * (A_BYTES + B_BYTES));
+                    tma_load_2d_cg2(sA + stage * A_BYTES, &tmA, lbar, kb * BK, arow);
+                    tma_load_2d_cg2(sB + stage * B_BYTES, &tmB, lbar, kb * BK, brow);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
         }
     } else if (warp == 1) {
-        // ------------------------------------------------ MMA issuer
-        int stage = 0;
-        uint32_t phase = 0;
-        int acc = 0;
-        uint32_t acc_phase = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-            mbar_wait(&tempty[acc], acc_phase ^ 1);
-            tc_fence_after();
-            const uint32_t d_tmem = tmem_base + acc * BN;
-            for (int kb = 0; kb < KB; ++kb) {
-                mbar_wait(&full[stage], phase);
+        // ------------------------------------------------ MMA issuer (leader CTA)
+        if (rank == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int tile = cid; tile < num_tiles; tile += ncl) {
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
-                if (lane == 0) {
-                    const uint32_t a0 = smem_u32(sA + stage * A_BYTES);
-                    const uint32_t b0 = smem_u32(sB + stage * B_BYTES);
+                const uint32_t d_tmem = tmem_base + acc * BN;
+                for (int kb = 0; kb < KB; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    if (lane == 0) {
+                        const uint32_t a0 = smem_u32(sA + stage * A_BYTES);
+                        const uint32_t b0 = smem_u32(sB + stage * B_BYTES);
 #pragma unroll
-                    for (int k = 0; k < BK / 16; ++k)
-                        umma_bf16(d_tmem, sdesc_k_sw128(a0 + k * 32), sdesc_k_sw128(b0 + k * 32), IDESC,
-                                  (kb | k) != 0);
-                    umma_commit(&empty[stage]);
+                        for (int k = 0; k < BK / 16; ++k)
+                            umma_bf16_cg2(d_tmem, sdesc_k_sw128(a0 + k * 32), sdesc_k_sw128(b0 + k * 32), IDESC,
+                                          (kb | k) != 0);
+                        umma_commit_cg2_mc(&empty[stage]);
+                    }
+                    __syncwarp();
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
+                if (lane == 0) umma_commit_cg2_mc(&tfull[acc]);
                 __syncwarp();
-                if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
             }
-            if (lane == 0) umma_commit(&tfull[acc]);
-            __syncwarp();
-            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
     } else {
         // ------------------------------------------------ epilogue
         const int q = warp & 3;  // TMEM lane quarter accessible to this warp
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-            int mb, nb;
-            tile_coords(tile, MB, NB, mb, nb);
+        for (int tile = cid; tile < num_tiles; tile += ncl) {
+            int mb, nb, wi;
+            tile_coords(tile, s_gmb, s_gw, p.ngroups, NB, p.band, mb, nb, wi);
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
-            const long row = (long)mb * BM + q * 32 + lane;
+            const long row = (long)mb * 2 * BM + rank * BM + q * 32 + lane;
             const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
             if constexpr (EPI == EPI_F32) {
                 float* out = reinterpret_cast<float*>(p.out) + row * p.ldo;
@@ -209,15 +234,15 @@ __global__ void __launch_bounds__(THREADS, 1)
             }
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (lane == 0) mbar_arrive_cluster(smem_u32(&tempty[acc]) & kPeerBitMask);
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
     }
     tc_fence_before();
-    __syncthreads();
+    cluster_sync();
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc<512>(tmem_base);
+        tmem_dealloc_cg2<512>(tmem_base);
     }
 }
 
@@ -255,10 +280,11 @@ bool make_tmap_2d(void* tmap, const void* base, uint64_t inner, uint64_t outer, 
 }
 
 void launch_grouped_gemm(EpiMode mode, const GemmArgs& a, int num_sms, cudaStream_t st) {
-    Params p{a.K, a.N, a.b_rows_per_e, a.act, a.n_mblk, a.mblk_w, a.row_w, a.out, a.ldo};
+    Params p{a.K, a.N, a.b_rows_per_e, a.act, a.grp_mb, a.grp_w, a.ngroups, a.band, a.row_w, a.out, a.ldo};
     const CUtensorMap& ta = *reinterpret_cast<const CUtensorMap*>(a.tmap_a);
     const CUtensorMap& tb = *reinterpret_cast<const CUtensorMap*>(a.tmap_b);
-    int grid = a.max_tiles < num_sms ? a.max_tiles : num_sms;
+    int grid = 2 * a.max_tiles < num_sms ? 2 * a.max_tiles : num_sms;
+    grid &= ~1;  // CTA pairs
     if (grid <= 0) return;
     const int smem = SMEM_BYTES + 1024;
     switch (mode) {

@@ -9,7 +9,7 @@ namespace occ {
 constexpr int kMaxDev = 64;    // N_d <= 64 (uint64 device masks)
 constexpr int kMaxLocal = 64;  // P <= 64 experts per device
 constexpr int kRankChunk = 256;
-constexpr int kBM = 128;       // GEMM M tile (EPD segments are padded to it)
+constexpr int kBM = 256;       // GEMM pair-tile rows (Epd segments are padded to it)
 
 extern long long g_launches;
 inline void count_launch(int n = 1) { g_launches += n; }
@@ -122,12 +122,12 @@ struct ComputeOffsets {
     int* seg_base;     // [G*P] padded Epd base per group
     int* unp_base;     // [G*P] unpadded BRIM1 base per group (within device)
     int* n_mblk;       // [1] total m-blocks
-    int* mblk_w;       // [max_mblk] weight index of each m-block
+    int* grp_mb;       // [G*P+1] prefix of m-blocks per group (GEMM tile decode)
     int* q_total;      // [1] padded Epd rows
     const int32_t* widx;  // [G*P] weight index of each group
     long long* stats;  // stats[6] += n_epd
 };
-void launch_compute_finalize(int G, int P, const int* totals, ComputeOffsets o, int max_mblk, cudaStream_t st);
+void launch_compute_finalize(int G, int P, const int* totals, ComputeOffsets o, cudaStream_t st);
 
 struct EmitCompute {
     int k, P, dev_base;
@@ -154,6 +154,11 @@ void launch_partial_combine(int R_max, const int* R_total, int P, int D, const i
 // Final combine: out[t] = bf16( sum_{d asc} ret[row_of(t,d)] ).
 void launch_combine(int n, int nd, int k, int dedup, int D, const uint64_t* mask, const int32_t* tok_row,
                     const __nv_bfloat16* ret, __nv_bfloat16* out, cudaStream_t st);
+
+// world_size == 1: partial combine + return + combine fused (reads Y once).
+void launch_combine_fused(int n, int nd, int k, int P, int dedup, int D, const uint64_t* mask,
+                          const int32_t* tok_row, const int32_t* row_epd, const float* Y, __nv_bfloat16* out,
+                          cudaStream_t st);
 
 // Saved-index extraction (parity): unpadded BRIM1 per device, P x R_d.
 void launch_extract_cindex(int R_max, const int* R_total, int P, const int32_t* row_dev, const int* in_base,
@@ -194,8 +199,10 @@ struct GemmArgs {
     int K;                    // reduction dim
     int N;                    // output columns per expert (GEMM-1 SwiGLU: F; B rows per expert = 2F)
     int b_rows_per_e;         // rows of B per expert in the stacked K-major weight matrix
-    const int* n_mblk;        // device
-    const int* mblk_w;        // device: weight index per m-block
+    const int* grp_mb;        // device [ngroups+1]: m-block prefix per expert group
+    const int* grp_w;         // device [ngroups]: weight index of each group
+    int ngroups;
+    int band;                 // m-blocks per raster band inside a group
     const float* row_w;       // per padded Epd row routing weight (EPI_ACT/SWIGLU), null = 1
     void* out;                // [Q, N] bf16 or f32
     int ldo;                  // output row stride (elements)

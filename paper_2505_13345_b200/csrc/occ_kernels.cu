@@ -16,6 +16,7 @@ long long g_launches = 0;
 
 namespace {
 
+constexpr int kMaxTopK = 64;
 constexpr int kRankThreads = kRankChunk;  // one item per thread, 8 warps
 constexpr int kRankWarps = kRankThreads / 32;
 
@@ -337,28 +338,25 @@ __global__ void compute_mask_kernel(ComputeArgs a) {
 // Epd segment layout: group g = (local device, slot) in placement-list
 // order (pipeline.cpp:79-86, expert-major counters); each segment padded
 // to the GEMM M tile so no tile straddles two experts.
-__global__ void compute_finalize_kernel(int G, int P, const int* totals, ComputeOffsets o, int max_mblk) {
-    __shared__ int s_mb[1024];
-    __shared__ int s_mbbase[1024 + 1];
+__global__ void compute_finalize_kernel(int G, int P, const int* totals, ComputeOffsets o) {
     const int NG = G * P;
     for (int g = threadIdx.x; g < NG; g += blockDim.x) {
         const int d = g / P, p = g % P;
-        const int c = totals[d * (P + 1) + p];
-        o.cnt[g] = c;
-        s_mb[g] = (c + kBM - 1) / kBM;
+        o.cnt[g] = totals[d * (P + 1) + p];
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         int run = 0, mb = 0;
         long long nepd = 0;
         for (int g = 0; g < NG; ++g) {
+            const int m = (o.cnt[g] + kBM - 1) / kBM;
             o.seg_base[g] = run;
-            s_mbbase[g] = mb;
-            run += s_mb[g] * kBM;
-            mb += s_mb[g];
+            o.grp_mb[g] = mb;
+            run += m * kBM;
+            mb += m;
             nepd += o.cnt[g];
         }
-        s_mbbase[NG] = mb;
+        o.grp_mb[NG] = mb;
         for (int d = 0; d < G; ++d) {
             int u = 0;
             for (int p = 0; p < P; ++p) {
@@ -366,14 +364,10 @@ __global__ void compute_finalize_kernel(int G, int P, const int* totals, Compute
                 u += o.cnt[d * P + p];
             }
         }
-        *o.n_mblk = mb < max_mblk ? mb : max_mblk;
+        *o.n_mblk = mb;
         *o.q_total = run;
         o.stats[6] += nepd;
     }
-    __syncthreads();
-    for (int g = 0; g < NG; ++g)
-        for (int i = threadIdx.x; i < s_mb[g]; i += blockDim.x)
-            if (s_mbbase[g] + i < max_mblk) o.mblk_w[s_mbbase[g] + i] = o.widx[g];
 }
 
 struct ComputeEmitter {
@@ -496,6 +490,70 @@ __global__ void __launch_bounds__(256) combine_kernel(int n, int nd, int k, int 
         o.z = pack_bf16(acc[4], acc[5]);
         o.w = pack_bf16(acc[6], acc[7]);
         reinterpret_cast<uint4*>(out + (long)t * D)[v] = o;
+    }
+}
+
+// world_size == 1: intra-device partial combine + return + combine in one
+// pass.  Each token gathers its k Epd product rows (exactly one per selected
+// expert) ordered by device ascending, then placement slot; every device's
+// partial sum is rounded to the bf16 return payload exactly as the
+// multi-GPU exchange would carry it, then summed over devices in fp32.
+__global__ void __launch_bounds__(256) combine_fused_kernel(int n, int nd, int k, int P, int dedup, int D,
+                                                            const uint64_t* mask, const int32_t* tok_row,
+                                                            const int32_t* row_epd, const float* Y,
+                                                            __nv_bfloat16* out) {
+    const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (t >= n) return;
+    int qs[kMaxTopK];
+    bool newdev[kMaxTopK];
+    int nq = 0;
+    if (dedup) {
+        uint64_t m = mask[t];
+        while (m) {
+            const int d = __ffsll(m) - 1;
+            m &= m - 1;
+            const int r = tok_row[(long)t * nd + d];
+            bool first = true;
+            for (int p = 0; p < P && nq < kMaxTopK; ++p) {
+                const int q = row_epd[(long)r * P + p];
+                if (q < 0) continue;
+                qs[nq] = q;
+                newdev[nq++] = first;
+                first = false;
+            }
+        }
+    } else {
+        for (int j = 0; j < k; ++j) {
+            const int r = tok_row[(long)t * k + j];
+            for (int p = 0; p < P; ++p) {
+                const int q = row_epd[(long)r * P + p];
+                if (q >= 0) { qs[nq] = q; newdev[nq++] = true; }
+            }
+        }
+    }
+    const int nv = D / 4;
+    for (int v = lane; v < nv; v += 32) {
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f), dev = acc;
+        for (int i = 0; i < nq; ++i) {
+            if (i && newdev[i]) {
+                acc.x += __bfloat162float(__float2bfloat16(dev.x));
+                acc.y += __bfloat162float(__float2bfloat16(dev.y));
+                acc.z += __bfloat162float(__float2bfloat16(dev.z));
+                acc.w += __bfloat162float(__float2bfloat16(dev.w));
+                dev = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            const float4 y = __ldg(reinterpret_cast<const float4*>(Y + (long)qs[i] * D) + v);
+            dev.x += y.x; dev.y += y.y; dev.z += y.z; dev.w += y.w;
+        }
+        acc.x += __bfloat162float(__float2bfloat16(dev.x));
+        acc.y += __bfloat162float(__float2bfloat16(dev.y));
+        acc.z += __bfloat162float(__float2bfloat16(dev.z));
+        acc.w += __bfloat162float(__float2bfloat16(dev.w));
+        uint2 o;
+        o.x = pack_bf16(acc.x, acc.y);
+        o.y = pack_bf16(acc.z, acc.w);
+        reinterpret_cast<uint2*>(out + (long)t * D)[v] = o;
     }
 }
 
@@ -764,54 +822,10 @@ __global__ void prune_f64_kernel(const double* s, int n, int e, int k, const int
 }
 
 // ------------------------------------------------- production router ---
-// logits[t, j] = sum_c x[t,c] g[j,c]: bf16 inputs, fp32 accumulation.
-// Block tile: 32 tokens x 64 experts, D staged through shared memory.
-constexpr int kRT = 32, kRE = 64, kRK = 64;
-__global__ void __launch_bounds__(256) router_logits_kernel(const __nv_bfloat16* x, const __nv_bfloat16* g, int n,
-                                                            int d, int e, float* logits) {
-    __shared__ float xs[kRT][kRK + 1];
-    __shared__ float gs[kRE][kRK + 1];
-    const int t0 = blockIdx.x * kRT, e0 = blockIdx.y * kRE;
-    const int tid = threadIdx.x;
-    const int tr = tid / 16, ec = tid % 16;  // each thread: 2 tokens x 4 experts
-    float acc[2][4] = {};
-    for (int k0 = 0; k0 < d; k0 += kRK) {
-        for (int i = tid; i < kRT * kRK; i += 256) {
-            const int r = i / kRK, c = i % kRK;
-            xs[r][c] = (t0 + r < n && k0 + c < d) ? __bfloat162float(x[(long)(t0 + r) * d + k0 + c]) : 0.f;
-        }
-        for (int i = tid; i < kRE * kRK; i += 256) {
-            const int r = i / kRK, c = i % kRK;
-            gs[r][c] = (e0 + r < e && k0 + c < d) ? __bfloat162float(g[(long)(e0 + r) * d + k0 + c]) : 0.f;
-        }
-        __syncthreads();
-#pragma unroll 8
-        for (int c = 0; c < kRK; ++c) {
-            const float a0 = xs[tr * 2][c], a1 = xs[tr * 2 + 1][c];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const float b = gs[ec + 16 * q][c];
-                acc[0][q] = fmaf(a0, b, acc[0][q]);
-                acc[1][q] = fmaf(a1, b, acc[1][q]);
-            }
-        }
-        __syncthreads();
-    }
-#pragma unroll
-    for (int r = 0; r < 2; ++r)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int t = t0 + tr * 2 + r, j = e0 + ec + 16 * q;
-            if (t < n && j < e) logits[(long)t * e + j] = acc[r][q];
-        }
-}
-
-// softmax + top-k + renormalise (+ pruning) per token, fp32.
-__global__ void router_select_kernel(float* logits, int n, int e, int k, int renorm, PruneDev p, int32_t* ids,
-                                     float* w, float* scores, int32_t* err) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= n) return;
-    float* row = logits + (long)t * e;
+// softmax + top-k + renormalise (+ pruning) for one token, fp32; `row`
+// holds the logits and is overwritten with the softmax scores.
+__device__ void route_token(float* row, int t, int e, int k, int renorm, const PruneDev& p, int32_t* ids, float* w,
+                            float* scores, int32_t* err) {
     float mx = row[0];
     for (int j = 1; j < e; ++j) mx = fmaxf(mx, row[j]);
     float sum = 0.f;
@@ -823,11 +837,11 @@ __global__ void router_select_kernel(float* logits, int n, int e, int k, int ren
     for (int j = 0; j < e; ++j) row[j] *= inv;
     if (scores)
         for (int j = 0; j < e; ++j) scores[(long)t * e + j] = row[j];
-    int sel[256];
-    float wt[256];
+    int sel[kMaxTopK];
+    float wt[kMaxTopK];
     select_topk(row, e, k, sel);
     if (p.mode != 0) {
-        int oi[256];
+        int oi[kMaxTopK];
         const int rc = prune_token(row, e, k, sel, p, oi, wt);
         if (rc) { atomicExch(err, rc); return; }
         for (int j = 0; j < k; ++j) sel[j] = oi[j];
@@ -839,6 +853,84 @@ __global__ void router_select_kernel(float* logits, int n, int e, int k, int ren
         ids[(long)t * k + j] = sel[j];
         w[(long)t * k + j] = wt[j];
     }
+}
+
+__global__ void router_select_kernel(float* logits, int n, int e, int k, int renorm, PruneDev p, int32_t* ids,
+                                     float* w, float* scores, int32_t* err) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n) return;
+    route_token(logits + (long)t * e, t, e, k, renorm, p, ids, w, scores, err);
+}
+
+// Fused router: logits = x g^T (bf16 in, fp32 accumulate) + softmax + top-k
+// (+ pruning).  One warp per 8 tokens; lanes split D in 8-element (16-byte)
+// slices, a chunk of 8 experts of the gate lives in registers, x rows are
+// streamed once per expert chunk (HBM-bound on x for E <= 8).  Per-token
+// selection runs one thread per token on the logits staged in shared memory.
+constexpr int kRTokW = 8, kRWarps = 4, kREC = 8;
+__global__ void __launch_bounds__(kRWarps * 32) router_fused_kernel(const __nv_bfloat16* __restrict__ x,
+                                                                   const __nv_bfloat16* __restrict__ g, int n, int d,
+                                                                   int e, int k, int renorm, PruneDev p, int32_t* ids,
+                                                                   float* w, float* scores, int32_t* err) {
+    extern __shared__ float lg[];  // [kRWarps*kRTokW][e]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int t0 = (blockIdx.x * kRWarps + warp) * kRTokW;
+    for (int ec = 0; ec < e; ec += kREC) {
+        float acc[kRTokW][kREC];
+#pragma unroll
+        for (int t = 0; t < kRTokW; ++t)
+#pragma unroll
+            for (int j = 0; j < kREC; ++j) acc[t][j] = 0.f;
+        for (int c = lane * 8; c < d; c += 256) {
+            float gv[kREC][8];
+#pragma unroll
+            for (int j = 0; j < kREC; ++j) {
+                uint4 u = make_uint4(0, 0, 0, 0);
+                if (ec + j < e) u = __ldg(reinterpret_cast<const uint4*>(g + (long)(ec + j) * d + c));
+                const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float2 f = __bfloat1622float2(h[q]);
+                    gv[j][2 * q] = f.x;
+                    gv[j][2 * q + 1] = f.y;
+                }
+            }
+            uint4 xu[kRTokW];
+#pragma unroll
+            for (int t = 0; t < kRTokW; ++t) {  // all token loads in flight before the FMAs
+                const int tt = t0 + t < n ? t0 + t : n - 1;
+                xu[t] = __ldg(reinterpret_cast<const uint4*>(x + (long)tt * d + c));
+            }
+#pragma unroll
+            for (int t = 0; t < kRTokW; ++t) {
+                const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&xu[t]);
+                float xv[8];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float2 f = __bfloat1622float2(h[q]);
+                    xv[2 * q] = f.x;
+                    xv[2 * q + 1] = f.y;
+                }
+#pragma unroll
+                for (int j = 0; j < kREC; ++j)
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) acc[t][j] = fmaf(xv[i], gv[j][i], acc[t][j]);
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < kRTokW; ++t)
+#pragma unroll
+            for (int j = 0; j < kREC; ++j) {
+                float v = acc[t][j];
+#pragma unroll
+                for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (lane == 0 && ec + j < e) lg[(warp * kRTokW + t) * e + ec + j] = v;
+            }
+    }
+    __syncthreads();
+    const int tl = threadIdx.x;
+    const int t = blockIdx.x * kRWarps * kRTokW + tl;
+    if (tl < kRWarps * kRTokW && t < n) route_token(lg + tl * e, t, e, k, renorm, p, ids, w, scores, err);
 }
 
 // -------------------------------------------------- weight re-layout ---
@@ -943,8 +1035,8 @@ void launch_compute_mask(const ComputeArgs& a, cudaStream_t st) {
     count_launch();
 }
 
-void launch_compute_finalize(int G, int P, const int* totals, ComputeOffsets o, int max_mblk, cudaStream_t st) {
-    compute_finalize_kernel<<<1, 256, 0, st>>>(G, P, totals, o, max_mblk);
+void launch_compute_finalize(int G, int P, const int* totals, ComputeOffsets o, cudaStream_t st) {
+    compute_finalize_kernel<<<1, 256, 0, st>>>(G, P, totals, o);
     count_launch();
 }
 
@@ -977,6 +1069,14 @@ void launch_combine(int n, int nd, int k, int dedup, int D, const uint64_t* mask
                     const __nv_bfloat16* ret, __nv_bfloat16* out, cudaStream_t st) {
     if (!n) return;
     combine_kernel<<<(n + 7) / 8, 256, 0, st>>>(n, nd, k, dedup, D, mask, tok_row, ret, out);
+    count_launch();
+}
+
+void launch_combine_fused(int n, int nd, int k, int P, int dedup, int D, const uint64_t* mask,
+                          const int32_t* tok_row, const int32_t* row_epd, const float* Y, __nv_bfloat16* out,
+                          cudaStream_t st) {
+    if (!n) return;
+    combine_fused_kernel<<<(n + 7) / 8, 256, 0, st>>>(n, nd, k, P, dedup, D, mask, tok_row, row_epd, Y, out);
     count_launch();
 }
 
@@ -1033,10 +1133,12 @@ void launch_router_bf16(const __nv_bfloat16* x, const __nv_bfloat16* g, int n, i
                         PruneDev p, int32_t* ids, float* w, float* scores, float* logits_ws, int32_t* err,
                         cudaStream_t st) {
     if (!n) return;
-    dim3 grid((n + kRT - 1) / kRT, (e + kRE - 1) / kRE);
-    router_logits_kernel<<<grid, 256, 0, st>>>(x, g, n, d, e, logits_ws);
-    router_select_kernel<<<(n + 127) / 128, 128, 0, st>>>(logits_ws, n, e, k, renorm, p, ids, w, scores, err);
-    count_launch(2);
+    const int per_block = kRWarps * kRTokW;
+    const size_t smem = sizeof(float) * per_block * e;
+    router_fused_kernel<<<(n + per_block - 1) / per_block, kRWarps * 32, smem, st>>>(x, g, n, d, e, k, renorm, p, ids,
+                                                                                      w, scores, err);
+    count_launch();
+    (void)logits_ws;
 }
 
 void launch_transpose_weights(const __nv_bfloat16* w, int E, int K, int N, __nv_bfloat16* out, int out_rows_per_e,
