@@ -159,6 +159,19 @@ occ_status occ_forward(occ_handle* h, const void* x, const int32_t* ids, const f
 /* forward_expert_parallel (pipeline.cpp:503-517): occ_route + occ_forward. */
 occ_status occ_forward_expert_parallel(occ_handle* h, const void* x, const void* gate, const occ_prune* prune,
                                        const int32_t* sources, int n, void* out, occ_stream_t stream);
+/* forward_expert_parallel end to end from pinned HOST memory: x_host and
+ * out_host are [n, D] bf16 host buffers (pinned for overlap), gate is a
+ * DEVICE pointer.  Asynchronous and double-buffered: the host->device copy
+ * of this call and the device->host copy of the previous one overlap the
+ * layer, on two copy streams owned by the handle; the batch may further be
+ * cut into `chunks` token chunks (rows are independent given routing,
+ * pipeline.cpp:548-560).  x_host must stay unchanged, and out_host may only
+ * be read, after occ_host_wait has been ordered on a stream and that stream
+ * has completed. */
+occ_status occ_forward_host(occ_handle* h, const void* x_host, const void* gate, const occ_prune* prune, int n,
+                            void* out_host, int chunks, occ_stream_t stream);
+/* Make `stream` wait until every enqueued occ_forward_host result is in host memory. */
+occ_status occ_host_wait(occ_handle* h, occ_stream_t stream);
 /* CommReport of the last forward (synchronises the stream).
  * bytes_per_scalar as in forward_given_routing's argument. */
 occ_status occ_comm_report_get(occ_handle* h, int bytes_per_scalar, occ_comm_report* rep, occ_stream_t stream);

@@ -83,7 +83,7 @@ EXPORTS = (
     "occ_comm_unique_id", "occ_comm_init", "occ_gate_scores_f64", "occ_topk_route_f64", "occ_prune_routing_f64",
     "occ_route", "occ_build_dispatch", "occ_forward", "occ_forward_expert_parallel", "occ_comm_report_get",
     "occ_saved_index", "occ_coactivation_histogram", "occ_normalize_graph", "occ_reschedule_placement",
-    "occ_allreduce_histogram", "occ_last_error", "occ_launch_count", "occ_set_profiling", "occ_stage_ms",
+    "occ_allreduce_histogram", "occ_last_error", "occ_launch_count", "occ_set_profiling", "occ_stage_ms", "occ_forward_host", "occ_host_wait",
 )
 
 STAGES = ("route", "plan", "pack", "compute_index", "gather", "gemm1", "gemm2", "partial_combine", "combine")
@@ -350,6 +350,24 @@ class ExpertParallelLayer:
         _check(lib().occ_forward_expert_parallel(self._h, _ptr(x), _ptr(gate), C.byref(pr) if pr else None,
                                                  _ptr(sources), x.shape[0], _ptr(out), _stream()), "forward_ep")
         return out
+
+    def forward_host(self, x_host: torch.Tensor, gate: torch.Tensor, out_host: torch.Tensor,
+                     prune: Optional[PruneSpec] = None, chunks: int = 1, wait: bool = True):
+        """End to end from pinned host memory (occ_forward_host): the H2D copy
+        of this call and the D2H copy of the previous call overlap the layer.
+        ``wait=False`` leaves the result pending until ``host_wait()``."""
+        if x_host.is_cuda or out_host.is_cuda:
+            raise ShapeError("forward_host: x and out are host tensors")
+        _need_cuda(gate)
+        pr = self._prune(prune)
+        _check(lib().occ_forward_host(self._h, _ptr(x_host), _ptr(gate), C.byref(pr) if pr else None,
+                                      x_host.shape[0], _ptr(out_host), chunks, _stream()), "forward_host")
+        if wait:
+            self.host_wait()
+        return out_host
+
+    def host_wait(self):
+        _check(lib().occ_host_wait(self._h, _stream()), "host_wait")
 
     def comm_report(self, bytes_per_scalar: int = 4, cap_replicas: Optional[float] = None) -> CommReport:
         r = _Report()

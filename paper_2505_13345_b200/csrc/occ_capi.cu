@@ -116,6 +116,12 @@ struct occ_handle {
     cudaEvent_t ev[kStages + 1] = {};
     int ev_recorded = 0;
     int in_ep = 0;
+    // host-buffer pipeline (occ_forward_host)
+    cudaStream_t s_in = nullptr, s_out = nullptr;
+    std::vector<cudaEvent_t> pev;
+    DevBuf<__nv_bfloat16> x_stage, o_stage;
+    long long host_calls = 0;
+    bool host_slot_used[2] = {false, false};
 };
 
 namespace {
@@ -340,6 +346,11 @@ occ_status occ_destroy(occ_handle* h) {
     h->rt_ids.release();
     for (auto& e : h->ev)
         if (e) cudaEventDestroy(e);
+    for (auto& e : h->pev) cudaEventDestroy(e);
+    if (h->s_in) cudaStreamDestroy(h->s_in);
+    if (h->s_out) cudaStreamDestroy(h->s_out);
+    h->x_stage.release();
+    h->o_stage.release();
     delete h;
     return OCC_OK;
 }
@@ -604,6 +615,78 @@ int occ_stage_ms(occ_handle* h, float* ms, int max_stages) {
         cudaEventElapsedTime(&ms[i], h->ev[i], h->ev[j]);
     }
     return n;
+}
+
+occ_status occ_forward_host(occ_handle* h, const void* x_host, const void* gate, const occ_prune* prune, int n,
+                            void* out_host, int chunks, occ_stream_t stream) {
+    // Double-buffered host pipeline.  Call i uses staging slot i % 2:
+    //   s_in   : wait slot's x buffer free -> H2D chunks -> ev_in[c]
+    //   stream : wait ev_in[c] (+ slot's out buffer free) -> layer -> ev_comp[c]
+    //   s_out  : wait ev_comp[c] -> D2H chunks -> slot's out buffer free
+    // so the copies of call i+1 / i-1 overlap the layer of call i.  Results
+    // are in out_host once occ_host_wait() has been ordered on a stream.
+    if (!h) return fail(OCC_ERR_ARG, "null handle");
+    if (n > 0 && (!x_host || !gate || !out_host)) return fail(OCC_ERR_ARG, "null argument");
+    if (h->world != 1) return fail(OCC_ERR_UNSUPPORTED, "forward_host: world_size 1");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    chunks = std::max(1, std::min(chunks, 16));
+    if (n < chunks) chunks = std::max(1, n);
+    const size_t row = (size_t)h->D * sizeof(__nv_bfloat16);
+    const size_t slot_elems = (size_t)std::max(n, 1) * h->D;
+    if (h->x_stage.n < 2 * slot_elems) {
+        CUDA_TRY(cudaDeviceSynchronize());  // staging regrow: no copy may be in flight
+        CUDA_TRY(h->x_stage.ensure(2 * slot_elems));
+        CUDA_TRY(h->o_stage.ensure(2 * slot_elems));
+        h->host_slot_used[0] = h->host_slot_used[1] = false;
+    }
+    if (!h->s_in) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking));
+        CUDA_TRY(cudaStreamCreateWithFlags(&h->s_out, cudaStreamNonBlocking));
+    }
+    // events: [slot][0] x free, [slot][1] out free, [slot][2 + 2c] in, [slot][3 + 2c] comp
+    const int per_slot = 2 + 2 * 16;
+    while ((int)h->pev.size() < 2 * per_slot + 1) {
+        cudaEvent_t e;
+        CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        h->pev.push_back(e);
+    }
+    const int slot = h->host_calls++ & 1;
+    cudaEvent_t* ev = h->pev.data() + slot * per_slot;
+    const size_t base_el = slot * slot_elems;
+    if (h->host_slot_used[slot]) {
+        CUDA_TRY(cudaStreamWaitEvent(h->s_in, ev[0], 0));  // previous layer on this slot read x
+        CUDA_TRY(cudaStreamWaitEvent(st, ev[1], 0));       // previous D2H on this slot read out
+    }
+    const char* xh = reinterpret_cast<const char*>(x_host);
+    char* oh = reinterpret_cast<char*>(out_host);
+    int base = 0;
+    for (int c = 0; c < chunks; ++c) {
+        const int nc = n / chunks + (c < n % chunks ? 1 : 0);
+        auto* xs = h->x_stage.p + base_el + (size_t)base * h->D;
+        auto* os = h->o_stage.p + base_el + (size_t)base * h->D;
+        CUDA_TRY(cudaMemcpyAsync(xs, xh + base * row, nc * row, cudaMemcpyHostToDevice, h->s_in));
+        CUDA_TRY(cudaEventRecord(ev[2 + 2 * c], h->s_in));
+        CUDA_TRY(cudaStreamWaitEvent(st, ev[2 + 2 * c], 0));
+        occ_status s = occ_forward_expert_parallel(h, xs, gate, prune, nullptr, nc, os, stream);
+        if (s != OCC_OK) return s;
+        CUDA_TRY(cudaEventRecord(ev[3 + 2 * c], st));
+        CUDA_TRY(cudaStreamWaitEvent(h->s_out, ev[3 + 2 * c], 0));
+        CUDA_TRY(cudaMemcpyAsync(oh + base * row, os, nc * row, cudaMemcpyDeviceToHost, h->s_out));
+        base += nc;
+    }
+    CUDA_TRY(cudaEventRecord(ev[0], st));
+    CUDA_TRY(cudaEventRecord(ev[1], h->s_out));
+    h->host_slot_used[slot] = true;
+    return OCC_OK;
+}
+
+occ_status occ_host_wait(occ_handle* h, occ_stream_t stream) {
+    if (!h) return fail(OCC_ERR_ARG, "null handle");
+    if (!h->s_out) return OCC_OK;
+    cudaEvent_t e = h->pev[2 * (2 + 2 * 16)];
+    CUDA_TRY(cudaEventRecord(e, h->s_out));
+    CUDA_TRY(cudaStreamWaitEvent(reinterpret_cast<cudaStream_t>(stream), e, 0));
+    return OCC_OK;
 }
 
 occ_status occ_comm_report_get(occ_handle* h, int bytes_per_scalar, occ_comm_report* rep, occ_stream_t stream) {
