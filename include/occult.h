@@ -121,6 +121,11 @@ occ_status occ_set_validate(occ_handle* h, int on);
 /* NCCL plumbing for world_size > 1 (one process per GPU). */
 occ_status occ_comm_unique_id(void* id128);
 occ_status occ_comm_init(occ_handle* h, const void* id128);
+/* Validation transport: the world_size ranks are host threads of ONE process
+ * sharing one GPU (each with its own handle and stream); the exchanges become
+ * device-to-device copies between the ranks' buffers.  Same layer code path
+ * as NCCL, for checking world_size > 1 on a single GPU. */
+occ_status occ_comm_init_loopback(occ_handle* h, long group_key);
 
 /* -------------------------------------------------------------- routing */
 /* gate_scores (routing.cpp:33-52), exact fp64 mode: logits accumulated
@@ -199,6 +204,15 @@ occ_status occ_allreduce_histogram(occ_handle* h, int64_t* counts, occ_stream_t 
  * partial_combine, combine (ms < 0: stage not recorded); returns the count. */
 occ_status occ_set_profiling(occ_handle* h, int on);
 int occ_stage_ms(occ_handle* h, float* ms, int max_stages);
+
+/* Host-side layout of the dispatch/return all-to-alls for EP rank `rank`
+ * from the all-gathered (source, destination) Sfd row counts C [nd * nd]
+ * (row s = source s): per peer p, where this rank's rows for p start in its
+ * device-major Sfd batch and how many there are, and where the rows from
+ * p land in this device's (source asc, counter asc) inbox
+ * (all_to_all_exchange, pipeline.cpp:125-176).  HOST buffers. */
+occ_status occ_exchange_layout(const int32_t* C, int nd, int rank, int64_t* send_off, int64_t* send_cnt,
+                               int64_t* recv_off, int64_t* recv_cnt);
 
 /* Human-readable message of the last error on this thread. */
 const char* occ_last_error(void);

@@ -83,7 +83,7 @@ EXPORTS = (
     "occ_comm_unique_id", "occ_comm_init", "occ_gate_scores_f64", "occ_topk_route_f64", "occ_prune_routing_f64",
     "occ_route", "occ_build_dispatch", "occ_forward", "occ_forward_expert_parallel", "occ_comm_report_get",
     "occ_saved_index", "occ_coactivation_histogram", "occ_normalize_graph", "occ_reschedule_placement",
-    "occ_allreduce_histogram", "occ_last_error", "occ_launch_count", "occ_set_profiling", "occ_stage_ms", "occ_forward_host", "occ_host_wait",
+    "occ_allreduce_histogram", "occ_last_error", "occ_launch_count", "occ_set_profiling", "occ_stage_ms", "occ_forward_host", "occ_host_wait", "occ_comm_init_loopback", "occ_exchange_layout",
 )
 
 STAGES = ("route", "plan", "pack", "compute_index", "gather", "gemm1", "gemm2", "partial_combine", "combine")
@@ -265,6 +265,26 @@ class ExpertParallelLayer:
         import numpy as np
         v = np.ascontiguousarray(values, dtype=np.float64)
         _check(lib().occ_set_similarity(self._h, v.ctypes.data_as(C.c_void_p)), "set_similarity")
+
+    def comm_init(self, group=None):
+        """NCCL communicator for world_size > 1 (one process per GPU): rank 0
+        creates the unique id, torch.distributed broadcasts it."""
+        import torch.distributed as dist
+        buf = (C.c_uint8 * 128)()
+        if dist.get_rank(group) == 0:
+            _check(lib().occ_comm_unique_id(buf), "comm_unique_id")
+        obj = [bytes(buf)]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        idb = (C.c_uint8 * 128).from_buffer_copy(obj[0])
+        _check(lib().occ_comm_init(self._h, idb), "comm_init")
+
+    def comm_init_loopback(self, key: int):
+        """Validation transport: world_size ranks as threads on one GPU."""
+        _check(lib().occ_comm_init_loopback(self._h, C.c_long(key)), "comm_init_loopback")
+
+    def allreduce_histogram(self, counts: torch.Tensor):
+        _check(lib().occ_allreduce_histogram(self._h, _ptr(counts), _stream()), "allreduce_histogram")
+        return counts
 
     def set_validate(self, on: bool):
         _check(lib().occ_set_validate(self._h, int(on)), "set_validate")
@@ -450,6 +470,17 @@ def reschedule_placement(p, num_devices: int) -> Placement:
                                           out.ctypes.data_as(C.c_void_p)), "reschedule_placement")
     per = e // num_devices
     return Placement([out[d * per:(d + 1) * per].tolist() for d in range(num_devices)])
+
+
+def exchange_layout(counts, rank: int):
+    """occ_exchange_layout: (send_off, send_cnt, recv_off, recv_cnt) per peer."""
+    import numpy as np
+    c = np.ascontiguousarray(counts, dtype=np.int32)
+    nd = c.shape[0]
+    outs = [np.zeros(nd, np.int64) for _ in range(4)]
+    _check(lib().occ_exchange_layout(c.ctypes.data_as(C.c_void_p), nd, rank,
+                                     *[o.ctypes.data_as(C.c_void_p) for o in outs]), "exchange_layout")
+    return tuple(outs)
 
 
 def round_robin_sources(num_tokens: int, num_devices: int, device="cuda") -> torch.Tensor:

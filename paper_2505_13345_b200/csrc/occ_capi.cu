@@ -20,10 +20,16 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <condition_variable>
+#include <map>
+#include <memory>
+#include <mutex>
 #include <cstdio>
 #include <cstring>
 #include <string>
 #include <vector>
+
+#include <nccl.h>
 
 #include "../../include/occult.h"
 #include "occ_internal.h"
@@ -38,6 +44,12 @@ occ_status fail(occ_status s, const std::string& msg) {
     g_err = msg;
     return s;
 }
+
+#define NCCL_TRY(x)                                                                        \
+    do {                                                                                   \
+        ncclResult_t r_ = (x);                                                             \
+        if (r_ != ncclSuccess) return fail(OCC_ERR_NCCL, std::string(#x) + ": " + ncclGetErrorString(r_)); \
+    } while (0)
 
 #define CUDA_TRY(x)                                                                        \
     do {                                                                                   \
@@ -70,6 +82,24 @@ struct DevBuf {
 // Stage boundaries recorded by occ_forward_expert_parallel / occ_forward.
 enum Stage { ST_ROUTE = 0, ST_PLAN, ST_PACK, ST_CINDEX, ST_GATHER, ST_GEMM1, ST_GEMM2, ST_PCOMBINE, ST_COMBINE, kStages };
 
+// ------------------------------------------------------------ transport --
+// The two exchanges of the EP layer are an all-gather of the per-source
+// count rows and variable-size all-to-alls.  NcclTransport is the product
+// multi-GPU path (NVLink/NVSwitch); LoopbackTransport runs N ranks as host
+// threads on ONE GPU (device-to-device copies between the ranks' buffers) so
+// the world_size > 1 code path can be validated on a single B200.
+struct Transport {
+    virtual ~Transport() {}
+    virtual const char* name() const = 0;
+    // send: this rank's nd ints (device); recv: nd x nd ints (device), row s = rank s
+    virtual occ_status allgather_counts(const int* send, int* recv, int nd, cudaStream_t st) = 0;
+    // variable all-to-all in elements of `es` bytes; offsets/counts in elements per peer
+    virtual occ_status alltoallv(const void* send, const std::vector<size_t>& soff, const std::vector<size_t>& scnt,
+                                 void* recv, const std::vector<size_t>& roff, const std::vector<size_t>& rcnt, int es,
+                                 cudaStream_t st) = 0;
+    virtual occ_status allreduce_i64(int64_t* buf, size_t count, cudaStream_t st) = 0;
+};
+
 struct alignas(64) TmapBox {
     alignas(64) unsigned char bytes[128];
 };
@@ -91,7 +121,13 @@ struct occ_handle {
     // workspace
     int n_cap = -1;
     DevBuf<uint64_t> mask, rmask;
-    DevBuf<int32_t> group, rgroup, chunk_cnt, totals, totals2;
+    DevBuf<int32_t> group, rgroup, chunk_cnt, chunk_cnt2, totals, totals2, c_all;
+    DevBuf<__nv_bfloat16> snd_x, y_src;  // world_size > 1: Sfd send batch, returned rows
+    DevBuf<int32_t> snd_ids;
+    DevBuf<float> snd_w;
+    int* d_R = nullptr;                   // device copy of the received row count
+    int last_R = 0;
+    std::vector<int> h_C;                 // host copy of the (source, destination) counts
     DevBuf<int> offs;  // dispatch + compute offset arrays
     DevBuf<long long> stats;
     DevBuf<int32_t> err;
@@ -109,8 +145,8 @@ struct occ_handle {
     int* d_tok_base = nullptr;
     int* d_n_mblk = nullptr;
     int* d_q_total = nullptr;
-    // NCCL (world_size > 1)
-    void* nccl_comm = nullptr;
+    // world_size > 1
+    Transport* tp = nullptr;
     // stage profiling (CUDA events on the launching stream)
     int profiling = 0;
     cudaEvent_t ev[kStages + 1] = {};
@@ -125,6 +161,117 @@ struct occ_handle {
 };
 
 namespace {
+
+
+// ---------------------------------------------------------- transports ---
+struct NcclTransport : Transport {
+    ncclComm_t comm;
+    int world;
+    explicit NcclTransport(ncclComm_t c, int w) : comm(c), world(w) {}
+    ~NcclTransport() override { ncclCommDestroy(comm); }
+    const char* name() const override { return "nccl"; }
+    occ_status allgather_counts(const int* send, int* recv, int nd, cudaStream_t st) override {
+        NCCL_TRY(ncclAllGather(send, recv, nd, ncclInt32, comm, st));
+        return OCC_OK;
+    }
+    occ_status alltoallv(const void* send, const std::vector<size_t>& soff, const std::vector<size_t>& scnt, void* recv,
+                         const std::vector<size_t>& roff, const std::vector<size_t>& rcnt, int es,
+                         cudaStream_t st) override {
+        const char* sp = reinterpret_cast<const char*>(send);
+        char* rp = reinterpret_cast<char*>(recv);
+        NCCL_TRY(ncclGroupStart());
+        for (int p = 0; p < world; ++p) {
+            if (scnt[p]) NCCL_TRY(ncclSend(sp + soff[p] * es, scnt[p] * es, ncclUint8, p, comm, st));
+            if (rcnt[p]) NCCL_TRY(ncclRecv(rp + roff[p] * es, rcnt[p] * es, ncclUint8, p, comm, st));
+        }
+        NCCL_TRY(ncclGroupEnd());
+        return OCC_OK;
+    }
+    occ_status allreduce_i64(int64_t* buf, size_t count, cudaStream_t st) override {
+        NCCL_TRY(ncclAllReduce(buf, buf, count, ncclInt64, ncclSum, comm, st));
+        return OCC_OK;
+    }
+};
+
+// N ranks as host threads of one process on one GPU.
+struct LoopGroup {
+    int world;
+    std::mutex m;
+    std::condition_variable cv;
+    int arrived = 0;
+    long gen = 0;
+    std::vector<const void*> send;
+    std::vector<std::vector<size_t>> soff, scnt;
+    std::vector<std::vector<int>> counts;
+    std::vector<std::vector<int64_t>> vals;
+    explicit LoopGroup(int w) : world(w), send(w), soff(w), scnt(w), counts(w), vals(w) {}
+    void barrier() {
+        std::unique_lock<std::mutex> lk(m);
+        const long g = gen;
+        if (++arrived == world) {
+            arrived = 0;
+            ++gen;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return gen != g; });
+        }
+    }
+};
+std::mutex g_loop_m;
+std::map<long, std::shared_ptr<LoopGroup>> g_loop;
+
+struct LoopbackTransport : Transport {
+    std::shared_ptr<LoopGroup> grp;
+    int rank;
+    LoopbackTransport(std::shared_ptr<LoopGroup> g, int r) : grp(std::move(g)), rank(r) {}
+    const char* name() const override { return "loopback"; }
+    occ_status allgather_counts(const int* send, int* recv, int nd, cudaStream_t st) override {
+        std::vector<int> mine(nd);
+        CUDA_TRY(cudaMemcpyAsync(mine.data(), send, sizeof(int) * nd, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        grp->counts[rank] = mine;
+        grp->barrier();
+        std::vector<int> all((size_t)nd * nd);
+        for (int s = 0; s < nd; ++s) std::copy(grp->counts[s].begin(), grp->counts[s].end(), all.begin() + (size_t)s * nd);
+        grp->barrier();
+        CUDA_TRY(cudaMemcpyAsync(recv, all.data(), sizeof(int) * all.size(), cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        return OCC_OK;
+    }
+    occ_status alltoallv(const void* send, const std::vector<size_t>& soff, const std::vector<size_t>& scnt, void* recv,
+                         const std::vector<size_t>& roff, const std::vector<size_t>& rcnt, int es,
+                         cudaStream_t st) override {
+        CUDA_TRY(cudaStreamSynchronize(st));  // send data complete
+        grp->send[rank] = send;
+        grp->soff[rank] = soff;
+        grp->scnt[rank] = scnt;
+        grp->barrier();
+        char* rp = reinterpret_cast<char*>(recv);
+        for (int p = 0; p < grp->world; ++p) {
+            if (grp->scnt[p][rank] != rcnt[p]) return fail(OCC_ERR_SHAPE, "loopback: send/recv count mismatch");
+            if (!rcnt[p]) continue;
+            const char* src = reinterpret_cast<const char*>(grp->send[p]) + grp->soff[p][rank] * es;
+            CUDA_TRY(cudaMemcpyAsync(rp + roff[p] * es, src, rcnt[p] * es, cudaMemcpyDeviceToDevice, st));
+        }
+        CUDA_TRY(cudaStreamSynchronize(st));
+        grp->barrier();  // peers may reuse their send buffers only after every copy landed
+        return OCC_OK;
+    }
+    occ_status allreduce_i64(int64_t* buf, size_t count, cudaStream_t st) override {
+        std::vector<int64_t> mine(count);
+        CUDA_TRY(cudaMemcpyAsync(mine.data(), buf, sizeof(int64_t) * count, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        grp->vals[rank] = mine;
+        grp->barrier();
+        std::vector<int64_t> sum(count, 0);
+        for (int p = 0; p < grp->world; ++p)
+            for (size_t i = 0; i < count; ++i) sum[i] += grp->vals[p][i];
+        grp->barrier();
+        CUDA_TRY(cudaMemcpyAsync(buf, sum.data(), sizeof(int64_t) * count, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        return OCC_OK;
+    }
+};
 
 occ_status validate_placement(const occ_config& c, const int32_t* pl, std::vector<int32_t>& dev_of,
                               std::vector<int32_t>& slot_of) {
@@ -156,51 +303,79 @@ occ_status upload_tables(occ_handle* h) {
     return OCC_OK;
 }
 
-// Grow-only workspace for n tokens.
+// Receive-side (expert-compute) workspace for R inbox rows.  world_size
+// == 1: R is the static dedup bound n * min(k, N_d) (n * k for the naive
+// path) and n_epd = n * k exactly; world_size > 1: R is the exact received
+// row count (known after the count exchange) and n_epd <= R * min(k, P).
+occ_status ensure_recv(occ_handle* h, size_t R, size_t epd_bound) {
+    const int k = h->k, P = h->P, D = h->D, F = h->F;
+    const int G = h->world == 1 ? h->nd : 1;
+    size_t Q = epd_bound + (size_t)G * P * (kBM - 1);
+    Q = (Q + kBM - 1) / kBM * kBM;
+    const size_t nchunks = (R + kRankChunk - 1) / kRankChunk + 1;
+    const size_t K2 = (size_t)G * (P + 1);
+    CUDA_TRY(h->chunk_cnt2.ensure(nchunks * K2));
+    if (R > h->R_max || !h->in_x.p) {
+        CUDA_TRY(h->in_x.ensure(R * D));
+        CUDA_TRY(h->in_ids.ensure(R * k));
+        CUDA_TRY(h->in_w.ensure(R * k));
+        CUDA_TRY(h->in_tok.ensure(R));
+        CUDA_TRY(h->in_src.ensure(R));
+        CUDA_TRY(h->in_slot.ensure(R));
+        CUDA_TRY(h->in_dev.ensure(R));
+        CUDA_TRY(h->rmask.ensure(R));
+        CUDA_TRY(h->rgroup.ensure(R));
+        CUDA_TRY(h->row_epd.ensure(R * P));
+        CUDA_TRY(h->ret.ensure(R * D));
+        h->R_max = R;
+    }
+    if (Q > h->Q_max || !h->x_epd.p) {
+        CUDA_TRY(h->epd_src.ensure(Q));
+        CUDA_TRY(h->epd_w.ensure(Q));
+        CUDA_TRY(h->x_epd.ensure(Q * D));
+        CUDA_TRY(h->hbuf.ensure(Q * F));
+        CUDA_TRY(h->ybuf.ensure(Q * D));
+        h->Q_max = Q;
+        h->max_mblk = Q / kBM;
+        if (!make_tmap_2d(h->tmA1.bytes, h->x_epd.p, D, h->Q_max, 64, kBM / 2) ||
+            !make_tmap_2d(h->tmA2.bytes, h->hbuf.p, F, h->Q_max, 64, kBM / 2))
+            return fail(OCC_ERR_CUDA, "cuTensorMapEncodeTiled failed (A operands)");
+    }
+    return OCC_OK;
+}
+
+// Grow-only token-side workspace for n tokens (+ the receive side when all
+// devices are local).
 occ_status ensure_ws(occ_handle* h, int n) {
     if (n <= h->n_cap) return OCC_OK;
-    const int nd = h->nd, k = h->k, P = h->P, D = h->D, F = h->F;
+    const int nd = h->nd, k = h->k, P = h->P, D = h->D;
     const int G = h->world == 1 ? nd : 1;
     const int dedup = h->cfg.dedup;
     const size_t items = dedup ? (size_t)n : (size_t)n * k;
     const size_t span_max = dedup ? (size_t)std::min(k, nd) : (size_t)k;
-    h->R_max = (size_t)n * span_max;
-    if (h->world > 1) h->R_max = h->R_max * 1;  // recv rows bounded by the same per-source bound x world
-    h->Q_max = (size_t)n * k + (size_t)G * P * (kBM - 1);
-    h->Q_max = (h->Q_max + kBM - 1) / kBM * kBM;
-    h->max_mblk = h->Q_max / kBM;
-    const size_t K1 = (size_t)nd * (nd + 1), K2 = (size_t)G * (P + 1);
-    const size_t nchunks = (std::max(items, h->R_max) + kRankChunk - 1) / kRankChunk + 1;
+    const size_t nchunks = (items + kRankChunk - 1) / kRankChunk + 1;
+    const size_t K1 = (size_t)nd * (nd + 1);
     CUDA_TRY(h->mask.ensure(items));
     CUDA_TRY(h->group.ensure(items));
-    CUDA_TRY(h->chunk_cnt.ensure(nchunks * std::max(K1, K2)));
+    CUDA_TRY(h->chunk_cnt.ensure(nchunks * K1));
     CUDA_TRY(h->totals.ensure(K1));
-    CUDA_TRY(h->totals2.ensure(K2));
+    CUDA_TRY(h->totals2.ensure((size_t)G * (P + 1)));
+    CUDA_TRY(h->c_all.ensure((size_t)nd * nd + nd));
     // offsets: C, off_sd, inoff (3 nd^2) + in_base(nd+1) + nsfd(nd) + src_base(nd+1) + tok_base(2nd)
-    //          + cnt/seg_base/unp_base (3 G P) + grp_mb (G P + 1) + n_mblk + q_total
-    const size_t noffs = 3 * (size_t)nd * nd + (nd + 1) + nd + (nd + 1) + 2 * nd + 4 * (size_t)G * P + 3;
+    //          + cnt/seg_base/unp_base (3 G P) + grp_mb (G P + 1) + n_mblk + q_total + R_dev
+    const size_t noffs = 3 * (size_t)nd * nd + (nd + 1) + nd + (nd + 1) + 2 * nd + 4 * (size_t)G * P + 4;
     CUDA_TRY(h->offs.ensure(noffs));
     CUDA_TRY(h->stats.ensure(8));
     CUDA_TRY(h->err.ensure(1));
     CUDA_TRY(h->tok_row.ensure(dedup ? (size_t)n * nd : items));
     CUDA_TRY(h->tok_sfd.ensure(dedup ? (size_t)n * nd : items));
     CUDA_TRY(h->lam.ensure(n));
-    CUDA_TRY(h->in_x.ensure(h->R_max * D));
-    CUDA_TRY(h->in_ids.ensure(h->R_max * k));
-    CUDA_TRY(h->in_w.ensure(h->R_max * k));
-    CUDA_TRY(h->in_tok.ensure(h->R_max));
-    CUDA_TRY(h->in_src.ensure(h->R_max));
-    CUDA_TRY(h->in_slot.ensure(h->R_max));
-    CUDA_TRY(h->in_dev.ensure(h->R_max));
-    CUDA_TRY(h->rmask.ensure(h->R_max));
-    CUDA_TRY(h->rgroup.ensure(h->R_max));
-    CUDA_TRY(h->row_epd.ensure(h->R_max * P));
-    CUDA_TRY(h->epd_src.ensure(h->Q_max));
-    CUDA_TRY(h->epd_w.ensure(h->Q_max));
-    CUDA_TRY(h->x_epd.ensure(h->Q_max * D));
-    CUDA_TRY(h->hbuf.ensure(h->Q_max * F));
-    CUDA_TRY(h->ybuf.ensure(h->Q_max * D));
-    CUDA_TRY(h->ret.ensure(h->R_max * D));
+    if (h->world > 1) {  // send batch (Sfd, device-major) and the returned rows
+        CUDA_TRY(h->snd_x.ensure((size_t)n * span_max * D));
+        CUDA_TRY(h->snd_ids.ensure((size_t)n * span_max * k));
+        CUDA_TRY(h->snd_w.ensure((size_t)n * span_max * k));
+        CUDA_TRY(h->y_src.ensure((size_t)n * span_max * D));
+    }
     int* o = h->offs.p;
     DispatchOffsets& d = h->dofs;
     d.C = o; o += nd * nd;
@@ -219,14 +394,15 @@ occ_status ensure_ws(occ_handle* h, int n) {
     c.grp_mb = o; o += G * P + 1;
     c.n_mblk = o; o += 1;
     c.q_total = o; o += 1;
+    h->d_R = o; o += 1;
     c.widx = h->d_widx.p;
     c.stats = h->stats.p;
     h->d_n_mblk = c.n_mblk;
     h->d_q_total = c.q_total;
-    // A-operand tensor maps (buffers just (re)allocated)
-    if (!make_tmap_2d(h->tmA1.bytes, h->x_epd.p, D, h->Q_max, 64, kBM / 2) ||
-        !make_tmap_2d(h->tmA2.bytes, h->hbuf.p, F, h->Q_max, 64, kBM / 2))
-        return fail(OCC_ERR_CUDA, "cuTensorMapEncodeTiled failed (A operands)");
+    if (h->world == 1) {
+        occ_status s = ensure_recv(h, (size_t)n * span_max, (size_t)n * k);
+        if (s != OCC_OK) return s;
+    }
     h->n_cap = n;
     return OCC_OK;
 }
@@ -283,6 +459,119 @@ occ_status check_err(occ_handle* h, cudaStream_t st) {
 
 }  // namespace
 
+__global__ void c_to_totals_kernel(int nd, const int* C, int* totals) {
+    // full (source, destination) count matrix -> the rank-key layout s*(nd+1)+d
+    for (int i = threadIdx.x; i < nd * (nd + 1); i += blockDim.x) {
+        const int s = i / (nd + 1), d = i % (nd + 1);
+        totals[i] = d < nd ? C[s * nd + d] : 0;
+    }
+}
+
+// Expert-parallel forward across world_size == N_d GPUs (this rank = EP
+// device `rank`, owning the tokens in x).  Exchange layout (all_to_all_exchange,
+// pipeline.cpp:125-176): the send batch is this source's Sfd batch
+// (device-major BRIM0 counters, so the rows for destination d are contiguous
+// at off[rank][d]); the inbox of this device is ordered (source asc, counter
+// asc), i.e. source s lands at inoff[rank][s] = sum_{s'<s} C[s'][rank].  The
+// return exchange is the exact inverse: inbox rows go back into the source's
+// Sfd slots, which combine (pipeline.cpp:285-300) reads by BRIM0 counter.
+occ_status forward_multi(occ_handle* h, const __nv_bfloat16* x, const int32_t* ids, const float* weights, int n,
+                         __nv_bfloat16* out, cudaStream_t st) {
+    if (!h->tp) return fail(OCC_ERR_STATE, "forward: world_size > 1 needs occ_comm_init");
+    Transport* tp = h->tp;
+    const int nd = h->nd, k = h->k, P = h->P, D = h->D, F = h->F, dedup = h->cfg.dedup, r = h->rank;
+    const int items = dedup ? n : n * k;
+    occ_status s = ensure_ws(h, std::max(n, 1));
+    if (s != OCC_OK) return s;
+    CUDA_TRY(cudaMemsetAsync(h->stats.p, 0, sizeof(long long) * 8, st));
+    CUDA_TRY(cudaMemsetAsync(h->err.p, 0, sizeof(int32_t), st));
+    if (!h->in_ep) h->ev_recorded = 0;
+    mark(h, ST_PLAN, st);
+    // 1. local dispatch plan: counts to every destination, all-gathered
+    PlanArgs pa{n, k, nd, dedup, ids, weights, nullptr, r, h->d_dev_of.p, h->d_slot_of.p, h->E, h->mask.p,
+                h->group.p, h->err.p};
+    launch_plan_mask(pa, st);
+    RankWs ws{h->chunk_cnt.p, h->totals.p};
+    launch_rank_count(items, h->group.p, h->mask.p, 1, nd, ws, st);
+    launch_rank_scan(items, 1, nd, ws, st);
+    int* C_all = h->c_all.p;
+    s = tp->allgather_counts(h->totals.p, C_all, nd, st);
+    if (s != OCC_OK) return s;
+    c_to_totals_kernel<<<1, 256, 0, st>>>(nd, C_all, h->totals.p);
+    count_launch();
+    launch_dispatch_finalize(nd, h->totals.p, h->dofs, st);
+    EmitDispatch em{n, k, nd, dedup, ids, weights, nullptr, r, h->d_dev_of.p, h->dofs, 0, h->tok_row.p,
+                    h->tok_sfd.p, h->lam.p, nullptr, nullptr, nullptr, nullptr};
+    launch_rank_emit_dispatch(items, h->group.p, h->mask.p, 1, nd, ws, em, st);
+    launch_token_stats(n, k, nd, ids, nullptr, r, h->d_dev_of.p, h->stats.p, st);
+    // 2. pack this source's Sfd batch
+    mark(h, ST_PACK, st);
+    PackArgs pk{n, k, nd, D, dedup, x, ids, weights, h->mask.p, h->tok_row.p, h->snd_x.p, h->snd_ids.p, h->snd_w.p};
+    launch_pack(pk, st);
+    // 3. dispatch all-to-all (counts are needed on the host for NCCL)
+    h->h_C.resize((size_t)nd * nd);
+    CUDA_TRY(cudaMemcpyAsync(h->h_C.data(), C_all, sizeof(int) * nd * nd, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    std::vector<int64_t> off(nd), scnt64(nd), inoff(nd), rcnt64(nd);
+    occ_exchange_layout(h->h_C.data(), nd, r, off.data(), scnt64.data(), inoff.data(), rcnt64.data());
+    long long R = 0;
+    for (int p = 0; p < nd; ++p) R += rcnt64[p];
+    s = ensure_recv(h, (size_t)std::max<long long>(R, 1), (size_t)std::max<long long>(R, 1) * std::min(k, P));
+    if (s != OCC_OK) return s;
+    h->last_R = (int)R;
+    CUDA_TRY(cudaMemcpyAsync(h->d_R, &h->last_R, sizeof(int), cudaMemcpyHostToDevice, st));
+    std::vector<size_t> so(nd), sc(nd), ro(nd), rc(nd);
+    for (int p = 0; p < nd; ++p) {
+        so[p] = (size_t)off[p];
+        sc[p] = (size_t)scnt64[p];
+        ro[p] = (size_t)inoff[p];
+        rc[p] = (size_t)rcnt64[p];
+    }
+    if ((s = tp->alltoallv(h->snd_x.p, so, sc, h->in_x.p, ro, rc, D * 2, st)) != OCC_OK) return s;
+    if ((s = tp->alltoallv(h->snd_ids.p, so, sc, h->in_ids.p, ro, rc, k * 4, st)) != OCC_OK) return s;
+    if ((s = tp->alltoallv(h->snd_w.p, so, sc, h->in_w.p, ro, rc, k * 4, st)) != OCC_OK) return s;
+    // 4. compute index over the received rows
+    mark(h, ST_CINDEX, st);
+    const int Rm = (int)std::max<long long>(R, 1);
+    ComputeArgs ca{Rm, h->d_R, k, P, 1, h->in_ids.p, h->in_w.p, nullptr, h->d_dev_of.p, h->d_slot_of.p, r,
+                   h->rmask.p, h->rgroup.p, h->err.p};
+    launch_compute_mask(ca, st);
+    RankWs ws2{h->chunk_cnt2.p, h->totals2.p};
+    launch_rank_count_dev(Rm, h->d_R, h->rgroup.p, h->rmask.p, 1, P, ws2, st);
+    launch_rank_scan(Rm, 1, P, ws2, st);
+    launch_compute_finalize(1, P, h->totals2.p, h->cofs, st);
+    launch_init_epd((int)h->Q_max, h->epd_src.p, h->epd_w.p, st);
+    EmitCompute ec{k, P, r, h->in_ids.p, h->in_w.p, h->d_slot_of.p, h->d_dev_of.p, h->cofs, h->row_epd.p,
+                   h->epd_src.p, h->epd_w.p};
+    launch_rank_emit_compute(Rm, h->d_R, h->rgroup.p, h->rmask.p, 1, P, ws2, ec, st);
+    // 5. grouped expert FFN
+    mark(h, ST_GATHER, st);
+    launch_gather_rows((int)h->Q_max, h->d_q_total, h->epd_src.p, h->in_x.p, D, h->x_epd.p, st);
+    mark(h, ST_GEMM1, st);
+    const int max_mb = (int)h->max_mblk;
+    GemmArgs g1{h->tmA1.bytes, h->tmB1.bytes, D, F, h->n1rows, h->cofs.grp_mb, h->d_widx.p, P, 1 << 20,
+                h->epd_w.p, h->hbuf.p, F, h->cfg.activation, max_mb * (h->gated ? F / 128 : (F + 255) / 256)};
+    launch_grouped_gemm(h->gated ? EPI_SWIGLU_BF16 : EPI_ACT_BF16, g1, h->num_sms, st);
+    mark(h, ST_GEMM2, st);
+    GemmArgs g2{h->tmA2.bytes, h->tmB2.bytes, F, D, D, h->cofs.grp_mb, h->d_widx.p, P, 8, nullptr, h->ybuf.p, D, 0,
+                max_mb * ((D + 255) / 256)};
+    launch_grouped_gemm(EPI_F32, g2, h->num_sms, st);
+    // 6. intra-device partial combine -> bf16 return payload in inbox order
+    mark(h, ST_PCOMBINE, st);
+    launch_partial_combine(Rm, h->d_R, P, D, h->row_epd.p, h->ybuf.p, h->ret.p, st);
+    // 7. return all-to-all: inbox rows back to their source's Sfd slots
+    if ((s = tp->alltoallv(h->ret.p, ro, rc, h->y_src.p, so, sc, D * 2, st)) != OCC_OK) return s;
+    // 8. combine over devices ascending
+    mark(h, ST_COMBINE, st);
+    launch_combine(n, nd, k, dedup, D, h->mask.p, h->tok_row.p, h->y_src.p, out, st);
+    mark(h, kStages, st);
+    CUDA_TRY(cudaGetLastError());
+    h->last_n = n;
+    h->have_forward = true;
+    if (h->validate) return check_err(h, st);
+    return OCC_OK;
+}
+
 extern "C" {
 
 const char* occ_last_error(void) { return g_err.c_str(); }
@@ -334,19 +623,21 @@ occ_status occ_create(const occ_config* cfg, const int32_t* placement, int world
 occ_status occ_destroy(occ_handle* h) {
     if (!h) return OCC_OK;
     for (auto* b : {&h->d_dev_of, &h->d_slot_of, &h->d_widx, &h->d_ranking, &h->group, &h->rgroup, &h->chunk_cnt,
-                    &h->totals, &h->totals2, &h->err, &h->tok_row, &h->tok_sfd, &h->lam, &h->in_ids, &h->in_tok,
+                    &h->chunk_cnt2, &h->totals, &h->totals2, &h->c_all, &h->snd_ids, &h->err, &h->tok_row, &h->tok_sfd, &h->lam, &h->in_ids, &h->in_tok,
                     &h->in_src, &h->in_slot, &h->in_dev, &h->row_epd, &h->epd_src})
         b->release();
     h->offs.release();
     h->stats.release();
     h->mask.release();
     h->rmask.release();
-    for (auto* b : {&h->w13t, &h->w2t, &h->in_x, &h->x_epd, &h->hbuf, &h->ret}) b->release();
+    for (auto* b : {&h->w13t, &h->w2t, &h->in_x, &h->x_epd, &h->hbuf, &h->ret, &h->snd_x, &h->y_src}) b->release();
+    h->snd_w.release();
     for (auto* b : {&h->in_w, &h->epd_w, &h->ybuf, &h->logits, &h->rt_w}) b->release();
     h->rt_ids.release();
     for (auto& e : h->ev)
         if (e) cudaEventDestroy(e);
     for (auto& e : h->pev) cudaEventDestroy(e);
+    delete h->tp;
     if (h->s_in) cudaStreamDestroy(h->s_in);
     if (h->s_out) cudaStreamDestroy(h->s_out);
     h->x_stage.release();
@@ -516,9 +807,11 @@ occ_status occ_forward(occ_handle* h, const void* x, const int32_t* ids, const f
     if (!h) return fail(OCC_ERR_ARG, "null handle");
     if (n > 0 && (!x || !ids || !weights || !out)) return fail(OCC_ERR_ARG, "null argument");
     if (!h->weights_loaded) return fail(OCC_ERR_STATE, "forward: experts not loaded");
-    if (h->world != 1) return fail(OCC_ERR_UNSUPPORTED, "forward: world_size > 1 needs occ_comm_init");
     if (n < 0) return fail(OCC_ERR_SHAPE, "forward: negative token count");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (h->world > 1)
+        return forward_multi(h, reinterpret_cast<const __nv_bfloat16*>(x), ids, weights, n,
+                             reinterpret_cast<__nv_bfloat16*>(out), st);
     occ_status s = ensure_ws(h, n);
     if (s != OCC_OK) return s;
     h->last_n = n;
@@ -546,7 +839,7 @@ occ_status occ_forward(occ_handle* h, const void* x, const int32_t* ids, const f
     ComputeArgs ca{R_max, R_total, k, P, G, h->in_ids.p, h->in_w.p, h->in_dev.p, h->d_dev_of.p, h->d_slot_of.p, 0,
                    h->rmask.p, h->rgroup.p, h->err.p};
     launch_compute_mask(ca, st);
-    RankWs ws{h->chunk_cnt.p, h->totals2.p};
+    RankWs ws{h->chunk_cnt2.p, h->totals2.p};
     launch_rank_count_dev(R_max, R_total, h->rgroup.p, h->rmask.p, G, P, ws, st);
     launch_rank_scan(R_max, G, P, ws, st);
     launch_compute_finalize(G, P, h->totals2.p, h->cofs, st);
@@ -627,7 +920,6 @@ occ_status occ_forward_host(occ_handle* h, const void* x_host, const void* gate,
     // are in out_host once occ_host_wait() has been ordered on a stream.
     if (!h) return fail(OCC_ERR_ARG, "null handle");
     if (n > 0 && (!x_host || !gate || !out_host)) return fail(OCC_ERR_ARG, "null argument");
-    if (h->world != 1) return fail(OCC_ERR_UNSUPPORTED, "forward_host: world_size 1");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     chunks = std::max(1, std::min(chunks, 16));
     if (n < chunks) chunks = std::max(1, n);
@@ -747,12 +1039,48 @@ occ_status occ_coactivation_histogram(const int32_t* ids, int n, int k, int e, i
     return OCC_OK;
 }
 
-occ_status occ_comm_unique_id(void*) { return fail(OCC_ERR_UNSUPPORTED, "NCCL path not built in this round"); }
-occ_status occ_comm_init(occ_handle*, const void*) {
-    return fail(OCC_ERR_UNSUPPORTED, "NCCL path not built in this round");
+static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+
+occ_status occ_comm_unique_id(void* id128) {
+    if (!id128) return fail(OCC_ERR_ARG, "null id buffer");
+    ncclUniqueId id;
+    NCCL_TRY(ncclGetUniqueId(&id));
+    std::memcpy(id128, &id, sizeof(id));
+    return OCC_OK;
 }
-occ_status occ_allreduce_histogram(occ_handle*, int64_t*, occ_stream_t) {
-    return fail(OCC_ERR_UNSUPPORTED, "NCCL path not built in this round");
+
+occ_status occ_comm_init(occ_handle* h, const void* id128) {
+    if (!h || !id128) return fail(OCC_ERR_ARG, "null argument");
+    if (h->world == 1) return OCC_OK;  // all devices local: no communicator needed
+    ncclUniqueId id;
+    std::memcpy(&id, id128, sizeof(id));
+    ncclComm_t comm;
+    NCCL_TRY(ncclCommInitRank(&comm, h->world, id, h->rank));
+    delete h->tp;
+    h->tp = new NcclTransport(comm, h->world);
+    return OCC_OK;
+}
+
+occ_status occ_comm_init_loopback(occ_handle* h, long group_key) {
+    if (!h) return fail(OCC_ERR_ARG, "null handle");
+    if (h->world == 1) return OCC_OK;
+    std::shared_ptr<LoopGroup> g;
+    {
+        std::lock_guard<std::mutex> lk(g_loop_m);
+        auto& slot = g_loop[group_key];
+        if (!slot || slot->world != h->world) slot = std::make_shared<LoopGroup>(h->world);
+        g = slot;
+    }
+    delete h->tp;
+    h->tp = new LoopbackTransport(g, h->rank);
+    return OCC_OK;
+}
+
+occ_status occ_allreduce_histogram(occ_handle* h, int64_t* counts, occ_stream_t stream) {
+    if (!h || !counts) return fail(OCC_ERR_ARG, "null argument");
+    if (h->world == 1) return OCC_OK;
+    if (!h->tp) return fail(OCC_ERR_STATE, "occ_comm_init first");
+    return h->tp->allreduce_i64(counts, (size_t)h->E * h->E, reinterpret_cast<cudaStream_t>(stream));
 }
 
 }  // extern "C"

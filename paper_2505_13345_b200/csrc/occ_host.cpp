@@ -84,3 +84,31 @@ extern "C" occ_status occ_reschedule_placement(const double* p, int ne, int nd, 
     }
     return OCC_OK;
 }
+
+// Layout of the two all-to-alls for EP rank `rank` given the all-gathered
+// (source, destination) Sfd row counts C [nd x nd] (all_to_all_exchange,
+// pipeline.cpp:125-176):
+//   send to p  : this source's Sfd batch is device-major (BRIM0 counters,
+//                pipeline.cpp:31-47), so the rows for p start at
+//                sum_{d<p} C[rank][d] and number C[rank][p];
+//   recv from p: the inbox is ordered (source asc, counter asc), so source p
+//                lands at sum_{s<p} C[s][rank] and brings C[p][rank] rows.
+// The return all-to-all uses the same four arrays with send/recv swapped.
+extern "C" occ_status occ_exchange_layout(const int32_t* C, int nd, int rank, int64_t* send_off, int64_t* send_cnt,
+                                          int64_t* recv_off, int64_t* recv_cnt) {
+    if (!C || !send_off || !send_cnt || !recv_off || !recv_cnt) return OCC_ERR_ARG;
+    if (nd < 1 || rank < 0 || rank >= nd) return OCC_ERR_CONFIG;
+    int64_t so = 0, ro = 0;
+    for (int p = 0; p < nd; ++p) {
+        const int64_t sc = C[static_cast<size_t>(rank) * nd + p];
+        const int64_t rc = C[static_cast<size_t>(p) * nd + rank];
+        if (sc < 0 || rc < 0) return OCC_ERR_SHAPE;
+        send_off[p] = so;
+        send_cnt[p] = sc;
+        recv_off[p] = ro;
+        recv_cnt[p] = rc;
+        so += sc;
+        ro += rc;
+    }
+    return OCC_OK;
+}

@@ -414,3 +414,66 @@ def test_forward_host_pipeline_matches_device(chunks):
     layer.forward_host(xh, gs, oh, chunks=chunks)
     torch.cuda.synchronize()
     assert torch.equal(oh, want)
+
+
+# ------------------------------------------- world_size > 1 (loopback) -----
+
+@pytest.mark.parametrize("nd,ne,k,act,dedup", [(2, 8, 2, "silu", True), (4, 16, 4, "silu", True),
+                                               (8, 64, 8, "relu", True), (4, 8, 3, "identity", False),
+                                               (2, 8, 2, "swiglu", True)])
+def test_multi_rank_forward_loopback(nd, ne, k, act, dedup):
+    """The world_size == N_d code path (per-rank plan, count all-gather, two
+    variable all-to-alls, per-device BRIM1 + GEMMs + partial combine,
+    combine) with the ranks as threads on one GPU, against the reference's
+    single-process simulation with sources = owning rank."""
+    import threading
+    dm, dh = 128, 256
+    n_per = [37, 64, 5, 100, 0, 64, 33, 1][:nd]
+    n = sum(n_per)
+    gated = act == "swiglu"
+    x, g, w1, w2, w3 = make_layer_inputs(nd * 13 + k, n, dm, dh, ne, gated=gated)
+    ids, w = random_routing(n, ne, k, np.random.default_rng(nd + k))
+    w = w.astype(np.float32).astype(np.float64)
+    plist = _placement(ne, nd, "shuffled", seed=nd)
+    src = np.concatenate([np.full(c, r, np.int32) for r, c in enumerate(n_per)])
+    if gated:
+        want, rep = O.Port().forward_given_routing(x, ids, w, w1, w2, plist, src, act="silu", single=False, w3=w3,
+                                                   bytes_per_scalar=2)
+    else:
+        want, rep = ref().forward_given_routing(x, ids, w, w1, w2, plist, src, act=act, single=False,
+                                                bytes_per_scalar=2)
+    outs = [None] * nd
+    errs = []
+    starts = np.concatenate([[0], np.cumsum(n_per)])
+    key = np.random.default_rng().integers(1 << 30)
+
+    def rank_main(r):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                cfg = occ.MoEConfig(ne, k, nd, dm, dh, activation=act, dedup=dedup)
+                layer = occ.ExpertParallelLayer(cfg, occ.Placement([list(p) for p in plist]), world_size=nd, rank=r)
+                loc = plist[r]
+                layer.load_experts(cuda(w1[loc], torch.bfloat16), cuda(w2[loc], torch.bfloat16),
+                                   cuda(w3[loc], torch.bfloat16) if gated else None)
+                layer.comm_init_loopback(int(key))
+                a, b = starts[r], starts[r + 1]
+                out = layer.forward_given_routing(cuda(x[a:b], torch.bfloat16), cuda(ids[a:b]),
+                                                  cuda(w[a:b], torch.float32))
+                st.synchronize()
+                outs[r] = (out.double().cpu().numpy(), layer.comm_report(bytes_per_scalar=2))
+        except Exception as e:  # surface thread failures
+            errs.append(e)
+
+    ths = [threading.Thread(target=rank_main, args=(r,)) for r in range(nd)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join(timeout=120)
+    assert not errs, errs
+    got = np.concatenate([o[0] for o in outs])
+    assert rel_err(got, want) <= TOL
+    r0 = outs[0][1]
+    if dedup:
+        assert r0.cross_device_bytes == rep.cross_device_bytes
+        assert r0.per_device_token_counts == [rep.per_device_rows[d] for d in range(nd)]
