@@ -2,7 +2,7 @@
  * occult.h — C-ABI of the B200-native Occult expert-parallel MoE layer.
  *
  * Drop-in boundary for the reference's C++ library API (moesim, namespace
- * `moesim`; /root/reference/proj/include/moesim/*.hpp).  Every entry point
+ * `moesim`; /root/reference/proj/include/moesim/ headers).  Every entry point
  * below names the reference interface it replaces.  The reference is a
  * header-level C++ library with value semantics and exceptions; this ABI is
  * plain C: device buffers are caller-owned raw pointers, every call is

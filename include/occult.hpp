@@ -1,0 +1,123 @@
+// occult.hpp — header-only C++ host mirror of the reference API over the C-ABI
+// (occult.h).  Same names, argument meaning and error behaviour as namespace
+// moesim (/root/reference/proj/include/moesim/*.hpp); buffers are device
+// pointers (bf16 tokens/experts, int32 ids, f32 weights) and every call is
+// ordered on a CUDA stream.  Errors are thrown as the reference's exception
+// types (common.hpp:11-34), translated from occ_status.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "occult.h"
+
+namespace occult {
+
+struct ShapeError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct ConfigError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct PlacementError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct RoutingError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct CapacityError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct StateError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct DeviceError : std::runtime_error { using std::runtime_error::runtime_error; };
+
+inline void check(occ_status s, const char* what) {
+    if (s == OCC_OK) return;
+    const std::string msg = std::string(what) + ": " + occ_last_error();
+    switch (s) {
+        case OCC_ERR_SHAPE: throw ShapeError(msg);
+        case OCC_ERR_CONFIG: throw ConfigError(msg);
+        case OCC_ERR_PLACEMENT: throw PlacementError(msg);
+        case OCC_ERR_ROUTING: throw RoutingError(msg);
+        case OCC_ERR_CAPACITY: throw CapacityError(msg);
+        case OCC_ERR_STATE: throw StateError(msg);
+        default: throw DeviceError(msg);
+    }
+}
+
+// moesim::Placement (placement.hpp:14-25): per-device expert lists.
+struct Placement {
+    std::vector<std::vector<int>> devices;
+    int num_devices() const { return static_cast<int>(devices.size()); }
+    std::vector<int32_t> flat() const {
+        std::vector<int32_t> f;
+        for (const auto& d : devices) f.insert(f.end(), d.begin(), d.end());
+        return f;
+    }
+};
+
+inline Placement trivial_placement(int num_experts, int num_devices) {  // placement.cpp:47-58
+    if (num_devices < 1 || num_experts < 1 || num_experts % num_devices)
+        throw ConfigError("trivial_placement: num_experts must be a positive multiple of num_devices");
+    Placement p;
+    const int per = num_experts / num_devices;
+    p.devices.resize(num_devices);
+    for (int d = 0; d < num_devices; ++d)
+        for (int i = 0; i < per; ++i) p.devices[d].push_back(d * per + i);
+    return p;
+}
+
+// moesim::reschedule_placement (placement.cpp:88-148), host, bit-exact.
+inline Placement reschedule_placement(const std::vector<double>& norm_graph, int num_experts, int num_devices) {
+    std::vector<int32_t> flat(num_experts);
+    check(occ_reschedule_placement(norm_graph.data(), num_experts, num_devices, flat.data()), "reschedule_placement");
+    Placement p;
+    const int per = num_experts / num_devices;
+    for (int d = 0; d < num_devices; ++d) p.devices.emplace_back(flat.begin() + d * per, flat.begin() + (d + 1) * per);
+    return p;
+}
+
+struct CommReport {  // moesim::CommReport (collab.hpp:36-43)
+    double mean_replicas = 0, cap_replicas = 0, intra_share = 0, inter_share = 0;
+    long long cross_device_bytes = 0, naive_crossing_rows = 0;
+    std::vector<long long> per_device_token_counts;
+};
+
+// One GPU's share of the EP layer: router config + placement + resident experts.
+class Layer {
+  public:
+    Layer(const occ_config& cfg, const Placement& placement, int world_size = 1, int rank = 0) : cfg_(cfg) {
+        const auto flat = placement.flat();
+        if (static_cast<int>(flat.size()) != cfg.num_experts)
+            throw PlacementError("placement: covers " + std::to_string(flat.size()) + " experts");
+        check(occ_create(&cfg, flat.data(), world_size, rank, &h_), "occ_create");
+    }
+    ~Layer() { occ_destroy(h_); }
+    Layer(const Layer&) = delete;
+    Layer& operator=(const Layer&) = delete;
+
+    occ_handle* handle() const { return h_; }
+
+    // Reference layout (token.hpp:30-44): w1/w3 [E_l, D, F], w2 [E_l, F, D], bf16, device.
+    void load_experts(const void* w1, const void* w2, const void* w3, occ_stream_t s) {
+        check(occ_load_experts(h_, w1, w3, w2, s), "load_experts");
+    }
+    void set_validate(bool on) { check(occ_set_validate(h_, on), "set_validate"); }
+
+    // forward_given_routing (pipeline.cpp:360-501)
+    void forward_given_routing(const void* x, const int32_t* ids, const float* w, const int32_t* sources, int n,
+                               void* out, occ_stream_t s) {
+        check(occ_forward(h_, x, ids, w, sources, n, out, s), "forward_given_routing");
+    }
+    // forward_expert_parallel (pipeline.cpp:503-517)
+    void forward_expert_parallel(const void* x, const void* gate, const occ_prune* prune, const int32_t* sources,
+                                 int n, void* out, occ_stream_t s) {
+        check(occ_forward_expert_parallel(h_, x, gate, prune, sources, n, out, s), "forward_expert_parallel");
+    }
+    CommReport report(int bytes_per_scalar, occ_stream_t s) const {
+        occ_comm_report r{};
+        check(occ_comm_report_get(h_, bytes_per_scalar, &r, s), "comm_report");
+        CommReport c{r.mean_replicas, r.cap_replicas, r.intra_share, r.inter_share, r.cross_device_bytes,
+                     r.naive_crossing_rows, {}};
+        for (int d = 0; d < cfg_.num_devices; ++d) c.per_device_token_counts.push_back(r.per_device_rows[d]);
+        return c;
+    }
+
+  private:
+    occ_config cfg_;
+    occ_handle* h_ = nullptr;
+};
+
+}  // namespace occult
