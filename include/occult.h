@@ -177,6 +177,18 @@ occ_status occ_forward_host(occ_handle* h, const void* x_host, const void* gate,
                             void* out_host, int chunks, occ_stream_t stream);
 /* Make `stream` wait until every enqueued occ_forward_host result is in host memory. */
 occ_status occ_host_wait(occ_handle* h, occ_stream_t stream);
+/* Training: keep the pre-activations and the reference-orientation weights
+ * so occ_backward can follow the next forward (call before occ_load_experts).
+ * world_size 1 in this build. */
+occ_status occ_set_training(occ_handle* h, int on);
+/* backward_vjps (backward.cpp:24-161) for the last occ_forward: routing ids
+ * held fixed, gradients for tokens, expert weights and routing weights.
+ *   upstream  [n, D] bf16 (d loss / d out)
+ *   g_x       [n, D] f32;  g_w1, g_w3 [E_l, D, F] f32 (g_w3 only for SwiGLU);
+ *   g_w2      [E_l, F, D] f32;  g_weights [n, k] f32, aligned with the routing.
+ * StateError if the forward was not run with occ_set_training(h, 1). */
+occ_status occ_backward(occ_handle* h, const void* upstream, float* g_x, float* g_w1, float* g_w3, float* g_w2,
+                        float* g_weights, occ_stream_t stream);
 /* CommReport of the last forward (synchronises the stream).
  * bytes_per_scalar as in forward_given_routing's argument. */
 occ_status occ_comm_report_get(occ_handle* h, int bytes_per_scalar, occ_comm_report* rep, occ_stream_t stream);

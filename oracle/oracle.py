@@ -135,6 +135,7 @@ def ref_lib():
         lib.ref_rng_uniform_stream.argtypes = [C.c_uint64, _i, _p]
         lib.ref_random_matrix.argtypes = [C.c_uint64, _i, _i, _i, _p]
         lib.ref_forward_expert_parallel_mt.argtypes = [_p, _i, _i, _p, _i, _i, _p, _p, _i, _i, _i, _i, _i, _p]
+        lib.ref_backward.argtypes = [_p, _i, _i, _p, _p, _i, _p, _p, _i, _i, _p, _i, _p, _i, _i] + [_p] * 5
         _REF = lib
     return _REF
 
@@ -283,6 +284,26 @@ class _Backend:
         rk = np.empty((ne, ne - 1), np.int32)
         _check(self._fn("similarity_table")(_ptr(h), n, ne, _ptr(v), _ptr(rk)) or 0, "similarity")
         return v, rk
+
+
+def ref_backward(x, ids, w, w1, w2, plist, sources, upstream, act="silu", single=False):
+    """backward_vjps (backward.cpp:24-161) of the REFERENCE after a saving
+    forward: returns (gx, gw1, gw2, g_routing_weights)."""
+    L = ref_lib()
+    x, w, w1, w2, up = _f64(x), _f64(w), _f64(w1), _f64(w2), _f64(upstream)
+    ids, plist, sources = _i32(ids), _i32(plist), _i32(sources)
+    n, dm = x.shape
+    k = ids.shape[1]
+    ne, _, dh = w1.shape
+    gx = np.empty_like(x)
+    gw1 = np.empty_like(w1)
+    gw2 = np.empty_like(w2)
+    gr = np.empty_like(w)
+    rc = L.ref_backward(_ptr(x), n, dm, _ptr(ids), _ptr(w), k, _ptr(w1), _ptr(w2), ne, dh, _ptr(plist),
+                        plist.shape[0], _ptr(sources), ACT[act], int(single), _ptr(up), _ptr(gx), _ptr(gw1),
+                        _ptr(gw2), _ptr(gr))
+    _check(rc, "backward_vjps")
+    return gx, gw1, gw2, gr
 
 
 def ranking_from_values(values):

@@ -275,6 +275,35 @@ int ref_forward_given_routing(const double* x, int n, int dm, const int* ids, co
     })
 }
 
+// backward_vjps (backward.cpp:24-161) after a saving forward_given_routing.
+// Outputs: gx [n, dm], gw1 [ne, dm, dh], gw2 [ne, dh, dm], gr [n, k].
+int ref_backward(const double* x, int n, int dm, const int* ids, const double* w, int k, const double* w1,
+                 const double* w2, int ne, int dh, const int* plist, int nd, const int* sources, int act, int single,
+                 const double* upstream, double* gx, double* gw1, double* gw2, double* gr) {
+    GUARD({
+        MoEConfig cfg;
+        cfg.num_experts = ne;
+        cfg.top_k = k;
+        cfg.num_devices = nd;
+        cfg.embed_dim = dm;
+        cfg.hidden_dim = dh;
+        cfg.precision = single ? Precision::Single : Precision::Double;
+        cfg.activation = static_cast<Activation>(act);
+        TokenMatrix tx(mat(x, n, dm), TokenState::Ori);
+        ForwardState st;
+        (void)forward_given_routing(tx, routing_of(ids, w, n, k), experts_of(w1, w2, ne, dm, dh, act),
+                                    placement_of(plist, nd, ne / nd), cfg, std::span<const int>(sources, n), 4, -1.0,
+                                    &st);
+        Gradients g = backward_vjps(mat(upstream, n, dm), st);
+        std::memcpy(gx, g.x.data.data(), sizeof(double) * g.x.data.size());
+        for (int e = 0; e < ne; ++e) {
+            std::memcpy(gw1 + static_cast<size_t>(e) * dm * dh, g.w1[e].data.data(), sizeof(double) * dm * dh);
+            std::memcpy(gw2 + static_cast<size_t>(e) * dh * dm, g.w2[e].data.data(), sizeof(double) * dh * dm);
+        }
+        std::memcpy(gr, g.routing_weights.data(), sizeof(double) * g.routing_weights.size());
+    })
+}
+
 int ref_dense_given_routing(const double* x, int n, int dm, const int* ids, const double* w, int k,
                             const double* w1, const double* w2, int ne, int dh, int act, int single,
                             double* out) {

@@ -83,7 +83,7 @@ EXPORTS = (
     "occ_comm_unique_id", "occ_comm_init", "occ_gate_scores_f64", "occ_topk_route_f64", "occ_prune_routing_f64",
     "occ_route", "occ_build_dispatch", "occ_forward", "occ_forward_expert_parallel", "occ_comm_report_get",
     "occ_saved_index", "occ_coactivation_histogram", "occ_normalize_graph", "occ_reschedule_placement",
-    "occ_allreduce_histogram", "occ_last_error", "occ_launch_count", "occ_set_profiling", "occ_stage_ms", "occ_forward_host", "occ_host_wait", "occ_comm_init_loopback", "occ_exchange_layout",
+    "occ_allreduce_histogram", "occ_last_error", "occ_launch_count", "occ_set_profiling", "occ_stage_ms", "occ_forward_host", "occ_host_wait", "occ_comm_init_loopback", "occ_exchange_layout", "occ_set_training", "occ_backward",
 )
 
 STAGES = ("route", "plan", "pack", "compute_index", "gather", "gemm1", "gemm2", "partial_combine", "combine")
@@ -285,6 +285,28 @@ class ExpertParallelLayer:
     def allreduce_histogram(self, counts: torch.Tensor):
         _check(lib().occ_allreduce_histogram(self._h, _ptr(counts), _stream()), "allreduce_histogram")
         return counts
+
+    def set_training(self, on: bool = True):
+        """Keep what backward needs (call before load_experts)."""
+        _check(lib().occ_set_training(self._h, int(on)), "set_training")
+
+    def backward(self, upstream: torch.Tensor):
+        """backward_vjps (backward.cpp:24-161) of the last forward: returns
+        dict(x, w1, w3, w2, routing_weights) of fp32 gradients (ids fixed)."""
+        _need_cuda(upstream)
+        c = self.config
+        dev = upstream.device
+        e_l = c.num_experts
+        n = upstream.shape[0]
+        g = {"x": torch.empty((n, c.embed_dim), dtype=torch.float32, device=dev),
+             "w1": torch.empty((e_l, c.embed_dim, c.hidden_dim), dtype=torch.float32, device=dev),
+             "w2": torch.empty((e_l, c.hidden_dim, c.embed_dim), dtype=torch.float32, device=dev),
+             "routing_weights": torch.empty((n, c.top_k), dtype=torch.float32, device=dev)}
+        g["w3"] = torch.empty_like(g["w1"]) if c.activation == "swiglu" else None
+        _check(lib().occ_backward(self._h, _ptr(upstream.to(torch.bfloat16).contiguous()), _ptr(g["x"]),
+                                  _ptr(g["w1"]), _ptr(g["w3"]), _ptr(g["w2"]), _ptr(g["routing_weights"]),
+                                  _stream()), "backward")
+        return g
 
     def set_validate(self, on: bool):
         _check(lib().occ_set_validate(self._h, int(on)), "set_validate")

@@ -133,7 +133,7 @@ struct occ_handle {
     DevBuf<int32_t> err;
     DevBuf<int32_t> tok_row, tok_sfd, lam;
     DevBuf<__nv_bfloat16> in_x, x_epd, hbuf, ret;
-    DevBuf<int32_t> in_ids, in_tok, in_src, in_slot, in_dev, row_epd, epd_src;
+    DevBuf<int32_t> in_ids, in_tok, in_src, in_slot, in_dev, row_epd, epd_src, epd_j;
     DevBuf<float> in_w, epd_w, ybuf, logits, rt_w;
     DevBuf<int32_t> rt_ids;  // routing of occ_forward_expert_parallel
     size_t R_max = 0, Q_max = 0, max_mblk = 0;
@@ -152,6 +152,13 @@ struct occ_handle {
     cudaEvent_t ev[kStages + 1] = {};
     int ev_recorded = 0;
     int in_ep = 0;
+    // training: saved pre-activations + backward workspace
+    int training = 0;
+    bool have_train_state = false;
+    DevBuf<__nv_bfloat16> save_a, save_b, w13o, w2o, g_epd, gpre;
+    DevBuf<float> gw_part, gw_row;
+    TmapBox tmG_k, tmW2o, tmP_k, tmW1o, tmH_mn, tmG_mn, tmX_mn, tmP_mn;
+    int bwd_tmaps_q = -1;
     // host-buffer pipeline (occ_forward_host)
     cudaStream_t s_in = nullptr, s_out = nullptr;
     std::vector<cudaEvent_t> pev;
@@ -329,14 +336,20 @@ occ_status ensure_recv(occ_handle* h, size_t R, size_t epd_bound) {
         CUDA_TRY(h->ret.ensure(R * D));
         h->R_max = R;
     }
+    if (h->training) {
+        CUDA_TRY(h->save_a.ensure(std::max(Q, h->Q_max) * F));
+        if (h->gated) CUDA_TRY(h->save_b.ensure(std::max(Q, h->Q_max) * F));
+    }
     if (Q > h->Q_max || !h->x_epd.p) {
         CUDA_TRY(h->epd_src.ensure(Q));
+        CUDA_TRY(h->epd_j.ensure(Q));
         CUDA_TRY(h->epd_w.ensure(Q));
         CUDA_TRY(h->x_epd.ensure(Q * D));
         CUDA_TRY(h->hbuf.ensure(Q * F));
         CUDA_TRY(h->ybuf.ensure(Q * D));
         h->Q_max = Q;
         h->max_mblk = Q / kBM;
+        h->bwd_tmaps_q = -1;
         if (!make_tmap_2d(h->tmA1.bytes, h->x_epd.p, D, h->Q_max, 64, kBM / 2) ||
             !make_tmap_2d(h->tmA2.bytes, h->hbuf.p, F, h->Q_max, 64, kBM / 2))
             return fail(OCC_ERR_CUDA, "cuTensorMapEncodeTiled failed (A operands)");
@@ -405,6 +418,46 @@ occ_status ensure_ws(occ_handle* h, int n) {
     }
     h->n_cap = n;
     return OCC_OK;
+}
+
+// Forward GEMM-1 (scatter + activation + modulation) and GEMM-2 (merge products).
+void launch_gemm1(occ_handle* h, int ngroups, cudaStream_t st) {
+    GemmArgs g;
+    g.tmap_a = h->tmA1.bytes;
+    g.tmap_b = h->tmB1.bytes;
+    g.K = h->D;
+    g.N = h->F;
+    g.b_rows_per_e = h->n1rows;
+    g.grp_mb = h->cofs.grp_mb;
+    g.grp_w = h->d_widx.p;
+    g.ngroups = ngroups;
+    g.row_w = h->epd_w.p;
+    g.out = h->hbuf.p;
+    g.ldo = h->F;
+    g.act = h->cfg.activation;
+    if (h->training) {
+        g.save_a = h->save_a.p;
+        g.save_b = h->gated ? h->save_b.p : nullptr;
+    }
+    g.max_tiles = (int)h->max_mblk * (h->gated ? h->F / 128 : (h->F + 255) / 256);
+    launch_grouped_gemm(h->gated ? EPI_SWIGLU_BF16 : EPI_ACT_BF16, g, h->num_sms, st);
+}
+
+void launch_gemm2(occ_handle* h, int ngroups, cudaStream_t st) {
+    GemmArgs g;
+    g.tmap_a = h->tmA2.bytes;
+    g.tmap_b = h->tmB2.bytes;
+    g.K = h->F;
+    g.N = h->D;
+    g.b_rows_per_e = h->D;
+    g.grp_mb = h->cofs.grp_mb;
+    g.grp_w = h->d_widx.p;
+    g.ngroups = ngroups;
+    g.band = 8;
+    g.out = h->ybuf.p;
+    g.ldo = h->D;
+    g.max_tiles = (int)h->max_mblk * ((h->D + 255) / 256);
+    launch_grouped_gemm(EPI_F32, g, h->num_sms, st);
 }
 
 __global__ void tok_base_kernel(int nd, int* tok_base) {
@@ -542,20 +595,15 @@ occ_status forward_multi(occ_handle* h, const __nv_bfloat16* x, const int32_t* i
     launch_compute_finalize(1, P, h->totals2.p, h->cofs, st);
     launch_init_epd((int)h->Q_max, h->epd_src.p, h->epd_w.p, st);
     EmitCompute ec{k, P, r, h->in_ids.p, h->in_w.p, h->d_slot_of.p, h->d_dev_of.p, h->cofs, h->row_epd.p,
-                   h->epd_src.p, h->epd_w.p};
+                   h->epd_src.p, h->epd_w.p, h->epd_j.p};
     launch_rank_emit_compute(Rm, h->d_R, h->rgroup.p, h->rmask.p, 1, P, ws2, ec, st);
     // 5. grouped expert FFN
     mark(h, ST_GATHER, st);
     launch_gather_rows((int)h->Q_max, h->d_q_total, h->epd_src.p, h->in_x.p, D, h->x_epd.p, st);
     mark(h, ST_GEMM1, st);
-    const int max_mb = (int)h->max_mblk;
-    GemmArgs g1{h->tmA1.bytes, h->tmB1.bytes, D, F, h->n1rows, h->cofs.grp_mb, h->d_widx.p, P, 1 << 20,
-                h->epd_w.p, h->hbuf.p, F, h->cfg.activation, max_mb * (h->gated ? F / 128 : (F + 255) / 256)};
-    launch_grouped_gemm(h->gated ? EPI_SWIGLU_BF16 : EPI_ACT_BF16, g1, h->num_sms, st);
+    launch_gemm1(h, P, st);
     mark(h, ST_GEMM2, st);
-    GemmArgs g2{h->tmA2.bytes, h->tmB2.bytes, F, D, D, h->cofs.grp_mb, h->d_widx.p, P, 8, nullptr, h->ybuf.p, D, 0,
-                max_mb * ((D + 255) / 256)};
-    launch_grouped_gemm(EPI_F32, g2, h->num_sms, st);
+    launch_gemm2(h, P, st);
     // 6. intra-device partial combine -> bf16 return payload in inbox order
     mark(h, ST_PCOMBINE, st);
     launch_partial_combine(Rm, h->d_R, P, D, h->row_epd.p, h->ybuf.p, h->ret.p, st);
@@ -642,6 +690,10 @@ occ_status occ_destroy(occ_handle* h) {
     if (h->s_out) cudaStreamDestroy(h->s_out);
     h->x_stage.release();
     h->o_stage.release();
+    for (auto* b : {&h->save_a, &h->save_b, &h->w13o, &h->w2o, &h->g_epd, &h->gpre}) b->release();
+    h->gw_part.release();
+    h->gw_row.release();
+    h->epd_j.release();
     delete h;
     return OCC_OK;
 }
@@ -677,6 +729,22 @@ occ_status occ_load_experts(occ_handle* h, const void* w1, const void* w3, const
     }
     launch_transpose_weights(b2, El, F, D, h->w2t.p, D, 0, st);
     CUDA_TRY(cudaGetLastError());
+    if (h->training) {
+        // backward needs the reference orientation: w2 [E, F, D] is K-major for
+        // the merge adjoint (K = D); [w1 | w3] [E, D, F or 2F] for the scatter
+        // adjoint (K = F or 2F).
+        const int kw = h->gated ? 2 * F : F;
+        CUDA_TRY(h->w2o.ensure((size_t)El * F * D));
+        CUDA_TRY(h->w13o.ensure((size_t)El * D * kw));
+        CUDA_TRY(cudaMemcpyAsync(h->w2o.p, b2, sizeof(__nv_bfloat16) * El * F * D, cudaMemcpyDeviceToDevice, st));
+        CUDA_TRY(cudaMemcpy2DAsync(h->w13o.p, kw * 2, b1, F * 2, F * 2, (size_t)El * D, cudaMemcpyDeviceToDevice, st));
+        if (h->gated)
+            CUDA_TRY(cudaMemcpy2DAsync(h->w13o.p + F, kw * 2, w3, F * 2, F * 2, (size_t)El * D,
+                                       cudaMemcpyDeviceToDevice, st));
+        if (!make_tmap_2d(h->tmW2o.bytes, h->w2o.p, D, (uint64_t)El * F, 64, 128) ||
+            !make_tmap_2d(h->tmW1o.bytes, h->w13o.p, kw, (uint64_t)El * D, 64, 128))
+            return fail(OCC_ERR_CUDA, "cuTensorMapEncodeTiled failed (backward weights)");
+    }
     if (!make_tmap_2d(h->tmB1.bytes, h->w13t.p, D, (uint64_t)El * h->n1rows, 64, 128) ||
         !make_tmap_2d(h->tmB2.bytes, h->w2t.p, F, (uint64_t)El * D, 64, 128))
         return fail(OCC_ERR_CUDA, "cuTensorMapEncodeTiled failed (weights)");
@@ -814,8 +882,13 @@ occ_status occ_forward(occ_handle* h, const void* x, const int32_t* ids, const f
                              reinterpret_cast<__nv_bfloat16*>(out), st);
     occ_status s = ensure_ws(h, n);
     if (s != OCC_OK) return s;
+    if (h->training) {
+        CUDA_TRY(h->save_a.ensure(h->Q_max * h->F));
+        if (h->gated) CUDA_TRY(h->save_b.ensure(h->Q_max * h->F));
+    }
     h->last_n = n;
     h->have_forward = true;
+    h->have_train_state = h->training && h->world == 1;
     if (n == 0) return OCC_OK;
     const int nd = h->nd, k = h->k, P = h->P, D = h->D, F = h->F, dedup = h->cfg.dedup;
     const int G = nd;
@@ -845,21 +918,16 @@ occ_status occ_forward(occ_handle* h, const void* x, const int32_t* ids, const f
     launch_compute_finalize(G, P, h->totals2.p, h->cofs, st);
     launch_init_epd((int)h->Q_max, h->epd_src.p, h->epd_w.p, st);
     EmitCompute ec{k, P, 0, h->in_ids.p, h->in_w.p, h->d_slot_of.p, h->d_dev_of.p, h->cofs, h->row_epd.p,
-                   h->epd_src.p, h->epd_w.p};
+                   h->epd_src.p, h->epd_w.p, h->epd_j.p};
     launch_rank_emit_compute(R_max, R_total, h->rgroup.p, h->rmask.p, G, P, ws, ec, st);
     // 4. gather + grouped GEMM-1 (activation / SwiGLU, routing weight fused)
     mark(h, ST_GATHER, st);
     launch_gather_rows((int)h->Q_max, h->d_q_total, h->epd_src.p, h->in_x.p, D, h->x_epd.p, st);
     mark(h, ST_GEMM1, st);
-    const int max_mb = (int)h->max_mblk;
-    GemmArgs g1{h->tmA1.bytes, h->tmB1.bytes, D, F, h->n1rows, h->cofs.grp_mb, h->d_widx.p, G * P, 1 << 20,
-                h->epd_w.p, h->hbuf.p, F, h->cfg.activation, max_mb * (h->gated ? F / 128 : (F + 255) / 256)};
-    launch_grouped_gemm(h->gated ? EPI_SWIGLU_BF16 : EPI_ACT_BF16, g1, h->num_sms, st);
+    launch_gemm1(h, G * P, st);
     mark(h, ST_GEMM2, st);
     // 5. grouped GEMM-2 (per-expert products, fp32)
-    GemmArgs g2{h->tmA2.bytes, h->tmB2.bytes, F, D, D, h->cofs.grp_mb, h->d_widx.p, G * P, 8, nullptr, h->ybuf.p,
-                D, 0, max_mb * ((D + 255) / 256)};
-    launch_grouped_gemm(EPI_F32, g2, h->num_sms, st);
+    launch_gemm2(h, G * P, st);
     // 6+7. intra-device partial combine (placement order) -> bf16 return
     // payload -> combine over devices ascending, fused on one GPU
     mark(h, ST_COMBINE, st);
@@ -886,6 +954,128 @@ occ_status occ_forward_expert_parallel(occ_handle* h, const void* x, const void*
     if (s == OCC_OK) s = occ_forward(h, x, ids, w, sources, n, out, stream);
     h->in_ep = 0;
     return s;
+}
+
+occ_status occ_set_training(occ_handle* h, int on) {
+    if (!h) return fail(OCC_ERR_ARG, "null handle");
+    if (on && h->world != 1) return fail(OCC_ERR_UNSUPPORTED, "backward: world_size 1 in this build");
+    h->training = on;
+    h->have_train_state = false;
+    return OCC_OK;
+}
+
+static occ_status ensure_bwd(occ_handle* h) {
+    const size_t Q = h->Q_max;
+    const int D = h->D, F = h->F, kw = h->gated ? 2 * F : F;
+    const int NBf = (F + 255) / 256;
+    CUDA_TRY(h->g_epd.ensure(Q * D));
+    CUDA_TRY(h->gpre.ensure(Q * kw));
+    CUDA_TRY(h->gw_part.ensure(Q * NBf));
+    if (h->bwd_tmaps_q != (int)Q) {
+        if (!make_tmap_2d(h->tmG_k.bytes, h->g_epd.p, D, Q, 64, 128) ||
+            !make_tmap_2d(h->tmP_k.bytes, h->gpre.p, kw, Q, 64, 128) ||
+            !make_tmap_2d(h->tmH_mn.bytes, h->hbuf.p, F, Q, 64, 64) ||
+            !make_tmap_2d(h->tmG_mn.bytes, h->g_epd.p, D, Q, 64, 64) ||
+            !make_tmap_2d(h->tmX_mn.bytes, h->x_epd.p, D, Q, 64, 64) ||
+            !make_tmap_2d(h->tmP_mn.bytes, h->gpre.p, kw, Q, 64, 64))
+            return fail(OCC_ERR_CUDA, "cuTensorMapEncodeTiled failed (backward)");
+        h->bwd_tmaps_q = (int)Q;
+    }
+    return OCC_OK;
+}
+
+occ_status occ_backward(occ_handle* h, const void* upstream, float* g_x, float* g_w1, float* g_w3, float* g_w2,
+                        float* g_weights, occ_stream_t stream) {
+    if (!h) return fail(OCC_ERR_ARG, "null handle");
+    if (!h->have_train_state) return fail(OCC_ERR_STATE, "backward: forward state was not saved (occ_set_training)");
+    const int n = h->last_n, k = h->k, P = h->P, D = h->D, F = h->F, nd = h->nd, E = h->E;
+    if (n > 0 && (!upstream || !g_x || !g_w1 || !g_w2 || !g_weights || (h->gated && !g_w3)))
+        return fail(OCC_ERR_ARG, "null argument");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int G = nd, NG = G * P, kw = h->gated ? 2 * F : F;
+    CUDA_TRY(cudaMemsetAsync(g_w1, 0, sizeof(float) * E * D * F, st));
+    CUDA_TRY(cudaMemsetAsync(g_w2, 0, sizeof(float) * E * F * D, st));
+    if (h->gated) CUDA_TRY(cudaMemsetAsync(g_w3, 0, sizeof(float) * E * D * F, st));
+    if (n == 0) return OCC_OK;
+    occ_status s = ensure_bwd(h);
+    if (s != OCC_OK) return s;
+    // combine + return adjoints: the token's upstream row on every Epd row
+    launch_gather_token_rows((int)h->Q_max, h->d_q_total, h->epd_src.p, h->in_tok.p,
+                             reinterpret_cast<const __nv_bfloat16*>(upstream), D, h->g_epd.p, st);
+    // merge adjoint (data): g_mod = g_y w2^T, with modulation + activation
+    // adjoints and the routing-weight partials fused in the epilogue
+    GemmArgs g;
+    g.tmap_a = h->tmG_k.bytes;
+    g.tmap_b = h->tmW2o.bytes;
+    g.K = D;
+    g.N = F;
+    g.b_rows_per_e = F;
+    g.grp_mb = h->cofs.grp_mb;
+    g.grp_w = h->d_widx.p;
+    g.ngroups = NG;
+    g.row_w = h->epd_w.p;
+    g.out = h->gpre.p;
+    g.ldo = kw;
+    g.act = h->cfg.activation;
+    g.pre_a = h->save_a.p;
+    g.pre_b = h->gated ? h->save_b.p : nullptr;
+    g.gw_part = h->gw_part.p;
+    g.max_tiles = (int)h->max_mblk * ((F + 255) / 256);
+    launch_grouped_gemm(h->gated ? EPI_BWD_SWIGLU : EPI_BWD_ACT, g, h->num_sms, st);
+    // scatter adjoint (data): g_x per Epd row = g_pre [w1 | w3]^T (fp32)
+    GemmArgs d1;
+    d1.tmap_a = h->tmP_k.bytes;
+    d1.tmap_b = h->tmW1o.bytes;
+    d1.K = kw;
+    d1.N = D;
+    d1.b_rows_per_e = D;
+    d1.grp_mb = h->cofs.grp_mb;
+    d1.grp_w = h->d_widx.p;
+    d1.ngroups = NG;
+    d1.band = 8;
+    d1.out = h->ybuf.p;
+    d1.ldo = D;
+    d1.max_tiles = (int)h->max_mblk * ((D + 255) / 256);
+    launch_grouped_gemm(EPI_F32, d1, h->num_sms, st);
+    // merge adjoint (weights): g_w2[e] = mod_e^T g_y_e (backward.cpp:84-93)
+    GemmArgs w2;
+    w2.tmap_a = h->tmH_mn.bytes;
+    w2.tmap_b = h->tmG_mn.bytes;
+    w2.N = D;
+    w2.M = F;
+    w2.grp_cnt = h->cofs.cnt;
+    w2.seg_base = h->cofs.seg_base;
+    w2.grp_w = h->d_widx.p;
+    w2.ngroups = NG;
+    w2.out = g_w2;
+    w2.ldo = D;
+    w2.out_estride = (long)F * D;
+    w2.max_tiles = NG * ((F + 255) / 256) * ((D + 255) / 256);
+    launch_grouped_gemm(EPI_WGRAD, w2, h->num_sms, st);
+    // scatter adjoint (weights): [g_w1 | g_w3][e] = x_e^T g_pre_e (backward.cpp:123-133)
+    GemmArgs w1;
+    w1.tmap_a = h->tmX_mn.bytes;
+    w1.tmap_b = h->tmP_mn.bytes;
+    w1.N = kw;
+    w1.M = D;
+    w1.grp_cnt = h->cofs.cnt;
+    w1.seg_base = h->cofs.seg_base;
+    w1.grp_w = h->d_widx.p;
+    w1.ngroups = NG;
+    w1.out = g_w1;
+    w1.out2 = h->gated ? g_w3 : nullptr;
+    w1.split = F;
+    w1.ldo = F;
+    w1.out_estride = (long)D * F;
+    w1.max_tiles = NG * ((D + 255) / 256) * ((kw + 255) / 256);
+    launch_grouped_gemm(EPI_WGRAD, w1, h->num_sms, st);
+    // dispatch adjoint: sum each token's rows (device ascending), fp32
+    launch_combine_grad(n, nd, k, P, h->cfg.dedup, D, h->mask.p, h->tok_row.p, h->row_epd.p, h->ybuf.p, g_x, st);
+    launch_gw_scatter((int)h->Q_max, h->d_q_total, (F + 255) / 256, h->gw_part.p, h->epd_src.p, h->in_tok.p,
+                      h->epd_j.p, k, g_weights, st);
+    CUDA_TRY(cudaGetLastError());
+    if (h->validate) CUDA_TRY(cudaStreamSynchronize(st));
+    return OCC_OK;
 }
 
 occ_status occ_set_profiling(occ_handle* h, int on) {

@@ -1,24 +1,34 @@
-// occ_gemm.cu — grouped per-expert GEMM on 5th-generation tensor cores
+// occ_gemm.cu — grouped per-expert GEMMs on 5th-generation tensor cores
 // (tcgen05.mma, accumulators in TMEM, operands staged by TMA).
 //
-// Replaces the reference's two indexed matmul loops, scatter_matmul
-// (pipeline.cpp:178-211, Alg. 6; fused here with apply_activation
-// :213-224 and weight_modulate :226-248, Alg. 7) and merge_matmul
-// (pipeline.cpp:250-283, Alg. 8).  Rows of every expert are contiguous and
-// padded to the 128-row M tile (compute-index segments, see
-// compute_finalize_kernel), so each tile belongs to exactly one expert and
-// the B operand is that expert's resident K-major weight slice.
+// Forward: replaces the reference's two indexed matmul loops,
+// scatter_matmul (pipeline.cpp:178-211, Alg. 6; fused here with
+// apply_activation :213-224 and weight_modulate :226-248, Alg. 7) and
+// merge_matmul (pipeline.cpp:250-283, Alg. 8).  Backward (backward.cpp:24-161):
+// the two data-gradient GEMMs (merge/scatter adjoints, pipeline.cpp:302-344)
+// with the modulation/activation adjoints fused in the epilogue, and the two
+// per-expert weight-gradient GEMMs.
+//
+// Rows of every expert are contiguous and padded to the 256-row pair tile
+// (compute-index segments), so each forward/data-gradient tile belongs to
+// exactly one expert and B is that expert's resident weight slice; a
+// weight-gradient tile reduces over exactly one expert's rows.
 //
 // Persistent, warp-specialised, CTA pairs (cluster 2x1x1, cta_group::2):
-// one 256x256 output tile per pair and K-step, each CTA staging its 128 A
-// rows and its half (128 rows) of the B tile, so per-SM operand traffic is
-// 32 KB per 64-deep K block (6 stages in 192 KB of shared memory).
+// one 256x256 output tile per pair, each CTA staging its 128 A rows and its
+// half (128 rows) of the B tile per 64-deep K block (32 KB per CTA, 6 stages
+// in 192 KB of shared memory, 128-byte swizzle).
 //   warp 0      TMA producer in both CTAs (completion on the leader's barrier)
 //   warp 1      TMEM allocator (both CTAs) + single-thread tcgen05.mma issuer
 //               in the leader CTA (M=256, N=256, K=16, fp32 accumulate)
-//   warps 2..5  epilogue in both CTAs: tcgen05.ld -> activation / SwiGLU /
-//               routing weight -> global stores; double-buffered TMEM
-//               accumulators (2 x 256 columns) overlap the next tile.
+//   warps 2..5  epilogue in both CTAs: tcgen05.ld -> fused epilogue ->
+//               global stores; double-buffered TMEM accumulators (2 x 256
+//               columns) overlap the epilogue with the next tile's MMAs.
+// Operand majorness: forward/data-gradient GEMMs read both operands K-major
+// ([rows, K] row-major, 64x128 TMA boxes); weight-gradient GEMMs reduce over
+// the token rows, so both operands are read MN-major straight from the same
+// row-major activation buffers (2 x 64x64 boxes, tcgen05 MN-major
+// descriptors) — no transposes.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -32,28 +42,48 @@ namespace {
 
 constexpr int BM = 128;               // rows per CTA (pair tile: 256)
 constexpr int BN = 256, BK = 64, STAGES = 6;
-constexpr int A_BYTES = BM * BK * 2;   // 16 KB
+constexpr int A_BYTES = BM * BK * 2;  // 16 KB
 constexpr int B_BYTES = (BN / 2) * BK * 2;  // 16 KB: this CTA's half of the B tile
 constexpr int SMEM_BYTES = STAGES * (A_BYTES + B_BYTES) + 256;
 constexpr int THREADS = 192;
 constexpr int MAX_GROUPS = 256;
-constexpr uint32_t IDESC = idesc_bf16_f32(2 * BM, BN);
 static_assert(kBM == 2 * BM, "Epd segments are padded to the pair tile");
+
+// K-major SW128 descriptors advance 32 B per K=16 step inside the swizzle
+// atom; MN-major SW128 tiles are two 64-column boxes (LBO = 8 KB apart) of
+// 8-row x 128 B atoms (SBO = 1 KB), advancing 16 rows = 2 KB per K step.
+OCC_DEV uint64_t sdesc_mn_sw128(uint32_t smem_addr) {
+    return (uint64_t)((smem_addr & 0x3FFFF) >> 4) | ((uint64_t)(8192 >> 4) << 16) | ((uint64_t)(1024 >> 4) << 32) |
+           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+__host__ __device__ constexpr uint32_t idesc_mn(int m, int n) {
+    return idesc_bf16_f32(m, n) | (1u << 15) | (1u << 16);  // A and B MN-major
+}
 
 struct Params {
     int K, N, b_rows_per_e, act;
-    const int* grp_mb;
+    const int* grp_mb;  // forward: m-tile prefix per group
     const int* grp_w;
     int ngroups, band;
+    const int* grp_cnt;   // wgrad: rows per group
+    const int* seg_base;  // wgrad: first padded row per group
+    int M;                // wgrad: output rows (the MN extent of A)
     const float* row_w;
     void* out;
     int ldo;
+    long out_estride;  // wgrad: elements per expert in out/out2
+    void* out2;
+    int split;
+    __nv_bfloat16* save_a;  // forward training: pre-activations
+    __nv_bfloat16* save_b;
+    const __nv_bfloat16* pre_a;  // backward epilogue inputs
+    const __nv_bfloat16* pre_b;
+    float* gw_part;
 };
 
-// Tile -> (m-block, n-block, weight slice).  Tiles are enumerated expert
-// group by expert group, and inside a group in bands of `band` m-blocks
-// walked n-block-major, so concurrently resident CTAs share B (weight)
-// n-blocks and a band's A rows stay in L2; no band straddles two experts.
+// Forward / data-gradient tiles: expert group by group, bands of `band`
+// m-tiles walked n-block-major (resident CTAs share B n-blocks, a band's A
+// rows stay in L2; no band straddles two experts).
 __device__ __forceinline__ void tile_coords(int tile, const int* gmb, const int* gw, int ng, int NB, int band,
                                             int& mb, int& nb, int& w) {
     int g = 0;
@@ -69,13 +99,56 @@ __device__ __forceinline__ void tile_coords(int tile, const int* gmb, const int*
     w = gw[g];
 }
 
+// Weight-gradient tiles: (group, m-tile, n-tile) over groups with rows.
+__device__ __forceinline__ void wtile_coords(int tile, const int* tb, int ng, int NB, int& g, int& mt, int& nt) {
+    g = 0;
+    while (g < ng - 1 && tb[g + 1] <= tile) ++g;
+    const int lt = tile - tb[g];
+    mt = lt / NB;
+    nt = lt - mt * NB;
+}
+
 __device__ __forceinline__ float act_f(float v, int act) {
     if (act == 1) return silu(v);
     if (act == 2) return v > 0.f ? v : 0.f;
     return v;
 }
+__device__ __forceinline__ float act_grad(float v, int act) {  // backward.cpp:11-20
+    if (act == 1) {
+        const float s = 1.0f / (1.0f + __expf(-v));
+        return s * (1.0f + v * (1.0f - s));
+    }
+    if (act == 2) return v > 0.f ? 1.f : 0.f;
+    return 1.f;
+}
 
-template <int EPI>
+__device__ __forceinline__ void load_bf16x32(const __nv_bfloat16* p, float (&f)[32]) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const uint4 w = *reinterpret_cast<const uint4*>(p + 8 * u);
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float2 x = __bfloat1622float2(h[q]);
+            f[8 * u + 2 * q] = x.x;
+            f[8 * u + 2 * q + 1] = x.y;
+        }
+    }
+}
+__device__ __forceinline__ void store_bf16x32(__nv_bfloat16* p, const float (&h)[32], int valid_cols) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+        if (u * 8 < valid_cols) {
+            uint4 o;
+            o.x = pack_bf16(h[8 * u + 0], h[8 * u + 1]);
+            o.y = pack_bf16(h[8 * u + 2], h[8 * u + 3]);
+            o.z = pack_bf16(h[8 * u + 4], h[8 * u + 5]);
+            o.w = pack_bf16(h[8 * u + 6], h[8 * u + 7]);
+            *reinterpret_cast<uint4*>(p + 8 * u) = o;
+        }
+}
+
+template <int EPI, bool WGRAD>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Params p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -87,13 +160,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-    __shared__ int s_gmb[MAX_GROUPS + 1];
+    __shared__ int s_gmb[MAX_GROUPS + 1];  // forward: m-tile prefix; wgrad: tile prefix
     __shared__ int s_gw[MAX_GROUPS];
-    for (int i = threadIdx.x; i <= p.ngroups; i += blockDim.x) s_gmb[i] = p.grp_mb[i];
-    for (int i = threadIdx.x; i < p.ngroups; i += blockDim.x) s_gw[i] = p.grp_w[i];
+    __shared__ int s_kb0[MAX_GROUPS];      // wgrad: first K block / K block count per group
+    __shared__ int s_kbn[MAX_GROUPS];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
+    const int NB = WGRAD ? (p.N + BN - 1) / BN : (EPI == EPI_SWIGLU_BF16 ? (p.N + 127) / 128 : (p.N + BN - 1) / BN);
+    const int MT = (p.M + 2 * BM - 1) / (2 * BM);  // wgrad m-tiles
+    if constexpr (WGRAD) {
+        if (threadIdx.x == 0) {
+            int run = 0;
+            for (int g = 0; g < p.ngroups; ++g) {
+                s_gmb[g] = run;
+                const int rows = p.grp_cnt[g];
+                s_kb0[g] = p.seg_base[g] / BK;
+                s_kbn[g] = (rows + BK - 1) / BK;
+                if (rows > 0) run += MT * NB;
+            }
+            s_gmb[p.ngroups] = run;
+        }
+        for (int i = threadIdx.x; i < p.ngroups; i += blockDim.x) s_gw[i] = p.grp_w[i];
+    } else {
+        for (int i = threadIdx.x; i <= p.ngroups; i += blockDim.x) s_gmb[i] = p.grp_mb[i];
+        for (int i = threadIdx.x; i < p.ngroups; i += blockDim.x) s_gw[i] = p.grp_w[i];
+    }
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
@@ -113,10 +205,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
-    const int MB = s_gmb[p.ngroups];  // pair tiles of 256 rows
-    const int NB = EPI == EPI_SWIGLU_BF16 ? (p.N + 127) / 128 : (p.N + BN - 1) / BN;
-    const int num_tiles = MB * NB;
-    const int KB = (p.K + BK - 1) / BK;
+    const int num_tiles = WGRAD ? s_gmb[p.ngroups] : s_gmb[p.ngroups] * NB;
+    const int KB_fwd = (p.K + BK - 1) / BK;
     const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
 
     if (warp == 0) {
@@ -125,16 +215,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = cid; tile < num_tiles; tile += ncl) {
-                int mb, nb, wi;
-                tile_coords(tile, s_gmb, s_gw, p.ngroups, NB, p.band, mb, nb, wi);
-                const int arow = mb * 2 * BM + rank * BM;
-                const int brow = wi * p.b_rows_per_e + nb * BN + rank * (BN / 2);
+                int kb0 = 0, KB = KB_fwd, ax = 0, ay = 0, bx = 0, by = 0;
+                if constexpr (WGRAD) {
+                    int g, mt, nt;
+                    wtile_coords(tile, s_gmb, p.ngroups, NB, g, mt, nt);
+                    kb0 = s_kb0[g];
+                    KB = s_kbn[g];
+                    ax = mt * 2 * BM + rank * BM;    // MN columns of A
+                    bx = nt * BN + rank * (BN / 2);  // MN columns of B
+                } else {
+                    int mb, nb, wi;
+                    tile_coords(tile, s_gmb, s_gw, p.ngroups, NB, p.band, mb, nb, wi);
+                    ay = mb * 2 * BM + rank * BM;
+                    by = wi * p.b_rows_per_e + nb * BN + rank * (BN / 2);
+                }
                 for (int kb = 0; kb < KB; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     const uint32_t lbar = smem_u32(&full[stage]) & kPeerBitMask;
                     if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * (A_BYTES + B_BYTES));
-                    tma_load_2d_cg2(sA + stage * A_BYTES, &tmA, lbar, kb * BK, arow);
-                    tma_load_2d_cg2(sB + stage * B_BYTES, &tmB, lbar, kb * BK, brow);
+                    uint8_t* a_dst = sA + stage * A_BYTES;
+                    uint8_t* b_dst = sB + stage * B_BYTES;
+                    if constexpr (WGRAD) {
+                        const int k = (kb0 + kb) * BK;  // token rows of this K block
+                        tma_load_2d_cg2(a_dst, &tmA, lbar, ax, k);
+                        tma_load_2d_cg2(a_dst + A_BYTES / 2, &tmA, lbar, ax + 64, k);
+                        tma_load_2d_cg2(b_dst, &tmB, lbar, bx, k);
+                        tma_load_2d_cg2(b_dst + B_BYTES / 2, &tmB, lbar, bx + 64, k);
+                    } else {
+                        tma_load_2d_cg2(a_dst, &tmA, lbar, kb * BK, ay);
+                        tma_load_2d_cg2(b_dst, &tmB, lbar, kb * BK, by);
+                    }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
@@ -142,11 +252,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     } else if (warp == 1) {
         // ------------------------------------------------ MMA issuer (leader CTA)
         if (rank == 0) {
+            constexpr uint32_t IDESC = WGRAD ? idesc_mn(2 * BM, BN) : idesc_bf16_f32(2 * BM, BN);
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
             for (int tile = cid; tile < num_tiles; tile += ncl) {
+                int KB = KB_fwd;
+                if constexpr (WGRAD) {
+                    int g, mt, nt;
+                    wtile_coords(tile, s_gmb, p.ngroups, NB, g, mt, nt);
+                    KB = s_kbn[g];
+                }
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
@@ -157,9 +274,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                         const uint32_t a0 = smem_u32(sA + stage * A_BYTES);
                         const uint32_t b0 = smem_u32(sB + stage * B_BYTES);
 #pragma unroll
-                        for (int k = 0; k < BK / 16; ++k)
-                            umma_bf16_cg2(d_tmem, sdesc_k_sw128(a0 + k * 32), sdesc_k_sw128(b0 + k * 32), IDESC,
-                                          (kb | k) != 0);
+                        for (int k = 0; k < BK / 16; ++k) {
+                            const uint64_t ad = WGRAD ? sdesc_mn_sw128(a0 + k * 2048) : sdesc_k_sw128(a0 + k * 32);
+                            const uint64_t bd = WGRAD ? sdesc_mn_sw128(b0 + k * 2048) : sdesc_k_sw128(b0 + k * 32);
+                            umma_bf16_cg2(d_tmem, ad, bd, IDESC, (kb | k) != 0);
+                        }
                         umma_commit_cg2_mc(&empty[stage]);
                     }
                     __syncwarp();
@@ -176,60 +295,139 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int tile = cid; tile < num_tiles; tile += ncl) {
-            int mb, nb, wi;
-            tile_coords(tile, s_gmb, s_gw, p.ngroups, NB, p.band, mb, nb, wi);
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
-            const long row = (long)mb * 2 * BM + rank * BM + q * 32 + lane;
             const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
-            if constexpr (EPI == EPI_F32) {
-                float* out = reinterpret_cast<float*>(p.out) + row * p.ldo;
+            if constexpr (WGRAD) {
+                // dW[e][m][n] = sum over the expert's rows; every tile is complete
+                int g, mt, nt;
+                wtile_coords(tile, s_gmb, p.ngroups, NB, g, mt, nt);
+                const int m = mt * 2 * BM + rank * BM + q * 32 + lane;
+                const long ebase = (long)s_gw[g] * p.out_estride;
 #pragma unroll 1
                 for (int c = 0; c < BN / 32; ++c) {
                     uint32_t v[32];
                     tmem_ld32(tbase + c * 32, v);
                     tmem_ld_wait();
-                    const int col0 = nb * BN + c * 32;
+                    const int col0 = nt * BN + c * 32;
+                    if (m >= p.M) continue;
+                    float* o = reinterpret_cast<float*>(p.out) + ebase + (long)m * p.ldo;
+                    int c0 = col0;
+                    if (p.out2 && col0 >= p.split) {
+                        o = reinterpret_cast<float*>(p.out2) + ebase + (long)m * p.ldo;
+                        c0 = col0 - p.split;
+                    }
 #pragma unroll
                     for (int u = 0; u < 8; ++u)
                         if (col0 + u * 4 < p.N)
-                            *reinterpret_cast<float4*>(out + col0 + u * 4) =
+                            *reinterpret_cast<float4*>(o + c0 + u * 4) =
                                 make_float4(__uint_as_float(v[4 * u]), __uint_as_float(v[4 * u + 1]),
                                             __uint_as_float(v[4 * u + 2]), __uint_as_float(v[4 * u + 3]));
                 }
             } else {
-                const float wr = p.row_w ? p.row_w[row] : 1.0f;
-                __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out) + row * p.ldo;
-                constexpr int NCH = EPI == EPI_SWIGLU_BF16 ? 4 : BN / 32;
-                const int ncol = EPI == EPI_SWIGLU_BF16 ? 128 : BN;
+                int mb, nb, wi;
+                tile_coords(tile, s_gmb, s_gw, p.ngroups, NB, p.band, mb, nb, wi);
+                const long row = (long)mb * 2 * BM + rank * BM + q * 32 + lane;
+                if constexpr (EPI == EPI_F32) {
+                    float* out = reinterpret_cast<float*>(p.out) + row * p.ldo;
 #pragma unroll 1
-                for (int c = 0; c < NCH; ++c) {
-                    uint32_t v[32];
-                    float h[32];
-                    tmem_ld32(tbase + c * 32, v);
-                    if constexpr (EPI == EPI_SWIGLU_BF16) {
-                        uint32_t g[32];
-                        tmem_ld32(tbase + 128 + c * 32, g);
+                    for (int c = 0; c < BN / 32; ++c) {
+                        uint32_t v[32];
+                        tmem_ld32(tbase + c * 32, v);
                         tmem_ld_wait();
+                        const int col0 = nb * BN + c * 32;
 #pragma unroll
-                        for (int i = 0; i < 32; ++i)
-                            h[i] = silu(__uint_as_float(v[i])) * __uint_as_float(g[i]) * wr;
-                    } else {
-                        tmem_ld_wait();
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) h[i] = act_f(__uint_as_float(v[i]), p.act) * wr;
+                        for (int u = 0; u < 8; ++u)
+                            if (col0 + u * 4 < p.N)
+                                *reinterpret_cast<float4*>(out + col0 + u * 4) =
+                                    make_float4(__uint_as_float(v[4 * u]), __uint_as_float(v[4 * u + 1]),
+                                                __uint_as_float(v[4 * u + 2]), __uint_as_float(v[4 * u + 3]));
                     }
-                    const int col0 = nb * ncol + c * 32;
+                } else if constexpr (EPI == EPI_BWD_ACT || EPI == EPI_BWD_SWIGLU) {
+                    // g_mod = g_y W2^T in TMEM; modulation + activation adjoints
+                    // (backward.cpp:95-118): routing-weight partial <act, g_mod>,
+                    // g_pre = g_mod * w * act'(pre)  (SwiGLU: g_a, g_b).
+                    const float wr = p.row_w[row];
+                    const int F = p.N;
+                    float gw = 0.f;
+                    __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out) + row * p.ldo;
+#pragma unroll 1
+                    for (int c = 0; c < BN / 32; ++c) {
+                        const int col0 = nb * BN + c * 32;
+                        uint32_t v[32];
+                        tmem_ld32(tbase + c * 32, v);
+                        tmem_ld_wait();
+                        if (col0 >= F) continue;
+                        const int nv = F - col0 < 32 ? F - col0 : 32;
+                        float a[32], r0[32];
+                        load_bf16x32(p.pre_a + row * F + col0, a);
+                        if constexpr (EPI == EPI_BWD_SWIGLU) {
+                            float b[32], r1[32];
+                            load_bf16x32(p.pre_b + row * F + col0, b);
 #pragma unroll
-                    for (int u = 0; u < 4; ++u)
-                        if (col0 + u * 8 < p.N) {
-                            uint4 o;
-                            o.x = pack_bf16(h[8 * u + 0], h[8 * u + 1]);
-                            o.y = pack_bf16(h[8 * u + 2], h[8 * u + 3]);
-                            o.z = pack_bf16(h[8 * u + 4], h[8 * u + 5]);
-                            o.w = pack_bf16(h[8 * u + 6], h[8 * u + 7]);
-                            *reinterpret_cast<uint4*>(out + col0 + u * 8) = o;
+                            for (int i = 0; i < 32; ++i) {
+                                const float gm = i < nv ? __uint_as_float(v[i]) : 0.f;
+                                const float s = 1.0f / (1.0f + __expf(-a[i]));
+                                const float sa = a[i] * s;
+                                gw += sa * b[i] * gm;
+                                const float gh = gm * wr;
+                                r0[i] = gh * b[i] * s * (1.0f + a[i] * (1.0f - s));
+                                r1[i] = gh * sa;
+                            }
+                            store_bf16x32(out + col0, r0, F - col0);
+                            store_bf16x32(out + F + col0, r1, F - col0);
+                        } else {
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) {
+                                const float gm = i < nv ? __uint_as_float(v[i]) : 0.f;
+                                gw += act_f(a[i], p.act) * gm;
+                                r0[i] = gm * wr * act_grad(a[i], p.act);
+                            }
+                            store_bf16x32(out + col0, r0, F - col0);
                         }
+                    }
+                    p.gw_part[row * NB + nb] = gw;
+                } else {
+                    const float wr = p.row_w ? p.row_w[row] : 1.0f;
+                    __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out) + row * p.ldo;
+                    constexpr int NCH = EPI == EPI_SWIGLU_BF16 ? 4 : BN / 32;
+                    const int ncol = EPI == EPI_SWIGLU_BF16 ? 128 : BN;
+#pragma unroll 1
+                    for (int c = 0; c < NCH; ++c) {
+                        uint32_t v[32];
+                        float h[32];
+                        const int col0 = nb * ncol + c * 32;
+                        tmem_ld32(tbase + c * 32, v);
+                        if constexpr (EPI == EPI_SWIGLU_BF16) {
+                            uint32_t g[32];
+                            tmem_ld32(tbase + 128 + c * 32, g);
+                            tmem_ld_wait();
+                            if (p.save_a && col0 < p.N) {  // training: keep a = x w1, b = x w3
+                                float fa[32], fb[32];
+#pragma unroll
+                                for (int i = 0; i < 32; ++i) {
+                                    fa[i] = __uint_as_float(v[i]);
+                                    fb[i] = __uint_as_float(g[i]);
+                                }
+                                store_bf16x32(p.save_a + row * p.N + col0, fa, p.N - col0);
+                                store_bf16x32(p.save_b + row * p.N + col0, fb, p.N - col0);
+                            }
+#pragma unroll
+                            for (int i = 0; i < 32; ++i)
+                                h[i] = silu(__uint_as_float(v[i])) * __uint_as_float(g[i]) * wr;
+                        } else {
+                            tmem_ld_wait();
+                            if (p.save_a && col0 < p.N) {  // training: keep the pre-activation
+                                float fa[32];
+#pragma unroll
+                                for (int i = 0; i < 32; ++i) fa[i] = __uint_as_float(v[i]);
+                                store_bf16x32(p.save_a + row * p.N + col0, fa, p.N - col0);
+                            }
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) h[i] = act_f(__uint_as_float(v[i]), p.act) * wr;
+                        }
+                        if (col0 < p.N) store_bf16x32(out + col0, h, p.N - col0);
+                    }
                 }
             }
             tc_fence_before();
@@ -262,6 +460,13 @@ EncodeTiledFn get_encode() {
     return fn;
 }
 
+template <int EPI, bool WGRAD>
+void launch_one(int grid, const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, cudaStream_t st) {
+    const int smem = SMEM_BYTES + 1024;
+    cudaFuncSetAttribute(grouped_gemm_kernel<EPI, WGRAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    grouped_gemm_kernel<EPI, WGRAD><<<grid, THREADS, smem, st>>>(ta, tb, p);
+}
+
 }  // namespace
 
 // Row-major bf16 matrix [outer, inner], 128-byte swizzled boxes of
@@ -280,27 +485,41 @@ bool make_tmap_2d(void* tmap, const void* base, uint64_t inner, uint64_t outer, 
 }
 
 void launch_grouped_gemm(EpiMode mode, const GemmArgs& a, int num_sms, cudaStream_t st) {
-    Params p{a.K, a.N, a.b_rows_per_e, a.act, a.grp_mb, a.grp_w, a.ngroups, a.band, a.row_w, a.out, a.ldo};
+    Params p{};
+    p.K = a.K;
+    p.N = a.N;
+    p.b_rows_per_e = a.b_rows_per_e;
+    p.act = a.act;
+    p.grp_mb = a.grp_mb;
+    p.grp_w = a.grp_w;
+    p.ngroups = a.ngroups;
+    p.band = a.band;
+    p.grp_cnt = a.grp_cnt;
+    p.seg_base = a.seg_base;
+    p.M = a.M;
+    p.row_w = a.row_w;
+    p.out = a.out;
+    p.ldo = a.ldo;
+    p.out_estride = a.out_estride;
+    p.out2 = a.out2;
+    p.split = a.split;
+    p.save_a = a.save_a;
+    p.save_b = a.save_b;
+    p.pre_a = a.pre_a;
+    p.pre_b = a.pre_b;
+    p.gw_part = a.gw_part;
     const CUtensorMap& ta = *reinterpret_cast<const CUtensorMap*>(a.tmap_a);
     const CUtensorMap& tb = *reinterpret_cast<const CUtensorMap*>(a.tmap_b);
     int grid = 2 * a.max_tiles < num_sms ? 2 * a.max_tiles : num_sms;
     grid &= ~1;  // CTA pairs
     if (grid <= 0) return;
-    const int smem = SMEM_BYTES + 1024;
     switch (mode) {
-        case EPI_ACT_BF16:
-            cudaFuncSetAttribute(grouped_gemm_kernel<EPI_ACT_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-            grouped_gemm_kernel<EPI_ACT_BF16><<<grid, THREADS, smem, st>>>(ta, tb, p);
-            break;
-        case EPI_SWIGLU_BF16:
-            cudaFuncSetAttribute(grouped_gemm_kernel<EPI_SWIGLU_BF16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 smem);
-            grouped_gemm_kernel<EPI_SWIGLU_BF16><<<grid, THREADS, smem, st>>>(ta, tb, p);
-            break;
-        case EPI_F32:
-            cudaFuncSetAttribute(grouped_gemm_kernel<EPI_F32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-            grouped_gemm_kernel<EPI_F32><<<grid, THREADS, smem, st>>>(ta, tb, p);
-            break;
+        case EPI_ACT_BF16: launch_one<EPI_ACT_BF16, false>(grid, ta, tb, p, st); break;
+        case EPI_SWIGLU_BF16: launch_one<EPI_SWIGLU_BF16, false>(grid, ta, tb, p, st); break;
+        case EPI_F32: launch_one<EPI_F32, false>(grid, ta, tb, p, st); break;
+        case EPI_BWD_ACT: launch_one<EPI_BWD_ACT, false>(grid, ta, tb, p, st); break;
+        case EPI_BWD_SWIGLU: launch_one<EPI_BWD_SWIGLU, false>(grid, ta, tb, p, st); break;
+        case EPI_WGRAD: launch_one<EPI_F32, true>(grid, ta, tb, p, st); break;
     }
     count_launch();
 }

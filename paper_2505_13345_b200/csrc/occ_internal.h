@@ -139,6 +139,7 @@ struct EmitCompute {
     int32_t* row_epd;     // [R*P] padded Epd row per (row, slot)
     int32_t* epd_src;     // [Q] inbox row feeding each padded Epd row
     float* epd_w;         // [Q] routing weight of each Epd row
+    int32_t* epd_j;       // [Q] routing slot (0..k-1) of each Epd row within its row's routing (nullable)
 };
 void launch_rank_emit_compute(int R_max, const int* R_total, const int32_t* group, const uint64_t* mask, int G,
                               int B, RankWs ws, const EmitCompute& e, cudaStream_t st);
@@ -163,6 +164,15 @@ void launch_combine_fused(int n, int nd, int k, int P, int dedup, int D, const u
 // Saved-index extraction (parity): unpadded BRIM1 per device, P x R_d.
 void launch_extract_cindex(int R_max, const int* R_total, int P, const int32_t* row_dev, const int* in_base,
                            const int32_t* row_epd, const ComputeOffsets& o, int32_t* cindex, cudaStream_t st);
+
+// Backward (world_size == 1): upstream rows gathered into the Epd layout,
+// the scatter-adjoint rows summed back onto tokens, routing-weight gradients.
+void launch_gather_token_rows(int Q_max, const int* q_total, const int32_t* epd_src, const int32_t* in_tok,
+                              const __nv_bfloat16* src, int D, __nv_bfloat16* dst, cudaStream_t st);
+void launch_combine_grad(int n, int nd, int k, int P, int dedup, int D, const uint64_t* mask, const int32_t* tok_row,
+                         const int32_t* row_epd, const float* Y, float* out, cudaStream_t st);
+void launch_gw_scatter(int Q_max, const int* q_total, int NB, const float* gw_part, const int32_t* epd_src,
+                       const int32_t* in_tok, const int32_t* epd_j, int k, float* g_weights, cudaStream_t st);
 
 // Collaboration histogram (K8).
 void launch_histogram(const int32_t* ids, int n, int k, int e, int64_t* counts, cudaStream_t st);
@@ -192,22 +202,40 @@ void launch_transpose_weights(const __nv_bfloat16* w, int E, int K, int N, __nv_
                               int interleave_half, cudaStream_t st);
 
 // Grouped GEMM on tcgen05 (occ_gemm.cu).
-enum EpiMode { EPI_ACT_BF16 = 0, EPI_SWIGLU_BF16 = 1, EPI_F32 = 2 };
+enum EpiMode {
+    EPI_ACT_BF16 = 0,    // forward GEMM-1: act(acc) * w -> bf16 (+ pre-activation when training)
+    EPI_SWIGLU_BF16 = 1, // forward GEMM-1: silu(a) * b * w -> bf16 (+ a, b when training)
+    EPI_F32 = 2,         // plain fp32 output (GEMM-2, data gradient of the scatter)
+    EPI_BWD_ACT = 3,     // data gradient of the merge + modulation/activation adjoints
+    EPI_BWD_SWIGLU = 4,  // same for SwiGLU: g_a | g_b
+    EPI_WGRAD = 5        // per-expert weight gradient (MN-major operands, K = the expert's rows)
+};
 struct GemmArgs {
-    const void* tmap_a;       // CUtensorMap* (host object, passed by value to the kernel)
-    const void* tmap_b;
-    int K;                    // reduction dim
-    int N;                    // output columns per expert (GEMM-1 SwiGLU: F; B rows per expert = 2F)
-    int b_rows_per_e;         // rows of B per expert in the stacked K-major weight matrix
-    const int* grp_mb;        // device [ngroups+1]: m-block prefix per expert group
-    const int* grp_w;         // device [ngroups]: weight index of each group
-    int ngroups;
-    int band;                 // m-blocks per raster band inside a group
-    const float* row_w;       // per padded Epd row routing weight (EPI_ACT/SWIGLU), null = 1
-    void* out;                // [Q, N] bf16 or f32
-    int ldo;                  // output row stride (elements)
-    int act;                  // occ_activation for EPI_ACT_BF16
-    int max_tiles;            // static upper bound (grid sizing)
+    const void* tmap_a = nullptr;  // CUtensorMap* (host object, passed by value to the kernel)
+    const void* tmap_b = nullptr;
+    int K = 0;                     // reduction dim (forward / data gradient)
+    int N = 0;                     // output columns per expert (GEMM-1 SwiGLU: F; B rows per expert = 2F)
+    int b_rows_per_e = 0;          // rows of B per expert in the stacked K-major weight matrix
+    const int* grp_mb = nullptr;   // device [ngroups+1]: pair-tile prefix per expert group
+    const int* grp_w = nullptr;    // device [ngroups]: weight index of each group
+    int ngroups = 0;
+    int band = 1 << 20;            // pair tiles per raster band inside a group
+    const int* grp_cnt = nullptr;  // wgrad: rows per group
+    const int* seg_base = nullptr; // wgrad: first padded row per group
+    int M = 0;                     // wgrad: output rows
+    const float* row_w = nullptr;  // per padded Epd row routing weight, null = 1
+    void* out = nullptr;           // [Q, N] bf16 / f32, or wgrad [E, M, ldo] f32
+    int ldo = 0;                   // output row stride (elements)
+    long out_estride = 0;          // wgrad: elements per expert
+    void* out2 = nullptr;          // wgrad: columns >= split go here (SwiGLU w3 gradient)
+    int split = 1 << 30;
+    int act = 0;                   // occ_activation
+    __nv_bfloat16* save_a = nullptr;  // forward training outputs
+    __nv_bfloat16* save_b = nullptr;
+    const __nv_bfloat16* pre_a = nullptr;  // backward epilogue inputs
+    const __nv_bfloat16* pre_b = nullptr;
+    float* gw_part = nullptr;      // backward: routing-weight gradient partial per (row, n-tile)
+    int max_tiles = 0;             // static upper bound (grid sizing)
 };
 void launch_grouped_gemm(EpiMode mode, const GemmArgs& a, int num_sms, cudaStream_t st);
 bool make_tmap_2d(void* tmap, const void* base, uint64_t inner, uint64_t outer, uint32_t box_inner,

@@ -378,15 +378,18 @@ struct ComputeEmitter {
         e.row_epd[(long)r * e.P + p] = q;
         e.epd_src[q] = r;
         float wt = 0.0f;
+        int jj = -1;
         const int gdev = e.dev_base + g;
         for (int j = 0; j < e.k; ++j) {
             const int ex = e.row_ids[(long)r * e.k + j];
             if (ex >= 0 && e.dev_of[ex] == gdev && e.slot_of[ex] == p) {
                 wt = e.row_w[(long)r * e.k + j];
+                jj = j;
                 break;
             }
         }
         e.epd_w[q] = wt;
+        if (e.epd_j) e.epd_j[q] = jj;
     }
     __device__ void miss(int r, int p) { e.row_epd[(long)r * e.P + p] = -1; }
 };
@@ -571,6 +574,81 @@ __global__ void extract_cindex_kernel(int R_max, const int* R_total, int P, cons
     const int v = q < 0 ? -1 : q - o.seg_base[g] + o.unp_base[g];
     // per device: P x R_d block, blocks concatenated in device order
     cindex[(long)base * P + (long)p * Rd + (r - base)] = v;
+}
+
+// -------------------------------------------------------------- backward --
+// Combine adjoint + return adjoint (backward.cpp:43-78): every Epd row of a
+// token receives the token's upstream row.
+__global__ void __launch_bounds__(256) gather_token_rows_kernel(int Q_max, const int* q_total, const int32_t* epd_src,
+                                                                const int32_t* in_tok, const __nv_bfloat16* src,
+                                                                int D, __nv_bfloat16* dst) {
+    const int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (q >= *q_total) return;
+    const int r = epd_src[q];
+    const int nvec = D / 8;
+    uint4* out = reinterpret_cast<uint4*>(dst + (long)q * D);
+    if (r < 0) {
+        for (int v = lane; v < nvec; v += 32) out[v] = make_uint4(0, 0, 0, 0);
+        return;
+    }
+    const uint4* in = reinterpret_cast<const uint4*>(src + (long)in_tok[r] * D);
+    for (int v = lane; v < nvec; v += 32) out[v] = __ldg(in + v);
+}
+
+// Scatter adjoint summed per device then over devices (backward.cpp:136-152):
+// g_x[t] = sum over the token's k Epd rows, device ascending, placement
+// order inside a device; fp32 throughout.
+__global__ void __launch_bounds__(256) combine_grad_kernel(int n, int nd, int k, int P, int dedup, int D,
+                                                           const uint64_t* mask, const int32_t* tok_row,
+                                                           const int32_t* row_epd, const float* Y, float* out) {
+    const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (t >= n) return;
+    int qs[kMaxTopK];
+    int nq = 0;
+    if (dedup) {
+        uint64_t m = mask[t];
+        while (m) {
+            const int d = __ffsll(m) - 1;
+            m &= m - 1;
+            const int r = tok_row[(long)t * nd + d];
+            for (int p = 0; p < P && nq < kMaxTopK; ++p) {
+                const int q = row_epd[(long)r * P + p];
+                if (q >= 0) qs[nq++] = q;
+            }
+        }
+    } else {
+        for (int j = 0; j < k; ++j) {
+            const int r = tok_row[(long)t * k + j];
+            for (int p = 0; p < P; ++p) {
+                const int q = row_epd[(long)r * P + p];
+                if (q >= 0) qs[nq++] = q;
+            }
+        }
+    }
+    const int nv = D / 4;
+    for (int v = lane; v < nv; v += 32) {
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int i = 0; i < nq; ++i) {
+            const float4 y = __ldg(reinterpret_cast<const float4*>(Y + (long)qs[i] * D) + v);
+            acc.x += y.x; acc.y += y.y; acc.z += y.z; acc.w += y.w;
+        }
+        reinterpret_cast<float4*>(out + (long)t * D)[v] = acc;
+    }
+}
+
+// Routing-weight gradients (backward.cpp:97-111): reduce the per-n-tile
+// partials of each Epd row in order and write them to (token, slot).
+__global__ void gw_scatter_kernel(int Q_max, const int* q_total, int NB, const float* gw_part, const int32_t* epd_src,
+                                  const int32_t* in_tok, const int32_t* epd_j, int k, float* g_weights) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= *q_total) return;
+    const int r = epd_src[q];
+    if (r < 0) return;
+    float s = 0.f;
+    for (int b = 0; b < NB; ++b) s += gw_part[(long)q * NB + b];
+    g_weights[(long)in_tok[r] * k + epd_j[q]] = s;
 }
 
 // ------------------------------------------------------------- histogram --
@@ -1077,6 +1155,28 @@ void launch_combine_fused(int n, int nd, int k, int P, int dedup, int D, const u
                           cudaStream_t st) {
     if (!n) return;
     combine_fused_kernel<<<(n + 7) / 8, 256, 0, st>>>(n, nd, k, P, dedup, D, mask, tok_row, row_epd, Y, out);
+    count_launch();
+}
+
+void launch_gather_token_rows(int Q_max, const int* q_total, const int32_t* epd_src, const int32_t* in_tok,
+                              const __nv_bfloat16* src, int D, __nv_bfloat16* dst, cudaStream_t st) {
+    if (!Q_max) return;
+    gather_token_rows_kernel<<<(Q_max + 7) / 8, 256, 0, st>>>(Q_max, q_total, epd_src, in_tok, src, D, dst);
+    count_launch();
+}
+
+void launch_combine_grad(int n, int nd, int k, int P, int dedup, int D, const uint64_t* mask, const int32_t* tok_row,
+                         const int32_t* row_epd, const float* Y, float* out, cudaStream_t st) {
+    if (!n) return;
+    combine_grad_kernel<<<(n + 7) / 8, 256, 0, st>>>(n, nd, k, P, dedup, D, mask, tok_row, row_epd, Y, out);
+    count_launch();
+}
+
+void launch_gw_scatter(int Q_max, const int* q_total, int NB, const float* gw_part, const int32_t* epd_src,
+                       const int32_t* in_tok, const int32_t* epd_j, int k, float* g_weights, cudaStream_t st) {
+    if (!Q_max) return;
+    gw_scatter_kernel<<<(Q_max + 255) / 256, 256, 0, st>>>(Q_max, q_total, NB, gw_part, epd_src, in_tok, epd_j, k,
+                                                           g_weights);
     count_launch();
 }
 

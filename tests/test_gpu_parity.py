@@ -477,3 +477,74 @@ def test_multi_rank_forward_loopback(nd, ne, k, act, dedup):
     if dedup:
         assert r0.cross_device_bytes == rep.cross_device_bytes
         assert r0.per_device_token_counts == [rep.per_device_rows[d] for d in range(nd)]
+
+
+# ------------------------------------------------------------------ backward --
+
+BWD_CASES = [(8, 2, 2, 64, 128, "silu", 200), (8, 3, 4, 128, 256, "identity", 300), (16, 4, 4, 64, 320, "relu", 150),
+             (8, 2, 1, 256, 512, "silu", 513)]
+
+
+@pytest.mark.parametrize("ne,k,nd,dm,dh,act,n", BWD_CASES)
+def test_backward_matches_reference(ne, k, nd, dm, dh, act, n):
+    """backward_vjps (backward.cpp:24-161) of the reference on identical
+    bf16-representable inputs: every gradient block within 2e-2 normwise."""
+    x, g, w1, w2, _ = make_layer_inputs(ne + n, n, dm, dh, ne)
+    ids, w = random_routing(n, ne, k, np.random.default_rng(n))
+    w = w.astype(np.float32).astype(np.float64)
+    plist = _placement(ne, nd, "shuffled", seed=3)
+    src = (np.arange(n) % nd).astype(np.int32)
+    up = bf16_round(np.random.default_rng(1).uniform(-1, 1, (n, dm)))
+    rgx, rgw1, rgw2, rgr = O.ref_backward(x, ids, w, w1, w2, plist, src, up, act=act)
+    layer = occ.ExpertParallelLayer(occ.MoEConfig(ne, k, nd, dm, dh, activation=act),
+                                    occ.Placement([list(p) for p in plist]))
+    layer.set_training(True)
+    layer.load_experts(cuda(w1, torch.bfloat16), cuda(w2, torch.bfloat16))
+    layer.forward_given_routing(cuda(x, torch.bfloat16), cuda(ids), cuda(w, torch.float32), cuda(src))
+    gr = layer.backward(cuda(up, torch.bfloat16))
+    errs = {"x": rel_err(gr["x"].cpu().numpy(), rgx), "w1": rel_err(gr["w1"].cpu().numpy(), rgw1),
+            "w2": rel_err(gr["w2"].cpu().numpy(), rgw2),
+            "routing": rel_err(gr["routing_weights"].cpu().numpy(), rgr)}
+    assert max(errs.values()) <= 2e-2, errs
+
+
+def test_backward_swiglu_matches_autograd():
+    """SwiGLU extension: against torch autograd in fp64 on the CPU."""
+    ne, k, nd, dm, dh, n = 8, 2, 2, 128, 256, 300
+    x, g, w1, w2, w3 = make_layer_inputs(11, n, dm, dh, ne, gated=True)
+    ids, w = random_routing(n, ne, k, np.random.default_rng(5))
+    w = w.astype(np.float32).astype(np.float64)
+    up = bf16_round(np.random.default_rng(2).uniform(-1, 1, (n, dm)))
+    T = lambda a: torch.tensor(a, dtype=torch.float64, requires_grad=True)
+    tx, tw1, tw2, tw3, tw = T(x), T(w1), T(w2), T(w3), T(w)
+    out = torch.zeros(n, dm, dtype=torch.float64)
+    for j in range(k):
+        e = torch.from_numpy(ids[:, j]).long()
+        a = torch.einsum("nd,ndf->nf", tx, tw1[e])
+        b = torch.einsum("nd,ndf->nf", tx, tw3[e])
+        out = out + tw[:, j:j + 1] * torch.einsum("nf,nfd->nd", torch.nn.functional.silu(a) * b, tw2[e])
+    (out * torch.from_numpy(up)).sum().backward()
+    layer = occ.ExpertParallelLayer(occ.MoEConfig(ne, k, nd, dm, dh, activation="swiglu"))
+    layer.set_training(True)
+    layer.load_experts(cuda(w1, torch.bfloat16), cuda(w2, torch.bfloat16), cuda(w3, torch.bfloat16))
+    y = layer.forward_given_routing(cuda(x, torch.bfloat16), cuda(ids), cuda(w, torch.float32))
+    assert rel_err(y.double().cpu().numpy(), out.detach().numpy()) <= TOL
+    gr = layer.backward(cuda(up, torch.bfloat16))
+    errs = {name: rel_err(gr[name].cpu().numpy(), ref_t.grad.numpy())
+            for name, ref_t in (("x", tx), ("w1", tw1), ("w3", tw3), ("w2", tw2), ("routing_weights", tw))}
+    assert max(errs.values()) <= 2e-2, errs
+
+
+def test_backward_zero_upstream_and_state_error():
+    ne, k, nd, dm, dh, n = 8, 2, 2, 64, 128, 64
+    x, g, w1, w2, _ = make_layer_inputs(3, n, dm, dh, ne)
+    ids, w = random_routing(n, ne, k, np.random.default_rng(0))
+    layer = occ.ExpertParallelLayer(occ.MoEConfig(ne, k, nd, dm, dh, activation="silu"))
+    with pytest.raises(occ.StateError):  # backward.cpp:25 / test_pipeline.cpp:533-536
+        layer.backward(torch.zeros(n, dm, device="cuda"))
+    layer.set_training(True)
+    layer.load_experts(cuda(w1, torch.bfloat16), cuda(w2, torch.bfloat16))
+    layer.forward_given_routing(cuda(x, torch.bfloat16), cuda(ids), cuda(w, torch.float32))
+    gr = layer.backward(torch.zeros(n, dm, device="cuda"))
+    for name in ("x", "w1", "w2", "routing_weights"):
+        assert not gr[name].any(), name
