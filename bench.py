@@ -28,9 +28,38 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "MoE layer tokens/s at 1/2/4/8 B200; all-to-all bytes/token vs naive top-k"
-E, K_TOP, D, F = 8, 2, 4096, 14336
-TOKENS = 16384
-WORKLOAD = "Mixtral-8x7B MoE layer (8 experts top-2, d=4096, ffn=14336, SwiGLU) prefill 16384 tokens, EP=#GPUs"
+# BASELINE.json configs.  The driver's bench line is "mixtral" (configs[1]);
+# the others are selectable with --workload for the record (profiles/).
+WORKLOADS = {
+    "mixtral": dict(E=8, k=2, D=4096, F=14336, act="swiglu", tokens=16384, nd_sim=1, plan_ep=8, train=False,
+                    prune=None, name="Mixtral-8x7B MoE layer (8 experts top-2, d=4096, ffn=14336, SwiGLU) "
+                                     "prefill 16384 tokens, EP=#GPUs"),
+    "c1": dict(E=8, k=2, D=512, F=1024, act="silu", tokens=2048, nd_sim=2, plan_ep=2, train=False, prune=None,
+               name="single MoE layer, 8 experts top-2, d=512, d_ff=1024, 2048 tokens, 2 simulated EP ranks "
+                    "(reference CPU oracle shape; 2-matrix SiLU experts)"),
+    "deepseek": dict(E=64, k=6, D=2048, F=1408, act="swiglu", tokens=16384, nd_sim=1, plan_ep=8, train=False,
+                     prune=None, name="DeepSeek-MoE-16B layer (64 routed experts top-6, d=2048, ffn=1408, SwiGLU; "
+                                      "the 2 shared experts are not included) 16384 tokens"),
+    "olmoe": dict(E=64, k=8, D=2048, F=1024, act="swiglu", tokens=65536, nd_sim=1, plan_ep=8, train=True,
+                  prune=None, name="OLMoE-1B-7B layer (64 experts top-8, d=2048, ffn=1024, SwiGLU) "
+                                   "forward+backward at 65536 tokens/step"),
+    "qwen": dict(E=60, k=4, D=2048, F=1408, act="swiglu", tokens=16384, nd_sim=4, plan_ep=4, train=False,
+                 prune=("router", 2), name="Qwen1.5-MoE-A2.7B layer (60 routed experts top-4, d=2048, ffn=1408, "
+                                           "SwiGLU; shared expert not included) with collaboration pruning to <=2 "
+                                           "devices/token, EP=4 simulated on one GPU"),
+}
+W = WORKLOADS["mixtral"]
+E, K_TOP, D, F = W["E"], W["k"], W["D"], W["F"]
+TOKENS = W["tokens"]
+WORKLOAD = W["name"]
+
+
+def select_workload(name):
+    global W, E, K_TOP, D, F, TOKENS, WORKLOAD
+    W = WORKLOADS[name]
+    E, K_TOP, D, F = W["E"], W["k"], W["D"], W["F"]
+    TOKENS = W["tokens"]
+    WORKLOAD = W["name"]
 
 
 def load_peaks():
@@ -220,13 +249,19 @@ def run_ours(args):
     n_local = args.tokens // world
     torch.manual_seed(1234 + rank)
 
-    cfg = occ.MoEConfig(E, K_TOP, world, D, F, activation="swiglu")
+    nd = W["nd_sim"] if world == 1 else world
+    gated = W["act"] == "swiglu"
+    cfg = occ.MoEConfig(E, K_TOP, nd, D, F, activation=W["act"])
     layer = occ.ExpertParallelLayer(cfg, world_size=world, rank=rank)
     if world > 1:
         layer.comm_init()
+    if W["train"]:
+        layer.set_training(True)
+    prune = occ.PruneSpec(W["prune"][0], W["prune"][1]) if W["prune"] else None
     e_local = E if world == 1 else E // world
     w1 = torch.empty((e_local, D, F), dtype=torch.bfloat16, device=dev).uniform_(-1, 1).mul_(D ** -0.5)
-    w3 = torch.empty((e_local, D, F), dtype=torch.bfloat16, device=dev).uniform_(-1, 1).mul_(D ** -0.5)
+    w3 = torch.empty((e_local, D, F), dtype=torch.bfloat16, device=dev).uniform_(-1, 1).mul_(D ** -0.5) \
+        if gated else None
     w2 = torch.empty((e_local, F, D), dtype=torch.bfloat16, device=dev).uniform_(-1, 1).mul_(F ** -0.5)
     layer.load_experts(w1, w2, w3)
     del w1, w2, w3
@@ -244,8 +279,12 @@ def run_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    upstream = torch.empty_like(x).uniform_(-1, 1) if W["train"] else None
+
     def step():
-        layer.forward_expert_parallel(x, gate, out=out)
+        layer.forward_expert_parallel(x, gate, prune=prune, out=out)
+        if W["train"]:
+            layer.backward(upstream)
 
     for _ in range(args.warmup):
         flush.zero_()
@@ -277,10 +316,19 @@ def run_ours(args):
     xh = torch.empty_like(x, device="cpu").pin_memory()
     xh.copy_(x)
     oh = torch.empty_like(xh).pin_memory()
+    uh = upstream.cpu().pin_memory() if W["train"] else None
+    gxh = torch.empty((x.shape[0], D), dtype=torch.float32).pin_memory() if W["train"] else None
+
     def e2e_step():
+        if W["train"]:  # H2D tokens + upstream, forward + backward, D2H token gradient
+            x.copy_(xh, non_blocking=True)
+            upstream.copy_(uh, non_blocking=True)
+            layer.forward_expert_parallel(x, gate, prune=prune, out=out)
+            gxh.copy_(layer.backward(upstream)["x"], non_blocking=True)
+            return
         # public API, host buffers: this step's H2D copy and the previous
         # step's D2H copy overlap the layer (double-buffered staging)
-        layer.forward_host(xh, gate, oh, chunks=args.e2e_chunks, wait=False)
+        layer.forward_host(xh, gate, oh, prune=prune, chunks=args.e2e_chunks, wait=False)
 
     for _ in range(3):
         e2e_step()
@@ -300,7 +348,8 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
     e2e = {"value": args.tokens * args.steps / (e2e_ms / 1e3), "unit": "tokens/s",
-           "h2d_bytes_per_step": x.numel() * x.element_size(), "d2h_bytes_per_step": out.numel() * out.element_size(),
+           "h2d_bytes_per_step": x.numel() * x.element_size() * (2 if W["train"] else 1),
+           "d2h_bytes_per_step": out.numel() * (4 if W["train"] else out.element_size()),
            "ms_per_step": e2e_ms / args.steps,
            "api": f"ExpertParallelLayer.forward_host (occ_forward_host: pinned host buffers, double-buffered so "
                   f"H2D of step i+1 and D2H of step i-1 overlap the layer of step i; {args.e2e_chunks} chunk(s)); "
@@ -318,8 +367,9 @@ def run_ours(args):
     stages = {kk: statistics.mean(v) for kk, v in acc.items()}
     rep = layer.comm_report(bytes_per_scalar=2)
     n_epd = rep.n_epd
-    flops1 = 2.0 * n_epd * D * (2 * F)
+    flops1 = 2.0 * n_epd * D * ((2 if gated else 1) * F)
     flops2 = 2.0 * n_epd * F * D
+    train_flops = 2.0 * (flops1 + flops2) if W["train"] else 0.0
     tflops1 = flops1 / (stages["gemm1"] / 1e3) / 1e12
     tflops2 = flops2 / (stages["gemm2"] / 1e3) / 1e12
     # burst peak (cuBLAS timed alone): our timed loop is ~0.1 s, far shorter than
@@ -338,19 +388,25 @@ def run_ours(args):
                 "flops_per_launch": flops1, "launch_ms": stages["gemm1"],
                 "gemm2": {"achieved": tflops2, "frac": tflops2 / peak, "launch_ms": stages["gemm2"]},
                 "layer_frac": (flops1 + flops2) / (sum(stages.values()) / 1e3) / 1e12 / peak}
+    if W["train"]:
+        roofline["step_tflops_fwd_bwd"] = (flops1 + flops2 + train_flops) / (tot_ms / args.steps / 1e3) / 1e12
 
     # --- all-to-all bytes/token: dedup vs naive top-k at the config's EP=8 ---
-    ids, w = layer.route(x, gate)
-    plan8 = occ.ExpertParallelLayer(occ.MoEConfig(E, K_TOP, 8, D, F, activation="swiglu"))
-    plan8.build_dispatch_index(ids)
-    r8 = plan8.comm_report(bytes_per_scalar=2)
-    a2a = {"ep": 8, "payload": "bf16", "dedup_bytes_per_token": r8.crossing_rows * D * 2 / n_local,
+    ep = W["plan_ep"]
+    plan = occ.ExpertParallelLayer(occ.MoEConfig(E, K_TOP, ep, D, F, activation=W["act"]))
+    ids, w = plan.route(x, gate, prune=prune)
+    plan.build_dispatch_index(ids)
+    r8 = plan.comm_report(bytes_per_scalar=2)
+    a2a = {"ep": ep, "payload": "bf16", "dedup_bytes_per_token": r8.crossing_rows * D * 2 / n_local,
            "naive_bytes_per_token": r8.naive_crossing_rows * D * 2 / n_local,
            "ratio": (r8.crossing_rows / r8.naive_crossing_rows) if r8.naive_crossing_rows else None,
-           "mean_replicas": r8.mean_replicas, "note": "Mixtral at EP=8 hosts one expert per GPU: dedup == naive"}
+           "mean_replicas": r8.mean_replicas, "intra_share": r8.intra_share,
+           "pruning": W["prune"],
+           "note": ("Mixtral at EP=8 hosts one expert per GPU: dedup == naive" if E == 8 and ep == 8 else
+                    "round-robin sources over the EP ranks; naive = one row per (token, expert)")}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.workload == "mixtral":
         try:
             cpu = cpu_port_baseline(args.cpu_seconds)
         except Exception as exc:  # report, never fake
@@ -361,11 +417,14 @@ def run_ours(args):
         line = {"metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
-                "data": "synthetic (uniform tokens, random-init experts and gate of the Mixtral layer shape)",
+                "data": "synthetic (uniform tokens, random-init experts and gate of the named layer shape)",
                 "config": {"workload": WORKLOAD, "experts": E, "top_k": K_TOP, "d_model": D, "d_ff": F,
-                           "ffn": "SwiGLU", "tokens_per_step": args.tokens, "ep": world,
-                           "l2": "flushed between steps (512 MiB write); weights 2.8 GB >> L2",
-                           "step": "route + plan + pack + grouped GEMM-1/2 + partial combine + combine"},
+                           "ffn": "SwiGLU" if gated else W["act"], "tokens_per_step": args.tokens, "ep": world,
+                           "ep_simulated_on_one_gpu": nd if world == 1 else None,
+                           "l2": "flushed between steps (512 MiB write)",
+                           "step": ("route + plan + pack + grouped GEMM-1/2 + partial combine + combine"
+                                    + (" + backward (dgrad x2, wgrad x2, routing-weight grads)" if W["train"]
+                                       else ""))},
                 "e2e": e2e, "gpu_launches": launches, "clocks": clk, "roofline": roofline,
                 "stages_ms": stages, "a2a": a2a, "cpu_baseline": cpu,
                 "comm_report": {"mean_replicas": rep.mean_replicas, "n_sfd": rep.n_sfd, "n_epd": rep.n_epd}}
@@ -381,12 +440,16 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--tokens", type=int, default=TOKENS)
+    ap.add_argument("--workload", default="mixtral", choices=sorted(WORKLOADS))
+    ap.add_argument("--tokens", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-chunks", type=int, default=1)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-tokens-per-thread", type=int, default=2)
     args = ap.parse_args()
+    select_workload(args.workload)
+    if args.tokens is None:
+        args.tokens = TOKENS
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
