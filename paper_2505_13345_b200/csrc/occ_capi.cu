@@ -132,14 +132,14 @@ struct occ_handle {
     DevBuf<long long> stats;
     DevBuf<int32_t> err;
     DevBuf<int32_t> tok_row, tok_sfd, lam;
-    DevBuf<__nv_bfloat16> in_x, x_epd, hbuf, ret;
+    DevBuf<__nv_bfloat16> in_x, x_epd, hbuf, ret, y16;
     DevBuf<int32_t> in_ids, in_tok, in_src, in_slot, in_dev, row_epd, epd_src, epd_j;
     DevBuf<float> in_w, epd_w, ybuf, logits, rt_w;
     DevBuf<int32_t> rt_ids;  // routing of occ_forward_expert_parallel
     size_t R_max = 0, Q_max = 0, max_mblk = 0;
     int last_n = 0;
     bool have_forward = false;
-    TmapBox tmA1, tmA2, tmB1, tmB2;
+    TmapBox tmA1, tmA2, tmB1, tmB2, tmRX, tmRG;
     DispatchOffsets dofs{};
     ComputeOffsets cofs{};
     int* d_tok_base = nullptr;
@@ -346,7 +346,8 @@ occ_status ensure_recv(occ_handle* h, size_t R, size_t epd_bound) {
         CUDA_TRY(h->epd_w.ensure(Q));
         CUDA_TRY(h->x_epd.ensure(Q * D));
         CUDA_TRY(h->hbuf.ensure(Q * F));
-        CUDA_TRY(h->ybuf.ensure(Q * D));
+        CUDA_TRY(h->y16.ensure(Q * D));
+        if (h->training) CUDA_TRY(h->ybuf.ensure(Q * D));
         h->Q_max = Q;
         h->max_mblk = Q / kBM;
         h->bwd_tmaps_q = -1;
@@ -454,10 +455,11 @@ void launch_gemm2(occ_handle* h, int ngroups, cudaStream_t st) {
     g.grp_w = h->d_widx.p;
     g.ngroups = ngroups;
     g.band = 8;
-    g.out = h->ybuf.p;
+    g.out = h->y16.p;  // per-expert products in bf16 (halves the store + combine traffic)
     g.ldo = h->D;
+    g.act = OCC_ACT_IDENTITY;
     g.max_tiles = (int)h->max_mblk * ((h->D + 255) / 256);
-    launch_grouped_gemm(EPI_F32, g, h->num_sms, st);
+    launch_grouped_gemm(EPI_ACT_BF16, g, h->num_sms, st);
 }
 
 __global__ void tok_base_kernel(int nd, int* tok_base) {
@@ -606,7 +608,7 @@ occ_status forward_multi(occ_handle* h, const __nv_bfloat16* x, const int32_t* i
     launch_gemm2(h, P, st);
     // 6. intra-device partial combine -> bf16 return payload in inbox order
     mark(h, ST_PCOMBINE, st);
-    launch_partial_combine(Rm, h->d_R, P, D, h->row_epd.p, h->ybuf.p, h->ret.p, st);
+    launch_partial_combine(Rm, h->d_R, P, D, h->row_epd.p, h->y16.p, h->ret.p, st);
     // 7. return all-to-all: inbox rows back to their source's Sfd slots
     if ((s = tp->alltoallv(h->ret.p, ro, rc, h->y_src.p, so, sc, D * 2, st)) != OCC_OK) return s;
     // 8. combine over devices ascending
@@ -678,7 +680,7 @@ occ_status occ_destroy(occ_handle* h) {
     h->stats.release();
     h->mask.release();
     h->rmask.release();
-    for (auto* b : {&h->w13t, &h->w2t, &h->in_x, &h->x_epd, &h->hbuf, &h->ret, &h->snd_x, &h->y_src}) b->release();
+    for (auto* b : {&h->w13t, &h->w2t, &h->in_x, &h->x_epd, &h->hbuf, &h->ret, &h->snd_x, &h->y_src, &h->y16}) b->release();
     h->snd_w.release();
     for (auto* b : {&h->in_w, &h->epd_w, &h->ybuf, &h->logits, &h->rt_w}) b->release();
     h->rt_ids.release();
@@ -842,8 +844,21 @@ occ_status occ_route(occ_handle* h, const void* x, const void* gate, int n, cons
     CUDA_TRY(h->logits.ensure((size_t)std::max(n, 1) * h->E));
     CUDA_TRY(h->err.ensure(1));
     CUDA_TRY(cudaMemsetAsync(h->err.p, 0, sizeof(int32_t), st));
-    launch_router_bf16(reinterpret_cast<const __nv_bfloat16*>(x), reinterpret_cast<const __nv_bfloat16*>(gate), n,
-                       h->D, h->E, h->k, h->cfg.renormalize, p, ids, weights, scores, h->logits.p, h->err.p, st);
+    if (n > 0) {
+        // logits = x g^T on tcgen05; softmax + top-k fused in the epilogue
+        // unless pruning / score rows need the full rows (router_select)
+        const int np = (h->E + 31) / 32 * 32;
+        const bool need_rows = p.mode != 0 || scores != nullptr || np > 128;
+        if (!make_tmap_2d(h->tmRX.bytes, x, h->D, n, 64, 128) ||
+            !make_tmap_2d(h->tmRG.bytes, gate, h->D, h->E, 64, np))
+            return fail(OCC_ERR_CUDA, "cuTensorMapEncodeTiled failed (router)");
+        if (!launch_router_tc(h->tmRX.bytes, h->tmRG.bytes, n, h->D, h->E, h->k, h->cfg.renormalize, ids, weights,
+                              need_rows ? h->logits.p : nullptr, h->num_sms, st))
+            return fail(OCC_ERR_UNSUPPORTED, "router: E <= 256 and k <= 64");
+        if (need_rows)
+            launch_router_select(h->logits.p, n, h->E, h->k, h->cfg.renormalize, p, ids, weights, scores, h->err.p,
+                                 st);
+    }
     CUDA_TRY(cudaGetLastError());
     if (h->validate) return check_err(h, st);
     return OCC_OK;
@@ -931,7 +946,7 @@ occ_status occ_forward(occ_handle* h, const void* x, const int32_t* ids, const f
     // 6+7. intra-device partial combine (placement order) -> bf16 return
     // payload -> combine over devices ascending, fused on one GPU
     mark(h, ST_COMBINE, st);
-    launch_combine_fused(n, nd, k, P, dedup, D, h->mask.p, h->tok_row.p, h->row_epd.p, h->ybuf.p,
+    launch_combine_fused(n, nd, k, P, dedup, D, h->mask.p, h->tok_row.p, h->row_epd.p, h->y16.p,
                          reinterpret_cast<__nv_bfloat16*>(out), st);
     mark(h, kStages, st);
     CUDA_TRY(cudaGetLastError());
@@ -971,6 +986,7 @@ static occ_status ensure_bwd(occ_handle* h) {
     CUDA_TRY(h->g_epd.ensure(Q * D));
     CUDA_TRY(h->gpre.ensure(Q * kw));
     CUDA_TRY(h->gw_part.ensure(Q * NBf));
+    CUDA_TRY(h->ybuf.ensure(Q * D));
     if (h->bwd_tmaps_q != (int)Q) {
         if (!make_tmap_2d(h->tmG_k.bytes, h->g_epd.p, D, Q, 64, 128) ||
             !make_tmap_2d(h->tmP_k.bytes, h->gpre.p, kw, Q, 64, 128) ||

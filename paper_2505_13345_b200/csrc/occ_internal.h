@@ -9,6 +9,7 @@ namespace occ {
 constexpr int kMaxDev = 64;    // N_d <= 64 (uint64 device masks)
 constexpr int kMaxLocal = 64;  // P <= 64 experts per device
 constexpr int kRankChunk = 256;
+constexpr int kMaxTopK = 64;  // k <= 64 on the device path
 constexpr int kBM = 256;       // GEMM pair-tile rows (Epd segments are padded to it)
 
 extern long long g_launches;
@@ -150,16 +151,16 @@ void launch_gather_rows(int Q_max, const int* q_total, const int32_t* epd_src, c
                         __nv_bfloat16* dst, cudaStream_t st);
 
 // Intra-device partial combine: ret[r] = bf16( sum_{p asc} Y[row_epd[r,p]] ).
-void launch_partial_combine(int R_max, const int* R_total, int P, int D, const int32_t* row_epd, const float* Y,
-                            __nv_bfloat16* ret, cudaStream_t st);
+void launch_partial_combine(int R_max, const int* R_total, int P, int D, const int32_t* row_epd,
+                            const __nv_bfloat16* Y, __nv_bfloat16* ret, cudaStream_t st);
 // Final combine: out[t] = bf16( sum_{d asc} ret[row_of(t,d)] ).
 void launch_combine(int n, int nd, int k, int dedup, int D, const uint64_t* mask, const int32_t* tok_row,
                     const __nv_bfloat16* ret, __nv_bfloat16* out, cudaStream_t st);
 
 // world_size == 1: partial combine + return + combine fused (reads Y once).
 void launch_combine_fused(int n, int nd, int k, int P, int dedup, int D, const uint64_t* mask,
-                          const int32_t* tok_row, const int32_t* row_epd, const float* Y, __nv_bfloat16* out,
-                          cudaStream_t st);
+                          const int32_t* tok_row, const int32_t* row_epd, const __nv_bfloat16* Y,
+                          __nv_bfloat16* out, cudaStream_t st);
 
 // Saved-index extraction (parity): unpadded BRIM1 per device, P x R_d.
 void launch_extract_cindex(int R_max, const int* R_total, int P, const int32_t* row_dev, const int* in_base,
@@ -192,9 +193,12 @@ struct PruneDev {
 };
 void launch_prune_f64(const double* s, int n, int e, int k, const int32_t* ids_in, const double* w_in, PruneDev p,
                       int32_t* ids, double* w, int32_t* err, cudaStream_t st);
-void launch_router_bf16(const __nv_bfloat16* x, const __nv_bfloat16* g, int n, int d, int e, int k, int renorm,
-                        PruneDev p, int32_t* ids, float* w, float* scores, float* logits_ws, int32_t* err,
-                        cudaStream_t st);
+// Tensor-core router (occ_router.cu): returns false when the shape needs the
+// logits path (E > 128 without logits_out, or k > 64).
+bool launch_router_tc(const void* tmap_x, const void* tmap_g, int n, int d, int e, int k, int renorm, int32_t* ids,
+                      float* w, float* logits_out, int num_sms, cudaStream_t st);
+void launch_router_select(float* logits, int n, int e, int k, int renorm, PruneDev p, int32_t* ids, float* w,
+                          float* scores, int32_t* err, cudaStream_t st);
 
 // Weight layout conversion: reference [E, K, N] row-major -> K-major [E, N, K]
 // (optionally interleaving w1/w3 in 128-column blocks for SwiGLU).

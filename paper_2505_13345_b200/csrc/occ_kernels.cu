@@ -16,7 +16,6 @@ long long g_launches = 0;
 
 namespace {
 
-constexpr int kMaxTopK = 64;
 constexpr int kRankThreads = kRankChunk;  // one item per thread, 8 warps
 constexpr int kRankWarps = kRankThreads / 32;
 
@@ -427,8 +426,15 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(int Q_max, const int* 
 // ------------------------------------------------------- partial combine --
 // merge_matmul's per-row sum over local experts (pipeline.cpp:263-281),
 // done after the grouped GEMM: ascending placement-list order, fp32.
+__device__ __forceinline__ float4 ld_bf16x4(const __nv_bfloat16* p) {
+    const uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
+    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+    return make_float4(a.x, a.y, b.x, b.y);
+}
+
 __global__ void __launch_bounds__(256) partial_combine_kernel(int R_max, const int* R_total, int P, int D,
-                                                              const int32_t* row_epd, const float* Y,
+                                                              const int32_t* row_epd, const __nv_bfloat16* Y,
                                                               __nv_bfloat16* ret) {
     const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
@@ -443,7 +449,7 @@ __global__ void __launch_bounds__(256) partial_combine_kernel(int R_max, const i
     for (int v = lane; v < nv; v += 32) {
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
         for (int i = 0; i < nq; ++i) {
-            const float4 y = __ldg(reinterpret_cast<const float4*>(Y + (long)qs[i] * D) + v);
+            const float4 y = ld_bf16x4(Y + (long)qs[i] * D + 4 * v);
             acc.x += y.x; acc.y += y.y; acc.z += y.z; acc.w += y.w;
         }
         uint2 o;
@@ -503,7 +509,7 @@ __global__ void __launch_bounds__(256) combine_kernel(int n, int nd, int k, int 
 // multi-GPU exchange would carry it, then summed over devices in fp32.
 __global__ void __launch_bounds__(256) combine_fused_kernel(int n, int nd, int k, int P, int dedup, int D,
                                                             const uint64_t* mask, const int32_t* tok_row,
-                                                            const int32_t* row_epd, const float* Y,
+                                                            const int32_t* row_epd, const __nv_bfloat16* Y,
                                                             __nv_bfloat16* out) {
     const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
@@ -546,7 +552,7 @@ __global__ void __launch_bounds__(256) combine_fused_kernel(int n, int nd, int k
                 acc.w += __bfloat162float(__float2bfloat16(dev.w));
                 dev = make_float4(0.f, 0.f, 0.f, 0.f);
             }
-            const float4 y = __ldg(reinterpret_cast<const float4*>(Y + (long)qs[i] * D) + v);
+            const float4 y = ld_bf16x4(Y + (long)qs[i] * D + 4 * v);
             dev.x += y.x; dev.y += y.y; dev.z += y.z; dev.w += y.w;
         }
         acc.x += __bfloat162float(__float2bfloat16(dev.x));
@@ -940,77 +946,6 @@ __global__ void router_select_kernel(float* logits, int n, int e, int k, int ren
     route_token(logits + (long)t * e, t, e, k, renorm, p, ids, w, scores, err);
 }
 
-// Fused router: logits = x g^T (bf16 in, fp32 accumulate) + softmax + top-k
-// (+ pruning).  One warp per 8 tokens; lanes split D in 8-element (16-byte)
-// slices, a chunk of 8 experts of the gate lives in registers, x rows are
-// streamed once per expert chunk (HBM-bound on x for E <= 8).  Per-token
-// selection runs one thread per token on the logits staged in shared memory.
-constexpr int kRTokW = 8, kRWarps = 4, kREC = 8;
-__global__ void __launch_bounds__(kRWarps * 32) router_fused_kernel(const __nv_bfloat16* __restrict__ x,
-                                                                   const __nv_bfloat16* __restrict__ g, int n, int d,
-                                                                   int e, int k, int renorm, PruneDev p, int32_t* ids,
-                                                                   float* w, float* scores, int32_t* err) {
-    extern __shared__ float lg[];  // [kRWarps*kRTokW][e]
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int t0 = (blockIdx.x * kRWarps + warp) * kRTokW;
-    for (int ec = 0; ec < e; ec += kREC) {
-        float acc[kRTokW][kREC];
-#pragma unroll
-        for (int t = 0; t < kRTokW; ++t)
-#pragma unroll
-            for (int j = 0; j < kREC; ++j) acc[t][j] = 0.f;
-        for (int c = lane * 8; c < d; c += 256) {
-            float gv[kREC][8];
-#pragma unroll
-            for (int j = 0; j < kREC; ++j) {
-                uint4 u = make_uint4(0, 0, 0, 0);
-                if (ec + j < e) u = __ldg(reinterpret_cast<const uint4*>(g + (long)(ec + j) * d + c));
-                const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const float2 f = __bfloat1622float2(h[q]);
-                    gv[j][2 * q] = f.x;
-                    gv[j][2 * q + 1] = f.y;
-                }
-            }
-            uint4 xu[kRTokW];
-#pragma unroll
-            for (int t = 0; t < kRTokW; ++t) {  // all token loads in flight before the FMAs
-                const int tt = t0 + t < n ? t0 + t : n - 1;
-                xu[t] = __ldg(reinterpret_cast<const uint4*>(x + (long)tt * d + c));
-            }
-#pragma unroll
-            for (int t = 0; t < kRTokW; ++t) {
-                const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&xu[t]);
-                float xv[8];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const float2 f = __bfloat1622float2(h[q]);
-                    xv[2 * q] = f.x;
-                    xv[2 * q + 1] = f.y;
-                }
-#pragma unroll
-                for (int j = 0; j < kREC; ++j)
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) acc[t][j] = fmaf(xv[i], gv[j][i], acc[t][j]);
-            }
-        }
-#pragma unroll
-        for (int t = 0; t < kRTokW; ++t)
-#pragma unroll
-            for (int j = 0; j < kREC; ++j) {
-                float v = acc[t][j];
-#pragma unroll
-                for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-                if (lane == 0 && ec + j < e) lg[(warp * kRTokW + t) * e + ec + j] = v;
-            }
-    }
-    __syncthreads();
-    const int tl = threadIdx.x;
-    const int t = blockIdx.x * kRWarps * kRTokW + tl;
-    if (tl < kRWarps * kRTokW && t < n) route_token(lg + tl * e, t, e, k, renorm, p, ids, w, scores, err);
-}
-
 // -------------------------------------------------- weight re-layout ---
 // Reference expert matrices are [K, N] row-major (token.hpp:30-44); the
 // tensor-core path wants them K-major ([N, K]).  For SwiGLU the w1/w3 rows
@@ -1136,8 +1071,8 @@ void launch_gather_rows(int Q_max, const int* q_total, const int32_t* epd_src, c
     count_launch();
 }
 
-void launch_partial_combine(int R_max, const int* R_total, int P, int D, const int32_t* row_epd, const float* Y,
-                            __nv_bfloat16* ret, cudaStream_t st) {
+void launch_partial_combine(int R_max, const int* R_total, int P, int D, const int32_t* row_epd,
+                            const __nv_bfloat16* Y, __nv_bfloat16* ret, cudaStream_t st) {
     if (!R_max) return;
     partial_combine_kernel<<<(R_max + 7) / 8, 256, 0, st>>>(R_max, R_total, P, D, row_epd, Y, ret);
     count_launch();
@@ -1151,8 +1086,8 @@ void launch_combine(int n, int nd, int k, int dedup, int D, const uint64_t* mask
 }
 
 void launch_combine_fused(int n, int nd, int k, int P, int dedup, int D, const uint64_t* mask,
-                          const int32_t* tok_row, const int32_t* row_epd, const float* Y, __nv_bfloat16* out,
-                          cudaStream_t st) {
+                          const int32_t* tok_row, const int32_t* row_epd, const __nv_bfloat16* Y,
+                          __nv_bfloat16* out, cudaStream_t st) {
     if (!n) return;
     combine_fused_kernel<<<(n + 7) / 8, 256, 0, st>>>(n, nd, k, P, dedup, D, mask, tok_row, row_epd, Y, out);
     count_launch();
@@ -1229,16 +1164,11 @@ void launch_prune_f64(const double* s, int n, int e, int k, const int32_t* ids_i
     count_launch();
 }
 
-void launch_router_bf16(const __nv_bfloat16* x, const __nv_bfloat16* g, int n, int d, int e, int k, int renorm,
-                        PruneDev p, int32_t* ids, float* w, float* scores, float* logits_ws, int32_t* err,
-                        cudaStream_t st) {
+void launch_router_select(float* logits, int n, int e, int k, int renorm, PruneDev p, int32_t* ids, float* w,
+                          float* scores, int32_t* err, cudaStream_t st) {
     if (!n) return;
-    const int per_block = kRWarps * kRTokW;
-    const size_t smem = sizeof(float) * per_block * e;
-    router_fused_kernel<<<(n + per_block - 1) / per_block, kRWarps * 32, smem, st>>>(x, g, n, d, e, k, renorm, p, ids,
-                                                                                      w, scores, err);
+    router_select_kernel<<<(n + 127) / 128, 128, 0, st>>>(logits, n, e, k, renorm, p, ids, w, scores, err);
     count_launch();
-    (void)logits_ws;
 }
 
 void launch_transpose_weights(const __nv_bfloat16* w, int E, int K, int N, __nv_bfloat16* out, int out_rows_per_e,
