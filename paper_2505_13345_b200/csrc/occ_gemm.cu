@@ -33,6 +33,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "occ_common.cuh"
 #include "occ_internal.h"
@@ -510,6 +511,11 @@ void launch_grouped_gemm(EpiMode mode, const GemmArgs& a, int num_sms, cudaStrea
     p.gw_part = a.gw_part;
     const CUtensorMap& ta = *reinterpret_cast<const CUtensorMap*>(a.tmap_a);
     const CUtensorMap& tb = *reinterpret_cast<const CUtensorMap*>(a.tmap_b);
+    static const int band_override = [] {  // raster experiments (profiles/), not a product knob
+        const char* e = getenv("OCC_GEMM_BAND");
+        return e ? atoi(e) : 0;
+    }();
+    if (band_override > 0 && !(mode == EPI_WGRAD)) p.band = band_override;
     int grid = 2 * a.max_tiles < num_sms ? 2 * a.max_tiles : num_sms;
     grid &= ~1;  // CTA pairs
     if (grid <= 0) return;

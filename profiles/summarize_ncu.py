@@ -18,10 +18,32 @@ KEYS = [
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "occupancy_%"),
     ("launch__registers_per_thread", "regs"),
     ("sm__cycles_elapsed.avg.per_second", "sm_clk"),
+    ("lts__t_sector_hit_rate.pct", "l2_hit_%"),
+    ("lts__throughput.avg.pct_of_peak_sustained_elapsed", "l2_%"),
 ]
 
 
+def launch_shares(path):
+    """Per-kernel totals and shares from a `--metrics gpu__time_duration.sum` launch list."""
+    rows = [r for r in csv.reader(open(path)) if len(r) > 10]
+    hdr = rows[0]
+    ki, vi = hdr.index("Kernel Name"), hdr.index("Metric Value")
+    agg = {}
+    for r in rows[1:]:
+        n = r[ki].replace("(anonymous namespace)::", "").replace("<unnamed>::", "").split("(")[0]
+        a = agg.setdefault(n, [0, 0.0])
+        a[0] += 1
+        a[1] += float(r[vi].replace(",", ""))
+    tot = sum(a[1] for a in agg.values())
+    print(f"# launch list `{path}` (cold-cache, serialised: compare shares)\n")
+    print("| kernel | launches | total ms | share |\n|---|---|---|---|")
+    for n, (c, t) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        print(f"| {n} | {c} | {t / 1e6:.3f} | {100 * t / tot:.1f}% |")
+
+
 def main(path):
+    if path.endswith(".csv"):
+        return launch_shares(path)
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
