@@ -38,15 +38,16 @@ WORKLOADS = {
                name="single MoE layer, 8 experts top-2, d=512, d_ff=1024, 2048 tokens, 2 simulated EP ranks "
                     "(reference CPU oracle shape; 2-matrix SiLU experts)"),
     "deepseek": dict(E=64, k=6, D=2048, F=1408, act="swiglu", tokens=16384, nd_sim=1, plan_ep=8, train=False,
-                     prune=None, name="DeepSeek-MoE-16B layer (64 routed experts top-6, d=2048, ffn=1408, SwiGLU; "
-                                      "the 2 shared experts are not included) 16384 tokens"),
+                     prune=None, shared=(2, 1408, False),
+                     name="DeepSeek-MoE-16B layer (64 routed experts top-6 + 2 shared experts, d=2048, ffn=1408, "
+                          "SwiGLU) 16384 tokens"),
     "olmoe": dict(E=64, k=8, D=2048, F=1024, act="swiglu", tokens=65536, nd_sim=1, plan_ep=8, train=True,
                   prune=None, name="OLMoE-1B-7B layer (64 experts top-8, d=2048, ffn=1024, SwiGLU) "
                                    "forward+backward at 65536 tokens/step"),
     "qwen": dict(E=60, k=4, D=2048, F=1408, act="swiglu", tokens=16384, nd_sim=4, plan_ep=4, train=False,
-                 prune=("router", 2), name="Qwen1.5-MoE-A2.7B layer (60 routed experts top-4, d=2048, ffn=1408, "
-                                           "SwiGLU; shared expert not included) with collaboration pruning to <=2 "
-                                           "devices/token, EP=4 simulated on one GPU"),
+                 prune=("router", 2), shared=(1, 5632, True),
+                 name="Qwen1.5-MoE-A2.7B layer (60 routed experts top-4, d=2048, ffn=1408, SwiGLU; + gated shared "
+                      "expert ffn=5632) with collaboration pruning to <=2 devices/token, EP=4 simulated on one GPU"),
 }
 W = WORKLOADS["mixtral"]
 E, K_TOP, D, F = W["E"], W["k"], W["D"], W["F"]
@@ -265,6 +266,15 @@ def run_ours(args):
     w2 = torch.empty((e_local, F, D), dtype=torch.bfloat16, device=dev).uniform_(-1, 1).mul_(F ** -0.5)
     layer.load_experts(w1, w2, w3)
     del w1, w2, w3
+    sh = W.get("shared")
+    if sh:  # shared experts: dense FFN on every token at its source (+ Qwen's sigmoid gate)
+        ns, fs, with_gate = sh
+        s1 = torch.empty((ns, D, fs), dtype=torch.bfloat16, device=dev).uniform_(-1, 1).mul_(D ** -0.5)
+        s3 = torch.empty_like(s1).uniform_(-1, 1).mul_(D ** -0.5) if gated else None
+        s2 = torch.empty((ns, fs, D), dtype=torch.bfloat16, device=dev).uniform_(-1, 1).mul_((ns * fs) ** -0.5)
+        sg = torch.empty(D, dtype=torch.bfloat16, device=dev).uniform_(-1, 1).mul_(D ** -0.5) if with_gate else None
+        layer.load_shared_experts(s1, s2, s3, sg)
+        del s1, s2, s3, sg
     torch.cuda.empty_cache()
     gate = torch.empty((E, D), dtype=torch.bfloat16, device=dev).uniform_(-1, 1).mul_(3.0 / D ** 0.5)
     x = torch.empty((n_local, D), dtype=torch.bfloat16, device=dev).uniform_(-1, 1)
@@ -370,6 +380,10 @@ def run_ours(args):
     flops1 = 2.0 * n_epd * D * ((2 if gated else 1) * F)
     flops2 = 2.0 * n_epd * F * D
     train_flops = 2.0 * (flops1 + flops2) if W["train"] else 0.0
+    shared_flops = 0.0
+    if W.get("shared"):
+        ns, fs, _ = W["shared"]
+        shared_flops = 2.0 * args.tokens * D * ns * fs * (3 if gated else 2)
     tflops1 = flops1 / (stages["gemm1"] / 1e3) / 1e12
     tflops2 = flops2 / (stages["gemm2"] / 1e3) / 1e12
     # burst peak (cuBLAS timed alone): our timed loop is ~0.1 s, far shorter than
@@ -378,7 +392,7 @@ def run_ours(args):
     peak_sus = peaks.get("bf16_tflops_sustained", peak)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "gemm1_traffic.json")
-    if os.path.exists(tpath):
+    if os.path.exists(tpath) and args.workload == "mixtral":
         with open(tpath) as f:
             traffic = json.load(f).get("bytes_per_launch")
     roofline = {"kernel": "grouped_gemm_kernel<SWIGLU> (GEMM-1: x @ [w1|w3], silu*up*gate-weight epilogue)",
@@ -387,7 +401,9 @@ def run_ours(args):
                 "traffic": traffic,
                 "flops_per_launch": flops1, "launch_ms": stages["gemm1"],
                 "gemm2": {"achieved": tflops2, "frac": tflops2 / peak, "launch_ms": stages["gemm2"]},
-                "layer_frac": (flops1 + flops2) / (sum(stages.values()) / 1e3) / 1e12 / peak}
+                "layer_frac": (flops1 + flops2 + shared_flops) / (sum(stages.values()) / 1e3) / 1e12 / peak}
+    if shared_flops:
+        roofline["shared_tflops"] = shared_flops / (stages["shared"] / 1e3) / 1e12
     if W["train"]:
         roofline["step_tflops_fwd_bwd"] = (flops1 + flops2 + train_flops) / (tot_ms / args.steps / 1e3) / 1e12
 

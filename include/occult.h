@@ -109,6 +109,21 @@ occ_status occ_set_placement(occ_handle* h, const int32_t* placement);
  * world_size > 1: this rank's P local experts in placement-list order.
  * w3 is required iff activation == OCC_ACT_SWIGLU, else NULL. */
 occ_status occ_load_experts(occ_handle* h, const void* w1, const void* w3, const void* w2, occ_stream_t stream);
+/* Shared (always-active) experts of DeepSeek-MoE / Qwen-MoE layers
+ * (BASELINE configs 3 and 5).  Not in the reference
+ * (SPEC.md:9): the layer output becomes
+ *     out[t] = bf16( sum_d return_d[t] + bf16(g_t * sum_s FFN_s(x[t])) )
+ * with FFN_s the same expert type as the routed experts (SwiGLU or the
+ * 2-matrix act expert) and g_t = sigmoid(x[t] . gate) when `gate` is given
+ * (Qwen's shared_expert_gate) or 1.  Shared experts run on every token's
+ * SOURCE device — no all-to-all — as one dense FFN of width
+ * num_shared * d_ff_shared (the S experts stacked along the hidden dim,
+ * which sums their outputs).  Restated in oracle/occ_oracle.c
+ * (orc_shared_experts).  DEVICE pointers, reference layout:
+ *   w1, w3 [S, D, F_s] bf16 (w3 iff SwiGLU), w2 [S, F_s, D] bf16,
+ *   gate [D] bf16 or NULL.  num_shared = 0 detaches them. */
+occ_status occ_load_shared_experts(occ_handle* h, int num_shared, int d_ff_shared, const void* w1, const void* w3,
+                                   const void* w2, const void* gate, occ_stream_t stream);
 /* Squared-cosine similarity table (SimilarityTable::values, pruning.hpp:25-30),
  * HOST pointer [E * E]; the per-expert ranking is built as the reference does. */
 occ_status occ_set_similarity(occ_handle* h, const double* values);
@@ -211,9 +226,10 @@ occ_status occ_reschedule_placement(const double* p, int e, int num_devices, int
 occ_status occ_allreduce_histogram(occ_handle* h, int64_t* counts, occ_stream_t stream);
 
 /* Stage profiling with CUDA events on the launching stream (default off).
- * occ_stage_ms fills ms[0..8) for the last occ_forward_expert_parallel /
+ * occ_stage_ms fills ms[0..10) for the last occ_forward_expert_parallel /
  * occ_forward: route, plan, pack, compute_index, gather, gemm1, gemm2,
- * partial_combine, combine (ms < 0: stage not recorded); returns the count. */
+ * shared, partial_combine, combine (ms < 0: stage not recorded); returns
+ * the count. */
 occ_status occ_set_profiling(occ_handle* h, int on);
 int occ_stage_ms(occ_handle* h, float* ms, int max_stages);
 

@@ -730,6 +730,58 @@ void orc_dense_given_routing(const double* x, int n, int dm, const int* ids, con
     free(acc);
 }
 
+/* Shared (always-active) experts — NOT in the reference; the
+ * DeepSeek-MoE / Qwen-MoE extension of BASELINE configs 3 and 5, restated
+ * with the same per-expert arithmetic as dense_given_routing above
+ * (pipeline.cpp:542-562): for every token t and shared expert s,
+ *   h = act(x w1_s)            (2-matrix expert)   or
+ *   h = silu(x w1_s) * (x w3_s) (SwiGLU),
+ *   y_t += g_t * (h w2_s),  g_t = sigmoid(x_t . gate) if gate, else 1,
+ * accumulated in double in ascending s, q, c order and added to out[t]
+ * (out is the routed layer output; the product path adds the shared rows
+ * last).  Pinned against an independent torch fp64 computation
+ * (tests/test_oracle.py::test_shared_experts_oracle_vs_torch).
+ *   w1, w3: ns x dm x dh, w2: ns x dh x dm, gate: dm or NULL. */
+void orc_shared_experts(const double* x, int n, int dm, const double* w1, const double* w2, const double* w3,
+                        int ns, int dh, int act, const double* gate, double* out) {
+    double* h = (double*)malloc(sizeof(double) * (size_t)dh);
+    double* acc = (double*)malloc(sizeof(double) * (size_t)dm);
+    for (int t = 0; t < n; ++t) {
+        const double* xr = x + (long)t * dm;
+        double g = 1.0;
+        if (gate) {
+            double z = 0.0;
+            for (int c = 0; c < dm; ++c) z += xr[c] * gate[c];
+            g = 1.0 / (1.0 + exp(-z));
+        }
+        for (int c = 0; c < dm; ++c) acc[c] = 0.0;
+        for (int s = 0; s < ns; ++s) {
+            const double* W1 = w1 + (long)s * dm * dh;
+            const double* W2 = w2 + (long)s * dh * dm;
+            for (int q = 0; q < dh; ++q) {
+                double a = 0.0;
+                for (int c = 0; c < dm; ++c) a += xr[c] * W1[(long)c * dh + q];
+                if (w3) {
+                    const double* W3 = w3 + (long)s * dm * dh;
+                    double b = 0.0;
+                    for (int c = 0; c < dm; ++c) b += xr[c] * W3[(long)c * dh + q];
+                    h[q] = act_fn(a, 1) * b;
+                } else {
+                    h[q] = act_fn(a, act);
+                }
+            }
+            for (int c = 0; c < dm; ++c) {
+                double o = 0.0;
+                for (int q = 0; q < dh; ++q) o += h[q] * W2[(long)q * dm + c];
+                acc[c] += o;
+            }
+        }
+        for (int c = 0; c < dm; ++c) out[(long)t * dm + c] += g * acc[c];
+    }
+    free(h);
+    free(acc);
+}
+
 /* matrix.cpp:52-60 */
 double orc_max_rel_error(const double* a, const double* b, long n) {
     double diff = 0.0, ref = 0.0;

@@ -109,13 +109,14 @@ def port_lib():
         lib.orc_max_rel_error.restype = _d
         for fn in ("orc_gate_scores", "orc_gate_logits", "orc_softmax_rows", "orc_normalize_graph",
                    "orc_similarity_table", "orc_random_matrix", "orc_dense_given_routing", "orc_rng_seed",
-                   "orc_trivial_placement", "orc_collaboration_shares"):
+                   "orc_trivial_placement", "orc_collaboration_shares", "orc_shared_experts"):
             getattr(lib, fn).restype = None
         lib.orc_rng_seed.argtypes = [_p, C.c_uint64]
         lib.orc_max_rel_error.argtypes = [_p, _p, C.c_long]
         lib.orc_forward_given_routing.argtypes = (
             [_p, _i, _i, _p, _p, _i, _p, _p, _p, _i, _i, _p, _i, _p, _i, _i, _i, _d] + [_p] * 7)
         lib.orc_dense_given_routing.argtypes = [_p, _i, _i, _p, _p, _i, _p, _p, _p, _i, _i, _i, _p, _i, _p]
+        lib.orc_shared_experts.argtypes = [_p, _i, _i, _p, _p, _p, _i, _i, _i, _p, _p]
         _PORT = lib
     return _PORT
 
@@ -252,6 +253,19 @@ class _Backend:
         self.lib.orc_dense_given_routing(_ptr(x), n, dm, _ptr(ids), _ptr(w), k, _ptr(w1), _ptr(w2),
                                          None if w3 is None else _ptr(_f64(w3)), dh, ACT[act], int(single),
                                          _ptr(r), cnt, _ptr(out))
+        return out
+
+    def shared_experts(self, x, w1, w2, w3=None, gate=None, act="silu", out=None):
+        """Shared-expert extension (not in the reference): out += g * sum_s FFN_s(x)
+        (occ_oracle.c orc_shared_experts).  Port only."""
+        if self.prefix == "ref_":
+            raise ValueError("the reference has no shared experts (SPEC.md:9)")
+        x, w1, w2 = _f64(x), _f64(w1), _f64(w2)
+        n, dm = x.shape
+        ns, _, dh = w1.shape
+        out = np.zeros((n, dm), np.float64) if out is None else np.array(out, dtype=np.float64, copy=True)
+        self.lib.orc_shared_experts(_ptr(x), n, dm, _ptr(w1), _ptr(w2), None if w3 is None else _ptr(_f64(w3)),
+                                    ns, dh, ACT[act], None if gate is None else _ptr(_f64(gate)), _ptr(out))
         return out
 
     def prune_routing(self, scores, ids, w, plist, mode, budget, sim_values=None, own_score=False,

@@ -84,9 +84,10 @@ EXPORTS = (
     "occ_route", "occ_build_dispatch", "occ_forward", "occ_forward_expert_parallel", "occ_comm_report_get",
     "occ_saved_index", "occ_coactivation_histogram", "occ_normalize_graph", "occ_reschedule_placement",
     "occ_allreduce_histogram", "occ_last_error", "occ_launch_count", "occ_set_profiling", "occ_stage_ms", "occ_forward_host", "occ_host_wait", "occ_comm_init_loopback", "occ_exchange_layout", "occ_set_training", "occ_backward",
+    "occ_load_shared_experts",
 )
 
-STAGES = ("route", "plan", "pack", "compute_index", "gather", "gemm1", "gemm2", "partial_combine", "combine")
+STAGES = ("route", "plan", "pack", "compute_index", "gather", "gemm1", "gemm2", "shared", "partial_combine", "combine")
 
 _LIB = None
 
@@ -255,6 +256,20 @@ class ExpertParallelLayer:
         _check(lib().occ_load_experts(self._h, _ptr(ts[0]), _ptr(ts[1]), _ptr(ts[2]), _stream()), "load_experts")
         torch.cuda.current_stream().synchronize()
         self._weights = ts
+
+    def load_shared_experts(self, w1: torch.Tensor, w2: torch.Tensor, w3: Optional[torch.Tensor] = None,
+                            gate: Optional[torch.Tensor] = None):
+        """Shared (always-active) experts, DeepSeek-MoE / Qwen-MoE style (not in
+        the reference): w1/w3 [S, D, F_s], w2 [S, F_s, D]; optional
+        gate [D] gives each token the weight sigmoid(x . gate) (Qwen's
+        shared_expert_gate).  Computed at every token's source device and
+        added last in the combine (include/occult.h)."""
+        _need_cuda(w1, w2, w3, gate)
+        ts = [t.to(torch.bfloat16).contiguous() if t is not None else None for t in (w1, w3, w2, gate)]
+        _check(lib().occ_load_shared_experts(self._h, int(ts[0].shape[0]), int(ts[0].shape[2]), _ptr(ts[0]),
+                                             _ptr(ts[1]), _ptr(ts[2]), _ptr(ts[3]), _stream()), "load_shared_experts")
+        torch.cuda.current_stream().synchronize()
+        self._shared = ts
 
     def set_placement(self, placement: Placement):
         pl = (C.c_int32 * self.config.num_experts)(*placement.flat())

@@ -80,7 +80,8 @@ struct DevBuf {
 }  // namespace
 
 // Stage boundaries recorded by occ_forward_expert_parallel / occ_forward.
-enum Stage { ST_ROUTE = 0, ST_PLAN, ST_PACK, ST_CINDEX, ST_GATHER, ST_GEMM1, ST_GEMM2, ST_PCOMBINE, ST_COMBINE, kStages };
+enum Stage { ST_ROUTE = 0, ST_PLAN, ST_PACK, ST_CINDEX, ST_GATHER, ST_GEMM1, ST_GEMM2, ST_SHARED, ST_PCOMBINE, ST_COMBINE,
+             kStages };
 
 // ------------------------------------------------------------ transport --
 // The two exchanges of the EP layer are an all-gather of the per-source
@@ -165,6 +166,17 @@ struct occ_handle {
     DevBuf<__nv_bfloat16> x_stage, o_stage;
     long long host_calls = 0;
     bool host_slot_used[2] = {false, false};
+    // shared experts (occ_load_shared_experts): one dense FFN of width Fsh on
+    // every token at its source
+    int n_shared = 0, Fsh = 0, sh_rows = 0;
+    bool sh_gate = false;
+    DevBuf<__nv_bfloat16> w13s, w2s, sgate, hs, ys;
+    DevBuf<float> sw;
+    DevBuf<int> sh_grp;
+    size_t sh_cap = 0;
+    TmapBox tmBS1, tmBS2, tmAS1, tmAS2;
+    cudaStream_t s_aux = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 namespace {
@@ -462,6 +474,57 @@ void launch_gemm2(occ_handle* h, int ngroups, cudaStream_t st) {
     launch_grouped_gemm(EPI_ACT_BF16, g, h->num_sms, st);
 }
 
+// Shared experts on this device's n tokens: g = sigmoid(x . gate) (or 1),
+// GEMM-1 x @ [w1s|w3s] with the act/SwiGLU x g epilogue, GEMM-2 h @ w2s
+// -> ys [n, D] bf16 (added last by the combine).
+occ_status run_shared(occ_handle* h, const __nv_bfloat16* x, int n, cudaStream_t st) {
+    const int D = h->D, Fs = h->Fsh;
+    const size_t n_pad = (size_t)(n + kBM - 1) / kBM * kBM;
+    if (n_pad > h->sh_cap || !h->hs.p) {
+        CUDA_TRY(h->hs.ensure(n_pad * Fs));
+        CUDA_TRY(h->ys.ensure(n_pad * D));
+        CUDA_TRY(h->sw.ensure(n_pad));
+        h->sh_cap = n_pad;
+        if (!make_tmap_2d(h->tmAS2.bytes, h->hs.p, Fs, n_pad, 64, kBM / 2))
+            return fail(OCC_ERR_CUDA, "cuTensorMapEncodeTiled failed (shared h)");
+    }
+    if (!make_tmap_2d(h->tmAS1.bytes, x, D, (uint64_t)n, 64, kBM / 2))
+        return fail(OCC_ERR_CUDA, "cuTensorMapEncodeTiled failed (tokens; x must be 16-byte aligned)");
+    launch_shared_gate(n, (int)n_pad, D, x, h->sh_gate ? h->sgate.p : nullptr, h->sw.p, h->sh_grp.p, st);
+    const int nmb = (int)(n_pad / kBM);
+    GemmArgs g;
+    g.tmap_a = h->tmAS1.bytes;
+    g.tmap_b = h->tmBS1.bytes;
+    g.K = D;
+    g.N = Fs;
+    g.b_rows_per_e = h->sh_rows;
+    g.grp_mb = h->sh_grp.p;
+    g.grp_w = h->sh_grp.p + 2;
+    g.ngroups = 1;
+    g.row_w = h->sw.p;
+    g.out = h->hs.p;
+    g.ldo = Fs;
+    g.act = h->cfg.activation;
+    g.max_tiles = nmb * (h->gated ? Fs / 128 : (Fs + 255) / 256);
+    launch_grouped_gemm(h->gated ? EPI_SWIGLU_BF16 : EPI_ACT_BF16, g, h->num_sms, st);
+    GemmArgs g2;
+    g2.tmap_a = h->tmAS2.bytes;
+    g2.tmap_b = h->tmBS2.bytes;
+    g2.K = Fs;
+    g2.N = D;
+    g2.b_rows_per_e = D;
+    g2.grp_mb = h->sh_grp.p;
+    g2.grp_w = h->sh_grp.p + 2;
+    g2.ngroups = 1;
+    g2.band = 8;
+    g2.out = h->ys.p;
+    g2.ldo = D;
+    g2.act = OCC_ACT_IDENTITY;
+    g2.max_tiles = nmb * ((D + 255) / 256);
+    launch_grouped_gemm(EPI_ACT_BF16, g2, h->num_sms, st);
+    return OCC_OK;
+}
+
 __global__ void tok_base_kernel(int nd, int* tok_base) {
     // tok_base[0..nd) = exclusive prefix of ntok = tok_base[nd..2nd)
     if (threadIdx.x == 0) {
@@ -563,6 +626,15 @@ occ_status forward_multi(occ_handle* h, const __nv_bfloat16* x, const int32_t* i
     mark(h, ST_PACK, st);
     PackArgs pk{n, k, nd, D, dedup, x, ids, weights, h->mask.p, h->tok_row.p, h->snd_x.p, h->snd_ids.p, h->snd_w.p};
     launch_pack(pk, st);
+    // shared experts: source-side dense FFN on a second stream, overlapping
+    // the dispatch exchange and the routed expert compute
+    const bool shared = h->n_shared > 0 && n > 0;
+    if (shared) {
+        CUDA_TRY(cudaEventRecord(h->ev_fork, st));
+        CUDA_TRY(cudaStreamWaitEvent(h->s_aux, h->ev_fork, 0));
+        if ((s = run_shared(h, x, n, h->s_aux)) != OCC_OK) return s;
+        CUDA_TRY(cudaEventRecord(h->ev_join, h->s_aux));
+    }
     // 3. dispatch all-to-all (counts are needed on the host for NCCL)
     h->h_C.resize((size_t)nd * nd);
     CUDA_TRY(cudaMemcpyAsync(h->h_C.data(), C_all, sizeof(int) * nd * nd, cudaMemcpyDeviceToHost, st));
@@ -613,7 +685,8 @@ occ_status forward_multi(occ_handle* h, const __nv_bfloat16* x, const int32_t* i
     if ((s = tp->alltoallv(h->ret.p, ro, rc, h->y_src.p, so, sc, D * 2, st)) != OCC_OK) return s;
     // 8. combine over devices ascending
     mark(h, ST_COMBINE, st);
-    launch_combine(n, nd, k, dedup, D, h->mask.p, h->tok_row.p, h->y_src.p, out, st);
+    if (shared) CUDA_TRY(cudaStreamWaitEvent(st, h->ev_join, 0));
+    launch_combine(n, nd, k, dedup, D, h->mask.p, h->tok_row.p, h->y_src.p, shared ? h->ys.p : nullptr, out, st);
     mark(h, kStages, st);
     CUDA_TRY(cudaGetLastError());
     h->last_n = n;
@@ -696,6 +769,12 @@ occ_status occ_destroy(occ_handle* h) {
     h->gw_part.release();
     h->gw_row.release();
     h->epd_j.release();
+    for (auto* b : {&h->w13s, &h->w2s, &h->sgate, &h->hs, &h->ys}) b->release();
+    h->sw.release();
+    h->sh_grp.release();
+    if (h->s_aux) cudaStreamDestroy(h->s_aux);
+    if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+    if (h->ev_join) cudaEventDestroy(h->ev_join);
     delete h;
     return OCC_OK;
 }
@@ -751,6 +830,55 @@ occ_status occ_load_experts(occ_handle* h, const void* w1, const void* w3, const
         !make_tmap_2d(h->tmB2.bytes, h->w2t.p, F, (uint64_t)El * D, 64, 128))
         return fail(OCC_ERR_CUDA, "cuTensorMapEncodeTiled failed (weights)");
     h->weights_loaded = true;
+    return OCC_OK;
+}
+
+occ_status occ_load_shared_experts(occ_handle* h, int num_shared, int d_ff_shared, const void* w1, const void* w3,
+                                   const void* w2, const void* gate, occ_stream_t stream) {
+    if (!h) return fail(OCC_ERR_ARG, "null handle");
+    if (num_shared < 0) return fail(OCC_ERR_CONFIG, "shared experts: num_shared must be >= 0");
+    if (num_shared == 0) {
+        h->n_shared = 0;
+        return OCC_OK;
+    }
+    if (!w1 || !w2) return fail(OCC_ERR_ARG, "null weight pointer");
+    if (h->gated != (w3 != nullptr)) return fail(OCC_ERR_SHAPE, "w3 must be given iff activation is SwiGLU");
+    if (d_ff_shared < 1 || d_ff_shared % 8) return fail(OCC_ERR_UNSUPPORTED, "d_ff_shared must be a multiple of 8");
+    if (h->gated && d_ff_shared % 128) return fail(OCC_ERR_UNSUPPORTED, "SwiGLU needs d_ff_shared % 128 == 0");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    const int S = num_shared, F = d_ff_shared, D = h->D, Fs = S * F;
+    h->sh_rows = h->gated ? 2 * Fs : Fs;
+    CUDA_TRY(h->w13s.ensure((size_t)h->sh_rows * D));
+    CUDA_TRY(h->w2s.ensure((size_t)D * Fs));
+    const auto* b1 = reinterpret_cast<const __nv_bfloat16*>(w1);
+    // stacking the S experts along the hidden dim: expert s's K-major rows
+    // land at s*F (s*2F with the 128-row w1/w3 interleave), which is exactly
+    // the layout of one FFN of width S*F; w2 [S, F, D] is already [S*F, D].
+    if (h->gated) {
+        launch_transpose_weights(b1, S, D, F, h->w13s.p, 2 * F, 1, st);
+        launch_transpose_weights(reinterpret_cast<const __nv_bfloat16*>(w3), S, D, F, h->w13s.p, 2 * F, 2, st);
+    } else {
+        launch_transpose_weights(b1, S, D, F, h->w13s.p, F, 0, st);
+    }
+    launch_transpose_weights(reinterpret_cast<const __nv_bfloat16*>(w2), 1, Fs, D, h->w2s.p, D, 0, st);
+    h->sh_gate = gate != nullptr;
+    if (gate) {
+        CUDA_TRY(h->sgate.ensure(D));
+        CUDA_TRY(cudaMemcpyAsync(h->sgate.p, gate, sizeof(__nv_bfloat16) * D, cudaMemcpyDeviceToDevice, st));
+    }
+    CUDA_TRY(h->sh_grp.ensure(4));
+    if (!h->s_aux) {
+        CUDA_TRY(cudaStreamCreateWithFlags(&h->s_aux, cudaStreamNonBlocking));
+        CUDA_TRY(cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming));
+        CUDA_TRY(cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming));
+    }
+    CUDA_TRY(cudaGetLastError());
+    if (!make_tmap_2d(h->tmBS1.bytes, h->w13s.p, D, (uint64_t)h->sh_rows, 64, 128) ||
+        !make_tmap_2d(h->tmBS2.bytes, h->w2s.p, Fs, (uint64_t)D, 64, 128))
+        return fail(OCC_ERR_CUDA, "cuTensorMapEncodeTiled failed (shared weights)");
+    h->n_shared = S;
+    h->Fsh = Fs;
+    h->sh_cap = 0;  // h tensor map follows Fs
     return OCC_OK;
 }
 
@@ -943,11 +1071,18 @@ occ_status occ_forward(occ_handle* h, const void* x, const int32_t* ids, const f
     mark(h, ST_GEMM2, st);
     // 5. grouped GEMM-2 (per-expert products, fp32)
     launch_gemm2(h, G * P, st);
+    // shared experts (every token, at its source; no exchange)
+    const bool shared = h->n_shared > 0;
+    if (shared) {
+        mark(h, ST_SHARED, st);
+        s = run_shared(h, reinterpret_cast<const __nv_bfloat16*>(x), n, st);
+        if (s != OCC_OK) return s;
+    }
     // 6+7. intra-device partial combine (placement order) -> bf16 return
     // payload -> combine over devices ascending, fused on one GPU
     mark(h, ST_COMBINE, st);
     launch_combine_fused(n, nd, k, P, dedup, D, h->mask.p, h->tok_row.p, h->row_epd.p, h->y16.p,
-                         reinterpret_cast<__nv_bfloat16*>(out), st);
+                         shared ? h->ys.p : nullptr, reinterpret_cast<__nv_bfloat16*>(out), st);
     mark(h, kStages, st);
     CUDA_TRY(cudaGetLastError());
     if (h->validate) return check_err(h, st);
@@ -1004,6 +1139,7 @@ occ_status occ_backward(occ_handle* h, const void* upstream, float* g_x, float* 
                         float* g_weights, occ_stream_t stream) {
     if (!h) return fail(OCC_ERR_ARG, "null handle");
     if (!h->have_train_state) return fail(OCC_ERR_STATE, "backward: forward state was not saved (occ_set_training)");
+    if (h->n_shared) return fail(OCC_ERR_UNSUPPORTED, "backward: shared experts are forward-only in this build");
     const int n = h->last_n, k = h->k, P = h->P, D = h->D, F = h->F, nd = h->nd, E = h->E;
     if (n > 0 && (!upstream || !g_x || !g_w1 || !g_w2 || !g_weights || (h->gated && !g_w3)))
         return fail(OCC_ERR_ARG, "null argument");

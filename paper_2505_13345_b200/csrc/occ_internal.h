@@ -154,13 +154,19 @@ void launch_gather_rows(int Q_max, const int* q_total, const int32_t* epd_src, c
 void launch_partial_combine(int R_max, const int* R_total, int P, int D, const int32_t* row_epd,
                             const __nv_bfloat16* Y, __nv_bfloat16* ret, cudaStream_t st);
 // Final combine: out[t] = bf16( sum_{d asc} ret[row_of(t,d)] ).
+// ys (nullable): shared-expert output rows [n, D], added last.
 void launch_combine(int n, int nd, int k, int dedup, int D, const uint64_t* mask, const int32_t* tok_row,
-                    const __nv_bfloat16* ret, __nv_bfloat16* out, cudaStream_t st);
+                    const __nv_bfloat16* ret, const __nv_bfloat16* ys, __nv_bfloat16* out, cudaStream_t st);
 
 // world_size == 1: partial combine + return + combine fused (reads Y once).
 void launch_combine_fused(int n, int nd, int k, int P, int dedup, int D, const uint64_t* mask,
                           const int32_t* tok_row, const int32_t* row_epd, const __nv_bfloat16* Y,
-                          __nv_bfloat16* out, cudaStream_t st);
+                          const __nv_bfloat16* ys, __nv_bfloat16* out, cudaStream_t st);
+// Shared experts: per-token weight g[0..n_pad) (sigmoid(x . gate), or 1 when
+// gate is null; 0 on the padded rows) and the one-group GEMM tile table
+// grp = {0, n_pad / kBM, 0}.
+void launch_shared_gate(int n, int n_pad, int D, const __nv_bfloat16* x, const __nv_bfloat16* gate, float* g,
+                        int* grp, cudaStream_t st);
 
 // Saved-index extraction (parity): unpadded BRIM1 per device, P x R_d.
 void launch_extract_cindex(int R_max, const int* R_total, int P, const int32_t* row_dev, const int* in_base,

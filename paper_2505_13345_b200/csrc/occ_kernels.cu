@@ -464,7 +464,7 @@ __global__ void __launch_bounds__(256) partial_combine_kernel(int R_max, const i
 // the returned rows; fp32 accumulation, bf16 out.
 __global__ void __launch_bounds__(256) combine_kernel(int n, int nd, int k, int dedup, int D, const uint64_t* mask,
                                                       const int32_t* tok_row, const __nv_bfloat16* ret,
-                                                      __nv_bfloat16* out) {
+                                                      const __nv_bfloat16* ys, __nv_bfloat16* out) {
     const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (t >= n) return;
@@ -493,6 +493,16 @@ __global__ void __launch_bounds__(256) combine_kernel(int n, int nd, int k, int 
                 acc[2 * q + 1] += f.y;
             }
         }
+        if (ys) {  // shared experts, computed at the source: added last
+            const uint4 u = __ldg(reinterpret_cast<const uint4*>(ys + (long)t * D) + v);
+            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const float2 f = __bfloat1622float2(h[q]);
+                acc[2 * q] += f.x;
+                acc[2 * q + 1] += f.y;
+            }
+        }
         uint4 o;
         o.x = pack_bf16(acc[0], acc[1]);
         o.y = pack_bf16(acc[2], acc[3]);
@@ -510,7 +520,7 @@ __global__ void __launch_bounds__(256) combine_kernel(int n, int nd, int k, int 
 __global__ void __launch_bounds__(256) combine_fused_kernel(int n, int nd, int k, int P, int dedup, int D,
                                                             const uint64_t* mask, const int32_t* tok_row,
                                                             const int32_t* row_epd, const __nv_bfloat16* Y,
-                                                            __nv_bfloat16* out) {
+                                                            const __nv_bfloat16* ys, __nv_bfloat16* out) {
     const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (t >= n) return;
@@ -559,11 +569,55 @@ __global__ void __launch_bounds__(256) combine_fused_kernel(int n, int nd, int k
         acc.y += __bfloat162float(__float2bfloat16(dev.y));
         acc.z += __bfloat162float(__float2bfloat16(dev.z));
         acc.w += __bfloat162float(__float2bfloat16(dev.w));
+        if (ys) {  // shared experts (source device), added last
+            const float4 y = ld_bf16x4(ys + (long)t * D + 4 * v);
+            acc.x += y.x; acc.y += y.y; acc.z += y.z; acc.w += y.w;
+        }
         uint2 o;
         o.x = pack_bf16(acc.x, acc.y);
         o.y = pack_bf16(acc.z, acc.w);
         reinterpret_cast<uint2*>(out + (long)t * D)[v] = o;
     }
+}
+
+// Shared-expert gate (Qwen's shared_expert_gate): g_t = sigmoid(x[t] . gate),
+// one warp per token, fp32 accumulation.  Rows n..n_pad of the padded
+// GEMM m-tile get 0 so the padded rows stay finite.
+__global__ void __launch_bounds__(256) shared_gate_kernel(int n, int n_pad, int D, const __nv_bfloat16* x,
+                                                          const __nv_bfloat16* gate, float* g) {
+    const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (t >= n_pad) return;
+    if (t >= n) {
+        if (lane == 0) g[t] = 0.f;
+        return;
+    }
+    float acc = 0.f;
+    for (int v = lane; v < D / 8; v += 32) {
+        const uint4 a = __ldg(reinterpret_cast<const uint4*>(x + (long)t * D) + v);
+        const uint4 b = __ldg(reinterpret_cast<const uint4*>(gate) + v);
+        const __nv_bfloat162* ha = reinterpret_cast<const __nv_bfloat162*>(&a);
+        const __nv_bfloat162* hb = reinterpret_cast<const __nv_bfloat162*>(&b);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float2 fa = __bfloat1622float2(ha[q]), fb = __bfloat1622float2(hb[q]);
+            acc += fa.x * fb.x + fa.y * fb.y;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) g[t] = 1.0f / (1.0f + __expf(-acc));
+}
+
+__global__ void fill_f32_kernel(float* p, int n, int n_pad, float v) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n_pad) p[i] = i < n ? v : 0.f;
+}
+
+__global__ void set_group_kernel(int* g, int nmb) {
+    g[0] = 0;
+    g[1] = nmb;
+    g[2] = 0;
 }
 
 __global__ void extract_cindex_kernel(int R_max, const int* R_total, int P, const int32_t* row_dev,
@@ -1079,18 +1133,29 @@ void launch_partial_combine(int R_max, const int* R_total, int P, int D, const i
 }
 
 void launch_combine(int n, int nd, int k, int dedup, int D, const uint64_t* mask, const int32_t* tok_row,
-                    const __nv_bfloat16* ret, __nv_bfloat16* out, cudaStream_t st) {
+                    const __nv_bfloat16* ret, const __nv_bfloat16* ys, __nv_bfloat16* out, cudaStream_t st) {
     if (!n) return;
-    combine_kernel<<<(n + 7) / 8, 256, 0, st>>>(n, nd, k, dedup, D, mask, tok_row, ret, out);
+    combine_kernel<<<(n + 7) / 8, 256, 0, st>>>(n, nd, k, dedup, D, mask, tok_row, ret, ys, out);
     count_launch();
 }
 
 void launch_combine_fused(int n, int nd, int k, int P, int dedup, int D, const uint64_t* mask,
                           const int32_t* tok_row, const int32_t* row_epd, const __nv_bfloat16* Y,
-                          __nv_bfloat16* out, cudaStream_t st) {
+                          const __nv_bfloat16* ys, __nv_bfloat16* out, cudaStream_t st) {
     if (!n) return;
-    combine_fused_kernel<<<(n + 7) / 8, 256, 0, st>>>(n, nd, k, P, dedup, D, mask, tok_row, row_epd, Y, out);
+    combine_fused_kernel<<<(n + 7) / 8, 256, 0, st>>>(n, nd, k, P, dedup, D, mask, tok_row, row_epd, Y, ys, out);
     count_launch();
+}
+
+void launch_shared_gate(int n, int n_pad, int D, const __nv_bfloat16* x, const __nv_bfloat16* gate, float* g,
+                        int* grp, cudaStream_t st) {
+    if (!n_pad) return;
+    if (gate)
+        shared_gate_kernel<<<(n_pad + 7) / 8, 256, 0, st>>>(n, n_pad, D, x, gate, g);
+    else
+        fill_f32_kernel<<<(n_pad + 255) / 256, 256, 0, st>>>(g, n, n_pad, 1.0f);
+    set_group_kernel<<<1, 1, 0, st>>>(grp, n_pad / kBM);
+    count_launch(2);
 }
 
 void launch_gather_token_rows(int Q_max, const int* q_total, const int32_t* epd_src, const int32_t* in_tok,

@@ -253,6 +253,48 @@ def test_forward_swiglu(ne, k, nd, dm, dh, n):
     assert rel_err(out.double().cpu().numpy(), want) <= TOL
 
 
+def make_shared(ns, dm, dh, gated, seed=0, gate=True):
+    rng = np.random.default_rng(seed + 100)
+    s1 = bf16_round(rng.uniform(-1, 1, (ns, dm, dh)) / np.sqrt(dm))
+    s3 = bf16_round(rng.uniform(-1, 1, (ns, dm, dh)) / np.sqrt(dm)) if gated else None
+    s2 = bf16_round(rng.uniform(-1, 1, (ns, dh, dm)) / np.sqrt(dh * ns))
+    sg = bf16_round(rng.uniform(-1, 1, dm) * (2.0 / np.sqrt(dm))) if gate else None
+    return s1, s2, s3, sg
+
+
+@pytest.mark.parametrize("ne,k,nd,dm,dh,act,n,ns,dhs,gate", [
+    (8, 2, 2, 128, 128, "swiglu", 300, 2, 128, False),   # DeepSeek-style: 2 shared experts, no gate
+    (16, 4, 4, 128, 256, "swiglu", 513, 1, 512, True),   # Qwen-style: one wide shared expert + sigmoid gate
+    (8, 2, 1, 64, 128, "silu", 100, 1, 64, True),        # 2-matrix experts
+    (8, 2, 2, 256, 128, "relu", 1, 3, 96, False),        # one token, 3 shared experts of width 96
+])
+def test_forward_shared_experts(ne, k, nd, dm, dh, act, n, ns, dhs, gate):
+    """Routed layer + shared experts (DeepSeek / Qwen extension) against the
+    oracle: forward_given_routing restatement + orc_shared_experts."""
+    gated = act == "swiglu"
+    x, g, w1, w2, w3 = make_layer_inputs(ne + n + ns, n, dm, dh, ne, gated=gated)
+    ids, w = random_routing(n, ne, k, np.random.default_rng(ns))
+    w = w.astype(np.float32).astype(np.float64)
+    plist = _placement(ne, nd, "shuffled", seed=1)
+    s1, s2, s3, sg = make_shared(ns, dm, dhs, gated, seed=n, gate=gate)
+    a = "silu" if gated else act
+    want, _ = O.Port().forward_given_routing(x, ids, w, w1, w2, plist, None, act=a, single=False, w3=w3)
+    want = O.Port().shared_experts(x, s1, s2, w3=s3, gate=sg, act=a, out=want)
+    layer = occ.ExpertParallelLayer(occ.MoEConfig(ne, k, nd, dm, dh, activation=act),
+                                    occ.Placement([list(p) for p in plist]))
+    layer.load_experts(cuda(w1, torch.bfloat16), cuda(w2, torch.bfloat16), cuda(w3, torch.bfloat16) if gated else None)
+    layer.load_shared_experts(cuda(s1, torch.bfloat16), cuda(s2, torch.bfloat16),
+                              cuda(s3, torch.bfloat16) if gated else None,
+                              cuda(sg, torch.bfloat16) if gate else None)
+    out = layer.forward_given_routing(cuda(x, torch.bfloat16), cuda(ids), cuda(w, torch.float32))
+    assert rel_err(out.double().cpu().numpy(), want) <= TOL
+    # detaching the shared experts gives the routed layer back
+    layer.load_shared_experts(cuda(s1[:0], torch.bfloat16), cuda(s2[:0], torch.bfloat16))
+    plain, _ = O.Port().forward_given_routing(x, ids, w, w1, w2, plist, None, act=a, single=False, w3=w3)
+    out2 = layer.forward_given_routing(cuda(x, torch.bfloat16), cuda(ids), cuda(w, torch.float32))
+    assert rel_err(out2.double().cpu().numpy(), plain) <= TOL
+
+
 def test_forward_bit_identical_reruns():
     # test_pipeline.cpp:490-509: deterministic (no atomics on the data path)
     ne, k, nd, dm, dh, n = 16, 4, 4, 128, 256, 1000
@@ -418,10 +460,11 @@ def test_forward_host_pipeline_matches_device(chunks):
 
 # ------------------------------------------- world_size > 1 (loopback) -----
 
-@pytest.mark.parametrize("nd,ne,k,act,dedup", [(2, 8, 2, "silu", True), (4, 16, 4, "silu", True),
-                                               (8, 64, 8, "relu", True), (4, 8, 3, "identity", False),
-                                               (2, 8, 2, "swiglu", True)])
-def test_multi_rank_forward_loopback(nd, ne, k, act, dedup):
+@pytest.mark.parametrize("nd,ne,k,act,dedup,shared", [(2, 8, 2, "silu", True, 0), (4, 16, 4, "silu", True, 0),
+                                                      (8, 64, 8, "relu", True, 0), (4, 8, 3, "identity", False, 0),
+                                                      (2, 8, 2, "swiglu", True, 0), (4, 16, 4, "swiglu", True, 2),
+                                                      (2, 8, 2, "relu", False, 1)])
+def test_multi_rank_forward_loopback(nd, ne, k, act, dedup, shared):
     """The world_size == N_d code path (per-rank plan, count all-gather, two
     variable all-to-alls, per-device BRIM1 + GEMMs + partial combine,
     combine) with the ranks as threads on one GPU, against the reference's
@@ -442,6 +485,9 @@ def test_multi_rank_forward_loopback(nd, ne, k, act, dedup):
     else:
         want, rep = ref().forward_given_routing(x, ids, w, w1, w2, plist, src, act=act, single=False,
                                                 bytes_per_scalar=2)
+    if shared:  # shared experts at every source (extension), Qwen-style gate
+        s1, s2, s3, sg = make_shared(shared, dm, 128, gated, seed=nd)
+        want = O.Port().shared_experts(x, s1, s2, w3=s3, gate=sg, act="silu" if gated else act, out=want)
     outs = [None] * nd
     errs = []
     starts = np.concatenate([[0], np.cumsum(n_per)])
@@ -456,6 +502,9 @@ def test_multi_rank_forward_loopback(nd, ne, k, act, dedup):
                 loc = plist[r]
                 layer.load_experts(cuda(w1[loc], torch.bfloat16), cuda(w2[loc], torch.bfloat16),
                                    cuda(w3[loc], torch.bfloat16) if gated else None)
+                if shared:
+                    layer.load_shared_experts(cuda(s1, torch.bfloat16), cuda(s2, torch.bfloat16),
+                                              cuda(s3, torch.bfloat16) if gated else None, cuda(sg, torch.bfloat16))
                 layer.comm_init_loopback(int(key))
                 a, b = starts[r], starts[r + 1]
                 out = layer.forward_given_routing(cuda(x[a:b], torch.bfloat16), cuda(ids[a:b]),

@@ -168,3 +168,31 @@ def test_capacity_error_matches_reference():
         with pytest.raises(O.OracleError) as ei:
             be.prune_routing(s, ids, w, plist, "router", 1, renormalize=False)
         assert ei.value.code == 5
+
+
+@pytest.mark.parametrize("gated,gate,act", [(True, False, "silu"), (True, True, "silu"), (False, True, "relu"),
+                                            (False, False, "identity")])
+def test_shared_experts_oracle_vs_torch(gated, gate, act):
+    """orc_shared_experts (the DeepSeek/Qwen shared-expert extension, not in
+    the reference) pinned against an independent torch fp64 computation."""
+    import torch
+    rng = np.random.default_rng(5)
+    n, dm, dh, ns = 37, 24, 40, 2
+    x = rng.uniform(-1, 1, (n, dm))
+    w1 = rng.uniform(-1, 1, (ns, dm, dh)) / np.sqrt(dm)
+    w3 = rng.uniform(-1, 1, (ns, dm, dh)) / np.sqrt(dm) if gated else None
+    w2 = rng.uniform(-1, 1, (ns, dh, dm)) / np.sqrt(dh)
+    g = rng.uniform(-1, 1, dm) if gate else None
+    base = rng.uniform(-1, 1, (n, dm))
+    got = P.shared_experts(x, w1, w2, w3=w3, gate=g, act=act, out=base)
+    T = torch.from_numpy
+    acc = torch.zeros(n, dm, dtype=torch.float64)
+    fn = {"silu": torch.nn.functional.silu, "relu": torch.relu, "identity": lambda v: v}[act]
+    for s in range(ns):
+        a = T(x) @ T(w1[s])
+        h = torch.nn.functional.silu(a) * (T(x) @ T(w3[s])) if gated else fn(a)
+        acc += h @ T(w2[s])
+    if gate:
+        acc *= torch.sigmoid(T(x) @ T(g))[:, None]
+    want = base + acc.numpy()
+    assert np.max(np.abs(got - want)) / np.max(np.abs(want)) < 1e-12
