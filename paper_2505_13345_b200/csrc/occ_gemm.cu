@@ -80,6 +80,7 @@ struct Params {
     const __nv_bfloat16* pre_a;  // backward epilogue inputs
     const __nv_bfloat16* pre_b;
     float* gw_part;
+    int hint_a, hint_b;  // L2 policy of the A / B loads (0 = none)
 };
 
 // Forward / data-gradient tiles: expert group by group, bands of `band`
@@ -116,7 +117,7 @@ __device__ __forceinline__ float act_f(float v, int act) {
 }
 __device__ __forceinline__ float act_grad(float v, int act) {  // backward.cpp:11-20
     if (act == 1) {
-        const float s = 1.0f / (1.0f + __expf(-v));
+        const float s = sigmoid_fast(v);
         return s * (1.0f + v * (1.0f - s));
     }
     if (act == 2) return v > 0.f ? 1.f : 0.f;
@@ -215,6 +216,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
+            const uint64_t pol_a = l2_policy(p.hint_a), pol_b = l2_policy(p.hint_b);
             for (int tile = cid; tile < num_tiles; tile += ncl) {
                 int kb0 = 0, KB = KB_fwd, ax = 0, ay = 0, bx = 0, by = 0;
                 if constexpr (WGRAD) {
@@ -243,8 +245,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                         tma_load_2d_cg2(b_dst, &tmB, lbar, bx, k);
                         tma_load_2d_cg2(b_dst + B_BYTES / 2, &tmB, lbar, bx + 64, k);
                     } else {
-                        tma_load_2d_cg2(a_dst, &tmA, lbar, kb * BK, ay);
-                        tma_load_2d_cg2(b_dst, &tmB, lbar, kb * BK, by);
+                        if (p.hint_a) tma_load_2d_cg2_hint(a_dst, &tmA, lbar, kb * BK, ay, pol_a);
+                        else tma_load_2d_cg2(a_dst, &tmA, lbar, kb * BK, ay);
+                        if (p.hint_b) tma_load_2d_cg2_hint(b_dst, &tmB, lbar, kb * BK, by, pol_b);
+                        else tma_load_2d_cg2(b_dst, &tmB, lbar, kb * BK, by);
                     }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
@@ -368,7 +372,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #pragma unroll
                             for (int i = 0; i < 32; ++i) {
                                 const float gm = i < nv ? __uint_as_float(v[i]) : 0.f;
-                                const float s = 1.0f / (1.0f + __expf(-a[i]));
+                                const float s = sigmoid_fast(a[i]);
                                 const float sa = a[i] * s;
                                 gw += sa * b[i] * gm;
                                 const float gh = gm * wr;
@@ -516,6 +520,12 @@ void launch_grouped_gemm(EpiMode mode, const GemmArgs& a, int num_sms, cudaStrea
         return e ? atoi(e) : 0;
     }();
     if (band_override > 0 && !(mode == EPI_WGRAD)) p.band = band_override;
+    static const int hint_env = [] {  // L2 policy experiments: OCC_GEMM_HINT = 10 * a + b
+        const char* e = getenv("OCC_GEMM_HINT");
+        return e ? atoi(e) : 0;
+    }();
+    p.hint_a = hint_env / 10;
+    p.hint_b = hint_env % 10;
     int grid = 2 * a.max_tiles < num_sms ? 2 * a.max_tiles : num_sms;
     grid &= ~1;  // CTA pairs
     if (grid <= 0) return;
