@@ -140,7 +140,7 @@ struct occ_handle {
     size_t R_max = 0, Q_max = 0, max_mblk = 0;
     int last_n = 0;
     bool have_forward = false;
-    TmapBox tmA1, tmA2, tmB1, tmB2, tmRX, tmRG;
+    TmapBox tmA1, tmA2, tmB1, tmB2, tmRX, tmRG, tmC1, tmC2;
     DispatchOffsets dofs{};
     ComputeOffsets cofs{};
     int* d_tok_base = nullptr;
@@ -174,7 +174,7 @@ struct occ_handle {
     DevBuf<float> sw;
     DevBuf<int> sh_grp;
     size_t sh_cap = 0;
-    TmapBox tmBS1, tmBS2, tmAS1, tmAS2;
+    TmapBox tmBS1, tmBS2, tmAS1, tmAS2, tmCS1, tmCS2;
     cudaStream_t s_aux = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
@@ -364,7 +364,9 @@ occ_status ensure_recv(occ_handle* h, size_t R, size_t epd_bound) {
         h->max_mblk = Q / kBM;
         h->bwd_tmaps_q = -1;
         if (!make_tmap_2d(h->tmA1.bytes, h->x_epd.p, D, h->Q_max, 64, kBM / 2) ||
-            !make_tmap_2d(h->tmA2.bytes, h->hbuf.p, F, h->Q_max, 64, kBM / 2))
+            !make_tmap_2d(h->tmA2.bytes, h->hbuf.p, F, h->Q_max, 64, kBM / 2) ||
+            !make_tmap_out(h->tmC1.bytes, h->hbuf.p, F, h->Q_max) ||
+            !make_tmap_out(h->tmC2.bytes, h->y16.p, D, h->Q_max))
             return fail(OCC_ERR_CUDA, "cuTensorMapEncodeTiled failed (A operands)");
     }
     return OCC_OK;
@@ -438,6 +440,7 @@ void launch_gemm1(occ_handle* h, int ngroups, cudaStream_t st) {
     GemmArgs g;
     g.tmap_a = h->tmA1.bytes;
     g.tmap_b = h->tmB1.bytes;
+    g.tmap_c = h->tmC1.bytes;
     g.K = h->D;
     g.N = h->F;
     g.b_rows_per_e = h->n1rows;
@@ -460,6 +463,7 @@ void launch_gemm2(occ_handle* h, int ngroups, cudaStream_t st) {
     GemmArgs g;
     g.tmap_a = h->tmA2.bytes;
     g.tmap_b = h->tmB2.bytes;
+    g.tmap_c = h->tmC2.bytes;
     g.K = h->F;
     g.N = h->D;
     g.b_rows_per_e = h->D;
@@ -485,7 +489,8 @@ occ_status run_shared(occ_handle* h, const __nv_bfloat16* x, int n, cudaStream_t
         CUDA_TRY(h->ys.ensure(n_pad * D));
         CUDA_TRY(h->sw.ensure(n_pad));
         h->sh_cap = n_pad;
-        if (!make_tmap_2d(h->tmAS2.bytes, h->hs.p, Fs, n_pad, 64, kBM / 2))
+        if (!make_tmap_2d(h->tmAS2.bytes, h->hs.p, Fs, n_pad, 64, kBM / 2) ||
+            !make_tmap_out(h->tmCS1.bytes, h->hs.p, Fs, n_pad) || !make_tmap_out(h->tmCS2.bytes, h->ys.p, D, n_pad))
             return fail(OCC_ERR_CUDA, "cuTensorMapEncodeTiled failed (shared h)");
     }
     if (!make_tmap_2d(h->tmAS1.bytes, x, D, (uint64_t)n, 64, kBM / 2))
@@ -495,6 +500,7 @@ occ_status run_shared(occ_handle* h, const __nv_bfloat16* x, int n, cudaStream_t
     GemmArgs g;
     g.tmap_a = h->tmAS1.bytes;
     g.tmap_b = h->tmBS1.bytes;
+    g.tmap_c = h->tmCS1.bytes;
     g.K = D;
     g.N = Fs;
     g.b_rows_per_e = h->sh_rows;
@@ -510,6 +516,7 @@ occ_status run_shared(occ_handle* h, const __nv_bfloat16* x, int n, cudaStream_t
     GemmArgs g2;
     g2.tmap_a = h->tmAS2.bytes;
     g2.tmap_b = h->tmBS2.bytes;
+    g2.tmap_c = h->tmCS2.bytes;
     g2.K = Fs;
     g2.N = D;
     g2.b_rows_per_e = D;
@@ -1120,7 +1127,7 @@ static occ_status ensure_bwd(occ_handle* h) {
     const int NBf = (F + 255) / 256;
     CUDA_TRY(h->g_epd.ensure(Q * D));
     CUDA_TRY(h->gpre.ensure(Q * kw));
-    CUDA_TRY(h->gw_part.ensure(Q * NBf));
+    CUDA_TRY(h->gw_part.ensure(Q * NBf * 2));  // per (row, n-tile, epilogue column half)
     CUDA_TRY(h->ybuf.ensure(Q * D));
     if (h->bwd_tmaps_q != (int)Q) {
         if (!make_tmap_2d(h->tmG_k.bytes, h->g_epd.p, D, Q, 64, 128) ||
@@ -1223,7 +1230,7 @@ occ_status occ_backward(occ_handle* h, const void* upstream, float* g_x, float* 
     launch_grouped_gemm(EPI_WGRAD, w1, h->num_sms, st);
     // dispatch adjoint: sum each token's rows (device ascending), fp32
     launch_combine_grad(n, nd, k, P, h->cfg.dedup, D, h->mask.p, h->tok_row.p, h->row_epd.p, h->ybuf.p, g_x, st);
-    launch_gw_scatter((int)h->Q_max, h->d_q_total, (F + 255) / 256, h->gw_part.p, h->epd_src.p, h->in_tok.p,
+    launch_gw_scatter((int)h->Q_max, h->d_q_total, 2 * ((F + 255) / 256), h->gw_part.p, h->epd_src.p, h->in_tok.p,
                       h->epd_j.p, k, g_weights, st);
     CUDA_TRY(cudaGetLastError());
     if (h->validate) CUDA_TRY(cudaStreamSynchronize(st));

@@ -45,8 +45,13 @@ constexpr int BM = 128;               // rows per CTA (pair tile: 256)
 constexpr int BN = 256, BK = 64, STAGES = 6;
 constexpr int A_BYTES = BM * BK * 2;  // 16 KB
 constexpr int B_BYTES = (BN / 2) * BK * 2;  // 16 KB: this CTA's half of the B tile
-constexpr int SMEM_BYTES = STAGES * (A_BYTES + B_BYTES) + 256;
-constexpr int THREADS = 192;
+// Epilogue staging for TMA stores: per epilogue warp two 32-row x 32-column
+// bf16 buffers (2 KB each, 64-byte swizzle) = 16 KB.
+constexpr int EPI_WARPS = 8;  // two per TMEM lane quarter, each on half of the tile's columns
+constexpr int STG_BYTES = 2048;
+constexpr int EPI_STAGE_BYTES = EPI_WARPS * STG_BYTES;
+constexpr int SMEM_BYTES = STAGES * (A_BYTES + B_BYTES) + EPI_STAGE_BYTES + 256;
+constexpr int THREADS = 64 + 32 * 8;  // producer + MMA + EPI_WARPS epilogue warps
 constexpr int MAX_GROUPS = 256;
 static_assert(kBM == 2 * BM, "Epd segments are padded to the pair tile");
 
@@ -81,6 +86,8 @@ struct Params {
     const __nv_bfloat16* pre_b;
     float* gw_part;
     int hint_a, hint_b;  // L2 policy of the A / B loads (0 = none)
+    int nostore;         // experiment: skip the bf16 output stores (timing only)
+    int tma_out;         // bf16 forward outputs leave through smem + TMA stores (tmC)
 };
 
 // Forward / data-gradient tiles: expert group by group, bands of `band`
@@ -152,12 +159,14 @@ __device__ __forceinline__ void store_bf16x32(__nv_bfloat16* p, const float (&h)
 
 template <int EPI, bool WGRAD>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
-    grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Params p) {
+    grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                        const __grid_constant__ CUtensorMap tmC, Params p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
     uint8_t* sB = smem + STAGES * A_BYTES;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+    uint8_t* sC = sB + STAGES * B_BYTES;  // epilogue staging (1024-aligned)
+    uint64_t* full = reinterpret_cast<uint64_t*>(sC + EPI_STAGE_BYTES);
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
@@ -191,13 +200,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
+        if (p.tma_out) tma_prefetch_desc(&tmC);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);   // leader: one expect_tx arrival + both CTAs' bytes
             mbar_init(&empty[s], 1);  // one multicast commit per phase
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 8);  // leader: 4 epilogue warps x 2 CTAs
+            mbar_init(&tempty[a], 2 * EPI_WARPS);  // leader: epilogue warps of both CTAs
         }
         fence_barrier_init();
     }
@@ -296,7 +306,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         }
     } else {
         // ------------------------------------------------ epilogue
-        const int q = warp & 3;  // TMEM lane quarter accessible to this warp
+        const int q = warp & 3;           // TMEM lane quarter accessible to this warp
+        const int hsel = (warp - 2) >> 2;  // which half of the tile's 32-column chunks
+        uint32_t stg_n = 0;      // TMA-store staging buffer counter
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int tile = cid; tile < num_tiles; tile += ncl) {
@@ -310,7 +322,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 const int m = mt * 2 * BM + rank * BM + q * 32 + lane;
                 const long ebase = (long)s_gw[g] * p.out_estride;
 #pragma unroll 1
-                for (int c = 0; c < BN / 32; ++c) {
+                for (int c = hsel * (BN / 64); c < (hsel + 1) * (BN / 64); ++c) {
                     uint32_t v[32];
                     tmem_ld32(tbase + c * 32, v);
                     tmem_ld_wait();
@@ -336,7 +348,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 if constexpr (EPI == EPI_F32) {
                     float* out = reinterpret_cast<float*>(p.out) + row * p.ldo;
 #pragma unroll 1
-                    for (int c = 0; c < BN / 32; ++c) {
+                    for (int c = hsel * (BN / 64); c < (hsel + 1) * (BN / 64); ++c) {
                         uint32_t v[32];
                         tmem_ld32(tbase + c * 32, v);
                         tmem_ld_wait();
@@ -357,7 +369,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                     float gw = 0.f;
                     __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out) + row * p.ldo;
 #pragma unroll 1
-                    for (int c = 0; c < BN / 32; ++c) {
+                    for (int c = hsel * (BN / 64); c < (hsel + 1) * (BN / 64); ++c) {
                         const int col0 = nb * BN + c * 32;
                         uint32_t v[32];
                         tmem_ld32(tbase + c * 32, v);
@@ -391,14 +403,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                             store_bf16x32(out + col0, r0, F - col0);
                         }
                     }
-                    p.gw_part[row * NB + nb] = gw;
+                    p.gw_part[(row * NB + nb) * 2 + hsel] = gw;
                 } else {
                     const float wr = p.row_w ? p.row_w[row] : 1.0f;
                     __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out) + row * p.ldo;
                     constexpr int NCH = EPI == EPI_SWIGLU_BF16 ? 4 : BN / 32;
                     const int ncol = EPI == EPI_SWIGLU_BF16 ? 128 : BN;
 #pragma unroll 1
-                    for (int c = 0; c < NCH; ++c) {
+                    for (int c = hsel * (NCH / 2); c < (hsel + 1) * (NCH / 2); ++c) {
                         uint32_t v[32];
                         float h[32];
                         const int col0 = nb * ncol + c * 32;
@@ -431,7 +443,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #pragma unroll
                             for (int i = 0; i < 32; ++i) h[i] = act_f(__uint_as_float(v[i]), p.act) * wr;
                         }
-                        if (col0 < p.N) store_bf16x32(out + col0, h, p.N - col0);
+                        if (col0 < p.N && !p.nostore) {
+                            if (p.tma_out) {
+                                // coalesced: stage the warp's 32 x 32 bf16 block in smem
+                                // (64-byte swizzle: 16-byte chunk u of row r at u ^ ((r >> 1) & 3)),
+                                // one TMA store per block; two buffers per warp rotate
+                                uint8_t* stg = sC + (warp - 2) * STG_BYTES;
+                                if (lane == 0) bulk_wait_read<0>();
+                                __syncwarp();
+#pragma unroll
+                                for (int u = 0; u < 4; ++u) {
+                                    uint4 o;
+                                    o.x = pack_bf16(h[8 * u + 0], h[8 * u + 1]);
+                                    o.y = pack_bf16(h[8 * u + 2], h[8 * u + 3]);
+                                    o.z = pack_bf16(h[8 * u + 4], h[8 * u + 5]);
+                                    o.w = pack_bf16(h[8 * u + 6], h[8 * u + 7]);
+                                    *reinterpret_cast<uint4*>(stg + lane * 64 + ((u ^ ((lane >> 1) & 3)) << 4)) = o;
+                                }
+                                fence_proxy_async();
+                                __syncwarp();
+                                if (lane == 0) {
+                                    tma_store_2d(&tmC, stg, col0, (int)(row - lane));
+                                    bulk_commit();
+                                }
+                                ++stg_n;
+                            } else {
+                                store_bf16x32(out + col0, h, p.N - col0);
+                            }
+                        }
                     }
                 }
             }
@@ -440,6 +479,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             if (lane == 0) mbar_arrive_cluster(smem_u32(&tempty[acc]) & kPeerBitMask);
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
     tc_fence_before();
     cluster_sync();
@@ -466,10 +506,11 @@ EncodeTiledFn get_encode() {
 }
 
 template <int EPI, bool WGRAD>
-void launch_one(int grid, const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, cudaStream_t st) {
+void launch_one(int grid, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const Params& p,
+                cudaStream_t st) {
     const int smem = SMEM_BYTES + 1024;
     cudaFuncSetAttribute(grouped_gemm_kernel<EPI, WGRAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    grouped_gemm_kernel<EPI, WGRAD><<<grid, THREADS, smem, st>>>(ta, tb, p);
+    grouped_gemm_kernel<EPI, WGRAD><<<grid, THREADS, smem, st>>>(ta, tb, tc, p);
 }
 
 }  // namespace
@@ -477,7 +518,7 @@ void launch_one(int grid, const CUtensorMap& ta, const CUtensorMap& tb, const Pa
 // Row-major bf16 matrix [outer, inner], 128-byte swizzled boxes of
 // box_inner (=64) x box_outer elements.  OOB reads are zero-filled.
 bool make_tmap_2d(void* tmap, const void* base, uint64_t inner, uint64_t outer, uint32_t box_inner,
-                  uint32_t box_outer) {
+                  uint32_t box_outer, int swizzle_bytes) {
     EncodeTiledFn enc = get_encode();
     if (!enc) return false;
     cuuint64_t dims[2] = {inner, outer};
@@ -485,7 +526,8 @@ bool make_tmap_2d(void* tmap, const void* base, uint64_t inner, uint64_t outer, 
     cuuint32_t box[2] = {box_inner, box_outer};
     cuuint32_t estr[2] = {1, 1};
     return enc(reinterpret_cast<CUtensorMap*>(tmap), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base),
-               dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+               dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -515,6 +557,9 @@ void launch_grouped_gemm(EpiMode mode, const GemmArgs& a, int num_sms, cudaStrea
     p.gw_part = a.gw_part;
     const CUtensorMap& ta = *reinterpret_cast<const CUtensorMap*>(a.tmap_a);
     const CUtensorMap& tb = *reinterpret_cast<const CUtensorMap*>(a.tmap_b);
+    static const int tma_store_env = getenv("OCC_GEMM_TMASTORE") ? atoi(getenv("OCC_GEMM_TMASTORE")) : 1;
+    p.tma_out = tma_store_env && a.tmap_c != nullptr && (mode == EPI_ACT_BF16 || mode == EPI_SWIGLU_BF16);
+    const CUtensorMap& tc = p.tma_out ? *reinterpret_cast<const CUtensorMap*>(a.tmap_c) : ta;
     static const int band_override = [] {  // raster experiments (profiles/), not a product knob
         const char* e = getenv("OCC_GEMM_BAND");
         return e ? atoi(e) : 0;
@@ -526,16 +571,18 @@ void launch_grouped_gemm(EpiMode mode, const GemmArgs& a, int num_sms, cudaStrea
     }();
     p.hint_a = hint_env / 10;
     p.hint_b = hint_env % 10;
+    static const int nostore_env = getenv("OCC_GEMM_NOSTORE") ? atoi(getenv("OCC_GEMM_NOSTORE")) : 0;
+    p.nostore = nostore_env;
     int grid = 2 * a.max_tiles < num_sms ? 2 * a.max_tiles : num_sms;
     grid &= ~1;  // CTA pairs
     if (grid <= 0) return;
     switch (mode) {
-        case EPI_ACT_BF16: launch_one<EPI_ACT_BF16, false>(grid, ta, tb, p, st); break;
-        case EPI_SWIGLU_BF16: launch_one<EPI_SWIGLU_BF16, false>(grid, ta, tb, p, st); break;
-        case EPI_F32: launch_one<EPI_F32, false>(grid, ta, tb, p, st); break;
-        case EPI_BWD_ACT: launch_one<EPI_BWD_ACT, false>(grid, ta, tb, p, st); break;
-        case EPI_BWD_SWIGLU: launch_one<EPI_BWD_SWIGLU, false>(grid, ta, tb, p, st); break;
-        case EPI_WGRAD: launch_one<EPI_F32, true>(grid, ta, tb, p, st); break;
+        case EPI_ACT_BF16: launch_one<EPI_ACT_BF16, false>(grid, ta, tb, tc, p, st); break;
+        case EPI_SWIGLU_BF16: launch_one<EPI_SWIGLU_BF16, false>(grid, ta, tb, tc, p, st); break;
+        case EPI_F32: launch_one<EPI_F32, false>(grid, ta, tb, tc, p, st); break;
+        case EPI_BWD_ACT: launch_one<EPI_BWD_ACT, false>(grid, ta, tb, tc, p, st); break;
+        case EPI_BWD_SWIGLU: launch_one<EPI_BWD_SWIGLU, false>(grid, ta, tb, tc, p, st); break;
+        case EPI_WGRAD: launch_one<EPI_F32, true>(grid, ta, tb, tc, p, st); break;
     }
     count_launch();
 }

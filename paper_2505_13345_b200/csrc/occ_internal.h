@@ -223,6 +223,7 @@ enum EpiMode {
 struct GemmArgs {
     const void* tmap_a = nullptr;  // CUtensorMap* (host object, passed by value to the kernel)
     const void* tmap_b = nullptr;
+    const void* tmap_c = nullptr;  // bf16 forward output [rows, ldo] (box 32 x 32, 64 B swizzle): TMA-store epilogue
     int K = 0;                     // reduction dim (forward / data gradient)
     int N = 0;                     // output columns per expert (GEMM-1 SwiGLU: F; B rows per expert = 2F)
     int b_rows_per_e = 0;          // rows of B per expert in the stacked K-major weight matrix
@@ -249,6 +250,10 @@ struct GemmArgs {
 };
 void launch_grouped_gemm(EpiMode mode, const GemmArgs& a, int num_sms, cudaStream_t st);
 bool make_tmap_2d(void* tmap, const void* base, uint64_t inner, uint64_t outer, uint32_t box_inner,
-                  uint32_t box_outer);
+                  uint32_t box_outer, int swizzle_bytes = 128);
+// Output map of the TMA-store epilogue: bf16 [outer, inner] row-major, 32 x 32 boxes.
+inline bool make_tmap_out(void* tmap, const void* base, uint64_t inner, uint64_t outer) {
+    return make_tmap_2d(tmap, base, inner, outer, 32, 32, 64);
+}
 
 }  // namespace occ
