@@ -55,11 +55,30 @@ def run(name, E, k, D, F, n, routings, steps=10, reps=4):
                     acc[r].setdefault(kk, []).append(v)
     f1 = 2.0 * n * k * D * 2 * F
     f2 = 2.0 * n * k * F * D
+    # same-box cuBLAS reference: one dense GEMM with the same FLOPs/shape (one weight matrix)
+    cub = {}
+    if os.environ.get("OCC_MICRO_CUBLAS", "1") == "1":
+        a1 = torch.empty((n * k, D), dtype=torch.bfloat16, device=dev).uniform_(-1, 1)
+        b1 = torch.empty((D, 2 * F), dtype=torch.bfloat16, device=dev).uniform_(-1, 1)
+        a2 = torch.empty((n * k, F), dtype=torch.bfloat16, device=dev).uniform_(-1, 1)
+        b2 = torch.empty((F, D), dtype=torch.bfloat16, device=dev).uniform_(-1, 1)
+        for nm, (a, b, fl) in {"cublas1": (a1, b1, f1), "cublas2": (a2, b2, f2)}.items():
+            ts = []
+            for _ in range(reps * steps):
+                flush.zero_()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                torch.matmul(a, b)
+                e1.record()
+                e1.synchronize()
+                ts.append(e0.elapsed_time(e1))
+            cub[nm + "_tflops"] = round(fl / sorted(ts)[len(ts) // 2] / 1e9)
+        del a1, b1, a2, b2
     for r in routings:
         med = {kk: sorted(v)[len(v) // 2] for kk, v in acc[r].items()}
         print(json.dumps({"case": name, "routing": r, "band": os.environ.get("OCC_GEMM_BAND"),
                           "gemm1_ms": med["gemm1"], "gemm2_ms": med["gemm2"],
-                          "gemm1_tflops": f1 / med["gemm1"] / 1e9, "gemm2_tflops": f2 / med["gemm2"] / 1e9,
+                          "gemm1_tflops": f1 / med["gemm1"] / 1e9, "gemm2_tflops": f2 / med["gemm2"] / 1e9, **cub,
                           "other_ms": {kk: round(v, 4) for kk, v in med.items() if not kk.startswith("gemm")}}),
               flush=True)
     del layer
