@@ -140,7 +140,12 @@ struct occ_handle {
     size_t R_max = 0, Q_max = 0, max_mblk = 0;
     int last_n = 0;
     bool have_forward = false;
-    TmapBox tmA1, tmA2, tmB1, tmB2, tmRX, tmRG, tmC1, tmC2;
+    TmapBox tmA1, tmA2, tmB1, tmB2, tmRX, tmRG, tmC1, tmC2, tmAX;
+    // OCC_GEMM_GATHER=1: GEMM-1 reads its A rows straight from the inbox with
+    // TMA tile::gather4 instead of the Epd copy.  Measured 3x slower (32
+    // gather4 per K block saturate the TMA unit: profiles/r01_gemm_micro.md),
+    // so the copy is the default.
+    int gather_a = 0;
     DispatchOffsets dofs{};
     ComputeOffsets cofs{};
     int* d_tok_base = nullptr;
@@ -347,6 +352,8 @@ occ_status ensure_recv(occ_handle* h, size_t R, size_t epd_bound) {
         CUDA_TRY(h->row_epd.ensure(R * P));
         CUDA_TRY(h->ret.ensure(R * D));
         h->R_max = R;
+        if (!make_tmap_2d(h->tmAX.bytes, h->in_x.p, D, std::max<size_t>(R, 1), 64, 1))
+            return fail(OCC_ERR_CUDA, "cuTensorMapEncodeTiled failed (inbox rows)");
     }
     if (h->training) {
         CUDA_TRY(h->save_a.ensure(std::max(Q, h->Q_max) * F));
@@ -436,9 +443,10 @@ occ_status ensure_ws(occ_handle* h, int n) {
 }
 
 // Forward GEMM-1 (scatter + activation + modulation) and GEMM-2 (merge products).
-void launch_gemm1(occ_handle* h, int ngroups, cudaStream_t st) {
+void launch_gemm1(occ_handle* h, int ngroups, cudaStream_t st, bool gathered) {
     GemmArgs g;
-    g.tmap_a = h->tmA1.bytes;
+    g.tmap_a = gathered ? h->tmAX.bytes : h->tmA1.bytes;
+    g.a_rows = gathered ? h->epd_src.p : nullptr;
     g.tmap_b = h->tmB1.bytes;
     g.tmap_c = h->tmC1.bytes;
     g.K = h->D;
@@ -678,11 +686,14 @@ occ_status forward_multi(occ_handle* h, const __nv_bfloat16* x, const int32_t* i
     EmitCompute ec{k, P, r, h->in_ids.p, h->in_w.p, h->d_slot_of.p, h->d_dev_of.p, h->cofs, h->row_epd.p,
                    h->epd_src.p, h->epd_w.p, h->epd_j.p};
     launch_rank_emit_compute(Rm, h->d_R, h->rgroup.p, h->rmask.p, 1, P, ws2, ec, st);
-    // 5. grouped expert FFN
-    mark(h, ST_GATHER, st);
-    launch_gather_rows((int)h->Q_max, h->d_q_total, h->epd_src.p, h->in_x.p, D, h->x_epd.p, st);
+    // 5. grouped expert FFN (A rows gathered from the inbox by TMA, or copied)
+    const bool gathered = h->gather_a && !h->training;
+    if (!gathered) {
+        mark(h, ST_GATHER, st);
+        launch_gather_rows((int)h->Q_max, h->d_q_total, h->epd_src.p, h->in_x.p, D, h->x_epd.p, st);
+    }
     mark(h, ST_GEMM1, st);
-    launch_gemm1(h, P, st);
+    launch_gemm1(h, P, st, gathered);
     mark(h, ST_GEMM2, st);
     launch_gemm2(h, P, st);
     // 6. intra-device partial combine -> bf16 return payload in inbox order
@@ -738,6 +749,7 @@ occ_status occ_create(const occ_config* cfg, const int32_t* placement, int world
     h->world = world_size;
     h->rank = rank;
     h->gated = c.activation == OCC_ACT_SWIGLU;
+    if (const char* e = getenv("OCC_GEMM_GATHER")) h->gather_a = atoi(e);
     h->plist.assign(placement, placement + h->E);
     occ_status s = validate_placement(c, placement, h->dev_of, h->slot_of);
     if (s != OCC_OK) { delete h; return s; }
@@ -1070,11 +1082,16 @@ occ_status occ_forward(occ_handle* h, const void* x, const int32_t* ids, const f
     EmitCompute ec{k, P, 0, h->in_ids.p, h->in_w.p, h->d_slot_of.p, h->d_dev_of.p, h->cofs, h->row_epd.p,
                    h->epd_src.p, h->epd_w.p, h->epd_j.p};
     launch_rank_emit_compute(R_max, R_total, h->rgroup.p, h->rmask.p, G, P, ws, ec, st);
-    // 4. gather + grouped GEMM-1 (activation / SwiGLU, routing weight fused)
-    mark(h, ST_GATHER, st);
-    launch_gather_rows((int)h->Q_max, h->d_q_total, h->epd_src.p, h->in_x.p, D, h->x_epd.p, st);
+    // 4. grouped GEMM-1 (activation / SwiGLU, routing weight fused); its A rows
+    // come straight from the inbox (TMA gather4) unless training needs the
+    // Epd copy for the weight gradient
+    const bool gathered = h->gather_a && !h->training;
+    if (!gathered) {
+        mark(h, ST_GATHER, st);
+        launch_gather_rows((int)h->Q_max, h->d_q_total, h->epd_src.p, h->in_x.p, D, h->x_epd.p, st);
+    }
     mark(h, ST_GEMM1, st);
-    launch_gemm1(h, G * P, st);
+    launch_gemm1(h, G * P, st, gathered);
     mark(h, ST_GEMM2, st);
     // 5. grouped GEMM-2 (per-expert products, fp32)
     launch_gemm2(h, G * P, st);

@@ -67,6 +67,16 @@ OCC_DEV void tma_gather4(void* smem_dst, const void* desc, uint64_t* bar, int x,
         : "memory");
 }
 
+// tile::gather4 into a CTA pair: completion on the leader CTA's barrier.
+OCC_DEV void tma_gather4_cg2(void* smem_dst, const void* desc, uint32_t bar_cluster, int x, int4 rows) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%3, %4, %5, %6, %7}], [%2];" ::"r"(smem_u32(smem_dst)),
+        "l"(reinterpret_cast<uint64_t>(desc)), "r"(bar_cluster), "r"(x), "r"(rows.x), "r"(rows.y), "r"(rows.z),
+        "r"(rows.w)
+        : "memory");
+}
+
 // -------------------------------------------------------- clusters -------
 constexpr uint32_t kPeerBitMask = 0xFEFFFFFFu;  // shared::cluster address of the pair's even CTA
 OCC_DEV uint32_t cluster_ctarank() {

@@ -88,6 +88,8 @@ struct Params {
     int hint_a, hint_b;  // L2 policy of the A / B loads (0 = none)
     int nostore;         // experiment: skip the bf16 output stores (timing only)
     int tma_out;         // bf16 forward outputs leave through smem + TMA stores (tmC)
+    const int* a_rows;   // non-null: A row q of the padded Epd layout is row a_rows[q] of tmA
+                         // (tile::gather4, box 64 x 1; -1 = zero padding row)
 };
 
 // Forward / data-gradient tiles: expert group by group, bands of `band`
@@ -221,7 +223,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     const int KB_fwd = (p.K + BK - 1) / BK;
     const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
 
-    if (warp == 0) {
+    if (warp == 0 && !WGRAD && p.a_rows) {
+        // ------------------------------------------------ TMA producer, gathered A rows:
+        // each lane gathers 4 of the CTA's 128 A rows per K block (tile::gather4
+        // straight from the inbox / token rows: no Epd copy of the activations)
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int tile = cid; tile < num_tiles; tile += ncl) {
+            int mb, nb, wi;
+            tile_coords(tile, s_gmb, s_gw, p.ngroups, NB, p.band, mb, nb, wi);
+            const int q0 = mb * 2 * BM + rank * BM;
+            const int4 rows = __ldg(reinterpret_cast<const int4*>(p.a_rows + q0) + lane);
+            const int by = wi * p.b_rows_per_e + nb * BN + rank * (BN / 2);
+            for (int kb = 0; kb < KB_fwd; ++kb) {
+                if (lane == 0) mbar_wait(&empty[stage], phase ^ 1);
+                __syncwarp();
+                const uint32_t lbar = smem_u32(&full[stage]) & kPeerBitMask;
+                uint8_t* a_dst = sA + stage * A_BYTES;
+                if (lane == 0) {
+                    if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * (A_BYTES + B_BYTES));
+                    tma_load_2d_cg2(sB + stage * B_BYTES, &tmB, lbar, kb * BK, by);
+                }
+                tma_gather4_cg2(a_dst + lane * 512, &tmA, lbar, kb * BK, rows);
+                if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            }
+        }
+    } else if (warp == 0) {
         // ------------------------------------------------ TMA producer
         if (lane == 0) {
             int stage = 0;
@@ -555,6 +582,7 @@ void launch_grouped_gemm(EpiMode mode, const GemmArgs& a, int num_sms, cudaStrea
     p.pre_a = a.pre_a;
     p.pre_b = a.pre_b;
     p.gw_part = a.gw_part;
+    p.a_rows = a.a_rows;
     const CUtensorMap& ta = *reinterpret_cast<const CUtensorMap*>(a.tmap_a);
     const CUtensorMap& tb = *reinterpret_cast<const CUtensorMap*>(a.tmap_b);
     static const int tma_store_env = getenv("OCC_GEMM_TMASTORE") ? atoi(getenv("OCC_GEMM_TMASTORE")) : 1;

@@ -223,7 +223,8 @@ enum EpiMode {
 struct GemmArgs {
     const void* tmap_a = nullptr;  // CUtensorMap* (host object, passed by value to the kernel)
     const void* tmap_b = nullptr;
-    const void* tmap_c = nullptr;  // bf16 forward output [rows, ldo] (box 32 x 32, 64 B swizzle): TMA-store epilogue
+    const void* tmap_c = nullptr;
+    const int* a_rows = nullptr;   // gathered A: row of tmap_a (box 64 x 1) for each padded Epd row, -1 = zero  // bf16 forward output [rows, ldo] (box 32 x 32, 64 B swizzle): TMA-store epilogue
     int K = 0;                     // reduction dim (forward / data gradient)
     int N = 0;                     // output columns per expert (GEMM-1 SwiGLU: F; B rows per expert = 2F)
     int b_rows_per_e = 0;          // rows of B per expert in the stacked K-major weight matrix
