@@ -688,9 +688,9 @@ occ_status forward_multi(occ_handle* h, const __nv_bfloat16* x, const int32_t* i
     launch_rank_emit_compute(Rm, h->d_R, h->rgroup.p, h->rmask.p, 1, P, ws2, ec, st);
     // 5. grouped expert FFN (A rows gathered from the inbox by TMA, or copied)
     const bool gathered = h->gather_a && !h->training;
-    if (!gathered) {
+    if (!gathered) {  // Epd A operand: each received row read once, written to its Epd rows
         mark(h, ST_GATHER, st);
-        launch_gather_rows((int)h->Q_max, h->d_q_total, h->epd_src.p, h->in_x.p, D, h->x_epd.p, st);
+        launch_scatter_rows(Rm, h->d_R, P, D, h->in_x.p, nullptr, h->row_epd.p, P, h->cofs, h->x_epd.p, st);
     }
     mark(h, ST_GEMM1, st);
     launch_gemm1(h, P, st, gathered);
@@ -1064,8 +1064,10 @@ occ_status occ_forward(occ_handle* h, const void* x, const int32_t* ids, const f
     mark(h, ST_PACK, st);
     // 2. pack: x rows -> inbox rows of every destination device
     const int32_t* rowmap = h->tok_row.p;
+    // (all devices are local: the Epd scatter below reads x itself, so the
+    // inbox carries only the routing rows unless the gather4 GEMM path needs them)
     PackArgs pk{n, k, nd, D, dedup, reinterpret_cast<const __nv_bfloat16*>(x), ids, weights, h->mask.p, rowmap,
-                h->in_x.p, h->in_ids.p, h->in_w.p};
+                h->gather_a ? h->in_x.p : nullptr, h->in_ids.p, h->in_w.p};
     launch_pack(pk, st);
     mark(h, ST_CINDEX, st);
     // 3. compute index (BRIM1) over the inbox rows
@@ -1086,9 +1088,10 @@ occ_status occ_forward(occ_handle* h, const void* x, const int32_t* ids, const f
     // come straight from the inbox (TMA gather4) unless training needs the
     // Epd copy for the weight gradient
     const bool gathered = h->gather_a && !h->training;
-    if (!gathered) {
+    if (!gathered) {  // Epd A operand: each token row read once, written to its Epd rows
         mark(h, ST_GATHER, st);
-        launch_gather_rows((int)h->Q_max, h->d_q_total, h->epd_src.p, h->in_x.p, D, h->x_epd.p, st);
+        launch_scatter_rows(R_max, R_total, P, D, reinterpret_cast<const __nv_bfloat16*>(x), h->in_tok.p,
+                            h->row_epd.p, G * P, h->cofs, h->x_epd.p, st);
     }
     mark(h, ST_GEMM1, st);
     launch_gemm1(h, G * P, st, gathered);
@@ -1176,8 +1179,8 @@ occ_status occ_backward(occ_handle* h, const void* upstream, float* g_x, float* 
     occ_status s = ensure_bwd(h);
     if (s != OCC_OK) return s;
     // combine + return adjoints: the token's upstream row on every Epd row
-    launch_gather_token_rows((int)h->Q_max, h->d_q_total, h->epd_src.p, h->in_tok.p,
-                             reinterpret_cast<const __nv_bfloat16*>(upstream), D, h->g_epd.p, st);
+    launch_scatter_rows((int)h->R_max, h->dofs.in_base + nd, P, D, reinterpret_cast<const __nv_bfloat16*>(upstream),
+                        h->in_tok.p, h->row_epd.p, nd * P, h->cofs, h->g_epd.p, st);
     // merge adjoint (data): g_mod = g_y w2^T, with modulation + activation
     // adjoints and the routing-weight partials fused in the epilogue
     GemmArgs g;

@@ -150,6 +150,13 @@ void launch_init_epd(int Q_max, int32_t* epd_src, float* epd_w, cudaStream_t st)
 void launch_gather_rows(int Q_max, const int* q_total, const int32_t* epd_src, const __nv_bfloat16* src, int D,
                         __nv_bfloat16* dst, cudaStream_t st);
 
+// Epd A operand by scatter: every inbox row read once, written to each of its
+// Epd rows (row_epd); padding rows of the NG segments zeroed.  src row of
+// inbox row r = src_rows ? src_rows[r] : r.
+void launch_scatter_rows(int R_max, const int* R_total, int P, int D, const __nv_bfloat16* src,
+                         const int32_t* src_rows, const int32_t* row_epd, int NG, const ComputeOffsets& o,
+                         __nv_bfloat16* dst, cudaStream_t st);
+
 // Intra-device partial combine: ret[r] = bf16( sum_{p asc} Y[row_epd[r,p]] ).
 void launch_partial_combine(int R_max, const int* R_total, int P, int D, const int32_t* row_epd,
                             const __nv_bfloat16* Y, __nv_bfloat16* ret, cudaStream_t st);

@@ -6,6 +6,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <algorithm>
 
 #include "occ_common.cuh"
 #include "occ_internal.h"
@@ -289,7 +290,7 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs a) {
     } else {
         for (int j = 0; j < a.k; ++j) rows[nrows++] = a.tok_row[(long)t * a.k + j];
     }
-    for (int v0 = 0; v0 < nvec; v0 += 8 * 32) {
+    for (int v0 = 0; a.dst_x && v0 < nvec; v0 += 8 * 32) {
         uint4 buf[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
@@ -421,6 +422,64 @@ __global__ void __launch_bounds__(256) gather_rows_kernel(int Q_max, const int* 
         for (int u = 0; u < 4; ++u)
             if (v0 + u * 32 + lane < nvec) out[v0 + u * 32 + lane] = b[u];
     }
+}
+
+// Scatter (replaces the Epd-order gather): each inbox row is read ONCE and
+// written to every Epd row that uses it (its local experts, placement order)
+// — n_epd row writes but only R row reads, instead of n_epd scattered reads.
+// src row of inbox row r = src_rows ? src_rows[r] : r (world_size == 1 reads
+// the tokens themselves: src = x, src_rows = inbox token).
+__global__ void __launch_bounds__(256) scatter_rows_kernel(int R_max, const int* R_total, int P, int D,
+                                                           const __nv_bfloat16* src, const int32_t* src_rows,
+                                                           const int32_t* row_epd, __nv_bfloat16* dst) {
+    // one warp per (row, 2 KB slice): 4 uint4 per lane in flight
+    constexpr int kSlice = 128;  // uint4 per slice
+    const int nvec = D / 8;
+    const int nsl = (nvec + kSlice - 1) / kSlice;
+    const long w = ((long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int r = (int)(w / nsl), sl = (int)(w % nsl);
+    if (r >= *R_total) return;
+    const int sr = src_rows ? src_rows[r] : r;
+    const uint4* in = reinterpret_cast<const uint4*>(src + (long)sr * D);
+    // destinations: lane p holds row_epd[r, p] (P <= 64: two words)
+    const int q_lo = lane < P ? row_epd[(long)r * P + lane] : -1;
+    const int q_hi = lane + 32 < P ? row_epd[(long)r * P + lane + 32] : -1;
+    const unsigned m_lo = __ballot_sync(0xffffffffu, q_lo >= 0), m_hi = __ballot_sync(0xffffffffu, q_hi >= 0);
+    const int v0 = sl * kSlice;
+    uint4 buf[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int v = v0 + u * 32 + lane;
+        if (v < nvec) buf[u] = __ldg(in + v);
+    }
+    for (int half = 0; half < 2; ++half) {
+        unsigned m = half ? m_hi : m_lo;
+        while (m) {
+            const int p = __ffs(m) - 1;
+            m &= m - 1;
+            const int q = __shfl_sync(0xffffffffu, half ? q_hi : q_lo, p);
+            uint4* out = reinterpret_cast<uint4*>(dst + (long)q * D);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int v = v0 + u * 32 + lane;
+                if (v < nvec) out[v] = buf[u];
+            }
+        }
+    }
+}
+
+// Zero the padding rows of every Epd segment (rows cnt..roundup(cnt, kBM)).
+__global__ void __launch_bounds__(256) zero_pad_rows_kernel(int NG, ComputeOffsets o, int D, __nv_bfloat16* dst) {
+    const int g = blockIdx.x;
+    if (g >= NG) return;
+    const int cnt = o.cnt[g];
+    const int pad = (cnt + kBM - 1) / kBM * kBM - cnt;
+    if (!pad) return;
+    uint4* base = reinterpret_cast<uint4*>(dst + (long)(o.seg_base[g] + cnt) * D);
+    const long nvec = (long)pad * D / 8;
+    for (long v = (long)blockIdx.y * blockDim.x + threadIdx.x; v < nvec; v += (long)gridDim.y * blockDim.x)
+        base[v] = make_uint4(0, 0, 0, 0);
 }
 
 // ------------------------------------------------------- partial combine --
@@ -1123,6 +1182,19 @@ void launch_gather_rows(int Q_max, const int* q_total, const int32_t* epd_src, c
     if (!Q_max) return;
     gather_rows_kernel<<<(Q_max + 7) / 8, 256, 0, st>>>(Q_max, q_total, epd_src, src, D, dst);
     count_launch();
+}
+
+void launch_scatter_rows(int R_max, const int* R_total, int P, int D, const __nv_bfloat16* src,
+                         const int32_t* src_rows, const int32_t* row_epd, int NG, const ComputeOffsets& o,
+                         __nv_bfloat16* dst, cudaStream_t st) {
+    if (!R_max) return;
+    const long warps = (long)R_max * ((D / 8 + 127) / 128);
+    scatter_rows_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(R_max, R_total, P, D, src, src_rows, row_epd,
+                                                                     dst);
+    // up to kBM - 1 padding rows per segment: spread each over enough blocks
+    const int ny = std::max(1, std::min(64, (int)((long)(kBM - 1) * D / 8 / (256 * 16))));
+    zero_pad_rows_kernel<<<dim3(NG, ny), 256, 0, st>>>(NG, o, D, dst);
+    count_launch(2);
 }
 
 void launch_partial_combine(int R_max, const int* R_total, int P, int D, const int32_t* row_epd,
