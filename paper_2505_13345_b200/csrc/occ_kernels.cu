@@ -610,32 +610,53 @@ __global__ void __launch_bounds__(256) combine_fused_kernel(int n, int nd, int k
             }
         }
     }
-    const int nv = D / 4;
+    // 16-byte vectors; all nq product rows of a vector loaded before the
+    // ordered sum (device ascending, placement order within a device)
+    const int nv = D / 8;
     for (int v = lane; v < nv; v += 32) {
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f), dev = acc;
-        for (int i = 0; i < nq; ++i) {
-            if (i && newdev[i]) {
-                acc.x += __bfloat162float(__float2bfloat16(dev.x));
-                acc.y += __bfloat162float(__float2bfloat16(dev.y));
-                acc.z += __bfloat162float(__float2bfloat16(dev.z));
-                acc.w += __bfloat162float(__float2bfloat16(dev.w));
-                dev = make_float4(0.f, 0.f, 0.f, 0.f);
+        float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, dev[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int i0 = 0; i0 < nq; i0 += 8) {
+            uint4 u[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (i0 + j < nq) u[j] = __ldg(reinterpret_cast<const uint4*>(Y + (long)qs[i0 + j] * D) + v);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (i0 + j >= nq) break;
+                if (i0 + j && newdev[i0 + j]) {
+#pragma unroll
+                    for (int e = 0; e < 8; ++e) {
+                        acc[e] += __bfloat162float(__float2bfloat16(dev[e]));
+                        dev[e] = 0.f;
+                    }
+                }
+                const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&u[j]);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float2 f = __bfloat1622float2(hh[e]);
+                    dev[2 * e] += f.x;
+                    dev[2 * e + 1] += f.y;
+                }
             }
-            const float4 y = ld_bf16x4(Y + (long)qs[i] * D + 4 * v);
-            dev.x += y.x; dev.y += y.y; dev.z += y.z; dev.w += y.w;
         }
-        acc.x += __bfloat162float(__float2bfloat16(dev.x));
-        acc.y += __bfloat162float(__float2bfloat16(dev.y));
-        acc.z += __bfloat162float(__float2bfloat16(dev.z));
-        acc.w += __bfloat162float(__float2bfloat16(dev.w));
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] += __bfloat162float(__float2bfloat16(dev[e]));
         if (ys) {  // shared experts (source device), added last
-            const float4 y = ld_bf16x4(ys + (long)t * D + 4 * v);
-            acc.x += y.x; acc.y += y.y; acc.z += y.z; acc.w += y.w;
+            const uint4 w = __ldg(reinterpret_cast<const uint4*>(ys + (long)t * D) + v);
+            const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float2 f = __bfloat1622float2(hh[e]);
+                acc[2 * e] += f.x;
+                acc[2 * e + 1] += f.y;
+            }
         }
-        uint2 o;
-        o.x = pack_bf16(acc.x, acc.y);
-        o.y = pack_bf16(acc.z, acc.w);
-        reinterpret_cast<uint2*>(out + (long)t * D)[v] = o;
+        uint4 o;
+        o.x = pack_bf16(acc[0], acc[1]);
+        o.y = pack_bf16(acc[2], acc[3]);
+        o.z = pack_bf16(acc[4], acc[5]);
+        o.w = pack_bf16(acc[6], acc[7]);
+        reinterpret_cast<uint4*>(out + (long)t * D)[v] = o;
     }
 }
 
