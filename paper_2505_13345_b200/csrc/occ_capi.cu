@@ -135,7 +135,7 @@ struct occ_handle {
     DevBuf<int32_t> tok_row, tok_sfd, lam;
     DevBuf<__nv_bfloat16> in_x, x_epd, hbuf, ret, y16;
     DevBuf<int32_t> in_ids, in_tok, in_src, in_slot, in_dev, row_epd, epd_src, epd_j;
-    DevBuf<float> in_w, epd_w, ybuf, logits, rt_w;
+    DevBuf<float> in_w, epd_w, logits, rt_w;
     DevBuf<int32_t> rt_ids;  // routing of occ_forward_expert_parallel
     size_t R_max = 0, Q_max = 0, max_mblk = 0;
     int last_n = 0;
@@ -366,7 +366,6 @@ occ_status ensure_recv(occ_handle* h, size_t R, size_t epd_bound) {
         CUDA_TRY(h->x_epd.ensure(Q * D));
         CUDA_TRY(h->hbuf.ensure(Q * F));
         CUDA_TRY(h->y16.ensure(Q * D));
-        if (h->training) CUDA_TRY(h->ybuf.ensure(Q * D));
         h->Q_max = Q;
         h->max_mblk = Q / kBM;
         h->bwd_tmaps_q = -1;
@@ -774,7 +773,7 @@ occ_status occ_destroy(occ_handle* h) {
     h->rmask.release();
     for (auto* b : {&h->w13t, &h->w2t, &h->in_x, &h->x_epd, &h->hbuf, &h->ret, &h->snd_x, &h->y_src, &h->y16}) b->release();
     h->snd_w.release();
-    for (auto* b : {&h->in_w, &h->epd_w, &h->ybuf, &h->logits, &h->rt_w}) b->release();
+    for (auto* b : {&h->in_w, &h->epd_w, &h->logits, &h->rt_w}) b->release();
     h->rt_ids.release();
     for (auto& e : h->ev)
         if (e) cudaEventDestroy(e);
@@ -1148,7 +1147,6 @@ static occ_status ensure_bwd(occ_handle* h) {
     CUDA_TRY(h->g_epd.ensure(Q * D));
     CUDA_TRY(h->gpre.ensure(Q * kw));
     CUDA_TRY(h->gw_part.ensure(Q * NBf * 2));  // per (row, n-tile, epilogue column half)
-    CUDA_TRY(h->ybuf.ensure(Q * D));
     if (h->bwd_tmaps_q != (int)Q) {
         if (!make_tmap_2d(h->tmG_k.bytes, h->g_epd.p, D, Q, 64, 128) ||
             !make_tmap_2d(h->tmP_k.bytes, h->gpre.p, kw, Q, 64, 128) ||
@@ -1201,10 +1199,12 @@ occ_status occ_backward(occ_handle* h, const void* upstream, float* g_x, float* 
     g.gw_part = h->gw_part.p;
     g.max_tiles = (int)h->max_mblk * ((F + 255) / 256);
     launch_grouped_gemm(h->gated ? EPI_BWD_SWIGLU : EPI_BWD_ACT, g, h->num_sms, st);
-    // scatter adjoint (data): g_x per Epd row = g_pre [w1 | w3]^T (fp32)
+    // scatter adjoint (data): g_x per Epd row = g_pre [w1 | w3]^T, fp32
+    // accumulate, bf16 rows (the forward's product buffer is free by now)
     GemmArgs d1;
     d1.tmap_a = h->tmP_k.bytes;
     d1.tmap_b = h->tmW1o.bytes;
+    d1.tmap_c = h->tmC2.bytes;
     d1.K = kw;
     d1.N = D;
     d1.b_rows_per_e = D;
@@ -1212,10 +1212,11 @@ occ_status occ_backward(occ_handle* h, const void* upstream, float* g_x, float* 
     d1.grp_w = h->d_widx.p;
     d1.ngroups = NG;
     d1.band = 8;
-    d1.out = h->ybuf.p;
+    d1.out = h->y16.p;
     d1.ldo = D;
+    d1.act = OCC_ACT_IDENTITY;
     d1.max_tiles = (int)h->max_mblk * ((D + 255) / 256);
-    launch_grouped_gemm(EPI_F32, d1, h->num_sms, st);
+    launch_grouped_gemm(EPI_ACT_BF16, d1, h->num_sms, st);
     // merge adjoint (weights): g_w2[e] = mod_e^T g_y_e (backward.cpp:84-93)
     GemmArgs w2;
     w2.tmap_a = h->tmH_mn.bytes;
@@ -1249,7 +1250,7 @@ occ_status occ_backward(occ_handle* h, const void* upstream, float* g_x, float* 
     w1.max_tiles = NG * ((D + 255) / 256) * ((kw + 255) / 256);
     launch_grouped_gemm(EPI_WGRAD, w1, h->num_sms, st);
     // dispatch adjoint: sum each token's rows (device ascending), fp32
-    launch_combine_grad(n, nd, k, P, h->cfg.dedup, D, h->mask.p, h->tok_row.p, h->row_epd.p, h->ybuf.p, g_x, st);
+    launch_combine_grad(n, nd, k, P, h->cfg.dedup, D, h->mask.p, h->tok_row.p, h->row_epd.p, h->y16.p, g_x, st);
     launch_gw_scatter((int)h->Q_max, h->d_q_total, 2 * ((F + 255) / 256), h->gw_part.p, h->epd_src.p, h->in_tok.p,
                       h->epd_j.p, k, g_weights, st);
     CUDA_TRY(cudaGetLastError());

@@ -741,7 +741,8 @@ __global__ void __launch_bounds__(256) gather_token_rows_kernel(int Q_max, const
 // order inside a device; fp32 throughout.
 __global__ void __launch_bounds__(256) combine_grad_kernel(int n, int nd, int k, int P, int dedup, int D,
                                                            const uint64_t* mask, const int32_t* tok_row,
-                                                           const int32_t* row_epd, const float* Y, float* out) {
+                                                           const int32_t* row_epd, const __nv_bfloat16* Y,
+                                                           float* out) {
     const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (t >= n) return;
@@ -767,14 +768,29 @@ __global__ void __launch_bounds__(256) combine_grad_kernel(int n, int nd, int k,
             }
         }
     }
-    const int nv = D / 4;
+    const int nv = D / 8;
     for (int v = lane; v < nv; v += 32) {
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int i = 0; i < nq; ++i) {
-            const float4 y = __ldg(reinterpret_cast<const float4*>(Y + (long)qs[i] * D) + v);
-            acc.x += y.x; acc.y += y.y; acc.z += y.z; acc.w += y.w;
+        float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int i0 = 0; i0 < nq; i0 += 8) {
+            uint4 u[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (i0 + j < nq) u[j] = __ldg(reinterpret_cast<const uint4*>(Y + (long)qs[i0 + j] * D) + v);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (i0 + j >= nq) break;
+                const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&u[j]);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float2 f = __bfloat1622float2(hh[e]);
+                    acc[2 * e] += f.x;
+                    acc[2 * e + 1] += f.y;
+                }
+            }
         }
-        reinterpret_cast<float4*>(out + (long)t * D)[v] = acc;
+        float4* o = reinterpret_cast<float4*>(out + (long)t * D) + 2 * v;
+        o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
     }
 }
 
@@ -1259,7 +1275,7 @@ void launch_gather_token_rows(int Q_max, const int* q_total, const int32_t* epd_
 }
 
 void launch_combine_grad(int n, int nd, int k, int P, int dedup, int D, const uint64_t* mask, const int32_t* tok_row,
-                         const int32_t* row_epd, const float* Y, float* out, cudaStream_t st) {
+                         const int32_t* row_epd, const __nv_bfloat16* Y, float* out, cudaStream_t st) {
     if (!n) return;
     combine_grad_kernel<<<(n + 7) / 8, 256, 0, st>>>(n, nd, k, P, dedup, D, mask, tok_row, row_epd, Y, out);
     count_launch();

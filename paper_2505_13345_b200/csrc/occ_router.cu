@@ -19,7 +19,10 @@
 namespace occ {
 namespace {
 
-constexpr int RM = 128, RK = 64, RSTAGES = 4, RTHREADS = 192;
+constexpr int RM = 128, RK = 64, RTHREADS = 192;
+// deeper TMA ring for narrow gates (more bytes of x in flight per SM)
+template <int NPMAX>
+constexpr int rstages() { return NPMAX <= 64 ? 8 : (NPMAX <= 128 ? 6 : 4); }
 constexpr int R_A_BYTES = RM * RK * 2;  // 16 KB
 
 struct RouterParams {
@@ -32,6 +35,7 @@ struct RouterParams {
 template <int NPMAX>
 __global__ void __launch_bounds__(RTHREADS, 1)
     router_tc_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmG, RouterParams p) {
+    constexpr int RSTAGES = rstages<NPMAX>();
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const int b_bytes = p.np * RK * 2;
@@ -163,33 +167,38 @@ __global__ void __launch_bounds__(RTHREADS, 1)
                         sum += s;
                     }
             const float inv = 1.0f / sum;
-            // top-k by (score desc, index asc): streaming insertion
-            float bs[kMaxTopK];
-            int bi[kMaxTopK];
-            int m = 0;
 #pragma unroll
             for (int c = 0; c < NCH; ++c)
 #pragma unroll
-                for (int i = 0; i < 32; ++i) {
-                    const int j = c * 32 + i;
-                    if (j >= p.e) continue;
-                    const float s = __uint_as_float(v[c][i]) * inv;
-                    if (m == p.k && !(s > bs[m - 1])) continue;  // equal -> the earlier index wins
-                    int pos = m < p.k ? m++ : p.k - 1;
-                    while (pos > 0 && s > bs[pos - 1]) {
-                        bs[pos] = bs[pos - 1];
-                        bi[pos] = bi[pos - 1];
-                        --pos;
-                    }
-                    bs[pos] = s;
-                    bi[pos] = j;
-                }
+                for (int i = 0; i < 32; ++i)
+                    v[c][i] = __float_as_uint(c * 32 + i < p.e ? __uint_as_float(v[c][i]) * inv : -1.0f);
+            // top-k by (score desc, index asc): k argmax rounds over the
+            // register-resident row (strict > in ascending index order keeps
+            // the lower index on ties); selected entries become -1
             float tot = 0.f;
-            for (int j = 0; j < p.k; ++j) tot += bs[j];
-            for (int j = 0; j < p.k; ++j) {
-                p.ids[(long)t * p.k + j] = bi[j];
-                p.w[(long)t * p.k + j] = p.renorm ? bs[j] / tot : bs[j];
+            int32_t* ids = p.ids + (long)t * p.k;
+            float* wout = p.w + (long)t * p.k;
+            for (int r = 0; r < p.k; ++r) {
+                float best = -2.0f;
+                int bj = 0;
+#pragma unroll
+                for (int c = 0; c < NCH; ++c)
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        const float s = __uint_as_float(v[c][i]);
+                        if (s > best) { best = s; bj = c * 32 + i; }
+                    }
+#pragma unroll
+                for (int c = 0; c < NCH; ++c)
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        if (c * 32 + i == bj) v[c][i] = __float_as_uint(-1.0f);
+                ids[r] = bj;
+                wout[r] = best;
+                tot += best;
             }
+            if (p.renorm)
+                for (int r = 0; r < p.k; ++r) wout[r] = wout[r] / tot;
             }  // NPMAX <= 128
         }
     }
@@ -206,7 +215,7 @@ void launch_router_np(const CUtensorMap& tx, const CUtensorMap& tg, const Router
                       cudaStream_t st) {
     const int tiles = (p.n + RM - 1) / RM;
     const int grid = tiles < num_sms ? tiles : num_sms;
-    const int smem = RSTAGES * (R_A_BYTES + p.np * RK * 2) + 256 + 1024;
+    const int smem = rstages<NPMAX>() * (R_A_BYTES + p.np * RK * 2) + 256 + 1024;
     cudaFuncSetAttribute(router_tc_kernel<NPMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     router_tc_kernel<NPMAX><<<grid, RTHREADS, smem, st>>>(tx, tg, p);
 }
