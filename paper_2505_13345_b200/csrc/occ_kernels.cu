@@ -391,7 +391,7 @@ struct ComputeEmitter {
         e.epd_w[q] = wt;
         if (e.epd_j) e.epd_j[q] = jj;
     }
-    __device__ void miss(int r, int p) { e.row_epd[(long)r * e.P + p] = -1; }
+    __device__ void miss(int, int) {}  // row_epd is pre-filled with -1 (launch_rank_emit_compute)
 };
 
 __global__ void init_epd_kernel(int Q, int32_t* src, float* w) {
@@ -1205,6 +1205,8 @@ void launch_compute_finalize(int G, int P, const int* totals, ComputeOffsets o, 
 
 void launch_rank_emit_compute(int R_max, const int* R_total, const int32_t* group, const uint64_t* mask, int G,
                               int B, RankWs ws, const EmitCompute& e, cudaStream_t st) {
+    // misses: one coalesced fill instead of P scattered 4-byte stores per row
+    cudaMemsetAsync(e.row_epd, 0xFF, sizeof(int32_t) * (size_t)R_max * e.P, st);
     launch_rank_emit(R_max, R_total, group, mask, G, B, ws, ComputeEmitter{e}, st);
 }
 
