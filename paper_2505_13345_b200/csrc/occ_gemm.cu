@@ -159,6 +159,34 @@ __device__ __forceinline__ void store_bf16x32(__nv_bfloat16* p, const float (&h)
         }
 }
 
+__device__ __forceinline__ void unpack_bf16x32(const uint4 (&w)[4], float (&f)[32]) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w[u]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const float2 x = __bfloat1622float2(h[q]);
+            f[8 * u + 2 * q] = x.x;
+            f[8 * u + 2 * q + 1] = x.y;
+        }
+    }
+}
+
+// Backward epilogue inputs: 32 pre-activation columns of one row (a, and b
+// for SwiGLU) as packed bf16; columns past N are never used.
+template <int EPI>
+__device__ __forceinline__ void load_pre_chunk(const Params& p, long row, int col0, uint4 (&A)[4], uint4 (&B)[4]) {
+    if (col0 >= p.N) return;
+    const uint4* pa = reinterpret_cast<const uint4*>(p.pre_a + row * p.N + col0);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) A[u] = __ldg(pa + u);
+    if constexpr (EPI == EPI_BWD_SWIGLU) {
+        const uint4* pb = reinterpret_cast<const uint4*>(p.pre_b + row * p.N + col0);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) B[u] = __ldg(pb + u);
+    }
+}
+
 template <int EPI, bool WGRAD>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -339,6 +367,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int tile = cid; tile < num_tiles; tile += ncl) {
+            // backward epilogue inputs (pre-activations) of this tile's first
+            // chunk are fetched before waiting for the accumulator, so their
+            // latency hides under the tile's MMAs
+            uint4 pa_cur[4], pb_cur[4];
+            if constexpr (!WGRAD && (EPI == EPI_BWD_ACT || EPI == EPI_BWD_SWIGLU)) {
+                int mb0, nb0, wi0;
+                tile_coords(tile, s_gmb, s_gw, p.ngroups, NB, p.band, mb0, nb0, wi0);
+                const long row0 = (long)mb0 * 2 * BM + rank * BM + q * 32 + lane;
+                load_pre_chunk<EPI>(p, row0, nb0 * BN + hsel * (BN / 64) * 32, pa_cur, pb_cur);
+            }
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
@@ -398,36 +436,44 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #pragma unroll 1
                     for (int c = hsel * (BN / 64); c < (hsel + 1) * (BN / 64); ++c) {
                         const int col0 = nb * BN + c * 32;
+                        uint4 pa_nxt[4], pb_nxt[4];  // prefetch the next chunk's inputs
+                        if (c + 1 < (hsel + 1) * (BN / 64)) load_pre_chunk<EPI>(p, row, col0 + 32, pa_nxt, pb_nxt);
                         uint32_t v[32];
                         tmem_ld32(tbase + c * 32, v);
                         tmem_ld_wait();
-                        if (col0 >= F) continue;
-                        const int nv = F - col0 < 32 ? F - col0 : 32;
-                        float a[32], r0[32];
-                        load_bf16x32(p.pre_a + row * F + col0, a);
-                        if constexpr (EPI == EPI_BWD_SWIGLU) {
-                            float b[32], r1[32];
-                            load_bf16x32(p.pre_b + row * F + col0, b);
+                        if (col0 < F) {
+                            const int nv = F - col0 < 32 ? F - col0 : 32;
+                            float a[32], r0[32];
+                            unpack_bf16x32(pa_cur, a);
+                            if constexpr (EPI == EPI_BWD_SWIGLU) {
+                                float b[32], r1[32];
+                                unpack_bf16x32(pb_cur, b);
 #pragma unroll
-                            for (int i = 0; i < 32; ++i) {
-                                const float gm = i < nv ? __uint_as_float(v[i]) : 0.f;
-                                const float s = sigmoid_fast(a[i]);
-                                const float sa = a[i] * s;
-                                gw += sa * b[i] * gm;
-                                const float gh = gm * wr;
-                                r0[i] = gh * b[i] * s * (1.0f + a[i] * (1.0f - s));
-                                r1[i] = gh * sa;
-                            }
-                            store_bf16x32(out + col0, r0, F - col0);
-                            store_bf16x32(out + F + col0, r1, F - col0);
-                        } else {
+                                for (int i = 0; i < 32; ++i) {
+                                    const float gm = i < nv ? __uint_as_float(v[i]) : 0.f;
+                                    const float s = sigmoid_fast(a[i]);
+                                    const float sa = a[i] * s;
+                                    gw += sa * b[i] * gm;
+                                    const float gh = gm * wr;
+                                    r0[i] = gh * b[i] * s * (1.0f + a[i] * (1.0f - s));
+                                    r1[i] = gh * sa;
+                                }
+                                store_bf16x32(out + col0, r0, F - col0);
+                                store_bf16x32(out + F + col0, r1, F - col0);
+                            } else {
 #pragma unroll
-                            for (int i = 0; i < 32; ++i) {
-                                const float gm = i < nv ? __uint_as_float(v[i]) : 0.f;
-                                gw += act_f(a[i], p.act) * gm;
-                                r0[i] = gm * wr * act_grad(a[i], p.act);
+                                for (int i = 0; i < 32; ++i) {
+                                    const float gm = i < nv ? __uint_as_float(v[i]) : 0.f;
+                                    gw += act_f(a[i], p.act) * gm;
+                                    r0[i] = gm * wr * act_grad(a[i], p.act);
+                                }
+                                store_bf16x32(out + col0, r0, F - col0);
                             }
-                            store_bf16x32(out + col0, r0, F - col0);
+                        }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            pa_cur[u] = pa_nxt[u];
+                            pb_cur[u] = pb_nxt[u];
                         }
                     }
                     p.gw_part[(row * NB + nb) * 2 + hsel] = gw;
