@@ -439,6 +439,63 @@ def test_c1_full_size_vs_reference_rows():
     assert rep.per_device_token_counts == [rr.per_device_rows[d] for d in range(nd)]
 
 
+@pytest.mark.parametrize("name,ne,k,nd,n,prune", [
+    ("olmoe", 64, 8, 8, 65536, None),          # BASELINE config 4 token count, EP=8
+    ("deepseek", 64, 6, 8, 16384, None),       # config 3
+    ("qwen_ep4_budget2", 60, 4, 4, 16384, 2),  # config 5 with collaboration pruning
+    ("mixtral", 8, 2, 8, 16384, None),         # config 2
+])
+def test_full_size_indices_vs_reference(name, ne, k, nd, n, prune):
+    """Integer parity at the BASELINE token counts: BRIM0 of every source,
+    inbox records, BRIM1 and CommReport against the reference's own
+    forward_given_routing replayed at width 1 (indices do not depend on D or
+    F); routing from the fp64 top-k (+ pruning) path, itself
+    bit-exact with the reference."""
+    rng = np.random.default_rng(ne * 1000 + k)
+    scores = rng.dirichlet(np.ones(ne), size=n)  # softmax-like rows
+    plist = _placement(ne, nd, "shuffled", seed=k)
+    ids, w = O.Port().topk_route(scores, k, True)
+    if prune:
+        ids, w = O.Port().prune_routing(scores, ids, w, plist, "router", prune)
+    ids = ids.astype(np.int32)
+    w = w.astype(np.float32).astype(np.float64)
+    src = rng.integers(0, nd, n).astype(np.int32)
+    _, rep, idx = ref().forward_given_routing(np.full((n, 1), 0.5), ids, w, np.ones((ne, 1, 8)),
+                                              np.ones((ne, 8, 1)), plist, src, act="identity", single=False,
+                                              bytes_per_scalar=2, want_index=True)
+    dm, dh = 64, 128
+    layer = occ.ExpertParallelLayer(occ.MoEConfig(ne, k, nd, dm, dh, activation="silu"),
+                                    occ.Placement([list(r) for r in plist]))
+    layer.load_experts(torch.zeros(ne, dm, dh, dtype=torch.bfloat16, device="cuda"),
+                       torch.zeros(ne, dh, dm, dtype=torch.bfloat16, device="cuda"))
+    brim0, counts = layer.build_dispatch_index(cuda(ids), cuda(src))
+    brim0 = brim0.cpu().numpy()
+    pos = 0
+    for s_ in range(nd):
+        want = idx["dindex"][s_]
+        got = brim0[pos:pos + want.size].reshape(want.shape)
+        pos += want.size
+        assert np.array_equal(got, want), f"{name}: BRIM0 of source {s_}"
+    x = torch.zeros(n, dm, dtype=torch.bfloat16, device="cuda")
+    layer.forward_given_routing(x, cuda(ids), cuda(w, torch.float32), cuda(src))
+    r = layer.comm_report(bytes_per_scalar=2)
+    assert r.mean_replicas == rep.mean_replicas and r.crossing_rows == rep.crossing_rows
+    assert r.intra_share == rep.intra_share and r.inter_share == rep.inter_share
+    assert r.per_device_token_counts == [rep.per_device_rows[d] for d in range(nd)]
+    tok, srcs, slot, cix, rows = layer.saved_index()
+    tok, srcs, slot, cix = (t.cpu().numpy() for t in (tok, srcs, slot, cix))
+    pos = cpos = 0
+    P = ne // nd
+    for d in range(nd):
+        R = rows[d]
+        assert np.array_equal(tok[pos:pos + R], idx["inbox"][d][0]), f"{name}: inbox tokens of device {d}"
+        assert np.array_equal(srcs[pos:pos + R], idx["inbox"][d][1])
+        assert np.array_equal(slot[pos:pos + R], idx["inbox"][d][2])
+        assert np.array_equal(cix[cpos:cpos + P * R].reshape(P, R), idx["cindex"][d]), f"{name}: BRIM1 of device {d}"
+        pos += R
+        cpos += P * R
+
+
 @pytest.mark.parametrize("chunks", [1, 3, 4])
 def test_forward_host_pipeline_matches_device(chunks):
     """occ_forward_host (pinned host in/out, chunked H2D/layer/D2H pipeline)
