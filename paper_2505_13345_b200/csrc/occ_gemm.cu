@@ -172,19 +172,59 @@ __device__ __forceinline__ void unpack_bf16x32(const uint4 (&w)[4], float (&f)[3
     }
 }
 
-// Backward epilogue inputs: 32 pre-activation columns of one row (a, and b
-// for SwiGLU) as packed bf16; columns past N are never used.
-template <int EPI>
-__device__ __forceinline__ void load_pre_chunk(const Params& p, long row, int col0, uint4 (&A)[4], uint4 (&B)[4]) {
-    if (col0 >= p.N) return;
-    const uint4* pa = reinterpret_cast<const uint4*>(p.pre_a + row * p.N + col0);
+// Backward epilogue I/O, warp-cooperative and coalesced: a warp's 32 rows x
+// 32 columns bf16 block is moved as 4 instructions of 8 rows x 64 B (instead
+// of 32 row-scattered 16 B accesses per instruction), and transposed through
+// the warp's 2 KB smem staging buffer (64-byte swizzle, conflict-free both
+// ways) to/from the one-row-per-thread layout of tcgen05.ld 32x32b.
+// Lane L, step u covers row u*8 + L/4, 16-byte chunk L%4.
+__device__ __forceinline__ uint32_t stg_off(int r, int c) { return r * 64 + ((c ^ ((r >> 1) & 3)) << 4); }
+
+__device__ __forceinline__ void load_block_coalesced(const __nv_bfloat16* base, long ld, int ncols, int lane,
+                                                     uint4 (&R)[4]) {
+    const int c = lane & 3;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) A[u] = __ldg(pa + u);
-    if constexpr (EPI == EPI_BWD_SWIGLU) {
-        const uint4* pb = reinterpret_cast<const uint4*>(p.pre_b + row * p.N + col0);
+    for (int u = 0; u < 4; ++u)
+        R[u] = c * 8 < ncols ? __ldg(reinterpret_cast<const uint4*>(base + (long)(u * 8 + (lane >> 2)) * ld) + c)
+                             : make_uint4(0, 0, 0, 0);
+}
+// coalesced registers -> this lane's row (4 x 16 B)
+__device__ __forceinline__ void block_to_row(uint8_t* stg, const uint4 (&R)[4], int lane, uint4 (&row)[4]) {
 #pragma unroll
-        for (int u = 0; u < 4; ++u) B[u] = __ldg(pb + u);
+    for (int u = 0; u < 4; ++u) *reinterpret_cast<uint4*>(stg + stg_off(u * 8 + (lane >> 2), lane & 3)) = R[u];
+    __syncwarp();
+#pragma unroll
+    for (int c = 0; c < 4; ++c) row[c] = *reinterpret_cast<const uint4*>(stg + stg_off(lane, c));
+    __syncwarp();
+}
+// this lane's row (32 floats -> bf16) -> coalesced global stores
+__device__ __forceinline__ void row_to_global(uint8_t* stg, const float (&h)[32], __nv_bfloat16* base, long ld,
+                                              int ncols, int lane) {
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        uint4 o;
+        o.x = pack_bf16(h[8 * c + 0], h[8 * c + 1]);
+        o.y = pack_bf16(h[8 * c + 2], h[8 * c + 3]);
+        o.z = pack_bf16(h[8 * c + 4], h[8 * c + 5]);
+        o.w = pack_bf16(h[8 * c + 6], h[8 * c + 7]);
+        *reinterpret_cast<uint4*>(stg + stg_off(lane, c)) = o;
     }
+    __syncwarp();
+    const int c = lane & 3;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+        if (c * 8 < ncols)
+            reinterpret_cast<uint4*>(base + (long)(u * 8 + (lane >> 2)) * ld)[c] =
+                *reinterpret_cast<const uint4*>(stg + stg_off(u * 8 + (lane >> 2), c));
+    __syncwarp();
+}
+// pre-activation block(s) of one chunk: rows rowbase..+31, columns col0..+31
+template <int EPI>
+__device__ __forceinline__ void load_pre_chunk(const Params& p, long rowbase, int col0, int lane, uint4 (&A)[4],
+                                               uint4 (&B)[4]) {
+    if (col0 >= p.N) return;
+    load_block_coalesced(p.pre_a + rowbase * p.N + col0, p.N, p.N - col0, lane, A);
+    if constexpr (EPI == EPI_BWD_SWIGLU) load_block_coalesced(p.pre_b + rowbase * p.N + col0, p.N, p.N - col0, lane, B);
 }
 
 template <int EPI, bool WGRAD>
@@ -374,8 +414,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             if constexpr (!WGRAD && (EPI == EPI_BWD_ACT || EPI == EPI_BWD_SWIGLU)) {
                 int mb0, nb0, wi0;
                 tile_coords(tile, s_gmb, s_gw, p.ngroups, NB, p.band, mb0, nb0, wi0);
-                const long row0 = (long)mb0 * 2 * BM + rank * BM + q * 32 + lane;
-                load_pre_chunk<EPI>(p, row0, nb0 * BN + hsel * (BN / 64) * 32, pa_cur, pb_cur);
+                const long rowbase0 = (long)mb0 * 2 * BM + rank * BM + q * 32;
+                load_pre_chunk<EPI>(p, rowbase0, nb0 * BN + hsel * (BN / 64) * 32, lane, pa_cur, pb_cur);
             }
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
@@ -432,22 +472,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                     const float wr = p.row_w[row];
                     const int F = p.N;
                     float gw = 0.f;
-                    __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out) + row * p.ldo;
+                    const long rowbase = row - lane;
+                    uint8_t* stg = sC + (warp - 2) * STG_BYTES;
+                    __nv_bfloat16* outb = reinterpret_cast<__nv_bfloat16*>(p.out) + rowbase * p.ldo;
 #pragma unroll 1
                     for (int c = hsel * (BN / 64); c < (hsel + 1) * (BN / 64); ++c) {
                         const int col0 = nb * BN + c * 32;
                         uint4 pa_nxt[4], pb_nxt[4];  // prefetch the next chunk's inputs
-                        if (c + 1 < (hsel + 1) * (BN / 64)) load_pre_chunk<EPI>(p, row, col0 + 32, pa_nxt, pb_nxt);
+                        if (c + 1 < (hsel + 1) * (BN / 64)) load_pre_chunk<EPI>(p, rowbase, col0 + 32, lane, pa_nxt, pb_nxt);
                         uint32_t v[32];
                         tmem_ld32(tbase + c * 32, v);
                         tmem_ld_wait();
-                        if (col0 < F) {
+                        if (col0 < F) {  // warp-uniform
                             const int nv = F - col0 < 32 ? F - col0 : 32;
                             float a[32], r0[32];
-                            unpack_bf16x32(pa_cur, a);
+                            uint4 rowa[4];
+                            block_to_row(stg, pa_cur, lane, rowa);
+                            unpack_bf16x32(rowa, a);
                             if constexpr (EPI == EPI_BWD_SWIGLU) {
                                 float b[32], r1[32];
-                                unpack_bf16x32(pb_cur, b);
+                                uint4 rowb[4];
+                                block_to_row(stg, pb_cur, lane, rowb);
+                                unpack_bf16x32(rowb, b);
 #pragma unroll
                                 for (int i = 0; i < 32; ++i) {
                                     const float gm = i < nv ? __uint_as_float(v[i]) : 0.f;
@@ -458,8 +504,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                                     r0[i] = gh * b[i] * s * (1.0f + a[i] * (1.0f - s));
                                     r1[i] = gh * sa;
                                 }
-                                store_bf16x32(out + col0, r0, F - col0);
-                                store_bf16x32(out + F + col0, r1, F - col0);
+                                row_to_global(stg, r0, outb + col0, p.ldo, F - col0, lane);
+                                row_to_global(stg, r1, outb + F + col0, p.ldo, F - col0, lane);
                             } else {
 #pragma unroll
                                 for (int i = 0; i < 32; ++i) {
@@ -467,7 +513,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                                     gw += act_f(a[i], p.act) * gm;
                                     r0[i] = gm * wr * act_grad(a[i], p.act);
                                 }
-                                store_bf16x32(out + col0, r0, F - col0);
+                                row_to_global(stg, r0, outb + col0, p.ldo, F - col0, lane);
                             }
                         }
 #pragma unroll
@@ -499,8 +545,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                                     fa[i] = __uint_as_float(v[i]);
                                     fb[i] = __uint_as_float(g[i]);
                                 }
-                                store_bf16x32(p.save_a + row * p.N + col0, fa, p.N - col0);
-                                store_bf16x32(p.save_b + row * p.N + col0, fb, p.N - col0);
+                                // coalesced through the warp's staging buffer (free once
+                                // the previous TMA store has read it)
+                                uint8_t* stg = sC + (warp - 2) * STG_BYTES;
+                                if (lane == 0) bulk_wait_read<0>();
+                                __syncwarp();
+                                const long rb = row - lane;
+                                row_to_global(stg, fa, p.save_a + rb * p.N + col0, p.N, p.N - col0, lane);
+                                row_to_global(stg, fb, p.save_b + rb * p.N + col0, p.N, p.N - col0, lane);
                             }
 #pragma unroll
                             for (int i = 0; i < 32; ++i)
@@ -511,7 +563,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                                 float fa[32];
 #pragma unroll
                                 for (int i = 0; i < 32; ++i) fa[i] = __uint_as_float(v[i]);
-                                store_bf16x32(p.save_a + row * p.N + col0, fa, p.N - col0);
+                                uint8_t* stg = sC + (warp - 2) * STG_BYTES;
+                                if (lane == 0) bulk_wait_read<0>();
+                                __syncwarp();
+                                row_to_global(stg, fa, p.save_a + (row - lane) * p.N + col0, p.N, p.N - col0, lane);
                             }
 #pragma unroll
                             for (int i = 0; i < 32; ++i) h[i] = act_f(__uint_as_float(v[i]), p.act) * wr;
