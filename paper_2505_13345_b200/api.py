@@ -241,6 +241,7 @@ class ExpertParallelLayer:
         h = C.c_void_p()
         _check(lib().occ_create(C.byref(cfg), pl, world_size, rank, C.byref(h)), "occ_create")
         self._h = h
+        self._world = world_size
         self._prune_cache = None
 
     def __del__(self):
@@ -507,6 +508,25 @@ def reschedule_placement(p, num_devices: int) -> Placement:
                                           out.ctypes.data_as(C.c_void_p)), "reschedule_placement")
     per = e // num_devices
     return Placement([out[d * per:(d + 1) * per].tolist() for d in range(num_devices)])
+
+
+def collaboration_aware_placement(routing_batches, num_experts: int, num_devices: int,
+                                  layer: Optional["ExpertParallelLayer"] = None) -> Placement:
+    """The profiling -> placement loop (Occult Alg. 1):
+    co-activation histogram of the profiled routing batches on the device
+    (accumulate_collab, collab.cpp:10-23; summed across ranks with
+    occ_allreduce_histogram when `layer` is a world_size > 1 handle), then the
+    host normalize_graph + reschedule_placement (placement.cpp:88-148)."""
+    counts = None
+    for ids in routing_batches:
+        if counts is None:
+            counts = torch.zeros((num_experts, num_experts), dtype=torch.int64, device=ids.device)
+        accumulate_collab(counts, ids)
+    if counts is None:
+        raise ShapeError("collaboration_aware_placement: no routing batches")
+    if layer is not None and getattr(layer, "_world", 1) > 1:
+        layer.allreduce_histogram(counts)
+    return reschedule_placement(normalize_graph(counts), num_devices)
 
 
 def exchange_layout(counts, rank: int):
