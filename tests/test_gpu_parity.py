@@ -677,3 +677,33 @@ def test_collaboration_aware_placement_on_gpu():
         layer.build_dispatch_index(ids)
         ct[name] = layer.comm_report(bytes_per_scalar=2).mean_replicas
     assert ct["rescheduled"] <= 0.9 * ct["trivial"], ct
+
+
+@pytest.mark.parametrize("ne,k,nd,n", [(8, 2, 2, 2048), (64, 8, 8, 8192), (16, 4, 4, 999)])
+def test_simulate_report_matches_reference(ne, k, nd, n):
+    """`#moesim-report v1` from the GPU run == the same report rendered from
+    the reference's own CommReport and accumulate_collab:
+    every line, integers and doubles."""
+    from types import SimpleNamespace
+    from paper_2505_13345_b200 import report as R
+    rng = np.random.default_rng(n + ne)
+    ids, w = random_routing(n, ne, k, rng)
+    w = w.astype(np.float32).astype(np.float64)
+    plist = _placement(ne, nd, "shuffled", seed=2)
+    _, rr = ref().forward_given_routing(np.full((n, 1), 0.5), ids, w, np.ones((ne, 1, 8)), np.ones((ne, 8, 1)),
+                                        plist, None, act="identity", single=False, bytes_per_scalar=2)
+    cfg = occ.MoEConfig(ne, k, nd, 64, 64, activation="silu")
+    layer = occ.ExpertParallelLayer(cfg, occ.Placement([list(p) for p in plist]))
+    layer.load_experts(torch.zeros(ne, 64, 64, dtype=torch.bfloat16, device="cuda"),
+                       torch.zeros(ne, 64, 64, dtype=torch.bfloat16, device="cuda"))
+    layer.forward_given_routing(torch.zeros(n, 64, dtype=torch.bfloat16, device="cuda"), cuda(ids),
+                                cuda(w, torch.float32))
+    got = R.simulate_report(layer, cuda(ids), bytes_per_scalar=2)
+    ref_rep = SimpleNamespace(mean_replicas=rr.mean_replicas, cap_replicas=rr.cap_replicas,
+                              intra_share=rr.intra_share, inter_share=rr.inter_share,
+                              cross_device_bytes=rr.crossing_rows * 64 * 2,  # width-1 replay: bytes at D = 64
+                              per_device_token_counts=[rr.per_device_rows[d] for d in range(nd)])
+    want = R.render_simulate_report(cfg, ref_rep, ref().accumulate_collab(ids, ne), [list(p) for p in plist], n,
+                                    bytes_per_scalar=2)
+    diff = [(a, b) for a, b in zip(got.splitlines(), want.splitlines()) if a != b]
+    assert not diff and len(got) == len(want), diff
