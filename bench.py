@@ -300,6 +300,24 @@ def run_ours(args):
         flush.zero_()
         step()
     barrier()
+    # one step captured as a CUDA graph (world_size 1: the layer runs with
+    # device-side counts and no host synchronisation), replayed per step
+    graph, per_step = None, None
+    if world == 1 and not args.no_graph:
+        s_cap = torch.cuda.Stream()
+        s_cap.wait_stream(stream)
+        with torch.cuda.stream(s_cap):
+            step()
+        stream.wait_stream(s_cap)
+        graph = torch.cuda.CUDAGraph()
+        c0 = occ.launch_count()
+        with torch.cuda.graph(graph):
+            step()
+        per_step = occ.launch_count() - c0
+        for _ in range(2):
+            graph.replay()
+        torch.cuda.synchronize()
+    run_step = graph.replay if graph is not None else step
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     clocks = ClockSampler(local)
     clocks.start()
@@ -308,10 +326,10 @@ def run_ours(args):
     for i in range(args.steps):
         flush.zero_()
         ev[i][0].record(stream)
-        step()
+        run_step()
         ev[i][1].record(stream)
     barrier()
-    launches = occ.launch_count() - l0
+    launches = occ.launch_count() - l0 if graph is None else per_step * args.steps
     clk = clocks.stop()
     step_ms = [a.elapsed_time(b) for a, b in ev]
     tot_ms = sum(step_ms)
@@ -441,7 +459,8 @@ def run_ours(args):
                            "step": ("route + plan + pack + grouped GEMM-1/2 + partial combine + combine"
                                     + (" + backward (dgrad x2, wgrad x2, routing-weight grads)" if W["train"]
                                        else ""))},
-                "e2e": e2e, "gpu_launches": launches, "clocks": clk, "roofline": roofline,
+                "e2e": e2e, "gpu_launches": launches, "cuda_graph": graph is not None, "clocks": clk,
+                "roofline": roofline,
                 "stages_ms": stages, "a2a": a2a, "cpu_baseline": cpu,
                 "comm_report": {"mean_replicas": rep.mean_replicas, "n_sfd": rep.n_sfd, "n_epd": rep.n_epd}}
         print(json.dumps(line), flush=True)
@@ -459,6 +478,7 @@ def main():
     ap.add_argument("--workload", default="mixtral", choices=sorted(WORKLOADS))
     ap.add_argument("--tokens", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of the captured CUDA graph")
     ap.add_argument("--e2e-chunks", type=int, default=1)
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-tokens-per-thread", type=int, default=2)

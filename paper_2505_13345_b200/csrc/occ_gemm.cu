@@ -693,7 +693,12 @@ void launch_grouped_gemm(EpiMode mode, const GemmArgs& a, int num_sms, cudaStrea
         const char* e = getenv("OCC_GEMM_BAND");
         return e ? atoi(e) : 0;
     }();
-    if (band_override > 0 && !(mode == EPI_WGRAD)) p.band = band_override;
+    static const int band1_override = [] {
+        const char* e = getenv("OCC_GEMM_BAND_G1");
+        return e ? atoi(e) : 0;
+    }();
+    if (mode == EPI_SWIGLU_BF16 && band1_override > 0) p.band = band1_override;
+    else if (band_override > 0 && !(mode == EPI_WGRAD)) p.band = band_override;
     static const int hint_env = [] {  // L2 policy experiments: OCC_GEMM_HINT = 10 * a + b
         const char* e = getenv("OCC_GEMM_HINT");
         return e ? atoi(e) : 0;
