@@ -707,3 +707,48 @@ def test_simulate_report_matches_reference(ne, k, nd, n):
                                     bytes_per_scalar=2)
     diff = [(a, b) for a, b in zip(got.splitlines(), want.splitlines()) if a != b]
     assert not diff and len(got) == len(want), diff
+
+
+@pytest.mark.parametrize("train,shared", [(False, False), (False, True), (True, False)])
+def test_cuda_graph_replay_bit_identical(train, shared):
+    """With validation off the whole step (route + forward [+ backward]) has no
+    host synchronisation and captures into a CUDA graph; replays equal eager
+    calls bit for bit (this is what bench.py times)."""
+    ne, k, nd, dm, dh, n = 16, 4, 2, 128, 256, 700
+    x, g, w1, w2, w3 = make_layer_inputs(5, n, dm, dh, ne, gated=True)
+    layer = occ.ExpertParallelLayer(occ.MoEConfig(ne, k, nd, dm, dh, activation="swiglu"))
+    if train:
+        layer.set_training(True)
+    layer.load_experts(cuda(w1, torch.bfloat16), cuda(w2, torch.bfloat16), cuda(w3, torch.bfloat16))
+    if shared:
+        s1, s2, s3, sg = make_shared(2, dm, 128, True, seed=3)
+        layer.load_shared_experts(cuda(s1, torch.bfloat16), cuda(s2, torch.bfloat16), cuda(s3, torch.bfloat16),
+                                  cuda(sg, torch.bfloat16))
+    layer.set_validate(False)
+    xs, gs = cuda(x, torch.bfloat16), cuda(g, torch.bfloat16)
+    up = torch.empty_like(xs).uniform_(-1, 1)
+    out = torch.empty_like(xs)
+    res = {}
+
+    def step():
+        layer.forward_expert_parallel(xs, gs, out=out)
+        if train:
+            res["gx"] = layer.backward(up)["x"]
+
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        step()
+    torch.cuda.current_stream().wait_stream(s)
+    torch.cuda.synchronize()
+    eager = out.clone()
+    eager_gx = res["gx"].clone() if train else None
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        step()
+    out.zero_()
+    graph.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(out, eager)
+    if train:
+        assert torch.equal(res["gx"], eager_gx)
