@@ -348,11 +348,8 @@ def run_ours(args):
     gxh = torch.empty((x.shape[0], D), dtype=torch.float32).pin_memory() if W["train"] else None
 
     def e2e_step():
-        if W["train"]:  # H2D tokens + upstream, forward + backward, D2H token gradient
-            x.copy_(xh, non_blocking=True)
-            upstream.copy_(uh, non_blocking=True)
-            layer.forward_expert_parallel(x, gate, prune=prune, out=out)
-            gxh.copy_(layer.backward(upstream)["x"], non_blocking=True)
+        if W["train"]:  # H2D tokens + upstream, forward + backward, D2H token gradient (double-buffered)
+            layer.train_step_host(xh, gate, uh, gxh, prune=prune, wait=False)
             return
         # public API, host buffers: this step's H2D copy and the previous
         # step's D2H copy overlap the layer (double-buffered staging)
@@ -364,8 +361,13 @@ def run_ours(args):
     barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
+    # L2 between e2e steps: flushed unless one step's working set (resident
+    # experts + tokens in + tokens out) is already > 2x the 126 MB L2
+    ws_bytes = (e_local * D * F * (3 if gated else 2) + 2 * x.numel()) * 2
+    e2e_flush = args.e2e_flush or ws_bytes < 2 * 126 * 2 ** 20
     for i in range(args.steps):
-        flush.zero_()
+        if e2e_flush:
+            flush.zero_()
         e2e_step()
     layer.host_wait()  # the last step's result has landed in host memory
     e1.record(stream)
@@ -379,9 +381,13 @@ def run_ours(args):
            "h2d_bytes_per_step": x.numel() * x.element_size() * (2 if W["train"] else 1),
            "d2h_bytes_per_step": out.numel() * (4 if W["train"] else out.element_size()),
            "ms_per_step": e2e_ms / args.steps,
-           "api": f"ExpertParallelLayer.forward_host (occ_forward_host: pinned host buffers, double-buffered so "
-                  f"H2D of step i+1 and D2H of step i-1 overlap the layer of step i; {args.e2e_chunks} chunk(s)); "
-                  f"timed from before the first H2D to after the last D2H"}
+           "l2": ("flushed between steps" if e2e_flush else
+                  f"not flushed: per-step working set {ws_bytes / 2 ** 30:.2f} GiB > 2x L2"),
+           "api": (f"ExpertParallelLayer.train_step_host (pinned host tokens + upstream in, fp32 token gradient "
+                   f"out; double-buffered so the copies of steps i+1 / i-1 overlap step i)" if W["train"] else
+                   f"ExpertParallelLayer.forward_host (occ_forward_host: pinned host buffers, double-buffered so "
+                   f"H2D of step i+1 and D2H of step i-1 overlap the layer of step i; {args.e2e_chunks} chunk(s))")
+           + "; timed from before the first H2D to after the last D2H"}
 
     # --- stage profile (CUDA events on the launching stream) --------------
     layer.set_profiling(True)
@@ -480,6 +486,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of the captured CUDA graph")
     ap.add_argument("--e2e-chunks", type=int, default=1)
+    ap.add_argument("--e2e-flush", action="store_true", help="flush L2 between e2e steps even for large layers")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--ref-tokens-per-thread", type=int, default=2)
     args = ap.parse_args()

@@ -426,6 +426,62 @@ class ExpertParallelLayer:
 
     def host_wait(self):
         _check(lib().occ_host_wait(self._h, _stream()), "host_wait")
+        tp = getattr(self, "_tpipe", None)
+        if tp is not None and tp["last"] is not None:
+            torch.cuda.current_stream().wait_event(tp["last"])
+
+    def train_step_host(self, x_host: torch.Tensor, gate: torch.Tensor, upstream_host: torch.Tensor,
+                        grad_x_host: torch.Tensor, prune: Optional[PruneSpec] = None, wait: bool = True):
+        """Training step end to end from pinned host memory: H2D of tokens and
+        upstream gradient, forward_expert_parallel + backward_vjps on the
+        device, D2H of the token gradient (fp32); expert / routing-weight
+        gradients stay on the device (returned).  Double-buffered like
+        forward_host: the copies of step i+1 / i-1 run on two copy streams
+        while step i computes.  ``wait=False`` leaves the D2H pending until
+        ``host_wait()``; host buffers must stay untouched until then."""
+        if x_host.is_cuda or upstream_host.is_cuda or grad_x_host.is_cuda:
+            raise ShapeError("train_step_host: x, upstream and grad_x are host tensors")
+        _need_cuda(gate)
+        dev = gate.device
+        tp = getattr(self, "_tpipe", None)
+        if tp is None or tp["shape"] != tuple(x_host.shape):
+            torch.cuda.synchronize(dev)
+            tp = {"shape": tuple(x_host.shape), "calls": 0, "last": None,
+                  "s_in": torch.cuda.Stream(dev), "s_out": torch.cuda.Stream(dev),
+                  "x": [torch.empty(x_host.shape, dtype=torch.bfloat16, device=dev) for _ in range(2)],
+                  "up": [torch.empty(x_host.shape, dtype=torch.bfloat16, device=dev) for _ in range(2)],
+                  "out": [torch.empty(x_host.shape, dtype=torch.bfloat16, device=dev) for _ in range(2)],
+                  "free": [None, None], "gx": [None, None], "gdone": [None, None]}
+            self._tpipe = tp
+        slot = tp["calls"] & 1
+        tp["calls"] += 1
+        main = torch.cuda.current_stream(dev)
+        with torch.cuda.stream(tp["s_in"]):
+            if tp["free"][slot] is not None:  # the step that last used this slot has read x / upstream
+                tp["s_in"].wait_event(tp["free"][slot])
+            tp["x"][slot].copy_(x_host, non_blocking=True)
+            tp["up"][slot].copy_(upstream_host, non_blocking=True)
+            ev_in = torch.cuda.Event()
+            ev_in.record(tp["s_in"])
+        main.wait_event(ev_in)
+        if tp["gdone"][slot] is not None:  # the D2H that last read this slot's gradient finished
+            main.wait_event(tp["gdone"][slot])
+        self.forward_expert_parallel(tp["x"][slot], gate, prune=prune, out=tp["out"][slot])
+        g = self.backward(tp["up"][slot])
+        ev_c = torch.cuda.Event()
+        ev_c.record(main)
+        tp["free"][slot] = ev_c
+        tp["gx"][slot] = g["x"]
+        with torch.cuda.stream(tp["s_out"]):
+            tp["s_out"].wait_event(ev_c)
+            grad_x_host.copy_(g["x"], non_blocking=True)
+            ev_o = torch.cuda.Event()
+            ev_o.record(tp["s_out"])
+        tp["gdone"][slot] = ev_o
+        tp["last"] = ev_o
+        if wait:
+            self.host_wait()
+        return g
 
     def comm_report(self, bytes_per_scalar: int = 4, cap_replicas: Optional[float] = None) -> CommReport:
         r = _Report()
