@@ -57,12 +57,17 @@ occ_status fail(occ_status s, const std::string& msg) {
         if (e_ != cudaSuccess) return fail(OCC_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
     } while (0)
 
+// Bumped whenever any device buffer is (re)allocated or freed: captured
+// CUDA graphs hold raw pointers and are re-captured when it moves.
+long long g_buf_gen = 0;
+
 template <class T>
 struct DevBuf {
     T* p = nullptr;
     size_t n = 0;
     cudaError_t ensure(size_t count) {
         if (count <= n && p) return cudaSuccess;
+        ++g_buf_gen;
         if (p) cudaFree(p);
         p = nullptr;
         n = 0;
@@ -71,6 +76,7 @@ struct DevBuf {
         return e;
     }
     void release() {
+        if (p) ++g_buf_gen;
         if (p) cudaFree(p);
         p = nullptr;
         n = 0;
@@ -166,7 +172,19 @@ struct occ_handle {
     TmapBox tmG_k, tmW2o, tmP_k, tmW1o, tmH_mn, tmG_mn, tmX_mn, tmP_mn;
     int bwd_tmaps_q = -1;
     // host-buffer pipeline (occ_forward_host)
-    cudaStream_t s_in = nullptr, s_out = nullptr;
+    cudaStream_t s_in = nullptr, s_out = nullptr, s_cap = nullptr;
+    // per staging slot: the layer on that slot captured as a CUDA graph
+    // (validation off, world_size 1), re-captured when the call changes
+    struct HostGraph {
+        cudaGraphExec_t exec = nullptr;
+        int n = -1;
+        const void* gate = nullptr;
+        occ_prune prune{};
+        bool has_prune = false;
+        int chunks = 0;
+        long long gen = -1;  // g_buf_gen at capture
+        int training = 0;
+    } hgraph[2];
     std::vector<cudaEvent_t> pev;
     DevBuf<__nv_bfloat16> x_stage, o_stage;
     long long host_calls = 0;
@@ -779,6 +797,9 @@ occ_status occ_destroy(occ_handle* h) {
         if (e) cudaEventDestroy(e);
     for (auto& e : h->pev) cudaEventDestroy(e);
     delete h->tp;
+    for (auto& hg : h->hgraph)
+        if (hg.exec) cudaGraphExecDestroy(hg.exec);
+    if (h->s_cap) cudaStreamDestroy(h->s_cap);
     if (h->s_in) cudaStreamDestroy(h->s_in);
     if (h->s_out) cudaStreamDestroy(h->s_out);
     h->x_stage.release();
@@ -1300,6 +1321,7 @@ occ_status occ_forward_host(occ_handle* h, const void* x_host, const void* gate,
         CUDA_TRY(h->x_stage.ensure(2 * slot_elems));
         CUDA_TRY(h->o_stage.ensure(2 * slot_elems));
         h->host_slot_used[0] = h->host_slot_used[1] = false;
+        for (auto& g : h->hgraph) g.n = -1;  // buffers moved: re-capture
     }
     if (!h->s_in) {
         CUDA_TRY(cudaStreamCreateWithFlags(&h->s_in, cudaStreamNonBlocking));
@@ -1321,6 +1343,45 @@ occ_status occ_forward_host(occ_handle* h, const void* x_host, const void* gate,
     }
     const char* xh = reinterpret_cast<const char*>(x_host);
     char* oh = reinterpret_cast<char*>(out_host);
+    // With validation off (no host synchronisation inside the layer) and all
+    // devices local, the layer of each (slot, chunk) replays as a CUDA graph:
+    // small batches are otherwise bound by the ~20 kernel launches per call.
+    auto& hg = h->hgraph[slot];
+    const bool use_graph = !h->validate && h->world == 1 && !h->profiling && chunks == 1 && n > 0;
+    if (use_graph) {
+        const bool same = hg.exec && hg.n == n && hg.gate == gate && hg.chunks == chunks && hg.gen == g_buf_gen &&
+                          hg.training == h->training &&
+                          hg.has_prune == (prune != nullptr) &&
+                          (!prune || memcmp(&hg.prune, prune, sizeof(occ_prune)) == 0);
+        if (!same) {
+            if (hg.exec) cudaGraphExecDestroy(hg.exec);
+            hg.exec = nullptr;
+            if (!h->s_cap) CUDA_TRY(cudaStreamCreateWithFlags(&h->s_cap, cudaStreamNonBlocking));
+            auto* xs = h->x_stage.p + base_el;
+            auto* os = h->o_stage.p + base_el;
+            // eager once (grows the workspace), then capture on the handle's stream
+            CUDA_TRY(cudaStreamSynchronize(st));
+            occ_status s = occ_forward_expert_parallel(h, xs, gate, prune, nullptr, n, os,
+                                                       reinterpret_cast<occ_stream_t>(h->s_cap));
+            if (s != OCC_OK) return s;
+            CUDA_TRY(cudaStreamSynchronize(h->s_cap));
+            cudaGraph_t graph;
+            CUDA_TRY(cudaStreamBeginCapture(h->s_cap, cudaStreamCaptureModeThreadLocal));
+            s = occ_forward_expert_parallel(h, xs, gate, prune, nullptr, n, os, reinterpret_cast<occ_stream_t>(h->s_cap));
+            cudaError_t ce = cudaStreamEndCapture(h->s_cap, &graph);
+            if (s != OCC_OK) return s;
+            CUDA_TRY(ce);
+            CUDA_TRY(cudaGraphInstantiate(&hg.exec, graph, 0));
+            cudaGraphDestroy(graph);
+            hg.gen = g_buf_gen;
+            hg.training = h->training;
+            hg.n = n;
+            hg.gate = gate;
+            hg.chunks = chunks;
+            hg.has_prune = prune != nullptr;
+            if (prune) hg.prune = *prune;
+        }
+    }
     int base = 0;
     for (int c = 0; c < chunks; ++c) {
         const int nc = n / chunks + (c < n % chunks ? 1 : 0);
@@ -1329,8 +1390,12 @@ occ_status occ_forward_host(occ_handle* h, const void* x_host, const void* gate,
         CUDA_TRY(cudaMemcpyAsync(xs, xh + base * row, nc * row, cudaMemcpyHostToDevice, h->s_in));
         CUDA_TRY(cudaEventRecord(ev[2 + 2 * c], h->s_in));
         CUDA_TRY(cudaStreamWaitEvent(st, ev[2 + 2 * c], 0));
-        occ_status s = occ_forward_expert_parallel(h, xs, gate, prune, nullptr, nc, os, stream);
-        if (s != OCC_OK) return s;
+        if (use_graph) {
+            CUDA_TRY(cudaGraphLaunch(hg.exec, st));
+        } else {
+            occ_status s = occ_forward_expert_parallel(h, xs, gate, prune, nullptr, nc, os, stream);
+            if (s != OCC_OK) return s;
+        }
         CUDA_TRY(cudaEventRecord(ev[3 + 2 * c], st));
         CUDA_TRY(cudaStreamWaitEvent(h->s_out, ev[3 + 2 * c], 0));
         CUDA_TRY(cudaMemcpyAsync(oh + base * row, os, nc * row, cudaMemcpyDeviceToHost, h->s_out));

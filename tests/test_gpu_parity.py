@@ -515,6 +515,27 @@ def test_forward_host_pipeline_matches_device(chunks):
     assert torch.equal(oh, want)
 
 
+def test_forward_host_graph_replay():
+    """Validation off: occ_forward_host replays the layer as a CUDA graph per
+    staging slot (captured once, re-captured when the batch shape or any
+    workspace buffer changes); results stay bit-identical across calls,
+    slots, new inputs, a batch-size change and a workspace regrow."""
+    ne, k, nd, dm, dh = 8, 2, 2, 256, 512
+    x, g, w1, w2, _ = make_layer_inputs(6, 1500, dm, dh, ne)
+    layer = occ.ExpertParallelLayer(occ.MoEConfig(ne, k, nd, dm, dh, activation="silu"))
+    layer.load_experts(cuda(w1, torch.bfloat16), cuda(w2, torch.bfloat16))
+    gs = cuda(g, torch.bfloat16)
+    layer.set_validate(False)
+    for n in (700, 700, 700, 300, 1500, 700):
+        xs = cuda(x[:n], torch.bfloat16) * (1 + n % 7)  # new values each time
+        want = layer.forward_expert_parallel(xs, gs).cpu()
+        xh = xs.cpu().pin_memory()
+        oh = torch.empty_like(xh).pin_memory()
+        layer.forward_host(xh, gs, oh)
+        torch.cuda.synchronize()
+        assert torch.equal(oh, want), n
+
+
 # ------------------------------------------- world_size > 1 (loopback) -----
 
 @pytest.mark.parametrize("nd,ne,k,act,dedup,shared", [(2, 8, 2, "silu", True, 0), (4, 16, 4, "silu", True, 0),
