@@ -576,54 +576,59 @@ __global__ void __launch_bounds__(256) combine_kernel(int n, int nd, int k, int 
 // expert) ordered by device ascending, then placement slot; every device's
 // partial sum is rounded to the bf16 return payload exactly as the
 // multi-GPU exchange would carry it, then summed over devices in fp32.
+// The token's row list is built warp-parallel (lane p reads row_epd[r, p],
+// ballot-compacted into shared memory); KU product rows are in flight per
+// 16-byte vector (KU = 2 / 4 / 8 picked from k at launch).
+template <int KU>
 __global__ void __launch_bounds__(256) combine_fused_kernel(int n, int nd, int k, int P, int dedup, int D,
                                                             const uint64_t* mask, const int32_t* tok_row,
                                                             const int32_t* row_epd, const __nv_bfloat16* Y,
                                                             const __nv_bfloat16* ys, __nv_bfloat16* out) {
+    __shared__ int s_q[8][kMaxTopK];
+    const int wib = threadIdx.x >> 5;
     const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (t >= n) return;
-    int qs[kMaxTopK];
-    bool newdev[kMaxTopK];
+    int* qs = s_q[wib];
+    uint64_t newdev = 0;  // bit i: entry i opens a new device group
     int nq = 0;
+    const uint32_t lt = (1u << lane) - 1u;
+    auto add_row = [&](int r) {  // the row's local experts, placement order
+        for (int p0 = 0; p0 < P; p0 += 32) {
+            const int q = p0 + lane < P ? row_epd[(long)r * P + p0 + lane] : -1;
+            const uint32_t b = __ballot_sync(0xffffffffu, q >= 0);
+            if (q >= 0 && nq + __popc(b & lt) < kMaxTopK) qs[nq + __popc(b & lt)] = q;
+            nq += __popc(b);
+        }
+    };
     if (dedup) {
         uint64_t m = mask[t];
         while (m) {
             const int d = __ffsll(m) - 1;
             m &= m - 1;
-            const int r = tok_row[(long)t * nd + d];
-            bool first = true;
-            for (int p = 0; p < P && nq < kMaxTopK; ++p) {
-                const int q = row_epd[(long)r * P + p];
-                if (q < 0) continue;
-                qs[nq] = q;
-                newdev[nq++] = first;
-                first = false;
-            }
+            if (nq < 64) newdev |= 1ull << nq;
+            add_row(tok_row[(long)t * nd + d]);
         }
     } else {
         for (int j = 0; j < k; ++j) {
-            const int r = tok_row[(long)t * k + j];
-            for (int p = 0; p < P; ++p) {
-                const int q = row_epd[(long)r * P + p];
-                if (q >= 0) { qs[nq] = q; newdev[nq++] = true; }
-            }
+            if (nq < 64) newdev |= 1ull << nq;
+            add_row(tok_row[(long)t * k + j]);
         }
     }
-    // 16-byte vectors; all nq product rows of a vector loaded before the
-    // ordered sum (device ascending, placement order within a device)
+    nq = nq < kMaxTopK ? nq : kMaxTopK;
+    __syncwarp();
     const int nv = D / 8;
     for (int v = lane; v < nv; v += 32) {
         float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, dev[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        for (int i0 = 0; i0 < nq; i0 += 8) {
-            uint4 u[8];
+        for (int i0 = 0; i0 < nq; i0 += KU) {
+            uint4 u[KU];
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
+            for (int j = 0; j < KU; ++j)
                 if (i0 + j < nq) u[j] = __ldg(reinterpret_cast<const uint4*>(Y + (long)qs[i0 + j] * D) + v);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
+            for (int j = 0; j < KU; ++j) {
                 if (i0 + j >= nq) break;
-                if (i0 + j && newdev[i0 + j]) {
+                if (i0 + j && ((newdev >> (i0 + j)) & 1)) {
 #pragma unroll
                     for (int e = 0; e < 8; ++e) {
                         acc[e] += __bfloat162float(__float2bfloat16(dev[e]));
@@ -1254,7 +1259,13 @@ void launch_combine_fused(int n, int nd, int k, int P, int dedup, int D, const u
                           const int32_t* tok_row, const int32_t* row_epd, const __nv_bfloat16* Y,
                           const __nv_bfloat16* ys, __nv_bfloat16* out, cudaStream_t st) {
     if (!n) return;
-    combine_fused_kernel<<<(n + 7) / 8, 256, 0, st>>>(n, nd, k, P, dedup, D, mask, tok_row, row_epd, Y, ys, out);
+    const dim3 grid((n + 7) / 8);
+    if (k <= 2)
+        combine_fused_kernel<2><<<grid, 256, 0, st>>>(n, nd, k, P, dedup, D, mask, tok_row, row_epd, Y, ys, out);
+    else if (k <= 4)
+        combine_fused_kernel<4><<<grid, 256, 0, st>>>(n, nd, k, P, dedup, D, mask, tok_row, row_epd, Y, ys, out);
+    else
+        combine_fused_kernel<8><<<grid, 256, 0, st>>>(n, nd, k, P, dedup, D, mask, tok_row, row_epd, Y, ys, out);
     count_launch();
 }
 
