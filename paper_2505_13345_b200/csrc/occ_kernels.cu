@@ -372,23 +372,41 @@ __global__ void compute_finalize_kernel(int G, int P, const int* totals, Compute
 
 struct ComputeEmitter {
     EmitCompute e;
-    __device__ void group_rank(int, int, int) {}
+    uint32_t slots[2];  // k <= 8: local slot of routing entry j in byte j (0xFF: other device)
+    __device__ void group_rank(int r, int g, int) {
+        if (e.k > 8) return;
+        const int gdev = e.dev_base + g;
+        slots[0] = slots[1] = 0xFFFFFFFFu;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            if (j >= e.k) break;
+            const int ex = e.row_ids[(long)r * e.k + j];
+            if (ex >= 0 && e.dev_of[ex] == gdev) {
+                const uint32_t sh = 8 * (j & 3);
+                slots[j >> 2] = (slots[j >> 2] & ~(0xFFu << sh)) | ((uint32_t)e.slot_of[ex] << sh);
+            }
+        }
+    }
     __device__ void emit(int r, int g, int p, int rank) {
         const int q = e.o.seg_base[g * e.P + p] + rank;
         e.row_epd[(long)r * e.P + p] = q;
         e.epd_src[q] = r;
-        float wt = 0.0f;
         int jj = -1;
-        const int gdev = e.dev_base + g;
-        for (int j = 0; j < e.k; ++j) {
-            const int ex = e.row_ids[(long)r * e.k + j];
-            if (ex >= 0 && e.dev_of[ex] == gdev && e.slot_of[ex] == p) {
-                wt = e.row_w[(long)r * e.k + j];
-                jj = j;
-                break;
+        if (e.k <= 8) {  // slot -> routing entry from the packed bytes (no loads)
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                if (jj < 0 && ((slots[j >> 2] >> (8 * (j & 3))) & 0xFFu) == (uint32_t)p) jj = j;
+        } else {
+            const int gdev = e.dev_base + g;
+            for (int j = 0; j < e.k; ++j) {
+                const int ex = e.row_ids[(long)r * e.k + j];
+                if (ex >= 0 && e.dev_of[ex] == gdev && e.slot_of[ex] == p) {
+                    jj = j;
+                    break;
+                }
             }
         }
-        e.epd_w[q] = wt;
+        e.epd_w[q] = jj >= 0 ? e.row_w[(long)r * e.k + jj] : 0.0f;
         if (e.epd_j) e.epd_j[q] = jj;
     }
     __device__ void miss(int, int) {}  // row_epd is pre-filled with -1 (launch_rank_emit_compute)
