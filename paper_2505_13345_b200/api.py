@@ -18,7 +18,7 @@ from typing import Optional, Sequence
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libocc.so")
+LIB_PATH = os.environ.get("OCC_LIB_EXPERIMENT") or os.path.join(_HERE, "libocc.so")  # env: A/B builds (profiles/)
 
 # ---------------------------------------------------------------- errors ---
 # common.hpp:11-34 taxonomy; occ_status 1..6.

@@ -42,14 +42,21 @@ namespace occ {
 namespace {
 
 constexpr int BM = 128;               // rows per CTA (pair tile: 256)
-constexpr int BN = 256, BK = 64, STAGES = 6;
+#ifndef OCC_GEMM_STAGES
+#define OCC_GEMM_STAGES 6
+#endif
+#ifndef OCC_STG_PER_WARP
+#define OCC_STG_PER_WARP 1
+#endif
+constexpr int BN = 256, BK = 64, STAGES = OCC_GEMM_STAGES;
 constexpr int A_BYTES = BM * BK * 2;  // 16 KB
 constexpr int B_BYTES = (BN / 2) * BK * 2;  // 16 KB: this CTA's half of the B tile
 // Epilogue staging for TMA stores: per epilogue warp two 32-row x 32-column
 // bf16 buffers (2 KB each, 64-byte swizzle) = 16 KB.
 constexpr int EPI_WARPS = 8;  // two per TMEM lane quarter, each on half of the tile's columns
 constexpr int STG_BYTES = 2048;
-constexpr int EPI_STAGE_BYTES = EPI_WARPS * STG_BYTES;
+constexpr int STG_PER_WARP = OCC_STG_PER_WARP;  // staging buffers per epilogue warp (TMA stores in flight)
+constexpr int EPI_STAGE_BYTES = EPI_WARPS * STG_PER_WARP * STG_BYTES;
 constexpr int SMEM_BYTES = STAGES * (A_BYTES + B_BYTES) + EPI_STAGE_BYTES + 256;
 constexpr int THREADS = 64 + 32 * 8;  // producer + MMA + EPI_WARPS epilogue warps
 constexpr int MAX_GROUPS = 256;
@@ -420,6 +427,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+            bool released = false;  // TMEM buffer handed back to the MMA warp early
             if constexpr (WGRAD) {
                 // dW[e][m][n] = sum over the expert's rows; every tile is complete
                 int g, mt, nt;
@@ -473,7 +481,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                     const int F = p.N;
                     float gw = 0.f;
                     const long rowbase = row - lane;
-                    uint8_t* stg = sC + (warp - 2) * STG_BYTES;
+                    uint8_t* stg = sC + (warp - 2) * STG_PER_WARP * STG_BYTES;
                     __nv_bfloat16* outb = reinterpret_cast<__nv_bfloat16*>(p.out) + rowbase * p.ldo;
 #pragma unroll 1
                     for (int c = hsel * (BN / 64); c < (hsel + 1) * (BN / 64); ++c) {
@@ -526,29 +534,42 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 } else {
                     const float wr = p.row_w ? p.row_w[row] : 1.0f;
                     __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out) + row * p.ldo;
-                    constexpr int NCH = EPI == EPI_SWIGLU_BF16 ? 4 : BN / 32;
-                    const int ncol = EPI == EPI_SWIGLU_BF16 ? 128 : BN;
-#pragma unroll 1
-                    for (int c = hsel * (NCH / 2); c < (hsel + 1) * (NCH / 2); ++c) {
-                        uint32_t v[32];
+                    constexpr bool SW = EPI == EPI_SWIGLU_BF16;
+                    constexpr int NCH = SW ? 4 : BN / 32;  // 32-column chunks per tile
+                    constexpr int MY = NCH / 2;            // this warp's half
+                    const int ncol = SW ? 128 : BN;
+                    // all of this warp's accumulator columns to registers first, then
+                    // release the TMEM buffer: the MMAs of tile i+2 no longer wait for
+                    // this tile's math and stores (short-K GEMMs were epilogue-bound)
+                    uint32_t v[MY][32], g[SW ? MY : 1][32];
+#pragma unroll
+                    for (int cc = 0; cc < MY; ++cc) {
+                        const int c = hsel * MY + cc;
+                        tmem_ld32(tbase + c * 32, v[cc]);
+                        if constexpr (SW) tmem_ld32(tbase + 128 + c * 32, g[cc]);
+                    }
+                    tmem_ld_wait();
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster(smem_u32(&tempty[acc]) & kPeerBitMask);
+                    released = true;
+#pragma unroll
+                    for (int cc = 0; cc < MY; ++cc) {
+                        const int c = hsel * MY + cc;
                         float h[32];
                         const int col0 = nb * ncol + c * 32;
-                        tmem_ld32(tbase + c * 32, v);
-                        if constexpr (EPI == EPI_SWIGLU_BF16) {
-                            uint32_t g[32];
-                            tmem_ld32(tbase + 128 + c * 32, g);
-                            tmem_ld_wait();
+                        if constexpr (SW) {
                             if (p.save_a && col0 < p.N) {  // training: keep a = x w1, b = x w3
                                 float fa[32], fb[32];
 #pragma unroll
                                 for (int i = 0; i < 32; ++i) {
-                                    fa[i] = __uint_as_float(v[i]);
-                                    fb[i] = __uint_as_float(g[i]);
+                                    fa[i] = __uint_as_float(v[cc][i]);
+                                    fb[i] = __uint_as_float(g[cc][i]);
                                 }
                                 // coalesced through the warp's staging buffer (free once
                                 // the previous TMA store has read it)
-                                uint8_t* stg = sC + (warp - 2) * STG_BYTES;
-                                if (lane == 0) bulk_wait_read<0>();
+                                uint8_t* stg = sC + ((warp - 2) * STG_PER_WARP + stg_n % STG_PER_WARP) * STG_BYTES;
+                                if (lane == 0) bulk_wait_read<STG_PER_WARP - 1>();
                                 __syncwarp();
                                 const long rb = row - lane;
                                 row_to_global(stg, fa, p.save_a + rb * p.N + col0, p.N, p.N - col0, lane);
@@ -556,28 +577,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                             }
 #pragma unroll
                             for (int i = 0; i < 32; ++i)
-                                h[i] = silu(__uint_as_float(v[i])) * __uint_as_float(g[i]) * wr;
+                                h[i] = silu(__uint_as_float(v[cc][i])) * __uint_as_float(g[cc][i]) * wr;
                         } else {
-                            tmem_ld_wait();
                             if (p.save_a && col0 < p.N) {  // training: keep the pre-activation
                                 float fa[32];
 #pragma unroll
-                                for (int i = 0; i < 32; ++i) fa[i] = __uint_as_float(v[i]);
-                                uint8_t* stg = sC + (warp - 2) * STG_BYTES;
-                                if (lane == 0) bulk_wait_read<0>();
+                                for (int i = 0; i < 32; ++i) fa[i] = __uint_as_float(v[cc][i]);
+                                uint8_t* stg = sC + ((warp - 2) * STG_PER_WARP + stg_n % STG_PER_WARP) * STG_BYTES;
+                                if (lane == 0) bulk_wait_read<STG_PER_WARP - 1>();
                                 __syncwarp();
                                 row_to_global(stg, fa, p.save_a + (row - lane) * p.N + col0, p.N, p.N - col0, lane);
                             }
 #pragma unroll
-                            for (int i = 0; i < 32; ++i) h[i] = act_f(__uint_as_float(v[i]), p.act) * wr;
+                            for (int i = 0; i < 32; ++i) h[i] = act_f(__uint_as_float(v[cc][i]), p.act) * wr;
                         }
                         if (col0 < p.N && !p.nostore) {
                             if (p.tma_out) {
                                 // coalesced: stage the warp's 32 x 32 bf16 block in smem
                                 // (64-byte swizzle: 16-byte chunk u of row r at u ^ ((r >> 1) & 3)),
-                                // one TMA store per block; two buffers per warp rotate
-                                uint8_t* stg = sC + (warp - 2) * STG_BYTES;
-                                if (lane == 0) bulk_wait_read<0>();
+                                // one TMA store per block
+                                uint8_t* stg = sC + ((warp - 2) * STG_PER_WARP + stg_n % STG_PER_WARP) * STG_BYTES;
+                                if (lane == 0) bulk_wait_read<STG_PER_WARP - 1>();
                                 __syncwarp();
 #pragma unroll
                                 for (int u = 0; u < 4; ++u) {
@@ -602,9 +622,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                     }
                 }
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(smem_u32(&tempty[acc]) & kPeerBitMask);
+            if (!released) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(smem_u32(&tempty[acc]) & kPeerBitMask);
+            }
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
         if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
