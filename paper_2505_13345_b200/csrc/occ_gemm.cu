@@ -34,6 +34,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdlib.h>
+#include <stdio.h>
 
 #include "occ_common.cuh"
 #include "occ_internal.h"
@@ -95,6 +96,7 @@ struct Params {
     int hint_a, hint_b;  // L2 policy of the A / B loads (0 = none)
     int nostore;         // experiment: skip the bf16 output stores (timing only)
     int tma_out;         // bf16 forward outputs leave through smem + TMA stores (tmC)
+    unsigned long long* dbg;  // OCC_GEMM_DEBUG: per-CTA stall cycles [cta][4]
     const int* a_rows;   // non-null: A row q of the padded Epd layout is row a_rows[q] of tmA
                          // (tile::gather4, box 64 x 1; -1 = zero padding row)
 };
@@ -345,7 +347,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                     by = wi * p.b_rows_per_e + nb * BN + rank * (BN / 2);
                 }
                 for (int kb = 0; kb < KB; ++kb) {
+                    { const long long t0 = p.dbg ? clock64() : 0;
                     mbar_wait(&empty[stage], phase ^ 1);
+                    if (p.dbg) p.dbg[blockIdx.x * 4 + 0] += clock64() - t0; }
                     const uint32_t lbar = smem_u32(&full[stage]) & kPeerBitMask;
                     if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * (A_BYTES + B_BYTES));
                     uint8_t* a_dst = sA + stage * A_BYTES;
@@ -381,11 +385,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                     wtile_coords(tile, s_gmb, p.ngroups, NB, g, mt, nt);
                     KB = s_kbn[g];
                 }
+                { const long long t0 = p.dbg ? clock64() : 0;
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
+                if (p.dbg && lane == 0) p.dbg[blockIdx.x * 4 + 1] += clock64() - t0; }
                 tc_fence_after();
                 const uint32_t d_tmem = tmem_base + acc * BN;
                 for (int kb = 0; kb < KB; ++kb) {
+                    { const long long t0 = p.dbg ? clock64() : 0;
                     mbar_wait(&full[stage], phase);
+                    if (p.dbg && lane == 0) p.dbg[blockIdx.x * 4 + 2] += clock64() - t0; }
                     tc_fence_after();
                     if (lane == 0) {
                         const uint32_t a0 = smem_u32(sA + stage * A_BYTES);
@@ -424,7 +432,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 const long rowbase0 = (long)mb0 * 2 * BM + rank * BM + q * 32;
                 load_pre_chunk<EPI>(p, rowbase0, nb0 * BN + hsel * (BN / 64) * 32, lane, pa_cur, pb_cur);
             }
+            { const long long t0 = p.dbg ? clock64() : 0;
             mbar_wait(&tfull[acc], acc_phase);
+            if (p.dbg && lane == 0 && warp == 2) p.dbg[blockIdx.x * 4 + 3] += clock64() - t0; }
             tc_fence_after();
             const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
             bool released = false;  // TMEM buffer handed back to the MMA warp early
@@ -706,6 +716,13 @@ void launch_grouped_gemm(EpiMode mode, const GemmArgs& a, int num_sms, cudaStrea
     p.pre_b = a.pre_b;
     p.gw_part = a.gw_part;
     p.a_rows = a.a_rows;
+    static const bool dbg_on = getenv("OCC_GEMM_DEBUG") != nullptr;
+    static unsigned long long* dbg_buf = nullptr;
+    if (dbg_on) {
+        if (!dbg_buf) cudaMalloc(&dbg_buf, sizeof(unsigned long long) * 4 * 1024);
+        cudaMemsetAsync(dbg_buf, 0, sizeof(unsigned long long) * 4 * 1024, st);
+        p.dbg = dbg_buf;
+    }
     const CUtensorMap& ta = *reinterpret_cast<const CUtensorMap*>(a.tmap_a);
     const CUtensorMap& tb = *reinterpret_cast<const CUtensorMap*>(a.tmap_b);
     static const int tma_store_env = getenv("OCC_GEMM_TMASTORE") ? atoi(getenv("OCC_GEMM_TMASTORE")) : 1;
@@ -739,6 +756,19 @@ void launch_grouped_gemm(EpiMode mode, const GemmArgs& a, int num_sms, cudaStrea
         case EPI_BWD_ACT: launch_one<EPI_BWD_ACT, false>(grid, ta, tb, tc, p, st); break;
         case EPI_BWD_SWIGLU: launch_one<EPI_BWD_SWIGLU, false>(grid, ta, tb, tc, p, st); break;
         case EPI_WGRAD: launch_one<EPI_F32, true>(grid, ta, tb, tc, p, st); break;
+    }
+    if (dbg_on) {  // stall-cycle breakdown, averaged over CTAs (diagnostics only)
+        unsigned long long h[4 * 1024];
+        cudaStreamSynchronize(st);
+        cudaMemcpy(h, dbg_buf, sizeof(unsigned long long) * 4 * grid, cudaMemcpyDeviceToHost);
+        double sum[4] = {0, 0, 0, 0};
+        int nl = 0;
+        for (int c = 0; c < grid; ++c) {
+            for (int i = 0; i < 4; ++i) sum[i] += (double)h[c * 4 + i];
+            nl += (c % 2 == 0);
+        }
+        fprintf(stderr, "[gemm dbg] mode=%d K=%d N=%d: producer-empty %.0f, mma-tempty %.0f, mma-full %.0f, epi-tfull %.0f (kcycles/CTA)\n",
+                (int)mode, a.K, a.N, sum[0] / grid / 1e3, sum[1] / nl / 1e3, sum[2] / nl / 1e3, sum[3] / grid / 1e3);
     }
     count_launch();
 }
