@@ -38,14 +38,14 @@ WORKLOADS = {
                name="single MoE layer, 8 experts top-2, d=512, d_ff=1024, 2048 tokens, 2 simulated EP ranks "
                     "(reference CPU oracle shape; 2-matrix SiLU experts)"),
     "deepseek": dict(E=64, k=6, D=2048, F=1408, act="swiglu", tokens=16384, nd_sim=1, plan_ep=8, train=False,
-                     prune=None, shared=(2, 1408, False),
+                     prune=None, shared=(2, 1408, False), coactivation_placement=True,
                      name="DeepSeek-MoE-16B layer (64 routed experts top-6 + 2 shared experts, d=2048, ffn=1408, "
                           "SwiGLU) 16384 tokens"),
     "olmoe": dict(E=64, k=8, D=2048, F=1024, act="swiglu", tokens=65536, nd_sim=1, plan_ep=8, train=True,
                   prune=None, name="OLMoE-1B-7B layer (64 experts top-8, d=2048, ffn=1024, SwiGLU) "
                                    "forward+backward at 65536 tokens/step"),
     "qwen": dict(E=60, k=4, D=2048, F=1408, act="swiglu", tokens=16384, nd_sim=4, plan_ep=4, train=False,
-                 prune=("router", 2), shared=(1, 5632, True),
+                 prune=("router", 2), shared=(1, 5632, True), extra_eps=(2, 8),
                  name="Qwen1.5-MoE-A2.7B layer (60 routed experts top-4, d=2048, ffn=1408, SwiGLU; + gated shared "
                       "expert ffn=5632) with collaboration pruning to <=2 devices/token, EP=4 simulated on one GPU"),
 }
@@ -431,19 +431,35 @@ def run_ours(args):
     if W["train"]:
         roofline["step_tflops_fwd_bwd"] = (flops1 + flops2 + train_flops) / (tot_ms / args.steps / 1e3) / 1e12
 
-    # --- all-to-all bytes/token: dedup vs naive top-k at the config's EP=8 ---
+    # --- all-to-all bytes/token: dedup vs naive top-k at the config's EP ------
+    def a2a_at(ep, placement=None):
+        e_pad = -(-E // ep) * ep  # Qwen's 60 experts at EP=8: 4 never-routed padding experts
+        plan = occ.ExpertParallelLayer(occ.MoEConfig(e_pad, K_TOP, ep, D, F, activation=W["act"]), placement)
+        if e_pad == E:
+            ids_, _ = plan.route(x, gate, prune=prune)
+        else:
+            base = occ.ExpertParallelLayer(occ.MoEConfig(E, K_TOP, 1, D, F, activation=W["act"]))
+            ids_, w_, sc = base.route(x, gate, want_scores=True)
+            if prune is not None:
+                sc = torch.cat([sc.double(), torch.zeros((sc.shape[0], e_pad - E), dtype=torch.float64,
+                                                         device=sc.device)], 1)
+                ids_, _ = plan.prune_routing(sc, ids_, w_.double(), prune)
+        plan.build_dispatch_index(ids_)
+        r = plan.comm_report(bytes_per_scalar=2)
+        return ids_, {"ep": ep, "payload": "bf16", "dedup_bytes_per_token": r.crossing_rows * D * 2 / n_local,
+                      "naive_bytes_per_token": r.naive_crossing_rows * D * 2 / n_local,
+                      "ratio": (r.crossing_rows / r.naive_crossing_rows) if r.naive_crossing_rows else None,
+                      "mean_replicas": r.mean_replicas, "intra_share": r.intra_share}
     ep = W["plan_ep"]
-    plan = occ.ExpertParallelLayer(occ.MoEConfig(E, K_TOP, ep, D, F, activation=W["act"]))
-    ids, w = plan.route(x, gate, prune=prune)
-    plan.build_dispatch_index(ids)
-    r8 = plan.comm_report(bytes_per_scalar=2)
-    a2a = {"ep": ep, "payload": "bf16", "dedup_bytes_per_token": r8.crossing_rows * D * 2 / n_local,
-           "naive_bytes_per_token": r8.naive_crossing_rows * D * 2 / n_local,
-           "ratio": (r8.crossing_rows / r8.naive_crossing_rows) if r8.naive_crossing_rows else None,
-           "mean_replicas": r8.mean_replicas, "intra_share": r8.intra_share,
-           "pruning": W["prune"],
-           "note": ("Mixtral at EP=8 hosts one expert per GPU: dedup == naive" if E == 8 and ep == 8 else
-                    "round-robin sources over the EP ranks; naive = one row per (token, expert)")}
+    ids8, a2a = a2a_at(ep)
+    a2a.update({"pruning": W["prune"],
+                "note": ("Mixtral at EP=8 hosts one expert per GPU: dedup == naive" if E == 8 and ep == 8 else
+                         "round-robin sources over the EP ranks; naive = one row per (token, expert)")})
+    if W.get("coactivation_placement"):  # config 3: Occult co-activation placement
+        pl = occ.collaboration_aware_placement([ids8], E, ep)
+        _, a2a["coactivation_placement"] = a2a_at(ep, pl)
+    for ep_x in W.get("extra_eps", ()):  # config 5: EP = 2 / 4 / 8
+        a2a.setdefault("by_ep", {})[ep_x] = a2a_at(ep_x)[1]
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline and args.workload == "mixtral":
