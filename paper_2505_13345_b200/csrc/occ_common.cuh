@@ -67,6 +67,13 @@ OCC_DEV void tma_gather4(void* smem_dst, const void* desc, uint64_t* bar, int x,
         : "memory");
 }
 
+// L2 prefetch of a 2-D tile (no smem, no completion): warms L2 ahead of the ring.
+OCC_DEV void tma_prefetch_l2(const void* desc, int x, int y) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                     reinterpret_cast<uint64_t>(desc)),
+                 "r"(x), "r"(y)
+                 : "memory");
+}
 // tile::gather4 into a CTA pair: completion on the leader CTA's barrier.
 OCC_DEV void tma_gather4_cg2(void* smem_dst, const void* desc, uint32_t bar_cluster, int x, int4 rows) {
     asm volatile(

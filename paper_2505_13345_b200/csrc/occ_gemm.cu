@@ -97,6 +97,7 @@ struct Params {
     int nostore;         // experiment: skip the bf16 output stores (timing only)
     int tma_out;         // bf16 forward outputs leave through smem + TMA stores (tmC)
     unsigned long long* dbg;  // OCC_GEMM_DEBUG: per-CTA stall cycles [cta][4]
+    int pf;                   // L2 prefetch distance in K blocks beyond the smem ring (0: off)
     const int* a_rows;   // non-null: A row q of the padded Epd layout is row a_rows[q] of tmA
                          // (tile::gather4, box 64 x 1; -1 = zero padding row)
 };
@@ -346,7 +347,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                     ay = mb * 2 * BM + rank * BM;
                     by = wi * p.b_rows_per_e + nb * BN + rank * (BN / 2);
                 }
+                // L2 prefetch p.pf K blocks ahead of the loads (into the next tile
+                // near the end of this one), so DRAM latency hides behind the ring
+                int n_ay = -1, n_by = -1;
+                if (!WGRAD && p.pf > 0) {
+                    if (tile + ncl < num_tiles) {
+                        int mb2, nb2, wi2;
+                        tile_coords(tile + ncl, s_gmb, s_gw, p.ngroups, NB, p.band, mb2, nb2, wi2);
+                        n_ay = mb2 * 2 * BM + rank * BM;
+                        n_by = wi2 * p.b_rows_per_e + nb2 * BN + rank * (BN / 2);
+                    }
+                    if (tile == cid)
+                        for (int kb = 0; kb < p.pf && kb < KB; ++kb) {
+                            tma_prefetch_l2(&tmA, kb * BK, ay);
+                            tma_prefetch_l2(&tmB, kb * BK, by);
+                        }
+                }
                 for (int kb = 0; kb < KB; ++kb) {
+                    if (!WGRAD && p.pf > 0) {
+                        const int pk = kb + p.pf;
+                        if (pk < KB) {
+                            tma_prefetch_l2(&tmA, pk * BK, ay);
+                            tma_prefetch_l2(&tmB, pk * BK, by);
+                        } else if (n_ay >= 0 && pk - KB < KB) {
+                            tma_prefetch_l2(&tmA, (pk - KB) * BK, n_ay);
+                            tma_prefetch_l2(&tmB, (pk - KB) * BK, n_by);
+                        }
+                    }
                     { const long long t0 = p.dbg ? clock64() : 0;
                     mbar_wait(&empty[stage], phase ^ 1);
                     if (p.dbg) p.dbg[blockIdx.x * 4 + 0] += clock64() - t0; }
@@ -716,6 +743,8 @@ void launch_grouped_gemm(EpiMode mode, const GemmArgs& a, int num_sms, cudaStrea
     p.pre_b = a.pre_b;
     p.gw_part = a.gw_part;
     p.a_rows = a.a_rows;
+    static const int pf_env = getenv("OCC_GEMM_PF") ? atoi(getenv("OCC_GEMM_PF")) : 0;
+    p.pf = a.a_rows ? 0 : pf_env;
     static const bool dbg_on = getenv("OCC_GEMM_DEBUG") != nullptr;
     static unsigned long long* dbg_buf = nullptr;
     if (dbg_on) {
