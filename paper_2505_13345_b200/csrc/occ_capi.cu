@@ -105,6 +105,21 @@ struct Transport {
                                  void* recv, const std::vector<size_t>& roff, const std::vector<size_t>& rcnt, int es,
                                  cudaStream_t st) = 0;
     virtual occ_status allreduce_i64(int64_t* buf, size_t count, cudaStream_t st) = 0;
+    // several all-to-alls with the same row layout (element sizes es[i]) as one exchange
+    struct Part {
+        const void* send;
+        void* recv;
+        int es;
+    };
+    virtual occ_status alltoallv_parts(const std::vector<Part>& parts, const std::vector<size_t>& soff,
+                                       const std::vector<size_t>& scnt, const std::vector<size_t>& roff,
+                                       const std::vector<size_t>& rcnt, cudaStream_t st) {
+        for (const Part& pt : parts) {
+            occ_status s = alltoallv(pt.send, soff, scnt, pt.recv, roff, rcnt, pt.es, st);
+            if (s != OCC_OK) return s;
+        }
+        return OCC_OK;
+    }
 };
 
 struct alignas(64) TmapBox {
@@ -231,6 +246,22 @@ struct NcclTransport : Transport {
     }
     occ_status allreduce_i64(int64_t* buf, size_t count, cudaStream_t st) override {
         NCCL_TRY(ncclAllReduce(buf, buf, count, ncclInt64, ncclSum, comm, st));
+        return OCC_OK;
+    }
+    // one NCCL group (one launch) for the token rows and their routing metadata
+    occ_status alltoallv_parts(const std::vector<Part>& parts, const std::vector<size_t>& soff,
+                               const std::vector<size_t>& scnt, const std::vector<size_t>& roff,
+                               const std::vector<size_t>& rcnt, cudaStream_t st) override {
+        NCCL_TRY(ncclGroupStart());
+        for (const Part& pt : parts) {
+            const char* sp = reinterpret_cast<const char*>(pt.send);
+            char* rp = reinterpret_cast<char*>(pt.recv);
+            for (int p = 0; p < world; ++p) {
+                if (scnt[p]) NCCL_TRY(ncclSend(sp + soff[p] * pt.es, scnt[p] * pt.es, ncclUint8, p, comm, st));
+                if (rcnt[p]) NCCL_TRY(ncclRecv(rp + roff[p] * pt.es, rcnt[p] * pt.es, ncclUint8, p, comm, st));
+            }
+        }
+        NCCL_TRY(ncclGroupEnd());
         return OCC_OK;
     }
 };
@@ -686,9 +717,10 @@ occ_status forward_multi(occ_handle* h, const __nv_bfloat16* x, const int32_t* i
         ro[p] = (size_t)inoff[p];
         rc[p] = (size_t)rcnt64[p];
     }
-    if ((s = tp->alltoallv(h->snd_x.p, so, sc, h->in_x.p, ro, rc, D * 2, st)) != OCC_OK) return s;
-    if ((s = tp->alltoallv(h->snd_ids.p, so, sc, h->in_ids.p, ro, rc, k * 4, st)) != OCC_OK) return s;
-    if ((s = tp->alltoallv(h->snd_w.p, so, sc, h->in_w.p, ro, rc, k * 4, st)) != OCC_OK) return s;
+    const std::vector<Transport::Part> parts{{h->snd_x.p, h->in_x.p, D * 2},
+                                             {h->snd_ids.p, h->in_ids.p, k * 4},
+                                             {h->snd_w.p, h->in_w.p, k * 4}};
+    if ((s = tp->alltoallv_parts(parts, so, sc, ro, rc, st)) != OCC_OK) return s;
     // 4. compute index over the received rows
     mark(h, ST_CINDEX, st);
     const int Rm = (int)std::max<long long>(R, 1);
