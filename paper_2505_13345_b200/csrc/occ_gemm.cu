@@ -143,19 +143,6 @@ __device__ __forceinline__ float act_grad(float v, int act) {  // backward.cpp:1
     return 1.f;
 }
 
-__device__ __forceinline__ void load_bf16x32(const __nv_bfloat16* p, float (&f)[32]) {
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-        const uint4 w = *reinterpret_cast<const uint4*>(p + 8 * u);
-        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const float2 x = __bfloat1622float2(h[q]);
-            f[8 * u + 2 * q] = x.x;
-            f[8 * u + 2 * q + 1] = x.y;
-        }
-    }
-}
 __device__ __forceinline__ void store_bf16x32(__nv_bfloat16* p, const float (&h)[32], int valid_cols) {
 #pragma unroll
     for (int u = 0; u < 4; ++u)

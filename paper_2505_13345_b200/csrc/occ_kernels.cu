@@ -503,81 +503,40 @@ __global__ void __launch_bounds__(256) zero_pad_rows_kernel(int NG, ComputeOffse
 // ------------------------------------------------------- partial combine --
 // merge_matmul's per-row sum over local experts (pipeline.cpp:263-281),
 // done after the grouped GEMM: ascending placement-list order, fp32.
-__device__ __forceinline__ float4 ld_bf16x4(const __nv_bfloat16* p) {
-    const uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
-    const float2 a = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
-    const float2 b = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
-    return make_float4(a.x, a.y, b.x, b.y);
-}
 
-__global__ void __launch_bounds__(256) partial_combine_kernel(int R_max, const int* R_total, int P, int D,
-                                                              const int32_t* row_epd, const __nv_bfloat16* Y,
-                                                              __nv_bfloat16* ret) {
-    const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (r >= *R_total) return;
-    int qs[kMaxLocal];
-    int nq = 0;
-    for (int p = 0; p < P; ++p) {
-        const int q = row_epd[(long)r * P + p];
-        if (q >= 0) qs[nq++] = q;
-    }
-    const int nv = D / 4;
-    for (int v = lane; v < nv; v += 32) {
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int i = 0; i < nq; ++i) {
-            const float4 y = ld_bf16x4(Y + (long)qs[i] * D + 4 * v);
-            acc.x += y.x; acc.y += y.y; acc.z += y.z; acc.w += y.w;
-        }
-        uint2 o;
-        o.x = pack_bf16(acc.x, acc.y);
-        o.y = pack_bf16(acc.z, acc.w);
-        reinterpret_cast<uint2*>(ret + (long)r * D)[v] = o;
-    }
-}
-
-// ---------------------------------------------------------------- combine --
-// combine (pipeline.cpp:285-300): Ori row = sum over devices ascending of
-// the returned rows; fp32 accumulation, bf16 out.
-__global__ void __launch_bounds__(256) combine_kernel(int n, int nd, int k, int dedup, int D, const uint64_t* mask,
-                                                      const int32_t* tok_row, const __nv_bfloat16* ret,
-                                                      const __nv_bfloat16* ys, __nv_bfloat16* out) {
-    const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (t >= n) return;
-    int rows[kMaxDev];
-    int nr = 0;
-    if (dedup) {
-        uint64_t m = mask[t];
-        while (m) {
-            const int d = __ffsll(m) - 1;
-            m &= m - 1;
-            rows[nr++] = tok_row[(long)t * nd + d];
-        }
-    } else {
-        for (int j = 0; j < k; ++j) rows[nr++] = tok_row[(long)t * k + j];
-    }
+// Sum of nq bf16 rows (indices in shared memory, summed in list order, fp32)
+// + an optional extra row, rounded to bf16: KU 16-byte row vectors in flight.
+template <int KU>
+__device__ __forceinline__ void sum_rows_ordered(const __nv_bfloat16* Y, const int* qs, int nq, int D, int lane,
+                                                 const __nv_bfloat16* extra, __nv_bfloat16* dst) {
     const int nv = D / 8;
     for (int v = lane; v < nv; v += 32) {
         float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        for (int i = 0; i < nr; ++i) {
-            const uint4 u = __ldg(reinterpret_cast<const uint4*>(ret + (long)rows[i] * D) + v);
-            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+        for (int i0 = 0; i0 < nq; i0 += KU) {
+            uint4 u[KU];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const float2 f = __bfloat1622float2(h[q]);
-                acc[2 * q] += f.x;
-                acc[2 * q + 1] += f.y;
+            for (int j = 0; j < KU; ++j)
+                if (i0 + j < nq) u[j] = __ldg(reinterpret_cast<const uint4*>(Y + (long)qs[i0 + j] * D) + v);
+#pragma unroll
+            for (int j = 0; j < KU; ++j) {
+                if (i0 + j >= nq) break;
+                const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&u[j]);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float2 f = __bfloat1622float2(hh[e]);
+                    acc[2 * e] += f.x;
+                    acc[2 * e + 1] += f.y;
+                }
             }
         }
-        if (ys) {  // shared experts, computed at the source: added last
-            const uint4 u = __ldg(reinterpret_cast<const uint4*>(ys + (long)t * D) + v);
-            const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+        if (extra) {
+            const uint4 w = __ldg(reinterpret_cast<const uint4*>(extra) + v);
+            const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&w);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const float2 f = __bfloat1622float2(h[q]);
-                acc[2 * q] += f.x;
-                acc[2 * q + 1] += f.y;
+            for (int e = 0; e < 4; ++e) {
+                const float2 f = __bfloat1622float2(hh[e]);
+                acc[2 * e] += f.x;
+                acc[2 * e + 1] += f.y;
             }
         }
         uint4 o;
@@ -585,8 +544,69 @@ __global__ void __launch_bounds__(256) combine_kernel(int n, int nd, int k, int 
         o.y = pack_bf16(acc[2], acc[3]);
         o.z = pack_bf16(acc[4], acc[5]);
         o.w = pack_bf16(acc[6], acc[7]);
-        reinterpret_cast<uint4*>(out + (long)t * D)[v] = o;
+        reinterpret_cast<uint4*>(dst)[v] = o;
     }
+}
+
+// Append the non-negative entries of idx[0..cnt) (lane-parallel, order kept)
+// to the warp's list qs[nq..]; returns the new length.
+__device__ __forceinline__ int warp_compact_append(const int32_t* idx, int cnt, int* qs, int nq, int cap, int lane) {
+    const uint32_t lt = (1u << lane) - 1u;
+    for (int p0 = 0; p0 < cnt; p0 += 32) {
+        const int q = p0 + lane < cnt ? idx[p0 + lane] : -1;
+        const uint32_t b = __ballot_sync(0xffffffffu, q >= 0);
+        const int pos = nq + __popc(b & lt);
+        if (q >= 0 && pos < cap) qs[pos] = q;
+        nq += __popc(b);
+    }
+    return nq < cap ? nq : cap;
+}
+
+// merge_matmul's per-row sum over local experts (pipeline.cpp:263-281),
+// done after the grouped GEMM: ascending placement-list order, fp32.
+template <int KU>
+__global__ void __launch_bounds__(256) partial_combine_kernel(int R_max, const int* R_total, int P, int D,
+                                                              const int32_t* row_epd, const __nv_bfloat16* Y,
+                                                              __nv_bfloat16* ret) {
+    __shared__ int s_q[8][kMaxLocal];
+    const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (r >= *R_total) return;
+    int* qs = s_q[threadIdx.x >> 5];
+    const int nq = warp_compact_append(row_epd + (long)r * P, P, qs, 0, kMaxLocal, lane);
+    __syncwarp();
+    sum_rows_ordered<KU>(Y, qs, nq, D, lane, nullptr, ret + (long)r * D);
+}
+
+// ---------------------------------------------------------------- combine --
+// combine (pipeline.cpp:285-300): Ori row = sum over devices ascending of
+// the returned rows; fp32 accumulation, bf16 out; shared-expert rows added last.
+template <int KU>
+__global__ void __launch_bounds__(256) combine_kernel(int n, int nd, int k, int dedup, int D, const uint64_t* mask,
+                                                      const int32_t* tok_row, const __nv_bfloat16* ret,
+                                                      const __nv_bfloat16* ys, __nv_bfloat16* out) {
+    __shared__ int s_q[8][kMaxDev];
+    const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (t >= n) return;
+    int* qs = s_q[threadIdx.x >> 5];
+    int nr = 0;
+    if (dedup) {  // devices ascending: tok_row of the devices in the token's mask
+        const uint64_t m = mask[t];
+        for (int d0 = 0; d0 < nd; d0 += 32) {
+            const int d = d0 + lane;
+            const int rr = d < nd && ((m >> d) & 1) ? tok_row[(long)t * nd + d] : -1;
+            const uint32_t b = __ballot_sync(0xffffffffu, rr >= 0);
+            const int pos = nr + __popc(b & ((1u << lane) - 1u));
+            if (rr >= 0 && pos < kMaxDev) qs[pos] = rr;
+            nr += __popc(b);
+        }
+        nr = nr < kMaxDev ? nr : kMaxDev;
+    } else {
+        nr = warp_compact_append(tok_row + (long)t * k, k, qs, 0, kMaxDev, lane);
+    }
+    __syncwarp();
+    sum_rows_ordered<KU>(ret, qs, nr, D, lane, ys ? ys + (long)t * D : nullptr, out + (long)t * D);
 }
 
 // world_size == 1: intra-device partial combine + return + combine in one
@@ -1262,14 +1282,24 @@ void launch_scatter_rows(int R_max, const int* R_total, int P, int D, const __nv
 void launch_partial_combine(int R_max, const int* R_total, int P, int D, const int32_t* row_epd,
                             const __nv_bfloat16* Y, __nv_bfloat16* ret, cudaStream_t st) {
     if (!R_max) return;
-    partial_combine_kernel<<<(R_max + 7) / 8, 256, 0, st>>>(R_max, R_total, P, D, row_epd, Y, ret);
+    if (P <= 2)
+        partial_combine_kernel<2><<<(R_max + 7) / 8, 256, 0, st>>>(R_max, R_total, P, D, row_epd, Y, ret);
+    else if (P <= 4)
+        partial_combine_kernel<4><<<(R_max + 7) / 8, 256, 0, st>>>(R_max, R_total, P, D, row_epd, Y, ret);
+    else
+        partial_combine_kernel<8><<<(R_max + 7) / 8, 256, 0, st>>>(R_max, R_total, P, D, row_epd, Y, ret);
     count_launch();
 }
 
 void launch_combine(int n, int nd, int k, int dedup, int D, const uint64_t* mask, const int32_t* tok_row,
                     const __nv_bfloat16* ret, const __nv_bfloat16* ys, __nv_bfloat16* out, cudaStream_t st) {
     if (!n) return;
-    combine_kernel<<<(n + 7) / 8, 256, 0, st>>>(n, nd, k, dedup, D, mask, tok_row, ret, ys, out);
+    if (k <= 2)
+        combine_kernel<2><<<(n + 7) / 8, 256, 0, st>>>(n, nd, k, dedup, D, mask, tok_row, ret, ys, out);
+    else if (k <= 4)
+        combine_kernel<4><<<(n + 7) / 8, 256, 0, st>>>(n, nd, k, dedup, D, mask, tok_row, ret, ys, out);
+    else
+        combine_kernel<8><<<(n + 7) / 8, 256, 0, st>>>(n, nd, k, dedup, D, mask, tok_row, ret, ys, out);
     count_launch();
 }
 
