@@ -504,7 +504,7 @@ def main():
     ap.add_argument("--e2e-chunks", type=int, default=1)
     ap.add_argument("--e2e-flush", action="store_true", help="flush L2 between e2e steps even for large layers")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--ref-tokens-per-thread", type=int, default=2)
+    ap.add_argument("--ref-tokens-per-thread", type=int, default=1)
     args = ap.parse_args()
     select_workload(args.workload)
     if args.tokens is None:
