@@ -508,7 +508,7 @@ int orc_forward_given_routing(const double* x, int n, int dm, const int* ids, co
                               int bytes_per_scalar, double cap_replicas, double* x_out,
                               orc_report* rep, int* dindex_out, int* inbox_token, int* inbox_source,
                               int* inbox_slot, int* cindex_out) {
-    if (nd > 64 || ne % nd) return ORC_CONFIG;
+    if (nd < 1 || nd > 64 || ne < 1 || ne % nd) return ORC_CONFIG;
     const int per = ne / nd;
     int* dev_of = (int*)malloc(sizeof(int) * (size_t)ne);
     if (orc_expert_to_device(plist, nd, per, dev_of)) { free(dev_of); return ORC_PLACEMENT; }
@@ -520,7 +520,7 @@ int orc_forward_given_routing(const double* x, int n, int dm, const int* ids, co
         for (int i = 0; i < per; ++i) slot_of[plist[d * per + i]] = i;
 
     /* source token lists, pipeline.cpp:384-388 */
-    int* ntok = (int*)calloc((size_t)nd, sizeof(int));
+    int* ntok = (int*)calloc((size_t)(unsigned)nd, sizeof(int));
     for (int t = 0; t < n; ++t) {
         if (sources[t] < 0 || sources[t] >= nd) { free(dev_of); free(slot_of); free(ntok); return ORC_SHAPE; }
         ntok[sources[t]]++;
