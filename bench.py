@@ -446,8 +446,11 @@ def run_ours(args):
                 ids_, _ = plan.prune_routing(sc, ids_, w_.double(), prune)
         plan.build_dispatch_index(ids_)
         r = plan.comm_report(bytes_per_scalar=2)
+        meta = 8 * K_TOP  # every dispatched row also carries its k ids (int32) + k weights (f32)
         return ids_, {"ep": ep, "payload": "bf16", "dedup_bytes_per_token": r.crossing_rows * D * 2 / n_local,
                       "naive_bytes_per_token": r.naive_crossing_rows * D * 2 / n_local,
+                      "dedup_bytes_per_token_with_metadata": r.crossing_rows * (D * 2 + meta) / n_local,
+                      "naive_bytes_per_token_with_metadata": r.naive_crossing_rows * (D * 2 + meta) / n_local,
                       "ratio": (r.crossing_rows / r.naive_crossing_rows) if r.naive_crossing_rows else None,
                       "mean_replicas": r.mean_replicas, "intra_share": r.intra_share}
     ep = W["plan_ep"]
