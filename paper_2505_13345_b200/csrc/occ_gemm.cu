@@ -663,6 +663,201 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     }
 }
 
+// ---------------------------------------------------------------------------
+// Wide tiles for the long-K forward GEMMs: one CTA pair computes a 256 x 512
+// super-tile as two 256 x 256 accumulators sharing each A K-block (both TMEM
+// halves, 512 columns).  Per CTA and K block it stages A 16 KB + 2 x B 16 KB =
+// 48 KB for two MMAs instead of 2 x 32 KB: 25% less L2 -> SM operand traffic.
+// The price is one accumulator buffer (no double buffering): the epilogue
+// drains it in two rounds and hands it back after the second round's TMEM
+// loads, so the MMAs of the next super-tile wait for about one round of
+// epilogue math — small against a K >= 2048 mainloop.  4-stage ring (192 KB).
+constexpr int W_STAGES = 4;
+constexpr int W_B2 = 2 * B_BYTES;  // both B halves of this CTA per stage
+constexpr int W_SMEM_BYTES = W_STAGES * (A_BYTES + W_B2) + EPI_STAGE_BYTES + 256;
+
+template <int EPI>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+    wide_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                     const __grid_constant__ CUtensorMap tmC, Params p) {
+    static_assert(EPI == EPI_ACT_BF16 || EPI == EPI_SWIGLU_BF16, "forward bf16 epilogues only");
+    constexpr bool SW = EPI == EPI_SWIGLU_BF16;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + W_STAGES * A_BYTES;
+    uint8_t* sC = sB + W_STAGES * W_B2;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sC + EPI_STAGE_BYTES);
+    uint64_t* empty = full + W_STAGES;
+    uint64_t* tfull = empty + W_STAGES;
+    uint64_t* tempty = tfull + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+    __shared__ int s_gmb[MAX_GROUPS + 1];
+    __shared__ int s_gw[MAX_GROUPS];
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const int NB = SW ? (p.N + 127) / 128 : (p.N + BN - 1) / BN;  // 256-row B blocks
+    const int NBW = NB / 2;                                        // super-tiles along N
+    for (int i = threadIdx.x; i <= p.ngroups; i += blockDim.x) s_gmb[i] = p.grp_mb[i];
+    for (int i = threadIdx.x; i < p.ngroups; i += blockDim.x) s_gw[i] = p.grp_w[i];
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
+        if (p.tma_out) tma_prefetch_desc(&tmC);
+        for (int s = 0; s < W_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(&tfull[0], 1);
+        mbar_init(&tempty[0], 2 * EPI_WARPS);
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc_cg2<512>(tmem_slot);
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const int num_tiles = s_gmb[p.ngroups] * NBW;
+    const int KB = (p.K + BK - 1) / BK;
+    const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+    if (warp == 0) {
+        if (lane == 0) {  // -------------------------------------------- TMA producer
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = cid; tile < num_tiles; tile += ncl) {
+                int mb, nbw, wi;
+                tile_coords(tile, s_gmb, s_gw, p.ngroups, NBW, p.band, mb, nbw, wi);
+                const int ay = mb * 2 * BM + rank * BM;
+                const int by0 = wi * p.b_rows_per_e + 2 * nbw * BN + rank * (BN / 2);
+                for (int kb = 0; kb < KB; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    const uint32_t lbar = smem_u32(&full[stage]) & kPeerBitMask;
+                    if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * (A_BYTES + W_B2));
+                    uint8_t* b_dst = sB + stage * W_B2;
+                    tma_load_2d_cg2(sA + stage * A_BYTES, &tmA, lbar, kb * BK, ay);
+                    tma_load_2d_cg2(b_dst, &tmB, lbar, kb * BK, by0);
+                    tma_load_2d_cg2(b_dst + B_BYTES, &tmB, lbar, kb * BK, by0 + BN);
+                    if (++stage == W_STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (rank == 0) {  // --------------------------------- MMA issuer (leader CTA)
+            constexpr uint32_t IDESC = idesc_bf16_f32(2 * BM, BN);
+            int stage = 0;
+            uint32_t phase = 0, acc_phase = 0;
+            for (int tile = cid; tile < num_tiles; tile += ncl) {
+                mbar_wait(&tempty[0], acc_phase ^ 1);
+                tc_fence_after();
+                for (int kb = 0; kb < KB; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    if (lane == 0) {
+                        const uint32_t a0 = smem_u32(sA + stage * A_BYTES);
+                        const uint32_t b0 = smem_u32(sB + stage * W_B2);
+#pragma unroll
+                        for (int k = 0; k < BK / 16; ++k) {
+                            const uint64_t ad = sdesc_k_sw128(a0 + k * 32);
+                            umma_bf16_cg2(tmem_base, ad, sdesc_k_sw128(b0 + k * 32), IDESC, (kb | k) != 0);
+                            umma_bf16_cg2(tmem_base + BN, ad, sdesc_k_sw128(b0 + B_BYTES + k * 32), IDESC,
+                                          (kb | k) != 0);
+                        }
+                        umma_commit_cg2_mc(&empty[stage]);
+                    }
+                    __syncwarp();
+                    if (++stage == W_STAGES) { stage = 0; phase ^= 1; }
+                }
+                if (lane == 0) umma_commit_cg2_mc(&tfull[0]);
+                __syncwarp();
+                acc_phase ^= 1;
+            }
+        }
+    } else {  // ------------------------------------------------------------ epilogue
+        const int q = warp & 3;            // TMEM lane quarter
+        const int t = (warp - 2) >> 2;     // which accumulator (256-column half of the super-tile)
+        uint8_t* stg = sC + (warp - 2) * STG_PER_WARP * STG_BYTES;
+        uint32_t acc_phase = 0;
+        constexpr int NCH = SW ? 4 : BN / 32;  // output chunks of 32 columns per accumulator
+        constexpr int HALF = NCH / 2;          // chunks per drain round (128 registers)
+        for (int tile = cid; tile < num_tiles; tile += ncl) {
+            int mb, nbw, wi;
+            tile_coords(tile, s_gmb, s_gw, p.ngroups, NBW, p.band, mb, nbw, wi);
+            mbar_wait(&tfull[0], acc_phase);
+            tc_fence_after();
+            const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + t * BN;
+            const long row = (long)mb * 2 * BM + rank * BM + q * 32 + lane;
+            const float wr = p.row_w ? p.row_w[row] : 1.0f;
+            const int nb = 2 * nbw + t;
+            const int ncol = SW ? 128 : BN;
+#pragma unroll 1
+            for (int round = 0; round < 2; ++round) {
+                uint32_t v[HALF][32], g[SW ? HALF : 1][32];
+#pragma unroll
+                for (int cc = 0; cc < HALF; ++cc) {
+                    const int c = round * HALF + cc;
+                    tmem_ld32(tbase + c * 32, v[cc]);
+                    if constexpr (SW) tmem_ld32(tbase + 128 + c * 32, g[cc]);
+                }
+                tmem_ld_wait();
+                if (round == 1) {  // every column is in registers: hand the accumulator back
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster(smem_u32(&tempty[0]) & kPeerBitMask);
+                }
+#pragma unroll
+                for (int cc = 0; cc < HALF; ++cc) {
+                    const int col0 = nb * ncol + (round * HALF + cc) * 32;
+                    float h[32];
+#pragma unroll
+                    for (int i = 0; i < 32; ++i)
+                        h[i] = SW ? silu(__uint_as_float(v[cc][i])) * __uint_as_float(g[cc][i]) * wr
+                                  : act_f(__uint_as_float(v[cc][i]), p.act) * wr;
+                    if (col0 >= p.N) continue;
+                    if (p.tma_out) {
+                        if (lane == 0) bulk_wait_read<0>();
+                        __syncwarp();
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            uint4 o;
+                            o.x = pack_bf16(h[8 * u + 0], h[8 * u + 1]);
+                            o.y = pack_bf16(h[8 * u + 2], h[8 * u + 3]);
+                            o.z = pack_bf16(h[8 * u + 4], h[8 * u + 5]);
+                            o.w = pack_bf16(h[8 * u + 6], h[8 * u + 7]);
+                            *reinterpret_cast<uint4*>(stg + lane * 64 + ((u ^ ((lane >> 1) & 3)) << 4)) = o;
+                        }
+                        fence_proxy_async();
+                        __syncwarp();
+                        if (lane == 0) {
+                            tma_store_2d(&tmC, stg, col0, (int)(row - lane));
+                            bulk_commit();
+                        }
+                    } else {
+                        store_bf16x32(reinterpret_cast<__nv_bfloat16*>(p.out) + row * p.ldo + col0, h, p.N - col0);
+                    }
+                }
+            }
+            acc_phase ^= 1;
+        }
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
+    tc_fence_before();
+    cluster_sync();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc_cg2<512>(tmem_base);
+    }
+}
+
+template <int EPI>
+void launch_wide(int grid, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const Params& p,
+                 cudaStream_t st) {
+    const int smem = W_SMEM_BYTES + 1024;
+    cudaFuncSetAttribute(wide_gemm_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    wide_gemm_kernel<EPI><<<grid, THREADS, smem, st>>>(ta, tb, tc, p);
+}
+
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -765,6 +960,19 @@ void launch_grouped_gemm(EpiMode mode, const GemmArgs& a, int num_sms, cudaStrea
     int grid = 2 * a.max_tiles < num_sms ? 2 * a.max_tiles : num_sms;
     grid &= ~1;  // CTA pairs
     if (grid <= 0) return;
+    // wide 256 x 512 super-tiles for long-K forward GEMMs (OCC_GEMM_WIDE: 0 off,
+    // 1 auto = K >= 2048 with an even number of 256-row B blocks, 2 force when even)
+    static const int wide_env = getenv("OCC_GEMM_WIDE") ? atoi(getenv("OCC_GEMM_WIDE")) : 1;
+    if ((mode == EPI_ACT_BF16 || mode == EPI_SWIGLU_BF16) && !a.a_rows && !a.save_a && !p.nostore) {
+        const int nbk = mode == EPI_SWIGLU_BF16 ? (a.N + 127) / 128 : (a.N + BN - 1) / BN;
+        const bool even = nbk % 2 == 0 && (mode != EPI_SWIGLU_BF16 || a.N % 128 == 0);
+        if (even && (wide_env == 2 || (wide_env == 1 && a.K >= 2048))) {
+            if (mode == EPI_ACT_BF16) launch_wide<EPI_ACT_BF16>(grid, ta, tb, tc, p, st);
+            else launch_wide<EPI_SWIGLU_BF16>(grid, ta, tb, tc, p, st);
+            count_launch();
+            return;
+        }
+    }
     switch (mode) {
         case EPI_ACT_BF16: launch_one<EPI_ACT_BF16, false>(grid, ta, tb, tc, p, st); break;
         case EPI_SWIGLU_BF16: launch_one<EPI_SWIGLU_BF16, false>(grid, ta, tb, tc, p, st); break;
