@@ -961,12 +961,12 @@ void launch_grouped_gemm(EpiMode mode, const GemmArgs& a, int num_sms, cudaStrea
     grid &= ~1;  // CTA pairs
     if (grid <= 0) return;
     // wide 256 x 512 super-tiles for long-K forward GEMMs (OCC_GEMM_WIDE: 0 off,
-    // 1 auto = K >= 2048 with an even number of 256-row B blocks, 2 force when even)
+    // 1 auto = K >= 1024 with an even number of 256-row B blocks, 2 force when even)
     static const int wide_env = getenv("OCC_GEMM_WIDE") ? atoi(getenv("OCC_GEMM_WIDE")) : 1;
     if ((mode == EPI_ACT_BF16 || mode == EPI_SWIGLU_BF16) && !a.a_rows && !a.save_a && !p.nostore) {
         const int nbk = mode == EPI_SWIGLU_BF16 ? (a.N + 127) / 128 : (a.N + BN - 1) / BN;
         const bool even = nbk % 2 == 0 && (mode != EPI_SWIGLU_BF16 || a.N % 128 == 0);
-        if (even && (wide_env == 2 || (wide_env == 1 && a.K >= 2048))) {
+        if (even && (wide_env == 2 || (wide_env == 1 && a.K >= 1024))) {
             if (mode == EPI_ACT_BF16) launch_wide<EPI_ACT_BF16>(grid, ta, tb, tc, p, st);
             else launch_wide<EPI_SWIGLU_BF16>(grid, ta, tb, tc, p, st);
             count_launch();
