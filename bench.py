@@ -419,7 +419,7 @@ def run_ours(args):
     if os.path.exists(tpath) and args.workload == "mixtral":
         with open(tpath) as f:
             traffic = json.load(f).get("bytes_per_launch")
-    roofline = {"kernel": "grouped_gemm_kernel<SWIGLU> (GEMM-1: x @ [w1|w3], silu*up*gate-weight epilogue)",
+    roofline = {"kernel": "wide_gemm_kernel<SWIGLU> (GEMM-1: x @ [w1|w3], 256x512 super-tiles, silu*up*gate-weight epilogue)",
                 "bound": "tensor", "achieved": tflops1, "peak": peak, "unit": "TFLOP/s", "frac": tflops1 / peak,
                 "peak_source": f"{peaks_src} bf16_tflops (burst)", "frac_of_sustained": tflops1 / peak_sus,
                 "traffic": traffic,
