@@ -1047,12 +1047,14 @@ occ_status occ_route(occ_handle* h, const void* x, const void* gate, int n, cons
         // logits = x g^T on tcgen05; softmax + top-k fused in the epilogue
         // unless pruning / score rows need the full rows (router_select)
         const int np = (h->E + 31) / 32 * 32;
-        const bool need_rows = p.mode != 0 || scores != nullptr || np > 128;
+        // router-score pruning runs in the epilogue too; similarity pruning and
+        // score rows go through router_select on the written logits
+        const bool need_rows = p.mode == OCC_PRUNE_SIMILARITY || scores != nullptr || np > 128;
         if (!make_tmap_2d(h->tmRX.bytes, x, h->D, n, 64, 128) ||
             !make_tmap_2d(h->tmRG.bytes, gate, h->D, h->E, 64, np))
             return fail(OCC_ERR_CUDA, "cuTensorMapEncodeTiled failed (router)");
         if (!launch_router_tc(h->tmRX.bytes, h->tmRG.bytes, n, h->D, h->E, h->k, h->cfg.renormalize, ids, weights,
-                              need_rows ? h->logits.p : nullptr, h->num_sms, st))
+                              need_rows ? h->logits.p : nullptr, h->num_sms, st, need_rows ? nullptr : &p, h->err.p))
             return fail(OCC_ERR_UNSUPPORTED, "router: E <= 256 and k <= 64");
         if (need_rows)
             launch_router_select(h->logits.p, n, h->E, h->k, h->cfg.renormalize, p, ids, weights, scores, h->err.p,

@@ -208,8 +208,12 @@ void launch_prune_f64(const double* s, int n, int e, int k, const int32_t* ids_i
                       int32_t* ids, double* w, int32_t* err, cudaStream_t st);
 // Tensor-core router (occ_router.cu): returns false when the shape needs the
 // logits path (E > 128 without logits_out, or k > 64).
+// prune (nullable): router-score pruning (mode 1) runs in the epilogue;
+// err receives CapacityError (5).
+struct PruneDev;
 bool launch_router_tc(const void* tmap_x, const void* tmap_g, int n, int d, int e, int k, int renorm, int32_t* ids,
-                      float* w, float* logits_out, int num_sms, cudaStream_t st);
+                      float* w, float* logits_out, int num_sms, cudaStream_t st, const PruneDev* prune = nullptr,
+                      int32_t* err = nullptr);
 void launch_router_select(float* logits, int n, int e, int k, int renorm, PruneDev p, int32_t* ids, float* w,
                           float* scores, int32_t* err, cudaStream_t st);
 

@@ -30,6 +30,10 @@ struct RouterParams {
     int32_t* ids;
     float* w;
     float* logits_out;  // non-null: write logits [n, e], skip the selection
+    // collaboration pruning in the epilogue (router-score mode, pruning.cpp:35-64)
+    int prune, budget, prune_renorm;
+    const int32_t* dev_of;  // [e]
+    int32_t* err;
 };
 
 template <int NPMAX>
@@ -47,6 +51,9 @@ __global__ void __launch_bounds__(RTHREADS, 1)
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __shared__ uint8_t s_dev[256];  // expert -> device (pruning)
+    if (p.prune)
+        for (int i = threadIdx.x; i < p.e; i += blockDim.x) s_dev[i] = (uint8_t)p.dev_of[i];
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmX);
         tma_prefetch_desc(&tmG);
@@ -172,6 +179,66 @@ __global__ void __launch_bounds__(RTHREADS, 1)
 #pragma unroll
                 for (int i = 0; i < 32; ++i)
                     v[c][i] = __float_as_uint(c * 32 + i < p.e ? __uint_as_float(v[c][i]) * inv : -1.0f);
+            if (p.prune) {
+                // prune_router_score (pruning.cpp:35-64) on the register row: the
+                // first `budget` distinct devices of the top-k in score order, then
+                // the k best experts on those devices.  Rounds walk the order
+                // (score desc, index asc) strictly after the previous pick.
+                uint64_t allowed = 0;
+                int na = 0;
+                float ls = 2.0f;
+                int lj = -1;
+                for (int r = 0; r < p.k; ++r) {
+                    float best = -2.0f;
+                    int bj = -1;
+#pragma unroll
+                    for (int c = 0; c < NCH; ++c)
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) {
+                            const int j = c * 32 + i;
+                            const float sv = __uint_as_float(v[c][i]);
+                            const bool after = sv < ls || (sv == ls && j > lj);
+                            if (after && sv > best) { best = sv; bj = j; }
+                        }
+                    ls = best;
+                    lj = bj;
+                    const uint64_t bit = 1ull << s_dev[bj];
+                    if (!(allowed & bit) && na < p.budget) { allowed |= bit; ++na; }
+                }
+                int32_t* ids = p.ids + (long)t * p.k;
+                float* wout = p.w + (long)t * p.k;
+                float tot = 0.f;
+                ls = 2.0f;
+                lj = -1;
+                for (int r = 0; r < p.k; ++r) {
+                    float best = -2.0f;
+                    int bj = -1;
+#pragma unroll
+                    for (int c = 0; c < NCH; ++c)
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) {
+                            const int j = c * 32 + i;
+                            const float sv = __uint_as_float(v[c][i]);
+                            const bool after = sv < ls || (sv == ls && j > lj);
+                            if (after && sv > best && j < p.e && ((allowed >> s_dev[j < p.e ? j : 0]) & 1)) {
+                                best = sv;
+                                bj = j;
+                            }
+                        }
+                    if (bj < 0) {  // CapacityError
+                        atomicExch(p.err, 5);
+                        break;
+                    }
+                    ids[r] = bj;
+                    wout[r] = best;
+                    tot += best;
+                    ls = best;
+                    lj = bj;
+                }
+                if (p.prune_renorm)
+                    for (int r = 0; r < p.k; ++r) wout[r] = wout[r] / tot;
+                continue;
+            }
             // top-k by (score desc, index asc): k argmax rounds over the
             // register-resident row (strict > in ascending index order keeps
             // the lower index on ties); selected entries become -1
@@ -223,11 +290,18 @@ void launch_router_np(const CUtensorMap& tx, const CUtensorMap& tg, const Router
 }  // namespace
 
 bool launch_router_tc(const void* tmap_x, const void* tmap_g, int n, int d, int e, int k, int renorm, int32_t* ids,
-                      float* w, float* logits_out, int num_sms, cudaStream_t st) {
+                      float* w, float* logits_out, int num_sms, cudaStream_t st, const PruneDev* prune,
+                      int32_t* err) {
     if (n <= 0) return true;
     const int np = (e + 31) / 32 * 32;
     if (np > 256 || k > kMaxTopK) return false;
-    RouterParams p{n, d, e, np, k, renorm, ids, w, logits_out};
+    RouterParams p{n, d, e, np, k, renorm, ids, w, logits_out, 0, 0, 0, nullptr, err};
+    if (prune && prune->mode == 1) {
+        p.prune = 1;
+        p.budget = prune->budget;
+        p.prune_renorm = prune->renorm;
+        p.dev_of = prune->dev_of;
+    }
     const CUtensorMap& tx = *reinterpret_cast<const CUtensorMap*>(tmap_x);
     const CUtensorMap& tg = *reinterpret_cast<const CUtensorMap*>(tmap_g);
     if (np > 128 && !logits_out) return false;  // wide gates: select in router_select

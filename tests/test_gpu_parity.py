@@ -410,6 +410,27 @@ def test_router_with_pruning_respects_budget():
     assert torch.allclose(w.sum(1), torch.ones(n, device="cuda"), atol=1e-5)
 
 
+@pytest.mark.parametrize("ne,k,nd,budget,renorm", [(64, 8, 8, 2, True), (60, 4, 4, 2, True), (16, 4, 4, 1, False),
+                                                   (128, 6, 8, 3, True), (32, 2, 2, 1, True)])
+def test_router_epilogue_pruning_matches_oracle(ne, k, nd, budget, renorm):
+    """Router-score pruning fused into the tcgen05 router's epilogue equals
+    prune_routing (pruning.cpp:35-64, oracle restatement) applied to the same
+    fp32 softmax rows, id for id; weights to fp32 rounding."""
+    dm, n = 256, 2000
+    x, g, *_ = make_layer_inputs(ne + k, n, dm, 8, ne)
+    plist = _placement(ne, nd, "shuffled", seed=budget)
+    layer = occ.ExpertParallelLayer(occ.MoEConfig(ne, k, nd, dm, 64, renormalize=renorm),
+                                    occ.Placement([list(r) for r in plist]))
+    xs, gs = cuda(x, torch.bfloat16), cuda(g, torch.bfloat16)
+    ids, w = layer.route(xs, gs, occ.PruneSpec("router", budget))
+    _, _, sc = layer.route(xs, gs, want_scores=True)
+    s64 = sc.double().cpu().numpy()
+    ids0, w0 = O.Port().topk_route(s64, k, renorm)
+    want_ids, want_w = O.Port().prune_routing(s64, ids0, w0, plist, "router", budget, renormalize=renorm)
+    assert np.array_equal(ids.cpu().numpy(), want_ids)
+    assert np.allclose(w.double().cpu().numpy(), want_w, rtol=2e-6, atol=1e-7)
+
+
 # --------------------------------------------------------- full-size checks --
 
 def test_c1_full_size_vs_reference_rows():
