@@ -809,6 +809,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #pragma unroll
                 for (int cc = 0; cc < HALF; ++cc) {
                     const int col0 = nb * ncol + (round * HALF + cc) * 32;
+                    if (p.save_a && col0 < p.N) {  // training: keep a = x w1 (and b = x w3), coalesced
+                        float fa[32];
+                        if (lane == 0) bulk_wait_read<0>();
+                        __syncwarp();
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) fa[i] = __uint_as_float(v[cc][i]);
+                        row_to_global(stg, fa, p.save_a + (row - lane) * p.N + col0, p.N, p.N - col0, lane);
+                        if constexpr (SW) {
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) fa[i] = __uint_as_float(g[cc][i]);
+                            row_to_global(stg, fa, p.save_b + (row - lane) * p.N + col0, p.N, p.N - col0, lane);
+                        }
+                    }
                     float h[32];
 #pragma unroll
                     for (int i = 0; i < 32; ++i)
@@ -963,7 +976,7 @@ void launch_grouped_gemm(EpiMode mode, const GemmArgs& a, int num_sms, cudaStrea
     // wide 256 x 512 super-tiles for long-K forward GEMMs (OCC_GEMM_WIDE: 0 off,
     // 1 auto = K >= 1024 with an even number of 256-row B blocks, 2 force when even)
     static const int wide_env = getenv("OCC_GEMM_WIDE") ? atoi(getenv("OCC_GEMM_WIDE")) : 1;
-    if ((mode == EPI_ACT_BF16 || mode == EPI_SWIGLU_BF16) && !a.a_rows && !a.save_a && !p.nostore) {
+    if ((mode == EPI_ACT_BF16 || mode == EPI_SWIGLU_BF16) && !a.a_rows && !p.nostore) {
         const int nbk = mode == EPI_SWIGLU_BF16 ? (a.N + 127) / 128 : (a.N + BN - 1) / BN;
         const bool even = nbk % 2 == 0 && (mode != EPI_SWIGLU_BF16 || a.N % 128 == 0);
         if (even && (wide_env == 2 || (wide_env == 1 && a.K >= 1024))) {

@@ -656,9 +656,10 @@ def test_backward_matches_reference(ne, k, nd, dm, dh, act, n):
     assert max(errs.values()) <= 2e-2, errs
 
 
-def test_backward_swiglu_matches_autograd():
+@pytest.mark.parametrize("dm,dh", [(128, 256), (1024, 512)])  # (1024, 512): wide-tile GEMMs with saved pre-activations
+def test_backward_swiglu_matches_autograd(dm, dh):
     """SwiGLU extension: against torch autograd in fp64 on the CPU."""
-    ne, k, nd, dm, dh, n = 8, 2, 2, 128, 256, 300
+    ne, k, nd, n = 8, 2, 2, 300
     x, g, w1, w2, w3 = make_layer_inputs(11, n, dm, dh, ne, gated=True)
     ids, w = random_routing(n, ne, k, np.random.default_rng(5))
     w = w.astype(np.float32).astype(np.float64)
