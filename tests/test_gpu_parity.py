@@ -178,6 +178,8 @@ FWD_CASES = [
     (64, 8, 8, 128, 64, "silu", 400, "shuffled"),
     (4, 4, 2, 32, 32, "silu", 50, "trivial"),
     (8, 1, 8, 64, 64, "silu", 129, "trivial"),
+    (8, 2, 2, 40, 72, "silu", 100, "shuffled"),       # D, F multiples of 8 only (TMA zero-fills the K tail)
+    (8, 2, 2, 1024, 1800, "relu", 300, "trivial"),   # wide super-tiles with a ragged last N block
 ]
 
 
