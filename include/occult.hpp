@@ -94,7 +94,30 @@ class Layer {
     void load_experts(const void* w1, const void* w2, const void* w3, occ_stream_t s) {
         check(occ_load_experts(h_, w1, w3, w2, s), "load_experts");
     }
+    // DeepSeek / Qwen shared experts (not in the reference): w1/w3 [S, D, F_s], w2 [S, F_s, D],
+    // gate [D] or nullptr; num_shared = 0 detaches them.
+    void load_shared_experts(int num_shared, int d_ff_shared, const void* w1, const void* w2, const void* w3,
+                             const void* gate, occ_stream_t s) {
+        check(occ_load_shared_experts(h_, num_shared, d_ff_shared, w1, w3, w2, gate, s), "load_shared_experts");
+    }
     void set_validate(bool on) { check(occ_set_validate(h_, on), "set_validate"); }
+    void set_placement(const Placement& placement) {
+        std::vector<int32_t> flat;
+        for (const auto& d : placement.devices) flat.insert(flat.end(), d.begin(), d.end());
+        check(occ_set_placement(h_, flat.data()), "set_placement");
+    }
+    // Training: keep what backward_vjps (backward.cpp:24-161) needs; call before load_experts.
+    void set_training(bool on) { check(occ_set_training(h_, on), "set_training"); }
+    void backward(const void* upstream, float* g_x, float* g_w1, float* g_w3, float* g_w2, float* g_weights,
+                  occ_stream_t s) {
+        check(occ_backward(h_, upstream, g_x, g_w1, g_w3, g_w2, g_weights, s), "backward");
+    }
+    // End to end from pinned host memory (copies overlapped with the neighbouring calls).
+    void forward_host(const void* x_host, const void* gate, const occ_prune* prune, int n, void* out_host,
+                      occ_stream_t s) {
+        check(occ_forward_host(h_, x_host, gate, prune, n, out_host, 1, s), "forward_host");
+    }
+    void host_wait(occ_stream_t s) { check(occ_host_wait(h_, s), "host_wait"); }
 
     // forward_given_routing (pipeline.cpp:360-501)
     void forward_given_routing(const void* x, const int32_t* ids, const float* w, const int32_t* sources, int n,
