@@ -50,14 +50,6 @@ OCC_DEV void tma_load_2d(void* smem_dst, const void* desc, uint64_t* bar, int x,
         "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar)), "r"(x), "r"(y)
         : "memory");
 }
-// 2-D tiled load with an L2 cache-policy hint.
-OCC_DEV void tma_load_2d_hint(void* smem_dst, const void* desc, uint64_t* bar, int x, int y, uint64_t policy) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%3, "
-        "%4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
-        "l"(reinterpret_cast<uint64_t>(desc)), "r"(smem_u32(bar)), "r"(x), "r"(y), "l"(policy)
-        : "memory");
-}
 // Four gathered rows (tile::gather4): rows y0..y3 of `desc`, columns [x, x+box).
 OCC_DEV void tma_gather4(void* smem_dst, const void* desc, uint64_t* bar, int x, int y0, int y1, int y2, int y3) {
     asm volatile(
@@ -67,13 +59,6 @@ OCC_DEV void tma_gather4(void* smem_dst, const void* desc, uint64_t* bar, int x,
         : "memory");
 }
 
-// L2 prefetch of a 2-D tile (no smem, no completion): warms L2 ahead of the ring.
-OCC_DEV void tma_prefetch_l2(const void* desc, int x, int y) {
-    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
-                     reinterpret_cast<uint64_t>(desc)),
-                 "r"(x), "r"(y)
-                 : "memory");
-}
 // tile::gather4 into a CTA pair: completion on the leader CTA's barrier.
 OCC_DEV void tma_gather4_cg2(void* smem_dst, const void* desc, uint32_t bar_cluster, int x, int4 rows) {
     asm volatile(
@@ -102,23 +87,6 @@ OCC_DEV void tma_load_2d_cg2(void* smem_dst, const void* desc, uint32_t bar_clus
         "[%2];" ::"r"(smem_u32(smem_dst)),
         "l"(reinterpret_cast<uint64_t>(desc)), "r"(bar_cluster), "r"(x), "r"(y)
         : "memory");
-}
-OCC_DEV void tma_load_2d_cg2_hint(void* smem_dst, const void* desc, uint32_t bar_cluster, int x, int y,
-                                  uint64_t policy) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
-        "[%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(smem_dst)),
-        "l"(reinterpret_cast<uint64_t>(desc)), "r"(bar_cluster), "r"(x), "r"(y), "l"(policy)
-        : "memory");
-}
-// L2 eviction-priority policies for the .L2::cache_hint operand (kind: 1
-// evict_first, 2 evict_last, 3 evict_normal).
-OCC_DEV uint64_t l2_policy(int kind) {
-    uint64_t p = 0;
-    if (kind == 1) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-    else if (kind == 2) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
-    else asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
-    return p;
 }
 // 2-D tiled TMA store shared -> global (bulk-group completion).
 OCC_DEV void tma_store_2d(const void* desc, const void* smem_src, int x, int y) {

@@ -93,11 +93,8 @@ struct Params {
     const __nv_bfloat16* pre_a;  // backward epilogue inputs
     const __nv_bfloat16* pre_b;
     float* gw_part;
-    int hint_a, hint_b;  // L2 policy of the A / B loads (0 = none)
-    int nostore;         // experiment: skip the bf16 output stores (timing only)
     int tma_out;         // bf16 forward outputs leave through smem + TMA stores (tmC)
     unsigned long long* dbg;  // OCC_GEMM_DEBUG: per-CTA stall cycles [cta][4]
-    int pf;                   // L2 prefetch distance in K blocks beyond the smem ring (0: off)
     const int* a_rows;   // non-null: A row q of the padded Epd layout is row a_rows[q] of tmA
                          // (tile::gather4, box 64 x 1; -1 = zero padding row)
 };
@@ -318,7 +315,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            const uint64_t pol_a = l2_policy(p.hint_a), pol_b = l2_policy(p.hint_b);
             for (int tile = cid; tile < num_tiles; tile += ncl) {
                 int kb0 = 0, KB = KB_fwd, ax = 0, ay = 0, bx = 0, by = 0;
                 if constexpr (WGRAD) {
@@ -334,33 +330,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                     ay = mb * 2 * BM + rank * BM;
                     by = wi * p.b_rows_per_e + nb * BN + rank * (BN / 2);
                 }
-                // L2 prefetch p.pf K blocks ahead of the loads (into the next tile
-                // near the end of this one), so DRAM latency hides behind the ring
-                int n_ay = -1, n_by = -1;
-                if (!WGRAD && p.pf > 0) {
-                    if (tile + ncl < num_tiles) {
-                        int mb2, nb2, wi2;
-                        tile_coords(tile + ncl, s_gmb, s_gw, p.ngroups, NB, p.band, mb2, nb2, wi2);
-                        n_ay = mb2 * 2 * BM + rank * BM;
-                        n_by = wi2 * p.b_rows_per_e + nb2 * BN + rank * (BN / 2);
-                    }
-                    if (tile == cid)
-                        for (int kb = 0; kb < p.pf && kb < KB; ++kb) {
-                            tma_prefetch_l2(&tmA, kb * BK, ay);
-                            tma_prefetch_l2(&tmB, kb * BK, by);
-                        }
-                }
                 for (int kb = 0; kb < KB; ++kb) {
-                    if (!WGRAD && p.pf > 0) {
-                        const int pk = kb + p.pf;
-                        if (pk < KB) {
-                            tma_prefetch_l2(&tmA, pk * BK, ay);
-                            tma_prefetch_l2(&tmB, pk * BK, by);
-                        } else if (n_ay >= 0 && pk - KB < KB) {
-                            tma_prefetch_l2(&tmA, (pk - KB) * BK, n_ay);
-                            tma_prefetch_l2(&tmB, (pk - KB) * BK, n_by);
-                        }
-                    }
                     { const long long t0 = p.dbg ? clock64() : 0;
                     mbar_wait(&empty[stage], phase ^ 1);
                     if (p.dbg) p.dbg[blockIdx.x * 4 + 0] += clock64() - t0; }
@@ -375,10 +345,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                         tma_load_2d_cg2(b_dst, &tmB, lbar, bx, k);
                         tma_load_2d_cg2(b_dst + B_BYTES / 2, &tmB, lbar, bx + 64, k);
                     } else {
-                        if (p.hint_a) tma_load_2d_cg2_hint(a_dst, &tmA, lbar, kb * BK, ay, pol_a);
-                        else tma_load_2d_cg2(a_dst, &tmA, lbar, kb * BK, ay);
-                        if (p.hint_b) tma_load_2d_cg2_hint(b_dst, &tmB, lbar, kb * BK, by, pol_b);
-                        else tma_load_2d_cg2(b_dst, &tmB, lbar, kb * BK, by);
+                        tma_load_2d_cg2(a_dst, &tmA, lbar, kb * BK, ay);
+                        tma_load_2d_cg2(b_dst, &tmB, lbar, kb * BK, by);
                     }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
@@ -615,7 +583,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #pragma unroll
                             for (int i = 0; i < 32; ++i) h[i] = act_f(__uint_as_float(v[cc][i]), p.act) * wr;
                         }
-                        if (col0 < p.N && !p.nostore) {
+                        if (col0 < p.N) {
                             if (p.tma_out) {
                                 // coalesced: stage the warp's 32 x 32 bf16 block in smem
                                 // (64-byte swizzle: 16-byte chunk u of row r at u ^ ((r >> 1) & 3)),
@@ -938,8 +906,6 @@ void launch_grouped_gemm(EpiMode mode, const GemmArgs& a, int num_sms, cudaStrea
     p.pre_b = a.pre_b;
     p.gw_part = a.gw_part;
     p.a_rows = a.a_rows;
-    static const int pf_env = getenv("OCC_GEMM_PF") ? atoi(getenv("OCC_GEMM_PF")) : 0;
-    p.pf = a.a_rows ? 0 : pf_env;
     static const bool dbg_on = getenv("OCC_GEMM_DEBUG") != nullptr;
     static unsigned long long* dbg_buf = nullptr;
     if (dbg_on) {
@@ -962,21 +928,13 @@ void launch_grouped_gemm(EpiMode mode, const GemmArgs& a, int num_sms, cudaStrea
     }();
     if (mode == EPI_SWIGLU_BF16 && band1_override > 0) p.band = band1_override;
     else if (band_override > 0 && !(mode == EPI_WGRAD)) p.band = band_override;
-    static const int hint_env = [] {  // L2 policy experiments: OCC_GEMM_HINT = 10 * a + b
-        const char* e = getenv("OCC_GEMM_HINT");
-        return e ? atoi(e) : 0;
-    }();
-    p.hint_a = hint_env / 10;
-    p.hint_b = hint_env % 10;
-    static const int nostore_env = getenv("OCC_GEMM_NOSTORE") ? atoi(getenv("OCC_GEMM_NOSTORE")) : 0;
-    p.nostore = nostore_env;
     int grid = 2 * a.max_tiles < num_sms ? 2 * a.max_tiles : num_sms;
     grid &= ~1;  // CTA pairs
     if (grid <= 0) return;
     // wide 256 x 512 super-tiles for long-K forward GEMMs (OCC_GEMM_WIDE: 0 off,
     // 1 auto = K >= 1024 with an even number of 256-row B blocks, 2 force when even)
     static const int wide_env = getenv("OCC_GEMM_WIDE") ? atoi(getenv("OCC_GEMM_WIDE")) : 1;
-    if ((mode == EPI_ACT_BF16 || mode == EPI_SWIGLU_BF16) && !a.a_rows && !p.nostore) {
+    if ((mode == EPI_ACT_BF16 || mode == EPI_SWIGLU_BF16) && !a.a_rows) {
         const int nbk = mode == EPI_SWIGLU_BF16 ? (a.N + 127) / 128 : (a.N + BN - 1) / BN;
         const bool even = nbk % 2 == 0 && (mode != EPI_SWIGLU_BF16 || a.N % 128 == 0);
         if (even && (wide_env == 2 || (wide_env == 1 && a.K >= 1024))) {
