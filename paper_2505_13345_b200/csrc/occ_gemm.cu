@@ -666,7 +666,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
     const int NB = SW ? (p.N + 127) / 128 : (p.N + BN - 1) / BN;  // 256-row B blocks
-    const int NBW = NB / 2;                                        // super-tiles along N
+    const int NBW = (NB + 1) / 2;  // super-tiles along N (an odd NB leaves a last single-block super-tile)
     for (int i = threadIdx.x; i <= p.ngroups; i += blockDim.x) s_gmb[i] = p.grp_mb[i];
     for (int i = threadIdx.x; i < p.ngroups; i += blockDim.x) s_gw[i] = p.grp_w[i];
     if (warp == 0 && lane == 0) {
@@ -699,14 +699,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 tile_coords(tile, s_gmb, s_gw, p.ngroups, NBW, p.band, mb, nbw, wi);
                 const int ay = mb * 2 * BM + rank * BM;
                 const int by0 = wi * p.b_rows_per_e + 2 * nbw * BN + rank * (BN / 2);
+                const bool two = 2 * nbw + 1 < NB;  // the second 256-row B block exists
                 for (int kb = 0; kb < KB; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     const uint32_t lbar = smem_u32(&full[stage]) & kPeerBitMask;
-                    if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * (A_BYTES + W_B2));
+                    if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * (A_BYTES + (two ? W_B2 : B_BYTES)));
                     uint8_t* b_dst = sB + stage * W_B2;
                     tma_load_2d_cg2(sA + stage * A_BYTES, &tmA, lbar, kb * BK, ay);
                     tma_load_2d_cg2(b_dst, &tmB, lbar, kb * BK, by0);
-                    tma_load_2d_cg2(b_dst + B_BYTES, &tmB, lbar, kb * BK, by0 + BN);
+                    if (two) tma_load_2d_cg2(b_dst + B_BYTES, &tmB, lbar, kb * BK, by0 + BN);
                     if (++stage == W_STAGES) { stage = 0; phase ^= 1; }
                 }
             }
@@ -717,6 +718,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             int stage = 0;
             uint32_t phase = 0, acc_phase = 0;
             for (int tile = cid; tile < num_tiles; tile += ncl) {
+                int mb, nbw, wi;
+                tile_coords(tile, s_gmb, s_gw, p.ngroups, NBW, p.band, mb, nbw, wi);
+                const bool two = 2 * nbw + 1 < NB;
                 mbar_wait(&tempty[0], acc_phase ^ 1);
                 tc_fence_after();
                 for (int kb = 0; kb < KB; ++kb) {
@@ -729,8 +733,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                         for (int k = 0; k < BK / 16; ++k) {
                             const uint64_t ad = sdesc_k_sw128(a0 + k * 32);
                             umma_bf16_cg2(tmem_base, ad, sdesc_k_sw128(b0 + k * 32), IDESC, (kb | k) != 0);
-                            umma_bf16_cg2(tmem_base + BN, ad, sdesc_k_sw128(b0 + B_BYTES + k * 32), IDESC,
-                                          (kb | k) != 0);
+                            if (two)
+                                umma_bf16_cg2(tmem_base + BN, ad, sdesc_k_sw128(b0 + B_BYTES + k * 32), IDESC,
+                                              (kb | k) != 0);
                         }
                         umma_commit_cg2_mc(&empty[stage]);
                     }
@@ -759,6 +764,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             const float wr = p.row_w ? p.row_w[row] : 1.0f;
             const int nb = 2 * nbw + t;
             const int ncol = SW ? 128 : BN;
+            if (nb >= NB) {  // last super-tile of an odd NB: this accumulator holds nothing
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(smem_u32(&tempty[0]) & kPeerBitMask);
+                acc_phase ^= 1;
+                continue;
+            }
 #pragma unroll 1
             for (int round = 0; round < 2; ++round) {
                 uint32_t v[HALF][32], g[SW ? HALF : 1][32];
@@ -932,12 +944,15 @@ void launch_grouped_gemm(EpiMode mode, const GemmArgs& a, int num_sms, cudaStrea
     grid &= ~1;  // CTA pairs
     if (grid <= 0) return;
     // wide 256 x 512 super-tiles for long-K forward GEMMs (OCC_GEMM_WIDE: 0 off,
-    // 1 auto = K >= 1024 with an even number of 256-row B blocks, 2 force when even)
+    // 1 auto = K >= 1024 and an even number of 256-row B blocks, 2 force, odd counts >= 5 too)
     static const int wide_env = getenv("OCC_GEMM_WIDE") ? atoi(getenv("OCC_GEMM_WIDE")) : 1;
     if ((mode == EPI_ACT_BF16 || mode == EPI_SWIGLU_BF16) && !a.a_rows) {
         const int nbk = mode == EPI_SWIGLU_BF16 ? (a.N + 127) / 128 : (a.N + BN - 1) / BN;
-        const bool even = nbk % 2 == 0 && (mode != EPI_SWIGLU_BF16 || a.N % 128 == 0);
-        if (even && (wide_env == 2 || (wide_env == 1 && a.K >= 1024))) {
+        // an odd block count ends in a single-block super-tile; worth it from 5 blocks up
+        // an odd block count ends in a single-block super-tile: supported (forced mode) but
+        // measured 3% slower than the narrow kernel on DeepSeek's 11 blocks, so auto needs even
+        const bool ok = (nbk % 2 == 0 || (nbk >= 5 && wide_env == 2)) && (mode != EPI_SWIGLU_BF16 || a.N % 128 == 0);
+        if (ok && (wide_env == 2 || (wide_env == 1 && a.K >= 1024))) {
             if (mode == EPI_ACT_BF16) launch_wide<EPI_ACT_BF16>(grid, ta, tb, tc, p, st);
             else launch_wide<EPI_SWIGLU_BF16>(grid, ta, tb, tc, p, st);
             count_launch();

@@ -826,7 +826,7 @@ def test_train_step_host_pipeline_matches_device():
         assert torch.equal(gi, want)
 
 
-@pytest.mark.parametrize("act,dm,dh", [("swiglu", 2048, 512), ("silu", 2048, 2048)])
+@pytest.mark.parametrize("act,dm,dh", [("swiglu", 2048, 512), ("silu", 2048, 2048), ("relu", 1024, 1280)])
 def test_wide_tile_gemm_path(act, dm, dh):
     """K >= 2048 with an even number of 256-row B blocks selects the 256 x 512
     super-tile GEMM (two accumulators sharing each A K-block); outputs match
@@ -840,5 +840,22 @@ def test_wide_tile_gemm_path(act, dm, dh):
     layer.load_experts(cuda(w1, torch.bfloat16), cuda(w2, torch.bfloat16), cuda(w3, torch.bfloat16) if gated else None)
     out = layer.forward_given_routing(cuda(x, torch.bfloat16), cuda(ids), cuda(w, torch.float32))
     rows = np.arange(0, n, 7)
-    want = O.Port().dense_given_routing(x, ids, w, w1, w2, act="silu", single=False, rows=rows, w3=w3)
+    want = O.Port().dense_given_routing(x, ids, w, w1, w2, act="silu" if gated else act, single=False, rows=rows,
+                                        w3=w3)
     assert rel_err(out.double().cpu().numpy()[rows], want) <= TOL
+
+
+def test_wide_tile_forced_odd_blocks():
+    """OCC_GEMM_WIDE=2 forces the wide kernel, including odd B-block counts
+    (a last single-block super-tile): torch fp32 reference, fresh process."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, OCC_GEMM_WIDE="2")
+    r = subprocess.run([sys.executable, "profiles/probes/wide_debug.py"], env=env, capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if " err " in l]
+    assert len(lines) == 5, r.stdout
+    for l in lines:
+        assert float(l.split(" err ")[1].split()[0]) <= 1e-2, l
