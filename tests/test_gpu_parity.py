@@ -706,8 +706,9 @@ def test_collaboration_aware_placement_on_gpu():
     planted-block traces (bit-exact with the reference's accumulate_collab),
     reschedule_placement, and the device dispatch plan's E(C_T) drops by
     >= 10% vs the trivial layout (acceptance.cpp:218-244 criterion) at EP=8."""
+    import os
     import sys
-    sys.path.insert(0, "profiles")
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles"))
     from placement_gain import planted_block_ids
     ne, k, nd, n = 64, 8, 8, 8192
     ids_np, _ = planted_block_ids(n, ne, k, 8, 0.9, np.random.default_rng(11))
@@ -852,8 +853,9 @@ def test_wide_tile_forced_odd_blocks():
     import subprocess
     import sys
     env = dict(os.environ, OCC_GEMM_WIDE="2")
-    r = subprocess.run([sys.executable, "profiles/probes/wide_debug.py"], env=env, capture_output=True, text=True,
-                       timeout=300)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "profiles", "probes", "wide_debug.py")], env=env,
+                       capture_output=True, text=True, timeout=300, cwd=root)
     assert r.returncode == 0, r.stderr[-2000:]
     lines = [l for l in r.stdout.splitlines() if " err " in l]
     assert len(lines) == 5, r.stdout
