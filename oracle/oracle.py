@@ -136,6 +136,10 @@ def ref_lib():
         lib.ref_rng_uniform_stream.argtypes = [C.c_uint64, _i, _p]
         lib.ref_random_matrix.argtypes = [C.c_uint64, _i, _i, _i, _p]
         lib.ref_forward_expert_parallel_mt.argtypes = [_p, _i, _i, _p, _i, _i, _p, _p, _i, _i, _i, _i, _i, _p]
+        lib.ref_session_create.restype = _p
+        lib.ref_session_create.argtypes = [_p, _i, _i, _p, _p, _i, _i, _i, _i, _i]
+        lib.ref_session_destroy.argtypes = [_p]
+        lib.ref_session_forward.argtypes = [_p, _p, _i, _i, _p]
         lib.ref_backward.argtypes = [_p, _i, _i, _p, _p, _i, _p, _p, _i, _i, _p, _i, _p, _i, _i] + [_p] * 5
         _REF = lib
     return _REF

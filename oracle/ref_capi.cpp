@@ -319,6 +319,64 @@ int ref_dense_given_routing(const double* x, int n, int dm, const int* ids, cons
 // reference's own path (cli.cpp:271-316), on `nthreads` independent token
 // chunks in parallel (the reference functions are pure).
 // Returns the number of tokens processed.
+// A reference "layer session": the experts, gate, placement and config are
+// converted to the reference's own types once (as a caller of the moesim
+// library would hold them); ref_session_forward then times only the
+// reference's forward_expert_parallel (pipeline.cpp:503-517) on `nthreads`
+// token shards.
+struct RefSession {
+    ExpertWeights ew;
+    GateMatrix gm;
+    Placement pl;
+    MoEConfig cfg;
+};
+
+void* ref_session_create(const double* gate, int ne, int k, const double* w1, const double* w2, int dm, int dh,
+                         int nd, int act, int single) {
+    try {
+        auto* s = new RefSession{experts_of(w1, w2, ne, dm, dh, act), GateMatrix{mat(gate, ne, dm)},
+                                 trivial_placement(ne, nd), MoEConfig{}};
+        s->cfg.num_experts = ne;
+        s->cfg.top_k = k;
+        s->cfg.num_devices = nd;
+        s->cfg.embed_dim = dm;
+        s->cfg.hidden_dim = dh;
+        s->cfg.precision = single ? Precision::Single : Precision::Double;
+        s->cfg.activation = static_cast<Activation>(act);
+        return s;
+    } catch (...) {
+        return nullptr;
+    }
+}
+
+void ref_session_destroy(void* s) { delete static_cast<RefSession*>(s); }
+
+int ref_session_forward(void* sp, const double* x, int n, int nthreads, double* x_out) {
+    RefSession& s = *static_cast<RefSession*>(sp);
+    const int dm = s.cfg.embed_dim;
+    std::vector<std::thread> pool;
+    std::vector<int> rc(nthreads, 0);
+    const int chunk = (n + nthreads - 1) / nthreads;
+    for (int th = 0; th < nthreads; ++th) {
+        pool.emplace_back([&, th] {
+            const int lo = th * chunk, hi = std::min(n, lo + chunk);
+            if (lo >= hi) return;
+            try {
+                TokenMatrix tx(mat(x + static_cast<size_t>(lo) * dm, hi - lo, dm), TokenState::Ori);
+                ForwardResult res = forward_expert_parallel(tx, s.gm, s.ew, s.pl, PruneSpec{}, s.cfg);
+                std::memcpy(x_out + static_cast<size_t>(lo) * dm, res.x_out.values.data.data(),
+                            sizeof(double) * res.x_out.values.data.size());
+            } catch (...) {
+                rc[th] = status_of(std::current_exception());
+            }
+        });
+    }
+    for (auto& t : pool) t.join();
+    for (int v : rc)
+        if (v) return -v;
+    return n;
+}
+
 int ref_forward_expert_parallel_mt(const double* x, int n, int dm, const double* gate, int ne, int k,
                                    const double* w1, const double* w2, int dh, int nd, int act, int single,
                                    int nthreads, double* x_out) {
