@@ -95,6 +95,7 @@ struct Params {
     float* gw_part;
     int tma_out;         // bf16 forward outputs leave through smem + TMA stores (tmC)
     unsigned long long* dbg;  // OCC_GEMM_DEBUG: per-CTA stall cycles [cta][4]
+    int tail_split;           // wide kernel: split the tail wave's super-tiles into halves
     const int* a_rows;   // non-null: A row q of the padded Epd layout is row a_rows[q] of tmA
                          // (tile::gather4, box 64 x 1; -1 = zero padding row)
 };
@@ -644,6 +645,31 @@ constexpr int W_STAGES = 4;
 constexpr int W_B2 = 2 * B_BYTES;  // both B halves of this CTA per stage
 constexpr int W_SMEM_BYTES = W_STAGES * (A_BYTES + W_B2) + EPI_STAGE_BYTES + 256;
 
+// Wide tile list: S super-tiles in raster order; when the last wave holds
+// r < half the pairs, its r super-tiles are issued as 2r single-block halves
+// so the tail wave takes half as long.  Every role decodes the same list.
+struct WTile {
+    int mb, wi, nb0;  // m-tile, weight index, first 256-row B block
+    bool two;         // both accumulators (else only the first, block nb0)
+    bool valid;
+};
+__device__ __forceinline__ WTile wide_decode(int tile, int S, int split, const int* gmb, const int* gw, int ng,
+                                             int NBW, int NB, int band) {
+    WTile w;
+    int nbw, half = 0;
+    int st = tile;
+    if (tile >= S - split) {
+        const int h = tile - (S - split);
+        st = S - split + (h >> 1);
+        half = h & 1;
+    }
+    tile_coords(st, gmb, gw, ng, NBW, band, w.mb, nbw, w.wi);
+    w.nb0 = 2 * nbw + half;
+    w.two = tile < S - split && w.nb0 + 1 < NB;
+    w.valid = w.nb0 < NB;
+    return w;
+}
+
 template <int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     wide_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -686,20 +712,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    const int num_tiles = s_gmb[p.ngroups] * NBW;
     const int KB = (p.K + BK - 1) / BK;
     const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+    const int S = s_gmb[p.ngroups] * NBW;        // super-tiles
+    const int tail = S % ncl;
+    const int split = p.tail_split && 2 * tail <= ncl ? tail : 0;  // tail super-tiles issued as halves
+    const int num_tiles = S + split;
 
     if (warp == 0) {
         if (lane == 0) {  // -------------------------------------------- TMA producer
             int stage = 0;
             uint32_t phase = 0;
             for (int tile = cid; tile < num_tiles; tile += ncl) {
-                int mb, nbw, wi;
-                tile_coords(tile, s_gmb, s_gw, p.ngroups, NBW, p.band, mb, nbw, wi);
-                const int ay = mb * 2 * BM + rank * BM;
-                const int by0 = wi * p.b_rows_per_e + 2 * nbw * BN + rank * (BN / 2);
-                const bool two = 2 * nbw + 1 < NB;  // the second 256-row B block exists
+                const WTile wt = wide_decode(tile, S, split, s_gmb, s_gw, p.ngroups, NBW, NB, p.band);
+                if (!wt.valid) continue;
+                const int ay = wt.mb * 2 * BM + rank * BM;
+                const int by0 = wt.wi * p.b_rows_per_e + wt.nb0 * BN + rank * (BN / 2);
+                const bool two = wt.two;  // the second 256-row B block is part of this tile
                 for (int kb = 0; kb < KB; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     const uint32_t lbar = smem_u32(&full[stage]) & kPeerBitMask;
@@ -718,9 +747,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             int stage = 0;
             uint32_t phase = 0, acc_phase = 0;
             for (int tile = cid; tile < num_tiles; tile += ncl) {
-                int mb, nbw, wi;
-                tile_coords(tile, s_gmb, s_gw, p.ngroups, NBW, p.band, mb, nbw, wi);
-                const bool two = 2 * nbw + 1 < NB;
+                const WTile wt = wide_decode(tile, S, split, s_gmb, s_gw, p.ngroups, NBW, NB, p.band);
+                if (!wt.valid) continue;
+                const bool two = wt.two;
                 mbar_wait(&tempty[0], acc_phase ^ 1);
                 tc_fence_after();
                 for (int kb = 0; kb < KB; ++kb) {
@@ -755,16 +784,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         constexpr int NCH = SW ? 4 : BN / 32;  // output chunks of 32 columns per accumulator
         constexpr int HALF = NCH / 2;          // chunks per drain round (128 registers)
         for (int tile = cid; tile < num_tiles; tile += ncl) {
-            int mb, nbw, wi;
-            tile_coords(tile, s_gmb, s_gw, p.ngroups, NBW, p.band, mb, nbw, wi);
+            const WTile wt = wide_decode(tile, S, split, s_gmb, s_gw, p.ngroups, NBW, NB, p.band);
+            if (!wt.valid) continue;
+            const int mb = wt.mb;
             mbar_wait(&tfull[0], acc_phase);
             tc_fence_after();
             const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + t * BN;
             const long row = (long)mb * 2 * BM + rank * BM + q * 32 + lane;
             const float wr = p.row_w ? p.row_w[row] : 1.0f;
-            const int nb = 2 * nbw + t;
+            const int nb = wt.nb0 + t;
             const int ncol = SW ? 128 : BN;
-            if (nb >= NB) {  // last super-tile of an odd NB: this accumulator holds nothing
+            if (t == 1 && !wt.two) {  // single-block tile: the second accumulator holds nothing
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive_cluster(smem_u32(&tempty[0]) & kPeerBitMask);
@@ -946,6 +976,8 @@ void launch_grouped_gemm(EpiMode mode, const GemmArgs& a, int num_sms, cudaStrea
     // wide 256 x 512 super-tiles for long-K forward GEMMs (OCC_GEMM_WIDE: 0 off,
     // 1 auto = K >= 1024 and an even number of 256-row B blocks, 2 force, odd counts >= 5 too)
     static const int wide_env = getenv("OCC_GEMM_WIDE") ? atoi(getenv("OCC_GEMM_WIDE")) : 1;
+    static const int tail_env = getenv("OCC_GEMM_TAILSPLIT") ? atoi(getenv("OCC_GEMM_TAILSPLIT")) : 1;
+    p.tail_split = tail_env;
     if ((mode == EPI_ACT_BF16 || mode == EPI_SWIGLU_BF16) && !a.a_rows) {
         const int nbk = mode == EPI_SWIGLU_BF16 ? (a.N + 127) / 128 : (a.N + BN - 1) / BN;
         // an odd block count ends in a single-block super-tile; worth it from 5 blocks up
