@@ -142,6 +142,15 @@ occ_status occ_comm_init(occ_handle* h, const void* id128);
  * as NCCL, for checking world_size > 1 on a single GPU. */
 occ_status occ_comm_init_loopback(occ_handle* h, long group_key);
 
+/* Fused exchange over peer memory (collective; call on every rank after
+ * occ_comm_init / occ_comm_init_loopback): each rank's inbox and
+ * returned-row buffers are mapped into every rank (CUDA IPC over NVLink /
+ * NVSwitch; plain pointers for loopback ranks), and the dispatch pack and the
+ * return partial combine store straight into the peers' buffers, with
+ * arrival flags instead of all-to-all calls.  Buffers are sized for
+ * max_tokens_per_rank tokens per forward (larger batches: OCC_ERR_SHAPE). */
+occ_status occ_comm_enable_peer(occ_handle* h, int max_tokens_per_rank);
+
 /* -------------------------------------------------------------- routing */
 /* gate_scores (routing.cpp:33-52), exact fp64 mode: logits accumulated
  * sequentially in ascending k without FMA, softmax with max subtraction. */

@@ -84,7 +84,7 @@ EXPORTS = (
     "occ_route", "occ_build_dispatch", "occ_forward", "occ_forward_expert_parallel", "occ_comm_report_get",
     "occ_saved_index", "occ_coactivation_histogram", "occ_normalize_graph", "occ_reschedule_placement",
     "occ_allreduce_histogram", "occ_last_error", "occ_launch_count", "occ_set_profiling", "occ_stage_ms", "occ_forward_host", "occ_host_wait", "occ_comm_init_loopback", "occ_exchange_layout", "occ_set_training", "occ_backward",
-    "occ_load_shared_experts",
+    "occ_load_shared_experts", "occ_comm_enable_peer",
 )
 
 STAGES = ("route", "plan", "pack", "compute_index", "gather", "gemm1", "gemm2", "shared", "partial_combine", "combine")
@@ -293,6 +293,11 @@ class ExpertParallelLayer:
         dist.broadcast_object_list(obj, src=0, group=group)
         idb = (C.c_uint8 * 128).from_buffer_copy(obj[0])
         _check(lib().occ_comm_init(self._h, idb), "comm_init")
+
+    def comm_enable_peer(self, max_tokens_per_rank: int):
+        """Fused dispatch / return over peer memory instead of all-to-all calls
+        (collective; after comm_init / comm_init_loopback)."""
+        _check(lib().occ_comm_enable_peer(self._h, int(max_tokens_per_rank)), "comm_enable_peer")
 
     def comm_init_loopback(self, key: int):
         """Validation transport: world_size ranks as threads on one GPU."""

@@ -105,6 +105,11 @@ struct Transport {
                                  void* recv, const std::vector<size_t>& roff, const std::vector<size_t>& rcnt, int es,
                                  cudaStream_t st) = 0;
     virtual occ_status allreduce_i64(int64_t* buf, size_t count, cudaStream_t st) = 0;
+    // peer-memory mapping: every rank's `mine` device pointers, usable by this
+    // rank (world x mine.size(), row p = rank p); opened mappings are returned
+    // in `opened` for release
+    virtual occ_status exchange_pointers(const std::vector<void*>& mine, std::vector<void*>& all,
+                                         std::vector<void*>& opened) = 0;
     // several all-to-alls with the same row layout (element sizes es[i]) as one exchange
     struct Part {
         const void* send;
@@ -215,6 +220,13 @@ struct occ_handle {
     TmapBox tmBS1, tmBS2, tmAS1, tmAS2, tmCS1, tmCS2;
     cudaStream_t s_aux = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // peer-memory exchange (occ_comm_enable_peer)
+    bool peer = false;
+    int peer_cap = 0;                  // max tokens per rank per forward
+    unsigned long long peer_seq = 0;   // forwards issued (arrival flag value)
+    DevBuf<unsigned long long> flags;  // [2 * world]: dispatch arrivals, return arrivals
+    DevBuf<void*> peer_tab;            // [world * kPeerSlots]
+    std::vector<void*> ipc_opened;
 };
 
 namespace {
@@ -248,6 +260,37 @@ struct NcclTransport : Transport {
         NCCL_TRY(ncclAllReduce(buf, buf, count, ncclInt64, ncclSum, comm, st));
         return OCC_OK;
     }
+    occ_status exchange_pointers(const std::vector<void*>& mine, std::vector<void*>& all,
+                                 std::vector<void*>& opened) override {
+        const size_t m = mine.size(), hb = sizeof(cudaIpcMemHandle_t);
+        std::vector<cudaIpcMemHandle_t> hs(m);
+        for (size_t i = 0; i < m; ++i) CUDA_TRY(cudaIpcGetMemHandle(&hs[i], mine[i]));
+        void* dsend = nullptr;
+        void* drecv = nullptr;
+        CUDA_TRY(cudaMalloc(&dsend, m * hb));
+        CUDA_TRY(cudaMalloc(&drecv, m * hb * world));
+        CUDA_TRY(cudaMemcpy(dsend, hs.data(), m * hb, cudaMemcpyHostToDevice));
+        int rank = 0;
+        NCCL_TRY(ncclCommUserRank(comm, &rank));
+        NCCL_TRY(ncclAllGather(dsend, drecv, m * hb, ncclUint8, comm, 0));
+        std::vector<cudaIpcMemHandle_t> allh(m * world);
+        CUDA_TRY(cudaMemcpy(allh.data(), drecv, m * hb * world, cudaMemcpyDeviceToHost));
+        cudaFree(dsend);
+        cudaFree(drecv);
+        all.assign(m * world, nullptr);
+        for (int p = 0; p < world; ++p)
+            for (size_t i = 0; i < m; ++i) {
+                if (p == rank) {
+                    all[p * m + i] = mine[i];
+                    continue;
+                }
+                void* ptr = nullptr;
+                CUDA_TRY(cudaIpcOpenMemHandle(&ptr, allh[p * m + i], cudaIpcMemLazyEnablePeerAccess));
+                all[p * m + i] = ptr;
+                opened.push_back(ptr);
+            }
+        return OCC_OK;
+    }
     // one NCCL group (one launch) for the token rows and their routing metadata
     occ_status alltoallv_parts(const std::vector<Part>& parts, const std::vector<size_t>& soff,
                                const std::vector<size_t>& scnt, const std::vector<size_t>& roff,
@@ -277,7 +320,8 @@ struct LoopGroup {
     std::vector<std::vector<size_t>> soff, scnt;
     std::vector<std::vector<int>> counts;
     std::vector<std::vector<int64_t>> vals;
-    explicit LoopGroup(int w) : world(w), send(w), soff(w), scnt(w), counts(w), vals(w) {}
+    std::vector<std::vector<void*>> ptrs;
+    explicit LoopGroup(int w) : world(w), send(w), soff(w), scnt(w), counts(w), vals(w), ptrs(w) {}
     void barrier() {
         std::unique_lock<std::mutex> lk(m);
         const long g = gen;
@@ -328,6 +372,15 @@ struct LoopbackTransport : Transport {
         }
         CUDA_TRY(cudaStreamSynchronize(st));
         grp->barrier();  // peers may reuse their send buffers only after every copy landed
+        return OCC_OK;
+    }
+    occ_status exchange_pointers(const std::vector<void*>& mine, std::vector<void*>& all,
+                                 std::vector<void*>&) override {
+        grp->ptrs[rank] = mine;  // same process, same device: the pointers themselves
+        grp->barrier();
+        all.clear();
+        for (int p = 0; p < grp->world; ++p) all.insert(all.end(), grp->ptrs[p].begin(), grp->ptrs[p].end());
+        grp->barrier();
         return OCC_OK;
     }
     occ_status allreduce_i64(int64_t* buf, size_t count, cudaStream_t st) override {
@@ -634,6 +687,7 @@ occ_status check_err(occ_handle* h, cudaStream_t st) {
     if (e == 1) return fail(OCC_ERR_SHAPE, "forward: source device out of range");
     if (e == 4) return fail(OCC_ERR_ROUTING, "routing: invalid expert id, duplicate id, non-positive weight, or a row with no local expert");
     if (e == 5) return fail(OCC_ERR_CAPACITY, "prune: device budget too small for top-k");
+    if (e == 7) return fail(OCC_ERR_CUDA, "peer exchange: a peer did not signal within the timeout");
     if (e) return fail(OCC_ERR_ROUTING, "routing error");
     return OCC_OK;
 }
@@ -662,6 +716,7 @@ occ_status forward_multi(occ_handle* h, const __nv_bfloat16* x, const int32_t* i
     Transport* tp = h->tp;
     const int nd = h->nd, k = h->k, P = h->P, D = h->D, F = h->F, dedup = h->cfg.dedup, r = h->rank;
     const int items = dedup ? n : n * k;
+    if (h->peer && n > h->peer_cap) return fail(OCC_ERR_SHAPE, "peer exchange: more tokens than max_tokens_per_rank");
     occ_status s = ensure_ws(h, std::max(n, 1));
     if (s != OCC_OK) return s;
     CUDA_TRY(cudaMemsetAsync(h->stats.p, 0, sizeof(long long) * 8, st));
@@ -685,10 +740,10 @@ occ_status forward_multi(occ_handle* h, const __nv_bfloat16* x, const int32_t* i
                     h->tok_sfd.p, h->lam.p, nullptr, nullptr, nullptr, nullptr};
     launch_rank_emit_dispatch(items, h->group.p, h->mask.p, 1, nd, ws, em, st);
     launch_token_stats(n, k, nd, ids, nullptr, r, h->d_dev_of.p, h->stats.p, st);
-    // 2. pack this source's Sfd batch
+    // 2. pack this source's Sfd batch (peer mode: straight into the peers' inboxes, below)
     mark(h, ST_PACK, st);
     PackArgs pk{n, k, nd, D, dedup, x, ids, weights, h->mask.p, h->tok_row.p, h->snd_x.p, h->snd_ids.p, h->snd_w.p};
-    launch_pack(pk, st);
+    if (!h->peer) launch_pack(pk, st);
     // shared experts: source-side dense FFN on a second stream, overlapping
     // the dispatch exchange and the routed expert compute
     const bool shared = h->n_shared > 0 && n > 0;
@@ -706,6 +761,8 @@ occ_status forward_multi(occ_handle* h, const __nv_bfloat16* x, const int32_t* i
     occ_exchange_layout(h->h_C.data(), nd, r, off.data(), scnt64.data(), inoff.data(), rcnt64.data());
     long long R = 0;
     for (int p = 0; p < nd; ++p) R += rcnt64[p];
+    if (h->peer && R > (long long)h->R_max)  // mapped buffers must not move
+        return fail(OCC_ERR_SHAPE, "peer exchange: received rows exceed the mapped capacity");
     s = ensure_recv(h, (size_t)std::max<long long>(R, 1), (size_t)std::max<long long>(R, 1) * std::min(k, P));
     if (s != OCC_OK) return s;
     h->last_R = (int)R;
@@ -717,10 +774,18 @@ occ_status forward_multi(occ_handle* h, const __nv_bfloat16* x, const int32_t* i
         ro[p] = (size_t)inoff[p];
         rc[p] = (size_t)rcnt64[p];
     }
-    const std::vector<Transport::Part> parts{{h->snd_x.p, h->in_x.p, D * 2},
-                                             {h->snd_ids.p, h->in_ids.p, k * 4},
-                                             {h->snd_w.p, h->in_w.p, k * 4}};
-    if ((s = tp->alltoallv_parts(parts, so, sc, ro, rc, st)) != OCC_OK) return s;
+    const unsigned long long seq = ++h->peer_seq;
+    void* const* tab = h->peer_tab.p;
+    if (h->peer) {  // fused dispatch: pack stores into every destination's inbox, then arrival flags
+        launch_peer_pack(pk, r, h->d_dev_of.p, h->dofs.off_sd, h->dofs.inoff, tab, st);
+        launch_peer_signal(tab, nd, r, 0, seq, st);
+        launch_peer_wait(h->flags.p, nd, 0, seq, 10000000000LL, h->err.p, st);
+    } else {
+        const std::vector<Transport::Part> parts{{h->snd_x.p, h->in_x.p, D * 2},
+                                                 {h->snd_ids.p, h->in_ids.p, k * 4},
+                                                 {h->snd_w.p, h->in_w.p, k * 4}};
+        if ((s = tp->alltoallv_parts(parts, so, sc, ro, rc, st)) != OCC_OK) return s;
+    }
     // 4. compute index over the received rows
     mark(h, ST_CINDEX, st);
     const int Rm = (int)std::max<long long>(R, 1);
@@ -747,9 +812,16 @@ occ_status forward_multi(occ_handle* h, const __nv_bfloat16* x, const int32_t* i
     launch_gemm2(h, P, st);
     // 6. intra-device partial combine -> bf16 return payload in inbox order
     mark(h, ST_PCOMBINE, st);
-    launch_partial_combine(Rm, h->d_R, P, D, h->row_epd.p, h->y16.p, h->ret.p, st);
-    // 7. return all-to-all: inbox rows back to their source's Sfd slots
-    if ((s = tp->alltoallv(h->ret.p, ro, rc, h->y_src.p, so, sc, D * 2, st)) != OCC_OK) return s;
+    if (h->peer) {  // fused partial combine + return straight into the sources' buffers
+        launch_peer_return((int)R, nd, r, P, D, h->row_epd.p, h->y16.p, h->dofs.C, h->dofs.off_sd, h->dofs.inoff,
+                           tab, st);
+        launch_peer_signal(tab, nd, r, nd, seq, st);
+        launch_peer_wait(h->flags.p, nd, nd, seq, 10000000000LL, h->err.p, st);
+    } else {
+        launch_partial_combine(Rm, h->d_R, P, D, h->row_epd.p, h->y16.p, h->ret.p, st);
+        // 7. return all-to-all: inbox rows back to their source's Sfd slots
+        if ((s = tp->alltoallv(h->ret.p, ro, rc, h->y_src.p, so, sc, D * 2, st)) != OCC_OK) return s;
+    }
     // 8. combine over devices ascending
     mark(h, ST_COMBINE, st);
     if (shared) CUDA_TRY(cudaStreamWaitEvent(st, h->ev_join, 0));
@@ -840,6 +912,9 @@ occ_status occ_destroy(occ_handle* h) {
     h->gw_part.release();
     h->gw_row.release();
     h->epd_j.release();
+    for (void* ptr : h->ipc_opened) cudaIpcCloseMemHandle(ptr);
+    h->flags.release();
+    h->peer_tab.release();
     for (auto* b : {&h->w13s, &h->w2s, &h->sgate, &h->hs, &h->ys}) b->release();
     h->sw.release();
     h->sh_grp.release();
@@ -1542,6 +1617,35 @@ occ_status occ_comm_init_loopback(occ_handle* h, long group_key) {
     }
     delete h->tp;
     h->tp = new LoopbackTransport(g, h->rank);
+    return OCC_OK;
+}
+
+occ_status occ_comm_enable_peer(occ_handle* h, int max_tokens_per_rank) {
+    if (!h) return fail(OCC_ERR_ARG, "null handle");
+    if (h->world == 1) return OCC_OK;
+    if (!h->tp) return fail(OCC_ERR_STATE, "peer exchange: call occ_comm_init / occ_comm_init_loopback first");
+    if (max_tokens_per_rank < 1) return fail(OCC_ERR_CONFIG, "peer exchange: max_tokens_per_rank must be >= 1");
+    const int nd = h->nd, k = h->k, P = h->P;
+    const size_t per_dev = h->cfg.dedup ? 1 : (size_t)std::min(k, P);   // rows per (token, device)
+    const size_t R_cap = (size_t)max_tokens_per_rank * nd * per_dev;
+    occ_status s = ensure_ws(h, max_tokens_per_rank);
+    if (s != OCC_OK) return s;
+    s = ensure_recv(h, R_cap, R_cap * std::min(k, P));
+    if (s != OCC_OK) return s;
+    CUDA_TRY(h->flags.ensure(2 * nd));
+    CUDA_TRY(cudaMemset(h->flags.p, 0, sizeof(unsigned long long) * 2 * nd));
+    CUDA_TRY(cudaDeviceSynchronize());
+    const std::vector<void*> mine{h->in_x.p, h->in_ids.p, h->in_w.p, h->y_src.p, h->flags.p};
+    std::vector<void*> all;
+    for (void* ptr : h->ipc_opened) cudaIpcCloseMemHandle(ptr);
+    h->ipc_opened.clear();
+    s = h->tp->exchange_pointers(mine, all, h->ipc_opened);
+    if (s != OCC_OK) return s;
+    CUDA_TRY(h->peer_tab.ensure(all.size()));
+    CUDA_TRY(cudaMemcpy(h->peer_tab.p, all.data(), sizeof(void*) * all.size(), cudaMemcpyHostToDevice));
+    h->peer = true;
+    h->peer_cap = max_tokens_per_rank;
+    h->peer_seq = 0;
     return OCC_OK;
 }
 

@@ -703,6 +703,116 @@ __global__ void __launch_bounds__(256) combine_fused_kernel(int n, int nd, int k
     }
 }
 
+// ------------------------------------------------- peer-memory exchange ---
+// world_size > 1 without a collective library on the data path: every rank's
+// inbox / return buffers are mapped into every other rank's address space
+// (CUDA IPC over NVLink / NVSwitch, or plain pointers for the single-GPU
+// loopback ranks), and the dispatch pack and the return partial combine store
+// straight into the peer's buffers — the all-to-all is fused into the
+// producing kernel.  Table layout: peer_tab[p * kPeerSlots + i].
+constexpr int kPeerInX = 0, kPeerInIds = 1, kPeerInW = 2, kPeerYSrc = 3, kPeerFlags = 4;
+static_assert(kPeerSlots == 5, "peer table slots");
+
+// pack_kernel, but rows go directly to each destination's inbox:
+// row = inoff[d][me] + (BRIM0 counter - off_sd[me][d]) (all_to_all_exchange
+// order: source ascending, counter ascending, pipeline.cpp:153-174).
+__global__ void __launch_bounds__(256) peer_pack_kernel(PackArgs a, int me, const int32_t* dev_of, const int* off_sd,
+                                                        const int* inoff, void* const* peer_tab) {
+    const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (t >= a.n) return;
+    const int nvec = a.D / 8;
+    const uint4* src = reinterpret_cast<const uint4*>(a.x + (long)t * a.D);
+    int nrow = 0, dsts[kMaxTopK], rows[kMaxTopK], jsel[kMaxTopK];
+    if (a.dedup) {  // one row per destination device
+        uint64_t m = a.mask[t];
+        while (m) {
+            const int d = __ffsll(m) - 1;
+            m &= m - 1;
+            dsts[nrow] = d;
+            jsel[nrow] = -1;
+            rows[nrow++] = inoff[d * a.nd + me] + a.tok_row[(long)t * a.nd + d] - off_sd[me * a.nd + d];
+        }
+    } else {  // replicate-k baseline: one row per (token, expert), carrying only that expert
+        for (int j = 0; j < a.k; ++j) {
+            const int d = dev_of[a.ids[(long)t * a.k + j]];
+            dsts[nrow] = d;
+            jsel[nrow] = j;
+            rows[nrow++] = inoff[d * a.nd + me] + a.tok_row[(long)t * a.k + j] - off_sd[me * a.nd + d];
+        }
+    }
+    for (int q = 0; q < nrow; ++q) {
+        const int d = dsts[q];
+        __nv_bfloat16* px = reinterpret_cast<__nv_bfloat16*>(peer_tab[d * kPeerSlots + kPeerInX]);
+        uint4* dst = reinterpret_cast<uint4*>(px + (long)rows[q] * a.D);
+        for (int v = lane; v < nvec; v += 32) dst[v] = __ldg(src + v);
+        if (lane < a.k) {
+            int32_t* pid = reinterpret_cast<int32_t*>(peer_tab[d * kPeerSlots + kPeerInIds]);
+            float* pw = reinterpret_cast<float*>(peer_tab[d * kPeerSlots + kPeerInW]);
+            const long di = (long)rows[q] * a.k + lane;
+            const bool keep = jsel[q] < 0 || lane == jsel[q];
+            pid[di] = keep ? a.ids[(long)t * a.k + lane] : -1;
+            pw[di] = keep ? a.w[(long)t * a.k + lane] : 0.0f;
+        }
+    }
+}
+
+// Arrival signal: after this stream's peer stores, publish `seq` into slot
+// (base + me) of every peer's flag array (release, system scope).
+__global__ void peer_signal_kernel(void* const* peer_tab, int nd, int me, int base, unsigned long long seq) {
+    const int d = threadIdx.x;
+    if (d >= nd) return;
+    __threadfence_system();
+    unsigned long long* f = reinterpret_cast<unsigned long long*>(peer_tab[d * kPeerSlots + kPeerFlags]);
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f + base + me), "l"(seq) : "memory");
+}
+
+// Wait until every peer has published `seq` in slots base..base+nd of this
+// rank's flags; bounded (err = 7 after `timeout_ns`) so a lost peer cannot
+// hang the device.
+__global__ void peer_wait_kernel(const unsigned long long* flags, int nd, int base, unsigned long long seq,
+                                 long long timeout_ns, int32_t* err) {
+    const int s = threadIdx.x;
+    if (s >= nd) return;
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (true) {
+        unsigned long long v;
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(flags + base + s) : "memory");
+        if (v >= seq) break;
+        unsigned long long t1;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        if ((long long)(t1 - t0) > timeout_ns) {
+            atomicExch(err, 7);
+            break;
+        }
+        __nanosleep(256);
+    }
+    __threadfence_system();
+}
+
+// Intra-device partial combine fused with the return exchange: inbox row r
+// (from source s, slot counter c) is summed over its local experts and
+// stored straight into source s's returned-row buffer at row c.
+__global__ void __launch_bounds__(256) peer_return_kernel(int R, int nd, int me, int P, int D, const int32_t* row_epd,
+                                                          const __nv_bfloat16* Y, const int* C, const int* off_sd,
+                                                          const int* inoff, void* const* peer_tab) {
+    __shared__ int s_q[8][kMaxLocal];
+    const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (r >= R) return;
+    int s = 0;  // source of inbox row r: rows of source s are [inoff[me][s], inoff[me][s] + C[s][me])
+    while (s < nd - 1 && r >= inoff[me * nd + s] + C[s * nd + me]) ++s;
+    const int c = off_sd[s * nd + me] + (r - inoff[me * nd + s]);
+    int* qs = s_q[threadIdx.x >> 5];
+    const int nq = warp_compact_append(row_epd + (long)r * P, P, qs, 0, kMaxLocal, lane);
+    __syncwarp();
+    __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(peer_tab[s * kPeerSlots + kPeerYSrc]) + (long)c * D;
+    if (P <= 2) sum_rows_ordered<2>(Y, qs, nq, D, lane, nullptr, dst);
+    else if (P <= 4) sum_rows_ordered<4>(Y, qs, nq, D, lane, nullptr, dst);
+    else sum_rows_ordered<8>(Y, qs, nq, D, lane, nullptr, dst);
+}
+
 // Shared-expert gate (Qwen's shared_expert_gate): g_t = sigmoid(x[t] . gate),
 // one warp per token, fp32 accumulation.  Rows n..n_pad of the padded
 // GEMM m-tile get 0 so the padded rows stay finite.
@@ -1326,6 +1436,28 @@ void launch_shared_gate(int n, int n_pad, int D, const __nv_bfloat16* x, const _
         fill_f32_kernel<<<(n_pad + 255) / 256, 256, 0, st>>>(g, n, n_pad, 1.0f);
     set_group_kernel<<<1, 1, 0, st>>>(grp, n_pad / kBM);
     count_launch(2);
+}
+
+void launch_peer_pack(const PackArgs& a, int me, const int32_t* dev_of, const int* off_sd, const int* inoff,
+                      void* const* peer_tab, cudaStream_t st) {
+    if (!a.n) return;
+    peer_pack_kernel<<<(a.n + 7) / 8, 256, 0, st>>>(a, me, dev_of, off_sd, inoff, peer_tab);
+    count_launch();
+}
+void launch_peer_signal(void* const* peer_tab, int nd, int me, int base, unsigned long long seq, cudaStream_t st) {
+    peer_signal_kernel<<<1, 64, 0, st>>>(peer_tab, nd, me, base, seq);
+    count_launch();
+}
+void launch_peer_wait(const unsigned long long* flags, int nd, int base, unsigned long long seq, long long timeout_ns,
+                      int32_t* err, cudaStream_t st) {
+    peer_wait_kernel<<<1, 64, 0, st>>>(flags, nd, base, seq, timeout_ns, err);
+    count_launch();
+}
+void launch_peer_return(int R, int nd, int me, int P, int D, const int32_t* row_epd, const __nv_bfloat16* Y,
+                        const int* C, const int* off_sd, const int* inoff, void* const* peer_tab, cudaStream_t st) {
+    if (!R) return;
+    peer_return_kernel<<<(R + 7) / 8, 256, 0, st>>>(R, nd, me, P, D, row_epd, Y, C, off_sd, inoff, peer_tab);
+    count_launch();
 }
 
 void launch_gather_token_rows(int Q_max, const int* q_total, const int32_t* epd_src, const int32_t* in_tok,

@@ -561,11 +561,19 @@ def test_forward_host_graph_replay():
 
 # ------------------------------------------- world_size > 1 (loopback) -----
 
-@pytest.mark.parametrize("nd,ne,k,act,dedup,shared", [(2, 8, 2, "silu", True, 0), (4, 16, 4, "silu", True, 0),
-                                                      (8, 64, 8, "relu", True, 0), (4, 8, 3, "identity", False, 0),
-                                                      (2, 8, 2, "swiglu", True, 0), (4, 16, 4, "swiglu", True, 2),
-                                                      (2, 8, 2, "relu", False, 1)])
-def test_multi_rank_forward_loopback(nd, ne, k, act, dedup, shared):
+@pytest.mark.parametrize("nd,ne,k,act,dedup,shared,peer", [(2, 8, 2, "silu", True, 0, False),
+                                                           (4, 16, 4, "silu", True, 0, False),
+                                                           (8, 64, 8, "relu", True, 0, False),
+                                                           (4, 8, 3, "identity", False, 0, False),
+                                                           (2, 8, 2, "swiglu", True, 0, False),
+                                                           (4, 16, 4, "swiglu", True, 2, False),
+                                                           (2, 8, 2, "relu", False, 1, False),
+                                                           # fused exchange over peer memory
+                                                           (2, 8, 2, "silu", True, 0, True),
+                                                           (8, 64, 8, "relu", True, 0, True),
+                                                           (4, 8, 3, "identity", False, 0, True),
+                                                           (4, 16, 4, "swiglu", True, 2, True)])
+def test_multi_rank_forward_loopback(nd, ne, k, act, dedup, shared, peer):
     """The world_size == N_d code path (per-rank plan, count all-gather, two
     variable all-to-alls, per-device BRIM1 + GEMMs + partial combine,
     combine) with the ranks as threads on one GPU, against the reference's
@@ -607,9 +615,12 @@ def test_multi_rank_forward_loopback(nd, ne, k, act, dedup, shared):
                     layer.load_shared_experts(cuda(s1, torch.bfloat16), cuda(s2, torch.bfloat16),
                                               cuda(s3, torch.bfloat16) if gated else None, cuda(sg, torch.bfloat16))
                 layer.comm_init_loopback(int(key))
+                if peer:
+                    layer.comm_enable_peer(128)
                 a, b = starts[r], starts[r + 1]
-                out = layer.forward_given_routing(cuda(x[a:b], torch.bfloat16), cuda(ids[a:b]),
-                                                  cuda(w[a:b], torch.float32))
+                for _rep in range(2 if peer else 1):  # peer mode: arrival flags advance per forward
+                    out = layer.forward_given_routing(cuda(x[a:b], torch.bfloat16), cuda(ids[a:b]),
+                                                      cuda(w[a:b], torch.float32))
                 st.synchronize()
                 outs[r] = (out.double().cpu().numpy(), layer.comm_report(bytes_per_scalar=2))
         except Exception as e:  # surface thread failures
