@@ -261,8 +261,16 @@ def run_ours(args):
     gated = W["act"] == "swiglu"
     cfg = occ.MoEConfig(E, K_TOP, nd, D, F, activation=W["act"])
     layer = occ.ExpertParallelLayer(cfg, world_size=world, rank=rank)
+    exchange = "local"
     if world > 1:
         layer.comm_init()
+        exchange = "nccl all-to-all"
+        if args.exchange == "peer":  # fused pack/return stores over NVLink peer memory
+            try:
+                layer.comm_enable_peer(n_local)
+                exchange = "peer memory (fused)"
+            except Exception as exc:  # keep the collective path, say so in the line
+                exchange = f"nccl all-to-all (peer mapping failed: {exc})"
     if W["train"]:
         layer.set_training(True)
     prune = occ.PruneSpec(W["prune"][0], W["prune"][1]) if W["prune"] else None
@@ -486,7 +494,7 @@ def run_ours(args):
                 "data": "synthetic (uniform tokens, random-init experts and gate of the named layer shape)",
                 "config": {"workload": WORKLOAD, "experts": E, "top_k": K_TOP, "d_model": D, "d_ff": F,
                            "ffn": "SwiGLU" if gated else W["act"], "tokens_per_step": args.tokens, "ep": world,
-                           "ep_simulated_on_one_gpu": nd if world == 1 else None,
+                           "ep_simulated_on_one_gpu": nd if world == 1 else None, "exchange": exchange,
                            "l2": "flushed between steps (512 MiB write)",
                            "step": ("route + plan + pack + grouped GEMM-1/2 + partial combine + combine"
                                     + (" + backward (dgrad x2, wgrad x2, routing-weight grads)" if W["train"]
@@ -511,6 +519,7 @@ def main():
     ap.add_argument("--tokens", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of the captured CUDA graph")
+    ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"], help="world > 1 token exchange")
     ap.add_argument("--e2e-chunks", type=int, default=1)
     ap.add_argument("--e2e-flush", action="store_true", help="flush L2 between e2e steps even for large layers")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
