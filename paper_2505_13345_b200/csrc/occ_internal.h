@@ -146,9 +146,6 @@ void launch_rank_emit_compute(int R_max, const int* R_total, const int32_t* grou
                               int B, RankWs ws, const EmitCompute& e, cudaStream_t st);
 void launch_init_epd(int Q_max, int32_t* epd_src, float* epd_w, cudaStream_t st);
 
-// Gather inbox rows into the padded Epd layout (GEMM-1 A operand).
-void launch_gather_rows(int Q_max, const int* q_total, const int32_t* epd_src, const __nv_bfloat16* src, int D,
-                        __nv_bfloat16* dst, cudaStream_t st);
 
 // Epd A operand by scatter: every inbox row read once, written to each of its
 // Epd rows (row_epd); padding rows of the NG segments zeroed.  src row of
@@ -179,10 +176,8 @@ void launch_shared_gate(int n, int n_pad, int D, const __nv_bfloat16* x, const _
 void launch_extract_cindex(int R_max, const int* R_total, int P, const int32_t* row_dev, const int* in_base,
                            const int32_t* row_epd, const ComputeOffsets& o, int32_t* cindex, cudaStream_t st);
 
-// Backward (world_size == 1): upstream rows gathered into the Epd layout,
+// Backward (world_size == 1; the upstream rows reach the Epd layout through launch_scatter_rows):
 // the scatter-adjoint rows summed back onto tokens, routing-weight gradients.
-void launch_gather_token_rows(int Q_max, const int* q_total, const int32_t* epd_src, const int32_t* in_tok,
-                              const __nv_bfloat16* src, int D, __nv_bfloat16* dst, cudaStream_t st);
 void launch_combine_grad(int n, int nd, int k, int P, int dedup, int D, const uint64_t* mask, const int32_t* tok_row,
                          const int32_t* row_epd, const __nv_bfloat16* Y, float* out, cudaStream_t st);
 void launch_gw_scatter(int Q_max, const int* q_total, int NB, const float* gw_part, const int32_t* epd_src,

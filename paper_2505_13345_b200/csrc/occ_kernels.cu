@@ -417,31 +417,6 @@ __global__ void init_epd_kernel(int Q, int32_t* src, float* w) {
     if (q < Q) { src[q] = -1; w[q] = 0.0f; }
 }
 
-// ---------------------------------------------------------------- gather --
-__global__ void __launch_bounds__(256) gather_rows_kernel(int Q_max, const int* q_total, const int32_t* epd_src,
-                                                          const __nv_bfloat16* src, int D, __nv_bfloat16* dst) {
-    const int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (q >= *q_total) return;
-    const int r = epd_src[q];
-    const int nvec = D / 8;
-    uint4* out = reinterpret_cast<uint4*>(dst + (long)q * D);
-    if (r < 0) {
-        for (int v = lane; v < nvec; v += 32) out[v] = make_uint4(0, 0, 0, 0);
-        return;
-    }
-    const uint4* in = reinterpret_cast<const uint4*>(src + (long)r * D);
-    for (int v0 = 0; v0 < nvec; v0 += 4 * 32) {
-        uint4 b[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-            if (v0 + u * 32 + lane < nvec) b[u] = __ldg(in + v0 + u * 32 + lane);
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-            if (v0 + u * 32 + lane < nvec) out[v0 + u * 32 + lane] = b[u];
-    }
-}
-
 // Scatter (replaces the Epd-order gather): each inbox row is read ONCE and
 // written to every Epd row that uses it (its local experts, placement order)
 // — n_epd row writes but only R row reads, instead of n_epd scattered reads.
@@ -870,24 +845,6 @@ __global__ void extract_cindex_kernel(int R_max, const int* R_total, int P, cons
 }
 
 // -------------------------------------------------------------- backward --
-// Combine adjoint + return adjoint (backward.cpp:43-78): every Epd row of a
-// token receives the token's upstream row.
-__global__ void __launch_bounds__(256) gather_token_rows_kernel(int Q_max, const int* q_total, const int32_t* epd_src,
-                                                                const int32_t* in_tok, const __nv_bfloat16* src,
-                                                                int D, __nv_bfloat16* dst) {
-    const int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (q >= *q_total) return;
-    const int r = epd_src[q];
-    const int nvec = D / 8;
-    uint4* out = reinterpret_cast<uint4*>(dst + (long)q * D);
-    if (r < 0) {
-        for (int v = lane; v < nvec; v += 32) out[v] = make_uint4(0, 0, 0, 0);
-        return;
-    }
-    const uint4* in = reinterpret_cast<const uint4*>(src + (long)in_tok[r] * D);
-    for (int v = lane; v < nvec; v += 32) out[v] = __ldg(in + v);
-}
 
 // Scatter adjoint summed per device then over devices (backward.cpp:136-152):
 // g_x[t] = sum over the token's k Epd rows, device ascending, placement
@@ -1369,13 +1326,6 @@ void launch_init_epd(int Q_max, int32_t* epd_src, float* epd_w, cudaStream_t st)
     count_launch();
 }
 
-void launch_gather_rows(int Q_max, const int* q_total, const int32_t* epd_src, const __nv_bfloat16* src, int D,
-                        __nv_bfloat16* dst, cudaStream_t st) {
-    if (!Q_max) return;
-    gather_rows_kernel<<<(Q_max + 7) / 8, 256, 0, st>>>(Q_max, q_total, epd_src, src, D, dst);
-    count_launch();
-}
-
 void launch_scatter_rows(int R_max, const int* R_total, int P, int D, const __nv_bfloat16* src,
                          const int32_t* src_rows, const int32_t* row_epd, int NG, const ComputeOffsets& o,
                          __nv_bfloat16* dst, cudaStream_t st) {
@@ -1460,12 +1410,6 @@ void launch_peer_return(int R, int nd, int me, int P, int D, const int32_t* row_
     count_launch();
 }
 
-void launch_gather_token_rows(int Q_max, const int* q_total, const int32_t* epd_src, const int32_t* in_tok,
-                              const __nv_bfloat16* src, int D, __nv_bfloat16* dst, cudaStream_t st) {
-    if (!Q_max) return;
-    gather_token_rows_kernel<<<(Q_max + 7) / 8, 256, 0, st>>>(Q_max, q_total, epd_src, in_tok, src, D, dst);
-    count_launch();
-}
 
 void launch_combine_grad(int n, int nd, int k, int P, int dedup, int D, const uint64_t* mask, const int32_t* tok_row,
                          const int32_t* row_epd, const __nv_bfloat16* Y, float* out, cudaStream_t st) {
