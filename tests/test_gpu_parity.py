@@ -872,3 +872,18 @@ def test_wide_tile_forced_odd_blocks():
     assert len(lines) == 5, r.stdout
     for l in lines:
         assert float(l.split(" err ")[1].split()[0]) <= 1e-2, l
+
+
+@pytest.mark.parametrize("ne,k,nd", [(256, 8, 4), (200, 64, 4), (130, 3, 5)])
+def test_wide_gate_router_matches_oracle_topk(ne, k, nd):
+    """Gates wider than 128 experts take the logits + router_select path:
+    ids equal the reference top-k (routing.cpp:60-84) on the same fp32
+    softmax rows."""
+    dm, n = 128, 700
+    x, g, *_ = make_layer_inputs(ne + k, n, dm, 8, ne)
+    layer = occ.ExpertParallelLayer(occ.MoEConfig(ne, k, nd, dm, 64))
+    xs, gs = cuda(x, torch.bfloat16), cuda(g, torch.bfloat16)
+    ids, w, sc = layer.route(xs, gs, want_scores=True)
+    want_ids, want_w = O.Port().topk_route(sc.double().cpu().numpy(), k, True)
+    assert np.array_equal(ids.cpu().numpy(), want_ids)
+    assert np.allclose(w.double().cpu().numpy(), want_w, rtol=2e-6, atol=1e-7)
