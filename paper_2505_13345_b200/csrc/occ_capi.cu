@@ -944,17 +944,21 @@ occ_status occ_load_experts(occ_handle* h, const void* w1, const void* w3, const
     const int El = h->world == 1 ? h->E : h->P;
     const int D = h->D, F = h->F;
     h->n1rows = h->gated ? 2 * F : F;
-    CUDA_TRY(h->w13t.ensure((size_t)El * h->n1rows * D));
-    CUDA_TRY(h->w2t.ensure((size_t)El * D * F));
+    // resident K-major rows (row pitch = K; padding the pitch to spread L2 sets
+    // was measured: no change in DRAM traffic or time, profiles/r01_l2_traffic.md)
+    const int p1 = D, p2 = F;
+    CUDA_TRY(h->w13t.ensure((size_t)El * h->n1rows * p1));
+    CUDA_TRY(h->w2t.ensure((size_t)El * D * p2));
     const auto* b1 = reinterpret_cast<const __nv_bfloat16*>(w1);
     const auto* b2 = reinterpret_cast<const __nv_bfloat16*>(w2);
     if (h->gated) {
-        launch_transpose_weights(b1, El, D, F, h->w13t.p, h->n1rows, 1, st);
-        launch_transpose_weights(reinterpret_cast<const __nv_bfloat16*>(w3), El, D, F, h->w13t.p, h->n1rows, 2, st);
+        launch_transpose_weights(b1, El, D, F, h->w13t.p, h->n1rows, 1, st, p1);
+        launch_transpose_weights(reinterpret_cast<const __nv_bfloat16*>(w3), El, D, F, h->w13t.p, h->n1rows, 2, st,
+                                 p1);
     } else {
-        launch_transpose_weights(b1, El, D, F, h->w13t.p, h->n1rows, 0, st);
+        launch_transpose_weights(b1, El, D, F, h->w13t.p, h->n1rows, 0, st, p1);
     }
-    launch_transpose_weights(b2, El, F, D, h->w2t.p, D, 0, st);
+    launch_transpose_weights(b2, El, F, D, h->w2t.p, D, 0, st, p2);
     CUDA_TRY(cudaGetLastError());
     if (h->training) {
         // backward needs the reference orientation: w2 [E, F, D] is K-major for
@@ -972,8 +976,8 @@ occ_status occ_load_experts(occ_handle* h, const void* w1, const void* w3, const
             !make_tmap_2d(h->tmW1o.bytes, h->w13o.p, kw, (uint64_t)El * D, 64, 128))
             return fail(OCC_ERR_CUDA, "cuTensorMapEncodeTiled failed (backward weights)");
     }
-    if (!make_tmap_2d(h->tmB1.bytes, h->w13t.p, D, (uint64_t)El * h->n1rows, 64, 128) ||
-        !make_tmap_2d(h->tmB2.bytes, h->w2t.p, F, (uint64_t)El * D, 64, 128))
+    if (!make_tmap_2d(h->tmB1.bytes, h->w13t.p, D, (uint64_t)El * h->n1rows, 64, 128, 128, p1) ||
+        !make_tmap_2d(h->tmB2.bytes, h->w2t.p, F, (uint64_t)El * D, 64, 128, 128, p2))
         return fail(OCC_ERR_CUDA, "cuTensorMapEncodeTiled failed (weights)");
     h->weights_loaded = true;
     return OCC_OK;

@@ -910,11 +910,11 @@ void launch_one(int grid, const CUtensorMap& ta, const CUtensorMap& tb, const CU
 // Row-major bf16 matrix [outer, inner], 128-byte swizzled boxes of
 // box_inner (=64) x box_outer elements.  OOB reads are zero-filled.
 bool make_tmap_2d(void* tmap, const void* base, uint64_t inner, uint64_t outer, uint32_t box_inner,
-                  uint32_t box_outer, int swizzle_bytes) {
+                  uint32_t box_outer, int swizzle_bytes, uint64_t pitch_elems) {
     EncodeTiledFn enc = get_encode();
     if (!enc) return false;
     cuuint64_t dims[2] = {inner, outer};
-    cuuint64_t strides[1] = {inner * 2};
+    cuuint64_t strides[1] = {(pitch_elems ? pitch_elems : inner) * 2};
     cuuint32_t box[2] = {box_inner, box_outer};
     cuuint32_t estr[2] = {1, 1};
     return enc(reinterpret_cast<CUtensorMap*>(tmap), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base),

@@ -230,7 +230,7 @@ void launch_router_select(float* logits, int n, int e, int k, int renorm, PruneD
 // Weight layout conversion: reference [E, K, N] row-major -> K-major [E, N, K]
 // (optionally interleaving w1/w3 in 128-column blocks for SwiGLU).
 void launch_transpose_weights(const __nv_bfloat16* w, int E, int K, int N, __nv_bfloat16* out, int out_rows_per_e,
-                              int interleave_half, cudaStream_t st);
+                              int interleave_half, cudaStream_t st, int pitch = 0);
 
 // Grouped GEMM on tcgen05 (occ_gemm.cu).
 enum EpiMode {
@@ -272,7 +272,7 @@ struct GemmArgs {
 };
 void launch_grouped_gemm(EpiMode mode, const GemmArgs& a, int num_sms, cudaStream_t st);
 bool make_tmap_2d(void* tmap, const void* base, uint64_t inner, uint64_t outer, uint32_t box_inner,
-                  uint32_t box_outer, int swizzle_bytes = 128);
+                  uint32_t box_outer, int swizzle_bytes = 128, uint64_t pitch_elems = 0);
 // Output map of the TMA-store epilogue: bf16 [outer, inner] row-major, 32 x 32 boxes.
 inline bool make_tmap_out(void* tmap, const void* base, uint64_t inner, uint64_t outer) {
     return make_tmap_2d(tmap, base, inner, outer, 32, 32, 64);

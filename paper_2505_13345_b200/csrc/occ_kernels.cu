@@ -1212,7 +1212,7 @@ __global__ void router_select_kernel(float* logits, int n, int e, int k, int ren
 // are interleaved in 128-row blocks so one 256-row B tile holds matching
 // gate/up columns.
 __global__ void transpose_weights_kernel(const __nv_bfloat16* w, int K, int N, __nv_bfloat16* out, int out_rows_per_e,
-                                         int interleave_half) {
+                                         int interleave_half, int pitch) {
     __shared__ __nv_bfloat16 tile[32][33];
     const int e = blockIdx.z;
     const int n0 = blockIdx.x * 32, k0 = blockIdx.y * 32;
@@ -1227,7 +1227,7 @@ __global__ void transpose_weights_kernel(const __nv_bfloat16* w, int K, int N, _
         if (kk < K && nn < N) {
             long orow = nn;
             if (interleave_half) orow = (long)(nn / 128) * 256 + (interleave_half - 1) * 128 + nn % 128;
-            out[((long)e * out_rows_per_e + orow) * K + kk] = tile[threadIdx.x][i];
+            out[((long)e * out_rows_per_e + orow) * pitch + kk] = tile[threadIdx.x][i];
         }
     }
 }
@@ -1483,9 +1483,10 @@ void launch_router_select(float* logits, int n, int e, int k, int renorm, PruneD
 }
 
 void launch_transpose_weights(const __nv_bfloat16* w, int E, int K, int N, __nv_bfloat16* out, int out_rows_per_e,
-                              int interleave_half, cudaStream_t st) {
+                              int interleave_half, cudaStream_t st, int pitch) {
     dim3 grid((N + 31) / 32, (K + 31) / 32, E);
-    transpose_weights_kernel<<<grid, dim3(32, 8), 0, st>>>(w, K, N, out, out_rows_per_e, interleave_half);
+    transpose_weights_kernel<<<grid, dim3(32, 8), 0, st>>>(w, K, N, out, out_rows_per_e, interleave_half,
+                                                              pitch > 0 ? pitch : K);
     count_launch();
 }
 
