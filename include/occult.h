@@ -124,6 +124,18 @@ occ_status occ_load_experts(occ_handle* h, const void* w1, const void* w3, const
  *   gate [D] bf16 or NULL.  num_shared = 0 detaches them. */
 occ_status occ_load_shared_experts(occ_handle* h, int num_shared, int d_ff_shared, const void* w1, const void* w3,
                                    const void* w2, const void* gate, occ_stream_t stream);
+/* Similarity profiling (SimilarityAccumulator, pruning.cpp:165-219):
+ * occ_similarity_accumulate adds one batch of router logits [n, e] (DEVICE,
+ * fp64 when logits_fp64, else f32) into the [e, e] DEVICE double Gram
+ * `inner` (zero it first); bit-exact with the reference for fp64 logits.
+ * occ_similarity_finalize turns a HOST copy of `inner` and the token count
+ * into the squared-cosine values (HOST) for occ_set_similarity.
+ * occ_router_logits writes the production router's f32 logits x g^T. */
+occ_status occ_similarity_accumulate(const void* logits, int logits_fp64, int n, int e, double* inner,
+                                     occ_stream_t stream);
+occ_status occ_similarity_finalize(const double* inner, long long tokens, int e, double* values);
+occ_status occ_router_logits(occ_handle* h, const void* x, const void* gate, int n, float* logits,
+                             occ_stream_t stream);
 /* Squared-cosine similarity table (SimilarityTable::values, pruning.hpp:25-30),
  * HOST pointer [E * E]; the per-expert ranking is built as the reference does. */
 occ_status occ_set_similarity(occ_handle* h, const double* values);

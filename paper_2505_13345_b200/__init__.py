@@ -8,6 +8,6 @@ include/occult.h (libocc.so); this package is the host-side mirror.
 from .api import (  # noqa: F401
     CapacityError, CommReport, ConfigError, DeviceError, ExpertParallelLayer, MoEConfig, MoesimError, Placement,
     PlacementError, PruneSpec, RoutingError, ShapeError, StateError, accumulate_collab, build_collab_graph,
-    collaboration_aware_placement, exchange_layout, gate_scores_f64, launch_count, lib, normalize_graph, reschedule_placement, round_robin_sources, topk_route,
+    build_similarity_table, collaboration_aware_placement, exchange_layout, gate_scores_f64, launch_count, lib, normalize_graph, reschedule_placement, round_robin_sources, topk_route,
     trivial_placement,
 )

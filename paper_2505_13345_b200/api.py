@@ -84,7 +84,8 @@ EXPORTS = (
     "occ_route", "occ_build_dispatch", "occ_forward", "occ_forward_expert_parallel", "occ_comm_report_get",
     "occ_saved_index", "occ_coactivation_histogram", "occ_normalize_graph", "occ_reschedule_placement",
     "occ_allreduce_histogram", "occ_last_error", "occ_launch_count", "occ_set_profiling", "occ_stage_ms", "occ_forward_host", "occ_host_wait", "occ_comm_init_loopback", "occ_exchange_layout", "occ_set_training", "occ_backward",
-    "occ_load_shared_experts", "occ_comm_enable_peer",
+    "occ_load_shared_experts", "occ_comm_enable_peer", "occ_similarity_accumulate", "occ_similarity_finalize",
+    "occ_router_logits",
 )
 
 STAGES = ("route", "plan", "pack", "compute_index", "gather", "gemm1", "gemm2", "shared", "partial_combine", "combine")
@@ -293,6 +294,15 @@ class ExpertParallelLayer:
         dist.broadcast_object_list(obj, src=0, group=group)
         idb = (C.c_uint8 * 128).from_buffer_copy(obj[0])
         _check(lib().occ_comm_init(self._h, idb), "comm_init")
+
+    def router_logits(self, x: torch.Tensor, gate: torch.Tensor) -> torch.Tensor:
+        """The production router's f32 logits x g^T [n, E] (tcgen05), e.g. to
+        profile the similarity table of the similarity pruning mode."""
+        _need_cuda(x, gate)
+        out = torch.empty((x.shape[0], self.config.num_experts), dtype=torch.float32, device=x.device)
+        _check(lib().occ_router_logits(self._h, _ptr(x.contiguous()), _ptr(gate.contiguous()), x.shape[0],
+                                       _ptr(out), _stream()), "router_logits")
+        return out
 
     def comm_enable_peer(self, max_tokens_per_rank: int):
         """Fused dispatch / return over peer memory instead of all-to-all calls
@@ -569,6 +579,33 @@ def reschedule_placement(p, num_devices: int) -> Placement:
                                           out.ctypes.data_as(C.c_void_p)), "reschedule_placement")
     per = e // num_devices
     return Placement([out[d * per:(d + 1) * per].tolist() for d in range(num_devices)])
+
+
+def build_similarity_table(logit_batches, num_experts: int):
+    """build_similarity_table (pruning.cpp:213-218): the squared-cosine table
+    of router-logit columns, accumulated batch by batch on the device
+    (SimilarityAccumulator::add in fp64; bit-exact for fp64 logits), finalised
+    on the host.  Batches: CUDA tensors [n, E], float64 or float32.
+    Returns the [E, E] float64 numpy table for ExpertParallelLayer.set_similarity."""
+    import numpy as np
+    inner = None
+    tokens = 0
+    for b in logit_batches:
+        _need_cuda(b)
+        if inner is None:
+            inner = torch.zeros((num_experts, num_experts), dtype=torch.float64, device=b.device)
+        fp64 = b.dtype == torch.float64
+        bb = b.contiguous() if fp64 else b.float().contiguous()
+        _check(lib().occ_similarity_accumulate(_ptr(bb), int(fp64), bb.shape[0], num_experts, _ptr(inner),
+                                               _stream()), "similarity_accumulate")
+        tokens += bb.shape[0]
+    if inner is None:
+        raise ShapeError("build_similarity_table: no batches")
+    h = np.ascontiguousarray(inner.cpu().numpy())
+    v = np.empty_like(h)
+    _check(lib().occ_similarity_finalize(h.ctypes.data_as(C.c_void_p), C.c_longlong(tokens), num_experts,
+                                         v.ctypes.data_as(C.c_void_p)), "similarity_finalize")
+    return v
 
 
 def collaboration_aware_placement(routing_batches, num_experts: int, num_devices: int,

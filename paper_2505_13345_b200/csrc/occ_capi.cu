@@ -1054,6 +1054,51 @@ occ_status occ_set_similarity(occ_handle* h, const double* values) {
     return OCC_OK;
 }
 
+occ_status occ_similarity_accumulate(const void* logits, int logits_fp64, int n, int e, double* inner,
+                                     occ_stream_t stream) {
+    if (n < 0 || e < 1) return fail(OCC_ERR_SHAPE, "similarity: bad shape");
+    if (n > 0 && (!logits || !inner)) return fail(OCC_ERR_ARG, "null argument");
+    launch_similarity_add(logits, logits_fp64, n, e, inner, reinterpret_cast<cudaStream_t>(stream));
+    CUDA_TRY(cudaGetLastError());
+    return OCC_OK;
+}
+
+occ_status occ_similarity_finalize(const double* inner, long long tokens, int e, double* values) {
+    if (!inner || !values || e < 1) return fail(OCC_ERR_ARG, "null argument");
+    // SimilarityAccumulator::finalize (pruning.cpp:186-201), same operation order
+    const double n = tokens > 0 ? (double)tokens : 1.0;
+    for (int i = 0; i < e; ++i)
+        for (int j = 0; j < e; ++j) {
+            const double si = inner[(size_t)i * e + i], sj = inner[(size_t)j * e + j];
+            double v = 0.0;
+            if (!(si <= 0.0 || sj <= 0.0)) {
+                const double mean_ip = inner[(size_t)i * e + j] / n;
+                const double denom = (si / n) * (sj / n);
+                v = std::min(1.0, mean_ip * mean_ip / denom);
+            }
+            values[(size_t)i * e + j] = v;
+        }
+    return OCC_OK;
+}
+
+occ_status occ_router_logits(occ_handle* h, const void* x, const void* gate, int n, float* logits,
+                             occ_stream_t stream) {
+    if (!h || !x || !gate || !logits) return fail(OCC_ERR_ARG, "null argument");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (n <= 0) return OCC_OK;
+    CUDA_TRY(h->rt_ids.ensure((size_t)n * h->k));
+    CUDA_TRY(h->rt_w.ensure((size_t)n * h->k));
+    CUDA_TRY(h->err.ensure(1));
+    const int np = (h->E + 31) / 32 * 32;
+    if (!make_tmap_2d(h->tmRX.bytes, x, h->D, n, 64, 128) || !make_tmap_2d(h->tmRG.bytes, gate, h->D, h->E, 64, np))
+        return fail(OCC_ERR_CUDA, "cuTensorMapEncodeTiled failed (router)");
+    if (!launch_router_tc(h->tmRX.bytes, h->tmRG.bytes, n, h->D, h->E, h->k, h->cfg.renormalize, h->rt_ids.p,
+                          h->rt_w.p, logits, h->num_sms, st))
+        return fail(OCC_ERR_UNSUPPORTED, "router: E <= 256");
+    CUDA_TRY(cudaGetLastError());
+    return OCC_OK;
+}
+
 occ_status occ_set_validate(occ_handle* h, int on) {
     if (!h) return fail(OCC_ERR_ARG, "null handle");
     h->validate = on;

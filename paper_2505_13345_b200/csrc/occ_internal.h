@@ -198,6 +198,10 @@ void launch_peer_wait(const unsigned long long* flags, int nd, int base, unsigne
 void launch_peer_return(int R, int nd, int me, int P, int D, const int32_t* row_epd, const __nv_bfloat16* Y,
                         const int* C, const int* off_sd, const int* inoff, void* const* peer_tab, cudaStream_t st);
 
+// SimilarityAccumulator::add (pruning.cpp:169-183) on the device: inner [E, E]
+// double accumulated in place from one batch of logits (fp64 or fp32 rows).
+void launch_similarity_add(const void* logits, int fp64, int n, int e, double* inner, cudaStream_t st);
+
 // Collaboration histogram (K8).
 void launch_histogram(const int32_t* ids, int n, int k, int e, int64_t* counts, cudaStream_t st);
 

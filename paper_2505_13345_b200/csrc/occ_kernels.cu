@@ -788,6 +788,20 @@ __global__ void __launch_bounds__(256) peer_return_kernel(int R, int nd, int me,
     else sum_rows_ordered<8>(Y, qs, nq, D, lane, nullptr, dst);
 }
 
+// SimilarityAccumulator::add (pruning.cpp:169-183): inner[i][j] += sum_t
+// l[t][i] * l[t][j] over one batch, accumulated in double in ascending t
+// (one thread per upper-triangle pair, the batch sum added once, mirrored),
+// bit-exact with the reference for fp64 logits.
+template <class T>
+__global__ void similarity_add_kernel(const T* logits, int n, int e, double* inner) {
+    const int i = blockIdx.y, j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < i || j >= e) return;
+    double dot = 0.0;
+    for (int t = 0; t < n; ++t) dot = __dadd_rn(dot, __dmul_rn((double)logits[(long)t * e + i], (double)logits[(long)t * e + j]));
+    inner[(long)i * e + j] = __dadd_rn(inner[(long)i * e + j], dot);
+    if (i != j) inner[(long)j * e + i] = __dadd_rn(inner[(long)j * e + i], dot);
+}
+
 // Shared-expert gate (Qwen's shared_expert_gate): g_t = sigmoid(x[t] . gate),
 // one warp per token, fp32 accumulation.  Rows n..n_pad of the padded
 // GEMM m-tile get 0 so the padded rows stay finite.
@@ -1323,6 +1337,14 @@ void launch_rank_emit_compute(int R_max, const int* R_total, const int32_t* grou
 void launch_init_epd(int Q_max, int32_t* epd_src, float* epd_w, cudaStream_t st) {
     if (!Q_max) return;
     init_epd_kernel<<<(Q_max + 255) / 256, 256, 0, st>>>(Q_max, epd_src, epd_w);
+    count_launch();
+}
+
+void launch_similarity_add(const void* logits, int fp64, int n, int e, double* inner, cudaStream_t st) {
+    if (n <= 0) return;
+    const dim3 grid((e + 63) / 64, e);
+    if (fp64) similarity_add_kernel<double><<<grid, 64, 0, st>>>(reinterpret_cast<const double*>(logits), n, e, inner);
+    else similarity_add_kernel<float><<<grid, 64, 0, st>>>(reinterpret_cast<const float*>(logits), n, e, inner);
     count_launch();
 }
 

@@ -887,3 +887,29 @@ def test_wide_gate_router_matches_oracle_topk(ne, k, nd):
     want_ids, want_w = O.Port().topk_route(sc.double().cpu().numpy(), k, True)
     assert np.array_equal(ids.cpu().numpy(), want_ids)
     assert np.allclose(w.double().cpu().numpy(), want_w, rtol=2e-6, atol=1e-7)
+
+
+@pytest.mark.parametrize("ne,n", [(8, 777), (64, 4000), (60, 1)])
+def test_similarity_table_on_gpu(ne, n):
+    """SimilarityAccumulator (pruning.cpp:165-219) on the device: values
+    bit-exact with the reference's build_similarity_table for fp64 logits;
+    two batches equal one concatenated batch within rounding; f32 router
+    logits from the tcgen05 router feed the same path."""
+    rng = np.random.default_rng(ne + n)
+    logits = rng.normal(size=(n, ne))
+    logits[:, 0] = np.abs(logits[:, 0])
+    want, want_rank = ref().similarity_table(logits)
+    got = occ.build_similarity_table([cuda(logits)], ne)
+    assert np.array_equal(got, want)
+    if n > 1:
+        h = n // 2
+        got2 = occ.build_similarity_table([cuda(logits[:h]), cuda(logits[h:])], ne)
+        assert np.allclose(got2, want, rtol=1e-12, atol=1e-14)
+    dm = 128
+    x, g, *_ = make_layer_inputs(ne, max(n, 2), dm, 8, ne)
+    layer = occ.ExpertParallelLayer(occ.MoEConfig(ne, 2, 1 if ne <= 64 else 2, dm, 64))
+    lg = layer.router_logits(cuda(x, torch.bfloat16), cuda(g, torch.bfloat16))
+    want_l = x.astype(np.float64) @ g.astype(np.float64).T
+    assert rel_err(lg.double().cpu().numpy(), want_l) < 1e-5
+    vals = occ.build_similarity_table([lg], ne)
+    layer.set_similarity(vals)  # ranking built as the reference does
