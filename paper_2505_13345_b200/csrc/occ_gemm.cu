@@ -873,6 +873,172 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     }
 }
 
+// Weight-gradient GEMMs with the same 256 x 512 super-tiles: per expert
+// group, dW[e] (M x N) = sum over the group's rows (K) of A^T B, both
+// operands read MN-major straight from the row-major activations; two
+// 256-column accumulators share every A K-block.  fp32 outputs (split into
+// out / out2 at `split` for the SwiGLU w1 | w3 gradient).
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+    wide_wgrad_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, Params p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + W_STAGES * A_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + W_STAGES * W_B2);
+    uint64_t* empty = full + W_STAGES;
+    uint64_t* tfull = empty + W_STAGES;
+    uint64_t* tempty = tfull + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+    __shared__ int s_tb[MAX_GROUPS + 1];  // super-tile prefix per group
+    __shared__ int s_gw[MAX_GROUPS];
+    __shared__ int s_kb0[MAX_GROUPS];
+    __shared__ int s_kbn[MAX_GROUPS];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const int NBW = (p.N + 2 * BN - 1) / (2 * BN);
+    const int MT = (p.M + 2 * BM - 1) / (2 * BM);
+    if (threadIdx.x == 0) {
+        int run = 0;
+        for (int g = 0; g < p.ngroups; ++g) {
+            s_tb[g] = run;
+            const int rows = p.grp_cnt[g];
+            s_kb0[g] = p.seg_base[g] / BK;
+            s_kbn[g] = (rows + BK - 1) / BK;
+            if (rows > 0) run += MT * NBW;
+        }
+        s_tb[p.ngroups] = run;
+    }
+    for (int i = threadIdx.x; i < p.ngroups; i += blockDim.x) s_gw[i] = p.grp_w[i];
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&tmA);
+        tma_prefetch_desc(&tmB);
+        for (int st = 0; st < W_STAGES; ++st) {
+            mbar_init(&full[st], 1);
+            mbar_init(&empty[st], 1);
+        }
+        mbar_init(&tfull[0], 1);
+        mbar_init(&tempty[0], 2 * EPI_WARPS);
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc_cg2<512>(tmem_slot);
+    tc_fence_before();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const int num_tiles = s_tb[p.ngroups];
+    const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+
+    if (warp == 0) {
+        if (lane == 0) {  // -------------------------------------------- TMA producer
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = cid; tile < num_tiles; tile += ncl) {
+                int g, mt, ntw;
+                wtile_coords(tile, s_tb, p.ngroups, NBW, g, mt, ntw);
+                const int ax = mt * 2 * BM + rank * BM;
+                const int bx = 2 * ntw * BN + rank * (BN / 2);
+                for (int kb = 0; kb < s_kbn[g]; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    const uint32_t lbar = smem_u32(&full[stage]) & kPeerBitMask;
+                    if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * (A_BYTES + W_B2));
+                    const int k = (s_kb0[g] + kb) * BK;  // token rows of this K block
+                    uint8_t* a_dst = sA + stage * A_BYTES;
+                    uint8_t* b_dst = sB + stage * W_B2;
+                    tma_load_2d_cg2(a_dst, &tmA, lbar, ax, k);
+                    tma_load_2d_cg2(a_dst + A_BYTES / 2, &tmA, lbar, ax + 64, k);
+                    tma_load_2d_cg2(b_dst, &tmB, lbar, bx, k);
+                    tma_load_2d_cg2(b_dst + B_BYTES / 2, &tmB, lbar, bx + 64, k);
+                    tma_load_2d_cg2(b_dst + B_BYTES, &tmB, lbar, bx + BN, k);
+                    tma_load_2d_cg2(b_dst + B_BYTES + B_BYTES / 2, &tmB, lbar, bx + BN + 64, k);
+                    if (++stage == W_STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (rank == 0) {  // --------------------------------- MMA issuer (leader CTA)
+            constexpr uint32_t IDESC = idesc_mn(2 * BM, BN);
+            int stage = 0;
+            uint32_t phase = 0, acc_phase = 0;
+            for (int tile = cid; tile < num_tiles; tile += ncl) {
+                int g, mt, ntw;
+                wtile_coords(tile, s_tb, p.ngroups, NBW, g, mt, ntw);
+                mbar_wait(&tempty[0], acc_phase ^ 1);
+                tc_fence_after();
+                for (int kb = 0; kb < s_kbn[g]; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    if (lane == 0) {
+                        const uint32_t a0 = smem_u32(sA + stage * A_BYTES);
+                        const uint32_t b0 = smem_u32(sB + stage * W_B2);
+#pragma unroll
+                        for (int k = 0; k < BK / 16; ++k) {
+                            const uint64_t ad = sdesc_mn_sw128(a0 + k * 2048);
+                            umma_bf16_cg2(tmem_base, ad, sdesc_mn_sw128(b0 + k * 2048), IDESC, (kb | k) != 0);
+                            umma_bf16_cg2(tmem_base + BN, ad, sdesc_mn_sw128(b0 + B_BYTES + k * 2048), IDESC,
+                                          (kb | k) != 0);
+                        }
+                        umma_commit_cg2_mc(&empty[stage]);
+                    }
+                    __syncwarp();
+                    if (++stage == W_STAGES) { stage = 0; phase ^= 1; }
+                }
+                if (lane == 0) umma_commit_cg2_mc(&tfull[0]);
+                __syncwarp();
+                acc_phase ^= 1;
+            }
+        }
+    } else {  // ------------------------------------------------------------ epilogue
+        const int q = warp & 3, t = (warp - 2) >> 2;
+        uint32_t acc_phase = 0;
+        for (int tile = cid; tile < num_tiles; tile += ncl) {
+            int g, mt, ntw;
+            wtile_coords(tile, s_tb, p.ngroups, NBW, g, mt, ntw);
+            mbar_wait(&tfull[0], acc_phase);
+            tc_fence_after();
+            const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + t * BN;
+            const int m = mt * 2 * BM + rank * BM + q * 32 + lane;
+            const long ebase = (long)s_gw[g] * p.out_estride;
+#pragma unroll 1
+            for (int round = 0; round < 2; ++round) {
+                uint32_t v[4][32];
+#pragma unroll
+                for (int cc = 0; cc < 4; ++cc) tmem_ld32(tbase + (round * 4 + cc) * 32, v[cc]);
+                tmem_ld_wait();
+                if (round == 1) {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster(smem_u32(&tempty[0]) & kPeerBitMask);
+                }
+                if (m >= p.M) continue;
+#pragma unroll
+                for (int cc = 0; cc < 4; ++cc) {
+                    const int col0 = (2 * ntw + t) * BN + (round * 4 + cc) * 32;
+                    if (col0 >= p.N) continue;
+                    float* o = reinterpret_cast<float*>(p.out) + ebase + (long)m * p.ldo;
+                    int c0 = col0;
+                    if (p.out2 && col0 >= p.split) {
+                        o = reinterpret_cast<float*>(p.out2) + ebase + (long)m * p.ldo;
+                        c0 = col0 - p.split;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        if (col0 + u * 4 < p.N)
+                            *reinterpret_cast<float4*>(o + c0 + u * 4) =
+                                make_float4(__uint_as_float(v[cc][4 * u]), __uint_as_float(v[cc][4 * u + 1]),
+                                            __uint_as_float(v[cc][4 * u + 2]), __uint_as_float(v[cc][4 * u + 3]));
+                }
+            }
+            acc_phase ^= 1;
+        }
+    }
+    tc_fence_before();
+    cluster_sync();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc_cg2<512>(tmem_base);
+    }
+}
+
 template <int EPI>
 void launch_wide(int grid, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tc, const Params& p,
                  cudaStream_t st) {
@@ -997,7 +1163,17 @@ void launch_grouped_gemm(EpiMode mode, const GemmArgs& a, int num_sms, cudaStrea
         case EPI_F32: launch_one<EPI_F32, false>(grid, ta, tb, tc, p, st); break;
         case EPI_BWD_ACT: launch_one<EPI_BWD_ACT, false>(grid, ta, tb, tc, p, st); break;
         case EPI_BWD_SWIGLU: launch_one<EPI_BWD_SWIGLU, false>(grid, ta, tb, tc, p, st); break;
-        case EPI_WGRAD: launch_one<EPI_F32, true>(grid, ta, tb, tc, p, st); break;
+        case EPI_WGRAD: {
+            // wide super-tiles when the output columns split into pairs of 256-column blocks
+            if (wide_env != 0 && ((a.N + BN - 1) / BN) % 2 == 0) {
+                const int smem = W_STAGES * (A_BYTES + W_B2) + 256 + 1024;
+                cudaFuncSetAttribute(wide_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+                wide_wgrad_kernel<<<grid, THREADS, smem, st>>>(ta, tb, p);
+            } else {
+                launch_one<EPI_F32, true>(grid, ta, tb, tc, p, st);
+            }
+            break;
+        }
     }
     if (dbg_on) {  // stall-cycle breakdown, averaged over CTAs (diagnostics only)
         unsigned long long h[4 * 1024];
