@@ -360,7 +360,8 @@ def run_ours(args):
     xh.copy_(x)
     oh = torch.empty_like(xh).pin_memory()
     uh = upstream.cpu().pin_memory() if W["train"] else None
-    gxh = torch.empty((x.shape[0], D), dtype=torch.float32).pin_memory() if W["train"] else None
+    # mixed-precision training: the token gradient leaves the device in bf16
+    gxh = torch.empty((x.shape[0], D), dtype=torch.bfloat16).pin_memory() if W["train"] else None
 
     def e2e_step():
         if W["train"]:  # H2D tokens + upstream, forward + backward, D2H token gradient (double-buffered)
@@ -394,11 +395,11 @@ def run_ours(args):
         e2e_ms = float(t.item())
     e2e = {"value": args.tokens * args.steps / (e2e_ms / 1e3), "unit": "tokens/s",
            "h2d_bytes_per_step": x.numel() * x.element_size() * (2 if W["train"] else 1),
-           "d2h_bytes_per_step": out.numel() * (4 if W["train"] else out.element_size()),
+           "d2h_bytes_per_step": out.numel() * out.element_size(),
            "ms_per_step": e2e_ms / args.steps,
            "l2": ("flushed between steps" if e2e_flush else
                   f"not flushed: per-step working set {ws_bytes / 2 ** 30:.2f} GiB > 2x L2"),
-           "api": (f"ExpertParallelLayer.train_step_host (pinned host tokens + upstream in, fp32 token gradient "
+           "api": (f"ExpertParallelLayer.train_step_host (pinned host tokens + upstream in, bf16 token gradient "
                    f"out; double-buffered so the copies of steps i+1 / i-1 overlap step i)" if W["train"] else
                    f"ExpertParallelLayer.forward_host (occ_forward_host: pinned host buffers, double-buffered so "
                    f"H2D of step i+1 and D2H of step i-1 overlap the layer of step i; {args.e2e_chunks} chunk(s))")

@@ -225,6 +225,9 @@ occ_status occ_set_training(occ_handle* h, int on);
  * StateError if the forward was not run with occ_set_training(h, 1). */
 occ_status occ_backward(occ_handle* h, const void* upstream, float* g_x, float* g_w1, float* g_w3, float* g_w2,
                         float* g_weights, occ_stream_t stream);
+/* Token gradient dtype of occ_backward: 0 (default) f32, 1 bf16 (g_x then
+ * points to [n, D] bf16; mixed-precision training halves its size). */
+occ_status occ_set_grad_x_bf16(occ_handle* h, int on);
 /* CommReport of the last forward (synchronises the stream).
  * bytes_per_scalar as in forward_given_routing's argument. */
 occ_status occ_comm_report_get(occ_handle* h, int bytes_per_scalar, occ_comm_report* rep, occ_stream_t stream);

@@ -85,7 +85,7 @@ EXPORTS = (
     "occ_saved_index", "occ_coactivation_histogram", "occ_normalize_graph", "occ_reschedule_placement",
     "occ_allreduce_histogram", "occ_last_error", "occ_launch_count", "occ_set_profiling", "occ_stage_ms", "occ_forward_host", "occ_host_wait", "occ_comm_init_loopback", "occ_exchange_layout", "occ_set_training", "occ_backward",
     "occ_load_shared_experts", "occ_comm_enable_peer", "occ_similarity_accumulate", "occ_similarity_finalize",
-    "occ_router_logits",
+    "occ_router_logits", "occ_set_grad_x_bf16",
 )
 
 STAGES = ("route", "plan", "pack", "compute_index", "gather", "gemm1", "gemm2", "shared", "partial_combine", "combine")
@@ -321,15 +321,19 @@ class ExpertParallelLayer:
         """Keep what backward needs (call before load_experts)."""
         _check(lib().occ_set_training(self._h, int(on)), "set_training")
 
-    def backward(self, upstream: torch.Tensor):
+    def backward(self, upstream: torch.Tensor, grad_x_dtype: torch.dtype = torch.float32):
         """backward_vjps (backward.cpp:24-161) of the last forward: returns
-        dict(x, w1, w3, w2, routing_weights) of fp32 gradients (ids fixed)."""
+        dict(x, w1, w3, w2, routing_weights) of gradients (ids fixed): fp32,
+        except the token gradient in ``grad_x_dtype`` (fp32 or bf16)."""
         _need_cuda(upstream)
         c = self.config
         dev = upstream.device
         e_l = c.num_experts
         n = upstream.shape[0]
-        g = {"x": torch.empty((n, c.embed_dim), dtype=torch.float32, device=dev),
+        if grad_x_dtype not in (torch.float32, torch.bfloat16):
+            raise ShapeError("backward: grad_x_dtype must be float32 or bfloat16")
+        _check(lib().occ_set_grad_x_bf16(self._h, int(grad_x_dtype == torch.bfloat16)), "set_grad_x_bf16")
+        g = {"x": torch.empty((n, c.embed_dim), dtype=grad_x_dtype, device=dev),
              "w1": torch.empty((e_l, c.embed_dim, c.hidden_dim), dtype=torch.float32, device=dev),
              "w2": torch.empty((e_l, c.hidden_dim, c.embed_dim), dtype=torch.float32, device=dev),
              "routing_weights": torch.empty((n, c.top_k), dtype=torch.float32, device=dev)}
@@ -449,7 +453,8 @@ class ExpertParallelLayer:
                         grad_x_host: torch.Tensor, prune: Optional[PruneSpec] = None, wait: bool = True):
         """Training step end to end from pinned host memory: H2D of tokens and
         upstream gradient, forward_expert_parallel + backward_vjps on the
-        device, D2H of the token gradient (fp32); expert / routing-weight
+        device, D2H of the token gradient (fp32, or bf16 when grad_x_host is
+        bf16 — mixed precision halves the D2H); expert / routing-weight
         gradients stay on the device (returned).  Double-buffered like
         forward_host: the copies of step i+1 / i-1 run on two copy streams
         while step i computes.  ``wait=False`` leaves the D2H pending until
@@ -482,7 +487,7 @@ class ExpertParallelLayer:
         if tp["gdone"][slot] is not None:  # the D2H that last read this slot's gradient finished
             main.wait_event(tp["gdone"][slot])
         self.forward_expert_parallel(tp["x"][slot], gate, prune=prune, out=tp["out"][slot])
-        g = self.backward(tp["up"][slot])
+        g = self.backward(tp["up"][slot], grad_x_dtype=grad_x_host.dtype)
         ev_c = torch.cuda.Event()
         ev_c.record(main)
         tp["free"][slot] = ev_c

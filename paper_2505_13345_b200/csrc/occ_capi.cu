@@ -221,6 +221,7 @@ struct occ_handle {
     cudaStream_t s_aux = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     // peer-memory exchange (occ_comm_enable_peer)
+    int gx_bf16 = 0;  // occ_set_grad_x_bf16: token gradient written as bf16
     bool peer = false;
     int peer_cap = 0;                  // max tokens per rank per forward
     unsigned long long peer_seq = 0;   // forwards issued (arrival flag value)
@@ -1099,6 +1100,12 @@ occ_status occ_router_logits(occ_handle* h, const void* x, const void* gate, int
     return OCC_OK;
 }
 
+occ_status occ_set_grad_x_bf16(occ_handle* h, int on) {
+    if (!h) return fail(OCC_ERR_ARG, "null handle");
+    h->gx_bf16 = on ? 1 : 0;
+    return OCC_OK;
+}
+
 occ_status occ_set_validate(occ_handle* h, int on) {
     if (!h) return fail(OCC_ERR_ARG, "null handle");
     h->validate = on;
@@ -1429,7 +1436,8 @@ occ_status occ_backward(occ_handle* h, const void* upstream, float* g_x, float* 
     w1.max_tiles = NG * ((D + 255) / 256) * ((kw + 255) / 256);
     launch_grouped_gemm(EPI_WGRAD, w1, h->num_sms, st);
     // dispatch adjoint: sum each token's rows (device ascending), fp32
-    launch_combine_grad(n, nd, k, P, h->cfg.dedup, D, h->mask.p, h->tok_row.p, h->row_epd.p, h->y16.p, g_x, st);
+    launch_combine_grad(n, nd, k, P, h->cfg.dedup, D, h->mask.p, h->tok_row.p, h->row_epd.p, h->y16.p, g_x,
+                        h->gx_bf16, st);
     launch_gw_scatter((int)h->Q_max, h->d_q_total, 2 * ((F + 255) / 256), h->gw_part.p, h->epd_src.p, h->in_tok.p,
                       h->epd_j.p, k, g_weights, st);
     CUDA_TRY(cudaGetLastError());

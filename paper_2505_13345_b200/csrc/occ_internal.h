@@ -179,7 +179,7 @@ void launch_extract_cindex(int R_max, const int* R_total, int P, const int32_t* 
 // Backward (world_size == 1; the upstream rows reach the Epd layout through launch_scatter_rows):
 // the scatter-adjoint rows summed back onto tokens, routing-weight gradients.
 void launch_combine_grad(int n, int nd, int k, int P, int dedup, int D, const uint64_t* mask, const int32_t* tok_row,
-                         const int32_t* row_epd, const __nv_bfloat16* Y, float* out, cudaStream_t st);
+                         const int32_t* row_epd, const __nv_bfloat16* Y, void* out, int out_bf16, cudaStream_t st);
 void launch_gw_scatter(int Q_max, const int* q_total, int NB, const float* gw_part, const int32_t* epd_src,
                        const int32_t* in_tok, const int32_t* epd_j, int k, float* g_weights, cudaStream_t st);
 

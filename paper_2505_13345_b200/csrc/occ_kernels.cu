@@ -863,10 +863,11 @@ __global__ void extract_cindex_kernel(int R_max, const int* R_total, int P, cons
 // Scatter adjoint summed per device then over devices (backward.cpp:136-152):
 // g_x[t] = sum over the token's k Epd rows, device ascending, placement
 // order inside a device; fp32 throughout.
+template <class OutT>
 __global__ void __launch_bounds__(256) combine_grad_kernel(int n, int nd, int k, int P, int dedup, int D,
                                                            const uint64_t* mask, const int32_t* tok_row,
                                                            const int32_t* row_epd, const __nv_bfloat16* Y,
-                                                           float* out) {
+                                                           OutT* out) {
     const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (t >= n) return;
@@ -912,9 +913,18 @@ __global__ void __launch_bounds__(256) combine_grad_kernel(int n, int nd, int k,
                 }
             }
         }
-        float4* o = reinterpret_cast<float4*>(out + (long)t * D) + 2 * v;
-        o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
-        o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+        if constexpr (sizeof(OutT) == 4) {
+            float4* o = reinterpret_cast<float4*>(out + (long)t * D) + 2 * v;
+            o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+            o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+        } else {  // bf16 token gradient (mixed-precision training output)
+            uint4 o;
+            o.x = pack_bf16(acc[0], acc[1]);
+            o.y = pack_bf16(acc[2], acc[3]);
+            o.z = pack_bf16(acc[4], acc[5]);
+            o.w = pack_bf16(acc[6], acc[7]);
+            reinterpret_cast<uint4*>(out + (long)t * D)[v] = o;
+        }
     }
 }
 
@@ -1434,9 +1444,14 @@ void launch_peer_return(int R, int nd, int me, int P, int D, const int32_t* row_
 
 
 void launch_combine_grad(int n, int nd, int k, int P, int dedup, int D, const uint64_t* mask, const int32_t* tok_row,
-                         const int32_t* row_epd, const __nv_bfloat16* Y, float* out, cudaStream_t st) {
+                         const int32_t* row_epd, const __nv_bfloat16* Y, void* out, int out_bf16, cudaStream_t st) {
     if (!n) return;
-    combine_grad_kernel<<<(n + 7) / 8, 256, 0, st>>>(n, nd, k, P, dedup, D, mask, tok_row, row_epd, Y, out);
+    if (out_bf16)
+        combine_grad_kernel<__nv_bfloat16><<<(n + 7) / 8, 256, 0, st>>>(n, nd, k, P, dedup, D, mask, tok_row, row_epd,
+                                                                        Y, reinterpret_cast<__nv_bfloat16*>(out));
+    else
+        combine_grad_kernel<float><<<(n + 7) / 8, 256, 0, st>>>(n, nd, k, P, dedup, D, mask, tok_row, row_epd, Y,
+                                                                reinterpret_cast<float*>(out));
     count_launch();
 }
 

@@ -836,6 +836,13 @@ def test_train_step_host_pipeline_matches_device():
         layer.forward_expert_parallel(xi.cuda(), gs)
         want = layer.backward(ui.cuda())["x"].cpu()
         assert torch.equal(gi, want)
+    # mixed precision: bf16 token gradient = the fp32 one rounded once
+    xi, ui, _ = hosts[0]
+    gb = torch.empty((n, dm), dtype=torch.bfloat16).pin_memory()
+    layer.train_step_host(xi, gs, ui, gb)
+    layer.forward_expert_parallel(xi.cuda(), gs)
+    want = layer.backward(ui.cuda())["x"].cpu()
+    assert torch.equal(gb, want.to(torch.bfloat16))
 
 
 @pytest.mark.parametrize("act,dm,dh", [("swiglu", 2048, 512), ("silu", 2048, 2048), ("relu", 1024, 1280)])
