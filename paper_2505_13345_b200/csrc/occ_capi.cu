@@ -565,6 +565,7 @@ void launch_gemm1(occ_handle* h, int ngroups, cudaStream_t st, bool gathered) {
         g.save_a = h->save_a.p;
         g.save_b = h->gated ? h->save_b.p : nullptr;
     }
+    g.band = h->D >= 4096 ? (1 << 20) : 8;  // see launch_gemm2
     g.max_tiles = (int)h->max_mblk * (h->gated ? h->F / 128 : (h->F + 255) / 256);
     launch_grouped_gemm(h->gated ? EPI_SWIGLU_BF16 : EPI_ACT_BF16, g, h->num_sms, st);
 }
@@ -580,7 +581,9 @@ void launch_gemm2(occ_handle* h, int ngroups, cudaStream_t st) {
     g.grp_mb = h->cofs.grp_mb;
     g.grp_w = h->d_widx.p;
     g.ngroups = ngroups;
-    g.band = 8;
+    // raster band (m-tiles per band): whole experts for long K (Mixtral GEMM-2,
+    // K = 14336: +5%), 8 for short K (64-expert layers: +3-4%); profiles/r01_gemm_micro.md
+    g.band = h->F >= 4096 ? (1 << 20) : 8;
     g.out = h->y16.p;  // per-expert products in bf16 (halves the store + combine traffic)
     g.ldo = h->D;
     g.act = OCC_ACT_IDENTITY;
@@ -633,7 +636,7 @@ occ_status run_shared(occ_handle* h, const __nv_bfloat16* x, int n, cudaStream_t
     g2.grp_mb = h->sh_grp.p;
     g2.grp_w = h->sh_grp.p + 2;
     g2.ngroups = 1;
-    g2.band = 8;
+    g2.band = h->Fsh >= 4096 ? (1 << 20) : 8;
     g2.out = h->ys.p;
     g2.ldo = D;
     g2.act = OCC_ACT_IDENTITY;
@@ -1397,7 +1400,7 @@ occ_status occ_backward(occ_handle* h, const void* upstream, float* g_x, float* 
     d1.grp_mb = h->cofs.grp_mb;
     d1.grp_w = h->d_widx.p;
     d1.ngroups = NG;
-    d1.band = 8;
+    d1.band = kw >= 4096 ? (1 << 20) : 8;
     d1.out = h->y16.p;
     d1.ldo = D;
     d1.act = OCC_ACT_IDENTITY;
