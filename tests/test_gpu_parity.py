@@ -643,7 +643,10 @@ def test_multi_rank_forward_loopback(nd, ne, k, act, dedup, shared, peer):
 # ------------------------------------------------------------------ backward --
 
 BWD_CASES = [(8, 2, 2, 64, 128, "silu", 200), (8, 3, 4, 128, 256, "identity", 300), (16, 4, 4, 64, 320, "relu", 150),
-             (8, 2, 1, 256, 512, "silu", 513)]
+             (8, 2, 1, 256, 512, "silu", 513),
+             # wide-tile paths: forward / data-gradient GEMMs with K >= 1024 and weight gradients with
+             # an even number of 256-column blocks
+             (8, 2, 2, 1024, 1024, "silu", 300), (4, 1, 2, 512, 1024, "relu", 97)]
 
 
 @pytest.mark.parametrize("ne,k,nd,dm,dh,act,n", BWD_CASES)
