@@ -168,6 +168,11 @@ occ_status occ_comm_enable_peer(occ_handle* h, int max_tokens_per_rank);
  * sequentially in ascending k without FMA, softmax with max subtraction. */
 occ_status occ_gate_scores_f64(const double* x, int n, int d, const double* gate, int e, double* scores,
                                occ_stream_t stream);
+/* The router logits x @ gate^T of gate_scores before the softmax
+ * (tiled_matmul in Precision::Double, matrix.cpp:9-38, k ascending): the
+ * similarity-table profiling input of the simulate driver (cli.cpp:296-299). */
+occ_status occ_gate_logits_f64(const double* x, int n, int d, const double* gate, int e, double* logits,
+                               occ_stream_t stream);
 /* topk_route (routing.cpp:60-84): (score desc, index asc), optional
  * renormalisation; bit-exact with the reference. */
 occ_status occ_topk_route_f64(const double* scores, int n, int e, int k, int renormalize, int32_t* ids,
@@ -248,6 +253,43 @@ occ_status occ_normalize_graph(const int64_t* counts, int e, double* p);
 occ_status occ_reschedule_placement(const double* p, int e, int num_devices, int32_t* placement);
 /* Sum the histogram across ranks (world_size > 1; ncclAllReduce). */
 occ_status occ_allreduce_histogram(occ_handle* h, int64_t* counts, occ_stream_t stream);
+/* ComponentTracker input (collab.cpp:120-169): first[i*E+j] (i < j) = the
+ * first batch index t / batch in which experts i and j co-activate, INT32
+ * 0x7f7f7f7f when never; DEVICE buffers, first [E, E] overwritten. */
+occ_status occ_coactivation_first_batch(const int32_t* ids, int n, int k, int e, int batch, int32_t* first,
+                                        occ_stream_t stream);
+/* ComponentTracker::points (collab.cpp:125-169) from `first` (copied to the
+ * HOST): largest[b] = size of the largest co-activation component after
+ * batch b (0 while there is no edge). HOST buffers. */
+occ_status occ_component_growth(const int32_t* first_batch, int e, int n_batches, int32_t* largest);
+
+/* --------------------------------------------- synthetic inputs and traces */
+/* Deterministic RNG (rng.hpp:12-38): std::mt19937_64 with the reference's
+ * draws, so seeds give the reference CLI's streams. */
+typedef struct occ_rng occ_rng;
+occ_status occ_rng_create(uint64_t seed, occ_rng** out);
+void occ_rng_destroy(occ_rng* r);
+uint64_t occ_rng_next(occ_rng* r);
+/* random_matrix (core.cpp:54-58): rows x cols uniform [-1, 1), row-major,
+ * rounded through float when single != 0. HOST buffer. */
+occ_status occ_rng_matrix(occ_rng* r, int rows, int cols, int single, double* out);
+
+typedef enum { OCC_TRACE_UNIFORM = 0, OCC_TRACE_ZIPF = 1, OCC_TRACE_BLOCKS = 2 } occ_trace_dist;
+/* TraceSpec (trace_gen.hpp:12-33). */
+typedef struct {
+    int dist;          /* occ_trace_dist */
+    int num_experts;
+    int top_k;
+    int num_tokens;
+    double alpha;      /* zipf exponent */
+    int num_blocks;    /* planted clusters */
+    double p_in;       /* in-cluster probability */
+} occ_trace_spec;
+/* gen_trace (trace_gen.cpp:56-122): ids int32 [n, k], weights f64 [n, k]
+ * (descending, summing to 1), HOST buffers; identical to the reference's
+ * trace for the same spec and seed. Invalid spec: OCC_ERR_CONFIG with
+ * TraceSpec::validate's message. */
+occ_status occ_gen_trace(const occ_trace_spec* spec, uint64_t seed, int32_t* ids, double* weights);
 
 /* Stage profiling with CUDA events on the launching stream (default off).
  * occ_stage_ms fills ms[0..10) for the last occ_forward_expert_parallel /

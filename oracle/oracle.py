@@ -141,8 +141,66 @@ def ref_lib():
         lib.ref_session_destroy.argtypes = [_p]
         lib.ref_session_forward.argtypes = [_p, _p, _i, _i, _p]
         lib.ref_backward.argtypes = [_p, _i, _i, _p, _p, _i, _p, _p, _i, _i, _p, _i, _p, _i, _i] + [_p] * 5
+        lib.ref_gen_trace_text.restype = C.c_longlong
+        lib.ref_gen_trace_text.argtypes = [_i] * 4 + [_d, _i, _d, C.c_char_p, C.c_uint64, C.c_char_p, C.c_longlong]
+        lib.ref_roundtrip_text.restype = C.c_longlong
+        lib.ref_roundtrip_text.argtypes = [_i, C.c_char_p, C.c_char_p, C.c_longlong]
+        lib.ref_write_matrix_text.restype = C.c_longlong
+        lib.ref_write_matrix_text.argtypes = [_p, _i, _i, C.c_char_p, C.c_longlong]
+        lib.ref_write_placement_text.restype = C.c_longlong
+        lib.ref_write_placement_text.argtypes = [_p, _i, _i, C.c_char_p, C.c_longlong]
+        lib.ref_component_points.argtypes = [_p, _i, _i, _i, _i, _p, _p]
         _REF = lib
     return _REF
+
+
+def _ref_text(call):
+    """Run a ref_*_text shim (returns the full length, -1 on error) with a
+    buffer that grows until the text fits: (ok, text)."""
+    cap = 1 << 16
+    while True:
+        buf = C.create_string_buffer(cap)
+        n = call(buf, cap)
+        if n < cap:
+            return n >= 0, buf.value.decode("latin-1")
+        cap = n + 1
+
+
+def ref_gen_trace(dist, ne, k, n, alpha, blocks, p_in, tag, seed):
+    """write_trace(gen_trace(spec, seed)) of the reference (trace_gen.cpp,
+    io.cpp:71-86); dist 0 uniform, 1 zipf, 2 blocks."""
+    L = ref_lib()
+    return _ref_text(lambda b, c: L.ref_gen_trace_text(dist, ne, k, n, alpha, blocks, p_in, tag.encode(),
+                                                       seed & (2 ** 64 - 1), b, c))
+
+
+def ref_roundtrip(kind, text):
+    """read_* then write_* in the reference (0 trace, 1 matrix, 2 placement)."""
+    L = ref_lib()
+    return _ref_text(lambda b, c: L.ref_roundtrip_text(kind, text.encode("latin-1"), b, c))
+
+
+def ref_write_matrix(m):
+    m = _f64(m)
+    L = ref_lib()
+    return _ref_text(lambda b, c: L.ref_write_matrix_text(_ptr(m), m.shape[0], m.shape[1], b, c))[1]
+
+
+def ref_write_placement(plist):
+    a = _i32(plist)
+    L = ref_lib()
+    return _ref_text(lambda b, c: L.ref_write_placement_text(_ptr(a), a.shape[0], a.shape[1], b, c))[1]
+
+
+def ref_component_points(ids, ne, batch=256):
+    """ComponentTracker over batch-token slices (collab.cpp:120-169)."""
+    ids = _i32(ids)
+    n, k = ids.shape
+    npts = (n + batch - 1) // batch + 1
+    tok = np.zeros(npts, np.int64)
+    size = np.zeros(npts, np.int32)
+    got = ref_lib().ref_component_points(_ptr(ids), n, k, ne, batch, _ptr(tok), _ptr(size))
+    return [(int(tok[i]), int(size[i])) for i in range(got)]
 
 
 class _Backend:

@@ -11,6 +11,8 @@
 #include <cstdint>
 #include <cstring>
 #include <exception>
+#include <sstream>
+#include <string>
 #include <span>
 #include <thread>
 #include <vector>
@@ -18,6 +20,8 @@
 #include "moesim/collab.hpp"
 #include "moesim/common.hpp"
 #include "moesim/config.hpp"
+#include "moesim/io.hpp"
+#include "moesim/trace_gen.hpp"
 #include "moesim/pipeline.hpp"
 #include "moesim/placement.hpp"
 #include "moesim/pruning.hpp"
@@ -412,6 +416,90 @@ int ref_forward_expert_parallel_mt(const double* x, int n, int dm, const double*
     for (int v : rc)
         if (v) return -v;
     return n;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------- formats (io.cpp) ----
+// Text results go to (buf, cap); the return value is the full length (the
+// caller retries with a larger buffer when it exceeds cap), or -1 with the
+// exception text in buf.
+namespace {
+long long emit(const std::string& text, char* buf, long long cap) {
+    if (buf && cap > 0) {
+        const size_t m = std::min<size_t>(text.size(), static_cast<size_t>(cap - 1));
+        std::memcpy(buf, text.data(), m);
+        buf[m] = 0;
+    }
+    return static_cast<long long>(text.size());
+}
+}  // namespace
+
+extern "C" {
+
+long long ref_gen_trace_text(int dist, int ne, int k, int n, double alpha, int blocks, double p_in, const char* tag,
+                             uint64_t seed, char* buf, long long cap) {
+    try {
+        TraceSpec spec;
+        spec.dist = static_cast<TraceSpec::Dist>(dist);
+        spec.num_experts = ne;
+        spec.top_k = k;
+        spec.num_tokens = n;
+        spec.alpha = alpha;
+        spec.num_blocks = blocks;
+        spec.p_in = p_in;
+        spec.tag = tag ? tag : "";
+        std::ostringstream os;
+        write_trace(os, gen_trace(spec, seed));
+        return emit(os.str(), buf, cap);
+    } catch (const std::exception& e) {
+        emit(e.what(), buf, cap);
+        return -1;
+    }
+}
+
+// read_* then write_* of the parsed value (the round trip), or the error.
+long long ref_roundtrip_text(int kind, const char* text, char* buf, long long cap) {
+    try {
+        std::istringstream is(text);
+        std::ostringstream os;
+        if (kind == 0) write_trace(os, read_trace(is));
+        else if (kind == 1) write_matrix(os, read_matrix(is));
+        else write_placement(os, read_placement(is));
+        return emit(os.str(), buf, cap);
+    } catch (const std::exception& e) {
+        emit(e.what(), buf, cap);
+        return -1;
+    }
+}
+
+long long ref_write_matrix_text(const double* m, int rows, int cols, char* buf, long long cap) {
+    std::ostringstream os;
+    write_matrix(os, mat(m, rows, cols));
+    return emit(os.str(), buf, cap);
+}
+
+long long ref_write_placement_text(const int* plist, int nd, int per, char* buf, long long cap) {
+    std::ostringstream os;
+    write_placement(os, placement_of(plist, nd, per));
+    return emit(os.str(), buf, cap);
+}
+
+// ComponentTracker over `batch`-token slices (cli.cpp:131-145): points as
+// (tokens_seen, largest); returns the point count.
+int ref_component_points(const int* ids, int n, int k, int ne, int batch, long long* tokens, int* largest) {
+    ComponentTracker tr(ne);
+    std::vector<double> w(static_cast<size_t>(n) * k, 1.0 / k);
+    for (int t0 = 0; t0 < n; t0 += batch) {
+        const int t1 = std::min(n, t0 + batch);
+        tr.add(routing_of(ids + static_cast<size_t>(t0) * k, w.data() + static_cast<size_t>(t0) * k, t1 - t0, k));
+    }
+    const auto& pts = tr.points();
+    for (size_t i = 0; i < pts.size(); ++i) {
+        tokens[i] = pts[i].first;
+        largest[i] = pts[i].second;
+    }
+    return static_cast<int>(pts.size());
 }
 
 }  // extern "C"

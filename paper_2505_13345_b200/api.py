@@ -52,6 +52,14 @@ class StateError(MoesimError):
     pass
 
 
+class DataError(MoesimError):
+    """common.hpp DataError: malformed input files (CLI exit code 3)."""
+
+
+class UsageError(MoesimError):
+    """common.hpp UsageError: bad command-line arguments (CLI exit code 2)."""
+
+
 class DeviceError(MoesimError):
     """CUDA / NCCL failure or unsupported configuration on the B200 path."""
 
@@ -85,7 +93,8 @@ EXPORTS = (
     "occ_saved_index", "occ_coactivation_histogram", "occ_normalize_graph", "occ_reschedule_placement",
     "occ_allreduce_histogram", "occ_last_error", "occ_launch_count", "occ_set_profiling", "occ_stage_ms", "occ_forward_host", "occ_host_wait", "occ_comm_init_loopback", "occ_exchange_layout", "occ_set_training", "occ_backward",
     "occ_load_shared_experts", "occ_comm_enable_peer", "occ_similarity_accumulate", "occ_similarity_finalize",
-    "occ_router_logits", "occ_set_grad_x_bf16",
+    "occ_router_logits", "occ_set_grad_x_bf16", "occ_gate_logits_f64", "occ_coactivation_first_batch",
+    "occ_component_growth", "occ_rng_create", "occ_rng_destroy", "occ_rng_next", "occ_rng_matrix", "occ_gen_trace",
 )
 
 STAGES = ("route", "plan", "pack", "compute_index", "gather", "gemm1", "gemm2", "shared", "partial_combine", "combine")
@@ -102,6 +111,10 @@ def lib():
         L = C.CDLL(LIB_PATH)
         L.occ_last_error.restype = C.c_char_p
         L.occ_launch_count.restype = C.c_longlong
+        L.occ_rng_next.restype = C.c_uint64
+        L.occ_rng_next.argtypes = [C.c_void_p]
+        L.occ_rng_destroy.argtypes = [C.c_void_p]
+        L.occ_rng_matrix.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p]
         _LIB = L
     return _LIB
 
@@ -539,6 +552,19 @@ def gate_scores_f64(x: torch.Tensor, gate: torch.Tensor) -> torch.Tensor:
     return out
 
 
+def gate_logits_f64(x: torch.Tensor, gate: torch.Tensor) -> torch.Tensor:
+    """Router logits x @ gate^T in fp64, k ascending (tiled_matmul Double,
+    matrix.cpp:9-38); bit-exact with the reference."""
+    _need_cuda(x, gate)
+    x, gate = x.double().contiguous(), gate.double().contiguous()
+    if x.shape[1] != gate.shape[1]:
+        raise ShapeError(f"gate_logits: token width {x.shape[1]} != gate width {gate.shape[1]}")
+    out = torch.empty((x.shape[0], gate.shape[0]), dtype=torch.float64, device=x.device)
+    _check(lib().occ_gate_logits_f64(_ptr(x), x.shape[0], x.shape[1], _ptr(gate), gate.shape[0], _ptr(out),
+                                     _stream()), "gate_logits")
+    return out
+
+
 def topk_route(scores: torch.Tensor, k: int, renormalize: bool = True):
     """topk_route (routing.cpp:60-84) on fp64 scores; bit-exact."""
     _need_cuda(scores)
@@ -562,6 +588,25 @@ def accumulate_collab(counts: torch.Tensor, ids: torch.Tensor) -> torch.Tensor:
 def build_collab_graph(ids: torch.Tensor, num_experts: int) -> torch.Tensor:
     counts = torch.zeros((num_experts, num_experts), dtype=torch.int64, device=ids.device)
     return accumulate_collab(counts, ids)
+
+
+def component_growth(ids: torch.Tensor, num_experts: int, batch: int = 256):
+    """ComponentTracker over `batch`-token slices (collab.cpp:120-169,
+    cli.cpp:131-145): [(tokens_seen, largest component)], starting at (0, 0).
+    The per-pair first co-activating batch is found on the device; the
+    union-find over those edges runs on the host."""
+    import numpy as np
+    _need_cuda(ids)
+    n, k = ids.shape
+    first = torch.empty((num_experts, num_experts), dtype=torch.int32, device=ids.device)
+    _check(lib().occ_coactivation_first_batch(_ptr(ids.contiguous()), n, k, num_experts, batch, _ptr(first),
+                                              _stream()), "first_batch")
+    nb = (n + batch - 1) // batch
+    fh = np.ascontiguousarray(first.cpu().numpy())
+    largest = np.zeros(nb, np.int32)
+    _check(lib().occ_component_growth(fh.ctypes.data_as(C.c_void_p), num_experts, nb,
+                                      largest.ctypes.data_as(C.c_void_p)), "component_growth")
+    return [(0, 0)] + [(min(n, (b + 1) * batch), int(largest[b])) for b in range(nb)]
 
 
 def normalize_graph(counts) -> "numpy.ndarray":

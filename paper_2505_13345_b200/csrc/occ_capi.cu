@@ -1124,6 +1124,14 @@ occ_status occ_gate_scores_f64(const double* x, int n, int d, const double* gate
     return OCC_OK;
 }
 
+occ_status occ_gate_logits_f64(const double* x, int n, int d, const double* gate, int e, double* logits,
+                               occ_stream_t stream) {
+    if (n < 0 || d < 1 || e < 1) return fail(OCC_ERR_SHAPE, "gate_logits: bad shape");
+    launch_gate_scores_f64(x, n, d, gate, e, logits, reinterpret_cast<cudaStream_t>(stream), false);
+    CUDA_TRY(cudaGetLastError());
+    return OCC_OK;
+}
+
 occ_status occ_topk_route_f64(const double* scores, int n, int e, int k, int renormalize, int32_t* ids,
                               double* weights, occ_stream_t stream) {
     if (k < 1 || k > e || e > 256) return fail(OCC_ERR_ROUTING, "topk_route: k out of range");
@@ -1593,13 +1601,13 @@ occ_status occ_comm_report_get(occ_handle* h, int bytes_per_scalar, occ_comm_rep
     CUDA_TRY(cudaStreamSynchronize(st));
     std::memset(rep, 0, sizeof(*rep));
     const int nd = h->nd, n = h->last_n;
+    rep->cap_replicas = (double)std::min(h->k, nd);
     if (n == 0) return OCC_OK;
     long long stats[8];
     CUDA_TRY(cudaMemcpy(stats, h->stats.p, sizeof(stats), cudaMemcpyDeviceToHost));
     std::vector<int> C(nd * nd);
     CUDA_TRY(cudaMemcpy(C.data(), h->dofs.C, sizeof(int) * nd * nd, cudaMemcpyDeviceToHost));
     rep->mean_replicas = (double)stats[2] / n;
-    rep->cap_replicas = (double)std::min(h->k, nd);
     const long long pairs = stats[3] + stats[4];
     rep->intra_share = pairs ? (double)stats[3] / pairs : 0.0;
     rep->inter_share = pairs ? (double)stats[4] / pairs : 0.0;
@@ -1637,9 +1645,20 @@ occ_status occ_saved_index(occ_handle* h, int32_t* inbox_token, int32_t* inbox_s
 }
 
 occ_status occ_coactivation_histogram(const int32_t* ids, int n, int k, int e, int64_t* counts, occ_stream_t stream) {
-    if (!ids || !counts) return fail(OCC_ERR_ARG, "null argument");
-    if (e < 1 || e > 110 || k < 1) return fail(OCC_ERR_UNSUPPORTED, "histogram: 1 <= E <= 110 (shared-memory bins)");
+    if ((!ids && n > 0) || !counts) return fail(OCC_ERR_ARG, "null argument");
+    if (e < 1 || k < 1 || n < 0) return fail(OCC_ERR_SHAPE, "histogram: need E >= 1, k >= 1, n >= 0");
     launch_histogram(ids, n, k, e, counts, reinterpret_cast<cudaStream_t>(stream));
+    CUDA_TRY(cudaGetLastError());
+    return OCC_OK;
+}
+
+occ_status occ_coactivation_first_batch(const int32_t* ids, int n, int k, int e, int batch, int32_t* first,
+                                        occ_stream_t stream) {
+    if ((!ids && n > 0) || !first) return fail(OCC_ERR_ARG, "null argument");
+    if (e < 1 || k < 1 || n < 0 || batch < 1) return fail(OCC_ERR_SHAPE, "first_batch: need E, k, batch >= 1");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    CUDA_TRY(cudaMemsetAsync(first, 0x7f, sizeof(int32_t) * (size_t)e * e, st));  // 0x7f7f7f7f: never seen
+    launch_first_coactivation(ids, n, k, e, batch, first, st);
     CUDA_TRY(cudaGetLastError());
     return OCC_OK;
 }
@@ -1718,3 +1737,8 @@ occ_status occ_allreduce_histogram(occ_handle* h, int64_t* counts, occ_stream_t 
 }
 
 }  // extern "C"
+
+namespace occ {
+// Error reporting for the host-only translation unit (occ_host.cpp).
+occ_status host_fail(occ_status s, const char* msg) { return fail(s, msg); }
+}  // namespace occ

@@ -203,14 +203,18 @@ void launch_peer_return(int R, int nd, int me, int P, int D, const int32_t* row_
 void launch_similarity_add(const void* logits, int fp64, int n, int e, double* inner, cudaStream_t st);
 
 // Collaboration histogram (K8).
+// Bins in shared memory up to kHistSmemMax bytes (E <= 236), global atomics above.
+constexpr size_t kHistSmemMax = 220 * 1024;
 void launch_histogram(const int32_t* ids, int n, int k, int e, int64_t* counts, cudaStream_t st);
+void launch_first_coactivation(const int32_t* ids, int n, int k, int e, int batch, int* first, cudaStream_t st);
 
 // Comm statistics (spans, pair shares, naive crossings) per token.
 void launch_token_stats(int n, int k, int nd, const int32_t* ids, const int32_t* sources, int src_fixed,
                         const int32_t* dev_of, long long* stats, cudaStream_t st);
 
 // Routers.
-void launch_gate_scores_f64(const double* x, int n, int d, const double* g, int e, double* s, cudaStream_t st);
+void launch_gate_scores_f64(const double* x, int n, int d, const double* g, int e, double* s, cudaStream_t st,
+                            bool softmax = true);
 void launch_topk_f64(const double* s, int n, int e, int k, int renorm, int32_t* ids, double* w, int32_t* err,
                      cudaStream_t st);
 struct PruneDev {

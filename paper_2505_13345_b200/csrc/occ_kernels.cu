@@ -965,6 +965,37 @@ __global__ void __launch_bounds__(256) histogram_kernel(const int32_t* ids, int 
         if (h[i]) atomicAdd(&counts[i], (unsigned long long)h[i]);
 }
 
+// Experts beyond the shared-memory bins: count straight into the int64 table.
+__global__ void __launch_bounds__(256) histogram_global_kernel(const int32_t* ids, int n, int k, int e,
+                                                               unsigned long long* counts) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        const int32_t* row = ids + (long)t * k;
+        for (int a = 0; a < k; ++a)
+            for (int b = a + 1; b < k; ++b) {
+                atomicAdd(&counts[(long)row[a] * e + row[b]], 1ull);
+                atomicAdd(&counts[(long)row[b] * e + row[a]], 1ull);
+            }
+    }
+}
+
+// ComponentTracker input (collab.cpp:125-137): for every expert pair, the
+// first token batch (t / batch) in which it co-activates; `first` is
+// pre-filled with INT_MAX.  A plain read filters the atomics: after the first
+// few batches nearly every pair already holds a smaller value.
+__global__ void __launch_bounds__(256) first_coactivation_kernel(const int32_t* ids, int n, int k, int e, int batch,
+                                                                 int* first) {
+    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
+        const int32_t* row = ids + (long)t * k;
+        const int bt = t / batch;
+        for (int a = 0; a < k; ++a)
+            for (int b = a + 1; b < k; ++b) {
+                const int lo = min(row[a], row[b]), hi = max(row[a], row[b]);
+                int* cell = first + (long)lo * e + hi;
+                if (*(volatile int*)cell > bt) atomicMin(cell, bt);
+            }
+    }
+}
+
 // ------------------------------------------------------------ token stats --
 // Per-pass accounting (CommReport, pipeline.cpp:479-487): device span
 // (mean_token_replicas, collab.cpp:41-61), co-activated pair shares
@@ -1477,9 +1508,21 @@ void launch_histogram(const int32_t* ids, int n, int k, int e, int64_t* counts, 
     int blocks = (n + 255) / 256;
     if (blocks > 148 * 4) blocks = 148 * 4;
     const size_t smem = sizeof(unsigned) * (size_t)e * e;
-    if (smem > 48 * 1024)
-        cudaFuncSetAttribute(histogram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    histogram_kernel<<<blocks, 256, smem, st>>>(ids, n, k, e, reinterpret_cast<unsigned long long*>(counts));
+    if (smem > kHistSmemMax) {
+        histogram_global_kernel<<<blocks, 256, 0, st>>>(ids, n, k, e, reinterpret_cast<unsigned long long*>(counts));
+    } else {
+        if (smem > 48 * 1024)
+            cudaFuncSetAttribute(histogram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        histogram_kernel<<<blocks, 256, smem, st>>>(ids, n, k, e, reinterpret_cast<unsigned long long*>(counts));
+    }
+    count_launch();
+}
+
+void launch_first_coactivation(const int32_t* ids, int n, int k, int e, int batch, int* first, cudaStream_t st) {
+    if (!n || k < 2) return;
+    int blocks = (n + 255) / 256;
+    if (blocks > 148 * 4) blocks = 148 * 4;
+    first_coactivation_kernel<<<blocks, 256, 0, st>>>(ids, n, k, e, batch, first);
     count_launch();
 }
 
@@ -1490,12 +1533,15 @@ void launch_token_stats(int n, int k, int nd, const int32_t* ids, const int32_t*
     count_launch();
 }
 
-void launch_gate_scores_f64(const double* x, int n, int d, const double* g, int e, double* s, cudaStream_t st) {
+void launch_gate_scores_f64(const double* x, int n, int d, const double* g, int e, double* s, cudaStream_t st,
+                            bool softmax) {
     const long total = (long)n * e;
     if (!total) return;
     gate_logits_f64_kernel<<<(unsigned)((total + 127) / 128), 128, 0, st>>>(x, n, d, g, e, s);
+    count_launch();
+    if (!softmax) return;
     softmax_f64_kernel<<<(n + 127) / 128, 128, 0, st>>>(n, e, s);
-    count_launch(2);
+    count_launch();
 }
 
 void launch_topk_f64(const double* s, int n, int e, int k, int renorm, int32_t* ids, double* w, int32_t* err,

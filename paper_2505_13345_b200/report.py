@@ -26,7 +26,8 @@ def format_double(v: float) -> str:
     and at least two digits."""
     v = float(v)
     if not math.isfinite(v):
-        raise ValueError("refusing to serialize non-finite value")
+        from .api import DataError
+        raise DataError("refusing to serialize non-finite value")
     if v == 0.0:
         return "-0" if math.copysign(1.0, v) < 0 else "0"
     sign, digits, exp = Decimal(repr(v)).as_tuple()
