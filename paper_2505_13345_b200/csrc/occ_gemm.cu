@@ -642,6 +642,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 // loads, so the MMAs of the next super-tile wait for about one round of
 // epilogue math — small against a K >= 2048 mainloop.  4-stage ring (192 KB).
 constexpr int W_STAGES = 4;
+#ifndef OCC_W_LDC
+#define OCC_W_LDC 4
+#endif
+constexpr int W_LDC = OCC_W_LDC;
+#ifndef OCC_W_FAST
+#define OCC_W_FAST 1
+#endif
+#ifndef OCC_W_FAST_ACT
+#define OCC_W_FAST_ACT 1
+#endif
+constexpr bool W_FAST = OCC_W_FAST, W_FAST_ACT = OCC_W_FAST_ACT;  // TMEM chunks loaded per wait in the inference drain (register bound: 168)
 constexpr int W_B2 = 2 * B_BYTES;  // both B halves of this CTA per stage
 constexpr int W_SMEM_BYTES = W_STAGES * (A_BYTES + W_B2) + EPI_STAGE_BYTES + 256;
 
@@ -730,7 +741,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 const int by0 = wt.wi * p.b_rows_per_e + wt.nb0 * BN + rank * (BN / 2);
                 const bool two = wt.two;  // the second 256-row B block is part of this tile
                 for (int kb = 0; kb < KB; ++kb) {
+                    { const long long t0 = p.dbg ? clock64() : 0;
                     mbar_wait(&empty[stage], phase ^ 1);
+                    if (p.dbg) p.dbg[blockIdx.x * 4 + 0] += clock64() - t0; }
                     const uint32_t lbar = smem_u32(&full[stage]) & kPeerBitMask;
                     if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * (A_BYTES + (two ? W_B2 : B_BYTES)));
                     uint8_t* b_dst = sB + stage * W_B2;
@@ -750,10 +763,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 const WTile wt = wide_decode(tile, S, split, s_gmb, s_gw, p.ngroups, NBW, NB, p.band);
                 if (!wt.valid) continue;
                 const bool two = wt.two;
+                { const long long t0 = p.dbg ? clock64() : 0;
                 mbar_wait(&tempty[0], acc_phase ^ 1);
+                if (p.dbg && lane == 0) p.dbg[blockIdx.x * 4 + 1] += clock64() - t0; }
                 tc_fence_after();
                 for (int kb = 0; kb < KB; ++kb) {
+                    { const long long t0 = p.dbg ? clock64() : 0;
                     mbar_wait(&full[stage], phase);
+                    if (p.dbg && lane == 0) p.dbg[blockIdx.x * 4 + 2] += clock64() - t0; }
                     tc_fence_after();
                     if (lane == 0) {
                         const uint32_t a0 = smem_u32(sA + stage * A_BYTES);
@@ -787,7 +804,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             const WTile wt = wide_decode(tile, S, split, s_gmb, s_gw, p.ngroups, NBW, NB, p.band);
             if (!wt.valid) continue;
             const int mb = wt.mb;
+            { const long long t0 = p.dbg ? clock64() : 0;
             mbar_wait(&tfull[0], acc_phase);
+            if (p.dbg && lane == 0 && warp == 2) p.dbg[blockIdx.x * 4 + 3] += clock64() - t0; }
             tc_fence_after();
             const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + t * BN;
             const long row = (long)mb * 2 * BM + rank * BM + q * 32 + lane;
@@ -798,6 +817,69 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive_cluster(smem_u32(&tempty[0]) & kPeerBitMask);
+                acc_phase ^= 1;
+                continue;
+            }
+            if (p.tma_out && !p.save_a && W_FAST && (SW || W_FAST_ACT)) {
+                // Inference: drain the whole accumulator into packed bf16 registers
+                // (two TMEM loads in flight per wait), hand TMEM back, and only then
+                // stage + TMA-store, so the stores overlap the next super-tile's MMAs
+                // instead of holding its accumulator.
+                uint32_t pk[NCH][16];
+                if constexpr (SW) {
+#pragma unroll
+                    for (int c = 0; c < NCH; ++c) {
+                        uint32_t v[32], g[32];
+                        tmem_ld32(tbase + c * 32, v);
+                        tmem_ld32(tbase + 128 + c * 32, g);
+                        tmem_ld_wait();
+                        if (c == NCH - 1) {
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive_cluster(smem_u32(&tempty[0]) & kPeerBitMask);
+                        }
+#pragma unroll
+                        for (int i = 0; i < 16; ++i)
+                            pk[c][i] = pack_bf16(silu(__uint_as_float(v[2 * i])) * __uint_as_float(g[2 * i]) * wr,
+                                                 silu(__uint_as_float(v[2 * i + 1])) * __uint_as_float(g[2 * i + 1]) * wr);
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < NCH; c += W_LDC) {
+                        uint32_t v[W_LDC][32];
+#pragma unroll
+                        for (int cc = 0; cc < W_LDC; ++cc) tmem_ld32(tbase + (c + cc) * 32, v[cc]);
+                        tmem_ld_wait();
+                        if (c == NCH - W_LDC) {
+                            tc_fence_before();
+                            __syncwarp();
+                            if (lane == 0) mbar_arrive_cluster(smem_u32(&tempty[0]) & kPeerBitMask);
+                        }
+#pragma unroll
+                        for (int cc = 0; cc < W_LDC; ++cc)
+#pragma unroll
+                            for (int i = 0; i < 16; ++i)
+                                pk[c + cc][i] = pack_bf16(act_f(__uint_as_float(v[cc][2 * i]), p.act) * wr,
+                                                          act_f(__uint_as_float(v[cc][2 * i + 1]), p.act) * wr);
+                    }
+                }
+#pragma unroll
+                for (int c = 0; c < NCH; ++c) {
+                    const int col0 = nb * ncol + c * 32;
+                    if (col0 >= p.N) break;
+                    if (lane == 0) bulk_wait_read<0>();
+                    __syncwarp();
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        *reinterpret_cast<uint4*>(stg + lane * 64 + ((u ^ ((lane >> 1) & 3)) << 4)) =
+                            make_uint4(pk[c][4 * u], pk[c][4 * u + 1], pk[c][4 * u + 2], pk[c][4 * u + 3]);
+                    fence_proxy_async();
+                    __syncwarp();
+                    if (lane == 0) {
+                        tma_store_2d(&tmC, stg, col0, (int)(row - lane));
+                        bulk_commit();
+                    }
+                }
                 acc_phase ^= 1;
                 continue;
             }
@@ -1116,10 +1198,16 @@ void launch_grouped_gemm(EpiMode mode, const GemmArgs& a, int num_sms, cudaStrea
     p.a_rows = a.a_rows;
     static const bool dbg_on = getenv("OCC_GEMM_DEBUG") != nullptr;
     static unsigned long long* dbg_buf = nullptr;
+    static cudaEvent_t dbg_ev[2];
     if (dbg_on) {
-        if (!dbg_buf) cudaMalloc(&dbg_buf, sizeof(unsigned long long) * 4 * 1024);
+        if (!dbg_buf) {
+            cudaMalloc(&dbg_buf, sizeof(unsigned long long) * 4 * 1024);
+            cudaEventCreate(&dbg_ev[0]);
+            cudaEventCreate(&dbg_ev[1]);
+        }
         cudaMemsetAsync(dbg_buf, 0, sizeof(unsigned long long) * 4 * 1024, st);
         p.dbg = dbg_buf;
+        cudaEventRecord(dbg_ev[0], st);
     }
     const CUtensorMap& ta = *reinterpret_cast<const CUtensorMap*>(a.tmap_a);
     const CUtensorMap& tb = *reinterpret_cast<const CUtensorMap*>(a.tmap_b);
@@ -1144,6 +1232,7 @@ void launch_grouped_gemm(EpiMode mode, const GemmArgs& a, int num_sms, cudaStrea
     static const int wide_env = getenv("OCC_GEMM_WIDE") ? atoi(getenv("OCC_GEMM_WIDE")) : 1;
     static const int tail_env = getenv("OCC_GEMM_TAILSPLIT") ? atoi(getenv("OCC_GEMM_TAILSPLIT")) : 1;
     p.tail_split = tail_env;
+    bool wide = false;
     if ((mode == EPI_ACT_BF16 || mode == EPI_SWIGLU_BF16) && !a.a_rows) {
         const int nbk = mode == EPI_SWIGLU_BF16 ? (a.N + 127) / 128 : (a.N + BN - 1) / BN;
         // an odd block count ends in a single-block super-tile; worth it from 5 blocks up
@@ -1153,11 +1242,10 @@ void launch_grouped_gemm(EpiMode mode, const GemmArgs& a, int num_sms, cudaStrea
         if (ok && (wide_env == 2 || (wide_env == 1 && a.K >= 1024))) {
             if (mode == EPI_ACT_BF16) launch_wide<EPI_ACT_BF16>(grid, ta, tb, tc, p, st);
             else launch_wide<EPI_SWIGLU_BF16>(grid, ta, tb, tc, p, st);
-            count_launch();
-            return;
+            wide = true;
         }
     }
-    switch (mode) {
+    if (!wide) switch (mode) {
         case EPI_ACT_BF16: launch_one<EPI_ACT_BF16, false>(grid, ta, tb, tc, p, st); break;
         case EPI_SWIGLU_BF16: launch_one<EPI_SWIGLU_BF16, false>(grid, ta, tb, tc, p, st); break;
         case EPI_F32: launch_one<EPI_F32, false>(grid, ta, tb, tc, p, st); break;
@@ -1177,7 +1265,10 @@ void launch_grouped_gemm(EpiMode mode, const GemmArgs& a, int num_sms, cudaStrea
     }
     if (dbg_on) {  // stall-cycle breakdown, averaged over CTAs (diagnostics only)
         unsigned long long h[4 * 1024];
+        cudaEventRecord(dbg_ev[1], st);
         cudaStreamSynchronize(st);
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, dbg_ev[0], dbg_ev[1]);
         cudaMemcpy(h, dbg_buf, sizeof(unsigned long long) * 4 * grid, cudaMemcpyDeviceToHost);
         double sum[4] = {0, 0, 0, 0};
         int nl = 0;
@@ -1185,8 +1276,8 @@ void launch_grouped_gemm(EpiMode mode, const GemmArgs& a, int num_sms, cudaStrea
             for (int i = 0; i < 4; ++i) sum[i] += (double)h[c * 4 + i];
             nl += (c % 2 == 0);
         }
-        fprintf(stderr, "[gemm dbg] mode=%d K=%d N=%d: producer-empty %.0f, mma-tempty %.0f, mma-full %.0f, epi-tfull %.0f (kcycles/CTA)\n",
-                (int)mode, a.K, a.N, sum[0] / grid / 1e3, sum[1] / nl / 1e3, sum[2] / nl / 1e3, sum[3] / grid / 1e3);
+        fprintf(stderr, "[gemm dbg] %s mode=%d K=%d N=%d: producer-empty %.0f, mma-tempty %.0f, mma-full %.0f, epi-tfull %.0f (kcycles/CTA), %.3f ms\n",
+                wide ? "wide" : "narrow", (int)mode, a.K, a.N, sum[0] / grid / 1e3, sum[1] / nl / 1e3, sum[2] / nl / 1e3, sum[3] / grid / 1e3, ms);
     }
     count_launch();
 }

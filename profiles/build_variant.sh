@@ -1,0 +1,17 @@
+#!/bin/bash
+# A/B builds for profiling: libocc with extra -D flags on occ_gemm.cu, written to
+# profiles/variants/libocc_<name>.so (git-ignored, travels with gpurun); select
+# with OCC_LIB_EXPERIMENT=profiles/variants/libocc_<name>.so.
+# usage: profiles/build_variant.sh <name> -DFOO=1 ...
+set -e
+HERE=$(cd "$(dirname "$0")" && pwd)
+CSRC=$HERE/../paper_2505_13345_b200/csrc
+NAME=$1; shift
+OUT=$HERE/variants; mkdir -p $OUT/$NAME
+NCCL=/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl
+FL="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O2 --expt-relaxed-constexpr -I$NCCL/include"
+nvcc $FL "$@" -c $CSRC/occ_gemm.cu -o $OUT/$NAME/occ_gemm.o
+OBJS=$(ls $CSRC/build/*.o | grep -v occ_gemm.o)
+nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $OUT/libocc_$NAME.so $OUT/$NAME/occ_gemm.o $OBJS -lcudart \
+    -L$NCCL/lib -l:libnccl.so.2 -Xlinker -rpath,$NCCL/lib
+echo $OUT/libocc_$NAME.so
