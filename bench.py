@@ -290,6 +290,8 @@ def run_ours(args):
         sg = torch.empty(D, dtype=torch.bfloat16, device=dev).uniform_(-1, 1).mul_(D ** -0.5) if with_gate else None
         layer.load_shared_experts(s1, s2, s3, sg)
         del s1, s2, s3, sg
+    if args.micro_batches > 1 and not W["train"]:  # two micro-batches: exchange of one overlaps GEMMs of the other
+        layer.set_micro_batches(args.micro_batches)
     torch.cuda.empty_cache()
     gate = torch.empty((E, D), dtype=torch.bfloat16, device=dev).uniform_(-1, 1).mul_(3.0 / D ** 0.5)
     x = torch.empty((n_local, D), dtype=torch.bfloat16, device=dev).uniform_(-1, 1)
@@ -496,6 +498,7 @@ def run_ours(args):
                 "config": {"workload": WORKLOAD, "experts": E, "top_k": K_TOP, "d_model": D, "d_ff": F,
                            "ffn": "SwiGLU" if gated else W["act"], "tokens_per_step": args.tokens, "ep": world,
                            "ep_simulated_on_one_gpu": nd if world == 1 else None, "exchange": exchange,
+                           "micro_batches": args.micro_batches if not W["train"] else 1,
                            "l2": "flushed between steps (512 MiB write)",
                            "step": ("route + plan + pack + grouped GEMM-1/2 + partial combine + combine"
                                     + (" + backward (dgrad x2, wgrad x2, routing-weight grads)" if W["train"]
@@ -521,6 +524,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of the captured CUDA graph")
     ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"], help="world > 1 token exchange")
+    ap.add_argument("--micro-batches", type=int, default=1, choices=[1, 2],
+                    help="run each forward as two micro-batches on two streams (overlap of exchange and GEMMs)")
     ap.add_argument("--e2e-chunks", type=int, default=1)
     ap.add_argument("--e2e-flush", action="store_true", help="flush L2 between e2e steps even for large layers")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)

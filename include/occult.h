@@ -162,6 +162,18 @@ occ_status occ_comm_init_loopback(occ_handle* h, long group_key);
  * arrival flags instead of all-to-all calls.  Buffers are sized for
  * max_tokens_per_rank tokens per forward (larger batches: OCC_ERR_SHAPE). */
 occ_status occ_comm_enable_peer(occ_handle* h, int max_tokens_per_rank);
+/* Compute/communication overlap: every forward runs as two
+ * micro-batches, tokens [0, ceil(n/2)) on this handle and the rest on an
+ * internal sibling handle (its own workspace and communicator — ncclCommSplit
+ * — the same resident weights) on a second stream, so one half's dispatch /
+ * return exchange overlaps the other half's expert GEMMs; outputs are
+ * identical to the unsplit forward (rows are independent given routing) and
+ * the CommReport covers both halves. The GEMMs leave comm_sms SMs to the other
+ * half's exchange kernels (-1: 16 when world_size > 1, else 0).
+ * micro_batches 1 or 2. Collective when world_size > 1 (every rank, after
+ * occ_comm_init / occ_comm_enable_peer). Inference only; occ_saved_index
+ * refuses a micro-batched forward. */
+occ_status occ_set_micro_batches(occ_handle* h, int micro_batches, int comm_sms);
 
 /* -------------------------------------------------------------- routing */
 /* gate_scores (routing.cpp:33-52), exact fp64 mode: logits accumulated

@@ -94,7 +94,7 @@ EXPORTS = (
     "occ_allreduce_histogram", "occ_last_error", "occ_launch_count", "occ_set_profiling", "occ_stage_ms", "occ_forward_host", "occ_host_wait", "occ_comm_init_loopback", "occ_exchange_layout", "occ_set_training", "occ_backward",
     "occ_load_shared_experts", "occ_comm_enable_peer", "occ_similarity_accumulate", "occ_similarity_finalize",
     "occ_router_logits", "occ_set_grad_x_bf16", "occ_gate_logits_f64", "occ_coactivation_first_batch",
-    "occ_component_growth", "occ_rng_create", "occ_rng_destroy", "occ_rng_next", "occ_rng_matrix", "occ_gen_trace",
+    "occ_component_growth", "occ_set_micro_batches", "occ_rng_create", "occ_rng_destroy", "occ_rng_next", "occ_rng_matrix", "occ_gen_trace",
 )
 
 STAGES = ("route", "plan", "pack", "compute_index", "gather", "gemm1", "gemm2", "shared", "partial_combine", "combine")
@@ -321,6 +321,12 @@ class ExpertParallelLayer:
         """Fused dispatch / return over peer memory instead of all-to-all calls
         (collective; after comm_init / comm_init_loopback)."""
         _check(lib().occ_comm_enable_peer(self._h, int(max_tokens_per_rank)), "comm_enable_peer")
+
+    def set_micro_batches(self, micro_batches: int = 2, comm_sms: int = -1):
+        """occ_set_micro_batches: run every forward as two micro-batches on two
+        streams so one half's exchange overlaps the other half's GEMMs
+        (collective when world_size > 1; after comm_init / comm_enable_peer)."""
+        _check(lib().occ_set_micro_batches(self._h, micro_batches, comm_sms), "set_micro_batches")
 
     def comm_init_loopback(self, key: int):
         """Validation transport: world_size ranks as threads on one GPU."""

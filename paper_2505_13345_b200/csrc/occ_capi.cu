@@ -110,6 +110,9 @@ struct Transport {
     // in `opened` for release
     virtual occ_status exchange_pointers(const std::vector<void*>& mine, std::vector<void*>& all,
                                          std::vector<void*>& opened) = 0;
+    // a second, independent channel between the same ranks (collective: every
+    // rank calls it once, in the same order)
+    virtual occ_status split(Transport** out) = 0;
     // several all-to-alls with the same row layout (element sizes es[i]) as one exchange
     struct Part {
         const void* send;
@@ -228,6 +231,18 @@ struct occ_handle {
     DevBuf<unsigned long long> flags;  // [2 * world]: dispatch arrivals, return arrivals
     DevBuf<void*> peer_tab;            // [world * kPeerSlots]
     std::vector<void*> ipc_opened;
+    // micro-batching (occ_set_micro_batches): the second half of every
+    // forward runs on a sibling handle (own workspace, own communicator,
+    // the parent's resident weights) on its own stream, so one half's
+    // exchange overlaps the other half's expert GEMMs
+    int mb = 1;
+    int comm_sms = 0;               // SMs the GEMMs leave to the other half's exchange
+    int full_sms = 148;
+    occ_handle* sib = nullptr;
+    bool borrowed = false;          // weights / shared weights / ranking belong to the parent
+    bool last_split = false;        // the last forward ran as two micro-batches
+    cudaStream_t s_mb = nullptr;
+    cudaEvent_t ev_mb[2] = {nullptr, nullptr};
 };
 
 namespace {
@@ -292,6 +307,14 @@ struct NcclTransport : Transport {
             }
         return OCC_OK;
     }
+    occ_status split(Transport** out) override {
+        ncclComm_t c2;
+        int rank = 0;
+        NCCL_TRY(ncclCommUserRank(comm, &rank));
+        NCCL_TRY(ncclCommSplit(comm, 0, rank, &c2, nullptr));
+        *out = new NcclTransport(c2, world);
+        return OCC_OK;
+    }
     // one NCCL group (one launch) for the token rows and their routing metadata
     occ_status alltoallv_parts(const std::vector<Part>& parts, const std::vector<size_t>& soff,
                                const std::vector<size_t>& scnt, const std::vector<size_t>& roff,
@@ -322,6 +345,7 @@ struct LoopGroup {
     std::vector<std::vector<int>> counts;
     std::vector<std::vector<int64_t>> vals;
     std::vector<std::vector<void*>> ptrs;
+    std::shared_ptr<LoopGroup> child;  // Transport::split: one more group of the same ranks
     explicit LoopGroup(int w) : world(w), send(w), soff(w), scnt(w), counts(w), vals(w), ptrs(w) {}
     void barrier() {
         std::unique_lock<std::mutex> lk(m);
@@ -382,6 +406,16 @@ struct LoopbackTransport : Transport {
         all.clear();
         for (int p = 0; p < grp->world; ++p) all.insert(all.end(), grp->ptrs[p].begin(), grp->ptrs[p].end());
         grp->barrier();
+        return OCC_OK;
+    }
+    occ_status split(Transport** out) override {
+        std::shared_ptr<LoopGroup> c;
+        {
+            std::lock_guard<std::mutex> lk(grp->m);
+            if (!grp->child) grp->child = std::make_shared<LoopGroup>(grp->world);
+            c = grp->child;
+        }
+        *out = new LoopbackTransport(c, rank);
         return OCC_OK;
     }
     occ_status allreduce_i64(int64_t* buf, size_t count, cudaStream_t st) override {
@@ -843,6 +877,8 @@ extern "C" {
 const char* occ_last_error(void) { return g_err.c_str(); }
 long long occ_launch_count(void) { return g_launches; }
 
+static void unborrow(occ_handle* b);
+
 occ_status occ_create(const occ_config* cfg, const int32_t* placement, int world_size, int rank, occ_handle** out) {
     if (!cfg || !placement || !out) return fail(OCC_ERR_ARG, "null argument");
     const occ_config& c = *cfg;
@@ -881,6 +917,7 @@ occ_status occ_create(const occ_config* cfg, const int32_t* placement, int world
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, dev);
+    h->full_sms = h->num_sms;
     s = upload_tables(h);
     if (s != OCC_OK) { delete h; return s; }
     *out = h;
@@ -889,6 +926,14 @@ occ_status occ_create(const occ_config* cfg, const int32_t* placement, int world
 
 occ_status occ_destroy(occ_handle* h) {
     if (!h) return OCC_OK;
+    if (h->sib) {
+        unborrow(h->sib);
+        occ_destroy(h->sib);
+        h->sib = nullptr;
+    }
+    if (h->s_mb) cudaStreamDestroy(h->s_mb);
+    for (auto& e : h->ev_mb)
+        if (e) cudaEventDestroy(e);
     for (auto* b : {&h->d_dev_of, &h->d_slot_of, &h->d_widx, &h->d_ranking, &h->group, &h->rgroup, &h->chunk_cnt,
                     &h->chunk_cnt2, &h->totals, &h->totals2, &h->c_all, &h->snd_ids, &h->err, &h->tok_row, &h->tok_sfd, &h->lam, &h->in_ids, &h->in_tok,
                     &h->in_src, &h->in_slot, &h->in_dev, &h->row_epd, &h->epd_src})
@@ -1228,6 +1273,73 @@ occ_status occ_build_dispatch(occ_handle* h, const int32_t* ids, const int32_t* 
     return check_err(h, st);
 }
 
+static occ_status forward_one(occ_handle* h, const void* x, const int32_t* ids, const float* weights,
+                              const int32_t* sources, int n, void* out, cudaStream_t st);
+
+// Sibling views of the parent's resident weights, shared experts and
+// similarity ranking (borrowed: never reallocated or freed by the sibling).
+static void sync_sibling(occ_handle* h) {
+    occ_handle* b = h->sib;
+    b->w13t.p = h->w13t.p, b->w13t.n = h->w13t.n;
+    b->w2t.p = h->w2t.p, b->w2t.n = h->w2t.n;
+    b->tmB1 = h->tmB1, b->tmB2 = h->tmB2;
+    b->n1rows = h->n1rows;
+    b->weights_loaded = h->weights_loaded;
+    b->n_shared = h->n_shared, b->Fsh = h->Fsh, b->sh_rows = h->sh_rows, b->sh_gate = h->sh_gate;
+    b->w13s.p = h->w13s.p, b->w13s.n = h->w13s.n;
+    b->w2s.p = h->w2s.p, b->w2s.n = h->w2s.n;
+    b->sgate.p = h->sgate.p, b->sgate.n = h->sgate.n;
+    b->tmBS1 = h->tmBS1, b->tmBS2 = h->tmBS2;
+    b->d_ranking.p = h->d_ranking.p, b->d_ranking.n = h->d_ranking.n;
+    b->have_ranking = h->have_ranking;
+    b->validate = h->validate;
+    b->num_sms = h->num_sms;
+    b->gather_a = h->gather_a;
+}
+
+static void unborrow(occ_handle* b) {
+    for (auto* d : {&b->w13t, &b->w2t, &b->w13s, &b->w2s, &b->sgate}) d->p = nullptr, d->n = 0;
+    b->d_ranking.p = nullptr, b->d_ranking.n = 0;
+}
+
+// Two micro-batches: tokens [0, n0) on this handle and `st`, [n0, n) on the
+// sibling and its stream, forked from and joined back into `st`.
+static occ_status forward_split(occ_handle* h, const void* x, const int32_t* ids, const float* weights,
+                                const int32_t* sources, int n, void* out, cudaStream_t st) {
+    occ_handle* b = h->sib;
+    sync_sibling(h);
+    if (b->n_shared > 0) {
+        CUDA_TRY(b->sh_grp.ensure(4));
+        if (!b->s_aux) {
+            CUDA_TRY(cudaStreamCreateWithFlags(&b->s_aux, cudaStreamNonBlocking));
+            CUDA_TRY(cudaEventCreateWithFlags(&b->ev_fork, cudaEventDisableTiming));
+            CUDA_TRY(cudaEventCreateWithFlags(&b->ev_join, cudaEventDisableTiming));
+        }
+    }
+    int n0 = (n + 1) / 2;
+    // round-robin sources (t mod N_d) stay those of the whole batch
+    if (h->world == 1 && !sources) n0 = std::min(n, (n0 + h->nd - 1) / h->nd * h->nd);
+    const int n1 = n - n0;
+    const size_t D = h->D, k = h->k;
+    CUDA_TRY(cudaEventRecord(h->ev_mb[0], st));
+    CUDA_TRY(cudaStreamWaitEvent(h->s_mb, h->ev_mb[0], 0));
+    occ_status s = forward_one(h, x, ids, weights, sources, n0, out, st);
+    if (s != OCC_OK) return s;
+    const bool second = n1 > 0 || h->world > 1;  // every rank joins the sibling's collectives
+    if (second) {
+        s = forward_one(b, reinterpret_cast<const __nv_bfloat16*>(x) + n0 * D, ids + n0 * k, weights + n0 * k,
+                        sources ? sources + n0 : nullptr, n1, reinterpret_cast<__nv_bfloat16*>(out) + n0 * D,
+                        h->s_mb);
+        if (s != OCC_OK) return s;
+    } else {
+        b->last_n = 0;
+    }
+    CUDA_TRY(cudaEventRecord(h->ev_mb[1], h->s_mb));
+    CUDA_TRY(cudaStreamWaitEvent(st, h->ev_mb[1], 0));
+    h->last_split = second;
+    return OCC_OK;
+}
+
 occ_status occ_forward(occ_handle* h, const void* x, const int32_t* ids, const float* weights,
                        const int32_t* sources, int n, void* out, occ_stream_t stream) {
     if (!h) return fail(OCC_ERR_ARG, "null handle");
@@ -1235,6 +1347,13 @@ occ_status occ_forward(occ_handle* h, const void* x, const int32_t* ids, const f
     if (!h->weights_loaded) return fail(OCC_ERR_STATE, "forward: experts not loaded");
     if (n < 0) return fail(OCC_ERR_SHAPE, "forward: negative token count");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (h->mb > 1 && h->sib) return forward_split(h, x, ids, weights, sources, n, out, st);
+    h->last_split = false;
+    return forward_one(h, x, ids, weights, sources, n, out, st);
+}
+
+static occ_status forward_one(occ_handle* h, const void* x, const int32_t* ids, const float* weights,
+                              const int32_t* sources, int n, void* out, cudaStream_t st) {
     if (h->world > 1)
         return forward_multi(h, reinterpret_cast<const __nv_bfloat16*>(x), ids, weights, n,
                              reinterpret_cast<__nv_bfloat16*>(out), st);
@@ -1332,6 +1451,7 @@ occ_status occ_forward_expert_parallel(occ_handle* h, const void* x, const void*
 occ_status occ_set_training(occ_handle* h, int on) {
     if (!h) return fail(OCC_ERR_ARG, "null handle");
     if (on && h->world != 1) return fail(OCC_ERR_UNSUPPORTED, "backward: world_size 1 in this build");
+    if (on && h->mb > 1) return fail(OCC_ERR_UNSUPPORTED, "training: micro-batching is inference-only");
     h->training = on;
     h->have_train_state = false;
     return OCC_OK;
@@ -1525,7 +1645,7 @@ occ_status occ_forward_host(occ_handle* h, const void* x_host, const void* gate,
     // devices local, the layer of each (slot, chunk) replays as a CUDA graph:
     // small batches are otherwise bound by the ~20 kernel launches per call.
     auto& hg = h->hgraph[slot];
-    const bool use_graph = !h->validate && h->world == 1 && !h->profiling && chunks == 1 && n > 0;
+    const bool use_graph = !h->validate && h->world == 1 && !h->profiling && chunks == 1 && n > 0 && h->mb == 1;
     if (use_graph) {
         const bool same = hg.exec && hg.n == n && hg.gate == gate && hg.chunks == chunks && hg.gen == g_buf_gen &&
                           hg.training == h->training &&
@@ -1600,13 +1720,25 @@ occ_status occ_comm_report_get(occ_handle* h, int bytes_per_scalar, occ_comm_rep
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
     CUDA_TRY(cudaStreamSynchronize(st));
     std::memset(rep, 0, sizeof(*rep));
-    const int nd = h->nd, n = h->last_n;
+    const int nd = h->nd;
     rep->cap_replicas = (double)std::min(h->k, nd);
+    // a micro-batched forward reports both halves together
+    occ_handle* parts[2] = {h, h->last_split ? h->sib : nullptr};
+    long long stats[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    std::vector<long long> C(nd * nd, 0);
+    long long n = 0;
+    for (occ_handle* x : parts) {
+        if (!x || x->last_n == 0) continue;
+        if (x != h) CUDA_TRY(cudaStreamSynchronize(h->s_mb));
+        long long st8[8];
+        std::vector<int> Cx(nd * nd);
+        CUDA_TRY(cudaMemcpy(st8, x->stats.p, sizeof(st8), cudaMemcpyDeviceToHost));
+        CUDA_TRY(cudaMemcpy(Cx.data(), x->dofs.C, sizeof(int) * nd * nd, cudaMemcpyDeviceToHost));
+        for (int i = 0; i < 8; ++i) stats[i] += st8[i];
+        for (int i = 0; i < nd * nd; ++i) C[i] += Cx[i];
+        n += x->last_n;
+    }
     if (n == 0) return OCC_OK;
-    long long stats[8];
-    CUDA_TRY(cudaMemcpy(stats, h->stats.p, sizeof(stats), cudaMemcpyDeviceToHost));
-    std::vector<int> C(nd * nd);
-    CUDA_TRY(cudaMemcpy(C.data(), h->dofs.C, sizeof(int) * nd * nd, cudaMemcpyDeviceToHost));
     rep->mean_replicas = (double)stats[2] / n;
     const long long pairs = stats[3] + stats[4];
     rep->intra_share = pairs ? (double)stats[3] / pairs : 0.0;
@@ -1618,7 +1750,7 @@ occ_status occ_comm_report_get(occ_handle* h, int bytes_per_scalar, occ_comm_rep
     rep->n_epd = stats[6];
     for (int d = 0; d < nd; ++d) {
         long long r = 0;
-        for (int s = 0; s < nd; ++s) r += C[s * nd + d];
+        for (int s2 = 0; s2 < nd; ++s2) r += C[s2 * nd + d];
         rep->per_device_rows[d] = r;
     }
     return OCC_OK;
@@ -1626,6 +1758,7 @@ occ_status occ_comm_report_get(occ_handle* h, int bytes_per_scalar, occ_comm_rep
 
 occ_status occ_saved_index(occ_handle* h, int32_t* inbox_token, int32_t* inbox_source, int32_t* inbox_slot,
                            int32_t* cindex, occ_stream_t stream) {
+    if (h && h->last_split) return fail(OCC_ERR_STATE, "saved index: the last forward ran as two micro-batches");
     if (!h) return fail(OCC_ERR_ARG, "null handle");
     if (!h->have_forward) return fail(OCC_ERR_STATE, "no saved forward state");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -1726,6 +1859,53 @@ occ_status occ_comm_enable_peer(occ_handle* h, int max_tokens_per_rank) {
     h->peer = true;
     h->peer_cap = max_tokens_per_rank;
     h->peer_seq = 0;
+    if (h->sib) return occ_comm_enable_peer(h->sib, max_tokens_per_rank);
+    return OCC_OK;
+}
+
+occ_status occ_set_micro_batches(occ_handle* h, int micro_batches, int comm_sms) {
+    if (!h) return fail(OCC_ERR_ARG, "null handle");
+    if (h->borrowed) return fail(OCC_ERR_STATE, "micro-batches: not on a sibling handle");
+    if (micro_batches < 1 || micro_batches > 2) return fail(OCC_ERR_UNSUPPORTED, "micro_batches must be 1 or 2");
+    if (micro_batches > 1 && h->training) return fail(OCC_ERR_UNSUPPORTED, "micro-batching is inference-only");
+    if (micro_batches == 1) {
+        if (h->sib) {
+            unborrow(h->sib);
+            occ_destroy(h->sib);
+            h->sib = nullptr;
+        }
+        h->mb = 1;
+        h->last_split = false;
+        h->num_sms = h->full_sms;
+        return OCC_OK;
+    }
+    if (h->world > 1 && !h->tp) return fail(OCC_ERR_STATE, "micro-batches: call occ_comm_init first");
+    if (!h->sib) {
+        occ_handle* b = nullptr;
+        occ_status s = occ_create(&h->cfg, h->plist.data(), h->world, h->rank, &b);
+        if (s != OCC_OK) return s;
+        b->borrowed = true;
+        if (h->world > 1) {
+            Transport* t2 = nullptr;
+            if ((s = h->tp->split(&t2)) != OCC_OK) {
+                occ_destroy(b);
+                return s;
+            }
+            b->tp = t2;
+            if (h->peer && (s = occ_comm_enable_peer(b, h->peer_cap)) != OCC_OK) {
+                occ_destroy(b);
+                return s;
+            }
+        }
+        if (!h->s_mb) {
+            CUDA_TRY(cudaStreamCreateWithFlags(&h->s_mb, cudaStreamNonBlocking));
+            for (auto& e : h->ev_mb) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+        h->sib = b;
+    }
+    h->mb = 2;
+    h->comm_sms = comm_sms >= 0 ? comm_sms : (h->world > 1 ? 16 : 0);
+    h->num_sms = std::max(2, (h->full_sms - h->comm_sms) & ~1);
     return OCC_OK;
 }
 

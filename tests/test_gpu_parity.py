@@ -573,11 +573,13 @@ def test_forward_host_graph_replay():
                                                            (8, 64, 8, "relu", True, 0, True),
                                                            (4, 8, 3, "identity", False, 0, True),
                                                            (4, 16, 4, "swiglu", True, 2, True)])
-def test_multi_rank_forward_loopback(nd, ne, k, act, dedup, shared, peer):
+@pytest.mark.parametrize("mb", [1, 2])
+def test_multi_rank_forward_loopback(nd, ne, k, act, dedup, shared, peer, mb):
     """The world_size == N_d code path (per-rank plan, count all-gather, two
     variable all-to-alls, per-device BRIM1 + GEMMs + partial combine,
     combine) with the ranks as threads on one GPU, against the reference's
-    single-process simulation with sources = owning rank."""
+    single-process simulation with sources = owning rank; mb = 2 runs every
+    forward as two micro-batches (the overlap path)."""
     import threading
     dm, dh = 128, 256
     n_per = [37, 64, 5, 100, 0, 64, 33, 1][:nd]
@@ -617,6 +619,8 @@ def test_multi_rank_forward_loopback(nd, ne, k, act, dedup, shared, peer):
                 layer.comm_init_loopback(int(key))
                 if peer:
                     layer.comm_enable_peer(128)
+                if mb > 1:  # two micro-batches per forward: sibling handle + split communicator
+                    layer.set_micro_batches(mb)
                 a, b = starts[r], starts[r + 1]
                 for _rep in range(2 if peer else 1):  # peer mode: arrival flags advance per forward
                     out = layer.forward_given_routing(cuda(x[a:b], torch.bfloat16), cuda(ids[a:b]),
@@ -923,3 +927,51 @@ def test_similarity_table_on_gpu(ne, n):
     assert rel_err(lg.double().cpu().numpy(), want_l) < 1e-5
     vals = occ.build_similarity_table([lg], ne)
     layer.set_similarity(vals)  # ranking built as the reference does
+
+
+# ------------------------------------------- micro-batched (overlapped) forward --
+@pytest.mark.parametrize("ne,k,nd,dm,dh,act,n,shared,sources", [
+    (8, 2, 2, 128, 256, "silu", 1000, 0, False), (8, 2, 2, 128, 256, "silu", 1, 0, False),
+    (16, 4, 4, 64, 128, "relu", 333, 0, True), (64, 6, 8, 256, 128, "swiglu", 777, 2, False),
+    (8, 3, 1, 128, 256, "identity", 5, 1, False)])
+def test_micro_batched_forward_bit_identical(ne, k, nd, dm, dh, act, n, shared, sources):
+    """occ_set_micro_batches(2): the two halves on two streams give the unsplit
+    forward's output bit for bit and the same CommReport (world_size 1; the
+    world_size > 1 split is in test_multi_rank_forward_loopback)."""
+    gated = act == "swiglu"
+    x, g, w1, w2, w3 = make_layer_inputs(ne + n, n, dm, dh, ne, gated=gated)
+    ids, w = random_routing(n, ne, k, np.random.default_rng(n))
+    src = cuda(np.random.default_rng(1).integers(0, nd, n).astype(np.int32)) if sources else None
+    res = {}
+    for mb in (1, 2):
+        layer = occ.ExpertParallelLayer(occ.MoEConfig(ne, k, nd, dm, dh, activation=act),
+                                        occ.Placement([list(p) for p in _placement(ne, nd, "shuffled", seed=3)]))
+        layer.load_experts(cuda(w1, torch.bfloat16), cuda(w2, torch.bfloat16), cuda(w3, torch.bfloat16) if gated else None)
+        if shared:
+            s1, s2, s3, sg = make_shared(shared, dm, 128, gated, seed=4)
+            layer.load_shared_experts(cuda(s1, torch.bfloat16), cuda(s2, torch.bfloat16),
+                                      cuda(s3, torch.bfloat16) if gated else None, cuda(sg, torch.bfloat16))
+        if mb == 2:
+            layer.set_micro_batches(2)
+        xs = cuda(x, torch.bfloat16)
+        a = layer.forward_given_routing(xs, cuda(ids), cuda(w, torch.float32), sources=src)
+        b = layer.forward_expert_parallel(xs, cuda(g, torch.bfloat16), sources=src)
+        rep = layer.comm_report(bytes_per_scalar=2)
+        torch.cuda.synchronize()
+        res[mb] = (a, b, rep)
+    assert torch.equal(res[1][0], res[2][0])
+    assert torch.equal(res[1][1], res[2][1])
+    r1, r2 = res[1][2], res[2][2]
+    assert (r1.mean_replicas, r1.cross_device_bytes, r1.per_device_token_counts, r1.intra_share) == \
+        (r2.mean_replicas, r2.cross_device_bytes, r2.per_device_token_counts, r2.intra_share)
+
+
+def test_micro_batches_guards():
+    layer = occ.ExpertParallelLayer(occ.MoEConfig(8, 2, 2, 64, 64, activation="silu"))
+    with pytest.raises(occ.api.MoesimError):
+        layer.set_micro_batches(3)
+    layer.set_micro_batches(2)
+    with pytest.raises(occ.api.MoesimError):
+        layer.set_training(True)
+    layer.set_micro_batches(1)
+    layer.set_training(True)
