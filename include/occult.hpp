@@ -101,6 +101,10 @@ class Layer {
         check(occ_load_shared_experts(h_, num_shared, d_ff_shared, w1, w3, w2, gate, s), "load_shared_experts");
     }
     void set_validate(bool on) { check(occ_set_validate(h_, on), "set_validate"); }
+    // Two micro-batches per forward on two streams (exchange / GEMM overlap); collective at world > 1.
+    void set_micro_batches(int micro_batches, int comm_sms = -1) {
+        check(occ_set_micro_batches(h_, micro_batches, comm_sms), "set_micro_batches");
+    }
     void set_placement(const Placement& placement) {
         std::vector<int32_t> flat;
         for (const auto& d : placement.devices) flat.insert(flat.end(), d.begin(), d.end());
