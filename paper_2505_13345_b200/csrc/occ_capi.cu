@@ -707,7 +707,7 @@ occ_status run_plan(occ_handle* h, const int32_t* ids, const float* w, const int
     EmitDispatch em{n, k, nd, dedup, ids, w, sources, -1, h->d_dev_of.p, h->dofs, 1, h->tok_row.p, h->tok_sfd.p,
                     h->lam.p, h->in_tok.p, h->in_src.p, h->in_slot.p, h->in_dev.p};
     launch_rank_emit_dispatch(items, h->group.p, h->mask.p, nd, nd, ws, em, st);
-    launch_token_stats(n, k, nd, ids, sources, -1, h->d_dev_of.p, h->stats.p, st);
+    launch_token_stats(n, k, nd, ids, sources, -1, h->d_dev_of.p, h->E, h->stats.p, st);
     return OCC_OK;
 }
 
@@ -777,7 +777,7 @@ occ_status forward_multi(occ_handle* h, const __nv_bfloat16* x, const int32_t* i
     EmitDispatch em{n, k, nd, dedup, ids, weights, nullptr, r, h->d_dev_of.p, h->dofs, 0, h->tok_row.p,
                     h->tok_sfd.p, h->lam.p, nullptr, nullptr, nullptr, nullptr};
     launch_rank_emit_dispatch(items, h->group.p, h->mask.p, 1, nd, ws, em, st);
-    launch_token_stats(n, k, nd, ids, nullptr, r, h->d_dev_of.p, h->stats.p, st);
+    launch_token_stats(n, k, nd, ids, nullptr, r, h->d_dev_of.p, h->E, h->stats.p, st);
     // 2. pack this source's Sfd batch (peer mode: straight into the peers' inboxes, below)
     mark(h, ST_PACK, st);
     PackArgs pk{n, k, nd, D, dedup, x, ids, weights, h->mask.p, h->tok_row.p, h->snd_x.p, h->snd_ids.p, h->snd_w.p};

@@ -210,7 +210,7 @@ void launch_first_coactivation(const int32_t* ids, int n, int k, int e, int batc
 
 // Comm statistics (spans, pair shares, naive crossings) per token.
 void launch_token_stats(int n, int k, int nd, const int32_t* ids, const int32_t* sources, int src_fixed,
-                        const int32_t* dev_of, long long* stats, cudaStream_t st);
+                        const int32_t* dev_of, int E, long long* stats, cudaStream_t st);
 
 // Routers.
 void launch_gate_scores_f64(const double* x, int n, int d, const double* g, int e, double* s, cudaStream_t st,

@@ -32,14 +32,22 @@ __global__ void plan_mask_kernel(PlanArgs a) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= a.n) return;
     const int s = a.src_fixed >= 0 ? 0 : (a.sources ? a.sources[t] : t % a.nd);
-    if (s < 0 || s >= a.nd) { atomicExch(a.err, 1); return; }  // ShapeError: source out of range
+    // an invalid token is flagged and planned with no destinations, so nothing
+    // downstream indexes by its ids / source (the forward then reports the error)
+    auto drop = [&](int code) {
+        atomicExch(a.err, code);
+        if (a.dedup) { a.mask[t] = 0; a.group[t] = 0; }
+        else
+            for (int j = 0; j < a.k; ++j) { a.mask[(long)t * a.k + j] = 0; a.group[(long)t * a.k + j] = 0; }
+    };
+    if (s < 0 || s >= a.nd) { drop(1); return; }  // ShapeError: source out of range
     uint64_t m = 0;
     for (int j = 0; j < a.k; ++j) {
         const int e = a.ids[(long)t * a.k + j];
         const float wt = a.w ? a.w[(long)t * a.k + j] : 1.0f;
         bool bad = e < 0 || e >= a.E || !(wt > 0.0f);
         for (int l = 0; l < j && !bad; ++l) bad = a.ids[(long)t * a.k + l] == e;
-        if (bad) { atomicExch(a.err, 4); return; }  // RoutingError
+        if (bad) { drop(4); return; }  // RoutingError
         const uint64_t bit = 1ull << a.dev_of[e];
         if (a.dedup) m |= bit;
         else { a.mask[(long)t * a.k + j] = bit; a.group[(long)t * a.k + j] = s; }
@@ -288,7 +296,8 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs a) {
             rows[nrows++] = a.tok_row[(long)t * a.nd + d];
         }
     } else {
-        for (int j = 0; j < a.k; ++j) rows[nrows++] = a.tok_row[(long)t * a.k + j];
+        for (int j = 0; j < a.k; ++j)
+            if (a.mask[(long)t * a.k + j]) rows[nrows++] = a.tok_row[(long)t * a.k + j];
     }
     for (int v0 = 0; a.dst_x && v0 < nvec; v0 += 8 * 32) {
         uint4 buf[8];
@@ -710,6 +719,7 @@ __global__ void __launch_bounds__(256) peer_pack_kernel(PackArgs a, int me, cons
         }
     } else {  // replicate-k baseline: one row per (token, expert), carrying only that expert
         for (int j = 0; j < a.k; ++j) {
+            if (!a.mask[(long)t * a.k + j]) continue;  // dropped (invalid) token
             const int d = dev_of[a.ids[(long)t * a.k + j]];
             dsts[nrow] = d;
             jsel[nrow] = j;
@@ -953,8 +963,10 @@ __global__ void __launch_bounds__(256) histogram_kernel(const int32_t* ids, int 
         const int32_t* row = ids + (long)t * k;
         for (int a = 0; a < k; ++a) {
             const int ea = row[a];
+            if ((unsigned)ea >= (unsigned)e) continue;  // invalid ids are not counted
             for (int b = a + 1; b < k; ++b) {
                 const int eb = row[b];
+                if ((unsigned)eb >= (unsigned)e) continue;
                 atomicAdd(&h[ea * e + eb], 1u);
                 atomicAdd(&h[eb * e + ea], 1u);
             }
@@ -972,6 +984,7 @@ __global__ void __launch_bounds__(256) histogram_global_kernel(const int32_t* id
         const int32_t* row = ids + (long)t * k;
         for (int a = 0; a < k; ++a)
             for (int b = a + 1; b < k; ++b) {
+                if ((unsigned)row[a] >= (unsigned)e || (unsigned)row[b] >= (unsigned)e) continue;
                 atomicAdd(&counts[(long)row[a] * e + row[b]], 1ull);
                 atomicAdd(&counts[(long)row[b] * e + row[a]], 1ull);
             }
@@ -990,6 +1003,7 @@ __global__ void __launch_bounds__(256) first_coactivation_kernel(const int32_t* 
         for (int a = 0; a < k; ++a)
             for (int b = a + 1; b < k; ++b) {
                 const int lo = min(row[a], row[b]), hi = max(row[a], row[b]);
+                if (lo < 0 || hi >= e) continue;
                 int* cell = first + (long)lo * e + hi;
                 if (*(volatile int*)cell > bt) atomicMin(cell, bt);
             }
@@ -1002,10 +1016,12 @@ __global__ void __launch_bounds__(256) first_coactivation_kernel(const int32_t* 
 // (collab.cpp:105-118) and naive replicate-k crossings
 // (test_simnet.cpp:167-180 brute force, per expert instead of per device).
 __global__ void token_stats_kernel(int n, int k, int nd, const int32_t* ids, const int32_t* sources, int src_fixed,
-                                   const int32_t* dev_of, long long* stats) {
+                                   const int32_t* dev_of, int E, long long* stats) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     long long span = 0, naive = 0, intra = 0, inter = 0;
-    if (t < n) {
+    bool ok = t < n;
+    for (int j = 0; ok && j < k; ++j) ok = (unsigned)ids[(long)t * k + j] < (unsigned)E;  // invalid: flagged by the plan
+    if (ok) {
         const int s = src_fixed >= 0 ? src_fixed : (sources ? sources[t] : t % nd);
         uint64_t m = 0;
         for (int j = 0; j < k; ++j) {
@@ -1527,9 +1543,9 @@ void launch_first_coactivation(const int32_t* ids, int n, int k, int e, int batc
 }
 
 void launch_token_stats(int n, int k, int nd, const int32_t* ids, const int32_t* sources, int src_fixed,
-                        const int32_t* dev_of, long long* stats, cudaStream_t st) {
+                        const int32_t* dev_of, int E, long long* stats, cudaStream_t st) {
     if (!n) return;
-    token_stats_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, k, nd, ids, sources, src_fixed, dev_of, stats);
+    token_stats_kernel<<<(n + 255) / 256, 256, 0, st>>>(n, k, nd, ids, sources, src_fixed, dev_of, E, stats);
     count_launch();
 }
 
