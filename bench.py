@@ -259,39 +259,46 @@ def run_ours(args):
 
     nd = W["nd_sim"] if world == 1 else world
     gated = W["act"] == "swiglu"
-    cfg = occ.MoEConfig(E, K_TOP, nd, D, F, activation=W["act"])
-    layer = occ.ExpertParallelLayer(cfg, world_size=world, rank=rank)
-    exchange = "local"
-    if world > 1:
-        layer.comm_init()
-        exchange = "nccl all-to-all"
-        if args.exchange == "peer":  # fused pack/return stores over NVLink peer memory
-            try:
-                layer.comm_enable_peer(n_local)
-                exchange = "peer memory (fused)"
-            except Exception as exc:  # keep the collective path, say so in the line
-                exchange = f"nccl all-to-all (peer mapping failed: {exc})"
-    if W["train"]:
-        layer.set_training(True)
     prune = occ.PruneSpec(W["prune"][0], W["prune"][1]) if W["prune"] else None
     e_local = E if world == 1 else E // world
-    w1 = torch.empty((e_local, D, F), dtype=torch.bfloat16, device=dev).uniform_(-1, 1).mul_(D ** -0.5)
-    w3 = torch.empty((e_local, D, F), dtype=torch.bfloat16, device=dev).uniform_(-1, 1).mul_(D ** -0.5) \
-        if gated else None
-    w2 = torch.empty((e_local, F, D), dtype=torch.bfloat16, device=dev).uniform_(-1, 1).mul_(F ** -0.5)
-    layer.load_experts(w1, w2, w3)
-    del w1, w2, w3
-    sh = W.get("shared")
-    if sh:  # shared experts: dense FFN on every token at its source (+ Qwen's sigmoid gate)
-        ns, fs, with_gate = sh
-        s1 = torch.empty((ns, D, fs), dtype=torch.bfloat16, device=dev).uniform_(-1, 1).mul_(D ** -0.5)
-        s3 = torch.empty_like(s1).uniform_(-1, 1).mul_(D ** -0.5) if gated else None
-        s2 = torch.empty((ns, fs, D), dtype=torch.bfloat16, device=dev).uniform_(-1, 1).mul_((ns * fs) ** -0.5)
-        sg = torch.empty(D, dtype=torch.bfloat16, device=dev).uniform_(-1, 1).mul_(D ** -0.5) if with_gate else None
-        layer.load_shared_experts(s1, s2, s3, sg)
-        del s1, s2, s3, sg
-    if args.micro_batches > 1 and not W["train"]:  # two micro-batches: exchange of one overlaps GEMMs of the other
-        layer.set_micro_batches(args.micro_batches)
+
+    def build_layer(use_peer):
+        """The layer of this rank: NCCL communicator, optionally the fused
+        peer-memory exchange, resident experts (+ shared experts)."""
+        cfg = occ.MoEConfig(E, K_TOP, nd, D, F, activation=W["act"])
+        layer = occ.ExpertParallelLayer(cfg, world_size=world, rank=rank)
+        exchange = "local"
+        if world > 1:
+            layer.comm_init()
+            exchange = "nccl all-to-all"
+            if use_peer:  # fused pack/return stores over NVLink peer memory
+                try:
+                    layer.comm_enable_peer(n_local)
+                    exchange = "peer memory (fused)"
+                except Exception as exc:  # keep the collective path, say so in the line
+                    exchange = f"nccl all-to-all (peer mapping failed: {exc})"
+        if W["train"]:
+            layer.set_training(True)
+        w1 = torch.empty((e_local, D, F), dtype=torch.bfloat16, device=dev).uniform_(-1, 1).mul_(D ** -0.5)
+        w3 = torch.empty((e_local, D, F), dtype=torch.bfloat16, device=dev).uniform_(-1, 1).mul_(D ** -0.5) \
+            if gated else None
+        w2 = torch.empty((e_local, F, D), dtype=torch.bfloat16, device=dev).uniform_(-1, 1).mul_(F ** -0.5)
+        layer.load_experts(w1, w2, w3)
+        del w1, w2, w3
+        sh = W.get("shared")
+        if sh:  # shared experts: dense FFN on every token at its source (+ Qwen's sigmoid gate)
+            ns, fs, with_gate = sh
+            s1 = torch.empty((ns, D, fs), dtype=torch.bfloat16, device=dev).uniform_(-1, 1).mul_(D ** -0.5)
+            s3 = torch.empty_like(s1).uniform_(-1, 1).mul_(D ** -0.5) if gated else None
+            s2 = torch.empty((ns, fs, D), dtype=torch.bfloat16, device=dev).uniform_(-1, 1).mul_((ns * fs) ** -0.5)
+            sg = torch.empty(D, dtype=torch.bfloat16, device=dev).uniform_(-1, 1).mul_(D ** -0.5) if with_gate else None
+            layer.load_shared_experts(s1, s2, s3, sg)
+            del s1, s2, s3, sg
+        if args.micro_batches > 1 and not W["train"]:  # two micro-batches: exchange of one overlaps GEMMs of the other
+            layer.set_micro_batches(args.micro_batches)
+        return layer, exchange
+
+    layer, exchange = build_layer(world > 1 and args.exchange == "peer")
     torch.cuda.empty_cache()
     gate = torch.empty((E, D), dtype=torch.bfloat16, device=dev).uniform_(-1, 1).mul_(3.0 / D ** 0.5)
     x = torch.empty((n_local, D), dtype=torch.bfloat16, device=dev).uniform_(-1, 1)
@@ -313,6 +320,25 @@ def run_ours(args):
         if W["train"]:
             layer.backward(upstream)
 
+    ok, fail_note = True, "on another rank"
+    try:  # world > 1: a peer mapping that does not deliver (arrival timeout) falls back to NCCL on every rank
+        step()
+        torch.cuda.synchronize()
+    except Exception as exc:  # noqa: BLE001
+        ok, fail_note = False, str(exc)
+    if world > 1:
+        import torch.distributed as dist
+        flag = torch.tensor([1 if ok else 0], device=dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        ok = bool(flag.item())
+    if not ok:
+        if world == 1 or args.exchange != "peer":
+            raise RuntimeError(f"first step failed: {fail_note}")
+        del layer
+        torch.cuda.empty_cache()
+        layer, exchange = build_layer(False)
+        exchange += " (peer-memory exchange failed its first step; fell back)"
+        layer.set_validate(False)
     for _ in range(args.warmup):
         flush.zero_()
         step()
