@@ -315,12 +315,13 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs a) {
             }
         }
     }
+    // (a token's naive rows are all kept or all dropped, so row q carries slot q)
     for (int q = 0; q < nrows; ++q) {
-        if (lane < a.k) {
-            const long di = (long)rows[q] * a.k + lane;
-            const bool keep = a.dedup || lane == q;  // naive rows carry only their own expert
-            a.dst_ids[di] = keep ? a.ids[(long)t * a.k + lane] : -1;
-            a.dst_w[di] = keep ? a.w[(long)t * a.k + lane] : 0.0f;
+        for (int j = lane; j < a.k; j += 32) {
+            const long di = (long)rows[q] * a.k + j;
+            const bool keep = a.dedup || j == q;  // naive rows carry only their own expert
+            a.dst_ids[di] = keep ? a.ids[(long)t * a.k + j] : -1;
+            a.dst_w[di] = keep ? a.w[(long)t * a.k + j] : 0.0f;
         }
     }
 }
@@ -731,13 +732,13 @@ __global__ void __launch_bounds__(256) peer_pack_kernel(PackArgs a, int me, cons
         __nv_bfloat16* px = reinterpret_cast<__nv_bfloat16*>(peer_tab[d * kPeerSlots + kPeerInX]);
         uint4* dst = reinterpret_cast<uint4*>(px + (long)rows[q] * a.D);
         for (int v = lane; v < nvec; v += 32) dst[v] = __ldg(src + v);
-        if (lane < a.k) {
-            int32_t* pid = reinterpret_cast<int32_t*>(peer_tab[d * kPeerSlots + kPeerInIds]);
-            float* pw = reinterpret_cast<float*>(peer_tab[d * kPeerSlots + kPeerInW]);
-            const long di = (long)rows[q] * a.k + lane;
-            const bool keep = jsel[q] < 0 || lane == jsel[q];
-            pid[di] = keep ? a.ids[(long)t * a.k + lane] : -1;
-            pw[di] = keep ? a.w[(long)t * a.k + lane] : 0.0f;
+        int32_t* pid = reinterpret_cast<int32_t*>(peer_tab[d * kPeerSlots + kPeerInIds]);
+        float* pw = reinterpret_cast<float*>(peer_tab[d * kPeerSlots + kPeerInW]);
+        for (int j = lane; j < a.k; j += 32) {
+            const long di = (long)rows[q] * a.k + j;
+            const bool keep = jsel[q] < 0 || j == jsel[q];
+            pid[di] = keep ? a.ids[(long)t * a.k + j] : -1;
+            pw[di] = keep ? a.w[(long)t * a.k + j] : 0.0f;
         }
     }
 }

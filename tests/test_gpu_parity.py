@@ -180,6 +180,10 @@ FWD_CASES = [
     (8, 1, 8, 64, 64, "silu", 129, "trivial"),
     (8, 2, 2, 40, 72, "silu", 100, "shuffled"),       # D, F multiples of 8 only (TMA zero-fills the K tail)
     (8, 2, 2, 1024, 1800, "relu", 300, "trivial"),   # wide super-tiles with a ragged last N block
+    # maximum sizes of the device path: E = 256 with 64 experts per device, top-k = 64, 64 devices
+    (256, 16, 4, 64, 64, "silu", 300, "shuffled"),
+    (128, 64, 2, 64, 64, "relu", 100, "shuffled"),
+    (64, 64, 64, 32, 32, "identity", 70, "shuffled"),
 ]
 
 
@@ -572,7 +576,10 @@ def test_forward_host_graph_replay():
                                                            (2, 8, 2, "silu", True, 0, True),
                                                            (8, 64, 8, "relu", True, 0, True),
                                                            (4, 8, 3, "identity", False, 0, True),
-                                                           (4, 16, 4, "swiglu", True, 2, True)])
+                                                           (4, 16, 4, "swiglu", True, 2, True),
+                                                           # maximum top-k, NCCL-free and peer
+                                                           (2, 128, 64, "relu", True, 0, False),
+                                                           (2, 128, 64, "silu", False, 0, True)])
 @pytest.mark.parametrize("mb", [1, 2])
 def test_multi_rank_forward_loopback(nd, ne, k, act, dedup, shared, peer, mb):
     """The world_size == N_d code path (per-rank plan, count all-gather, two
@@ -648,6 +655,7 @@ def test_multi_rank_forward_loopback(nd, ne, k, act, dedup, shared, peer, mb):
 
 BWD_CASES = [(8, 2, 2, 64, 128, "silu", 200), (8, 3, 4, 128, 256, "identity", 300), (16, 4, 4, 64, 320, "relu", 150),
              (8, 2, 1, 256, 512, "silu", 513),
+             (128, 64, 2, 64, 64, "relu", 100),  # maximum top-k
              # wide-tile paths: forward / data-gradient GEMMs with K >= 1024 and weight gradients with
              # an even number of 256-column blocks
              (8, 2, 2, 1024, 1024, "silu", 300), (4, 1, 2, 512, 1024, "relu", 97)]
