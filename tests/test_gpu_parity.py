@@ -368,7 +368,9 @@ def test_histogram_bit_exact(ne, k):
 
 @pytest.mark.parametrize("mode", ["router", "similarity"])
 @pytest.mark.parametrize("own", [False, True])
-@pytest.mark.parametrize("ne,nd,k,budget", [(8, 4, 2, 1), (16, 4, 4, 2), (64, 8, 8, 2), (64, 8, 6, 3), (60, 4, 4, 2)])
+@pytest.mark.parametrize("ne,nd,k,budget", [(8, 4, 2, 1), (16, 4, 4, 2), (64, 8, 8, 2), (64, 8, 6, 3), (60, 4, 4, 2),
+                                           # maximum sizes; (256, 16, 40, 2) cannot fit top-40 on 2 devices
+                                           (256, 4, 64, 1), (256, 64, 16, 4), (128, 2, 64, 2), (256, 16, 40, 2)])
 def test_prune_routing_bit_exact(mode, own, ne, nd, k, budget):
     if mode == "router" and own:
         pytest.skip("weight policy only applies to similarity replacement")
@@ -417,7 +419,8 @@ def test_router_with_pruning_respects_budget():
 
 
 @pytest.mark.parametrize("ne,k,nd,budget,renorm", [(64, 8, 8, 2, True), (60, 4, 4, 2, True), (16, 4, 4, 1, False),
-                                                   (128, 6, 8, 3, True), (32, 2, 2, 1, True)])
+                                                   (128, 6, 8, 3, True), (32, 2, 2, 1, True),
+                                                   (128, 64, 2, 1, True), (256, 16, 4, 2, True), (256, 64, 8, 4, False)])
 def test_router_epilogue_pruning_matches_oracle(ne, k, nd, budget, renorm):
     """Router-score pruning fused into the tcgen05 router's epilogue equals
     prune_routing (pruning.cpp:35-64, oracle restatement) applied to the same
