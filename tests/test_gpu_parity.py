@@ -526,8 +526,8 @@ def test_full_size_indices_vs_reference(name, ne, k, nd, n, prune):
         cpos += P * R
 
 
-@pytest.mark.parametrize("chunks", [1, 3, 4])
-def test_forward_host_pipeline_matches_device(chunks):
+@pytest.mark.parametrize("chunks,mb", [(1, 1), (3, 1), (4, 1), (1, 2), (3, 2)])
+def test_forward_host_pipeline_matches_device(chunks, mb):
     """occ_forward_host (pinned host in/out, chunked H2D/layer/D2H pipeline)
     gives bit-identical rows to the device-resident forward: rows are
     independent given routing and the kernels are order-deterministic."""
@@ -538,6 +538,9 @@ def test_forward_host_pipeline_matches_device(chunks):
     xs = cuda(x, torch.bfloat16)
     gs = cuda(g, torch.bfloat16)
     want = layer.forward_expert_parallel(xs, gs).cpu()
+    if mb > 1:  # the micro-batched forward inside the host pipeline
+        layer.set_micro_batches(mb)
+        layer.set_validate(False)
     xh = xs.cpu().pin_memory()
     oh = torch.empty_like(xh).pin_memory()
     layer.forward_host(xh, gs, oh, chunks=chunks)
