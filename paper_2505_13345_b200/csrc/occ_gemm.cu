@@ -637,22 +637,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 // super-tile as two 256 x 256 accumulators sharing each A K-block (both TMEM
 // halves, 512 columns).  Per CTA and K block it stages A 16 KB + 2 x B 16 KB =
 // 48 KB for two MMAs instead of 2 x 32 KB: 25% less L2 -> SM operand traffic.
-// The price is one accumulator buffer (no double buffering): the epilogue
-// drains it in two rounds and hands it back after the second round's TMEM
-// loads, so the MMAs of the next super-tile wait for about one round of
-// epilogue math — small against a K >= 2048 mainloop.  4-stage ring (192 KB).
+// The price is one accumulator buffer (no double buffering): the inference
+// epilogue drains it into packed bf16 registers, hands it back, and only then
+// stages + TMA-stores (training keeps a two-round drain, with the fp32
+// pre-activation stores between the rounds), so the MMAs of the next
+// super-tile wait for the TMEM loads alone.  4-stage ring (192 KB).
 constexpr int W_STAGES = 4;
-#ifndef OCC_W_LDC
-#define OCC_W_LDC 4
-#endif
-constexpr int W_LDC = OCC_W_LDC;
-#ifndef OCC_W_FAST
-#define OCC_W_FAST 1
-#endif
-#ifndef OCC_W_FAST_ACT
-#define OCC_W_FAST_ACT 1
-#endif
-constexpr bool W_FAST = OCC_W_FAST, W_FAST_ACT = OCC_W_FAST_ACT;  // TMEM chunks loaded per wait in the inference drain (register bound: 168)
+// TMEM chunks loaded per tcgen05.wait::ld in the inference drain of the
+// non-gated epilogue: 4 (two waits for the 8 chunks) measured best; 1-2 chunks
+// per wait expose the TMEM load latency (168-register cap with 10 warps,
+// profiles/r01_wide_drain_ab.md)
+constexpr int W_LDC = 4;
 constexpr int W_B2 = 2 * B_BYTES;  // both B halves of this CTA per stage
 constexpr int W_SMEM_BYTES = W_STAGES * (A_BYTES + W_B2) + EPI_STAGE_BYTES + 256;
 
@@ -820,7 +815,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 acc_phase ^= 1;
                 continue;
             }
-            if (p.tma_out && !p.save_a && W_FAST && (SW || W_FAST_ACT)) {
+            if (p.tma_out && !p.save_a) {
                 // Inference: drain the whole accumulator into packed bf16 registers
                 // (two TMEM loads in flight per wait), hand TMEM back, and only then
                 // stage + TMA-store, so the stores overlap the next super-tile's MMAs
