@@ -262,10 +262,11 @@ def run_ours(args):
     prune = occ.PruneSpec(W["prune"][0], W["prune"][1]) if W["prune"] else None
     e_local = E if world == 1 else E // world
 
-    def build_layer(use_peer):
+    def build_layer(use_peer, dedup=True):
         """The layer of this rank: NCCL communicator, optionally the fused
-        peer-memory exchange, resident experts (+ shared experts)."""
-        cfg = occ.MoEConfig(E, K_TOP, nd, D, F, activation=W["act"])
+        peer-memory exchange, resident experts (+ shared experts); dedup=False
+        is the replicate-k dispatch (one row per (token, expert))."""
+        cfg = occ.MoEConfig(E, K_TOP, nd, D, F, activation=W["act"], dedup=dedup)
         layer = occ.ExpertParallelLayer(cfg, world_size=world, rank=rank)
         exchange = "local"
         if world > 1:
@@ -475,6 +476,54 @@ def run_ours(args):
     if W["train"]:
         roofline["step_tflops_fwd_bwd"] = (flops1 + flops2 + train_flops) / (tot_ms / args.steps / 1e3) / 1e12
 
+    # --- the non-dedup GPU baseline of the north star: the same layer with the
+    # replicate-k dispatch (one Sfd row per (token, expert)), same steps, same
+    # exchange, timed the same way; speedup = its step time / ours ------------
+    non_dedup = None
+    if not W["train"] and not args.no_baseline_layer:
+        nlayer, _ = build_layer(world > 1 and exchange.startswith("peer"), dedup=False)
+        nlayer.set_validate(False)
+        nout = torch.empty_like(out)
+
+        def nstep():
+            nlayer.forward_expert_parallel(x, gate, prune=prune, out=nout)
+
+        for _ in range(args.warmup):
+            flush.zero_()
+            nstep()
+        barrier()
+        nrun = nstep
+        if world == 1 and not args.no_graph:
+            s2 = torch.cuda.Stream()
+            s2.wait_stream(stream)
+            with torch.cuda.stream(s2):
+                nstep()
+            stream.wait_stream(s2)
+            ngraph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(ngraph):
+                nstep()
+            nrun = ngraph.replay
+        nev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        barrier()
+        for i in range(args.steps):
+            flush.zero_()
+            nev[i][0].record(stream)
+            nrun()
+            nev[i][1].record(stream)
+        barrier()
+        n_ms = sum(a.elapsed_time(b) for a, b in nev)
+        if world > 1:
+            t = torch.tensor([n_ms], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            n_ms = float(t.item())
+        nrep = nlayer.comm_report(bytes_per_scalar=2)
+        non_dedup = {"what": "same layer, replicate-k dispatch (one row per (token, expert): the non-dedup GPU "
+                             "baseline of the north star), same exchange and timing",
+                     "ms_per_step": n_ms / args.steps, "speedup": n_ms / tot_ms,
+                     "crossing_rows_per_step": nrep.crossing_rows, "dedup_crossing_rows_per_step": rep.crossing_rows}
+        del nlayer, nout
+        torch.cuda.empty_cache()
+
     # --- all-to-all bytes/token: dedup vs naive top-k at the config's EP ------
     def a2a_at(ep, placement=None):
         e_pad = -(-E // ep) * ep  # Qwen's 60 experts at EP=8: 4 never-routed padding experts
@@ -531,7 +580,7 @@ def run_ours(args):
                                        else ""))},
                 "e2e": e2e, "gpu_launches": launches, "cuda_graph": graph is not None, "clocks": clk,
                 "roofline": roofline,
-                "stages_ms": stages, "a2a": a2a, "cpu_baseline": cpu,
+                "stages_ms": stages, "a2a": a2a, "non_dedup_baseline": non_dedup, "cpu_baseline": cpu,
                 "comm_report": {"mean_replicas": rep.mean_replicas, "n_sfd": rep.n_sfd, "n_epd": rep.n_epd}}
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -552,6 +601,8 @@ def main():
     ap.add_argument("--exchange", default="peer", choices=["peer", "nccl"], help="world > 1 token exchange")
     ap.add_argument("--micro-batches", type=int, default=1, choices=[1, 2],
                     help="run each forward as two micro-batches on two streams (overlap of exchange and GEMMs)")
+    ap.add_argument("--no-baseline-layer", action="store_true",
+                    help="skip timing the replicate-k (non-dedup) layer next to ours")
     ap.add_argument("--e2e-chunks", type=int, default=1)
     ap.add_argument("--e2e-flush", action="store_true", help="flush L2 between e2e steps even for large layers")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
