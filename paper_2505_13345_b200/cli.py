@@ -250,7 +250,9 @@ def write_simulate_report(o, result):
     cfg, placement, ids, rep, _baseline_k, err, n = result
     counts = api.build_collab_graph(ids, cfg.num_experts).cpu().numpy()
     text = render_simulate_report(
-        cfg, rep, counts, placement.devices, n, seed=o.seed, precision=o.precision, activation=o.activation,
+        # config.seed is printed as static_cast<long long> of the uint64 seed (cli.cpp:337)
+        cfg, rep, counts, placement.devices, n, seed=o.seed - (1 << 64) if o.seed >= 1 << 63 else o.seed,
+        precision=o.precision, activation=o.activation,
         prune_mode=o.prune, prune_budget=o.budget, trace=o.trace or "-", placement_name=o.placement or "trivial",
         bytes_per_scalar=o.bytes_per_scalar, oracle_max_rel_error=err)
     _write(o.out, text)
