@@ -1222,7 +1222,8 @@ occ_status occ_prune_routing_f64(occ_handle* h, const double* scores, const int3
 
 occ_status occ_route(occ_handle* h, const void* x, const void* gate, int n, const occ_prune* prune, int32_t* ids,
                      float* weights, float* scores, occ_stream_t stream) {
-    if (!h || !x || !gate || !ids || !weights) return fail(OCC_ERR_ARG, "null argument");
+    if (!h || !gate || (n > 0 && (!x || !ids || !weights))) return fail(OCC_ERR_ARG, "null argument");
+    if (n < 0) return fail(OCC_ERR_SHAPE, "route: negative token count");
     PruneDev p;
     occ_status s = prune_dev(h, prune, p);
     if (s != OCC_OK) return s;

@@ -668,7 +668,8 @@ BWD_CASES = [(8, 2, 2, 64, 128, "silu", 200), (8, 3, 4, 128, 256, "identity", 30
 
 
 @pytest.mark.parametrize("ne,k,nd,dm,dh,act,n", BWD_CASES)
-def test_backward_matches_reference(ne, k, nd, dm, dh, act, n):
+@pytest.mark.parametrize("dedup", [True, False])
+def test_backward_matches_reference(ne, k, nd, dm, dh, act, n, dedup):
     """backward_vjps (backward.cpp:24-161) of the reference on identical
     bf16-representable inputs: every gradient block within 2e-2 normwise."""
     x, g, w1, w2, _ = make_layer_inputs(ne + n, n, dm, dh, ne)
@@ -678,7 +679,7 @@ def test_backward_matches_reference(ne, k, nd, dm, dh, act, n):
     src = (np.arange(n) % nd).astype(np.int32)
     up = bf16_round(np.random.default_rng(1).uniform(-1, 1, (n, dm)))
     rgx, rgw1, rgw2, rgr = O.ref_backward(x, ids, w, w1, w2, plist, src, up, act=act)
-    layer = occ.ExpertParallelLayer(occ.MoEConfig(ne, k, nd, dm, dh, activation=act),
+    layer = occ.ExpertParallelLayer(occ.MoEConfig(ne, k, nd, dm, dh, activation=act, dedup=dedup),
                                     occ.Placement([list(p) for p in plist]))
     layer.set_training(True)
     layer.load_experts(cuda(w1, torch.bfloat16), cuda(w2, torch.bfloat16))
@@ -989,3 +990,36 @@ def test_micro_batches_guards():
         layer.set_training(True)
     layer.set_micro_batches(1)
     layer.set_training(True)
+
+
+def test_degenerate_batches():
+    """Zero tokens through every entry point: routed forward, micro-batched
+    forward, host pipeline, training step and CommReport; one token with the
+    maximum top-k."""
+    ne, k, nd, dm, dh = 8, 2, 2, 64, 128
+    x, g, w1, w2, _ = make_layer_inputs(3, 4, dm, dh, ne)
+    layer = occ.ExpertParallelLayer(occ.MoEConfig(ne, k, nd, dm, dh, activation="silu"))
+    layer.set_training(True)
+    layer.load_experts(cuda(w1, torch.bfloat16), cuda(w2, torch.bfloat16))
+    gs = cuda(g, torch.bfloat16)
+    x0 = torch.zeros(0, dm, dtype=torch.bfloat16, device="cuda")
+    assert layer.forward_expert_parallel(x0, gs).shape == (0, dm)
+    gr = layer.backward(torch.zeros(0, dm, dtype=torch.bfloat16, device="cuda"))
+    assert gr["x"].shape == (0, dm) and float(gr["w1"].abs().sum()) == 0.0
+    r = layer.comm_report()
+    assert r.mean_replicas == 0.0 and r.per_device_token_counts == [0, 0]
+    layer.set_training(False)
+    xh = x0.cpu().pin_memory()
+    layer.forward_host(xh, gs, torch.empty_like(xh).pin_memory())
+    layer.set_micro_batches(2)
+    assert layer.forward_expert_parallel(x0, gs).shape == (0, dm)
+    one = cuda(x[:1], torch.bfloat16)
+    full = occ.ExpertParallelLayer(occ.MoEConfig(ne, ne, nd, dm, dh, activation="silu"))  # k = E: every expert
+    full.load_experts(cuda(w1, torch.bfloat16), cuda(w2, torch.bfloat16))
+    ids = cuda(np.arange(ne, dtype=np.int32)[None, :])
+    w = cuda(np.full((1, ne), 1.0 / ne, np.float32))
+    got = full.forward_given_routing(one, ids, w).double().cpu().numpy()
+    want, _ = ref().forward_given_routing(x[:1], np.arange(ne, dtype=np.int32)[None, :], np.full((1, ne), 1.0 / ne),
+                                          w1, w2, _placement(ne, nd, "trivial"), np.zeros(1, np.int32), act="silu",
+                                          single=False)
+    assert rel_err(got, want) <= TOL
