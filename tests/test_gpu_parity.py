@@ -1023,3 +1023,25 @@ def test_degenerate_batches():
                                           w1, w2, _placement(ne, nd, "trivial"), np.zeros(1, np.int32), act="silu",
                                           single=False)
     assert rel_err(got, want) <= TOL
+
+
+@pytest.mark.parametrize("ne,k,dm", [(8, 2, 40), (60, 4, 72), (130, 3, 200), (16, 16, 8), (64, 8, 4104)])
+def test_router_ragged_widths(ne, k, dm):
+    """Production router at token widths that are multiples of 8 but not of
+    the 64-element K block (TMA zero-fills the tail): ids equal the reference
+    top-k of its own softmax rows, which match fp64 softmax to f32 rounding."""
+    n = 333
+    x, g, *_ = make_layer_inputs(ne + dm, n, dm, 8, ne)
+    nd = 1 if ne <= 64 else 5
+    layer = occ.ExpertParallelLayer(occ.MoEConfig(ne, k, nd, dm, 64))
+    xs, gs = cuda(x, torch.bfloat16), cuda(g, torch.bfloat16)
+    ids, w, sc = layer.route(xs, gs, want_scores=True)
+    want_ids, _ = O.Port().topk_route(sc.double().cpu().numpy(), k, True)
+    assert np.array_equal(ids.cpu().numpy(), want_ids)
+    xb = xs.double().cpu().numpy()
+    gb = gs.double().cpu().numpy()
+    lg = xb @ gb.T
+    p = np.exp(lg - lg.max(1, keepdims=True))
+    p /= p.sum(1, keepdims=True)
+    # f32 logits over K = D bf16 products: absolute error grows with D
+    assert np.allclose(sc.double().cpu().numpy(), p, rtol=1e-3, atol=1e-5)
