@@ -983,6 +983,10 @@ occ_status occ_set_placement(occ_handle* h, const int32_t* placement) {
     h->dev_of = dev_of;
     h->slot_of = slot_of;
     h->weights_loaded = h->world == 1 && h->weights_loaded;  // world>1: local experts changed
+    if (h->sib) {  // the micro-batch sibling plans with the same table
+        occ_status s2 = occ_set_placement(h->sib, placement);
+        if (s2 != OCC_OK) return s2;
+    }
     return upload_tables(h);
 }
 

@@ -1045,3 +1045,34 @@ def test_router_ragged_widths(ne, k, dm):
     p /= p.sum(1, keepdims=True)
     # f32 logits over K = D bf16 products: absolute error grows with D
     assert np.allclose(sc.double().cpu().numpy(), p, rtol=1e-3, atol=1e-5)
+
+
+def test_placement_change_at_runtime():
+    """occ_set_placement between forwards (the profiling -> placement loop
+    applied to a live layer): the next forward equals a fresh layer built with
+    the new placement, values and CommReport, with and without reloading the
+    experts (world_size 1 keeps every expert resident)."""
+    ne, k, nd, dm, dh, n = 16, 4, 4, 64, 128, 500
+    x, g, w1, w2, _ = make_layer_inputs(21, n, dm, dh, ne)
+    ids, w = random_routing(n, ne, k, np.random.default_rng(21))
+    new = _placement(ne, nd, "shuffled", seed=9)
+    args = (cuda(x, torch.bfloat16), cuda(ids), cuda(w, torch.float32))
+    fresh = occ.ExpertParallelLayer(occ.MoEConfig(ne, k, nd, dm, dh, activation="silu"),
+                                    occ.Placement([list(p) for p in new]))
+    fresh.load_experts(cuda(w1, torch.bfloat16), cuda(w2, torch.bfloat16))
+    want = fresh.forward_given_routing(*args)
+    want_rep = fresh.comm_report(bytes_per_scalar=2)
+    for reload, mb in ((False, 1), (True, 1), (False, 2), (True, 2)):
+        layer = occ.ExpertParallelLayer(occ.MoEConfig(ne, k, nd, dm, dh, activation="silu"))
+        layer.load_experts(cuda(w1, torch.bfloat16), cuda(w2, torch.bfloat16))
+        if mb > 1:
+            layer.set_micro_batches(mb)
+        layer.forward_given_routing(*args)
+        layer.set_placement(occ.Placement([list(p) for p in new]))
+        if reload:
+            layer.load_experts(cuda(w1, torch.bfloat16), cuda(w2, torch.bfloat16))
+        got = layer.forward_given_routing(*args)
+        rep = layer.comm_report(bytes_per_scalar=2)
+        assert torch.equal(got, want), reload
+        assert (rep.mean_replicas, rep.cross_device_bytes, rep.per_device_token_counts) == \
+            (want_rep.mean_replicas, want_rep.cross_device_bytes, want_rep.per_device_token_counts)
