@@ -663,6 +663,20 @@ __device__ __forceinline__ WTile wide_decode(int tile, int S, int split, const i
                                              int NBW, int NB, int band) {
     WTile w;
     int nbw, half = 0;
+    if (NB & 1) {  // odd block count: every double super-tile first, then the last block of each m-tile
+        const int S2 = gmb[ng] * (NB >> 1);
+        if (tile < S2) {
+            tile_coords(tile, gmb, gw, ng, NB >> 1, band, w.mb, nbw, w.wi);
+            w.nb0 = 2 * nbw;
+            w.two = true;
+        } else {
+            tile_coords(tile - S2, gmb, gw, ng, 1, band, w.mb, nbw, w.wi);
+            w.nb0 = NB - 1;
+            w.two = false;
+        }
+        w.valid = tile < S;
+        return w;
+    }
     int st = tile;
     if (tile >= S - split) {
         const int h = tile - (S - split);
@@ -722,7 +736,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
     const int S = s_gmb[p.ngroups] * NBW;        // super-tiles
     const int tail = S % ncl;
-    const int split = p.tail_split && 2 * tail <= ncl ? tail : 0;  // tail super-tiles issued as halves
+    // tail super-tiles issued as halves (odd block counts end in single-block tiles already)
+    const int split = p.tail_split && !(NB & 1) && 2 * tail <= ncl ? tail : 0;
     const int num_tiles = S + split;
 
     if (warp == 0) {
