@@ -150,6 +150,7 @@ def ref_lib():
         lib.ref_write_placement_text.restype = C.c_longlong
         lib.ref_write_placement_text.argtypes = [_p, _i, _i, C.c_char_p, C.c_longlong]
         lib.ref_component_points.argtypes = [_p, _i, _i, _i, _i, _p, _p]
+        lib.ref_fit_latency.argtypes = [_p, _p, _i, _p, C.c_char_p, C.c_longlong]
         _REF = lib
     return _REF
 
@@ -451,3 +452,12 @@ def synthetic_layer(seed, n, dm, dh, ne, single=True, gated=False):
             w3[e] = er.random_matrix(dm, dh, single)
     g = Rng(gs).random_matrix(ne, dm, single)
     return x, g, w1, w2, w3
+
+
+def ref_fit_latency(xs, ys):
+    """fit_latency (simnet.cpp:36-66) of the reference: (ok, (slope, intercept, r2) or message)."""
+    x, y = _f64(xs), _f64(ys)
+    out = np.zeros(3)
+    buf = C.create_string_buffer(4096)
+    rc = ref_lib().ref_fit_latency(_ptr(x), _ptr(y), len(x), _ptr(out), buf, 4096)
+    return (True, tuple(out)) if rc == 0 else (False, buf.value.decode())

@@ -16,8 +16,9 @@ inputs (tests/test_cli.py, tests/test_gpu_parity.py).  The simulate data path
 is bf16 storage with fp32 accumulation whatever `--precision` says: the
 precision only rounds the synthetic inputs (and therefore routing), as in the
 reference; `--check-oracle` reports the GPU output's max relative error
-against a dense fp64 evaluation of the same routing.  `fit-latency` (a
-least-squares fit over measured latencies) is not part of the B200 build.
+against a dense fp64 evaluation of the same routing.  `fit-latency` (the
+least-squares fit of measured latency on replicas, host arithmetic) completes
+the command set.
 """
 from __future__ import annotations
 
@@ -289,6 +290,52 @@ def cmd_sweep_prune(o, out) -> int:
     return 0
 
 
+# ---------------------------------------------------------- fit-latency --
+def fit_latency(points):
+    """fit_latency (simnet.cpp:36-66): least squares of latency on replicas,
+    the reference's summation order."""
+    distinct = sum(1 for i, p in enumerate(points) if all(q[0] != p[0] for q in points[:i]))
+    if len(points) < 2 or distinct < 2:
+        raise api.UsageError("fit: need at least 2 points with distinct x values")
+    n = float(len(points))
+    mx = my = 0.0
+    for px, py in points:
+        mx += px
+        my += py
+    mx /= n
+    my /= n
+    sxx = sxy = syy = 0.0
+    for px, py in points:
+        sxx += (px - mx) * (px - mx)
+        sxy += (px - mx) * (py - my)
+        syy += (py - my) * (py - my)
+    slope = sxy / sxx
+    return slope, my - slope * mx, 1.0 if syy == 0.0 else (sxy * sxy) / (sxx * syy)
+
+
+def cmd_fit_latency(o, out) -> int:
+    """cli.cpp:393-422: `replicas seconds` per line ('#' comments), one report."""
+    points = []
+    for line_no, line in enumerate(F._lines(_slurp(o.points)), 1):
+        if not line or line[0] == "#":
+            continue
+        parts = F._split_ws(line)
+        if len(parts) != 2:
+            raise api.DataError(f"line {line_no}: expected 'replicas seconds'")
+        points.append((F.parse_double(parts[0], line_no), F.parse_double(parts[1], line_no)))
+    slope, intercept, r2 = fit_latency(points)
+    from .report import ReportWriter
+    w = ReportWriter()
+    w.kv("command", "fit-latency")
+    w.kv("points.count", len(points))
+    w.kv("fit.slope", slope)
+    w.kv("fit.intercept", intercept)
+    w.kv("fit.r_squared", r2)
+    _write(o.out, w.text())
+    out.write(f"fit: slope {format_double(slope)}, intercept {format_double(intercept)}, R^2 {format_double(r2)}\n")
+    return 0
+
+
 # ---------------------------------------------------------------- parser --
 def _parser() -> argparse.ArgumentParser:
     p = argparse.ArgumentParser(prog="moesim", description="Expert-parallel MoE communication simulator (B200)")
@@ -338,6 +385,9 @@ def _parser() -> argparse.ArgumentParser:
     sim_common(s)
     s.add_argument("--prune", default="none")
     s.add_argument("--out", required=True)
+    fl = sub.add_parser("fit-latency", help="Least-squares fit of latency vs replicas")
+    fl.add_argument("--points", required=True)
+    fl.add_argument("--out", required=True)
     w = sub.add_parser("sweep-prune", help="Prune-budget sweep, one report per budget")
     sim_common(w)
     w.add_argument("--mode", required=True)
@@ -364,6 +414,8 @@ def run(argv: List[str], out=None, err=None) -> int:
             return cmd_simulate(o, out)
         if o.cmd == "sweep-prune":
             return cmd_sweep_prune(o, out)
+        if o.cmd == "fit-latency":
+            return cmd_fit_latency(o, out)
     except Exception as e:  # noqa: BLE001 — the reference's catch-all maps to exit 1
         for cls, code, label in EXIT:
             if isinstance(e, cls):

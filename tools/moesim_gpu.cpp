@@ -8,6 +8,7 @@
 //   moesim_gpu reschedule --graph F --devices D --out F
 //   moesim_gpu simulate   --seed S --out F [--trace F] [--placement F] [--prune none|router|similarity] ...
 //   moesim_gpu sweep-prune --seed S --mode router|similarity --out-prefix P ...
+//   moesim_gpu fit-latency --points F --out F
 //
 // Text formats follow io.cpp:55-204 with std::to_chars / std::from_chars, as
 // the reference does, so files round-trip byte for byte.  Trace generation and
@@ -782,12 +783,58 @@ int cmd_sweep_prune(const std::vector<std::string>& a, std::ostream& out) {  // 
     return 0;
 }
 
+int cmd_fit_latency(const std::vector<std::string>& a, std::ostream& out) {  // cli.cpp:393-422, simnet.cpp:36-66
+    const Args o = parse_args(a, {"--points", "--out"}, {});
+    std::istringstream in(slurp(o.need("--points")));
+    const std::string dst = o.need("--out");
+    std::vector<std::pair<double, double>> pts;
+    std::string line;
+    int line_no = 0;
+    while (std::getline(in, line)) {
+        ++line_no;
+        if (line.empty() || line[0] == '#') continue;
+        std::istringstream ss(line);
+        std::string x, y, extra;
+        if (!(ss >> x >> y) || (ss >> extra)) bad(line_no, "expected 'replicas seconds'");
+        pts.emplace_back(parse_double(x, line_no), parse_double(y, line_no));
+    }
+    int distinct = 0;
+    for (size_t i = 0; i < pts.size(); ++i) {
+        bool seen = false;
+        for (size_t j = 0; j < i; ++j) seen = seen || pts[j].first == pts[i].first;
+        distinct += !seen;
+    }
+    if (pts.size() < 2 || distinct < 2) throw UsageError("fit: need at least 2 points with distinct x values");
+    const double n = static_cast<double>(pts.size());
+    double mx = 0.0, my = 0.0;
+    for (const auto& p : pts) mx += p.first, my += p.second;
+    mx /= n;
+    my /= n;
+    double sxx = 0.0, sxy = 0.0, syy = 0.0;
+    for (const auto& p : pts) {
+        sxx += (p.first - mx) * (p.first - mx);
+        sxy += (p.first - mx) * (p.second - my);
+        syy += (p.second - my) * (p.second - my);
+    }
+    const double slope = sxy / sxx, intercept = my - slope * mx;
+    const double r2 = syy == 0.0 ? 1.0 : (sxy * sxy) / (sxx * syy);
+    Report r;
+    r.kv("command", std::string("fit-latency"));
+    r.kv("points.count", (long long)pts.size());
+    r.kv("fit.slope", slope);
+    r.kv("fit.intercept", intercept);
+    r.kv("fit.r_squared", r2);
+    write_file(dst, r.os.str());
+    out << "fit: slope " << fmt(slope) << ", intercept " << fmt(intercept) << ", R^2 " << fmt(r2) << "\n";
+    return 0;
+}
+
 }  // namespace
 
 int main(int argc, char** argv) {
     std::vector<std::string> a(argv + 1, argv + argc);
     if (a.empty()) {
-        std::cerr << "usage: moesim_gpu gen-trace|profile|reschedule|simulate|sweep-prune [options]\n";
+        std::cerr << "usage: moesim_gpu gen-trace|profile|reschedule|simulate|sweep-prune|fit-latency [options]\n";
         return 2;
     }
     const std::string cmd = a[0];
@@ -798,6 +845,7 @@ int main(int argc, char** argv) {
         if (cmd == "reschedule") return cmd_reschedule(a);
         if (cmd == "simulate") return cmd_simulate(a, std::cout);
         if (cmd == "sweep-prune") return cmd_sweep_prune(a, std::cout);
+        if (cmd == "fit-latency") return cmd_fit_latency(a, std::cout);
         std::cerr << "usage error: unknown command '" << cmd << "'\n";
         return 2;
     } catch (const UsageError& e) {
