@@ -140,6 +140,20 @@ def _need_cuda(*ts):
             raise DeviceError("B200 path: tensors must live on the GPU (no CPU fallback)")
 
 
+def _arg(t: Optional[torch.Tensor], name: str, dtype: torch.dtype, shape: tuple):
+    """Validate a tensor handed to the C-ABI (which takes raw pointers): the
+    dtype and shape must match exactly (a wrong dtype would be reinterpreted,
+    not converted), and the result is contiguous.  The caller keeps the
+    returned tensor alive until the call returns.  None passes through."""
+    if t is None:
+        return None
+    if t.dtype != dtype:
+        raise ShapeError(f"{name}: expected {dtype}, got {t.dtype}")
+    if tuple(t.shape) != tuple(shape):
+        raise ShapeError(f"{name}: expected shape {tuple(shape)}, got {tuple(t.shape)}")
+    return t.contiguous()
+
+
 def launch_count() -> int:
     return int(lib().occ_launch_count())
 
@@ -312,9 +326,12 @@ class ExpertParallelLayer:
         """The production router's f32 logits x g^T [n, E] (tcgen05), e.g. to
         profile the similarity table of the similarity pruning mode."""
         _need_cuda(x, gate)
-        out = torch.empty((x.shape[0], self.config.num_experts), dtype=torch.float32, device=x.device)
-        _check(lib().occ_router_logits(self._h, _ptr(x.contiguous()), _ptr(gate.contiguous()), x.shape[0],
-                                       _ptr(out), _stream()), "router_logits")
+        c = self.config
+        x = _arg(x, "router_logits: x", torch.bfloat16, (x.shape[0], c.embed_dim))
+        gate = _arg(gate, "router_logits: gate", torch.bfloat16, (c.num_experts, c.embed_dim))
+        out = torch.empty((x.shape[0], c.num_experts), dtype=torch.float32, device=x.device)
+        _check(lib().occ_router_logits(self._h, _ptr(x), _ptr(gate), x.shape[0], _ptr(out), _stream()),
+               "router_logits")
         return out
 
     def comm_enable_peer(self, max_tokens_per_rank: int):
@@ -380,11 +397,13 @@ class ExpertParallelLayer:
         _need_cuda(x, gate)
         n = x.shape[0]
         k = self.config.top_k
+        x = _arg(x, "route: x", torch.bfloat16, (n, self.config.embed_dim))
+        gate = _arg(gate, "route: gate", torch.bfloat16, (self.config.num_experts, self.config.embed_dim))
         ids = torch.empty((n, k), dtype=torch.int32, device=x.device)
         w = torch.empty((n, k), dtype=torch.float32, device=x.device)
         sc = torch.empty((n, self.config.num_experts), dtype=torch.float32, device=x.device) if want_scores else None
         pr = self._prune(prune)
-        _check(lib().occ_route(self._h, _ptr(x.contiguous()), _ptr(gate.contiguous()), n,
+        _check(lib().occ_route(self._h, _ptr(x), _ptr(gate), n,
                                C.byref(pr) if pr else None, _ptr(ids), _ptr(w), _ptr(sc), _stream()), "route")
         return (ids, w, sc) if want_scores else (ids, w)
 
@@ -412,9 +431,11 @@ class ExpertParallelLayer:
         _need_cuda(ids, sources)
         n = ids.shape[0]
         nd = self.config.num_devices
+        ids = _arg(ids, "build_dispatch_index: ids", torch.int32, (n, self.config.top_k))
+        sources = _arg(sources, "build_dispatch_index: sources", torch.int32, (n,))
         brim0 = torch.empty(n * nd, dtype=torch.int32, device=ids.device)
         counts = torch.empty((nd, nd), dtype=torch.int32, device=ids.device)
-        _check(lib().occ_build_dispatch(self._h, _ptr(ids.contiguous()), _ptr(sources), n, _ptr(brim0),
+        _check(lib().occ_build_dispatch(self._h, _ptr(ids), _ptr(sources), n, _ptr(brim0),
                                         _ptr(counts), _stream()), "build_dispatch")
         return brim0, counts
 
@@ -431,17 +452,31 @@ class ExpertParallelLayer:
             raise ShapeError("forward: token width != expert input width")
         if sources is not None and sources.shape[0] != n:
             raise ShapeError("forward: one source device per token required")
+        c = self.config
+        x = x.contiguous()
+        ids = _arg(ids, "forward: ids", torch.int32, (n, c.top_k))
+        w = w.float().contiguous() if w.dtype != torch.float32 else w.contiguous()
+        if tuple(w.shape) != (n, c.top_k):
+            raise ShapeError(f"forward: routing weights must be [{n}, {c.top_k}]")
+        sources = _arg(sources, "forward: sources", torch.int32, (n,))
         if out is None:
             out = torch.empty_like(x)
-        _check(lib().occ_forward(self._h, _ptr(x), _ptr(ids), _ptr(w.float().contiguous()) if w.dtype != torch.float32 else _ptr(w),
-                                 _ptr(sources), n, _ptr(out), _stream()), "forward")
+        out = _arg(out, "forward: out", torch.bfloat16, tuple(x.shape))
+        _check(lib().occ_forward(self._h, _ptr(x), _ptr(ids), _ptr(w), _ptr(sources), n, _ptr(out), _stream()),
+               "forward")
         return out
 
     def forward_expert_parallel(self, x, gate, prune: Optional[PruneSpec] = None, sources=None, out=None):
         """pipeline.cpp:503-517: route (+prune) then the indexed data path."""
         _need_cuda(x, gate, sources)
+        c = self.config
+        n = x.shape[0]
+        x = _arg(x, "forward_expert_parallel: x", torch.bfloat16, (n, c.embed_dim))
+        gate = _arg(gate, "forward_expert_parallel: gate", torch.bfloat16, (c.num_experts, c.embed_dim))
+        sources = _arg(sources, "forward_expert_parallel: sources", torch.int32, (n,))
         if out is None:
             out = torch.empty_like(x)
+        out = _arg(out, "forward_expert_parallel: out", torch.bfloat16, (n, c.embed_dim))
         pr = self._prune(prune)
         _check(lib().occ_forward_expert_parallel(self._h, _ptr(x), _ptr(gate), C.byref(pr) if pr else None,
                                                  _ptr(sources), x.shape[0], _ptr(out), _stream()), "forward_ep")
@@ -455,6 +490,15 @@ class ExpertParallelLayer:
         if x_host.is_cuda or out_host.is_cuda:
             raise ShapeError("forward_host: x and out are host tensors")
         _need_cuda(gate)
+        c = self.config
+        n = x_host.shape[0]
+        for t, nm in ((x_host, "x_host"), (out_host, "out_host")):
+            # asynchronous: the library keeps reading / writing these pointers
+            # after the call returns, so no temporary copies
+            if t.dtype != torch.bfloat16 or tuple(t.shape) != (n, c.embed_dim) or not t.is_contiguous():
+                raise ShapeError(f"forward_host: {nm} must be a contiguous bf16 [{n}, {c.embed_dim}] host tensor")
+        gate = _arg(gate, "forward_host: gate", torch.bfloat16, (c.num_experts, c.embed_dim))
+        self._host_gate = gate  # the captured graph reads it on later replays
         pr = self._prune(prune)
         _check(lib().occ_forward_host(self._h, _ptr(x_host), _ptr(gate), C.byref(pr) if pr else None,
                                       x_host.shape[0], _ptr(out_host), chunks, _stream()), "forward_host")
@@ -587,7 +631,10 @@ def accumulate_collab(counts: torch.Tensor, ids: torch.Tensor) -> torch.Tensor:
     _need_cuda(counts, ids)
     e = counts.shape[0]
     n, k = ids.shape
-    _check(lib().occ_coactivation_histogram(_ptr(ids.contiguous()), n, k, e, _ptr(counts), _stream()), "collab")
+    ids = _arg(ids, "accumulate_collab: ids", torch.int32, (n, k))
+    if counts.dtype != torch.int64 or tuple(counts.shape) != (e, e) or not counts.is_contiguous():
+        raise ShapeError("accumulate_collab: counts must be a contiguous int64 [E, E] tensor (accumulated in place)")
+    _check(lib().occ_coactivation_histogram(_ptr(ids), n, k, e, _ptr(counts), _stream()), "collab")
     return counts
 
 

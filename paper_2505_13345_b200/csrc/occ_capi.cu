@@ -190,6 +190,7 @@ struct occ_handle {
     // training: saved pre-activations + backward workspace
     int training = 0;
     bool have_train_state = false;
+    bool bwd_weights_ready = false;  // w13o / w2o + their tensor maps built (training on at occ_load_experts)
     DevBuf<__nv_bfloat16> save_a, save_b, w13o, w2o, g_epd, gpre;
     DevBuf<float> gw_part, gw_row;
     TmapBox tmG_k, tmW2o, tmP_k, tmW1o, tmH_mn, tmG_mn, tmX_mn, tmP_mn;
@@ -983,6 +984,7 @@ occ_status occ_set_placement(occ_handle* h, const int32_t* placement) {
     h->dev_of = dev_of;
     h->slot_of = slot_of;
     h->weights_loaded = h->world == 1 && h->weights_loaded;  // world>1: local experts changed
+    h->have_train_state = false;  // the saved Epd grouping belongs to the old table
     if (h->sib) {  // the micro-batch sibling plans with the same table
         occ_status s2 = occ_set_placement(h->sib, placement);
         if (s2 != OCC_OK) return s2;
@@ -997,6 +999,8 @@ occ_status occ_load_experts(occ_handle* h, const void* w1, const void* w3, const
     const int El = h->world == 1 ? h->E : h->P;
     const int D = h->D, F = h->F;
     h->n1rows = h->gated ? 2 * F : F;
+    h->have_train_state = false;
+    h->bwd_weights_ready = false;
     // resident K-major rows (row pitch = K; padding the pitch to spread L2 sets
     // was measured: no change in DRAM traffic or time, profiles/r01_l2_traffic.md)
     const int p1 = D, p2 = F;
@@ -1028,6 +1032,7 @@ occ_status occ_load_experts(occ_handle* h, const void* w1, const void* w3, const
         if (!make_tmap_2d(h->tmW2o.bytes, h->w2o.p, D, (uint64_t)El * F, 64, 128) ||
             !make_tmap_2d(h->tmW1o.bytes, h->w13o.p, kw, (uint64_t)El * D, 64, 128))
             return fail(OCC_ERR_CUDA, "cuTensorMapEncodeTiled failed (backward weights)");
+        h->bwd_weights_ready = true;
     }
     if (!make_tmap_2d(h->tmB1.bytes, h->w13t.p, D, (uint64_t)El * h->n1rows, 64, 128, 128, p1) ||
         !make_tmap_2d(h->tmB2.bytes, h->w2t.p, F, (uint64_t)El * D, 64, 128, 128, p2))
@@ -1040,6 +1045,11 @@ occ_status occ_load_shared_experts(occ_handle* h, int num_shared, int d_ff_share
                                    const void* w2, const void* gate, occ_stream_t stream) {
     if (!h) return fail(OCC_ERR_ARG, "null handle");
     if (num_shared < 0) return fail(OCC_ERR_CONFIG, "shared experts: num_shared must be >= 0");
+    // captured graphs (occ_forward_host) bake run_shared in or out and hold the
+    // old buffers / tensor maps: any change re-captures; the micro-batch
+    // sibling re-sizes its own h / ys buffers for the new width
+    ++g_buf_gen;
+    if (h->sib) h->sib->sh_cap = 0;
     if (num_shared == 0) {
         h->n_shared = 0;
         return OCC_OK;
@@ -1268,6 +1278,7 @@ occ_status occ_build_dispatch(occ_handle* h, const int32_t* ids, const int32_t* 
     if (s != OCC_OK) return s;
     CUDA_TRY(cudaMemsetAsync(h->stats.p, 0, sizeof(long long) * 8, st));
     CUDA_TRY(cudaMemsetAsync(h->err.p, 0, sizeof(int32_t), st));
+    h->have_train_state = false;  // the plan buffers no longer hold the saved forward
     s = run_plan(h, ids, nullptr, sources, n, st);
     if (s != OCC_OK) return s;
     if (brim0) launch_extract_brim0(n, h->nd, sources, -1, h->mask.p, h->lam.p, h->tok_sfd.p, h->d_tok_base, brim0, st);
@@ -1486,6 +1497,8 @@ occ_status occ_backward(occ_handle* h, const void* upstream, float* g_x, float* 
                         float* g_weights, occ_stream_t stream) {
     if (!h) return fail(OCC_ERR_ARG, "null handle");
     if (!h->have_train_state) return fail(OCC_ERR_STATE, "backward: forward state was not saved (occ_set_training)");
+    if (!h->bwd_weights_ready)
+        return fail(OCC_ERR_STATE, "backward: occ_set_training(h, 1) must precede occ_load_experts");
     if (h->n_shared) return fail(OCC_ERR_UNSUPPORTED, "backward: shared experts are forward-only in this build");
     const int n = h->last_n, k = h->k, P = h->P, D = h->D, F = h->F, nd = h->nd, E = h->E;
     if (n > 0 && (!upstream || !g_x || !g_w1 || !g_w2 || !g_weights || (h->gated && !g_w3)))
@@ -1639,7 +1652,11 @@ occ_status occ_forward_host(occ_handle* h, const void* x_host, const void* gate,
     }
     const int slot = h->host_calls++ & 1;
     cudaEvent_t* ev = h->pev.data() + slot * per_slot;
-    const size_t base_el = slot * slot_elems;
+    // slot stride = half the allocated staging capacity (fixed between
+    // regrows), not this call's n * D: with a shrinking batch the two slots
+    // must still never overlap the region the other slot's in-flight copies
+    // and layer use
+    const size_t base_el = slot * (h->x_stage.n / 2);
     if (h->host_slot_used[slot]) {
         CUDA_TRY(cudaStreamWaitEvent(h->s_in, ev[0], 0));  // previous layer on this slot read x
         CUDA_TRY(cudaStreamWaitEvent(st, ev[1], 0));       // previous D2H on this slot read out

@@ -569,6 +569,34 @@ def test_forward_host_graph_replay():
         assert torch.equal(oh, want), n
 
 
+def test_forward_host_async_shrinking_batches():
+    """wait=False with a batch size that shrinks and grows between calls (eager
+    chunked path and graph replay): the two staging slots keep a fixed stride,
+    so an in-flight call's inputs and outputs are never overwritten by the next
+    call's copies (slot 1 used to start at n * D of the CURRENT
+    call)."""
+    ne, k, nd, dm, dh = 8, 2, 2, 256, 512
+    x, g, w1, w2, _ = make_layer_inputs(9, 1200, dm, dh, ne)
+    layer = occ.ExpertParallelLayer(occ.MoEConfig(ne, k, nd, dm, dh, activation="silu"))
+    layer.load_experts(cuda(w1, torch.bfloat16), cuda(w2, torch.bfloat16))
+    gs = cuda(g, torch.bfloat16)
+    for validate, chunks in ((True, 3), (False, 1), (False, 2)):
+        layer.set_validate(validate)
+        sizes = (1200, 900, 400, 1100, 250, 1200, 800)
+        wants, hosts = [], []
+        for i, n in enumerate(sizes):
+            xs = cuda(x[:n], torch.bfloat16) * (1 + i % 5)
+            wants.append(layer.forward_expert_parallel(xs, gs).cpu())
+            hosts.append((xs.cpu().pin_memory(), torch.full((n, dm), float("nan"), dtype=torch.bfloat16).pin_memory()))
+        torch.cuda.synchronize()
+        for xh, oh in hosts:  # all enqueued back to back, no wait in between
+            layer.forward_host(xh, gs, oh, chunks=chunks, wait=False)
+        layer.host_wait()
+        torch.cuda.synchronize()
+        for i, ((xh, oh), want) in enumerate(zip(hosts, wants)):
+            assert torch.equal(oh, want), (validate, chunks, i, sizes[i])
+
+
 # ------------------------------------------- world_size > 1 (loopback) -----
 
 @pytest.mark.parametrize("nd,ne,k,act,dedup,shared,peer", [(2, 8, 2, "silu", True, 0, False),
@@ -732,6 +760,22 @@ def test_backward_zero_upstream_and_state_error():
     gr = layer.backward(torch.zeros(n, dm, device="cuda"))
     for name in ("x", "w1", "w2", "routing_weights"):
         assert not gr[name].any(), name
+    # state invalidation: a new placement, new weights or a bare
+    # dispatch plan drop the saved forward; training switched on after the
+    # weights were loaded has no backward weight copies -> StateError, not a
+    # device fault
+    layer.build_dispatch_index(cuda(ids))
+    with pytest.raises(occ.StateError):
+        layer.backward(torch.zeros(n, dm, device="cuda"))
+    late = occ.ExpertParallelLayer(occ.MoEConfig(ne, k, nd, dm, dh, activation="silu"))
+    late.load_experts(cuda(w1, torch.bfloat16), cuda(w2, torch.bfloat16))
+    late.set_training(True)
+    late.forward_given_routing(cuda(x, torch.bfloat16), cuda(ids), cuda(w, torch.float32))
+    with pytest.raises(occ.StateError):
+        late.backward(torch.zeros(n, dm, device="cuda"))
+    late.load_experts(cuda(w1, torch.bfloat16), cuda(w2, torch.bfloat16))  # reload: copies built now
+    late.forward_given_routing(cuda(x, torch.bfloat16), cuda(ids), cuda(w, torch.float32))
+    assert not late.backward(torch.zeros(n, dm, device="cuda"))["x"].any()
 
 
 def test_collaboration_aware_placement_on_gpu():
@@ -1118,3 +1162,28 @@ def test_repeated_forwards_stable():
     layer.set_micro_batches(2)
     for i in range(50):
         assert torch.equal(layer.forward_expert_parallel(xs, gs), want), i
+
+
+def test_api_rejects_wrong_dtypes_and_shapes():
+    """The C-ABI takes raw pointers: a float32 x / gate or int64 ids would be
+    reinterpreted, so the Python mirror refuses them."""
+    ne, k, nd, dm, dh, n = 8, 2, 2, 64, 128, 32
+    x, g, w1, w2, _ = make_layer_inputs(4, n, dm, dh, ne)
+    layer = occ.ExpertParallelLayer(occ.MoEConfig(ne, k, nd, dm, dh, activation="silu"))
+    layer.load_experts(cuda(w1, torch.bfloat16), cuda(w2, torch.bfloat16))
+    xb, gb = cuda(x, torch.bfloat16), cuda(g, torch.bfloat16)
+    with pytest.raises(occ.ShapeError):
+        layer.forward_expert_parallel(xb.float(), gb)
+    with pytest.raises(occ.ShapeError):
+        layer.forward_expert_parallel(xb, gb.float())
+    with pytest.raises(occ.ShapeError):
+        layer.route(xb, gb[:, :dm // 2])
+    ids, w = layer.route(xb, gb)
+    with pytest.raises(occ.ShapeError):
+        layer.forward_given_routing(xb, ids.long(), w)
+    with pytest.raises(occ.ShapeError):
+        layer.forward_given_routing(xb, ids, w, sources=torch.zeros(n, dtype=torch.int64, device="cuda"))
+    # non-contiguous but correctly typed inputs are accepted (copied, kept alive)
+    xt = torch.empty((dm, n), dtype=torch.bfloat16, device="cuda").t()
+    xt.copy_(xb)
+    assert torch.equal(layer.forward_expert_parallel(xt, gb), layer.forward_expert_parallel(xb, gb))
