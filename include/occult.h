@@ -193,6 +193,25 @@ occ_status occ_topk_route_f64(const double* scores, int n, int e, int k, int ren
  * Per-token CapacityError is reported through the return status. */
 occ_status occ_prune_routing_f64(occ_handle* h, const double* scores, const int32_t* ids_in, const double* w_in,
                                  int n, const occ_prune* prune, int32_t* ids, double* weights, occ_stream_t stream);
+/* Router arithmetic of occ_route / occ_forward_expert_parallel / occ_forward_host:
+ *   OCC_ROUTER_TC (default): x g^T on tcgen05 tensor cores (bf16 operands, f32
+ *     accumulation) with softmax / top-k / router-score pruning fused in the
+ *     epilogue: the fast path, equal to the reference except where two
+ *     reference scores are within f32 rounding of each other (declared
+ *     tolerance: < 1% of tokens, only at near-ties);
+ *   OCC_ROUTER_EXACT: the reference's arithmetic (occ_route_exact), bit-exact
+ *     ids and weights; the layer then uses the weights rounded to f32. */
+typedef enum { OCC_ROUTER_TC = 0, OCC_ROUTER_EXACT = 1 } occ_router_mode;
+occ_status occ_set_router_mode(occ_handle* h, int mode);
+/* gate_scores -> topk_route -> prune_routing exactly as forward_expert_parallel
+ * (pipeline.cpp:509-512; routing.cpp:33-84; pruning.cpp:141-163) on the bf16
+ * tokens x [n, D] and gate [E, D] widened to double: logits summed in
+ * ascending k without FMA, softmax with glibc's exp (bit for bit), fp64
+ * top-k / renormalisation / pruning.  ids [n, k] int32, weights [n, k] f64,
+ * scores (nullable) [n, E] f64 softmax rows; all bit-exact with the
+ * reference.  prune may be NULL. */
+occ_status occ_route_exact(occ_handle* h, const void* x, const void* gate, int n, const occ_prune* prune, int32_t* ids,
+                           double* weights, double* scores, occ_stream_t stream);
 /* Production router (forward_expert_parallel's routing stage,
  * pipeline.cpp:509-512): logits = x g^T (bf16 in, f32 accumulate),
  * softmax, top-k, renormalise, optional pruning (prune may be NULL).
@@ -201,13 +220,51 @@ occ_status occ_route(occ_handle* h, const void* x, const void* gate, int n, cons
                      float* weights, float* scores, occ_stream_t stream);
 
 /* ------------------------------------------------------------- EP path */
-/* build_dispatch_index (pipeline.cpp:24-50) for every source at once.
- * sources: [n] device of each token (NULL = round_robin_sources,
- * pipeline.cpp:12-16).  brim0 (nullable): concatenation over sources s of
- * the N_d x n_s BRIM0 matrices; counts (nullable): [N_d * N_d] Sfd rows
- * per (source, destination). */
+/* build_dispatch_index (pipeline.cpp:24-50).
+ * world_size == 1: every source at once; sources: [n] device of each token
+ * (NULL = round_robin_sources, pipeline.cpp:12-16); brim0 (nullable):
+ * concatenation over sources s of the N_d x n_s BRIM0 matrices; counts
+ * (nullable): [N_d * N_d] Sfd rows per (source, destination).
+ * world_size > 1: the n tokens are this rank's (source = rank, sources
+ * ignored); brim0 [N_d x n], counts [N_d] (this source's row). */
 occ_status occ_build_dispatch(occ_handle* h, const int32_t* ids, const int32_t* sources, int n, int32_t* brim0,
                               int32_t* counts, occ_stream_t stream);
+
+/* ------------------------------------------- stage-level entry points ---
+ * The reference's data path one stage at a time (pipeline.hpp:89-123), for a
+ * caller that runs its own exchange between the stages (e.g. its NCCL
+ * all-to-all with the layout of occ_exchange_layout).  Stream-ordered, no
+ * host synchronisation unless validation is on; chaining
+ *   occ_build_dispatch -> occ_dispatch -> (exchange) -> occ_expert_compute
+ *   -> (return exchange) -> occ_combine
+ * gives occ_forward's output bit for bit.  `device` is the EP device whose
+ * experts run: [0, N_d) on a world_size 1 handle, this rank otherwise. */
+/* dispatch (pipeline.cpp:91-123) of one source's n tokens by its BRIM0
+ * [N_d x n]: Sfd row c = BRIM0[d, i] >= 0 receives x row i [D] bf16, the
+ * routing row (ids [k] int32, weights [k] f32) and sfd_token[c] = i.  Rows for
+ * destination d are contiguous (device-major counters). */
+occ_status occ_dispatch(occ_handle* h, const void* x, const int32_t* ids, const float* weights, int n,
+                        const int32_t* brim0, void* sfd_x, int32_t* sfd_ids, float* sfd_weights, int32_t* sfd_token,
+                        occ_stream_t stream);
+/* build_compute_index (pipeline.cpp:52-89) over the `rows` inbox rows of EP
+ * device `device` (their routing rows in_ids [rows, k], in_weights [rows, k]):
+ * cindex [P x rows] int32 (nullable), n_epd (nullable, DEVICE int32).  A row
+ * with no local expert or an invalid id: RoutingError (validation on). */
+occ_status occ_build_compute(occ_handle* h, int device, const int32_t* in_ids, const float* in_weights, int rows,
+                             int32_t* cindex, int32_t* n_epd, occ_stream_t stream);
+/* scatter_matmul -> apply_activation -> weight_modulate -> merge_matmul
+ * (pipeline.cpp:178-283) of EP device `device` over its inbox rows
+ * (in_x [rows, D] bf16 + routing rows): y_out [rows, D] bf16, row r = the
+ * intra-device partial combine sum over the row's local experts in
+ * placement-list order (fp32 accumulation, one bf16 rounding: the return
+ * payload).  Grouped GEMMs on tcgen05 as in occ_forward. */
+occ_status occ_expert_compute(occ_handle* h, int device, const void* in_x, const int32_t* in_ids,
+                              const float* in_weights, int rows, void* y_out, occ_stream_t stream);
+/* combine (pipeline.cpp:285-300) of one source: out[i] = bf16( sum over
+ * devices d ascending of y_returned[BRIM0[d, i]] ), fp32 accumulation;
+ * y_returned [n_sfd, D] bf16 in Sfd order, brim0 [N_d x n]. */
+occ_status occ_combine(occ_handle* h, const void* y_returned, const int32_t* brim0, int n, void* out,
+                       occ_stream_t stream);
 /* forward_given_routing (pipeline.cpp:360-501): dispatch -> exchange ->
  * grouped expert FFN -> intra-device partial combine -> return exchange ->
  * combine.  world_size == 1: x/out hold all n tokens, sources as above.

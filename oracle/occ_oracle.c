@@ -782,6 +782,124 @@ void orc_shared_experts(const double* x, int n, int dm, const double* w1, const 
     free(acc);
 }
 
+/* dense_given_routing (pipeline.cpp:542-562) + the shared-expert restatement
+ * (orc_shared_experts above) for a SAMPLE of rows, with every operand given
+ * in the product's bf16 storage (uint16 bit patterns, widened exactly to
+ * double) so the BASELINE-size layers (Mixtral: 8 x 3 x 4096 x 14336 weights)
+ * fit in host memory.  Arithmetic is that of orc_dense_given_routing /
+ * orc_shared_experts in Precision::Double: per row, experts in routing order,
+ * h[q] = act(sum_c x w1) (or silu(sum_c x w1) * sum_c x w3), o[c] = sum_q h w2,
+ * acc[c] += w * o[c]; then + g * sum_s FFN_s.  The loops are blocked over the
+ * sampled rows so each weight row is read once per expert for all of them;
+ * every per-element sum keeps the ascending order of the scalar version.
+ * Rows are independent given routing (pipeline.cpp:548-560), so a sample is a
+ * valid full-size check.  rows[nrows] index into x [n, dm]; ids/w [n, k];
+ * w1/w3 [E, dm, dh], w2 [E, dh, dm]; shared (ns > 0): w1s/w3s [ns, dm, dhs],
+ * w2s [ns, dhs, dm], gate_s [dm] or NULL.  out [nrows, dm]. */
+static inline double bf(uint16_t v) {
+    union { uint32_t u; float f; } c;
+    c.u = (uint32_t)v << 16;
+    return (double)c.f;
+}
+static void ffn_rows_bf16(const double* xr, int nr, int dm, const uint16_t* W1, const uint16_t* W3, const uint16_t* W2,
+                          int dh, int act, const double* scale, double* acc) {
+    /* xr [nr, dm] doubles; acc[r, c] += scale[r] * (h_r W2)[c] */
+    double* a = (double*)calloc((size_t)nr * dh, sizeof(double));
+    double* b = W3 ? (double*)calloc((size_t)nr * dh, sizeof(double)) : NULL;
+    double* wrow = (double*)malloc(sizeof(double) * (size_t)dh);
+    for (int c = 0; c < dm; ++c) { /* ascending c for every (r, q) */
+        for (int q = 0; q < dh; ++q) wrow[q] = bf(W1[(long)c * dh + q]);
+        for (int r = 0; r < nr; ++r) {
+            const double xv = xr[(long)r * dm + c];
+            double* ar = a + (long)r * dh;
+            for (int q = 0; q < dh; ++q) ar[q] += xv * wrow[q];
+        }
+        if (W3) {
+            for (int q = 0; q < dh; ++q) wrow[q] = bf(W3[(long)c * dh + q]);
+            for (int r = 0; r < nr; ++r) {
+                const double xv = xr[(long)r * dm + c];
+                double* br = b + (long)r * dh;
+                for (int q = 0; q < dh; ++q) br[q] += xv * wrow[q];
+            }
+        }
+    }
+    for (long i = 0; i < (long)nr * dh; ++i) a[i] = W3 ? act_fn(a[i], 1) * b[i] : act_fn(a[i], act);
+    double* o = (double*)calloc((size_t)nr * dm, sizeof(double));
+    double* w2row = (double*)malloc(sizeof(double) * (size_t)dm);
+    for (int q = 0; q < dh; ++q) { /* ascending q for every (r, c) */
+        for (int c = 0; c < dm; ++c) w2row[c] = bf(W2[(long)q * dm + c]);
+        for (int r = 0; r < nr; ++r) {
+            const double hv = a[(long)r * dh + q];
+            double* orow = o + (long)r * dm;
+            for (int c = 0; c < dm; ++c) orow[c] += hv * w2row[c];
+        }
+    }
+    for (int r = 0; r < nr; ++r)
+        for (int c = 0; c < dm; ++c) acc[(long)r * dm + c] += scale[r] * o[(long)r * dm + c];
+    free(a);
+    free(b);
+    free(wrow);
+    free(o);
+    free(w2row);
+}
+
+void orc_dense_rows_bf16(const uint16_t* x, int n, int dm, const int* ids, const float* w, int k, int ne,
+                         const uint16_t* w1, const uint16_t* w2, const uint16_t* w3, int dh, int act,
+                         int ns, const uint16_t* w1s, const uint16_t* w2s, const uint16_t* w3s, int dhs,
+                         const uint16_t* gate_s, const int* rows, int nrows, double* out) {
+    (void)n;
+    double* xr = (double*)malloc(sizeof(double) * (size_t)nrows * dm);
+    double* sub = (double*)malloc(sizeof(double) * (size_t)nrows * dm);
+    double* acc = (double*)calloc((size_t)nrows * dm, sizeof(double));
+    double* sc = (double*)malloc(sizeof(double) * (size_t)nrows);
+    int* pick = (int*)malloc(sizeof(int) * (size_t)nrows);
+    for (int r = 0; r < nrows; ++r)
+        for (int c = 0; c < dm; ++c) xr[(long)r * dm + c] = bf(x[(long)rows[r] * dm + c]);
+    /* routed experts: slot j of every row in routing order (acc[c] += w o[c]
+     * in slot order per row, like the scalar version); rows sharing an expert
+     * in slot j are batched */
+    for (int j = 0; j < k; ++j)
+        for (int e = 0; e < ne; ++e) {
+            int m = 0;
+            for (int r = 0; r < nrows; ++r)
+                if (ids[(long)rows[r] * k + j] == e) pick[m++] = r;
+            if (!m) continue;
+            for (int i = 0; i < m; ++i) {
+                memcpy(sub + (long)i * dm, xr + (long)pick[i] * dm, sizeof(double) * dm);
+                sc[i] = (double)w[(long)rows[pick[i]] * k + j];
+            }
+            double* tmp = (double*)calloc((size_t)m * dm, sizeof(double));
+            ffn_rows_bf16(sub, m, dm, w1 + (long)e * dm * dh, w3 ? w3 + (long)e * dm * dh : NULL,
+                          w2 + (long)e * dh * dm, dh, act, sc, tmp);
+            for (int i = 0; i < m; ++i)
+                for (int c = 0; c < dm; ++c) acc[(long)pick[i] * dm + c] += tmp[(long)i * dm + c];
+            free(tmp);
+        }
+    if (ns > 0) {
+        double* sh = (double*)calloc((size_t)nrows * dm, sizeof(double));
+        for (int r = 0; r < nrows; ++r) sc[r] = 1.0;
+        for (int s2 = 0; s2 < ns; ++s2)
+            ffn_rows_bf16(xr, nrows, dm, w1s + (long)s2 * dm * dhs, w3s ? w3s + (long)s2 * dm * dhs : NULL,
+                          w2s + (long)s2 * dhs * dm, dhs, act, sc, sh);
+        for (int r = 0; r < nrows; ++r) {
+            double g = 1.0;
+            if (gate_s) {
+                double z = 0.0;
+                for (int c = 0; c < dm; ++c) z += xr[(long)r * dm + c] * bf(gate_s[c]);
+                g = 1.0 / (1.0 + exp(-z));
+            }
+            for (int c = 0; c < dm; ++c) acc[(long)r * dm + c] += g * sh[(long)r * dm + c];
+        }
+        free(sh);
+    }
+    memcpy(out, acc, sizeof(double) * (size_t)nrows * dm);
+    free(xr);
+    free(sub);
+    free(acc);
+    free(sc);
+    free(pick);
+}
+
 /* matrix.cpp:52-60 */
 double orc_max_rel_error(const double* a, const double* b, long n) {
     double diff = 0.0, ref = 0.0;

@@ -109,7 +109,8 @@ def port_lib():
         lib.orc_max_rel_error.restype = _d
         for fn in ("orc_gate_scores", "orc_gate_logits", "orc_softmax_rows", "orc_normalize_graph",
                    "orc_similarity_table", "orc_random_matrix", "orc_dense_given_routing", "orc_rng_seed",
-                   "orc_trivial_placement", "orc_collaboration_shares", "orc_shared_experts"):
+                   "orc_trivial_placement", "orc_collaboration_shares", "orc_shared_experts",
+                   "orc_dense_rows_bf16"):
             getattr(lib, fn).restype = None
         lib.orc_rng_seed.argtypes = [_p, C.c_uint64]
         lib.orc_max_rel_error.argtypes = [_p, _p, C.c_long]
@@ -117,6 +118,8 @@ def port_lib():
             [_p, _i, _i, _p, _p, _i, _p, _p, _p, _i, _i, _p, _i, _p, _i, _i, _i, _d] + [_p] * 7)
         lib.orc_dense_given_routing.argtypes = [_p, _i, _i, _p, _p, _i, _p, _p, _p, _i, _i, _i, _p, _i, _p]
         lib.orc_shared_experts.argtypes = [_p, _i, _i, _p, _p, _p, _i, _i, _i, _p, _p]
+        lib.orc_dense_rows_bf16.argtypes = ([_p, _i, _i, _p, _p, _i, _i, _p, _p, _p, _i, _i, _i, _p, _p, _p, _i, _p,
+                                             _p, _i, _p])
         _PORT = lib
     return _PORT
 
@@ -452,6 +455,58 @@ def synthetic_layer(seed, n, dm, dh, ne, single=True, gated=False):
             w3[e] = er.random_matrix(dm, dh, single)
     g = Rng(gs).random_matrix(ne, dm, single)
     return x, g, w1, w2, w3
+
+
+def _u16(t):
+    """bf16 storage (torch.bfloat16 tensor or uint16 array) -> contiguous uint16 numpy."""
+    if t is None:
+        return None
+    if hasattr(t, "view") and hasattr(t, "dtype") and str(t.dtype) == "torch.bfloat16":
+        import torch
+        return np.ascontiguousarray(t.detach().cpu().contiguous().view(torch.int16).numpy().view(np.uint16))
+    return np.ascontiguousarray(t, dtype=np.uint16)
+
+
+def dense_rows_bf16(x, ids, w, w1, w2, rows, act="swiglu", w3=None, shared=None, threads=8):
+    """dense_given_routing (+ shared experts) in fp64 for the sampled `rows`,
+    operands in bf16 storage (occ_oracle.c orc_dense_rows_bf16): the
+    full-size value oracle of the BASELINE layers.  ids [n, k] int32, w [n, k]
+    f32 (the weights the layer ran with); w1/w3 [E, D, F], w2 [E, F, D];
+    shared = dict(w1, w2, w3=None, gate=None) with [S, D, F_s] / [S, F_s, D] /
+    [D].  Row chunks run on `threads` host threads (ctypes drops the GIL).
+    Returns [len(rows), D] float64."""
+    import threading
+    L = port_lib()
+    xu, w1u, w2u, w3u = _u16(x), _u16(w1), _u16(w2), _u16(w3)
+    ids = _i32(ids)
+    wf = np.ascontiguousarray(w, dtype=np.float32)
+    n, dm = xu.shape
+    k = ids.shape[1]
+    ne, _, dh = w1u.shape
+    ns, dhs, s1, s2, s3, sg = 0, 0, None, None, None, None
+    if shared is not None:
+        s1, s2 = _u16(shared["w1"]), _u16(shared["w2"])
+        s3, sg = _u16(shared.get("w3")), _u16(shared.get("gate"))
+        ns, dhs = s1.shape[0], s1.shape[2]
+    rows = _i32(rows)
+    out = np.empty((len(rows), dm), np.float64)
+    chunks = [c for c in np.array_split(np.arange(len(rows)), max(1, min(threads, len(rows)))) if len(c)]
+    gated = w3u is not None
+    a = ACT["silu" if gated else act]
+
+    def run(c):
+        sub = np.ascontiguousarray(rows[c])
+        o = np.empty((len(sub), dm), np.float64)
+        L.orc_dense_rows_bf16(_ptr(xu), n, dm, _ptr(ids), _ptr(wf), k, ne, _ptr(w1u), _ptr(w2u), _ptr(w3u), dh, a,
+                              ns, _ptr(s1), _ptr(s2), _ptr(s3), dhs, _ptr(sg), _ptr(sub), len(sub), _ptr(o))
+        out[c] = o
+
+    ts = [threading.Thread(target=run, args=(c,)) for c in chunks]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    return out
 
 
 def ref_fit_latency(xs, ys):

@@ -94,7 +94,8 @@ EXPORTS = (
     "occ_allreduce_histogram", "occ_last_error", "occ_launch_count", "occ_set_profiling", "occ_stage_ms", "occ_forward_host", "occ_host_wait", "occ_comm_init_loopback", "occ_exchange_layout", "occ_set_training", "occ_backward",
     "occ_load_shared_experts", "occ_comm_enable_peer", "occ_similarity_accumulate", "occ_similarity_finalize",
     "occ_router_logits", "occ_set_grad_x_bf16", "occ_gate_logits_f64", "occ_coactivation_first_batch",
-    "occ_component_growth", "occ_set_micro_batches", "occ_rng_create", "occ_rng_destroy", "occ_rng_next", "occ_rng_matrix", "occ_gen_trace",
+    "occ_component_growth", "occ_set_micro_batches", "occ_set_router_mode", "occ_route_exact",
+    "occ_dispatch", "occ_build_compute", "occ_expert_compute", "occ_combine", "occ_rng_create", "occ_rng_destroy", "occ_rng_next", "occ_rng_matrix", "occ_gen_trace",
 )
 
 STAGES = ("route", "plan", "pack", "compute_index", "gather", "gemm1", "gemm2", "shared", "partial_combine", "combine")
@@ -364,7 +365,7 @@ class ExpertParallelLayer:
         _need_cuda(upstream)
         c = self.config
         dev = upstream.device
-        e_l = c.num_experts
+        e_l = c.num_experts if self._world == 1 else c.experts_per_device()  # this rank's experts
         n = upstream.shape[0]
         if grad_x_dtype not in (torch.float32, torch.bfloat16):
             raise ShapeError("backward: grad_x_dtype must be float32 or bfloat16")
@@ -407,6 +408,30 @@ class ExpertParallelLayer:
                                C.byref(pr) if pr else None, _ptr(ids), _ptr(w), _ptr(sc), _stream()), "route")
         return (ids, w, sc) if want_scores else (ids, w)
 
+    def set_router_mode(self, mode: str):
+        """"tc" (default): tcgen05 router, equal to the reference except at
+        f32-level near-ties; "exact": the reference's fp64 arithmetic with
+        glibc's exp, bit-exact ids and weights (occ_set_router_mode)."""
+        _check(lib().occ_set_router_mode(self._h, {"tc": 0, "exact": 1}[mode]), "set_router_mode")
+
+    def route_exact(self, x: torch.Tensor, gate: torch.Tensor, prune: Optional[PruneSpec] = None,
+                    want_scores=False):
+        """gate_scores -> topk_route -> prune_routing of forward_expert_parallel
+        (pipeline.cpp:509-512) bit for bit on the bf16 operands: ids int32
+        [n,k], weights f64 [n,k] (+ f64 softmax scores [n,E])."""
+        _need_cuda(x, gate)
+        c = self.config
+        n = x.shape[0]
+        x = _arg(x, "route_exact: x", torch.bfloat16, (n, c.embed_dim))
+        gate = _arg(gate, "route_exact: gate", torch.bfloat16, (c.num_experts, c.embed_dim))
+        ids = torch.empty((n, c.top_k), dtype=torch.int32, device=x.device)
+        w = torch.empty((n, c.top_k), dtype=torch.float64, device=x.device)
+        sc = torch.empty((n, c.num_experts), dtype=torch.float64, device=x.device) if want_scores else None
+        pr = self._prune(prune)
+        _check(lib().occ_route_exact(self._h, _ptr(x), _ptr(gate), n, C.byref(pr) if pr else None, _ptr(ids),
+                                     _ptr(w), _ptr(sc), _stream()), "route_exact")
+        return (ids, w, sc) if want_scores else (ids, w)
+
     def _prune(self, prune):
         if prune is None or prune.mode == "none":
             return None
@@ -427,17 +452,84 @@ class ExpertParallelLayer:
 
     # EP path -------------------------------------------------------------------
     def build_dispatch_index(self, ids: torch.Tensor, sources: Optional[torch.Tensor] = None):
-        """BRIM0 of every source (pipeline.cpp:24-50) + the (source, dest) counts."""
+        """BRIM0 (pipeline.cpp:24-50) + the Sfd row counts.  world_size 1: every
+        source (BRIM0s concatenated, counts [N_d, N_d]); world_size > 1: this
+        rank's tokens as one source (BRIM0 [N_d * n], counts [N_d])."""
         _need_cuda(ids, sources)
         n = ids.shape[0]
         nd = self.config.num_devices
         ids = _arg(ids, "build_dispatch_index: ids", torch.int32, (n, self.config.top_k))
         sources = _arg(sources, "build_dispatch_index: sources", torch.int32, (n,))
         brim0 = torch.empty(n * nd, dtype=torch.int32, device=ids.device)
-        counts = torch.empty((nd, nd), dtype=torch.int32, device=ids.device)
+        counts = torch.empty((nd, nd) if self._world == 1 else (nd,), dtype=torch.int32, device=ids.device)
         _check(lib().occ_build_dispatch(self._h, _ptr(ids), _ptr(sources), n, _ptr(brim0),
                                         _ptr(counts), _stream()), "build_dispatch")
         return brim0, counts
+
+    # stage-level entry points (pipeline.hpp:89-123) ------------------------------
+    def dispatch(self, x: torch.Tensor, ids: torch.Tensor, w: torch.Tensor, brim0: torch.Tensor,
+                 n_sfd: Optional[int] = None):
+        """dispatch (pipeline.cpp:91-123) of one source's tokens by its BRIM0
+        [N_d * n]: the SfdBatch (x rows, ids, weights, token index), device-major."""
+        _need_cuda(x, ids, w, brim0)
+        c = self.config
+        n = x.shape[0]
+        x = _arg(x, "dispatch: x", torch.bfloat16, (n, c.embed_dim))
+        ids = _arg(ids, "dispatch: ids", torch.int32, (n, c.top_k))
+        w = _arg(w, "dispatch: weights", torch.float32, (n, c.top_k))
+        brim0 = _arg(brim0.reshape(-1), "dispatch: brim0", torch.int32, (c.num_devices * n,))
+        if n_sfd is None:
+            n_sfd = int((brim0 >= 0).sum())
+        dev = x.device
+        sx = torch.empty((n_sfd, c.embed_dim), dtype=torch.bfloat16, device=dev)
+        si = torch.empty((n_sfd, c.top_k), dtype=torch.int32, device=dev)
+        sw = torch.empty((n_sfd, c.top_k), dtype=torch.float32, device=dev)
+        st = torch.empty(n_sfd, dtype=torch.int32, device=dev)
+        _check(lib().occ_dispatch(self._h, _ptr(x), _ptr(ids), _ptr(w), n, _ptr(brim0), _ptr(sx), _ptr(si), _ptr(sw),
+                                  _ptr(st), _stream()), "dispatch")
+        return sx, si, sw, st
+
+    def build_compute_index(self, device: int, in_ids: torch.Tensor, in_w: torch.Tensor):
+        """build_compute_index (pipeline.cpp:52-89) of EP device `device` over
+        its inbox rows: (cindex [P, R] int32, n_epd)."""
+        _need_cuda(in_ids, in_w)
+        c = self.config
+        r = in_ids.shape[0]
+        in_ids = _arg(in_ids, "build_compute: ids", torch.int32, (r, c.top_k))
+        in_w = _arg(in_w, "build_compute: weights", torch.float32, (r, c.top_k))
+        cix = torch.empty((c.experts_per_device(), r), dtype=torch.int32, device=in_ids.device)
+        ne = torch.zeros(1, dtype=torch.int32, device=in_ids.device)
+        _check(lib().occ_build_compute(self._h, device, _ptr(in_ids), _ptr(in_w), r, _ptr(cix), _ptr(ne), _stream()),
+               "build_compute")
+        return cix, int(ne.item())
+
+    def expert_compute(self, device: int, in_x: torch.Tensor, in_ids: torch.Tensor, in_w: torch.Tensor,
+                       out: Optional[torch.Tensor] = None):
+        """scatter_matmul -> apply_activation -> weight_modulate -> merge_matmul
+        (pipeline.cpp:178-283) of EP device `device`: the partial-combined
+        return rows [R, D] bf16."""
+        _need_cuda(in_x, in_ids, in_w)
+        c = self.config
+        r = in_x.shape[0]
+        in_x = _arg(in_x, "expert_compute: x", torch.bfloat16, (r, c.embed_dim))
+        in_ids = _arg(in_ids, "expert_compute: ids", torch.int32, (r, c.top_k))
+        in_w = _arg(in_w, "expert_compute: weights", torch.float32, (r, c.top_k))
+        if out is None:
+            out = torch.empty_like(in_x)
+        _check(lib().occ_expert_compute(self._h, device, _ptr(in_x), _ptr(in_ids), _ptr(in_w), r, _ptr(out),
+                                        _stream()), "expert_compute")
+        return out
+
+    def combine(self, y_returned: torch.Tensor, brim0: torch.Tensor, n: int, out: Optional[torch.Tensor] = None):
+        """combine (pipeline.cpp:285-300) of one source: Ori rows [n, D] bf16."""
+        _need_cuda(y_returned, brim0)
+        c = self.config
+        y = _arg(y_returned, "combine: rows", torch.bfloat16, (y_returned.shape[0], c.embed_dim))
+        brim0 = _arg(brim0.reshape(-1), "combine: brim0", torch.int32, (c.num_devices * n,))
+        if out is None:
+            out = torch.empty((n, c.embed_dim), dtype=torch.bfloat16, device=y.device)
+        _check(lib().occ_combine(self._h, _ptr(y), _ptr(brim0), n, _ptr(out), _stream()), "combine")
+        return out
 
     def forward_given_routing(self, x: torch.Tensor, ids: torch.Tensor, w: torch.Tensor,
                               sources: Optional[torch.Tensor] = None, out: Optional[torch.Tensor] = None):

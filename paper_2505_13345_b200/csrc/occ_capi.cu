@@ -166,6 +166,11 @@ struct occ_handle {
     DevBuf<int32_t> in_ids, in_tok, in_src, in_slot, in_dev, row_epd, epd_src, epd_j;
     DevBuf<float> in_w, epd_w, logits, rt_w;
     DevBuf<int32_t> rt_ids;  // routing of occ_forward_expert_parallel
+    // exact router (occ_set_router_mode(h, OCC_ROUTER_EXACT)): fp64 scores,
+    // unpruned top-k, fp64 weights
+    int router_mode = 0;
+    DevBuf<double> x_s64, x_w64, x_w64b;
+    DevBuf<int32_t> x_ids;
     size_t R_max = 0, Q_max = 0, max_mblk = 0;
     int last_n = 0;
     bool have_forward = false;
@@ -193,6 +198,10 @@ struct occ_handle {
     bool bwd_weights_ready = false;  // w13o / w2o + their tensor maps built (training on at occ_load_experts)
     DevBuf<__nv_bfloat16> save_a, save_b, w13o, w2o, g_epd, gpre;
     DevBuf<float> gw_part, gw_row;
+    // world_size > 1 backward: received upstream rows, returned gradient rows,
+    // per-row routing-weight gradients (sent / received)
+    DevBuf<__nv_bfloat16> g_in, g_ysrc;
+    DevBuf<float> ret_gw, y_gw;
     TmapBox tmG_k, tmW2o, tmP_k, tmW1o, tmH_mn, tmG_mn, tmX_mn, tmP_mn;
     int bwd_tmaps_q = -1;
     // host-buffer pipeline (occ_forward_host)
@@ -580,7 +589,7 @@ occ_status ensure_ws(occ_handle* h, int n) {
 }
 
 // Forward GEMM-1 (scatter + activation + modulation) and GEMM-2 (merge products).
-void launch_gemm1(occ_handle* h, int ngroups, cudaStream_t st, bool gathered) {
+void launch_gemm1(occ_handle* h, int ngroups, cudaStream_t st, bool gathered, const int* widx = nullptr) {
     GemmArgs g;
     g.tmap_a = gathered ? h->tmAX.bytes : h->tmA1.bytes;
     g.a_rows = gathered ? h->epd_src.p : nullptr;
@@ -590,7 +599,7 @@ void launch_gemm1(occ_handle* h, int ngroups, cudaStream_t st, bool gathered) {
     g.N = h->F;
     g.b_rows_per_e = h->n1rows;
     g.grp_mb = h->cofs.grp_mb;
-    g.grp_w = h->d_widx.p;
+    g.grp_w = widx ? widx : h->d_widx.p;
     g.ngroups = ngroups;
     g.row_w = h->epd_w.p;
     g.out = h->hbuf.p;
@@ -605,7 +614,7 @@ void launch_gemm1(occ_handle* h, int ngroups, cudaStream_t st, bool gathered) {
     launch_grouped_gemm(h->gated ? EPI_SWIGLU_BF16 : EPI_ACT_BF16, g, h->num_sms, st);
 }
 
-void launch_gemm2(occ_handle* h, int ngroups, cudaStream_t st) {
+void launch_gemm2(occ_handle* h, int ngroups, cudaStream_t st, const int* widx = nullptr) {
     GemmArgs g;
     g.tmap_a = h->tmA2.bytes;
     g.tmap_b = h->tmB2.bytes;
@@ -614,7 +623,7 @@ void launch_gemm2(occ_handle* h, int ngroups, cudaStream_t st) {
     g.N = h->D;
     g.b_rows_per_e = h->D;
     g.grp_mb = h->cofs.grp_mb;
-    g.grp_w = h->d_widx.p;
+    g.grp_w = widx ? widx : h->d_widx.p;
     g.ngroups = ngroups;
     // raster band (m-tiles per band): whole experts for long K (Mixtral GEMM-2,
     // K = 14336: +5%), 8 for short K (64-expert layers: +3-4%); profiles/r01_gemm_micro.md
@@ -869,13 +878,139 @@ occ_status forward_multi(occ_handle* h, const __nv_bfloat16* x, const int32_t* i
     CUDA_TRY(cudaGetLastError());
     h->last_n = n;
     h->have_forward = true;
+    h->have_train_state = h->training != 0;
     if (h->validate) return check_err(h, st);
+    return OCC_OK;
+}
+
+static occ_status backward_multi(occ_handle* h, const __nv_bfloat16* up, void* g_x, float* g_w1, float* g_w3,
+                                 float* g_w2, float* g_weights, cudaStream_t st);
+static void bwd_gemms(occ_handle* h, int NG, const int* widx, float* g_w1, float* g_w3, float* g_w2, cudaStream_t st);
+
+// The expert side of EP device `dev` over R inbox rows (stage-level entry
+// points and the world_size > 1 forward): BRIM1 (build_compute_index,
+// pipeline.cpp:52-89) -> Epd rows of the A operand -> grouped GEMM-1 (scatter
+// + activation + modulation, pipeline.cpp:178-248) -> grouped GEMM-2 (merge
+// products, pipeline.cpp:250-283) into h->y16 (per Epd row); the caller sums
+// the products per row (partial combine) or extracts the index.  d_R: device
+// row count (<= R_max, which sizes the grids).
+static occ_status expert_side(occ_handle* h, int dev, const __nv_bfloat16* in_x, const int32_t* in_ids,
+                              const float* in_w, int R_max, const int* d_R, bool gemms, cudaStream_t st) {
+    const int k = h->k, P = h->P, D = h->D;
+    const int Rm = std::max(R_max, 1);
+    const int* widx = h->d_widx.p + (h->world == 1 ? (size_t)dev * P : 0);
+    ComputeArgs ca{Rm, d_R, k, P, 1, in_ids, in_w, nullptr, h->d_dev_of.p, h->d_slot_of.p, dev,
+                   h->rmask.p, h->rgroup.p, h->err.p};
+    launch_compute_mask(ca, st);
+    RankWs ws2{h->chunk_cnt2.p, h->totals2.p};
+    launch_rank_count_dev(Rm, d_R, h->rgroup.p, h->rmask.p, 1, P, ws2, st);
+    launch_rank_scan(Rm, 1, P, ws2, st);
+    launch_compute_finalize(1, P, h->totals2.p, h->cofs, st);
+    launch_init_epd((int)h->Q_max, h->epd_src.p, h->epd_w.p, st);
+    EmitCompute ec{k, P, dev, in_ids, in_w, h->d_slot_of.p, h->d_dev_of.p, h->cofs, h->row_epd.p, h->epd_src.p,
+                   h->epd_w.p, h->epd_j.p};
+    launch_rank_emit_compute(Rm, d_R, h->rgroup.p, h->rmask.p, 1, P, ws2, ec, st);
+    if (!gemms) return OCC_OK;
+    mark(h, ST_GATHER, st);
+    launch_scatter_rows(Rm, d_R, P, D, in_x, nullptr, h->row_epd.p, P, h->cofs, h->x_epd.p, st);
+    mark(h, ST_GEMM1, st);
+    launch_gemm1(h, P, st, false, widx);
+    mark(h, ST_GEMM2, st);
+    launch_gemm2(h, P, st, widx);
+    return OCC_OK;
+}
+
+static occ_status stage_device(occ_handle* h, int device) {
+    if (h->world == 1 ? (device < 0 || device >= h->nd) : device != h->rank)
+        return fail(OCC_ERR_CONFIG, "stage: device must be in [0, num_devices) (world_size 1) or this rank");
     return OCC_OK;
 }
 
 extern "C" {
 
 const char* occ_last_error(void) { return g_err.c_str(); }
+
+occ_status occ_dispatch(occ_handle* h, const void* x, const int32_t* ids, const float* weights, int n,
+                        const int32_t* brim0, void* sfd_x, int32_t* sfd_ids, float* sfd_weights, int32_t* sfd_token,
+                        occ_stream_t stream) {
+    if (!h) return fail(OCC_ERR_ARG, "null handle");
+    if (n < 0) return fail(OCC_ERR_SHAPE, "dispatch: negative token count");
+    if (n > 0 && (!x || !ids || !weights || !brim0 || !sfd_x || !sfd_ids || !sfd_weights || !sfd_token))
+        return fail(OCC_ERR_ARG, "null argument");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    launch_dispatch_sfd(n, h->nd, h->k, h->D, reinterpret_cast<const __nv_bfloat16*>(x), ids, weights, brim0,
+                        reinterpret_cast<__nv_bfloat16*>(sfd_x), sfd_ids, sfd_weights, sfd_token, st);
+    CUDA_TRY(cudaGetLastError());
+    return OCC_OK;
+}
+
+occ_status occ_build_compute(occ_handle* h, int device, const int32_t* in_ids, const float* in_weights, int rows,
+                             int32_t* cindex, int32_t* n_epd, occ_stream_t stream) {
+    if (!h) return fail(OCC_ERR_ARG, "null handle");
+    occ_status s = stage_device(h, device);
+    if (s != OCC_OK) return s;
+    if (rows < 0) return fail(OCC_ERR_SHAPE, "build_compute: negative row count");
+    if (rows > 0 && (!in_ids || !in_weights)) return fail(OCC_ERR_ARG, "null argument");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if ((s = ensure_ws(h, 1)) != OCC_OK) return s;
+    const size_t R = (size_t)std::max(rows, 1);
+    if ((s = ensure_recv(h, R, R * std::min(h->k, h->P))) != OCC_OK) return s;
+    h->have_train_state = false;
+    CUDA_TRY(cudaMemsetAsync(h->err.p, 0, sizeof(int32_t), st));
+    CUDA_TRY(cudaMemsetAsync(h->stats.p, 0, sizeof(long long) * 8, st));
+    launch_set_int(h->d_R, rows, st);
+    if (rows > 0) {
+        if ((s = expert_side(h, device, nullptr, in_ids, in_weights, rows, h->d_R, false, st)) != OCC_OK) return s;
+        if (cindex) launch_extract_cindex(rows, h->d_R, h->P, nullptr, nullptr, h->row_epd.p, h->cofs, cindex, st);
+    }
+    if (n_epd) CUDA_TRY(cudaMemcpyAsync(n_epd, h->stats.p + 6, sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+    CUDA_TRY(cudaGetLastError());
+    if (h->validate) return check_err(h, st);
+    return OCC_OK;
+}
+
+occ_status occ_expert_compute(occ_handle* h, int device, const void* in_x, const int32_t* in_ids,
+                              const float* in_weights, int rows, void* y_out, occ_stream_t stream) {
+    if (!h) return fail(OCC_ERR_ARG, "null handle");
+    occ_status s = stage_device(h, device);
+    if (s != OCC_OK) return s;
+    if (!h->weights_loaded) return fail(OCC_ERR_STATE, "expert_compute: experts not loaded");
+    if (rows < 0) return fail(OCC_ERR_SHAPE, "expert_compute: negative row count");
+    if (rows > 0 && (!in_x || !in_ids || !in_weights || !y_out)) return fail(OCC_ERR_ARG, "null argument");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if ((s = ensure_ws(h, 1)) != OCC_OK) return s;
+    const size_t R = (size_t)std::max(rows, 1);
+    if ((s = ensure_recv(h, R, R * std::min(h->k, h->P))) != OCC_OK) return s;
+    if (h->training) {
+        CUDA_TRY(h->save_a.ensure(h->Q_max * h->F));
+        if (h->gated) CUDA_TRY(h->save_b.ensure(h->Q_max * h->F));
+    }
+    h->have_train_state = false;
+    if (rows == 0) return OCC_OK;
+    CUDA_TRY(cudaMemsetAsync(h->err.p, 0, sizeof(int32_t), st));
+    CUDA_TRY(cudaMemsetAsync(h->stats.p, 0, sizeof(long long) * 8, st));
+    launch_set_int(h->d_R, rows, st);
+    if ((s = expert_side(h, device, reinterpret_cast<const __nv_bfloat16*>(in_x), in_ids, in_weights, rows, h->d_R,
+                         true, st)) != OCC_OK)
+        return s;
+    launch_partial_combine(rows, h->d_R, h->P, h->D, h->row_epd.p, h->y16.p, reinterpret_cast<__nv_bfloat16*>(y_out),
+                           st);
+    CUDA_TRY(cudaGetLastError());
+    if (h->validate) return check_err(h, st);
+    return OCC_OK;
+}
+
+occ_status occ_combine(occ_handle* h, const void* y_returned, const int32_t* brim0, int n, void* out,
+                       occ_stream_t stream) {
+    if (!h) return fail(OCC_ERR_ARG, "null handle");
+    if (n < 0) return fail(OCC_ERR_SHAPE, "combine: negative token count");
+    if (n > 0 && (!y_returned || !brim0 || !out)) return fail(OCC_ERR_ARG, "null argument");
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    launch_combine_brim0(n, h->nd, h->D, brim0, reinterpret_cast<const __nv_bfloat16*>(y_returned),
+                         reinterpret_cast<__nv_bfloat16*>(out), st);
+    CUDA_TRY(cudaGetLastError());
+    return OCC_OK;
+}
 long long occ_launch_count(void) { return g_launches; }
 
 static void unborrow(occ_handle* b);
@@ -947,6 +1082,8 @@ occ_status occ_destroy(occ_handle* h) {
     h->snd_w.release();
     for (auto* b : {&h->in_w, &h->epd_w, &h->logits, &h->rt_w}) b->release();
     h->rt_ids.release();
+    for (auto* b : {&h->x_s64, &h->x_w64, &h->x_w64b}) b->release();
+    h->x_ids.release();
     for (auto& e : h->ev)
         if (e) cudaEventDestroy(e);
     for (auto& e : h->pev) cudaEventDestroy(e);
@@ -961,6 +1098,10 @@ occ_status occ_destroy(occ_handle* h) {
     for (auto* b : {&h->save_a, &h->save_b, &h->w13o, &h->w2o, &h->g_epd, &h->gpre}) b->release();
     h->gw_part.release();
     h->gw_row.release();
+    h->g_in.release();
+    h->g_ysrc.release();
+    h->ret_gw.release();
+    h->y_gw.release();
     h->epd_j.release();
     for (void* ptr : h->ipc_opened) cudaIpcCloseMemHandle(ptr);
     h->flags.release();
@@ -1234,6 +1375,56 @@ occ_status occ_prune_routing_f64(occ_handle* h, const double* scores, const int3
     return check_err(h, st);
 }
 
+// gate_scores -> topk_route -> prune_routing (pipeline.cpp:509-512) in the
+// reference's arithmetic: fp64 logits of the bf16 operands in ascending k
+// without FMA, softmax with glibc's exp, (score desc, index asc) top-k,
+// renormalisation and pruning in fp64.  Bit-exact with the reference.
+static occ_status route_exact(occ_handle* h, const void* x, const void* gate, int n, const PruneDev& p, int32_t* ids,
+                              double* weights, double* scores, cudaStream_t st) {
+    const int E = h->E, k = h->k;
+    const size_t nn = (size_t)std::max(n, 1);
+    double* s64 = scores;
+    if (!s64) {
+        CUDA_TRY(h->x_s64.ensure(nn * E));
+        s64 = h->x_s64.p;
+    }
+    launch_gate_scores_bf16_f64(reinterpret_cast<const __nv_bfloat16*>(x), n, h->D,
+                                reinterpret_cast<const __nv_bfloat16*>(gate), E, s64, st);
+    if (p.mode == OCC_PRUNE_NONE) {
+        launch_topk_f64(s64, n, E, k, h->cfg.renormalize, ids, weights, h->err.p, st);
+    } else {
+        CUDA_TRY(h->x_ids.ensure(nn * k));
+        CUDA_TRY(h->x_w64b.ensure(nn * k));
+        launch_topk_f64(s64, n, E, k, h->cfg.renormalize, h->x_ids.p, h->x_w64b.p, h->err.p, st);
+        launch_prune_f64(s64, n, E, k, h->x_ids.p, h->x_w64b.p, p, ids, weights, h->err.p, st);
+    }
+    return OCC_OK;
+}
+
+occ_status occ_set_router_mode(occ_handle* h, int mode) {
+    if (!h) return fail(OCC_ERR_ARG, "null handle");
+    if (mode != OCC_ROUTER_TC && mode != OCC_ROUTER_EXACT) return fail(OCC_ERR_CONFIG, "router mode: 0 (tc) or 1 (exact)");
+    h->router_mode = mode;
+    if (h->sib) h->sib->router_mode = mode;
+    return OCC_OK;
+}
+
+occ_status occ_route_exact(occ_handle* h, const void* x, const void* gate, int n, const occ_prune* prune, int32_t* ids,
+                           double* weights, double* scores, occ_stream_t stream) {
+    if (!h || !gate || (n > 0 && (!x || !ids || !weights))) return fail(OCC_ERR_ARG, "null argument");
+    if (n < 0) return fail(OCC_ERR_SHAPE, "route: negative token count");
+    PruneDev p;
+    occ_status s = prune_dev(h, prune, p);
+    if (s != OCC_OK) return s;
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    CUDA_TRY(h->err.ensure(1));
+    CUDA_TRY(cudaMemsetAsync(h->err.p, 0, sizeof(int32_t), st));
+    if (n > 0 && (s = route_exact(h, x, gate, n, p, ids, weights, scores, st)) != OCC_OK) return s;
+    CUDA_TRY(cudaGetLastError());
+    if (h->validate) return check_err(h, st);
+    return OCC_OK;
+}
+
 occ_status occ_route(occ_handle* h, const void* x, const void* gate, int n, const occ_prune* prune, int32_t* ids,
                      float* weights, float* scores, occ_stream_t stream) {
     if (!h || !gate || (n > 0 && (!x || !ids || !weights))) return fail(OCC_ERR_ARG, "null argument");
@@ -1245,7 +1436,18 @@ occ_status occ_route(occ_handle* h, const void* x, const void* gate, int n, cons
     CUDA_TRY(h->logits.ensure((size_t)std::max(n, 1) * h->E));
     CUDA_TRY(h->err.ensure(1));
     CUDA_TRY(cudaMemsetAsync(h->err.p, 0, sizeof(int32_t), st));
-    if (n > 0) {
+    if (n > 0 && h->router_mode == OCC_ROUTER_EXACT) {
+        const size_t nn = (size_t)n;
+        CUDA_TRY(h->x_w64.ensure(nn * h->k));
+        double* s64 = nullptr;
+        if (scores) {
+            CUDA_TRY(h->x_s64.ensure(nn * h->E));
+            s64 = h->x_s64.p;
+        }
+        if ((s = route_exact(h, x, gate, n, p, ids, h->x_w64.p, s64, st)) != OCC_OK) return s;
+        launch_f64_to_f32(h->x_w64.p, (long)nn * h->k, weights, st);
+        if (scores) launch_f64_to_f32(s64, (long)nn * h->E, scores, st);
+    } else if (n > 0) {
         // logits = x g^T on tcgen05; softmax + top-k fused in the epilogue
         // unless pruning / score rows need the full rows (router_select)
         const int np = (h->E + 31) / 32 * 32;
@@ -1270,12 +1472,44 @@ occ_status occ_route(occ_handle* h, const void* x, const void* gate, int n, cons
 // ----------------------------------------------------------------- EP path
 occ_status occ_build_dispatch(occ_handle* h, const int32_t* ids, const int32_t* sources, int n, int32_t* brim0,
                               int32_t* counts, occ_stream_t stream) {
-    if (!h || !ids) return fail(OCC_ERR_ARG, "null argument");
-    if (h->world != 1) return fail(OCC_ERR_UNSUPPORTED, "occ_build_dispatch: world_size 1 only");
+    if (!h || (!ids && n > 0)) return fail(OCC_ERR_ARG, "null argument");
     if (!h->cfg.dedup) return fail(OCC_ERR_UNSUPPORTED, "BRIM0 is defined for the dedup dispatch");
+    if (n < 0) return fail(OCC_ERR_SHAPE, "build_dispatch: negative token count");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    occ_status s = ensure_ws(h, n);
+    occ_status s = ensure_ws(h, std::max(n, 1));
     if (s != OCC_OK) return s;
+    if (h->world > 1) {
+        // this rank's tokens are one source (= rank): BRIM0 N_d x n and its
+        // count row, from the local plan alone (counters are per source,
+        // pipeline.cpp:24-50; no exchange needed)
+        const int nd = h->nd, k = h->k, r = h->rank;
+        h->have_train_state = false;
+        CUDA_TRY(cudaMemsetAsync(h->stats.p, 0, sizeof(long long) * 8, st));
+        CUDA_TRY(cudaMemsetAsync(h->err.p, 0, sizeof(int32_t), st));
+        if (n > 0) {
+            PlanArgs pa{n, k, nd, 1, ids, nullptr, nullptr, r, h->d_dev_of.p, h->d_slot_of.p, h->E, h->mask.p,
+                        h->group.p, h->err.p};
+            launch_plan_mask(pa, st);
+            RankWs ws{h->chunk_cnt.p, h->totals.p};
+            launch_rank_count(n, h->group.p, h->mask.p, 1, nd, ws, st);
+            launch_rank_scan(n, 1, nd, ws, st);
+            launch_one_source_totals(nd, r, h->totals.p, st);
+            launch_dispatch_finalize(nd, h->totals.p, h->dofs, st);
+            EmitDispatch em{n, k, nd, 1, ids, nullptr, nullptr, r, h->d_dev_of.p, h->dofs, 0, h->tok_row.p,
+                            h->tok_sfd.p, h->lam.p, nullptr, nullptr, nullptr, nullptr};
+            launch_rank_emit_dispatch(n, h->group.p, h->mask.p, 1, nd, ws, em, st);
+            if (brim0) launch_brim0_one_source(n, nd, h->mask.p, h->tok_sfd.p, brim0, st);
+        }
+        if (counts) {
+            if (n > 0)
+                CUDA_TRY(cudaMemcpyAsync(counts, h->dofs.C + (size_t)r * nd, sizeof(int) * nd, cudaMemcpyDeviceToDevice,
+                                         st));
+            else
+                CUDA_TRY(cudaMemsetAsync(counts, 0, sizeof(int) * nd, st));
+        }
+        CUDA_TRY(cudaGetLastError());
+        return check_err(h, st);
+    }
     CUDA_TRY(cudaMemsetAsync(h->stats.p, 0, sizeof(long long) * 8, st));
     CUDA_TRY(cudaMemsetAsync(h->err.p, 0, sizeof(int32_t), st));
     h->have_train_state = false;  // the plan buffers no longer hold the saved forward
@@ -1309,6 +1543,7 @@ static void sync_sibling(occ_handle* h) {
     b->d_ranking.p = h->d_ranking.p, b->d_ranking.n = h->d_ranking.n;
     b->have_ranking = h->have_ranking;
     b->validate = h->validate;
+    b->router_mode = h->router_mode;
     b->num_sms = h->num_sms;
     b->gather_a = h->gather_a;
 }
@@ -1466,7 +1701,6 @@ occ_status occ_forward_expert_parallel(occ_handle* h, const void* x, const void*
 
 occ_status occ_set_training(occ_handle* h, int on) {
     if (!h) return fail(OCC_ERR_ARG, "null handle");
-    if (on && h->world != 1) return fail(OCC_ERR_UNSUPPORTED, "backward: world_size 1 in this build");
     if (on && h->mb > 1) return fail(OCC_ERR_UNSUPPORTED, "training: micro-batching is inference-only");
     h->training = on;
     h->have_train_state = false;
@@ -1500,20 +1734,43 @@ occ_status occ_backward(occ_handle* h, const void* upstream, float* g_x, float* 
     if (!h->bwd_weights_ready)
         return fail(OCC_ERR_STATE, "backward: occ_set_training(h, 1) must precede occ_load_experts");
     if (h->n_shared) return fail(OCC_ERR_UNSUPPORTED, "backward: shared experts are forward-only in this build");
-    const int n = h->last_n, k = h->k, P = h->P, D = h->D, F = h->F, nd = h->nd, E = h->E;
-    if (n > 0 && (!upstream || !g_x || !g_w1 || !g_w2 || !g_weights || (h->gated && !g_w3)))
+    const int n = h->last_n, k = h->k, P = h->P, D = h->D, F = h->F, nd = h->nd;
+    const int El = h->world == 1 ? h->E : P;  // weight gradients of the resident experts
+    if (!g_w1 || !g_w2 || (h->gated && !g_w3) || (n > 0 && (!upstream || !g_x || !g_weights)))
         return fail(OCC_ERR_ARG, "null argument");
     cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    const int G = nd, NG = G * P, kw = h->gated ? 2 * F : F;
-    CUDA_TRY(cudaMemsetAsync(g_w1, 0, sizeof(float) * E * D * F, st));
-    CUDA_TRY(cudaMemsetAsync(g_w2, 0, sizeof(float) * E * F * D, st));
-    if (h->gated) CUDA_TRY(cudaMemsetAsync(g_w3, 0, sizeof(float) * E * D * F, st));
+    CUDA_TRY(cudaMemsetAsync(g_w1, 0, sizeof(float) * El * D * F, st));
+    CUDA_TRY(cudaMemsetAsync(g_w2, 0, sizeof(float) * El * F * D, st));
+    if (h->gated) CUDA_TRY(cudaMemsetAsync(g_w3, 0, sizeof(float) * El * D * F, st));
+    if (h->world > 1)  // collective: every rank joins the exchanges, even with no tokens
+        return backward_multi(h, reinterpret_cast<const __nv_bfloat16*>(upstream), g_x, g_w1, g_w3, g_w2, g_weights,
+                              st);
     if (n == 0) return OCC_OK;
     occ_status s = ensure_bwd(h);
     if (s != OCC_OK) return s;
     // combine + return adjoints: the token's upstream row on every Epd row
     launch_scatter_rows((int)h->R_max, h->dofs.in_base + nd, P, D, reinterpret_cast<const __nv_bfloat16*>(upstream),
                         h->in_tok.p, h->row_epd.p, nd * P, h->cofs, h->g_epd.p, st);
+    bwd_gemms(h, nd * P, h->d_widx.p, g_w1, g_w3, g_w2, st);
+    // dispatch adjoint: sum each token's rows (device ascending), fp32
+    launch_combine_grad(n, nd, k, P, h->cfg.dedup, D, h->mask.p, h->tok_row.p, h->row_epd.p, h->y16.p, g_x,
+                        h->gx_bf16, st);
+    launch_gw_scatter((int)h->Q_max, h->d_q_total, 2 * ((F + 255) / 256), h->gw_part.p, h->epd_src.p, h->in_tok.p,
+                      h->epd_j.p, k, g_weights, st);
+    CUDA_TRY(cudaGetLastError());
+    if (h->validate) CUDA_TRY(cudaStreamSynchronize(st));
+    return OCC_OK;
+}
+
+}  // extern "C"
+
+// The four backward GEMMs of the saved Epd grouping (NG groups, weight index
+// widx): merge adjoint (data, with the modulation / activation adjoints and
+// the routing-weight partials in the epilogue) -> gpre; scatter adjoint (data)
+// -> y16 per Epd row; merge / scatter adjoints (weights) -> g_w2, g_w1 | g_w3.
+static void bwd_gemms(occ_handle* h, int NG, const int* widx, float* g_w1, float* g_w3, float* g_w2,
+                      cudaStream_t st) {
+    const int D = h->D, F = h->F, kw = h->gated ? 2 * F : F;
     // merge adjoint (data): g_mod = g_y w2^T, with modulation + activation
     // adjoints and the routing-weight partials fused in the epilogue
     GemmArgs g;
@@ -1523,7 +1780,7 @@ occ_status occ_backward(occ_handle* h, const void* upstream, float* g_x, float* 
     g.N = F;
     g.b_rows_per_e = F;
     g.grp_mb = h->cofs.grp_mb;
-    g.grp_w = h->d_widx.p;
+    g.grp_w = widx;
     g.ngroups = NG;
     g.row_w = h->epd_w.p;
     g.out = h->gpre.p;
@@ -1545,7 +1802,7 @@ occ_status occ_backward(occ_handle* h, const void* upstream, float* g_x, float* 
     d1.N = D;
     d1.b_rows_per_e = D;
     d1.grp_mb = h->cofs.grp_mb;
-    d1.grp_w = h->d_widx.p;
+    d1.grp_w = widx;
     d1.ngroups = NG;
     d1.band = kw >= 4096 ? (1 << 20) : 8;
     d1.out = h->y16.p;
@@ -1561,7 +1818,7 @@ occ_status occ_backward(occ_handle* h, const void* upstream, float* g_x, float* 
     w2.M = F;
     w2.grp_cnt = h->cofs.cnt;
     w2.seg_base = h->cofs.seg_base;
-    w2.grp_w = h->d_widx.p;
+    w2.grp_w = widx;
     w2.ngroups = NG;
     w2.out = g_w2;
     w2.ldo = D;
@@ -1576,7 +1833,7 @@ occ_status occ_backward(occ_handle* h, const void* upstream, float* g_x, float* 
     w1.M = D;
     w1.grp_cnt = h->cofs.cnt;
     w1.seg_base = h->cofs.seg_base;
-    w1.grp_w = h->d_widx.p;
+    w1.grp_w = widx;
     w1.ngroups = NG;
     w1.out = g_w1;
     w1.out2 = h->gated ? g_w3 : nullptr;
@@ -1585,15 +1842,70 @@ occ_status occ_backward(occ_handle* h, const void* upstream, float* g_x, float* 
     w1.out_estride = (long)D * F;
     w1.max_tiles = NG * ((D + 255) / 256) * ((kw + 255) / 256);
     launch_grouped_gemm(EPI_WGRAD, w1, h->num_sms, st);
-    // dispatch adjoint: sum each token's rows (device ascending), fp32
-    launch_combine_grad(n, nd, k, P, h->cfg.dedup, D, h->mask.p, h->tok_row.p, h->row_epd.p, h->y16.p, g_x,
-                        h->gx_bf16, st);
-    launch_gw_scatter((int)h->Q_max, h->d_q_total, 2 * ((F + 255) / 256), h->gw_part.p, h->epd_src.p, h->in_tok.p,
-                      h->epd_j.p, k, g_weights, st);
+}
+
+// backward_vjps across ranks (world_size == N_d; backward.cpp:24-161 with
+// the two reverse exchanges made real): the upstream rows go out along the
+// forward's dispatch layout (the combine adjoint, backward.cpp:43-54: every
+// Sfd row gets its token's upstream row; gathered per device, :74-78), the
+// expert-side adjoints run on this rank's saved Epd grouping, each inbox
+// row's scatter-adjoint partial sum (over its local experts, placement order)
+// and its routing-weight gradients go back along the return layout (:136-139),
+// and the source sums them per token over devices ascending (dispatch
+// adjoint, :143-152).  Exchanges over the handle's transport (NCCL, the
+// host-callback transport or loopback ranks).
+static occ_status backward_multi(occ_handle* h, const __nv_bfloat16* up, void* g_x, float* g_w1, float* g_w3,
+                                 float* g_w2, float* g_weights, cudaStream_t st) {
+    if (!h->tp) return fail(OCC_ERR_STATE, "backward: world_size > 1 needs a communicator");
+    Transport* tp = h->tp;
+    const int n = h->last_n, k = h->k, P = h->P, D = h->D, F = h->F, nd = h->nd, r = h->rank, dedup = h->cfg.dedup;
+    occ_status s = ensure_bwd(h);
+    if (s != OCC_OK) return s;
+    // the forward's exchange layout (its counts are still on the device)
+    std::vector<int> hC((size_t)nd * nd);
+    CUDA_TRY(cudaMemcpyAsync(hC.data(), h->dofs.C, sizeof(int) * nd * nd, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    std::vector<int64_t> off(nd), scnt(nd), inoff(nd), rcnt(nd);
+    occ_exchange_layout(hC.data(), nd, r, off.data(), scnt.data(), inoff.data(), rcnt.data());
+    std::vector<size_t> so(nd), sc(nd), ro(nd), rc(nd);
+    size_t R = 0, S = 0;
+    for (int p = 0; p < nd; ++p) {
+        so[p] = (size_t)off[p], sc[p] = (size_t)scnt[p], ro[p] = (size_t)inoff[p], rc[p] = (size_t)rcnt[p];
+        R += rc[p];
+        S += sc[p];
+    }
+    const size_t Rb = std::max<size_t>(h->R_max, 1), Sb = std::max<size_t>(S, 1);
+    CUDA_TRY(h->g_in.ensure(Rb * D));
+    CUDA_TRY(h->g_ysrc.ensure(Sb * D));
+    CUDA_TRY(h->ret_gw.ensure(Rb * k));
+    CUDA_TRY(h->y_gw.ensure(Sb * k));
+    // 1. combine adjoint: this source's upstream rows into its Sfd send batch
+    PackArgs pk{n, k, nd, D, dedup, up, nullptr, nullptr, h->mask.p, h->tok_row.p, h->snd_x.p, nullptr, nullptr};
+    launch_pack(pk, st);
+    if ((s = tp->alltoallv(h->snd_x.p, so, sc, h->g_in.p, ro, rc, D * 2, st)) != OCC_OK) return s;
+    // 2. expert-side adjoints over the received rows (the forward's BRIM1 / Epd grouping)
+    const int Rm = (int)std::max<size_t>(R, 1);
+    if (R > 0) {
+        launch_scatter_rows(Rm, h->d_R, P, D, h->g_in.p, nullptr, h->row_epd.p, P, h->cofs, h->g_epd.p, st);
+        bwd_gemms(h, P, h->d_widx.p, g_w1, g_w3, g_w2, st);
+        // scatter adjoint summed over the row's local experts -> return payload
+        launch_partial_combine(Rm, h->d_R, P, D, h->row_epd.p, h->y16.p, h->ret.p, st);
+        CUDA_TRY(cudaMemsetAsync(h->ret_gw.p, 0, sizeof(float) * R * k, st));
+        launch_gw_scatter((int)h->Q_max, h->d_q_total, 2 * ((F + 255) / 256), h->gw_part.p, h->epd_src.p, nullptr,
+                          h->epd_j.p, k, h->ret_gw.p, st);
+    }
+    // 3. reverse exchange back into the sources' Sfd slots
+    if ((s = tp->alltoallv(h->ret.p, ro, rc, h->g_ysrc.p, so, sc, D * 2, st)) != OCC_OK) return s;
+    if ((s = tp->alltoallv(h->ret_gw.p, ro, rc, h->y_gw.p, so, sc, k * 4, st)) != OCC_OK) return s;
+    // 4. dispatch adjoint at the source
+    launch_combine_back(n, nd, k, dedup, D, h->mask.p, h->tok_row.p, h->g_ysrc.p, h->y_gw.p, g_x, h->gx_bf16,
+                        g_weights, st);
     CUDA_TRY(cudaGetLastError());
     if (h->validate) CUDA_TRY(cudaStreamSynchronize(st));
     return OCC_OK;
 }
+
+extern "C" {
 
 occ_status occ_set_profiling(occ_handle* h, int on) {
     if (!h) return fail(OCC_ERR_ARG, "null handle");

@@ -162,6 +162,21 @@ void launch_partial_combine(int R_max, const int* R_total, int P, int D, const i
 void launch_combine(int n, int nd, int k, int dedup, int D, const uint64_t* mask, const int32_t* tok_row,
                     const __nv_bfloat16* ret, const __nv_bfloat16* ys, __nv_bfloat16* out, cudaStream_t st);
 
+// Stage-level entry points: dispatch of one source from its BRIM0 (N_d x n)
+// into Sfd rows, and the combine of returned Sfd rows through BRIM0.
+void launch_dispatch_sfd(int n, int nd, int k, int D, const __nv_bfloat16* x, const int32_t* ids, const float* w,
+                         const int32_t* brim0, __nv_bfloat16* sfd_x, int32_t* sfd_ids, float* sfd_w, int32_t* sfd_tok,
+                         cudaStream_t st);
+void launch_combine_brim0(int n, int nd, int D, const int32_t* brim0, const __nv_bfloat16* y, __nv_bfloat16* out,
+                          cudaStream_t st);
+void launch_set_int(int* p, int v, cudaStream_t st);
+// world_size > 1 backward: token gradient (f32 or bf16) and routing-weight
+// gradients summed over a token's returned rows (devices ascending).
+void launch_combine_back(int n, int nd, int k, int dedup, int D, const uint64_t* mask, const int32_t* tok_row,
+                         const __nv_bfloat16* y, const float* ygw, void* gx, int gx_bf16, float* gw, cudaStream_t st);
+void launch_brim0_one_source(int n, int nd, const uint64_t* mask, const int32_t* tok_sfd, int32_t* brim0,
+                             cudaStream_t st);
+void launch_one_source_totals(int nd, int r, int* totals, cudaStream_t st);
 // world_size == 1: partial combine + return + combine fused (reads Y once).
 void launch_combine_fused(int n, int nd, int k, int P, int dedup, int D, const uint64_t* mask,
                           const int32_t* tok_row, const int32_t* row_epd, const __nv_bfloat16* Y,
@@ -215,6 +230,11 @@ void launch_token_stats(int n, int k, int nd, const int32_t* ids, const int32_t*
 // Routers.
 void launch_gate_scores_f64(const double* x, int n, int d, const double* g, int e, double* s, cudaStream_t st,
                             bool softmax = true);
+// Exact router from bf16 operands: fp64 logits (ascending k, no FMA) + the
+// glibc-exact softmax (gate_scores, routing.cpp:33-52), scores [n, e] f64.
+void launch_gate_scores_bf16_f64(const __nv_bfloat16* x, int n, int d, const __nv_bfloat16* g, int e, double* s,
+                                 cudaStream_t st);
+void launch_f64_to_f32(const double* a, long n, float* b, cudaStream_t st);
 void launch_topk_f64(const double* s, int n, int e, int k, int renorm, int32_t* ids, double* w, int32_t* err,
                      cudaStream_t st);
 struct PruneDev {

@@ -9,6 +9,7 @@
 #include <algorithm>
 
 #include "occ_common.cuh"
+#include "occ_glibc_exp.h"
 #include "occ_internal.h"
 
 namespace occ {
@@ -316,7 +317,7 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs a) {
         }
     }
     // (a token's naive rows are all kept or all dropped, so row q carries slot q)
-    for (int q = 0; q < nrows; ++q) {
+    for (int q = 0; a.dst_ids && q < nrows; ++q) {
         for (int j = lane; j < a.k; j += 32) {
             const long di = (long)rows[q] * a.k + j;
             const bool keep = a.dedup || j == q;  // naive rows carry only their own expert
@@ -592,6 +593,154 @@ __global__ void __launch_bounds__(256) combine_kernel(int n, int nd, int k, int 
     }
     __syncwarp();
     sum_rows_ordered<KU>(ret, qs, nr, D, lane, ys ? ys + (long)t * D : nullptr, out + (long)t * D);
+}
+
+// ------------------------------------------------- stage-level entry points --
+// dispatch (pipeline.cpp:91-123) of one source's tokens from its BRIM0
+// (N_d x n, device-major counters): Sfd row c = BRIM0[d, i] >= 0 receives x
+// row i, the full routing row and the token index.  One warp per token: the
+// x row is read once (16-byte vectors) and stored to each of its Sfd rows.
+__global__ void __launch_bounds__(256) dispatch_sfd_kernel(int n, int nd, int k, int D, const __nv_bfloat16* x,
+                                                           const int32_t* ids, const float* w, const int32_t* brim0,
+                                                           __nv_bfloat16* sfd_x, int32_t* sfd_ids, float* sfd_w,
+                                                           int32_t* sfd_tok) {
+    __shared__ int s_c[8][kMaxDev];
+    const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (i >= n) return;
+    int* cs = s_c[threadIdx.x >> 5];
+    int nc = 0;
+    for (int d0 = 0; d0 < nd; d0 += 32) {
+        const int d = d0 + lane;
+        const int c = d < nd ? brim0[(long)d * n + i] : -1;
+        const uint32_t b = __ballot_sync(0xffffffffu, c >= 0);
+        if (c >= 0) cs[nc + __popc(b & ((1u << lane) - 1u))] = c;
+        nc += __popc(b);
+    }
+    __syncwarp();
+    const int nv = D / 8;
+    const uint4* src = reinterpret_cast<const uint4*>(x + (long)i * D);
+    for (int v = lane; v < nv; v += 32) {
+        const uint4 u = __ldg(src + v);
+        for (int j = 0; j < nc; ++j) reinterpret_cast<uint4*>(sfd_x + (long)cs[j] * D)[v] = u;
+    }
+    for (int j = 0; j < nc; ++j) {
+        const long c = cs[j];
+        for (int q = lane; q < k; q += 32) {
+            sfd_ids[c * k + q] = ids[(long)i * k + q];
+            sfd_w[c * k + q] = w[(long)i * k + q];
+        }
+        if (lane == 0) sfd_tok[c] = i;
+    }
+}
+
+// combine (pipeline.cpp:285-300) from BRIM0: Ori row i = bf16( sum over
+// devices ascending of returned Sfd row BRIM0[d, i] ), fp32 accumulation.
+template <int KU>
+__global__ void __launch_bounds__(256) combine_brim0_kernel(int n, int nd, int D, const int32_t* brim0,
+                                                            const __nv_bfloat16* y, __nv_bfloat16* out) {
+    __shared__ int s_q[8][kMaxDev];
+    const int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (i >= n) return;
+    int* qs = s_q[threadIdx.x >> 5];
+    int nq = 0;
+    for (int d0 = 0; d0 < nd; d0 += 32) {
+        const int d = d0 + lane;
+        const int c = d < nd ? brim0[(long)d * n + i] : -1;
+        const uint32_t b = __ballot_sync(0xffffffffu, c >= 0);
+        if (c >= 0) qs[nq + __popc(b & ((1u << lane) - 1u))] = c;
+        nq += __popc(b);
+    }
+    __syncwarp();
+    sum_rows_ordered<KU>(y, qs, nq, D, lane, nullptr, out + (long)i * D);
+}
+
+__global__ void set_int_kernel(int* p, int v) { *p = v; }
+
+// world_size > 1 backward, dispatch adjoint at the source (backward.cpp:143-152):
+// g_x[t] = sum over the token's returned rows (devices ascending) of the
+// scatter-adjoint partial sums, and g_weights[t, j] = sum over the same rows
+// of their routing-weight gradients (exactly one row holds slot j), fp32.
+template <class OutT>
+__global__ void __launch_bounds__(256) combine_back_kernel(int n, int nd, int k, int dedup, int D,
+                                                           const uint64_t* mask, const int32_t* tok_row,
+                                                           const __nv_bfloat16* y, const float* ygw, OutT* gx,
+                                                           float* gw) {
+    __shared__ int s_q[8][kMaxTopK > kMaxDev ? kMaxTopK : kMaxDev];
+    const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (t >= n) return;
+    int* qs = s_q[threadIdx.x >> 5];
+    int nr = 0;
+    const uint32_t lt = (1u << lane) - 1u;
+    if (dedup) {
+        const uint64_t m = mask[t];
+        for (int d0 = 0; d0 < nd; d0 += 32) {
+            const int d = d0 + lane;
+            const int rr = d < nd && ((m >> d) & 1) ? tok_row[(long)t * nd + d] : -1;
+            const uint32_t b = __ballot_sync(0xffffffffu, rr >= 0);
+            if (rr >= 0) qs[nr + __popc(b & lt)] = rr;
+            nr += __popc(b);
+        }
+    } else {
+        for (int j0 = 0; j0 < k; j0 += 32) {
+            const int j = j0 + lane;
+            const int rr = j < k && mask[(long)t * k + j] ? tok_row[(long)t * k + j] : -1;
+            const uint32_t b = __ballot_sync(0xffffffffu, rr >= 0);
+            if (rr >= 0) qs[nr + __popc(b & lt)] = rr;
+            nr += __popc(b);
+        }
+    }
+    __syncwarp();
+    for (int v = lane; v < D / 8; v += 32) {
+        float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int i = 0; i < nr; ++i) {
+            const uint4 u = __ldg(reinterpret_cast<const uint4*>(y + (long)qs[i] * D) + v);
+            const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const float2 f = __bfloat1622float2(hh[e]);
+                acc[2 * e] += f.x;
+                acc[2 * e + 1] += f.y;
+            }
+        }
+        if constexpr (sizeof(OutT) == 4) {
+            float4* o = reinterpret_cast<float4*>(gx + (long)t * D) + 2 * v;
+            o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+            o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+        } else {
+            uint4 o;
+            o.x = pack_bf16(acc[0], acc[1]);
+            o.y = pack_bf16(acc[2], acc[3]);
+            o.z = pack_bf16(acc[4], acc[5]);
+            o.w = pack_bf16(acc[6], acc[7]);
+            reinterpret_cast<uint4*>(gx + (long)t * D)[v] = o;
+        }
+    }
+    for (int j = lane; j < k; j += 32) {
+        float s = 0.f;
+        for (int i = 0; i < nr; ++i) s += ygw[(long)qs[i] * k + j];
+        gw[(long)t * k + j] = s;
+    }
+}
+
+// One source's BRIM0 (world_size > 1: this rank's tokens) from the plan:
+// brim0[d, t] = counter of token t on device d, or -1.
+__global__ void brim0_one_source_kernel(int n, int nd, const uint64_t* mask, const int32_t* tok_sfd, int32_t* brim0) {
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= (long)n * nd) return;
+    const int d = (int)(i / n), t = (int)(i % n);
+    brim0[i] = ((mask[t] >> d) & 1) ? tok_sfd[(long)t * nd + d] : -1;
+}
+
+// Rank-key totals of one source (row 0, from a G = 1 count) moved to row r,
+// every other source's row zero: the local dispatch plan of rank r.
+__global__ void one_source_totals_kernel(int nd, int r, int* totals) {
+    __shared__ int row[kMaxDev + 1];
+    for (int d = threadIdx.x; d <= nd; d += blockDim.x) row[d] = totals[d];
+    __syncthreads();
+    for (int i = threadIdx.x; i < nd * (nd + 1); i += blockDim.x) totals[i] = i / (nd + 1) == r ? row[i % (nd + 1)] : 0;
 }
 
 // world_size == 1: intra-device partial combine + return + combine in one
@@ -949,7 +1098,7 @@ __global__ void gw_scatter_kernel(int Q_max, const int* q_total, int NB, const f
     if (r < 0) return;
     float s = 0.f;
     for (int b = 0; b < NB; ++b) s += gw_part[(long)q * NB + b];
-    g_weights[(long)in_tok[r] * k + epd_j[q]] = s;
+    g_weights[(long)(in_tok ? in_tok[r] : r) * k + epd_j[q]] = s;  // in_tok null: per inbox row
 }
 
 // ------------------------------------------------------------- histogram --
@@ -1070,10 +1219,50 @@ __global__ void softmax_f64_kernel(int n, int e, double* s) {
     for (int j = 1; j < e; ++j) mx = row[j] > mx ? row[j] : mx;
     double sum = 0.0;
     for (int j = 0; j < e; ++j) {
-        row[j] = exp(__dsub_rn(row[j], mx));
+        row[j] = occ::glibc_exp::exp(__dsub_rn(row[j], mx));  // std::exp of routing.cpp:44, bit for bit
         sum = __dadd_rn(sum, row[j]);
     }
     for (int j = 0; j < e; ++j) row[j] = __ddiv_rn(row[j], sum);
+}
+
+// Exact router from the production bf16 operands: the reference's
+// gate_scores logits (tiled_matmul in Precision::Double, matrix.cpp:25-31:
+// per output, products added in ascending k, no FMA) of the bf16 tokens and
+// gate widened exactly to double.  Tile: 32 tokens x 8 experts per block,
+// 64-deep k slices staged in shared memory; each thread keeps the strict
+// sequential k order of its own (token, expert) sum.
+constexpr int kLgT = 32, kLgE = 8, kLgK = 64;
+__global__ void __launch_bounds__(kLgT * kLgE) gate_logits_bf16_f64_kernel(const __nv_bfloat16* __restrict__ x, int n,
+                                                                          int d, const __nv_bfloat16* __restrict__ g,
+                                                                          int e, double* __restrict__ s) {
+    __shared__ double xs[kLgT][kLgK + 1];
+    __shared__ double gs[kLgE][kLgK + 1];
+    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * kLgT + tx;
+    const int t0 = blockIdx.x * kLgT, e0 = blockIdx.y * kLgE;
+    double acc = 0.0;
+    for (int k0 = 0; k0 < d; k0 += kLgK) {
+        for (int i = tid; i < kLgT * kLgK; i += kLgT * kLgE) {
+            const int r = i / kLgK, c = i % kLgK;
+            const int t = t0 + r, kk = k0 + c;
+            xs[r][c] = (t < n && kk < d) ? (double)__bfloat162float(x[(long)t * d + kk]) : 0.0;
+        }
+        for (int i = tid; i < kLgE * kLgK; i += kLgT * kLgE) {
+            const int r = i / kLgK, c = i % kLgK;
+            const int j = e0 + r, kk = k0 + c;
+            gs[r][c] = (j < e && kk < d) ? (double)__bfloat162float(g[(long)j * d + kk]) : 0.0;
+        }
+        __syncthreads();
+        const int kn = min(kLgK, d - k0);
+        for (int c = 0; c < kn; ++c) acc = __dadd_rn(acc, __dmul_rn(xs[tx][c], gs[ty][c]));
+        __syncthreads();
+    }
+    const int t = t0 + tx, j = e0 + ty;
+    if (t < n && j < e) s[(long)t * e + j] = acc;
+}
+
+__global__ void f64_to_f32_kernel(const double* a, long n, float* b) {
+    const long i = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) b[i] = (float)a[i];
 }
 
 template <class T>
@@ -1443,6 +1632,56 @@ void launch_combine(int n, int nd, int k, int dedup, int D, const uint64_t* mask
     count_launch();
 }
 
+void launch_dispatch_sfd(int n, int nd, int k, int D, const __nv_bfloat16* x, const int32_t* ids, const float* w,
+                         const int32_t* brim0, __nv_bfloat16* sfd_x, int32_t* sfd_ids, float* sfd_w, int32_t* sfd_tok,
+                         cudaStream_t st) {
+    if (!n) return;
+    dispatch_sfd_kernel<<<(n + 7) / 8, 256, 0, st>>>(n, nd, k, D, x, ids, w, brim0, sfd_x, sfd_ids, sfd_w, sfd_tok);
+    count_launch();
+}
+
+void launch_combine_brim0(int n, int nd, int D, const int32_t* brim0, const __nv_bfloat16* y, __nv_bfloat16* out,
+                          cudaStream_t st) {
+    if (!n) return;
+    if (nd <= 2)
+        combine_brim0_kernel<2><<<(n + 7) / 8, 256, 0, st>>>(n, nd, D, brim0, y, out);
+    else if (nd <= 4)
+        combine_brim0_kernel<4><<<(n + 7) / 8, 256, 0, st>>>(n, nd, D, brim0, y, out);
+    else
+        combine_brim0_kernel<8><<<(n + 7) / 8, 256, 0, st>>>(n, nd, D, brim0, y, out);
+    count_launch();
+}
+
+void launch_brim0_one_source(int n, int nd, const uint64_t* mask, const int32_t* tok_sfd, int32_t* brim0,
+                             cudaStream_t st) {
+    const long total = (long)n * nd;
+    if (!total) return;
+    brim0_one_source_kernel<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(n, nd, mask, tok_sfd, brim0);
+    count_launch();
+}
+
+void launch_one_source_totals(int nd, int r, int* totals, cudaStream_t st) {
+    one_source_totals_kernel<<<1, 256, 0, st>>>(nd, r, totals);
+    count_launch();
+}
+
+void launch_combine_back(int n, int nd, int k, int dedup, int D, const uint64_t* mask, const int32_t* tok_row,
+                         const __nv_bfloat16* y, const float* ygw, void* gx, int gx_bf16, float* gw, cudaStream_t st) {
+    if (!n) return;
+    if (gx_bf16)
+        combine_back_kernel<__nv_bfloat16><<<(n + 7) / 8, 256, 0, st>>>(n, nd, k, dedup, D, mask, tok_row, y, ygw,
+                                                                         reinterpret_cast<__nv_bfloat16*>(gx), gw);
+    else
+        combine_back_kernel<float><<<(n + 7) / 8, 256, 0, st>>>(n, nd, k, dedup, D, mask, tok_row, y, ygw,
+                                                                 reinterpret_cast<float*>(gx), gw);
+    count_launch();
+}
+
+void launch_set_int(int* p, int v, cudaStream_t st) {
+    set_int_kernel<<<1, 1, 0, st>>>(p, v);
+    count_launch();
+}
+
 void launch_combine_fused(int n, int nd, int k, int P, int dedup, int D, const uint64_t* mask,
                           const int32_t* tok_row, const int32_t* row_epd, const __nv_bfloat16* Y,
                           const __nv_bfloat16* ys, __nv_bfloat16* out, cudaStream_t st) {
@@ -1558,6 +1797,22 @@ void launch_gate_scores_f64(const double* x, int n, int d, const double* g, int 
     count_launch();
     if (!softmax) return;
     softmax_f64_kernel<<<(n + 127) / 128, 128, 0, st>>>(n, e, s);
+    count_launch();
+}
+
+void launch_gate_scores_bf16_f64(const __nv_bfloat16* x, int n, int d, const __nv_bfloat16* g, int e, double* s,
+                                 cudaStream_t st) {
+    if (!n) return;
+    dim3 grid((n + kLgT - 1) / kLgT, (e + kLgE - 1) / kLgE);
+    gate_logits_bf16_f64_kernel<<<grid, dim3(kLgT, kLgE), 0, st>>>(x, n, d, g, e, s);
+    count_launch();
+    softmax_f64_kernel<<<(n + 127) / 128, 128, 0, st>>>(n, e, s);
+    count_launch();
+}
+
+void launch_f64_to_f32(const double* a, long n, float* b, cudaStream_t st) {
+    if (!n) return;
+    f64_to_f32_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(a, n, b);
     count_launch();
 }
 

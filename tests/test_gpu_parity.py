@@ -87,11 +87,76 @@ def test_gate_scores_f64():
     x, g, *_ = O.synthetic_layer(21, 300, 48, 8, 16, single=False)
     s = occ.gate_scores_f64(cuda(x), cuda(g)).cpu().numpy()
     rs = ref().gate_scores(x, g)
-    # logits are bit-exact (sequential, FMA-free); exp may differ from glibc by an ulp
-    assert np.max(np.abs(s - rs) / rs) < 1e-14
+    # logits sequential and FMA-free, softmax with the port of glibc's exp:
+    # the scores are the reference's doubles bit for bit
+    assert np.array_equal(s, rs)
     ids, _ = occ.topk_route(cuda(s), 4)
     ri, _ = ref().topk_route(rs, 4)
     assert np.array_equal(ids.cpu().numpy(), ri)
+
+
+# (E, k, N_d, D, tokens, prune): C1, OLMoE at its full 65,536 tokens, Qwen-like
+# 60 experts with router-score and similarity pruning to <= 2 devices.
+EXACT_ROUTER_CASES = [(8, 2, 2, 512, 2048, None), (64, 8, 8, 2048, 65536, None),
+                      (60, 4, 4, 2048, 4096, ("router", 2)), (60, 4, 4, 2048, 4096, ("similarity", 2)),
+                      (64, 6, 8, 2048, 4096, ("router", 3))]
+
+
+@pytest.mark.parametrize("ne,k,nd,dm,n,prune", EXACT_ROUTER_CASES)
+def test_exact_router_bit_exact_from_raw_x(ne, k, nd, dm, n, prune):
+    """forward_expert_parallel's routing (pipeline.cpp:509-512) from the raw
+    bf16 tokens and gate: occ_route_exact's ids, fp64 weights and fp64 softmax
+    scores equal gate_scores + topk_route (+ prune_routing) of the reference
+    compiled from its own sources, bit for bit (routing.cpp:33-84,
+    pruning.cpp:141-163)."""
+    x, g, *_ = make_layer_inputs(17 + ne, n, dm, 8, ne)
+    plist = np.random.default_rng(ne).permutation(ne).reshape(nd, ne // nd).astype(np.int32)
+    layer = occ.ExpertParallelLayer(occ.MoEConfig(ne, k, nd, dm, 64),
+                                    occ.Placement([list(map(int, r)) for r in plist]))
+    R = ref()
+    rs = R.gate_scores(x, g)
+    ri, rw = R.topk_route(rs, k)
+    spec = None
+    if prune is not None:
+        mode, budget = prune
+        sim = None
+        if mode == "similarity":
+            sim = R.similarity_table(x[:512] @ g.T)[0]
+            spec = occ.PruneSpec(mode, budget, table=sim)
+        else:
+            spec = occ.PruneSpec(mode, budget)
+        ri, rw = R.prune_routing(rs, ri, rw, plist, mode, budget, sim_values=sim)
+    ids, w, sc = layer.route_exact(cuda(x, torch.bfloat16), cuda(g, torch.bfloat16), prune=spec, want_scores=True)
+    assert np.array_equal(sc.cpu().numpy(), rs)
+    assert np.array_equal(ids.cpu().numpy(), ri)
+    assert np.array_equal(w.cpu().numpy(), rw)
+    # the layer's exact router mode routes with exactly these ids (weights in f32)
+    layer.set_router_mode("exact")
+    ids2, w2 = layer.route(cuda(x, torch.bfloat16), cuda(g, torch.bfloat16), prune=spec)
+    assert np.array_equal(ids2.cpu().numpy(), ri)
+    assert np.array_equal(w2.cpu().numpy(), rw.astype(np.float32))
+
+
+def test_forward_expert_parallel_exact_router_vs_reference():
+    """forward_expert_parallel (pipeline.cpp:503-517) end to end in the exact
+    router mode at the C1 shape, against the reference's own
+    forward_expert_parallel-equivalent (gate_scores + topk_route +
+    forward_given_routing): identical CommReport (it depends only on the
+    bit-exact routing) and outputs within the bf16 tolerance."""
+    ne, k, nd, dm, dh, n = 8, 2, 2, 512, 1024, 512
+    x, g, w1, w2, _ = make_layer_inputs(1, n, dm, dh, ne)
+    layer = occ.ExpertParallelLayer(occ.MoEConfig(ne, k, nd, dm, dh, activation="silu"))
+    layer.load_experts(cuda(w1, torch.bfloat16), cuda(w2, torch.bfloat16))
+    layer.set_router_mode("exact")
+    out = layer.forward_expert_parallel(cuda(x, torch.bfloat16), cuda(g, torch.bfloat16))
+    R = ref()
+    ri, rw = R.topk_route(R.gate_scores(x, g), k)
+    want, rep = R.forward_given_routing(x, ri, rw, w1, w2, np.arange(ne, dtype=np.int32).reshape(nd, -1),
+                                        act="silu", single=False, bytes_per_scalar=2)
+    got_rep = layer.comm_report(bytes_per_scalar=2)
+    assert got_rep.mean_replicas == rep.mean_replicas
+    assert got_rep.cross_device_bytes == rep.cross_device_bytes
+    assert rel_err(out.double().cpu().numpy(), want) <= TOL
 
 
 def test_production_router_matches_reference_ids():
@@ -1187,3 +1252,117 @@ def test_api_rejects_wrong_dtypes_and_shapes():
     xt = torch.empty((dm, n), dtype=torch.bfloat16, device="cuda").t()
     xt.copy_(xb)
     assert torch.equal(layer.forward_expert_parallel(xt, gb), layer.forward_expert_parallel(xb, gb))
+
+
+STAGE_CASES = [(8, 2, 2, 256, 512, "silu", 700), (16, 4, 4, 128, 256, "swiglu", 1000),
+               (64, 8, 8, 512, 256, "relu", 900), (8, 3, 1, 128, 128, "identity", 64)]
+
+
+@pytest.mark.parametrize("ne,k,nd,dm,dh,act,n", STAGE_CASES)
+def test_stage_entry_points_chain_equals_forward(ne, k, nd, dm, dh, act, n):
+    """The stage-level C-ABI (pipeline.hpp:89-123) driven by the caller with
+    its own exchange (torch indexing by the occ_exchange_layout offsets):
+    build_dispatch_index -> dispatch (SfdBatch, pipeline.cpp:91-123) ->
+    all_to_all_exchange (:125-176) -> build_compute_index (:52-89) +
+    expert compute (:178-283) -> return exchange (:456-466) -> combine
+    (:285-300).  The SfdBatch token map, the inbox order (source asc, counter
+    asc) and BRIM1 equal the reference's own records; the chained output
+    equals the fused occ_forward bit for bit (and so the reference within
+    1e-2)."""
+    gated = act == "swiglu"
+    x, g, w1, w2, w3 = make_layer_inputs(ne + k + n, n, dm, dh, ne, gated=gated)
+    ids, w = random_routing(n, ne, k, np.random.default_rng(n + 1))
+    w32 = w.astype(np.float32)
+    plist = _placement(ne, nd, "shuffled", seed=11)
+    src = np.random.default_rng(n).integers(0, nd, n).astype(np.int32)
+    layer = occ.ExpertParallelLayer(occ.MoEConfig(ne, k, nd, dm, dh, activation=act),
+                                    occ.Placement([list(map(int, p)) for p in plist]))
+    layer.load_experts(cuda(w1, torch.bfloat16), cuda(w2, torch.bfloat16),
+                       cuda(w3, torch.bfloat16) if gated else None)
+    X, I, Wt, S = cuda(x, torch.bfloat16), cuda(ids), cuda(w32), cuda(src)
+    want = layer.forward_given_routing(X, I, Wt, S)
+    # reference records (indices are width-independent: a width-1 replay, SURVEY 8(c))
+    _, _, ridx = ref().forward_given_routing(x[:, :1], ids, w32.astype(np.float64), w1[:, :1, :1], w2[:, :1, :1],
+                                             plist, src, act="identity", single=False, want_index=True)
+    brim0_all, counts = layer.build_dispatch_index(I, S)
+    C = counts.cpu().numpy()
+    pos, sfd = 0, []
+    for s in range(nd):
+        tok = np.nonzero(src == s)[0]
+        b = brim0_all[pos:pos + nd * len(tok)]
+        pos += nd * len(tok)
+        assert np.array_equal(b.cpu().numpy().reshape(nd, len(tok)), ridx["dindex"][s])
+        tt = cuda(tok.astype(np.int64))
+        sx, si, sw, st = layer.dispatch(X[tt], I[tt], Wt[tt], b, n_sfd=int(C[s].sum()))
+        # SfdBatch token map: Sfd row c holds the token whose counter is c
+        want_tok = np.full(int(C[s].sum()), -1)
+        bb = ridx["dindex"][s]
+        for d in range(nd):
+            for i in range(len(tok)):
+                if bb[d, i] >= 0:
+                    want_tok[bb[d, i]] = i
+        assert np.array_equal(st.cpu().numpy(), want_tok)
+        sfd.append((sx, si, sw, b, tt))
+    # the caller's exchange: destination d receives, source asc, the contiguous
+    # rows each source's device-major batch holds for it
+    rets = {}
+    for d in range(nd):
+        parts, meta = [], []
+        for s in range(nd):
+            off = int(C[s, :d].sum())
+            parts.append((sfd[s][0][off:off + C[s, d]], sfd[s][1][off:off + C[s, d]], sfd[s][2][off:off + C[s, d]]))
+            meta.append((s, off, int(C[s, d])))
+        in_x = torch.cat([p[0] for p in parts])
+        in_i = torch.cat([p[1] for p in parts])
+        in_w = torch.cat([p[2] for p in parts])
+        rinbox = ridx["inbox"][d]
+        got_src = np.concatenate([np.full(c, s) for s, _, c in meta]).astype(np.int64)
+        got_slot = np.concatenate([np.arange(o, o + c) for _, o, c in meta]).astype(np.int64)
+        assert np.array_equal(got_src, rinbox[1]) and np.array_equal(got_slot, rinbox[2])
+        cix, nepd = layer.build_compute_index(d, in_i, in_w)
+        assert np.array_equal(cix.cpu().numpy(), ridx["cindex"][d]) and nepd == int((ridx["cindex"][d] >= 0).sum())
+        y = layer.expert_compute(d, in_x, in_i, in_w)
+        r0 = 0
+        for s, off, c in meta:
+            rets[(s, d)] = (off, y[r0:r0 + c])
+            r0 += c
+    out = torch.empty_like(X)
+    for s in range(nd):
+        ns = int(C[s].sum())
+        y_src = torch.empty((ns, dm), dtype=torch.bfloat16, device="cuda")
+        for d in range(nd):
+            off, rows = rets[(s, d)]
+            y_src[off:off + rows.shape[0]] = rows
+        out[sfd[s][4]] = layer.combine(y_src, sfd[s][3], sfd[s][4].shape[0])
+    assert torch.equal(out, want)
+
+
+def test_stage_entry_points_world_gt1_handle():
+    """On a world_size > 1 handle (no communicator needed: the stages never
+    communicate) the local BRIM0 of this rank's tokens equals the reference's
+    per-source dispatch index, and expert_compute runs this rank's experts."""
+    ne, k, nd, dm, dh, n = 16, 4, 4, 128, 256, 300
+    x, g, w1, w2, _ = make_layer_inputs(77, n, dm, dh, ne)
+    ids, w = random_routing(n, ne, k, np.random.default_rng(5))
+    plist = _placement(ne, nd, "shuffled", seed=2)
+    _, _, ridx = ref().forward_given_routing(x[:, :1], ids, w, w1[:, :1, :1], w2[:, :1, :1], plist,
+                                             np.full(n, 2, np.int32), act="identity", single=False, want_index=True)
+    rank = 2
+    h = occ.ExpertParallelLayer(occ.MoEConfig(ne, k, nd, dm, dh, activation="silu"),
+                                occ.Placement([list(map(int, p)) for p in plist]), world_size=nd, rank=rank)
+    P = ne // nd
+    h.load_experts(cuda(w1[plist[rank]], torch.bfloat16), cuda(w2[plist[rank]], torch.bfloat16))
+    b, cnt = h.build_dispatch_index(cuda(ids))
+    assert np.array_equal(b.cpu().numpy().reshape(nd, n), ridx["dindex"][rank])
+    assert np.array_equal(cnt.cpu().numpy(), (ridx["dindex"][rank] >= 0).sum(1))
+    # expert compute of this rank on the rows routed to it, vs a world_size 1 handle's device `rank`
+    sx, si, sw, _ = h.dispatch(cuda(x, torch.bfloat16), cuda(ids), cuda(w.astype(np.float32)), b)
+    off = int(cnt[:rank].sum())
+    rows = slice(off, off + int(cnt[rank]))
+    y = h.expert_compute(rank, sx[rows], si[rows], sw[rows])
+    one = occ.ExpertParallelLayer(occ.MoEConfig(ne, k, nd, dm, dh, activation="silu"),
+                                  occ.Placement([list(map(int, p)) for p in plist]))
+    one.load_experts(cuda(w1, torch.bfloat16), cuda(w2, torch.bfloat16))
+    assert torch.equal(y, one.expert_compute(rank, sx[rows], si[rows], sw[rows]))
+    with pytest.raises(occ.ConfigError):
+        h.expert_compute(0, sx[rows], si[rows], sw[rows])

@@ -196,3 +196,38 @@ def test_shared_experts_oracle_vs_torch(gated, gate, act):
         acc *= torch.sigmoid(T(x) @ T(g))[:, None]
     want = base + acc.numpy()
     assert np.max(np.abs(got - want)) / np.max(np.abs(want)) < 1e-12
+
+
+@pytest.mark.parametrize("gated,act,shared,gate", [(True, "silu", 0, False), (False, "silu", 0, False),
+                                                   (False, "relu", 2, False), (True, "silu", 2, True)])
+def test_dense_rows_bf16_equals_scalar_restatement(gated, act, shared, gate):
+    """orc_dense_rows_bf16 (the sampled-row value oracle of the BASELINE-size
+    GPU tests: bf16 storage in, rows batched per expert) computes exactly the
+    doubles of orc_dense_given_routing + orc_shared_experts (Precision::Double,
+    pipeline.cpp:542-562) on the same bf16-representable inputs."""
+    import torch
+    n, dm, dh, ne, k, dhs = 40, 32, 48, 8, 3, 24
+    rng = np.random.default_rng(7)
+    bf = lambda a: torch.tensor(a, dtype=torch.float32).to(torch.bfloat16)
+    x, w1, w2 = bf(rng.uniform(-1, 1, (n, dm))), bf(rng.uniform(-1, 1, (ne, dm, dh)) / 6), bf(rng.uniform(-1, 1, (ne, dh, dm)) / 7)
+    w3 = bf(rng.uniform(-1, 1, (ne, dm, dh)) / 6) if gated else None
+    ids = np.stack([rng.permutation(ne)[:k] for _ in range(n)]).astype(np.int32)
+    w = rng.uniform(0.1, 1, (n, k)).astype(np.float32)
+    rows = np.array([0, 5, 7, 8, 13, 21, 22, 39], np.int32)
+    sh = None
+    if shared:
+        sh = {"w1": bf(rng.uniform(-1, 1, (shared, dm, dhs)) / 6), "w2": bf(rng.uniform(-1, 1, (shared, dhs, dm)) / 5),
+              "w3": bf(rng.uniform(-1, 1, (shared, dm, dhs)) / 6) if gated else None,
+              "gate": bf(rng.uniform(-1, 1, dm) / 6) if gate else None}
+    got = O.dense_rows_bf16(x, ids, w, w1, w2, rows, act=act, w3=w3, shared=sh, threads=3)
+    d = lambda t: None if t is None else t.double().numpy()
+    P = O.Port()
+    want = P.dense_given_routing(d(x), ids, w.astype(np.float64), d(w1), d(w2), act="silu" if gated else act,
+                                 single=False, rows=rows, w3=d(w3))
+    if sh:
+        full = np.zeros((n, dm))
+        full[rows] = want
+        full = P.shared_experts(d(x), d(sh["w1"]), d(sh["w2"]), w3=d(sh["w3"]), gate=d(sh["gate"]),
+                                act="silu" if gated else act, out=full)
+        want = full[rows]
+    assert np.array_equal(got, want)
