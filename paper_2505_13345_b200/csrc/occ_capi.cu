@@ -238,7 +238,8 @@ struct occ_handle {
     bool peer = false;
     int peer_cap = 0;                  // max tokens per rank per forward
     unsigned long long peer_seq = 0;   // forwards issued (arrival flag value)
-    DevBuf<unsigned long long> flags;  // [2 * world]: dispatch arrivals, return arrivals
+    DevBuf<unsigned long long> flags;  // [3 * world]: dispatch arrivals, return arrivals, count rows
+    DevBuf<int> c_peer;                // [world * world] (source, destination) counts, rows written by the sources
     DevBuf<void*> peer_tab;            // [world * kPeerSlots]
     std::vector<void*> ipc_opened;
     // micro-batching (occ_set_micro_batches): the second half of every
@@ -742,11 +743,16 @@ occ_status check_err(occ_handle* h, cudaStream_t st) {
 
 }  // namespace
 
-__global__ void c_to_totals_kernel(int nd, const int* C, int* totals) {
+__global__ void c_to_totals_kernel(int nd, const int* C, int* totals, int r, int* R_out) {
     // full (source, destination) count matrix -> the rank-key layout s*(nd+1)+d
     for (int i = threadIdx.x; i < nd * (nd + 1); i += blockDim.x) {
         const int s = i / (nd + 1), d = i % (nd + 1);
         totals[i] = d < nd ? C[s * nd + d] : 0;
+    }
+    if (threadIdx.x == 0) {  // rows this device receives
+        int R = 0;
+        for (int s = 0; s < nd; ++s) R += C[s * nd + r];
+        *R_out = R;
     }
 }
 
@@ -779,9 +785,22 @@ occ_status forward_multi(occ_handle* h, const __nv_bfloat16* x, const int32_t* i
     launch_rank_count(items, h->group.p, h->mask.p, 1, nd, ws, st);
     launch_rank_scan(items, 1, nd, ws, st);
     int* C_all = h->c_all.p;
-    s = tp->allgather_counts(h->totals.p, C_all, nd, st);
-    if (s != OCC_OK) return s;
-    c_to_totals_kernel<<<1, 256, 0, st>>>(nd, C_all, h->totals.p);
+    const unsigned long long seq = h->peer ? ++h->peer_seq : 0;
+    void* const* tab = h->peer_tab.p;
+    if (h->peer) {
+        // count all-gather over peer memory: this source's row stored into
+        // every peer's count matrix, then an arrival flag (no collective, no
+        // host round trip: the whole forward stays stream-ordered)
+        C_all = h->c_peer.p;
+        launch_peer_counts(tab, nd, r, h->totals.p, st);
+        launch_peer_signal(tab, nd, r, 2 * nd, seq, st);
+        launch_peer_wait(h->flags.p, nd, 2 * nd, seq, 10000000000LL, h->err.p, st);
+    } else {
+        s = tp->allgather_counts(h->totals.p, C_all, nd, st);
+        if (s != OCC_OK) return s;
+    }
+    // (the received row count of this device, R = sum_s C[s][r], on the device)
+    c_to_totals_kernel<<<1, 256, 0, st>>>(nd, C_all, h->totals.p, r, h->d_R);
     count_launch();
     launch_dispatch_finalize(nd, h->totals.p, h->dofs, st);
     EmitDispatch em{n, k, nd, dedup, ids, weights, nullptr, r, h->d_dev_of.p, h->dofs, 0, h->tok_row.p,
@@ -801,29 +820,30 @@ occ_status forward_multi(occ_handle* h, const __nv_bfloat16* x, const int32_t* i
         if ((s = run_shared(h, x, n, h->s_aux)) != OCC_OK) return s;
         CUDA_TRY(cudaEventRecord(h->ev_join, h->s_aux));
     }
-    // 3. dispatch all-to-all (counts are needed on the host for NCCL)
-    h->h_C.resize((size_t)nd * nd);
-    CUDA_TRY(cudaMemcpyAsync(h->h_C.data(), C_all, sizeof(int) * nd * nd, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
-    std::vector<int64_t> off(nd), scnt64(nd), inoff(nd), rcnt64(nd);
-    occ_exchange_layout(h->h_C.data(), nd, r, off.data(), scnt64.data(), inoff.data(), rcnt64.data());
-    long long R = 0;
-    for (int p = 0; p < nd; ++p) R += rcnt64[p];
-    if (h->peer && R > (long long)h->R_max)  // mapped buffers must not move
-        return fail(OCC_ERR_SHAPE, "peer exchange: received rows exceed the mapped capacity");
-    s = ensure_recv(h, (size_t)std::max<long long>(R, 1), (size_t)std::max<long long>(R, 1) * std::min(k, P));
-    if (s != OCC_OK) return s;
-    h->last_R = (int)R;
-    CUDA_TRY(cudaMemcpyAsync(h->d_R, &h->last_R, sizeof(int), cudaMemcpyHostToDevice, st));
+    // 3. dispatch exchange.  Peer mode: sized by the static bound (at most one
+    // row per (token, device) from each of the N_d sources, fixed when the
+    // buffers were mapped), so the received count stays on the device.  NCCL
+    // / host transports: the counts are needed on the host.
+    long long R = (long long)h->R_max;
     std::vector<size_t> so(nd), sc(nd), ro(nd), rc(nd);
-    for (int p = 0; p < nd; ++p) {
-        so[p] = (size_t)off[p];
-        sc[p] = (size_t)scnt64[p];
-        ro[p] = (size_t)inoff[p];
-        rc[p] = (size_t)rcnt64[p];
+    if (!h->peer) {
+        h->h_C.resize((size_t)nd * nd);
+        CUDA_TRY(cudaMemcpyAsync(h->h_C.data(), C_all, sizeof(int) * nd * nd, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        std::vector<int64_t> off(nd), scnt64(nd), inoff(nd), rcnt64(nd);
+        occ_exchange_layout(h->h_C.data(), nd, r, off.data(), scnt64.data(), inoff.data(), rcnt64.data());
+        R = 0;
+        for (int p = 0; p < nd; ++p) {
+            so[p] = (size_t)off[p];
+            sc[p] = (size_t)scnt64[p];
+            ro[p] = (size_t)inoff[p];
+            rc[p] = (size_t)rcnt64[p];
+            R += rcnt64[p];
+        }
+        s = ensure_recv(h, (size_t)std::max<long long>(R, 1), (size_t)std::max<long long>(R, 1) * std::min(k, P));
+        if (s != OCC_OK) return s;
+        h->last_R = (int)R;
     }
-    const unsigned long long seq = ++h->peer_seq;
-    void* const* tab = h->peer_tab.p;
     if (h->peer) {  // fused dispatch: pack stores into every destination's inbox, then arrival flags
         launch_peer_pack(pk, r, h->d_dev_of.p, h->dofs.off_sd, h->dofs.inoff, tab, st);
         launch_peer_signal(tab, nd, r, 0, seq, st);
@@ -861,7 +881,7 @@ occ_status forward_multi(occ_handle* h, const __nv_bfloat16* x, const int32_t* i
     // 6. intra-device partial combine -> bf16 return payload in inbox order
     mark(h, ST_PCOMBINE, st);
     if (h->peer) {  // fused partial combine + return straight into the sources' buffers
-        launch_peer_return((int)R, nd, r, P, D, h->row_epd.p, h->y16.p, h->dofs.C, h->dofs.off_sd, h->dofs.inoff,
+        launch_peer_return(Rm, h->d_R, nd, r, P, D, h->row_epd.p, h->y16.p, h->dofs.C, h->dofs.off_sd, h->dofs.inoff,
                            tab, st);
         launch_peer_signal(tab, nd, r, nd, seq, st);
         launch_peer_wait(h->flags.p, nd, nd, seq, 10000000000LL, h->err.p, st);
@@ -1105,6 +1125,7 @@ occ_status occ_destroy(occ_handle* h) {
     h->epd_j.release();
     for (void* ptr : h->ipc_opened) cudaIpcCloseMemHandle(ptr);
     h->flags.release();
+    h->c_peer.release();
     h->peer_tab.release();
     for (auto* b : {&h->w13s, &h->w2s, &h->sgate, &h->hs, &h->ys}) b->release();
     h->sw.release();
@@ -2179,10 +2200,13 @@ occ_status occ_comm_enable_peer(occ_handle* h, int max_tokens_per_rank) {
     if (s != OCC_OK) return s;
     s = ensure_recv(h, R_cap, R_cap * std::min(k, P));
     if (s != OCC_OK) return s;
-    CUDA_TRY(h->flags.ensure(2 * nd));
-    CUDA_TRY(cudaMemset(h->flags.p, 0, sizeof(unsigned long long) * 2 * nd));
+    // flags: [0, nd) dispatch arrivals, [nd, 2nd) return arrivals, [2nd, 3nd) count rows
+    CUDA_TRY(h->flags.ensure(3 * nd));
+    CUDA_TRY(cudaMemset(h->flags.p, 0, sizeof(unsigned long long) * 3 * nd));
+    CUDA_TRY(h->c_peer.ensure((size_t)nd * nd));
+    CUDA_TRY(cudaMemset(h->c_peer.p, 0, sizeof(int) * nd * nd));
     CUDA_TRY(cudaDeviceSynchronize());
-    const std::vector<void*> mine{h->in_x.p, h->in_ids.p, h->in_w.p, h->y_src.p, h->flags.p};
+    const std::vector<void*> mine{h->in_x.p, h->in_ids.p, h->in_w.p, h->y_src.p, h->flags.p, h->c_peer.p};
     std::vector<void*> all;
     for (void* ptr : h->ipc_opened) cudaIpcCloseMemHandle(ptr);
     h->ipc_opened.clear();

@@ -199,9 +199,11 @@ void launch_gw_scatter(int Q_max, const int* q_total, int NB, const float* gw_pa
                        const int32_t* in_tok, const int32_t* epd_j, int k, float* g_weights, cudaStream_t st);
 
 // Peer-memory exchange (world_size > 1): every rank's inbox (x, ids, w),
-// returned-row buffer and arrival flags mapped for every rank;
-// peer_tab[p * kPeerSlots + {0 in_x, 1 in_ids, 2 in_w, 3 y_src, 4 flags}].
-constexpr int kPeerSlots = 5;
+// returned-row buffer, arrival flags and count matrix mapped for every rank;
+// peer_tab[p * kPeerSlots + {0 in_x, 1 in_ids, 2 in_w, 3 y_src, 4 flags, 5 counts}].
+constexpr int kPeerSlots = 6;
+// count all-gather: this source's row of counts into every peer's matrix
+void launch_peer_counts(void* const* peer_tab, int nd, int me, const int* totals, cudaStream_t st);
 // dispatch: each token row stored straight into every destination's inbox
 void launch_peer_pack(const PackArgs& a, int me, const int32_t* dev_of, const int* off_sd, const int* inoff,
                       void* const* peer_tab, cudaStream_t st);
@@ -210,8 +212,9 @@ void launch_peer_signal(void* const* peer_tab, int nd, int me, int base, unsigne
 void launch_peer_wait(const unsigned long long* flags, int nd, int base, unsigned long long seq, long long timeout_ns,
                       int32_t* err, cudaStream_t st);
 // intra-device partial combine fused with the return: rows go straight into the sources' buffers
-void launch_peer_return(int R, int nd, int me, int P, int D, const int32_t* row_epd, const __nv_bfloat16* Y,
-                        const int* C, const int* off_sd, const int* inoff, void* const* peer_tab, cudaStream_t st);
+void launch_peer_return(int R_max, const int* R_total, int nd, int me, int P, int D, const int32_t* row_epd,
+                        const __nv_bfloat16* Y, const int* C, const int* off_sd, const int* inoff,
+                        void* const* peer_tab, cudaStream_t st);
 
 // SimilarityAccumulator::add (pruning.cpp:169-183) on the device: inner [E, E]
 // double accumulated in place from one batch of logits (fp64 or fp32 rows).

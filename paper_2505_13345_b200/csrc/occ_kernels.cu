@@ -844,8 +844,19 @@ __global__ void __launch_bounds__(256) combine_fused_kernel(int n, int nd, int k
 // loopback ranks), and the dispatch pack and the return partial combine store
 // straight into the peer's buffers — the all-to-all is fused into the
 // producing kernel.  Table layout: peer_tab[p * kPeerSlots + i].
-constexpr int kPeerInX = 0, kPeerInIds = 1, kPeerInW = 2, kPeerYSrc = 3, kPeerFlags = 4;
-static_assert(kPeerSlots == 5, "peer table slots");
+constexpr int kPeerInX = 0, kPeerInIds = 1, kPeerInW = 2, kPeerYSrc = 3, kPeerFlags = 4, kPeerCounts = 5;
+static_assert(kPeerSlots == 6, "peer table slots");
+
+// Count all-gather over peer memory: this source's Sfd row counts per
+// destination (rank-key totals row 0) stored as row `me` of every peer's
+// (source, destination) count matrix.
+__global__ void peer_counts_kernel(void* const* peer_tab, int nd, int me, const int* totals) {
+    for (int i = threadIdx.x; i < nd * nd; i += blockDim.x) {
+        const int p = i / nd, d = i % nd;
+        int* cp = reinterpret_cast<int*>(peer_tab[p * kPeerSlots + kPeerCounts]);
+        cp[me * nd + d] = totals[d];
+    }
+}
 
 // pack_kernel, but rows go directly to each destination's inbox:
 // row = inoff[d][me] + (BRIM0 counter - off_sd[me][d]) (all_to_all_exchange
@@ -876,11 +887,27 @@ __global__ void __launch_bounds__(256) peer_pack_kernel(PackArgs a, int me, cons
             rows[nrow++] = inoff[d * a.nd + me] + a.tok_row[(long)t * a.k + j] - off_sd[me * a.nd + d];
         }
     }
+    // x row: read once, 8 16-byte vectors in flight per lane, stored to every
+    // destination inbox row (NVLink peer stores)
+    for (int v0 = 0; v0 < nvec; v0 += 8 * 32) {
+        uint4 buf[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int v = v0 + u * 32 + lane;
+            if (v < nvec) buf[u] = __ldg(src + v);
+        }
+        for (int q = 0; q < nrow; ++q) {
+            uint4* dst = reinterpret_cast<uint4*>(
+                reinterpret_cast<__nv_bfloat16*>(peer_tab[dsts[q] * kPeerSlots + kPeerInX]) + (long)rows[q] * a.D);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int v = v0 + u * 32 + lane;
+                if (v < nvec) dst[v] = buf[u];
+            }
+        }
+    }
     for (int q = 0; q < nrow; ++q) {
         const int d = dsts[q];
-        __nv_bfloat16* px = reinterpret_cast<__nv_bfloat16*>(peer_tab[d * kPeerSlots + kPeerInX]);
-        uint4* dst = reinterpret_cast<uint4*>(px + (long)rows[q] * a.D);
-        for (int v = lane; v < nvec; v += 32) dst[v] = __ldg(src + v);
         int32_t* pid = reinterpret_cast<int32_t*>(peer_tab[d * kPeerSlots + kPeerInIds]);
         float* pw = reinterpret_cast<float*>(peer_tab[d * kPeerSlots + kPeerInW]);
         for (int j = lane; j < a.k; j += 32) {
@@ -929,13 +956,13 @@ __global__ void peer_wait_kernel(const unsigned long long* flags, int nd, int ba
 // Intra-device partial combine fused with the return exchange: inbox row r
 // (from source s, slot counter c) is summed over its local experts and
 // stored straight into source s's returned-row buffer at row c.
-__global__ void __launch_bounds__(256) peer_return_kernel(int R, int nd, int me, int P, int D, const int32_t* row_epd,
-                                                          const __nv_bfloat16* Y, const int* C, const int* off_sd,
-                                                          const int* inoff, void* const* peer_tab) {
+__global__ void __launch_bounds__(256) peer_return_kernel(const int* R_total, int nd, int me, int P, int D,
+                                                          const int32_t* row_epd, const __nv_bfloat16* Y, const int* C,
+                                                          const int* off_sd, const int* inoff, void* const* peer_tab) {
     __shared__ int s_q[8][kMaxLocal];
     const int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    if (r >= R) return;
+    if (r >= *R_total) return;
     int s = 0;  // source of inbox row r: rows of source s are [inoff[me][s], inoff[me][s] + C[s][me])
     while (s < nd - 1 && r >= inoff[me * nd + s] + C[s * nd + me]) ++s;
     const int c = off_sd[s * nd + me] + (r - inoff[me * nd + s]);
@@ -1722,10 +1749,16 @@ void launch_peer_wait(const unsigned long long* flags, int nd, int base, unsigne
     peer_wait_kernel<<<1, 64, 0, st>>>(flags, nd, base, seq, timeout_ns, err);
     count_launch();
 }
-void launch_peer_return(int R, int nd, int me, int P, int D, const int32_t* row_epd, const __nv_bfloat16* Y,
-                        const int* C, const int* off_sd, const int* inoff, void* const* peer_tab, cudaStream_t st) {
-    if (!R) return;
-    peer_return_kernel<<<(R + 7) / 8, 256, 0, st>>>(R, nd, me, P, D, row_epd, Y, C, off_sd, inoff, peer_tab);
+void launch_peer_return(int R_max, const int* R_total, int nd, int me, int P, int D, const int32_t* row_epd,
+                        const __nv_bfloat16* Y, const int* C, const int* off_sd, const int* inoff,
+                        void* const* peer_tab, cudaStream_t st) {
+    if (!R_max) return;
+    peer_return_kernel<<<(R_max + 7) / 8, 256, 0, st>>>(R_total, nd, me, P, D, row_epd, Y, C, off_sd, inoff,
+                                                        peer_tab);
+    count_launch();
+}
+void launch_peer_counts(void* const* peer_tab, int nd, int me, const int* totals, cudaStream_t st) {
+    peer_counts_kernel<<<1, 256, 0, st>>>(peer_tab, nd, me, totals);
     count_launch();
 }
 
