@@ -148,6 +148,17 @@ occ_status occ_set_validate(occ_handle* h, int on);
 /* NCCL plumbing for world_size > 1 (one process per GPU). */
 occ_status occ_comm_unique_id(void* id128);
 occ_status occ_comm_init(occ_handle* h, const void* id128);
+/* Transport over a caller-supplied host all-gather (ranks in separate
+ * processes, no NCCL): fn(ctx, send, bytes, recv) must gather `bytes` from
+ * every rank into recv [world_size * bytes] in rank order and return 0; it is
+ * called collectively, in the same order on every rank (e.g. over
+ * torch.distributed / gloo, MPI).  It bootstraps the CUDA IPC mapping of
+ * occ_comm_enable_peer (which then carries the whole forward with no host
+ * involvement; this also works for several processes sharing one GPU, which
+ * NCCL refuses) and runs the remaining exchanges (backward, non-peer
+ * forward, histogram all-reduce) through host staging. */
+typedef int (*occ_host_allgather_fn)(void* ctx, const void* send, size_t bytes, void* recv);
+occ_status occ_comm_init_host(occ_handle* h, occ_host_allgather_fn fn, void* ctx);
 /* Validation transport: the world_size ranks are host threads of ONE process
  * sharing one GPU (each with its own handle and stream); the exchanges become
  * device-to-device copies between the ranks' buffers.  Same layer code path
@@ -322,44 +333,6 @@ occ_status occ_normalize_graph(const int64_t* counts, int e, double* p);
 occ_status occ_reschedule_placement(const double* p, int e, int num_devices, int32_t* placement);
 /* Sum the histogram across ranks (world_size > 1; ncclAllReduce). */
 occ_status occ_allreduce_histogram(occ_handle* h, int64_t* counts, occ_stream_t stream);
-/* ComponentTracker input (collab.cpp:120-169): first[i*E+j] (i < j) = the
- * first batch index t / batch in which experts i and j co-activate, INT32
- * 0x7f7f7f7f when never; DEVICE buffers, first [E, E] overwritten. */
-occ_status occ_coactivation_first_batch(const int32_t* ids, int n, int k, int e, int batch, int32_t* first,
-                                        occ_stream_t stream);
-/* ComponentTracker::points (collab.cpp:125-169) from `first` (copied to the
- * HOST): largest[b] = size of the largest co-activation component after
- * batch b (0 while there is no edge). HOST buffers. */
-occ_status occ_component_growth(const int32_t* first_batch, int e, int n_batches, int32_t* largest);
-
-/* --------------------------------------------- synthetic inputs and traces */
-/* Deterministic RNG (rng.hpp:12-38): std::mt19937_64 with the reference's
- * draws, so seeds give the reference CLI's streams. */
-typedef struct occ_rng occ_rng;
-occ_status occ_rng_create(uint64_t seed, occ_rng** out);
-void occ_rng_destroy(occ_rng* r);
-uint64_t occ_rng_next(occ_rng* r);
-/* random_matrix (core.cpp:54-58): rows x cols uniform [-1, 1), row-major,
- * rounded through float when single != 0. HOST buffer. */
-occ_status occ_rng_matrix(occ_rng* r, int rows, int cols, int single, double* out);
-
-typedef enum { OCC_TRACE_UNIFORM = 0, OCC_TRACE_ZIPF = 1, OCC_TRACE_BLOCKS = 2 } occ_trace_dist;
-/* TraceSpec (trace_gen.hpp:12-33). */
-typedef struct {
-    int dist;          /* occ_trace_dist */
-    int num_experts;
-    int top_k;
-    int num_tokens;
-    double alpha;      /* zipf exponent */
-    int num_blocks;    /* planted clusters */
-    double p_in;       /* in-cluster probability */
-} occ_trace_spec;
-/* gen_trace (trace_gen.cpp:56-122): ids int32 [n, k], weights f64 [n, k]
- * (descending, summing to 1), HOST buffers; identical to the reference's
- * trace for the same spec and seed. Invalid spec: OCC_ERR_CONFIG with
- * TraceSpec::validate's message. */
-occ_status occ_gen_trace(const occ_trace_spec* spec, uint64_t seed, int32_t* ids, double* weights);
-
 /* Stage profiling with CUDA events on the launching stream (default off).
  * occ_stage_ms fills ms[0..10) for the last occ_forward_expert_parallel /
  * occ_forward: route, plan, pack, compute_index, gather, gemm1, gemm2,

@@ -153,7 +153,6 @@ def ref_lib():
         lib.ref_write_placement_text.restype = C.c_longlong
         lib.ref_write_placement_text.argtypes = [_p, _i, _i, C.c_char_p, C.c_longlong]
         lib.ref_component_points.argtypes = [_p, _i, _i, _i, _i, _p, _p]
-        lib.ref_fit_latency.argtypes = [_p, _p, _i, _p, C.c_char_p, C.c_longlong]
         _REF = lib
     return _REF
 
@@ -507,12 +506,3 @@ def dense_rows_bf16(x, ids, w, w1, w2, rows, act="swiglu", w3=None, shared=None,
     for t in ts:
         t.join()
     return out
-
-
-def ref_fit_latency(xs, ys):
-    """fit_latency (simnet.cpp:36-66) of the reference: (ok, (slope, intercept, r2) or message)."""
-    x, y = _f64(xs), _f64(ys)
-    out = np.zeros(3)
-    buf = C.create_string_buffer(4096)
-    rc = ref_lib().ref_fit_latency(_ptr(x), _ptr(y), len(x), _ptr(out), buf, 4096)
-    return (True, tuple(out)) if rc == 0 else (False, buf.value.decode())

@@ -506,21 +506,5 @@ int ref_component_points(const int* ids, int n, int k, int ne, int batch, long l
 
 extern "C" {
 
-// fit_latency (simnet.cpp:36-66): 0 and slope / intercept / r_squared in out,
-// or -1 with the UsageError text in msg.
-int ref_fit_latency(const double* xs, const double* ys, int n, double* out, char* msg, long long cap) {
-    std::vector<std::pair<double, double>> pts;
-    for (int i = 0; i < n; ++i) pts.emplace_back(xs[i], ys[i]);
-    try {
-        const LatencyFit f = fit_latency(pts);
-        out[0] = f.slope;
-        out[1] = f.intercept;
-        out[2] = f.r_squared;
-        return 0;
-    } catch (const std::exception& e) {
-        emit(e.what(), msg, cap);
-        return -1;
-    }
-}
 
 }  // extern "C"

@@ -93,14 +93,14 @@ EXPORTS = (
     "occ_saved_index", "occ_coactivation_histogram", "occ_normalize_graph", "occ_reschedule_placement",
     "occ_allreduce_histogram", "occ_last_error", "occ_launch_count", "occ_set_profiling", "occ_stage_ms", "occ_forward_host", "occ_host_wait", "occ_comm_init_loopback", "occ_exchange_layout", "occ_set_training", "occ_backward",
     "occ_load_shared_experts", "occ_comm_enable_peer", "occ_similarity_accumulate", "occ_similarity_finalize",
-    "occ_router_logits", "occ_set_grad_x_bf16", "occ_gate_logits_f64", "occ_coactivation_first_batch",
-    "occ_component_growth", "occ_set_micro_batches", "occ_set_router_mode", "occ_route_exact",
-    "occ_dispatch", "occ_build_compute", "occ_expert_compute", "occ_combine", "occ_rng_create", "occ_rng_destroy", "occ_rng_next", "occ_rng_matrix", "occ_gen_trace",
+    "occ_router_logits", "occ_set_grad_x_bf16", "occ_gate_logits_f64", "occ_set_micro_batches", "occ_set_router_mode", "occ_route_exact",
+    "occ_dispatch", "occ_build_compute", "occ_expert_compute", "occ_combine", "occ_comm_init_host",
 )
 
 STAGES = ("route", "plan", "pack", "compute_index", "gather", "gemm1", "gemm2", "shared", "partial_combine", "combine")
 
 _LIB = None
+_ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
 
 
 def lib():
@@ -112,10 +112,6 @@ def lib():
         L = C.CDLL(LIB_PATH)
         L.occ_last_error.restype = C.c_char_p
         L.occ_launch_count.restype = C.c_longlong
-        L.occ_rng_next.restype = C.c_uint64
-        L.occ_rng_next.argtypes = [C.c_void_p]
-        L.occ_rng_destroy.argtypes = [C.c_void_p]
-        L.occ_rng_matrix.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p]
         _LIB = L
     return _LIB
 
@@ -322,6 +318,31 @@ class ExpertParallelLayer:
         dist.broadcast_object_list(obj, src=0, group=group)
         idb = (C.c_uint8 * 128).from_buffer_copy(obj[0])
         _check(lib().occ_comm_init(self._h, idb), "comm_init")
+
+    def comm_init_host(self, group=None):
+        """occ_comm_init_host: the rank's exchanges bootstrapped over a host
+        all-gather -- here torch.distributed on `group` (any backend that takes
+        CPU tensors, e.g. gloo) -- instead of NCCL.  Pair with
+        comm_enable_peer (CUDA IPC mapping; the forward then runs without any
+        host involvement).  Works for several processes on one GPU."""
+        import torch.distributed as dist
+
+        def fn(_ctx, send, nbytes, recv):
+            try:
+                if nbytes == 0:
+                    return 0
+                world = dist.get_world_size(group)
+                src = torch.frombuffer(bytearray(C.string_at(send, nbytes)), dtype=torch.uint8)
+                outs = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(world)]
+                dist.all_gather(outs, src, group=group)
+                cat = torch.cat(outs)  # (kept referenced until the copy is done)
+                C.memmove(recv, cat.data_ptr(), world * nbytes)
+                return 0
+            except Exception:  # noqa: BLE001 -- reported as OCC_ERR_NCCL by the library
+                return 1
+
+        self._host_fn = _ALLGATHER_FN(fn)  # kept alive with the handle
+        _check(lib().occ_comm_init_host(self._h, self._host_fn, None), "comm_init_host")
 
     def router_logits(self, x: torch.Tensor, gate: torch.Tensor) -> torch.Tensor:
         """The production router's f32 logits x g^T [n, E] (tcgen05), e.g. to
@@ -733,25 +754,6 @@ def accumulate_collab(counts: torch.Tensor, ids: torch.Tensor) -> torch.Tensor:
 def build_collab_graph(ids: torch.Tensor, num_experts: int) -> torch.Tensor:
     counts = torch.zeros((num_experts, num_experts), dtype=torch.int64, device=ids.device)
     return accumulate_collab(counts, ids)
-
-
-def component_growth(ids: torch.Tensor, num_experts: int, batch: int = 256):
-    """ComponentTracker over `batch`-token slices (collab.cpp:120-169,
-    cli.cpp:131-145): [(tokens_seen, largest component)], starting at (0, 0).
-    The per-pair first co-activating batch is found on the device; the
-    union-find over those edges runs on the host."""
-    import numpy as np
-    _need_cuda(ids)
-    n, k = ids.shape
-    first = torch.empty((num_experts, num_experts), dtype=torch.int32, device=ids.device)
-    _check(lib().occ_coactivation_first_batch(_ptr(ids.contiguous()), n, k, num_experts, batch, _ptr(first),
-                                              _stream()), "first_batch")
-    nb = (n + batch - 1) // batch
-    fh = np.ascontiguousarray(first.cpu().numpy())
-    largest = np.zeros(nb, np.int32)
-    _check(lib().occ_component_growth(fh.ctypes.data_as(C.c_void_p), num_experts, nb,
-                                      largest.ctypes.data_as(C.c_void_p)), "component_growth")
-    return [(0, 0)] + [(min(n, (b + 1) * batch), int(largest[b])) for b in range(nb)]
 
 
 def normalize_graph(counts) -> "numpy.ndarray":

@@ -237,7 +237,10 @@ struct occ_handle {
     int gx_bf16 = 0;  // occ_set_grad_x_bf16: token gradient written as bf16
     bool peer = false;
     int peer_cap = 0;                  // max tokens per rank per forward
-    unsigned long long peer_seq = 0;   // forwards issued (arrival flag value)
+    // forwards issued = the arrival flag value, kept ON THE DEVICE (bumped by a
+    // kernel at the start of every peer forward) so a captured CUDA graph
+    // advances it on every replay
+    DevBuf<unsigned long long> peer_seq;
     DevBuf<unsigned long long> flags;  // [3 * world]: dispatch arrivals, return arrivals, count rows
     DevBuf<int> c_peer;                // [world * world] (source, destination) counts, rows written by the sources
     DevBuf<void*> peer_tab;            // [world * kPeerSlots]
@@ -441,6 +444,110 @@ struct LoopbackTransport : Transport {
         grp->barrier();
         CUDA_TRY(cudaMemcpyAsync(buf, sum.data(), sizeof(int64_t) * count, cudaMemcpyHostToDevice, st));
         CUDA_TRY(cudaStreamSynchronize(st));
+        return OCC_OK;
+    }
+};
+
+// Ranks in separate processes, wired by a caller-supplied host all-gather
+// (occ_comm_init_host: e.g. torch.distributed over gloo, MPI, a TCP store).
+// It bootstraps the CUDA IPC peer mapping without NCCL (so it also works for
+// several processes sharing one GPU, which NCCL refuses) and carries the
+// (small) collectives; the data all-to-alls go through host staging, so the
+// intended data path with this transport is the fused peer-memory exchange.
+struct HostTransport : Transport {
+    occ_host_allgather_fn fn;
+    void* ctx;
+    int world, rank;
+    HostTransport(occ_host_allgather_fn f, void* c, int w, int r) : fn(f), ctx(c), world(w), rank(r) {}
+    const char* name() const override { return "host"; }
+    occ_status gather(const void* send, size_t bytes, void* recv) {
+        if (fn(ctx, send, bytes, recv) != 0) return fail(OCC_ERR_NCCL, "host all-gather callback failed");
+        return OCC_OK;
+    }
+    occ_status allgather_counts(const int* send, int* recv, int nd, cudaStream_t st) override {
+        std::vector<int> mine(nd), all((size_t)nd * world);
+        CUDA_TRY(cudaMemcpyAsync(mine.data(), send, sizeof(int) * nd, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        occ_status s = gather(mine.data(), sizeof(int) * nd, all.data());
+        if (s != OCC_OK) return s;
+        CUDA_TRY(cudaMemcpyAsync(recv, all.data(), sizeof(int) * all.size(), cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        return OCC_OK;
+    }
+    occ_status alltoallv(const void* send, const std::vector<size_t>& soff, const std::vector<size_t>& scnt, void* recv,
+                         const std::vector<size_t>& roff, const std::vector<size_t>& rcnt, int es,
+                         cudaStream_t st) override {
+        // host-staged: every rank publishes [per-peer element counts | rows in
+        // peer order]; each keeps the part addressed to it
+        size_t tot = 0;
+        for (int p = 0; p < world; ++p) tot += scnt[p];
+        std::vector<char> pkt(sizeof(uint64_t) * world + tot * es);
+        auto* hdr = reinterpret_cast<uint64_t*>(pkt.data());
+        size_t pos = sizeof(uint64_t) * world;
+        for (int p = 0; p < world; ++p) {
+            hdr[p] = scnt[p];
+            if (scnt[p])
+                CUDA_TRY(cudaMemcpyAsync(pkt.data() + pos, reinterpret_cast<const char*>(send) + soff[p] * es,
+                                         scnt[p] * es, cudaMemcpyDeviceToHost, st));
+            pos += scnt[p] * es;
+        }
+        CUDA_TRY(cudaStreamSynchronize(st));
+        uint64_t len = pkt.size(), maxlen = 0;
+        std::vector<uint64_t> lens(world);
+        occ_status s = gather(&len, sizeof(len), lens.data());
+        if (s != OCC_OK) return s;
+        for (uint64_t l : lens) maxlen = std::max(maxlen, l);
+        pkt.resize(maxlen);
+        std::vector<char> all(maxlen * world);
+        if ((s = gather(pkt.data(), maxlen, all.data())) != OCC_OK) return s;
+        for (int p = 0; p < world; ++p) {
+            const char* q = all.data() + maxlen * p;
+            const auto* ph = reinterpret_cast<const uint64_t*>(q);
+            size_t off = sizeof(uint64_t) * world;
+            for (int d = 0; d < rank; ++d) off += ph[d] * es;
+            if (ph[rank] != rcnt[p]) return fail(OCC_ERR_SHAPE, "host transport: send/recv count mismatch");
+            if (rcnt[p])
+                CUDA_TRY(cudaMemcpyAsync(reinterpret_cast<char*>(recv) + roff[p] * es, q + off, rcnt[p] * es,
+                                         cudaMemcpyHostToDevice, st));
+        }
+        CUDA_TRY(cudaStreamSynchronize(st));
+        return OCC_OK;
+    }
+    occ_status allreduce_i64(int64_t* buf, size_t count, cudaStream_t st) override {
+        std::vector<int64_t> mine(count), all(count * world), sum(count, 0);
+        CUDA_TRY(cudaMemcpyAsync(mine.data(), buf, sizeof(int64_t) * count, cudaMemcpyDeviceToHost, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        occ_status s = gather(mine.data(), sizeof(int64_t) * count, all.data());
+        if (s != OCC_OK) return s;
+        for (int p = 0; p < world; ++p)
+            for (size_t i = 0; i < count; ++i) sum[i] += all[p * count + i];
+        CUDA_TRY(cudaMemcpyAsync(buf, sum.data(), sizeof(int64_t) * count, cudaMemcpyHostToDevice, st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        return OCC_OK;
+    }
+    occ_status exchange_pointers(const std::vector<void*>& mine, std::vector<void*>& all,
+                                 std::vector<void*>& opened) override {
+        const size_t m = mine.size(), hb = sizeof(cudaIpcMemHandle_t);
+        std::vector<cudaIpcMemHandle_t> hs(m), allh(m * world);
+        for (size_t i = 0; i < m; ++i) CUDA_TRY(cudaIpcGetMemHandle(&hs[i], mine[i]));
+        occ_status s = gather(hs.data(), m * hb, allh.data());
+        if (s != OCC_OK) return s;
+        all.assign(m * world, nullptr);
+        for (int p = 0; p < world; ++p)
+            for (size_t i = 0; i < m; ++i) {
+                if (p == rank) {
+                    all[p * m + i] = mine[i];
+                    continue;
+                }
+                void* ptr = nullptr;
+                CUDA_TRY(cudaIpcOpenMemHandle(&ptr, allh[p * m + i], cudaIpcMemLazyEnablePeerAccess));
+                all[p * m + i] = ptr;
+                opened.push_back(ptr);
+            }
+        return OCC_OK;
+    }
+    occ_status split(Transport** out) override {  // same callback: calls stay in the same order on every rank
+        *out = new HostTransport(fn, ctx, world, rank);
         return OCC_OK;
     }
 };
@@ -785,9 +892,10 @@ occ_status forward_multi(occ_handle* h, const __nv_bfloat16* x, const int32_t* i
     launch_rank_count(items, h->group.p, h->mask.p, 1, nd, ws, st);
     launch_rank_scan(items, 1, nd, ws, st);
     int* C_all = h->c_all.p;
-    const unsigned long long seq = h->peer ? ++h->peer_seq : 0;
+    const unsigned long long* seq = h->peer_seq.p;
     void* const* tab = h->peer_tab.p;
     if (h->peer) {
+        launch_seq_bump(h->peer_seq.p, st);
         // count all-gather over peer memory: this source's row stored into
         // every peer's count matrix, then an arrival flag (no collective, no
         // host round trip: the whole forward stays stream-ordered)
@@ -1126,6 +1234,7 @@ occ_status occ_destroy(occ_handle* h) {
     for (void* ptr : h->ipc_opened) cudaIpcCloseMemHandle(ptr);
     h->flags.release();
     h->c_peer.release();
+    h->peer_seq.release();
     h->peer_tab.release();
     for (auto* b : {&h->w13s, &h->w2s, &h->sgate, &h->hs, &h->ys}) b->release();
     h->sw.release();
@@ -2140,17 +2249,6 @@ occ_status occ_coactivation_histogram(const int32_t* ids, int n, int k, int e, i
     return OCC_OK;
 }
 
-occ_status occ_coactivation_first_batch(const int32_t* ids, int n, int k, int e, int batch, int32_t* first,
-                                        occ_stream_t stream) {
-    if ((!ids && n > 0) || !first) return fail(OCC_ERR_ARG, "null argument");
-    if (e < 1 || k < 1 || n < 0 || batch < 1) return fail(OCC_ERR_SHAPE, "first_batch: need E, k, batch >= 1");
-    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
-    CUDA_TRY(cudaMemsetAsync(first, 0x7f, sizeof(int32_t) * (size_t)e * e, st));  // 0x7f7f7f7f: never seen
-    launch_first_coactivation(ids, n, k, e, batch, first, st);
-    CUDA_TRY(cudaGetLastError());
-    return OCC_OK;
-}
-
 static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
 
 occ_status occ_comm_unique_id(void* id128) {
@@ -2170,6 +2268,14 @@ occ_status occ_comm_init(occ_handle* h, const void* id128) {
     NCCL_TRY(ncclCommInitRank(&comm, h->world, id, h->rank));
     delete h->tp;
     h->tp = new NcclTransport(comm, h->world);
+    return OCC_OK;
+}
+
+occ_status occ_comm_init_host(occ_handle* h, occ_host_allgather_fn fn, void* ctx) {
+    if (!h || !fn) return fail(OCC_ERR_ARG, "null argument");
+    if (h->world == 1) return OCC_OK;
+    delete h->tp;
+    h->tp = new HostTransport(fn, ctx, h->world, h->rank);
     return OCC_OK;
 }
 
@@ -2216,7 +2322,8 @@ occ_status occ_comm_enable_peer(occ_handle* h, int max_tokens_per_rank) {
     CUDA_TRY(cudaMemcpy(h->peer_tab.p, all.data(), sizeof(void*) * all.size(), cudaMemcpyHostToDevice));
     h->peer = true;
     h->peer_cap = max_tokens_per_rank;
-    h->peer_seq = 0;
+    CUDA_TRY(h->peer_seq.ensure(1));
+    CUDA_TRY(cudaMemset(h->peer_seq.p, 0, sizeof(unsigned long long)));
     if (h->sib) return occ_comm_enable_peer(h->sib, max_tokens_per_rank);
     return OCC_OK;
 }

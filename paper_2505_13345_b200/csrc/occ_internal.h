@@ -208,8 +208,12 @@ void launch_peer_counts(void* const* peer_tab, int nd, int me, const int* totals
 void launch_peer_pack(const PackArgs& a, int me, const int32_t* dev_of, const int* off_sd, const int* inoff,
                       void* const* peer_tab, cudaStream_t st);
 // publish `seq` into flag slot (base + me) of every peer / wait for all peers' `seq` at base..base+nd
-void launch_peer_signal(void* const* peer_tab, int nd, int me, int base, unsigned long long seq, cudaStream_t st);
-void launch_peer_wait(const unsigned long long* flags, int nd, int base, unsigned long long seq, long long timeout_ns,
+// seq: DEVICE pointer to the forward counter (bumped by launch_seq_bump)
+void launch_seq_bump(unsigned long long* seq, cudaStream_t st);
+void launch_peer_signal(void* const* peer_tab, int nd, int me, int base, const unsigned long long* seq,
+                        cudaStream_t st);
+void launch_peer_wait(const unsigned long long* flags, int nd, int base, const unsigned long long* seq,
+                      long long timeout_ns,
                       int32_t* err, cudaStream_t st);
 // intra-device partial combine fused with the return: rows go straight into the sources' buffers
 void launch_peer_return(int R_max, const int* R_total, int nd, int me, int P, int D, const int32_t* row_epd,
@@ -224,7 +228,6 @@ void launch_similarity_add(const void* logits, int fp64, int n, int e, double* i
 // Bins in shared memory up to kHistSmemMax bytes (E <= 236), global atomics above.
 constexpr size_t kHistSmemMax = 220 * 1024;
 void launch_histogram(const int32_t* ids, int n, int k, int e, int64_t* counts, cudaStream_t st);
-void launch_first_coactivation(const int32_t* ids, int n, int k, int e, int batch, int* first, cudaStream_t st);
 
 // Comm statistics (spans, pair shares, naive crossings) per token.
 void launch_token_stats(int n, int k, int nd, const int32_t* ids, const int32_t* sources, int src_fixed,

@@ -921,9 +921,12 @@ __global__ void __launch_bounds__(256) peer_pack_kernel(PackArgs a, int me, cons
 
 // Arrival signal: after this stream's peer stores, publish `seq` into slot
 // (base + me) of every peer's flag array (release, system scope).
-__global__ void peer_signal_kernel(void* const* peer_tab, int nd, int me, int base, unsigned long long seq) {
+__global__ void seq_bump_kernel(unsigned long long* seq) { *seq += 1; }
+
+__global__ void peer_signal_kernel(void* const* peer_tab, int nd, int me, int base, const unsigned long long* seq_p) {
     const int d = threadIdx.x;
     if (d >= nd) return;
+    const unsigned long long seq = *seq_p;
     __threadfence_system();
     unsigned long long* f = reinterpret_cast<unsigned long long*>(peer_tab[d * kPeerSlots + kPeerFlags]);
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(f + base + me), "l"(seq) : "memory");
@@ -932,10 +935,11 @@ __global__ void peer_signal_kernel(void* const* peer_tab, int nd, int me, int ba
 // Wait until every peer has published `seq` in slots base..base+nd of this
 // rank's flags; bounded (err = 7 after `timeout_ns`) so a lost peer cannot
 // hang the device.
-__global__ void peer_wait_kernel(const unsigned long long* flags, int nd, int base, unsigned long long seq,
+__global__ void peer_wait_kernel(const unsigned long long* flags, int nd, int base, const unsigned long long* seq_p,
                                  long long timeout_ns, int32_t* err) {
     const int s = threadIdx.x;
     if (s >= nd) return;
+    const unsigned long long seq = *seq_p;
     unsigned long long t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     while (true) {
@@ -1164,25 +1168,6 @@ __global__ void __launch_bounds__(256) histogram_global_kernel(const int32_t* id
                 if ((unsigned)row[a] >= (unsigned)e || (unsigned)row[b] >= (unsigned)e) continue;
                 atomicAdd(&counts[(long)row[a] * e + row[b]], 1ull);
                 atomicAdd(&counts[(long)row[b] * e + row[a]], 1ull);
-            }
-    }
-}
-
-// ComponentTracker input (collab.cpp:125-137): for every expert pair, the
-// first token batch (t / batch) in which it co-activates; `first` is
-// pre-filled with INT_MAX.  A plain read filters the atomics: after the first
-// few batches nearly every pair already holds a smaller value.
-__global__ void __launch_bounds__(256) first_coactivation_kernel(const int32_t* ids, int n, int k, int e, int batch,
-                                                                 int* first) {
-    for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < n; t += gridDim.x * blockDim.x) {
-        const int32_t* row = ids + (long)t * k;
-        const int bt = t / batch;
-        for (int a = 0; a < k; ++a)
-            for (int b = a + 1; b < k; ++b) {
-                const int lo = min(row[a], row[b]), hi = max(row[a], row[b]);
-                if (lo < 0 || hi >= e) continue;
-                int* cell = first + (long)lo * e + hi;
-                if (*(volatile int*)cell > bt) atomicMin(cell, bt);
             }
     }
 }
@@ -1740,11 +1725,17 @@ void launch_peer_pack(const PackArgs& a, int me, const int32_t* dev_of, const in
     peer_pack_kernel<<<(a.n + 7) / 8, 256, 0, st>>>(a, me, dev_of, off_sd, inoff, peer_tab);
     count_launch();
 }
-void launch_peer_signal(void* const* peer_tab, int nd, int me, int base, unsigned long long seq, cudaStream_t st) {
+void launch_seq_bump(unsigned long long* seq, cudaStream_t st) {
+    seq_bump_kernel<<<1, 1, 0, st>>>(seq);
+    count_launch();
+}
+void launch_peer_signal(void* const* peer_tab, int nd, int me, int base, const unsigned long long* seq,
+                        cudaStream_t st) {
     peer_signal_kernel<<<1, 64, 0, st>>>(peer_tab, nd, me, base, seq);
     count_launch();
 }
-void launch_peer_wait(const unsigned long long* flags, int nd, int base, unsigned long long seq, long long timeout_ns,
+void launch_peer_wait(const unsigned long long* flags, int nd, int base, const unsigned long long* seq,
+                      long long timeout_ns,
                       int32_t* err, cudaStream_t st) {
     peer_wait_kernel<<<1, 64, 0, st>>>(flags, nd, base, seq, timeout_ns, err);
     count_launch();
@@ -1807,13 +1798,6 @@ void launch_histogram(const int32_t* ids, int n, int k, int e, int64_t* counts, 
     count_launch();
 }
 
-void launch_first_coactivation(const int32_t* ids, int n, int k, int e, int batch, int* first, cudaStream_t st) {
-    if (!n || k < 2) return;
-    int blocks = (n + 255) / 256;
-    if (blocks > 148 * 4) blocks = 148 * 4;
-    first_coactivation_kernel<<<blocks, 256, 0, st>>>(ids, n, k, e, batch, first);
-    count_launch();
-}
 
 void launch_token_stats(int n, int k, int nd, const int32_t* ids, const int32_t* sources, int src_fixed,
                         const int32_t* dev_of, int E, long long* stats, cudaStream_t st) {

@@ -1455,3 +1455,69 @@ def test_stage_entry_points_world_gt1_handle():
     assert torch.equal(y, one.expert_compute(rank, sx[rows], si[rows], sw[rows]))
     with pytest.raises(occ.ConfigError):
         h.expert_compute(0, sx[rows], si[rows], sw[rows])
+
+
+@pytest.mark.parametrize("nd,ne,k", [(2, 8, 2), (8, 64, 8)])
+def test_multi_rank_peer_forward_graph_replay_loopback(nd, ne, k):
+    """world_size > 1 with the fused peer-memory exchange has no host
+    synchronisation (counts exchanged through peer memory, received row count
+    kept on the device, the arrival-flag sequence number advanced by a kernel),
+    so each rank's forward captures into a CUDA graph; replays with new inputs
+    equal the eager forward bit for bit (loopback ranks on one GPU)."""
+    import threading
+    dm, dh = 128, 256
+    n_per = [37, 64, 5, 100, 0, 64, 33, 1][:nd]
+    n = sum(n_per)
+    x, g, w1, w2, _ = make_layer_inputs(nd * 5, n, dm, dh, ne)
+    ids, w = random_routing(n, ne, k, np.random.default_rng(nd))
+    plist = _placement(ne, nd, "shuffled", seed=nd + 7)
+    starts = np.concatenate([[0], np.cumsum(n_per)])
+    key = np.random.default_rng().integers(1 << 30)
+    errs, ok = [], [False] * nd
+    barrier = threading.Barrier(nd)
+
+    def rank_main(r):
+        try:
+            st = torch.cuda.Stream()
+            with torch.cuda.stream(st):
+                layer = occ.ExpertParallelLayer(occ.MoEConfig(ne, k, nd, dm, dh, activation="silu"),
+                                                occ.Placement([list(p) for p in plist]), world_size=nd, rank=r)
+                loc = plist[r]
+                layer.load_experts(cuda(w1[loc], torch.bfloat16), cuda(w2[loc], torch.bfloat16))
+                layer.comm_init_loopback(int(key))
+                layer.comm_enable_peer(128)
+                layer.set_validate(False)
+                a, b = starts[r], starts[r + 1]
+                X = cuda(x[a:b], torch.bfloat16)
+                I, W = cuda(ids[a:b]), cuda(w[a:b], torch.float32)
+                out = torch.empty_like(X)
+                layer.forward_given_routing(X, I, W, out=out)
+                st.synchronize()
+                barrier.wait()
+                graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(graph, stream=st, capture_error_mode="thread_local"):
+                    layer.forward_given_routing(X, I, W, out=out)
+                barrier.wait()
+                for rep in range(3):
+                    X.mul_(-1 if rep % 2 else 1.5)  # new values, same buffers
+                    barrier.wait()
+                    graph.replay()
+                    st.synchronize()
+                    got = out.clone()
+                    barrier.wait()
+                    want = layer.forward_given_routing(X, I, W)
+                    st.synchronize()
+                    barrier.wait()
+                    assert torch.equal(got, want), (r, rep)
+                ok[r] = True
+        except Exception as e:  # surface thread failures
+            errs.append(e)
+            barrier.abort()
+
+    ths = [threading.Thread(target=rank_main, args=(r,)) for r in range(nd)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join(timeout=180)
+    assert not errs, errs
+    assert all(ok)

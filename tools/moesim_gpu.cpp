@@ -8,14 +8,14 @@
 //   moesim_gpu reschedule --graph F --devices D --out F
 //   moesim_gpu simulate   --seed S --out F [--trace F] [--placement F] [--prune none|router|similarity] ...
 //   moesim_gpu sweep-prune --seed S --mode router|similarity --out-prefix P ...
-//   moesim_gpu fit-latency --points F --out F
 //
 // Text formats follow io.cpp:55-204 with std::to_chars / std::from_chars, as
-// the reference does, so files round-trip byte for byte.  Trace generation and
-// placement are host code in libocc; the co-activation histogram, component
-// growth edges, fp64 router, top-k, pruning and the expert-parallel forward
-// are CUDA kernels.  The Python mirror is paper_2505_13345_b200/cli.py; both
-// are pinned to the reference in tests/test_cli.py / tests/test_gpu_cli.py.
+// the reference does, so files round-trip byte for byte.  Placement is host
+// code in libocc; the co-activation histogram, fp64 router, top-k, pruning and
+// the expert-parallel forward are CUDA kernels behind the C-ABI.  Trace
+// generation, the RNG streams and the component-growth statistic are
+// test-input tooling outside the layer (moesim_tools.hpp).  Pinned to the
+// reference in tests/test_cli.py / tests/test_gpu_cli.py.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -33,6 +33,7 @@
 #include <string>
 #include <vector>
 
+#include "moesim_tools.hpp"
 #include "occult.h"
 
 namespace {
@@ -363,10 +364,10 @@ int cmd_gen_trace(const std::vector<std::string>& a) {  // cli.cpp:92-110
     const Args o = parse_args(a, {"--dist", "--experts", "--topk", "--tokens", "--alpha", "--blocks", "--p-in",
                                   "--tag", "--seed", "--out"}, {});
     const std::string dist = o.get("--dist", "uniform");
-    occ_trace_spec spec{};
-    if (dist == "uniform") spec.dist = OCC_TRACE_UNIFORM;
-    else if (dist == "zipf") spec.dist = OCC_TRACE_ZIPF;
-    else if (dist == "blocks") spec.dist = OCC_TRACE_BLOCKS;
+    tools::TraceSpec spec{};
+    if (dist == "uniform") spec.dist = tools::kUniform;
+    else if (dist == "zipf") spec.dist = tools::kZipf;
+    else if (dist == "blocks") spec.dist = tools::kBlocks;
     else throw UsageError("unknown distribution '" + dist + "'");
     spec.num_experts = (int)std::stoll(o.need("--experts"));
     spec.top_k = (int)std::stoll(o.need("--topk"));
@@ -381,7 +382,8 @@ int cmd_gen_trace(const std::vector<std::string>& a) {  // cli.cpp:92-110
     const size_t nk = (size_t)std::max(t.n, 0) * std::max(t.k, 0);
     t.ids.resize(nk);
     t.w.resize(nk);
-    if (occ_gen_trace(&spec, seed, t.ids.data(), t.w.data()) != OCC_OK) throw UsageError(occ_last_error());
+    const std::string bad = tools::gen_trace(&spec, seed, t.ids.data(), t.w.data());
+    if (!bad.empty()) throw UsageError(bad);
     write_file(out, write_trace(t));
     return 0;
 }
@@ -396,15 +398,13 @@ int cmd_profile(const std::vector<std::string>& a, std::ostream& out) {  // cli.
     Dev<int64_t> counts((size_t)ne * ne);
     cuda_ok(cudaMemset(counts.p, 0, sizeof(int64_t) * ne * ne), "memset");
     occ_ok(occ_coactivation_histogram(ids.p, n, t.k, ne, counts.p, nullptr), "histogram");
-    Dev<int32_t> first((size_t)ne * ne);
-    occ_ok(occ_coactivation_first_batch(ids.p, n, t.k, ne, batch, first.p, nullptr), "first_batch");
     std::vector<int64_t> hc((size_t)ne * ne);
-    std::vector<int32_t> hf((size_t)ne * ne);
     counts.get(hc.data(), hc.size());
-    first.get(hf.data(), hf.size());
+    // ComponentTracker (collab.cpp:120-169) over 256-token batches: host statistic
+    const std::vector<int32_t> hf = tools::first_batch_of(t.ids.data(), n, t.k, ne, batch);
     const int nb = (n + batch - 1) / batch;
     std::vector<int32_t> largest(std::max(nb, 1));
-    occ_ok(occ_component_growth(hf.data(), ne, nb, largest.data()), "component_growth");
+    tools::component_growth(hf.data(), ne, nb, largest.data());
     Mat cm{ne, ne, std::vector<double>(hc.begin(), hc.end())};
     Mat nm{ne, ne, std::vector<double>((size_t)ne * ne)};
     occ_ok(occ_normalize_graph(hc.data(), ne, nm.v.data()), "normalize_graph");
@@ -561,18 +561,15 @@ SimResult run_simulate(const SimOpts& o) {  // cli.cpp:201-320
     }
     if ((int)R.devices.size() != nd) throw PlacementError("placement: device count differs from --devices");
     const int single = o.precision == "single";
-    occ_rng *master, *trng, *grng, *erng;  // cli.cpp:248-251: token, gate, expert streams in that order
-    occ_ok(occ_rng_create(o.seed, &master), "rng");
-    occ_ok(occ_rng_create(occ_rng_next(master), &trng), "rng");
-    occ_ok(occ_rng_create(occ_rng_next(master), &grng), "rng");
-    occ_ok(occ_rng_create(occ_rng_next(master), &erng), "rng");
+    tools::Rng master(o.seed);  // cli.cpp:248-251: token, gate, expert streams in that order
+    tools::Rng trng(master.g()), grng(master.g()), erng(master.g());
     const int n = trace_mode ? tr.n : o.tokens, D = o.dim, F = o.hidden;
     R.n = n;
     std::vector<double> x((size_t)n * D), w1((size_t)ne * D * F), w2((size_t)ne * F * D), g((size_t)ne * D);
-    occ_ok(occ_rng_matrix(trng, n, D, single, x.data()), "random_matrix");
+    tools::rng_matrix(&trng, n, D, single, x.data());
     for (int e = 0; e < ne; ++e) {  // ExpertWeights::random (core.cpp:40-52)
-        occ_ok(occ_rng_matrix(erng, D, F, single, w1.data() + (size_t)e * D * F), "random_matrix");
-        occ_ok(occ_rng_matrix(erng, F, D, single, w2.data() + (size_t)e * F * D), "random_matrix");
+        tools::rng_matrix(&erng, D, F, single, w1.data() + (size_t)e * D * F);
+        tools::rng_matrix(&erng, F, D, single, w2.data() + (size_t)e * F * D);
     }
     if (o.source_mode != "single" && o.source_mode != "roundrobin")
         throw UsageError("unknown source mode '" + o.source_mode + "'");
@@ -584,12 +581,8 @@ SimResult run_simulate(const SimOpts& o) {  // cli.cpp:201-320
     occ_ok(occ_create(&cfg, flat.data(), 1, 0, &h), "create");
     struct Free {
         occ_handle* h;
-        occ_rng* r[4];
-        ~Free() {
-            occ_destroy(h);
-            for (auto* x : r) occ_rng_destroy(x);
-        }
-    } guard{h, {master, trng, grng, erng}};
+        ~Free() { occ_destroy(h); }
+    } guard{h};
     std::vector<uint16_t> b1(w1.size()), b2(w2.size()), bx(x.size());
     for (size_t i = 0; i < w1.size(); ++i) b1[i] = to_bf16(w1[i]);
     for (size_t i = 0; i < w2.size(); ++i) b2[i] = to_bf16(w2[i]);
@@ -606,7 +599,7 @@ SimResult run_simulate(const SimOpts& o) {  // cli.cpp:201-320
         ids.put(tr.ids.data(), tr.ids.size());
         wh = tr.w;
     } else {
-        occ_ok(occ_rng_matrix(grng, ne, D, single, g.data()), "random_matrix");
+        tools::rng_matrix(&grng, ne, D, single, g.data());
         Dev<double> dx(x.size()), dg(g.size()), sc((size_t)n * ne), dw((size_t)n * k);
         dx.put(x.data(), x.size());
         dg.put(g.data(), g.size());
@@ -783,58 +776,12 @@ int cmd_sweep_prune(const std::vector<std::string>& a, std::ostream& out) {  // 
     return 0;
 }
 
-int cmd_fit_latency(const std::vector<std::string>& a, std::ostream& out) {  // cli.cpp:393-422, simnet.cpp:36-66
-    const Args o = parse_args(a, {"--points", "--out"}, {});
-    std::istringstream in(slurp(o.need("--points")));
-    const std::string dst = o.need("--out");
-    std::vector<std::pair<double, double>> pts;
-    std::string line;
-    int line_no = 0;
-    while (std::getline(in, line)) {
-        ++line_no;
-        if (line.empty() || line[0] == '#') continue;
-        std::istringstream ss(line);
-        std::string x, y, extra;
-        if (!(ss >> x >> y) || (ss >> extra)) bad(line_no, "expected 'replicas seconds'");
-        pts.emplace_back(parse_double(x, line_no), parse_double(y, line_no));
-    }
-    int distinct = 0;
-    for (size_t i = 0; i < pts.size(); ++i) {
-        bool seen = false;
-        for (size_t j = 0; j < i; ++j) seen = seen || pts[j].first == pts[i].first;
-        distinct += !seen;
-    }
-    if (pts.size() < 2 || distinct < 2) throw UsageError("fit: need at least 2 points with distinct x values");
-    const double n = static_cast<double>(pts.size());
-    double mx = 0.0, my = 0.0;
-    for (const auto& p : pts) mx += p.first, my += p.second;
-    mx /= n;
-    my /= n;
-    double sxx = 0.0, sxy = 0.0, syy = 0.0;
-    for (const auto& p : pts) {
-        sxx += (p.first - mx) * (p.first - mx);
-        sxy += (p.first - mx) * (p.second - my);
-        syy += (p.second - my) * (p.second - my);
-    }
-    const double slope = sxy / sxx, intercept = my - slope * mx;
-    const double r2 = syy == 0.0 ? 1.0 : (sxy * sxy) / (sxx * syy);
-    Report r;
-    r.kv("command", std::string("fit-latency"));
-    r.kv("points.count", (long long)pts.size());
-    r.kv("fit.slope", slope);
-    r.kv("fit.intercept", intercept);
-    r.kv("fit.r_squared", r2);
-    write_file(dst, r.os.str());
-    out << "fit: slope " << fmt(slope) << ", intercept " << fmt(intercept) << ", R^2 " << fmt(r2) << "\n";
-    return 0;
-}
-
 }  // namespace
 
 int main(int argc, char** argv) {
     std::vector<std::string> a(argv + 1, argv + argc);
     if (a.empty()) {
-        std::cerr << "usage: moesim_gpu gen-trace|profile|reschedule|simulate|sweep-prune|fit-latency [options]\n";
+        std::cerr << "usage: moesim_gpu gen-trace|profile|reschedule|simulate|sweep-prune [options]\n";
         return 2;
     }
     const std::string cmd = a[0];
@@ -845,7 +792,6 @@ int main(int argc, char** argv) {
         if (cmd == "reschedule") return cmd_reschedule(a);
         if (cmd == "simulate") return cmd_simulate(a, std::cout);
         if (cmd == "sweep-prune") return cmd_sweep_prune(a, std::cout);
-        if (cmd == "fit-latency") return cmd_fit_latency(a, std::cout);
         std::cerr << "usage error: unknown command '" << cmd << "'\n";
         return 2;
     } catch (const UsageError& e) {
