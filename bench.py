@@ -344,10 +344,12 @@ def run_ours(args):
         flush.zero_()
         step()
     barrier()
-    # one step captured as a CUDA graph (world_size 1: the layer runs with
-    # device-side counts and no host synchronisation), replayed per step
+    # one step captured as a CUDA graph, replayed per step: world_size 1, and
+    # world_size > 1 with the fused peer-memory exchange (counts, arrivals and
+    # the received-row count all stay on the device: no host synchronisation)
     graph, per_step = None, None
-    if world == 1 and not args.no_graph:
+    capturable = world == 1 or (exchange.startswith("peer memory") and not W["train"])
+    if capturable and not args.no_graph:
         s_cap = torch.cuda.Stream()
         s_cap.wait_stream(stream)
         with torch.cuda.stream(s_cap):

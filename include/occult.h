@@ -333,6 +333,12 @@ occ_status occ_normalize_graph(const int64_t* counts, int e, double* p);
 occ_status occ_reschedule_placement(const double* p, int e, int num_devices, int32_t* placement);
 /* Sum the histogram across ranks (world_size > 1; ncclAllReduce). */
 occ_status occ_allreduce_histogram(occ_handle* h, int64_t* counts, occ_stream_t stream);
+/* Index-chain implementation of the one-GPU forward (world_size 1, dedup,
+ * E <= 64, k <= 8): 1 (default) = one cooperative kernel for BRIM0, the
+ * inbox records, BRIM1, the Epd A operand and the CommReport counters
+ * (occ_plan.cu); 0 = the multi-kernel chain.  Identical results. */
+occ_status occ_set_plan_kernels(occ_handle* h, int fused);
+
 /* Stage profiling with CUDA events on the launching stream (default off).
  * occ_stage_ms fills ms[0..10) for the last occ_forward_expert_parallel /
  * occ_forward: route, plan, pack, compute_index, gather, gemm1, gemm2,

@@ -95,6 +95,7 @@ EXPORTS = (
     "occ_load_shared_experts", "occ_comm_enable_peer", "occ_similarity_accumulate", "occ_similarity_finalize",
     "occ_router_logits", "occ_set_grad_x_bf16", "occ_gate_logits_f64", "occ_set_micro_batches", "occ_set_router_mode", "occ_route_exact",
     "occ_dispatch", "occ_build_compute", "occ_expert_compute", "occ_combine", "occ_comm_init_host",
+    "occ_set_plan_kernels",
 )
 
 STAGES = ("route", "plan", "pack", "compute_index", "gather", "gemm1", "gemm2", "shared", "partial_combine", "combine")
@@ -400,6 +401,11 @@ class ExpertParallelLayer:
                                   _ptr(g["w1"]), _ptr(g["w3"]), _ptr(g["w2"]), _ptr(g["routing_weights"]),
                                   _stream()), "backward")
         return g
+
+    def set_plan_kernels(self, fused: bool):
+        """One cooperative kernel for the one-GPU index chain (default) or the
+        multi-kernel chain (occ_set_plan_kernels); identical results."""
+        _check(lib().occ_set_plan_kernels(self._h, int(fused)), "set_plan_kernels")
 
     def set_validate(self, on: bool):
         _check(lib().occ_set_validate(self._h, int(on)), "set_validate")

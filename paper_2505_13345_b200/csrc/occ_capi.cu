@@ -105,6 +105,10 @@ struct Transport {
                                  void* recv, const std::vector<size_t>& roff, const std::vector<size_t>& rcnt, int es,
                                  cudaStream_t st) = 0;
     virtual occ_status allreduce_i64(int64_t* buf, size_t count, cudaStream_t st) = 0;
+    // host-level barrier of all ranks (collective set-up calls end with one so
+    // no rank starts a forward -- whose peer arrival waits spin on the device --
+    // while another is still allocating)
+    virtual occ_status barrier() = 0;
     // peer-memory mapping: every rank's `mine` device pointers, usable by this
     // rank (world x mine.size(), row p = rank p); opened mappings are returned
     // in `opened` for release
@@ -180,6 +184,10 @@ struct occ_handle {
     // gather4 per K block saturate the TMA unit: profiles/r01_gemm_micro.md),
     // so the copy is the default.
     int gather_a = 0;
+    // one-GPU index chain as ONE cooperative kernel (occ_plan.cu; default) or
+    // the multi-kernel chain (occ_set_plan_kernels(h, 0) / OCC_FUSED_PLAN=0)
+    int fused_plan = 1;
+    DevBuf<int> fp_ws;
     DispatchOffsets dofs{};
     ComputeOffsets cofs{};
     int* d_tok_base = nullptr;
@@ -267,7 +275,10 @@ struct NcclTransport : Transport {
     ncclComm_t comm;
     int world;
     explicit NcclTransport(ncclComm_t c, int w) : comm(c), world(w) {}
-    ~NcclTransport() override { ncclCommDestroy(comm); }
+    ~NcclTransport() override {
+        ncclCommDestroy(comm);
+        if (bar_buf) cudaFree(bar_buf);
+    }
     const char* name() const override { return "nccl"; }
     occ_status allgather_counts(const int* send, int* recv, int nd, cudaStream_t st) override {
         NCCL_TRY(ncclAllGather(send, recv, nd, ncclInt32, comm, st));
@@ -288,6 +299,13 @@ struct NcclTransport : Transport {
     }
     occ_status allreduce_i64(int64_t* buf, size_t count, cudaStream_t st) override {
         NCCL_TRY(ncclAllReduce(buf, buf, count, ncclInt64, ncclSum, comm, st));
+        return OCC_OK;
+    }
+    int* bar_buf = nullptr;
+    occ_status barrier() override {
+        if (!bar_buf) CUDA_TRY(cudaMalloc(&bar_buf, sizeof(int)));
+        NCCL_TRY(ncclAllReduce(bar_buf, bar_buf, 1, ncclInt32, ncclSum, comm, 0));
+        CUDA_TRY(cudaStreamSynchronize(0));
         return OCC_OK;
     }
     occ_status exchange_pointers(const std::vector<void*>& mine, std::vector<void*>& all,
@@ -422,6 +440,10 @@ struct LoopbackTransport : Transport {
         grp->barrier();
         return OCC_OK;
     }
+    occ_status barrier() override {
+        grp->barrier();
+        return OCC_OK;
+    }
     occ_status split(Transport** out) override {
         std::shared_ptr<LoopGroup> c;
         {
@@ -545,6 +567,11 @@ struct HostTransport : Transport {
                 opened.push_back(ptr);
             }
         return OCC_OK;
+    }
+    occ_status barrier() override {
+        const char mine = 1;
+        std::vector<char> all(world);
+        return gather(&mine, 1, all.data());
     }
     occ_status split(Transport** out) override {  // same callback: calls stay in the same order on every rank
         *out = new HostTransport(fn, ctx, world, rank);
@@ -691,6 +718,7 @@ occ_status ensure_ws(occ_handle* h, int n) {
     if (h->world == 1) {
         occ_status s = ensure_recv(h, (size_t)n * span_max, (size_t)n * k);
         if (s != OCC_OK) return s;
+        if (dedup && fused_plan_supported(nd, h->E, k)) CUDA_TRY(h->fp_ws.ensure(fused_plan_ws(n, nd, h->E)));
     }
     h->n_cap = n;
     return OCC_OK;
@@ -746,7 +774,8 @@ void launch_gemm2(occ_handle* h, int ngroups, cudaStream_t st, const int* widx =
 // Shared experts on this device's n tokens: g = sigmoid(x . gate) (or 1),
 // GEMM-1 x @ [w1s|w3s] with the act/SwiGLU x g epilogue, GEMM-2 h @ w2s
 // -> ys [n, D] bf16 (added last by the combine).
-occ_status run_shared(occ_handle* h, const __nv_bfloat16* x, int n, cudaStream_t st) {
+// Shared-expert workspace for n tokens (grow-only).
+occ_status ensure_shared(occ_handle* h, int n) {
     const int D = h->D, Fs = h->Fsh;
     const size_t n_pad = (size_t)(n + kBM - 1) / kBM * kBM;
     if (n_pad > h->sh_cap || !h->hs.p) {
@@ -758,6 +787,14 @@ occ_status run_shared(occ_handle* h, const __nv_bfloat16* x, int n, cudaStream_t
             !make_tmap_out(h->tmCS1.bytes, h->hs.p, Fs, n_pad) || !make_tmap_out(h->tmCS2.bytes, h->ys.p, D, n_pad))
             return fail(OCC_ERR_CUDA, "cuTensorMapEncodeTiled failed (shared h)");
     }
+    return OCC_OK;
+}
+
+occ_status run_shared(occ_handle* h, const __nv_bfloat16* x, int n, cudaStream_t st) {
+    const int D = h->D, Fs = h->Fsh;
+    const size_t n_pad = (size_t)(n + kBM - 1) / kBM * kBM;
+    occ_status s0 = ensure_shared(h, n);
+    if (s0 != OCC_OK) return s0;
     if (!make_tmap_2d(h->tmAS1.bytes, x, D, (uint64_t)n, 64, kBM / 2))
         return fail(OCC_ERR_CUDA, "cuTensorMapEncodeTiled failed (tokens; x must be 16-byte aligned)");
     launch_shared_gate(n, (int)n_pad, D, x, h->sh_gate ? h->sgate.p : nullptr, h->sw.p, h->sh_grp.p, st);
@@ -1056,6 +1093,8 @@ static occ_status stage_device(occ_handle* h, int device) {
 
 extern "C" {
 
+static void sync_sibling(occ_handle* h);
+
 const char* occ_last_error(void) { return g_err.c_str(); }
 
 occ_status occ_dispatch(occ_handle* h, const void* x, const int32_t* ids, const float* weights, int n,
@@ -1175,6 +1214,7 @@ occ_status occ_create(const occ_config* cfg, const int32_t* placement, int world
     h->rank = rank;
     h->gated = c.activation == OCC_ACT_SWIGLU;
     if (const char* e = getenv("OCC_GEMM_GATHER")) h->gather_a = atoi(e);
+    if (const char* e = getenv("OCC_FUSED_PLAN")) h->fused_plan = atoi(e);
     h->plist.assign(placement, placement + h->E);
     occ_status s = validate_placement(c, placement, h->dev_of, h->slot_of);
     if (s != OCC_OK) { delete h; return s; }
@@ -1203,6 +1243,7 @@ occ_status occ_destroy(occ_handle* h) {
                     &h->in_src, &h->in_slot, &h->in_dev, &h->row_epd, &h->epd_src})
         b->release();
     h->offs.release();
+    h->fp_ws.release();
     h->stats.release();
     h->mask.release();
     h->rmask.release();
@@ -1363,6 +1404,7 @@ occ_status occ_load_shared_experts(occ_handle* h, int num_shared, int d_ff_share
     h->n_shared = S;
     h->Fsh = Fs;
     h->sh_cap = 0;  // h tensor map follows Fs
+    if (h->peer) return ensure_shared(h, h->peer_cap);  // no allocation on the peer forward path
     return OCC_OK;
 }
 
@@ -1436,6 +1478,13 @@ occ_status occ_router_logits(occ_handle* h, const void* x, const void* gate, int
 occ_status occ_set_grad_x_bf16(occ_handle* h, int on) {
     if (!h) return fail(OCC_ERR_ARG, "null handle");
     h->gx_bf16 = on ? 1 : 0;
+    return OCC_OK;
+}
+
+occ_status occ_set_plan_kernels(occ_handle* h, int fused) {
+    if (!h) return fail(OCC_ERR_ARG, "null handle");
+    h->fused_plan = fused ? 1 : 0;
+    if (h->sib) h->sib->fused_plan = h->fused_plan;
     return OCC_OK;
 }
 
@@ -1676,6 +1725,7 @@ static void sync_sibling(occ_handle* h) {
     b->router_mode = h->router_mode;
     b->num_sms = h->num_sms;
     b->gather_a = h->gather_a;
+    b->fused_plan = h->fused_plan;
 }
 
 static void unborrow(occ_handle* b) {
@@ -1754,6 +1804,19 @@ static occ_status forward_one(occ_handle* h, const void* x, const int32_t* ids, 
     CUDA_TRY(cudaMemsetAsync(h->err.p, 0, sizeof(int32_t), st));
     if (!h->in_ep) h->ev_recorded = 0;
     mark(h, ST_PLAN, st);
+    const bool gathered = h->gather_a && !h->training;
+    bool fused = h->fused_plan && dedup && !h->gather_a && h->fp_ws.p && fused_plan_supported(nd, h->E, k);
+    if (fused) {  // BRIM0 + routing rows + BRIM1 + Epd A operand in one cooperative kernel
+        const size_t nchunks = (size_t)(n + kRankChunk - 1) / kRankChunk;
+        const size_t K = (size_t)nd * (nd + 1) + (size_t)nd * h->E;
+        FusedPlanArgs fa{n, k, nd, h->E, P, D, ids, weights, sources, h->d_dev_of.p, h->d_slot_of.p,
+                         reinterpret_cast<const __nv_bfloat16*>(x), h->fp_ws.p, h->fp_ws.p + K * nchunks, h->dofs,
+                         h->d_tok_base, h->cofs, h->mask.p, h->tok_row.p, h->tok_sfd.p, h->lam.p, h->in_tok.p, h->in_src.p,
+                         h->in_slot.p, h->in_dev.p, h->in_ids.p, h->in_w.p, h->row_epd.p, h->epd_src.p, h->epd_j.p,
+                         h->epd_w.p, h->x_epd.p, h->stats.p, h->err.p};
+        fused = launch_fused_plan(fa, h->num_sms, st);
+    }
+    if (!fused) {  // the multi-kernel chain
     // 1. dispatch plan (BRIM0) and exchange placement
     s = run_plan(h, ids, weights, sources, n, st);
     if (s != OCC_OK) return s;
@@ -1783,12 +1846,12 @@ static occ_status forward_one(occ_handle* h, const void* x, const int32_t* ids, 
     // 4. grouped GEMM-1 (activation / SwiGLU, routing weight fused); its A rows
     // come straight from the inbox (TMA gather4) unless training needs the
     // Epd copy for the weight gradient
-    const bool gathered = h->gather_a && !h->training;
     if (!gathered) {  // Epd A operand: each token row read once, written to its Epd rows
         mark(h, ST_GATHER, st);
         launch_scatter_rows(R_max, R_total, P, D, reinterpret_cast<const __nv_bfloat16*>(x), h->in_tok.p,
                             h->row_epd.p, G * P, h->cofs, h->x_epd.p, st);
     }
+    }  // !fused
     mark(h, ST_GEMM1, st);
     launch_gemm1(h, G * P, st, gathered);
     mark(h, ST_GEMM2, st);
@@ -2311,6 +2374,10 @@ occ_status occ_comm_enable_peer(occ_handle* h, int max_tokens_per_rank) {
     CUDA_TRY(cudaMemset(h->flags.p, 0, sizeof(unsigned long long) * 3 * nd));
     CUDA_TRY(h->c_peer.ensure((size_t)nd * nd));
     CUDA_TRY(cudaMemset(h->c_peer.p, 0, sizeof(int) * nd * nd));
+    CUDA_TRY(h->peer_tab.ensure((size_t)h->world * kPeerSlots));
+    CUDA_TRY(h->peer_seq.ensure(1));
+    CUDA_TRY(cudaMemset(h->peer_seq.p, 0, sizeof(unsigned long long)));
+    if (h->n_shared > 0 && (s = ensure_shared(h, max_tokens_per_rank)) != OCC_OK) return s;
     CUDA_TRY(cudaDeviceSynchronize());
     const std::vector<void*> mine{h->in_x.p, h->in_ids.p, h->in_w.p, h->y_src.p, h->flags.p, h->c_peer.p};
     std::vector<void*> all;
@@ -2318,14 +2385,14 @@ occ_status occ_comm_enable_peer(occ_handle* h, int max_tokens_per_rank) {
     h->ipc_opened.clear();
     s = h->tp->exchange_pointers(mine, all, h->ipc_opened);
     if (s != OCC_OK) return s;
-    CUDA_TRY(h->peer_tab.ensure(all.size()));
     CUDA_TRY(cudaMemcpy(h->peer_tab.p, all.data(), sizeof(void*) * all.size(), cudaMemcpyHostToDevice));
     h->peer = true;
     h->peer_cap = max_tokens_per_rank;
-    CUDA_TRY(h->peer_seq.ensure(1));
-    CUDA_TRY(cudaMemset(h->peer_seq.p, 0, sizeof(unsigned long long)));
-    if (h->sib) return occ_comm_enable_peer(h->sib, max_tokens_per_rank);
-    return OCC_OK;
+    if (h->sib) {
+        sync_sibling(h);  // (the sibling pre-sizes the shared-expert buffers too)
+        if ((s = occ_comm_enable_peer(h->sib, max_tokens_per_rank)) != OCC_OK) return s;
+    }
+    return h->tp->barrier();
 }
 
 occ_status occ_set_micro_batches(occ_handle* h, int micro_batches, int comm_sms) {
@@ -2371,6 +2438,15 @@ occ_status occ_set_micro_batches(occ_handle* h, int micro_batches, int comm_sms)
     h->mb = 2;
     h->comm_sms = comm_sms >= 0 ? comm_sms : (h->world > 1 ? 16 : 0);
     h->num_sms = std::max(2, (h->full_sms - h->comm_sms) & ~1);
+    if (h->world > 1) {  // the sibling's first forward allocates nothing; every rank is set up
+        if (h->n_shared > 0) {
+            sync_sibling(h);
+            occ_status s = ensure_shared(h->sib, h->peer ? h->peer_cap : 1);
+            if (s != OCC_OK) return s;
+            CUDA_TRY(h->sib->sh_grp.ensure(4));
+        }
+        return h->tp->barrier();
+    }
     return OCC_OK;
 }
 

@@ -266,6 +266,35 @@ void launch_router_select(float* logits, int n, int e, int k, int renorm, PruneD
 void launch_transpose_weights(const __nv_bfloat16* w, int E, int K, int N, __nv_bfloat16* out, int out_rows_per_e,
                               int interleave_half, cudaStream_t st, int pitch = 0);
 
+// The whole one-GPU index chain in one cooperative kernel (occ_plan.cu):
+// BRIM0 + inbox records + routing rows + BRIM1 + Epd A operand + CommReport
+// counters.  world_size == 1, dedup, E <= 64, k <= 8.
+struct FusedPlanArgs {
+    int n, k, nd, E, P, D;
+    const int32_t* ids;
+    const float* w;
+    const int32_t* sources;  // null: round robin
+    const int32_t* dev_of;
+    const int32_t* slot_of;
+    const __nv_bfloat16* x;
+    int* chunk_cnt;          // [K * nchunks], K = nd(nd+1) + nd E
+    int* totals;             // [K]
+    DispatchOffsets dofs;
+    int* tok_base;           // [nd] prefix of tokens per source
+    ComputeOffsets cofs;
+    uint64_t* mask;          // [n] destination-device mask per token
+    int32_t *tok_row, *tok_sfd, *lam, *in_tok, *in_src, *in_slot, *in_dev, *in_ids;
+    float* in_w;
+    int32_t *row_epd, *epd_src, *epd_j;
+    float* epd_w;
+    __nv_bfloat16* x_epd;    // null: no A-operand copy (TMA gather path)
+    long long* stats;
+    int32_t* err;
+};
+bool fused_plan_supported(int nd, int E, int k);
+size_t fused_plan_ws(int n, int nd, int E);  // chunk_cnt + totals ints
+bool launch_fused_plan(const FusedPlanArgs& a, int num_sms, cudaStream_t st);
+
 // Grouped GEMM on tcgen05 (occ_gemm.cu).
 enum EpiMode {
     EPI_ACT_BF16 = 0,    // forward GEMM-1: act(acc) * w -> bf16 (+ pre-activation when training)

@@ -709,6 +709,15 @@ def test_multi_rank_forward_loopback(nd, ne, k, act, dedup, shared, peer, mb):
     errs = []
     starts = np.concatenate([[0], np.cumsum(n_per)])
     key = np.random.default_rng().integers(1 << 30)
+    # Ranks are threads sharing one GPU: a device-synchronising call on one
+    # thread (cudaFree from a caching-allocator flush) while another rank's
+    # arrival wait spins would stall until the wait times out, so all device
+    # tensors are made up front and converted only after every rank is done.
+    X = [cuda(x[starts[r]:starts[r + 1]], torch.bfloat16) for r in range(nd)]
+    I = [cuda(ids[starts[r]:starts[r + 1]]) for r in range(nd)]
+    Wt = [cuda(w[starts[r]:starts[r + 1]], torch.float32) for r in range(nd)]
+    OUT = [torch.empty_like(X[r]) for r in range(nd)]
+    done = threading.Barrier(nd)
 
     def rank_main(r):
         try:
@@ -727,14 +736,15 @@ def test_multi_rank_forward_loopback(nd, ne, k, act, dedup, shared, peer, mb):
                     layer.comm_enable_peer(128)
                 if mb > 1:  # two micro-batches per forward: sibling handle + split communicator
                     layer.set_micro_batches(mb)
-                a, b = starts[r], starts[r + 1]
                 for _rep in range(2 if peer else 1):  # peer mode: arrival flags advance per forward
-                    out = layer.forward_given_routing(cuda(x[a:b], torch.bfloat16), cuda(ids[a:b]),
-                                                      cuda(w[a:b], torch.float32))
+                    layer.forward_given_routing(X[r], I[r], Wt[r], out=OUT[r])
                 st.synchronize()
-                outs[r] = (out.double().cpu().numpy(), layer.comm_report(bytes_per_scalar=2))
+                rep_r = layer.comm_report(bytes_per_scalar=2)
+                done.wait()
+                outs[r] = (OUT[r].double().cpu().numpy(), rep_r)
         except Exception as e:  # surface thread failures
             errs.append(e)
+            done.abort()
 
     ths = [threading.Thread(target=rank_main, args=(r,)) for r in range(nd)]
     for t in ths:
@@ -795,6 +805,13 @@ def test_multi_rank_backward_loopback(nd, ne, k, act, dedup, peer):
     errs = []
     starts = np.concatenate([[0], np.cumsum(n_per)])
     key = np.random.default_rng().integers(1 << 30)
+    sl = [slice(starts[r], starts[r + 1]) for r in range(nd)]  # device inputs up front (see the forward test)
+    X = [cuda(x[q], torch.bfloat16) for q in sl]
+    I = [cuda(ids[q]) for q in sl]
+    Wt = [cuda(w[q], torch.float32) for q in sl]
+    U = [cuda(up[q], torch.bfloat16) for q in sl]
+    OUT = [torch.empty_like(t) for t in X]
+    done = threading.Barrier(nd)
 
     def rank_main(r):
         try:
@@ -809,15 +826,15 @@ def test_multi_rank_backward_loopback(nd, ne, k, act, dedup, peer):
                 layer.comm_init_loopback(int(key))
                 if peer:
                     layer.comm_enable_peer(128)
-                a, b = starts[r], starts[r + 1]
                 for _rep in range(2):  # a second step reuses every buffer
-                    layer.forward_given_routing(cuda(x[a:b], torch.bfloat16), cuda(ids[a:b]),
-                                                cuda(w[a:b], torch.float32))
-                    gr = layer.backward(cuda(up[a:b], torch.bfloat16))
+                    layer.forward_given_routing(X[r], I[r], Wt[r], out=OUT[r])
+                    gr = layer.backward(U[r])
                 st.synchronize()
+                done.wait()
                 grads[r] = {kk: (v.cpu().numpy() if v is not None else None) for kk, v in gr.items()}
         except Exception as e:  # surface thread failures
             errs.append(e)
+            done.abort()
 
     ths = [threading.Thread(target=rank_main, args=(r,)) for r in range(nd)]
     for t in ths:
@@ -1521,3 +1538,41 @@ def test_multi_rank_peer_forward_graph_replay_loopback(nd, ne, k):
         t.join(timeout=180)
     assert not errs, errs
     assert all(ok)
+
+
+@pytest.mark.parametrize("ne,k,nd,dm,dh,act,n,srcmode", [(8, 2, 2, 256, 512, "silu", 1000, "rr"),
+                                                         (64, 8, 8, 256, 256, "swiglu", 3000, "random"),
+                                                         (60, 4, 4, 128, 256, "relu", 777, "random"),
+                                                         (8, 2, 1, 512, 1024, "silu", 4097, "rr"),
+                                                         (16, 3, 4, 128, 128, "identity", 1, "rr"),
+                                                         (64, 6, 8, 128, 128, "silu", 70000, "random")])
+def test_fused_plan_kernel_equals_multi_kernel_chain(ne, k, nd, dm, dh, act, n, srcmode):
+    """The one-GPU index chain as one cooperative kernel (occ_plan.cu, the
+    default) equals the multi-kernel chain bit for bit: layer output, inbox
+    records, BRIM1, CommReport, and the backward that consumes the saved
+    grouping."""
+    gated = act == "swiglu"
+    x, g, w1, w2, w3 = make_layer_inputs(ne + n, n, dm, dh, ne, gated=gated)
+    ids, w = random_routing(n, ne, k, np.random.default_rng(n))
+    plist = _placement(ne, nd, "shuffled", seed=n)
+    src = None if srcmode == "rr" else cuda(np.random.default_rng(1).integers(0, nd, n).astype(np.int32))
+    up = cuda(np.random.default_rng(2).uniform(-1, 1, (n, dm)), torch.bfloat16)
+    res = []
+    for fused in (True, False):
+        layer = occ.ExpertParallelLayer(occ.MoEConfig(ne, k, nd, dm, dh, activation=act),
+                                        occ.Placement([list(map(int, p)) for p in plist]))
+        layer.set_plan_kernels(fused)
+        layer.set_training(True)
+        layer.load_experts(cuda(w1, torch.bfloat16), cuda(w2, torch.bfloat16), cuda(w3, torch.bfloat16) if gated else None)
+        out = layer.forward_given_routing(cuda(x, torch.bfloat16), cuda(ids), cuda(w, torch.float32), src)
+        rep = layer.comm_report(bytes_per_scalar=2)
+        idx = [t.cpu() for t in layer.saved_index()[:4]]
+        gr = layer.backward(up)
+        res.append((out.cpu(), rep, idx, {kk: v.cpu() for kk, v in gr.items() if v is not None}))
+    (o1, r1, i1, g1), (o2, r2, i2, g2) = res
+    assert torch.equal(o1, o2)
+    assert r1 == r2
+    for a, b in zip(i1, i2):
+        assert torch.equal(a, b)
+    for kk in g1:
+        assert torch.equal(g1[kk], g2[kk]), kk
