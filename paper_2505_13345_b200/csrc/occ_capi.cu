@@ -718,7 +718,7 @@ occ_status ensure_ws(occ_handle* h, int n) {
     if (h->world == 1) {
         occ_status s = ensure_recv(h, (size_t)n * span_max, (size_t)n * k);
         if (s != OCC_OK) return s;
-        if (dedup && fused_plan_supported(nd, h->E, k)) CUDA_TRY(h->fp_ws.ensure(fused_plan_ws(n, nd, h->E)));
+        if (dedup && fused_plan_supported(nd, h->E, k)) CUDA_TRY(h->fp_ws.ensure(fused_plan_ws(n, nd, h->E, k)));
     }
     h->n_cap = n;
     return OCC_OK;
@@ -1807,14 +1807,24 @@ static occ_status forward_one(occ_handle* h, const void* x, const int32_t* ids, 
     const bool gathered = h->gather_a && !h->training;
     bool fused = h->fused_plan && dedup && !h->gather_a && h->fp_ws.p && fused_plan_supported(nd, h->E, k);
     if (fused) {  // BRIM0 + routing rows + BRIM1 + Epd A operand in one cooperative kernel
-        const size_t nchunks = (size_t)(n + kRankChunk - 1) / kRankChunk;
         const size_t K = (size_t)nd * (nd + 1) + (size_t)nd * h->E;
+        const size_t nchunks = fused_plan_chunks(n, k);
         FusedPlanArgs fa{n, k, nd, h->E, P, D, ids, weights, sources, h->d_dev_of.p, h->d_slot_of.p,
                          reinterpret_cast<const __nv_bfloat16*>(x), h->fp_ws.p, h->fp_ws.p + K * nchunks, h->dofs,
                          h->d_tok_base, h->cofs, h->mask.p, h->tok_row.p, h->tok_sfd.p, h->lam.p, h->in_tok.p, h->in_src.p,
                          h->in_slot.p, h->in_dev.p, h->in_ids.p, h->in_w.p, h->row_epd.p, h->epd_src.p, h->epd_j.p,
                          h->epd_w.p, h->x_epd.p, h->stats.p, h->err.p};
+        // the Epd A rows: copied inside the cooperative kernel for small batches
+        // (no extra launch), by the full-occupancy scatter kernel for large ones
+        static const int scatter_env = getenv("OCC_PLAN_SCATTER") ? atoi(getenv("OCC_PLAN_SCATTER")) : -1;
+        const long copy_bytes = (long)n * std::min(k, nd) * D * 2;
+        fa.scatter = scatter_env >= 0 ? scatter_env : copy_bytes <= (64l << 20);
         fused = launch_fused_plan(fa, h->num_sms, st);
+        if (fused && !fa.scatter) {
+            mark(h, ST_GATHER, st);
+            launch_scatter_rows((int)h->R_max, h->dofs.in_base + nd, P, D, reinterpret_cast<const __nv_bfloat16*>(x),
+                                h->in_tok.p, h->row_epd.p, nd * P, h->cofs, h->x_epd.p, st);
+        }
     }
     if (!fused) {  // the multi-kernel chain
     // 1. dispatch plan (BRIM0) and exchange placement

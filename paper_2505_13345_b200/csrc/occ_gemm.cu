@@ -1249,7 +1249,10 @@ void launch_grouped_gemm(EpiMode mode, const GemmArgs& a, int num_sms, cudaStrea
         // an odd block count ends in a single-block super-tile: supported (forced mode) but
         // measured 3% slower than the narrow kernel on DeepSeek's 11 blocks, so auto needs even
         const bool ok = (nbk % 2 == 0 || (nbk >= 5 && wide_env == 2)) && (mode != EPI_SWIGLU_BF16 || a.N % 128 == 0);
-        if (ok && (wide_env == 2 || (wide_env == 1 && a.K >= 1024))) {
+        // (auto also needs at least one full wave of narrow tiles: with fewer,
+        // halving the tile count only lengthens each pair's serial K loop --
+        // small batches, C1 GEMM-2 31 -> 20 us with narrow tiles)
+        if (ok && (wide_env == 2 || (wide_env == 1 && a.K >= 1024 && a.max_tiles >= num_sms))) {
             if (mode == EPI_ACT_BF16) launch_wide<EPI_ACT_BF16>(grid, ta, tb, tc, p, st);
             else launch_wide<EPI_SWIGLU_BF16>(grid, ta, tb, tc, p, st);
             wide = true;

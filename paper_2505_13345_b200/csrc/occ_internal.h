@@ -268,7 +268,7 @@ void launch_transpose_weights(const __nv_bfloat16* w, int E, int K, int N, __nv_
 
 // The whole one-GPU index chain in one cooperative kernel (occ_plan.cu):
 // BRIM0 + inbox records + routing rows + BRIM1 + Epd A operand + CommReport
-// counters.  world_size == 1, dedup, E <= 64, k <= 8.
+// counters.  world_size == 1, dedup, k <= 32, tables within 96 KB of shared memory.
 struct FusedPlanArgs {
     int n, k, nd, E, P, D;
     const int32_t* ids;
@@ -290,9 +290,12 @@ struct FusedPlanArgs {
     __nv_bfloat16* x_epd;    // null: no A-operand copy (TMA gather path)
     long long* stats;
     int32_t* err;
+    int scatter = 1;         // copy the Epd A rows in the kernel (else the caller runs launch_scatter_rows)
+    unsigned long long* dbg = nullptr;  // OCC_PLAN_DEBUG phase timeline
 };
 bool fused_plan_supported(int nd, int E, int k);
-size_t fused_plan_ws(int n, int nd, int E);  // chunk_cnt + totals ints
+size_t fused_plan_chunks(int n, int k);            // rank chunks of n tokens
+size_t fused_plan_ws(int n, int nd, int E, int k);  // chunk_cnt + totals ints
 bool launch_fused_plan(const FusedPlanArgs& a, int num_sms, cudaStream_t st);
 
 // Grouped GEMM on tcgen05 (occ_gemm.cu).

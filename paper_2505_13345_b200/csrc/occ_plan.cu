@@ -39,6 +39,8 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "occ_common.cuh"
 #include "occ_internal.h"
@@ -48,112 +50,128 @@ namespace cg = cooperative_groups;
 namespace occ {
 namespace {
 
-constexpr int kThreads = 256;  // = kRankChunk tokens per chunk, 8 warps
+constexpr int kThreads = 256;  // 8 warps per block
 constexpr int kWarps = kThreads / 32;
 
 struct Tables {  // phase C results, in shared memory
-    int *C, *off_sd, *inoff, *in_base, *ntok, *tok_base, *cnt, *seg_base, *ebase;
+    int *C, *off_sd, *inoff, *in_base, *ntok, *tok_base, *cnt, *seg_base, *ebase, *padpre, *dev, *slot;
 };
 
 __device__ __forceinline__ int token_src(const FusedPlanArgs& a, int t) {
     return a.sources ? a.sources[t] : t % a.nd;
 }
 
-// Token t's validated routing: device mask, expert mask, source (dropped
-// token: masks 0, source 0 -- the forward reports the error, as plan_mask).
-__device__ __forceinline__ void token_masks(const FusedPlanArgs& a, int t, uint64_t& dm, uint64_t& em, int& s) {
-    dm = 0, em = 0;
-    s = token_src(a, t);
-    if (s < 0 || s >= a.nd) {
-        atomicExch(a.err, 1);
-        s = 0;
-        return;
+constexpr unsigned kFull = 0xffffffffu;
+
+// One routing entry (token t, slot j) per lane: a warp covers tpw = 32 / k
+// tokens (lanes >= tpw * k idle), a block chunk 8 * tpw tokens.  Everything a
+// lane needs about its token comes from the token's other lanes by shuffles
+// (the token's lanes are adjacent: tok0 .. tok0 + k - 1).
+struct Entry {
+    int t, j, s, e, d, p;   // e, d, p = -1 unless the entry is valid
+    float w;
+    bool in;                // a token of the batch
+    bool valid;             // its routing is valid (RoutingOutcome::validate)
+    bool owner;             // first entry of the token on device d: holds the (t, d) Sfd / inbox row
+    int owner_lane;         // lane of that owner
+    uint64_t dm;            // the token's destination-device mask (0 for an invalid token)
+    uint64_t smask;         // the token's local-slot mask on device d
+    int tok0;
+};
+
+__device__ __forceinline__ Entry load_entry(const FusedPlanArgs& a, const Tables& T, int c, int tpw, int warp,
+                                            int lane) {
+    Entry x;
+    const int k = a.k;
+    const int lt = lane / k;
+    x.j = lane - lt * k;
+    x.tok0 = lane - x.j;
+    x.t = c * kWarps * tpw + warp * tpw + lt;
+    x.in = lt < tpw && x.t < a.n;
+    int e = -1, s = 0;
+    float w = 0.0f;
+    if (x.in) {
+        e = a.ids[(long)x.t * k + x.j];
+        w = a.w[(long)x.t * k + x.j];
+        s = token_src(a, x.t);
     }
-    for (int j = 0; j < a.k; ++j) {
-        const int e = a.ids[(long)t * a.k + j];
-        const float wt = a.w[(long)t * a.k + j];
-        bool bad = e < 0 || e >= a.E || !(wt > 0.0f);
-        for (int l = 0; l < j && !bad; ++l) bad = a.ids[(long)t * a.k + l] == e;
-        if (bad) {
-            atomicExch(a.err, 4);
-            dm = em = 0;
-            s = 0;
-            return;
-        }
-        dm |= 1ull << a.dev_of[e];
-        em |= 1ull << e;
+    const bool badsrc = x.in && (s < 0 || s >= a.nd);
+    bool bad = x.in && (e < 0 || e >= a.E || !(w > 0.0f));
+    const int de = x.in && !bad ? T.dev[e] : -1;
+    const int pe = x.in && !bad ? T.slot[e] : -1;
+    int jfirst = x.j;  // first slot of this token on device de
+    uint64_t dm = 0, sm = 0;
+    for (int jj = 0; jj < k; ++jj) {  // the token's other entries (uniform loop)
+        const int src = min(x.tok0 + jj, 31);
+        const int oe = __shfl_sync(kFull, e, src);
+        const int od = __shfl_sync(kFull, de, src);
+        const int op = __shfl_sync(kFull, pe, src);
+        if (jj != x.j && oe == e) bad = true;  // duplicate expert id
+        if (jj < jfirst && od == de) jfirst = jj;
+        if (od >= 0) dm |= 1ull << od;
+        if (od >= 0 && od == de) sm |= 1ull << op;
     }
+    bool tbad = bad || badsrc, any_bad = false, any_src = false;
+    for (int jj = 0; jj < k; ++jj) {
+        const int src = min(x.tok0 + jj, 31);
+        any_bad |= __shfl_sync(kFull, tbad, src);
+        any_src |= __shfl_sync(kFull, badsrc, src);
+    }
+    if (x.in && x.j == 0 && any_bad) atomicExch(a.err, any_src ? 1 : 4);  // ShapeError / RoutingError
+    x.valid = x.in && !any_bad;
+    // an invalid token is planned with no destinations and source 0 (as plan_mask)
+    x.s = any_bad ? 0 : s;
+    x.e = x.valid ? e : -1;
+    x.d = x.valid ? de : -1;
+    x.p = x.valid ? pe : -1;
+    x.w = w;
+    x.dm = x.valid ? dm : 0;
+    x.smask = sm;
+    x.owner = x.valid && jfirst == x.j;
+    x.owner_lane = x.tok0 + jfirst;
+    return x;
 }
 
-// Per-warp counts of every key held by this warp's tokens.
-__device__ __forceinline__ void warp_counts(const FusedPlanArgs& a, int valid, int s, uint64_t dm, uint64_t em,
-                                            int* wk, int lane) {
-    const int KD = a.nd * (a.nd + 1);
-    const uint32_t same = __match_any_sync(0xffffffffu, valid ? s : -1);
-    const bool leader = valid && (__ffs(same) - 1) == lane;
-    for (int d = 0; d < a.nd; ++d) {
-        const uint32_t b = __ballot_sync(0xffffffffu, valid && ((dm >> d) & 1));
-        if (leader) wk[s * (a.nd + 1) + d] = __popc(b & same);
-    }
-    if (leader) wk[s * (a.nd + 1) + a.nd] = __popc(same);
-    for (int e = 0; e < a.E; ++e) {
-        const uint32_t b = __ballot_sync(0xffffffffu, valid && ((em >> e) & 1));
-        if (leader) wk[KD + s * a.E + e] = __popc(b & same);
-    }
+// Per-warp key counts into wk[key] (zeroed): the leader of each equal-key
+// lane group writes the group size.  Keys: dispatch (s, d) per owner entry,
+// source group (s) per token, expert (s, e) per valid entry.
+__device__ __forceinline__ void entry_counts(const FusedPlanArgs& a, const Entry& x, int* wk, int lane,
+                                             uint32_t& md, uint32_t& mg, uint32_t& me) {
+    const int nd = a.nd, KD = nd * (nd + 1);
+    const int kd = x.owner ? x.s * (nd + 1) + x.d : -1;
+    const int kg = x.in && x.j == 0 ? x.s * (nd + 1) + nd : -1;
+    const int ke = x.valid ? KD + x.s * a.E + x.e : -1;
+    md = __match_any_sync(kFull, kd);
+    mg = __match_any_sync(kFull, kg);
+    me = __match_any_sync(kFull, ke);
+    if (kd >= 0 && __ffs(md) - 1 == lane) wk[kd] = __popc(md);
+    if (kg >= 0 && __ffs(mg) - 1 == lane) wk[kg] = __popc(mg);
+    if (ke >= 0 && __ffs(me) - 1 == lane) wk[ke] = __popc(me);
+}
+
+// OCC_PLAN_DEBUG: earliest block start / latest phase end over all blocks (ns).
+__device__ __forceinline__ void phase_mark(const FusedPlanArgs& a, int i) {
+    if (!a.dbg || threadIdx.x) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (i == 0) atomicMin(a.dbg, t);
+    else atomicMax(a.dbg + i, t);
 }
 
 __global__ void __launch_bounds__(kThreads) fused_plan_kernel(FusedPlanArgs a) {
+    phase_mark(a, 0);
     extern __shared__ int smem[];
     cg::grid_group grid = cg::this_grid();
     const int nd = a.nd, E = a.E, P = a.P, k = a.k;
     const int KD = nd * (nd + 1), K = KD + nd * E;
-    const int nchunks = (a.n + kThreads - 1) / kThreads;
+    const int tpw = 32 / k;                     // tokens per warp (one lane per routing entry)
+    const int tpb = kWarps * tpw;               // tokens per block chunk
+    const int nchunks = (a.n + tpb - 1) / tpb;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    int* wcnt = smem;  // [kWarps][K]
-    int* tab = wcnt + kWarps * K;
-
-    // ---------------------------------------------------------------- A --
-    for (int c = blockIdx.x; c < nchunks; c += gridDim.x) {
-        for (int i = threadIdx.x; i < kWarps * K; i += kThreads) wcnt[i] = 0;
-        __syncthreads();
-        const int t = c * kThreads + threadIdx.x;
-        const int valid = t < a.n;
-        uint64_t dm = 0, em = 0;
-        int s = 0;
-        if (valid) token_masks(a, t, dm, em, s);
-        warp_counts(a, valid, s, dm, em, wcnt + warp * K, lane);
-        __syncthreads();
-        for (int key = threadIdx.x; key < K; key += kThreads) {
-            int sum = 0;
-            for (int w = 0; w < kWarps; ++w) sum += wcnt[w * K + key];
-            a.chunk_cnt[(long)key * nchunks + c] = sum;
-        }
-        __syncthreads();
-    }
-    grid.sync();
-    // ---------------------------------------------------------------- B --
-    const int gw = (blockIdx.x * kThreads + threadIdx.x) >> 5, nw = gridDim.x * kWarps;
-    for (int key = gw; key < K; key += nw) {
-        int* row = a.chunk_cnt + (long)key * nchunks;
-        int run = 0;
-        for (int c0 = 0; c0 < nchunks; c0 += 32) {
-            const int c = c0 + lane;
-            const int v = c < nchunks ? row[c] : 0;
-            int x = v;
-            for (int o = 1; o < 32; o <<= 1) {
-                const int u = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += u;
-            }
-            if (c < nchunks) row[c] = run + x - v;
-            run += __shfl_sync(0xffffffffu, x, 31);
-        }
-        if (lane == 0) a.totals[key] = run;
-    }
-    grid.sync();
-    // ---------------------------------------------------------------- C --
+    int* wcnt = smem;  // [kWarps][K] per-warp key counts / bases (phase C: the totals)
     Tables T;
     {
-        int* p = tab;
+        int* p = wcnt + kWarps * K;
         T.C = p, p += nd * nd;
         T.off_sd = p, p += nd * nd;
         T.inoff = p, p += nd * nd;
@@ -162,15 +180,81 @@ __global__ void __launch_bounds__(kThreads) fused_plan_kernel(FusedPlanArgs a) {
         T.tok_base = p, p += nd;
         T.cnt = p, p += E;        // per group g = (d, p), E = nd * P groups
         T.seg_base = p, p += E;
-        T.ebase = p;               // [nd][E]
+        T.padpre = p, p += E + 1; // prefix of padding rows per group
+        T.dev = p, p += E;
+        T.slot = p, p += E;
+        T.ebase = p, p += nd * E; // [nd][E]
     }
-    for (int i = threadIdx.x; i < nd * nd; i += kThreads) T.C[i] = a.totals[(i / nd) * (nd + 1) + i % nd];
-    for (int g = threadIdx.x; g < E; g += kThreads) T.cnt[g] = 0;
+    // global warp index, spread so consecutive work items land on different SMs
+    // (blocks are placed round-robin over the SMs)
+    const int gw = warp * gridDim.x + blockIdx.x, nw = gridDim.x * kWarps;
+    for (int e = threadIdx.x; e < E; e += kThreads) {
+        T.dev[e] = a.dev_of[e];
+        T.slot[e] = a.slot_of[e];
+    }
     __syncthreads();
+
+    // ---------------------------------------------------------------- A --
+    for (int c = blockIdx.x; c < nchunks; c += gridDim.x) {
+        for (int i = threadIdx.x; i < kWarps * K; i += kThreads) wcnt[i] = 0;
+        __syncthreads();
+        const Entry x = load_entry(a, T, c, tpw, warp, lane);
+        uint32_t md, mg, me;
+        entry_counts(a, x, wcnt + warp * K, lane, md, mg, me);
+        __syncthreads();
+        for (int key = threadIdx.x; key < K; key += kThreads) {
+            int sum = 0;
+            for (int w = 0; w < kWarps; ++w) sum += wcnt[w * K + key];
+            a.chunk_cnt[(long)key * nchunks + c] = sum;
+        }
+        __syncthreads();
+    }
+    phase_mark(a, 1);
+    grid.sync();
+    // ---------------------------------------------------------------- B --
+    // one block per key: each thread scans a contiguous run of chunks (loads
+    // independent, in flight together), block exclusive scan of the run sums
+    {
+        __shared__ int s_part[kWarps];
+        const int per = (nchunks + kThreads - 1) / kThreads;
+        for (int key = blockIdx.x; key < K; key += gridDim.x) {
+            int* row = a.chunk_cnt + (long)key * nchunks;
+            const int c0 = threadIdx.x * per, c1 = min(c0 + per, nchunks);
+            int local = 0;
+            for (int c = c0; c < c1; ++c) local += row[c];
+            int x = local;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(kFull, x, o);
+                if (lane >= o) x += y;
+            }
+            if (lane == 31) s_part[warp] = x;
+            __syncthreads();
+            int wbase = 0, total = 0;
+            for (int w = 0; w < kWarps; ++w) {
+                if (w < warp) wbase += s_part[w];
+                total += s_part[w];
+            }
+            int run = wbase + x - local;
+            for (int c = c0; c < c1; ++c) {
+                const int v = row[c];
+                row[c] = run;
+                run += v;
+            }
+            if (threadIdx.x == 0) a.totals[key] = total;
+            __syncthreads();
+        }
+    }
+    phase_mark(a, 2);
+    grid.sync();
+    // ---------------------------------------------------------------- C --
+    int* tot = wcnt;  // the K totals, staged
+    for (int i = threadIdx.x; i < K; i += kThreads) tot[i] = a.totals[i];
+    __syncthreads();
+    for (int i = threadIdx.x; i < nd * nd; i += kThreads) T.C[i] = tot[(i / nd) * (nd + 1) + i % nd];
     for (int e = threadIdx.x; e < E; e += kThreads) {  // group counts from the expert keys
         int c = 0;
-        for (int s = 0; s < nd; ++s) c += a.totals[KD + s * E + e];
-        T.cnt[a.dev_of[e] * P + a.slot_of[e]] = c;
+        for (int s = 0; s < nd; ++s) c += tot[KD + s * E + e];
+        T.cnt[T.dev[e] * P + T.slot[e]] = c;
     }
     __syncthreads();
     if (threadIdx.x < nd) {  // per source: counter offsets (device-major), token counts
@@ -180,7 +264,7 @@ __global__ void __launch_bounds__(kThreads) fused_plan_kernel(FusedPlanArgs a) {
             T.off_sd[s * nd + d] = run;
             run += T.C[s * nd + d];
         }
-        T.ntok[s] = a.totals[s * (nd + 1) + nd];
+        T.ntok[s] = tot[s * (nd + 1) + nd];
     } else if (threadIdx.x >= 64 && threadIdx.x < 64 + nd) {  // per destination: inbox offsets
         const int d = threadIdx.x - 64;
         int run = 0;
@@ -190,11 +274,15 @@ __global__ void __launch_bounds__(kThreads) fused_plan_kernel(FusedPlanArgs a) {
         }
         T.in_base[d] = run;  // R_d for now
     } else if (threadIdx.x == 128) {  // Epd segments: padded to the 256-row GEMM tile
-        int run = 0;
+        int run = 0, pad = 0;
         for (int g = 0; g < E; ++g) {
             T.seg_base[g] = run;
-            run += (T.cnt[g] + kBM - 1) / kBM * kBM;
+            const int m = (T.cnt[g] + kBM - 1) / kBM * kBM;
+            T.padpre[g] = pad;
+            pad += m - T.cnt[g];
+            run += m;
         }
+        T.padpre[E] = pad;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -212,10 +300,10 @@ __global__ void __launch_bounds__(kThreads) fused_plan_kernel(FusedPlanArgs a) {
     }
     __syncthreads();
     for (int e = threadIdx.x; e < E; e += kThreads) {  // Epd base of (source, expert)
-        int run = T.seg_base[a.dev_of[e] * P + a.slot_of[e]];
+        int run = T.seg_base[T.dev[e] * P + T.slot[e]];
         for (int s = 0; s < nd; ++s) {
             T.ebase[s * E + e] = run;
-            run += a.totals[KD + s * E + e];
+            run += tot[KD + s * E + e];
         }
     }
     __syncthreads();
@@ -267,85 +355,83 @@ __global__ void __launch_bounds__(kThreads) fused_plan_kernel(FusedPlanArgs a) {
             a.stats[6] = nepd;
         }
     }
+    phase_mark(a, 3);
+    __syncthreads();  // (the staged totals in wcnt are dead from here)
     // ---------------------------------------------------------------- D --
     long long st_naive = 0, st_span = 0, st_intra = 0, st_inter = 0;
     for (int c = blockIdx.x; c < nchunks; c += gridDim.x) {
         for (int i = threadIdx.x; i < kWarps * K; i += kThreads) wcnt[i] = 0;
         __syncthreads();
-        const int t = c * kThreads + threadIdx.x;
-        const int valid = t < a.n;
-        uint64_t dm = 0, em = 0;
-        int s = 0;
-        if (valid) token_masks(a, t, dm, em, s);
-        warp_counts(a, valid, s, dm, em, wcnt + warp * K, lane);
+        const Entry x = load_entry(a, T, c, tpw, warp, lane);
+        uint32_t md, mg, me;
+        entry_counts(a, x, wcnt + warp * K, lane, md, mg, me);
         __syncthreads();
         for (int key = threadIdx.x; key < K; key += kThreads) {  // exclusive bases per warp
             int run = a.chunk_cnt[(long)key * nchunks + c];
             for (int w = 0; w < kWarps; ++w) {
-                const int x = wcnt[w * K + key];
+                const int v = wcnt[w * K + key];
                 wcnt[w * K + key] = run;
-                run += x;
+                run += v;
             }
         }
         __syncthreads();
         const int* wb = wcnt + warp * K;
-        const uint32_t same = __match_any_sync(0xffffffffu, valid ? s : -1);
         const uint32_t lt = lanemask_lt();
-        int rows[kMaxDev > 64 ? 64 : kMaxDev];  // inbox row per destination device (dedup)
-        if (valid) {
-            a.lam[t] = wb[s * (nd + 1) + nd] + __popc(same & lt);
-            a.mask[t] = dm;  // destination devices (combine, backward)
-        }
-        for (int d = 0; d < nd; ++d) {
-            const bool hit = valid && ((dm >> d) & 1);
-            const uint32_t b = __ballot_sync(0xffffffffu, hit);
-            if (!valid) continue;
+        const int s = x.s, t = x.t, d = x.d;
+        int row = -1, cc = -1;
+        if (x.owner) {  // BRIM0 counter and inbox row of (t, d)
+            const int r = wb[s * (nd + 1) + d] + __popc(md & lt);
+            cc = T.off_sd[s * nd + d] + r;
+            row = T.in_base[d] + T.inoff[d * nd + s] + r;
             const long slot = (long)t * nd + d;
-            if (!hit) {
-                a.tok_sfd[slot] = -1;
-                a.tok_row[slot] = -1;
-                continue;
-            }
-            const int r = wb[s * (nd + 1) + d] + __popc(b & same & lt);
-            const int cc = T.off_sd[s * nd + d] + r;
-            const int row = T.in_base[d] + T.inoff[d * nd + s] + r;
-            rows[d] = row;
             a.tok_sfd[slot] = cc;
             a.tok_row[slot] = row;
             a.in_tok[row] = t;
             a.in_src[row] = s;
             a.in_slot[row] = cc;
             a.in_dev[row] = d;
-            for (int j = 0; j < k; ++j) {  // the routing row carried with the inbox row
-                a.in_ids[(long)row * k + j] = a.ids[(long)t * k + j];
-                a.in_w[(long)row * k + j] = a.w[(long)t * k + j];
+            for (int p = 0; p < P; ++p)  // slots of this row the token does not use
+                if (!((x.smask >> p) & 1)) a.row_epd[(long)row * P + p] = -1;
+        }
+        const int my_row = __shfl_sync(kFull, row, x.owner_lane);
+        for (int jj = 0; jj < k; ++jj) {  // the routing row carried with each of the token's inbox rows
+            const int src = min(x.tok0 + jj, 31);
+            const int oe = __shfl_sync(kFull, x.e, src);
+            const float ow = __shfl_sync(kFull, x.w, src);
+            if (x.owner) {
+                a.in_ids[(long)row * k + jj] = oe;
+                a.in_w[(long)row * k + jj] = ow;
             }
-            for (int p = 0; p < P; ++p) a.row_epd[(long)row * P + p] = -1;
         }
-        for (int e = 0; e < E; ++e) {
-            const bool hit = valid && ((em >> e) & 1);
-            const uint32_t b = __ballot_sync(0xffffffffu, hit);
-            if (!hit) continue;
-            const int q = T.ebase[s * E + e] + wb[KD + s * E + e] + __popc(b & same & lt);
-            const int d = a.dev_of[e], p = a.slot_of[e];
-            int j = 0;
-            while (a.ids[(long)t * k + j] != e) ++j;
-            const int row = rows[d];
-            a.row_epd[(long)row * P + p] = q;
-            a.epd_src[q] = row;
-            a.epd_w[q] = a.w[(long)t * k + j];
-            a.epd_j[q] = j;
-        }
-        if (valid && dm) {  // CommReport (collab.cpp:41-118): span, naive crossings, pair shares
-            st_span += __popcll(dm);
-            for (int j = 0; j < k; ++j) {
-                const int dj = a.dev_of[a.ids[(long)t * k + j]];
-                st_naive += dj != s;
-                for (int l = j + 1; l < k; ++l) {
-                    if (a.dev_of[a.ids[(long)t * k + l]] == dj) ++st_intra;
-                    else ++st_inter;
+        if (x.in) {
+            for (int dd = x.j; dd < nd; dd += k)  // devices the token does not reach
+                if (!((x.dm >> dd) & 1)) {
+                    a.tok_sfd[(long)t * nd + dd] = -1;
+                    a.tok_row[(long)t * nd + dd] = -1;
                 }
+            if (x.j == 0) {
+                a.lam[t] = wb[s * (nd + 1) + nd] + __popc(mg & lt);
+                a.mask[t] = x.dm;
             }
+        }
+        if (x.valid) {  // BRIM1: the Epd row of (t, e), expert-major over device d's inbox
+            const int q = T.ebase[s * E + x.e] + wb[KD + s * E + x.e] + __popc(me & lt);
+            a.row_epd[(long)my_row * P + x.p] = q;
+            a.epd_src[q] = my_row;
+            a.epd_w[q] = x.w;
+            a.epd_j[q] = x.j;
+        }
+        // CommReport (collab.cpp:41-118): span, naive crossings, co-activated pair shares
+        for (int jj = 0; jj < k; ++jj) {
+            const int od = __shfl_sync(kFull, d, min(x.tok0 + jj, 31));
+            if (x.valid && jj > x.j) {
+                if (od == d) ++st_intra;
+                else ++st_inter;
+            }
+        }
+        if (x.valid) {
+            st_naive += d != s;
+            if (x.j == 0) st_span += __popcll(x.dm);
         }
         __syncthreads();
     }
@@ -361,29 +447,36 @@ __global__ void __launch_bounds__(kThreads) fused_plan_kernel(FusedPlanArgs a) {
         atomicAdd(reinterpret_cast<unsigned long long*>(&a.stats[3]), (unsigned long long)st_intra);
         atomicAdd(reinterpret_cast<unsigned long long*>(&a.stats[4]), (unsigned long long)st_inter);
     }
-    // padding rows of every segment: no source row, zero weight, zero A row
-    for (int g = blockIdx.x; g < E; g += gridDim.x) {
-        const int lo = T.seg_base[g] + T.cnt[g], hi = T.seg_base[g] + (T.cnt[g] + kBM - 1) / kBM * kBM;
-        for (int q = lo + threadIdx.x; q < hi; q += kThreads) {
-            a.epd_src[q] = -1;
-            a.epd_w[q] = 0.0f;
-        }
-        if (a.x_epd) {
-            uint4* base = reinterpret_cast<uint4*>(a.x_epd + (long)lo * a.D);
-            const long nv = (long)(hi - lo) * a.D / 8;
-            for (long v = threadIdx.x; v < nv; v += kThreads) base[v] = make_uint4(0, 0, 0, 0);
-        }
+    // padding rows of every segment: no source row, zero weight
+    for (int pr = blockIdx.x * kThreads + threadIdx.x; pr < T.padpre[E]; pr += gridDim.x * kThreads) {
+        int g = 0;
+        while (T.padpre[g + 1] <= pr) ++g;
+        const int q = T.seg_base[g] + T.cnt[g] + (pr - T.padpre[g]);
+        a.epd_src[q] = -1;
+        a.epd_w[q] = 0.0f;
     }
-    if (!a.x_epd) return;
+    phase_mark(a, 4);
+    if (!a.scatter) return;  // large batches: the Epd rows are copied by a full-occupancy kernel
     grid.sync();
     // ---------------------------------------------------------------- E --
-    // Epd A operand: inbox row r's token row (read once) to each of its
-    // expert rows; one warp per (row, 4 KB slice).
+    // Epd A operand: inbox row r's token row (read once) to each of its expert
+    // rows, one warp per (row, 4 KB slice); then every segment's padding rows
+    // (no source row, zero weight, zero A row), one warp per row.
     const int R = T.in_base[nd];
     const int nvec = a.D / 8;
     constexpr int kSl = 256;  // uint4 per slice: 8 per lane in flight
     const int nsl = (nvec + kSl - 1) / kSl;
-    for (long wi = gw; wi < (long)R * nsl; wi += nw) {
+    const long n_copy = (long)R * nsl, n_items = n_copy + T.padpre[E];
+    for (long wi = gw; wi < n_items; wi += nw) {
+        if (wi >= n_copy) {  // a padding row
+            const int pr = (int)(wi - n_copy);
+            int g = 0;
+            while (T.padpre[g + 1] <= pr) ++g;
+            const int q = T.seg_base[g] + T.cnt[g] + (pr - T.padpre[g]);
+            uint4* out = reinterpret_cast<uint4*>(a.x_epd + (long)q * a.D);
+            for (int v = lane; v < nvec; v += 32) out[v] = make_uint4(0, 0, 0, 0);
+            continue;
+        }
         const int r = (int)(wi / nsl), sl = (int)(wi % nsl);
         const uint4* in = reinterpret_cast<const uint4*>(a.x + (long)a.in_tok[r] * a.D);
         const int q_lo = lane < P ? a.row_epd[(long)r * P + lane] : -1;
@@ -411,28 +504,35 @@ __global__ void __launch_bounds__(kThreads) fused_plan_kernel(FusedPlanArgs a) {
             }
         }
     }
+    phase_mark(a, 5);
 }
 
-size_t fused_smem(int nd, int E) {
+size_t fused_smem(int nd, int E, int k) {
     const int K = nd * (nd + 1) + nd * E;
-    const int tabs = 3 * nd * nd + (nd + 1) + 2 * nd + 2 * E + nd * E;
+    const int tabs = 3 * nd * nd + (nd + 1) + 2 * nd + 5 * E + 1 + nd * E;
+    (void)k;
     return sizeof(int) * ((size_t)kWarps * K + tabs);
 }
 
 }  // namespace
 
-size_t fused_plan_ws(int n, int nd, int E) {
+size_t fused_plan_chunks(int n, int k) {
+    const int tpb = kWarps * (32 / k);
+    return (size_t)(n + tpb - 1) / tpb;
+}
+
+size_t fused_plan_ws(int n, int nd, int E, int k) {
     const size_t K = (size_t)nd * (nd + 1) + (size_t)nd * E;
-    return K * ((size_t)(n + kThreads - 1) / kThreads + 1);
+    return K * (fused_plan_chunks(n, k) + 1);
 }
 
 bool fused_plan_supported(int nd, int E, int k) {
-    return nd <= 64 && E <= 64 && k <= 8 && fused_smem(nd, E) <= 96 * 1024;
+    return nd <= 64 && E <= 256 && k <= 32 && fused_smem(nd, E, k) <= 96 * 1024;
 }
 
 bool launch_fused_plan(const FusedPlanArgs& a, int num_sms, cudaStream_t st) {
     if (a.n <= 0) return true;
-    const size_t smem = fused_smem(a.nd, a.E);
+    const size_t smem = fused_smem(a.nd, a.E, a.k);
     static int configured = 0;
     if (!configured) {
         cudaFuncSetAttribute(fused_plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
@@ -442,12 +542,28 @@ bool launch_fused_plan(const FusedPlanArgs& a, int num_sms, cudaStream_t st) {
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_plan_kernel, kThreads, smem) != cudaSuccess ||
         per_sm < 1)
         return false;
-    const int blocks = num_sms * std::min(per_sm, 2);
+    const int blocks = num_sms * std::min(per_sm, 4);
     FusedPlanArgs args = a;
+    static const bool dbg_on = getenv("OCC_PLAN_DEBUG") != nullptr;  // phase timeline (diagnostics only)
+    static unsigned long long* dbg = nullptr;
+    if (dbg_on) {
+        if (!dbg) cudaMalloc(&dbg, sizeof(unsigned long long) * 8);
+        cudaMemsetAsync(dbg, 0, sizeof(unsigned long long) * 8, st);
+        cudaMemsetAsync(dbg, 0xFF, sizeof(unsigned long long), st);
+        args.dbg = dbg;
+    }
     void* params[] = {&args};
     if (cudaLaunchCooperativeKernel((const void*)fused_plan_kernel, blocks, kThreads, params, smem, st) != cudaSuccess)
         return false;
     count_launch();
+    if (dbg_on) {
+        unsigned long long h[8];
+        cudaStreamSynchronize(st);
+        cudaMemcpy(h, dbg, sizeof(h), cudaMemcpyDeviceToHost);
+        fprintf(stderr, "[plan dbg] n=%d nd=%d E=%d blocks=%d: A %.1f  B %.1f  C %.1f  D %.1f  E %.1f us (from start)\n",
+                a.n, a.nd, a.E, blocks, (h[1] - h[0]) / 1e3, (h[2] - h[0]) / 1e3, (h[3] - h[0]) / 1e3,
+                (h[4] - h[0]) / 1e3, (h[5] - h[0]) / 1e3);
+    }
     return true;
 }
 

@@ -4,6 +4,14 @@ import sys
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+# The loopback tests run up to 8 EP ranks x 2 micro-batches as threads of ONE
+# process on ONE GPU, each on its own stream, with spin-waiting arrival
+# kernels.  CUDA multiplexes streams onto CUDA_DEVICE_MAX_CONNECTIONS hardware
+# queues (default 8): two ranks' streams sharing a queue would serialise a
+# rank's signal behind another rank's wait.  One queue per stream (before the
+# CUDA context exists).  One process per GPU -- the product setting -- uses
+# two or three streams and is unaffected.
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
