@@ -873,6 +873,15 @@ void mark(occ_handle* h, int i, cudaStream_t st) {
     h->ev_recorded |= 1 << i;
 }
 
+// Bound on a peer arrival wait (default 10 s, then an error instead of a
+// hang); OCC_PEER_TIMEOUT_MS shortens it for profiling runs that serialise the
+// ranks' kernels (ncu on loopback ranks).
+long long peer_timeout_ns() {
+    static const long long v = getenv("OCC_PEER_TIMEOUT_MS") ? atoll(getenv("OCC_PEER_TIMEOUT_MS")) * 1000000LL
+                                                              : 10000000000LL;
+    return v;
+}
+
 occ_status check_err(occ_handle* h, cudaStream_t st) {
     CUDA_TRY(cudaStreamSynchronize(st));
     int32_t e = 0;
@@ -939,7 +948,7 @@ occ_status forward_multi(occ_handle* h, const __nv_bfloat16* x, const int32_t* i
         C_all = h->c_peer.p;
         launch_peer_counts(tab, nd, r, h->totals.p, st);
         launch_peer_signal(tab, nd, r, 2 * nd, seq, st);
-        launch_peer_wait(h->flags.p, nd, 2 * nd, seq, 10000000000LL, h->err.p, st);
+        launch_peer_wait(h->flags.p, nd, 2 * nd, seq, peer_timeout_ns(), h->err.p, st);
     } else {
         s = tp->allgather_counts(h->totals.p, C_all, nd, st);
         if (s != OCC_OK) return s;
@@ -992,7 +1001,7 @@ occ_status forward_multi(occ_handle* h, const __nv_bfloat16* x, const int32_t* i
     if (h->peer) {  // fused dispatch: pack stores into every destination's inbox, then arrival flags
         launch_peer_pack(pk, r, h->d_dev_of.p, h->dofs.off_sd, h->dofs.inoff, tab, st);
         launch_peer_signal(tab, nd, r, 0, seq, st);
-        launch_peer_wait(h->flags.p, nd, 0, seq, 10000000000LL, h->err.p, st);
+        launch_peer_wait(h->flags.p, nd, 0, seq, peer_timeout_ns(), h->err.p, st);
     } else {
         const std::vector<Transport::Part> parts{{h->snd_x.p, h->in_x.p, D * 2},
                                                  {h->snd_ids.p, h->in_ids.p, k * 4},
@@ -1029,7 +1038,7 @@ occ_status forward_multi(occ_handle* h, const __nv_bfloat16* x, const int32_t* i
         launch_peer_return(Rm, h->d_R, nd, r, P, D, h->row_epd.p, h->y16.p, h->dofs.C, h->dofs.off_sd, h->dofs.inoff,
                            tab, st);
         launch_peer_signal(tab, nd, r, nd, seq, st);
-        launch_peer_wait(h->flags.p, nd, nd, seq, 10000000000LL, h->err.p, st);
+        launch_peer_wait(h->flags.p, nd, nd, seq, peer_timeout_ns(), h->err.p, st);
     } else {
         launch_partial_combine(Rm, h->d_R, P, D, h->row_epd.p, h->y16.p, h->ret.p, st);
         // 7. return all-to-all: inbox rows back to their source's Sfd slots

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <algorithm>
+#include <cstdlib>
 
 #include "occ_common.cuh"
 #include "occ_glibc_exp.h"
@@ -280,6 +281,8 @@ __global__ void extract_brim0_kernel(int n, int nd, const int32_t* sources, int 
 // to every destination row (one per device under dedup), with its routing
 // row alongside.  One warp per token, 16-byte vectors, 8 vectors in flight
 // per lane.
+constexpr int kPackVec = 8;  // 16-byte vectors per lane in flight in the pack kernels
+
 __global__ void __launch_bounds__(256) pack_kernel(PackArgs a) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
@@ -300,17 +303,18 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs a) {
         for (int j = 0; j < a.k; ++j)
             if (a.mask[(long)t * a.k + j]) rows[nrows++] = a.tok_row[(long)t * a.k + j];
     }
-    for (int v0 = 0; a.dst_x && v0 < nvec; v0 += 8 * 32) {
-        uint4 buf[8];
+    // the whole row in flight (16 x 16 B per lane covers D = 4096 in one round trip)
+    for (int v0 = 0; a.dst_x && v0 < nvec; v0 += kPackVec * 32) {
+        uint4 buf[kPackVec];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < kPackVec; ++u) {
             const int v = v0 + u * 32 + lane;
             if (v < nvec) buf[u] = __ldg(src + v);
         }
         for (int q = 0; q < nrows; ++q) {
             uint4* dst = reinterpret_cast<uint4*>(a.dst_x + (long)rows[q] * a.D);
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < kPackVec; ++u) {
                 const int v = v0 + u * 32 + lane;
                 if (v < nvec) dst[v] = buf[u];
             }
@@ -495,42 +499,60 @@ __global__ void __launch_bounds__(256) zero_pad_rows_kernel(int NG, ComputeOffse
 template <int KU>
 __device__ __forceinline__ void sum_rows_ordered(const __nv_bfloat16* Y, const int* qs, int nq, int D, int lane,
                                                  const __nv_bfloat16* extra, __nv_bfloat16* dst) {
+    // two 16-byte vectors of the row per lane per pass: 2 x KU row loads in flight
     const int nv = D / 8;
-    for (int v = lane; v < nv; v += 32) {
-        float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int v = lane; v < nv; v += 64) {
+        const bool two = v + 32 < nv;
+        float acc[2][8];
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[h][e] = 0.f;
         for (int i0 = 0; i0 < nq; i0 += KU) {
-            uint4 u[KU];
+            uint4 u[2][KU];
 #pragma unroll
             for (int j = 0; j < KU; ++j)
-                if (i0 + j < nq) u[j] = __ldg(reinterpret_cast<const uint4*>(Y + (long)qs[i0 + j] * D) + v);
+                if (i0 + j < nq) {
+                    const uint4* r = reinterpret_cast<const uint4*>(Y + (long)qs[i0 + j] * D);
+                    u[0][j] = __ldg(r + v);
+                    if (two) u[1][j] = __ldg(r + v + 32);
+                }
 #pragma unroll
             for (int j = 0; j < KU; ++j) {
                 if (i0 + j >= nq) break;
-                const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&u[j]);
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const float2 f = __bfloat1622float2(hh[e]);
-                    acc[2 * e] += f.x;
-                    acc[2 * e + 1] += f.y;
+                for (int h = 0; h < 2; ++h) {
+                    const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&u[h][j]);
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float2 f = __bfloat1622float2(hh[e]);
+                        acc[h][2 * e] += f.x;
+                        acc[h][2 * e + 1] += f.y;
+                    }
                 }
             }
         }
-        if (extra) {
-            const uint4 w = __ldg(reinterpret_cast<const uint4*>(extra) + v);
-            const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&w);
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const float2 f = __bfloat1622float2(hh[e]);
-                acc[2 * e] += f.x;
-                acc[2 * e + 1] += f.y;
+        for (int h = 0; h < 2; ++h) {
+            if (h == 1 && !two) break;
+            const int vv = v + 32 * h;
+            if (extra) {
+                const uint4 w = __ldg(reinterpret_cast<const uint4*>(extra) + vv);
+                const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const float2 f = __bfloat1622float2(hh[e]);
+                    acc[h][2 * e] += f.x;
+                    acc[h][2 * e + 1] += f.y;
+                }
             }
+            uint4 o;
+            o.x = pack_bf16(acc[h][0], acc[h][1]);
+            o.y = pack_bf16(acc[h][2], acc[h][3]);
+            o.z = pack_bf16(acc[h][4], acc[h][5]);
+            o.w = pack_bf16(acc[h][6], acc[h][7]);
+            reinterpret_cast<uint4*>(dst)[vv] = o;
         }
-        uint4 o;
-        o.x = pack_bf16(acc[0], acc[1]);
-        o.y = pack_bf16(acc[2], acc[3]);
-        o.z = pack_bf16(acc[4], acc[5]);
-        o.w = pack_bf16(acc[6], acc[7]);
-        reinterpret_cast<uint4*>(dst)[v] = o;
     }
 }
 
@@ -887,12 +909,12 @@ __global__ void __launch_bounds__(256) peer_pack_kernel(PackArgs a, int me, cons
             rows[nrow++] = inoff[d * a.nd + me] + a.tok_row[(long)t * a.k + j] - off_sd[me * a.nd + d];
         }
     }
-    // x row: read once, 8 16-byte vectors in flight per lane, stored to every
-    // destination inbox row (NVLink peer stores)
-    for (int v0 = 0; v0 < nvec; v0 += 8 * 32) {
-        uint4 buf[8];
+    // x row: read once, the whole row in flight (16 16-byte vectors per lane),
+    // stored to every destination inbox row (NVLink peer stores)
+    for (int v0 = 0; v0 < nvec; v0 += kPackVec * 32) {
+        uint4 buf[kPackVec];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < kPackVec; ++u) {
             const int v = v0 + u * 32 + lane;
             if (v < nvec) buf[u] = __ldg(src + v);
         }
@@ -900,7 +922,7 @@ __global__ void __launch_bounds__(256) peer_pack_kernel(PackArgs a, int me, cons
             uint4* dst = reinterpret_cast<uint4*>(
                 reinterpret_cast<__nv_bfloat16*>(peer_tab[dsts[q] * kPeerSlots + kPeerInX]) + (long)rows[q] * a.D);
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < kPackVec; ++u) {
                 const int v = v0 + u * 32 + lane;
                 if (v < nvec) dst[v] = buf[u];
             }

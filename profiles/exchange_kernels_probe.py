@@ -8,8 +8,9 @@ Non-peer transport (host barriers, no spin waits), so it is safe under ncu:
       -k regex:"pack_kernel|partial_combine|combine_kernel" python profiles/exchange_kernels_probe.py
 
 With --peer the fused peer-memory path runs instead (timed with CUDA events
-around whole forwards; do NOT run --peer under ncu: ncu serialises the ranks'
-arrival waits)."""
+around whole forwards).  Under ncu, which serialises the ranks' kernels, run
+--peer --once with OCC_PEER_TIMEOUT_MS=200: each arrival wait then gives up
+after 0.2 s (the forward's values are garbage, the kernels' traffic is real)."""
 import os
 import sys
 import threading
@@ -23,6 +24,7 @@ import paper_2505_13345_b200 as occ  # noqa: E402
 
 def main():
     peer = "--peer" in sys.argv
+    iters = 1 if "--once" in sys.argv else 10
     nd, ne, k, dm, dh, n = 2, 8, 2, 4096, 1024, 16384
     torch.manual_seed(0)
     plist = np.arange(ne).reshape(nd, ne // nd)
@@ -46,17 +48,17 @@ def main():
             if peer:
                 layer.comm_enable_peer(n)
             layer.set_validate(False)
-            for _ in range(3):
+            for _ in range(1 if iters == 1 else 3):
                 layer.forward_expert_parallel(X[r], G, out=OUT[r])
             st.synchronize()
             bar.wait()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(st)
-            for _ in range(10):
+            for _ in range(iters):
                 layer.forward_expert_parallel(X[r], G, out=OUT[r])
             e1.record(st)
             st.synchronize()
-            times[r] = e0.elapsed_time(e1) / 10
+            times[r] = e0.elapsed_time(e1) / iters
             bar.wait()
 
     ths = [threading.Thread(target=rank, args=(r,)) for r in range(nd)]
