@@ -283,11 +283,7 @@ __global__ void extract_brim0_kernel(int n, int nd, const int32_t* sources, int 
 // per lane.
 constexpr int kPackVec = 8;  // 16-byte vectors per lane in flight in the pack kernels
 
-__global__ void __launch_bounds__(256) pack_kernel(PackArgs a) {
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (warp >= a.n) return;
-    const int t = warp;
+__device__ __forceinline__ void pack_token(const PackArgs& a, int t, int lane) {
     const int nvec = a.D / 8;
     const uint4* src = reinterpret_cast<const uint4*>(a.x + (long)t * a.D);
     int rows[kMaxDev];
@@ -329,6 +325,14 @@ __global__ void __launch_bounds__(256) pack_kernel(PackArgs a) {
             a.dst_w[di] = keep ? a.w[(long)t * a.k + j] : 0.0f;
         }
     }
+}
+
+// persistent: one warp per token, grid-stride over the tokens (no partial
+// last wave of blocks)
+__global__ void __launch_bounds__(256) pack_kernel(PackArgs a) {
+    const int lane = threadIdx.x & 31;
+    for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < a.n; t += (gridDim.x * blockDim.x) >> 5)
+        pack_token(a, t, lane);
 }
 
 // -------------------------------------------------------- compute index ---
@@ -883,11 +887,8 @@ __global__ void peer_counts_kernel(void* const* peer_tab, int nd, int me, const 
 // pack_kernel, but rows go directly to each destination's inbox:
 // row = inoff[d][me] + (BRIM0 counter - off_sd[me][d]) (all_to_all_exchange
 // order: source ascending, counter ascending, pipeline.cpp:153-174).
-__global__ void __launch_bounds__(256) peer_pack_kernel(PackArgs a, int me, const int32_t* dev_of, const int* off_sd,
-                                                        const int* inoff, void* const* peer_tab) {
-    const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (t >= a.n) return;
+__device__ __forceinline__ void peer_pack_token(const PackArgs& a, int me, const int32_t* dev_of, const int* off_sd,
+                                                const int* inoff, void* const* peer_tab, int t, int lane) {
     const int nvec = a.D / 8;
     const uint4* src = reinterpret_cast<const uint4*>(a.x + (long)t * a.D);
     int nrow = 0, dsts[kMaxTopK], rows[kMaxTopK], jsel[kMaxTopK];
@@ -939,6 +940,13 @@ __global__ void __launch_bounds__(256) peer_pack_kernel(PackArgs a, int me, cons
             pw[di] = keep ? a.w[(long)t * a.k + j] : 0.0f;
         }
     }
+}
+
+__global__ void __launch_bounds__(256) peer_pack_kernel(PackArgs a, int me, const int32_t* dev_of, const int* off_sd,
+                                                        const int* inoff, void* const* peer_tab) {
+    const int lane = threadIdx.x & 31;
+    for (int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < a.n; t += (gridDim.x * blockDim.x) >> 5)
+        peer_pack_token(a, me, dev_of, off_sd, inoff, peer_tab, t, lane);
 }
 
 // Arrival signal: after this stream's peer stores, publish `seq` into slot
@@ -1593,7 +1601,7 @@ void launch_extract_brim0(int n, int nd, const int32_t* sources, int src_fixed, 
 
 void launch_pack(const PackArgs& a, cudaStream_t st) {
     if (a.n == 0) return;
-    pack_kernel<<<(a.n + 7) / 8, 256, 0, st>>>(a);
+    pack_kernel<<<std::min((a.n + 7) / 8, 148 * 8), 256, 0, st>>>(a);
     count_launch();
 }
 
@@ -1744,7 +1752,7 @@ void launch_shared_gate(int n, int n_pad, int D, const __nv_bfloat16* x, const _
 void launch_peer_pack(const PackArgs& a, int me, const int32_t* dev_of, const int* off_sd, const int* inoff,
                       void* const* peer_tab, cudaStream_t st) {
     if (!a.n) return;
-    peer_pack_kernel<<<(a.n + 7) / 8, 256, 0, st>>>(a, me, dev_of, off_sd, inoff, peer_tab);
+    peer_pack_kernel<<<std::min((a.n + 7) / 8, 148 * 8), 256, 0, st>>>(a, me, dev_of, off_sd, inoff, peer_tab);
     count_launch();
 }
 void launch_seq_bump(unsigned long long* seq, cudaStream_t st) {
