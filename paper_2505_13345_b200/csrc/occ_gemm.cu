@@ -95,6 +95,7 @@ struct Params {
     float* gw_part;
     int tma_out;         // bf16 forward outputs leave through smem + TMA stores (tmC)
     unsigned long long* dbg;  // OCC_GEMM_DEBUG: per-CTA stall cycles [cta][4]
+    unsigned long long* tl;   // OCC_GEMM_TIMELINE: globaltimer per CTA at 8 points [cta][8]
     int tail_split;           // wide kernel: split the tail wave's super-tiles into halves
     const int* a_rows;   // non-null: A row q of the padded Epd layout is row a_rows[q] of tmA
                          // (tile::gather4, box 64 x 1; -1 = zero padding row)
@@ -222,6 +223,13 @@ __device__ __forceinline__ void load_pre_chunk(const Params& p, long rowbase, in
     if constexpr (EPI == EPI_BWD_SWIGLU) load_block_coalesced(p.pre_b + rowbase * p.N + col0, p.N, p.N - col0, lane, B);
 }
 
+__device__ __forceinline__ void tl_mark(const Params& p, int i) {
+    if (!p.tl) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.tl[blockIdx.x * 8 + i] = t;
+}
+
 template <int EPI, bool WGRAD>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -243,6 +251,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
+    if (threadIdx.x == 0) tl_mark(p, 0);
     const int NB = WGRAD ? (p.N + BN - 1) / BN : (EPI == EPI_SWIGLU_BF16 ? (p.N + 127) / 128 : (p.N + BN - 1) / BN);
     const int MT = (p.M + 2 * BM - 1) / (2 * BM);  // wgrad m-tiles
     if constexpr (WGRAD) {
@@ -281,6 +290,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    if (threadIdx.x == 0) tl_mark(p, 1);
 
     const int num_tiles = WGRAD ? s_gmb[p.ngroups] : s_gmb[p.ngroups] * NB;
     const int KB_fwd = (p.K + BK - 1) / BK;
@@ -418,6 +428,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             { const long long t0 = p.dbg ? clock64() : 0;
             mbar_wait(&tfull[acc], acc_phase);
             if (p.dbg && lane == 0 && warp == 2) p.dbg[blockIdx.x * 4 + 3] += clock64() - t0; }
+            if (warp == 2 && lane == 0 && tile == cid) tl_mark(p, 2);  // first accumulator ready
             tc_fence_after();
             const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
             bool released = false;  // TMEM buffer handed back to the MMA warp early
@@ -542,6 +553,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                         if constexpr (SW) tmem_ld32(tbase + 128 + c * 32, g[cc]);
                     }
                     tmem_ld_wait();
+                    if (warp == 2 && lane == 0 && tile == cid) tl_mark(p, 6);  // accumulator in registers
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive_cluster(smem_u32(&tempty[acc]) & kPeerBitMask);
@@ -607,6 +619,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                                     tma_store_2d(&tmC, stg, col0, (int)(row - lane));
                                     bulk_commit();
                                 }
+                                if (warp == 2 && lane == 0 && tile == cid && cc == 0) tl_mark(p, 7);  // first store
                                 ++stg_n;
                             } else {
                                 store_bf16x32(out + col0, h, p.N - col0);
@@ -622,10 +635,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             }
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
+        if (warp == 2 && lane == 0) tl_mark(p, 3);  // epilogue issued everything
         if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        if (warp == 2 && lane == 0) tl_mark(p, 4);  // stores complete
     }
     tc_fence_before();
     cluster_sync();
+    if (threadIdx.x == 0) tl_mark(p, 5);
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc_cg2<512>(tmem_base);
@@ -1206,6 +1222,13 @@ void launch_grouped_gemm(EpiMode mode, const GemmArgs& a, int num_sms, cudaStrea
     p.pre_b = a.pre_b;
     p.gw_part = a.gw_part;
     p.a_rows = a.a_rows;
+    static const bool tl_on = getenv("OCC_GEMM_TIMELINE") != nullptr;
+    static unsigned long long* tl_buf = nullptr;
+    if (tl_on) {
+        if (!tl_buf) cudaMalloc(&tl_buf, sizeof(unsigned long long) * 8 * 1024);
+        cudaMemsetAsync(tl_buf, 0, sizeof(unsigned long long) * 8 * 1024, st);
+        p.tl = tl_buf;
+    }
     static const bool dbg_on = getenv("OCC_GEMM_DEBUG") != nullptr;
     static unsigned long long* dbg_buf = nullptr;
     static cudaEvent_t dbg_ev[2];
@@ -1275,6 +1298,27 @@ void launch_grouped_gemm(EpiMode mode, const GemmArgs& a, int num_sms, cudaStrea
             }
             break;
         }
+    }
+    if (tl_on) {  // per-CTA timeline (narrow kernel; diagnostics only)
+        unsigned long long h[8 * 1024];
+        cudaStreamSynchronize(st);
+        cudaMemcpy(h, tl_buf, sizeof(unsigned long long) * 8 * grid, cudaMemcpyDeviceToHost);
+        unsigned long long t0 = ~0ull;
+        for (int c = 0; c < grid; ++c)
+            if (h[c * 8] && h[c * 8] < t0) t0 = h[c * 8];
+        double mx[8] = {0, 0, 0, 0, 0, 0, 0, 0}, mn[8] = {1e30, 1e30, 1e30, 1e30, 1e30, 1e30, 1e30, 1e30};
+        for (int c = 0; c < grid; ++c)
+            for (int i = 0; i < 8; ++i)
+                if (h[c * 8 + i]) {
+                    const double v = (h[c * 8 + i] - t0) / 1e3;
+                    mx[i] = std::max(mx[i], v);
+                    mn[i] = std::min(mn[i], v);
+                }
+        fprintf(stderr, "[gemm tl] mode=%d K=%d N=%d grid=%d us from first CTA start (min..max over CTAs): start %.1f..%.1f "
+                "setup %.1f..%.1f acc-ready %.1f..%.1f in-regs %.1f..%.1f first-store %.1f..%.1f epi-issued %.1f..%.1f "
+                "stores-done %.1f..%.1f exit %.1f..%.1f\n",
+                (int)mode, a.K, a.N, grid, mn[0], mx[0], mn[1], mx[1], mn[2], mx[2], mn[6], mx[6], mn[7], mx[7], mn[3],
+                mx[3], mn[4], mx[4], mn[5], mx[5]);
     }
     if (dbg_on) {  // stall-cycle breakdown, averaged over CTAs (diagnostics only)
         unsigned long long h[4 * 1024];

@@ -27,7 +27,7 @@ def main():
     gate = (torch.rand(ne, dm, device=dev) * 2 - 1).mul_(3 / dm ** 0.5).bfloat16()
     layer.set_validate(False)
     out = torch.empty_like(x)
-    if os.environ.get("OCC_GEMM_DEBUG"):  # synchronising diagnostics: eager only
+    if os.environ.get("OCC_GEMM_DEBUG") or os.environ.get("OCC_GEMM_TIMELINE"):  # synchronising: eager only
         for _ in range(3):
             layer.forward_expert_parallel(x, gate, out=out)
         torch.cuda.synchronize()
