@@ -133,6 +133,44 @@ class Layer {
                                  int n, void* out, occ_stream_t s) {
         check(occ_forward_expert_parallel(h_, x, gate, prune, sources, n, out, s), "forward_expert_parallel");
     }
+    // Router arithmetic: OCC_ROUTER_TC (default) or OCC_ROUTER_EXACT (the
+    // reference's gate_scores + topk_route + prune_routing, bit-exact).
+    void set_router_mode(int mode) { check(occ_set_router_mode(h_, mode), "set_router_mode"); }
+    // gate_scores -> topk_route -> prune_routing (routing.cpp:33-84,
+    // pruning.cpp:141-163) on bf16 tokens / gate, bit-exact: ids int32, weights f64.
+    void route_exact(const void* x, const void* gate, int n, const occ_prune* prune, int32_t* ids, double* weights,
+                     double* scores, occ_stream_t s) {
+        check(occ_route_exact(h_, x, gate, n, prune, ids, weights, scores, s), "route_exact");
+    }
+
+    // ---- stage-level entry points (pipeline.hpp:89-123) ----
+    // build_dispatch_index: world_size 1 -> every source (sources nullable), BRIM0s
+    // concatenated + counts [N_d x N_d]; world_size > 1 -> this rank's tokens.
+    void build_dispatch_index(const int32_t* ids, const int32_t* sources, int n, int32_t* brim0, int32_t* counts,
+                              occ_stream_t s) {
+        check(occ_build_dispatch(h_, ids, sources, n, brim0, counts, s), "build_dispatch_index");
+    }
+    // dispatch (pipeline.cpp:91-123): one source's SfdBatch from its BRIM0 [N_d x n].
+    void dispatch(const void* x, const int32_t* ids, const float* w, int n, const int32_t* brim0, void* sfd_x,
+                  int32_t* sfd_ids, float* sfd_w, int32_t* sfd_token, occ_stream_t s) {
+        check(occ_dispatch(h_, x, ids, w, n, brim0, sfd_x, sfd_ids, sfd_w, sfd_token, s), "dispatch");
+    }
+    // build_compute_index (pipeline.cpp:52-89) of EP device `device` over its inbox rows.
+    void build_compute_index(int device, const int32_t* in_ids, const float* in_w, int rows, int32_t* cindex,
+                             int32_t* n_epd, occ_stream_t s) {
+        check(occ_build_compute(h_, device, in_ids, in_w, rows, cindex, n_epd, s), "build_compute_index");
+    }
+    // scatter_matmul -> apply_activation -> weight_modulate -> merge_matmul
+    // (pipeline.cpp:178-283): the partial-combined return rows of device `device`.
+    void expert_compute(int device, const void* in_x, const int32_t* in_ids, const float* in_w, int rows, void* y,
+                        occ_stream_t s) {
+        check(occ_expert_compute(h_, device, in_x, in_ids, in_w, rows, y, s), "expert_compute");
+    }
+    // combine (pipeline.cpp:285-300) of one source through its BRIM0.
+    void combine(const void* y_returned, const int32_t* brim0, int n, void* out, occ_stream_t s) {
+        check(occ_combine(h_, y_returned, brim0, n, out, s), "combine");
+    }
+
     CommReport report(int bytes_per_scalar, occ_stream_t s) const {
         occ_comm_report r{};
         check(occ_comm_report_get(h_, bytes_per_scalar, &r, s), "comm_report");

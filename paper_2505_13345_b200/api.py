@@ -326,23 +326,7 @@ class ExpertParallelLayer:
         CPU tensors, e.g. gloo) -- instead of NCCL.  Pair with
         comm_enable_peer (CUDA IPC mapping; the forward then runs without any
         host involvement).  Works for several processes on one GPU."""
-        import torch.distributed as dist
-
-        def fn(_ctx, send, nbytes, recv):
-            try:
-                if nbytes == 0:
-                    return 0
-                world = dist.get_world_size(group)
-                src = torch.frombuffer(bytearray(C.string_at(send, nbytes)), dtype=torch.uint8)
-                outs = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(world)]
-                dist.all_gather(outs, src, group=group)
-                cat = torch.cat(outs)  # (kept referenced until the copy is done)
-                C.memmove(recv, cat.data_ptr(), world * nbytes)
-                return 0
-            except Exception:  # noqa: BLE001 -- reported as OCC_ERR_NCCL by the library
-                return 1
-
-        self._host_fn = _ALLGATHER_FN(fn)  # kept alive with the handle
+        self._host_fn = host_allgather_fn(group)  # kept alive with the handle
         _check(lib().occ_comm_init_host(self._h, self._host_fn, None), "comm_init_host")
 
     def router_logits(self, x: torch.Tensor, gate: torch.Tensor) -> torch.Tensor:
@@ -828,6 +812,29 @@ def collaboration_aware_placement(routing_batches, num_experts: int, num_devices
     if layer is not None and getattr(layer, "_world", 1) > 1:
         layer.allreduce_histogram(counts)
     return reschedule_placement(normalize_graph(counts), num_devices)
+
+
+def host_allgather_fn(group=None):
+    """The occ_host_allgather_fn of occ_comm_init_host over torch.distributed:
+    fn(ctx, send, bytes, recv) gathers `bytes` from every rank of `group` into
+    recv [world * bytes] in rank order (CPU tensors: gloo), 0 on success."""
+    import torch.distributed as dist
+
+    def fn(_ctx, send, nbytes, recv):
+        try:
+            if nbytes == 0:
+                return 0
+            world = dist.get_world_size(group)
+            src = torch.frombuffer(bytearray(C.string_at(send, nbytes)), dtype=torch.uint8)
+            outs = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(world)]
+            dist.all_gather(outs, src, group=group)
+            cat = torch.cat(outs)  # (kept referenced until the copy is done)
+            C.memmove(recv, cat.data_ptr(), world * nbytes)
+            return 0
+        except Exception:  # noqa: BLE001 -- reported as OCC_ERR_NCCL by the library
+            return 1
+
+    return _ALLGATHER_FN(fn)
 
 
 def exchange_layout(counts, rank: int):

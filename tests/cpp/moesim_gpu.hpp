@@ -1,7 +1,8 @@
 // moesim_gpu.hpp — the reference-side binding a moesim maintainer adds to
-// route forward_given_routing / forward_expert_parallel through the B200
-// library.  Same signatures as pipeline.hpp:178-189 and the same exception
-// types; moesim's host Matrix values are converted to bf16 device buffers.
+// route forward_given_routing / forward_expert_parallel / build_dispatch_index
+// through the B200 library.  Same signatures as pipeline.hpp:83-84 and
+// :178-189 and the same exception types; moesim's host Matrix values are
+// converted to bf16 device buffers.
 #pragma once
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -104,6 +105,76 @@ inline moesim::ForwardResult forward_given_routing(const moesim::TokenMatrix& x,
         (void)F;
         return res;
     });
+}
+
+// moesim::build_dispatch_index (pipeline.hpp:83-84) for one source's tokens
+// (ascending Ori rows) on the B200: the BRIM0 counters, bit-exact.
+inline moesim::DispatchIndex build_dispatch_index(const moesim::RoutingOutcome& routing,
+                                                  const moesim::Placement& placement, std::span<const int> tokens) {
+    using namespace detail;
+    return translate([&] {
+        const int nd = placement.num_devices(), k = routing.k, n = static_cast<int>(tokens.size());
+        int ne = 0;
+        for (const auto& d : placement.devices) ne += static_cast<int>(d.size());
+        occ_config cfg{ne, k, nd, 8, 8, 1, 0, 1};
+        occult::Layer layer(cfg, occult::Placement{placement.devices});
+        std::vector<int32_t> ids((size_t)n * k), src(n, 0);  // all rows: one source
+        for (int i = 0; i < n; ++i)
+            for (int j = 0; j < k; ++j) ids[(size_t)i * k + j] = routing.ids[(size_t)tokens[i] * k + j];
+        Dev<int32_t> dids(ids.size()), dsrc(n), db((size_t)nd * n), dc((size_t)nd * nd);
+        cuda_check(cudaMemcpy(dids.p, ids.data(), sizeof(int32_t) * ids.size(), cudaMemcpyHostToDevice));
+        cuda_check(cudaMemcpy(dsrc.p, src.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice));
+        layer.build_dispatch_index(dids.p, dsrc.p, n, db.p, dc.p, nullptr);
+        moesim::DispatchIndex di;
+        di.num_devices = nd;
+        di.num_tokens = n;
+        di.entries.resize((size_t)nd * n);
+        cuda_check(cudaMemcpy(di.entries.data(), db.p, sizeof(int32_t) * di.entries.size(), cudaMemcpyDeviceToHost));
+        di.n_sfd = 0;
+        for (int v : di.entries) di.n_sfd += v >= 0;
+        return di;
+    });
+}
+
+// moesim::forward_expert_parallel (pipeline.hpp:185-189) on the B200 with the
+// exact router: gate_scores + topk_route (+ prune_routing) bit-exact with the
+// reference, then the indexed data path.
+inline moesim::ForwardResult forward_expert_parallel(const moesim::TokenMatrix& x, const moesim::GateMatrix& gate,
+                                                     const moesim::ExpertWeights& experts,
+                                                     const moesim::Placement& placement,
+                                                     const moesim::PruneSpec& prune,
+                                                     const moesim::MoEConfig& config,
+                                                     std::span<const int> sources = {}, int bytes_per_scalar = 4) {
+    using namespace detail;
+    moesim::RoutingOutcome routing = translate([&] {
+        config.validate();
+        const int n = x.rows(), D = config.embed_dim, E = config.num_experts, k = config.top_k;
+        occult::Layer layer(config_of(config), occult::Placement{placement.devices});
+        const auto xb = to_bf16(x.values.data), gb = to_bf16(gate.weights.data);
+        Dev<__nv_bfloat16> dx(xb.size()), dg(gb.size());
+        Dev<int32_t> dids((size_t)n * k);
+        Dev<double> dw((size_t)n * k);
+        cuda_check(cudaMemcpy(dx.p, xb.data(), xb.size() * 2, cudaMemcpyHostToDevice));
+        cuda_check(cudaMemcpy(dg.p, gb.data(), gb.size() * 2, cudaMemcpyHostToDevice));
+        occ_prune pr{static_cast<int>(prune.mode), prune.device_budget,
+                     prune.weight_policy == moesim::ReplacementWeightPolicy::OwnScore ? 1 : 0};
+        if (prune.mode == moesim::PruneMode::Similarity) throw moesim::ConfigError("binding: router-score pruning only");
+        layer.route_exact(dx.p, dg.p, n, prune.mode == moesim::PruneMode::None ? nullptr : &pr, dids.p, dw.p, nullptr,
+                          nullptr);
+        moesim::RoutingOutcome r;
+        r.num_tokens = n;
+        r.k = k;
+        r.ids.resize((size_t)n * k);
+        r.weights.resize((size_t)n * k);
+        cuda_check(cudaMemcpy(r.ids.data(), dids.p, sizeof(int32_t) * r.ids.size(), cudaMemcpyDeviceToHost));
+        cuda_check(cudaMemcpy(r.weights.data(), dw.p, sizeof(double) * r.weights.size(), cudaMemcpyDeviceToHost));
+        (void)D;
+        (void)E;
+        return r;
+    });
+    double cap = static_cast<double>(std::min(config.top_k, placement.num_devices()));
+    if (prune.mode != moesim::PruneMode::None) cap = std::min(cap, static_cast<double>(prune.device_budget));
+    return moesim_gpu::forward_given_routing(x, routing, experts, placement, config, sources, bytes_per_scalar, cap);
 }
 
 }  // namespace moesim_gpu

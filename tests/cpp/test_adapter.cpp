@@ -5,6 +5,7 @@
 #include <cstdio>
 
 #include "moesim/pipeline.hpp"
+#include "moesim/pruning.hpp"
 #include "moesim/routing.hpp"
 #include "moesim_gpu.hpp"
 
@@ -55,6 +56,39 @@ int main() {
         }
         std::printf("  duplicate id -> moesim::RoutingError: %s\n", threw ? "ok" : "FAIL");
         fails += !threw;
+        // build_dispatch_index of one source's tokens: the BRIM0 counters bit for bit
+        std::vector<int> tokens;
+        for (int t = 1; t < 300; t += 3) tokens.push_back(t);
+        const DispatchIndex di_ref = build_dispatch_index(r, p, tokens);
+        const DispatchIndex di_gpu = moesim_gpu::build_dispatch_index(r, p, tokens);
+        const bool di_ok = di_ref.entries == di_gpu.entries && di_ref.n_sfd == di_gpu.n_sfd;
+        std::printf("  build_dispatch_index: %s\n", di_ok ? "ok" : "FAIL");
+        fails += !di_ok;
+        // forward_expert_parallel with the exact router: routing bit-exact, so the
+        // CommReport is identical; values within the bf16 tolerance
+        PruneSpec none;
+        const ForwardResult fe_ref = forward_expert_parallel(x, gate, ex, p, none, cfg);
+        const ForwardResult fe_gpu = moesim_gpu::forward_expert_parallel(x, gate, ex, p, none, cfg);
+        const double fe_err = max_rel_error(fe_gpu.x_out.values, fe_ref.x_out.values);
+        const bool fe_ok = fe_err <= 1e-2 && fe_gpu.report.mean_replicas == fe_ref.report.mean_replicas &&
+                           fe_gpu.report.cross_device_bytes == fe_ref.report.cross_device_bytes &&
+                           fe_gpu.report.per_device_token_counts == fe_ref.report.per_device_token_counts &&
+                           fe_gpu.report.intra_share == fe_ref.report.intra_share &&
+                           fe_gpu.report.cap_replicas == fe_ref.report.cap_replicas;
+        std::printf("  forward_expert_parallel (exact router): max_rel_error=%.3e %s\n", fe_err, fe_ok ? "ok" : "FAIL");
+        fails += !fe_ok;
+        if (nd >= 2) {  // with router-score pruning to one device per token
+            PruneSpec pr;
+            pr.mode = PruneMode::RouterScore;
+            pr.device_budget = 1;
+            const ForwardResult pp_ref = forward_expert_parallel(x, gate, ex, p, pr, cfg);
+            const ForwardResult pp_gpu = moesim_gpu::forward_expert_parallel(x, gate, ex, p, pr, cfg);
+            const bool pp_ok = max_rel_error(pp_gpu.x_out.values, pp_ref.x_out.values) <= 1e-2 &&
+                               pp_gpu.report.mean_replicas == pp_ref.report.mean_replicas &&
+                               pp_gpu.report.cross_device_bytes == pp_ref.report.cross_device_bytes;
+            std::printf("  forward_expert_parallel (router pruning, budget 1): %s\n", pp_ok ? "ok" : "FAIL");
+            fails += !pp_ok;
+        }
     }
     std::printf(fails ? "ADAPTER FAIL\n" : "ADAPTER OK\n");
     return fails;

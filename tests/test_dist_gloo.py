@@ -141,3 +141,37 @@ def test_exchange_layout_golden():
     so, sc, ro, rc = occ.exchange_layout(C, 1)
     assert so.tolist() == [0, 2, 2] and sc.tolist() == [2, 0, 5]
     assert ro.tolist() == [0, 1, 1] and rc.tolist() == [1, 0, 1]
+
+
+def _allgather_worker(rank, world, port, q):
+    """One rank: the host all-gather callback of occ_comm_init_host (the
+    transport that bootstraps the IPC mapping without NCCL), called the way the
+    library calls it -- raw pointers through the C function-pointer type."""
+    import ctypes as C
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2505_13345_b200.api import host_allgather_fn
+    fn = host_allgather_fn()
+    ok = True
+    for nbytes in (1, 8, 100, 64 * (world + 3), 0):
+        send = (C.c_uint8 * max(nbytes, 1))(*[(rank * 37 + i) % 251 for i in range(max(nbytes, 1))])
+        recv = (C.c_uint8 * max(world * nbytes, 1))()
+        rc = fn(None, C.addressof(send), nbytes, C.addressof(recv))
+        want = [(r * 37 + i) % 251 for r in range(world) for i in range(nbytes)]
+        ok &= rc == 0 and list(recv)[:world * nbytes] == want
+    dist.destroy_process_group()
+    q.put((rank, ok))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_host_allgather_callback_multiprocess(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_allgather_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok in res), res
