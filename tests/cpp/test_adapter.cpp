@@ -30,6 +30,7 @@ int main() {
         ExpertWeights ex = ExpertWeights::random(8, 64, 128, expert_rng, Precision::Double, Activation::SiLU);
         GateMatrix gate{random_matrix(8, 64, gate_rng, Precision::Double)};
         for (double& v : x.values.data) v = bf16r(v);
+        for (double& v : gate.weights.data) v = bf16r(v);  // the device router reads a bf16 gate
         for (auto& m : ex.w1) for (double& v : m.data) v = bf16r(v / 8.0);
         for (auto& m : ex.w2) for (double& v : m.data) v = bf16r(v / std::sqrt(128.0));
         RoutingOutcome r = topk_route(gate_scores(x, gate), 2, true);
