@@ -1809,8 +1809,10 @@ static occ_status forward_one(occ_handle* h, const void* x, const int32_t* ids, 
     if (n == 0) return OCC_OK;
     const int nd = h->nd, k = h->k, P = h->P, D = h->D, F = h->F, dedup = h->cfg.dedup;
     const int G = nd;
-    CUDA_TRY(cudaMemsetAsync(h->stats.p, 0, sizeof(long long) * 8, st));
-    CUDA_TRY(cudaMemsetAsync(h->err.p, 0, sizeof(int32_t), st));
+    // (inside forward_expert_parallel the route has just zeroed the error flag,
+    // and a router error must survive to check_err; the fused plan zeroes the
+    // CommReport counters itself: no memset nodes between route and plan)
+    if (!h->in_ep) CUDA_TRY(cudaMemsetAsync(h->err.p, 0, sizeof(int32_t), st));
     if (!h->in_ep) h->ev_recorded = 0;
     mark(h, ST_PLAN, st);
     const bool gathered = h->gather_a && !h->training;
@@ -1828,6 +1830,7 @@ static occ_status forward_one(occ_handle* h, const void* x, const int32_t* ids, 
         static const int scatter_env = getenv("OCC_PLAN_SCATTER") ? atoi(getenv("OCC_PLAN_SCATTER")) : -1;
         const long copy_bytes = (long)n * std::min(k, nd) * D * 2;
         fa.scatter = scatter_env >= 0 ? scatter_env : copy_bytes <= (64l << 20);
+        fa.zero_stats = 1;
         fused = launch_fused_plan(fa, h->num_sms, st);
         if (fused && !fa.scatter) {
             mark(h, ST_GATHER, st);
@@ -1836,6 +1839,7 @@ static occ_status forward_one(occ_handle* h, const void* x, const int32_t* ids, 
         }
     }
     if (!fused) {  // the multi-kernel chain
+    CUDA_TRY(cudaMemsetAsync(h->stats.p, 0, sizeof(long long) * 8, st));
     // 1. dispatch plan (BRIM0) and exchange placement
     s = run_plan(h, ids, weights, sources, n, st);
     if (s != OCC_OK) return s;

@@ -208,6 +208,16 @@ OCC_DEV uint32_t pack_bf16(float a, float b) {
     return *reinterpret_cast<uint32_t*>(&h);
 }
 
+// Programmatic dependent launch (kernels launched with launch_pdl): the grid
+// may start while its predecessor in the stream is still running; everything
+// that reads the predecessor's results (or writes what it reads) must come
+// after pdl_wait(), which returns once the predecessor grid has completed and
+// its memory is visible.  pdl_trigger() lets the NEXT grid launch early (its
+// own pdl_wait still orders it after this grid's completion).  Both are no-ops
+// for a normal launch.
+OCC_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+OCC_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 OCC_DEV uint32_t lanemask_lt() {
     uint32_t m;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));

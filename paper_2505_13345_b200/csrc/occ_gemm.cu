@@ -36,6 +36,8 @@
 #include <stdlib.h>
 #include <stdio.h>
 
+#include <algorithm>
+
 #include "occ_common.cuh"
 #include "occ_internal.h"
 
@@ -128,18 +130,38 @@ __device__ __forceinline__ void wtile_coords(int tile, const int* tb, int ng, in
     nt = lt - mt * NB;
 }
 
-__device__ __forceinline__ float act_f(float v, int act) {
-    if (act == 1) return silu(v);
-    if (act == 2) return v > 0.f ? v : 0.f;
-    return v;
+// Activations (0 identity, 1 SiLU, 2 ReLU) as compile-time functors.  The
+// runtime activation is dispatched ONCE per 32-value chunk (act_dispatch), not
+// per element: a per-element switch puts a branch between the elements, so
+// their dependent MUFU chains (ex2 -> rcp) cannot interleave and a chunk took
+// ~1.5 us instead of ~0.1 us (OCC_GEMM_TIMELINE on the C1 layer; identity
+// chunks 0.6 us) -- the epilogue, not the MMAs, then bounded short-K GEMMs.
+template <int A>
+__device__ __forceinline__ float act_t(float v) {
+    if constexpr (A == 1) return silu(v);
+    else if constexpr (A == 2) return v > 0.f ? v : 0.f;
+    else return v;
 }
-__device__ __forceinline__ float act_grad(float v, int act) {  // backward.cpp:11-20
-    if (act == 1) {
+template <int A>
+__device__ __forceinline__ float act_grad_t(float v) {  // backward.cpp:11-20
+    if constexpr (A == 1) {
         const float s = sigmoid_fast(v);
         return s * (1.0f + v * (1.0f - s));
+    } else if constexpr (A == 2) {
+        return v > 0.f ? 1.f : 0.f;
+    } else {
+        return 1.f;
     }
-    if (act == 2) return v > 0.f ? 1.f : 0.f;
-    return 1.f;
+}
+template <int A>
+struct ActTag {
+    static constexpr int value = A;
+};
+template <typename Fn>
+__device__ __forceinline__ void act_dispatch(int act, Fn&& fn) {
+    if (act == 1) fn(ActTag<1>());
+    else if (act == 2) fn(ActTag<2>());
+    else fn(ActTag<0>());
 }
 
 __device__ __forceinline__ void store_bf16x32(__nv_bfloat16* p, const float (&h)[32], int valid_cols) {
@@ -227,7 +249,7 @@ __device__ __forceinline__ void tl_mark(const Params& p, int i) {
     if (!p.tl) return;
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    p.tl[blockIdx.x * 8 + i] = t;
+    p.tl[blockIdx.x * 16 + i] = t;
 }
 
 template <int EPI, bool WGRAD>
@@ -254,23 +276,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     if (threadIdx.x == 0) tl_mark(p, 0);
     const int NB = WGRAD ? (p.N + BN - 1) / BN : (EPI == EPI_SWIGLU_BF16 ? (p.N + 127) / 128 : (p.N + BN - 1) / BN);
     const int MT = (p.M + 2 * BM - 1) / (2 * BM);  // wgrad m-tiles
-    if constexpr (WGRAD) {
-        if (threadIdx.x == 0) {
-            int run = 0;
-            for (int g = 0; g < p.ngroups; ++g) {
-                s_gmb[g] = run;
-                const int rows = p.grp_cnt[g];
-                s_kb0[g] = p.seg_base[g] / BK;
-                s_kbn[g] = (rows + BK - 1) / BK;
-                if (rows > 0) run += MT * NB;
-            }
-            s_gmb[p.ngroups] = run;
-        }
-        for (int i = threadIdx.x; i < p.ngroups; i += blockDim.x) s_gw[i] = p.grp_w[i];
-    } else {
-        for (int i = threadIdx.x; i <= p.ngroups; i += blockDim.x) s_gmb[i] = p.grp_mb[i];
-        for (int i = threadIdx.x; i < p.ngroups; i += blockDim.x) s_gw[i] = p.grp_w[i];
-    }
+    pdl_trigger();
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
@@ -290,11 +296,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // the group tables come from the index chain (previous kernels): after the
+    // prologue above, which overlaps the predecessor's tail under PDL
+    pdl_wait();
+    if constexpr (WGRAD) {
+        if (threadIdx.x == 0) {
+            int run = 0;
+            for (int g = 0; g < p.ngroups; ++g) {
+                s_gmb[g] = run;
+                const int rows = p.grp_cnt[g];
+                s_kb0[g] = p.seg_base[g] / BK;
+                s_kbn[g] = (rows + BK - 1) / BK;
+                if (rows > 0) run += MT * NB;
+            }
+            s_gmb[p.ngroups] = run;
+        }
+        for (int i = threadIdx.x; i < p.ngroups; i += blockDim.x) s_gw[i] = p.grp_w[i];
+    } else {
+        for (int i = threadIdx.x; i <= p.ngroups; i += blockDim.x) s_gmb[i] = p.grp_mb[i];
+        for (int i = threadIdx.x; i < p.ngroups; i += blockDim.x) s_gw[i] = p.grp_w[i];
+    }
+    __syncthreads();
     if (threadIdx.x == 0) tl_mark(p, 1);
 
     const int num_tiles = WGRAD ? s_gmb[p.ngroups] : s_gmb[p.ngroups] * NB;
     const int KB_fwd = (p.K + BK - 1) / BK;
     const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+    const bool compact = num_tiles <= 2 * ncl;  // <= 2 tiles per CTA: rolled epilogue (see there)
 
     if (warp == 0 && !WGRAD && p.a_rows) {
         // ------------------------------------------------ TMA producer, gathered A rows:
@@ -519,12 +547,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                                 row_to_global(stg, r0, outb + col0, p.ldo, F - col0, lane);
                                 row_to_global(stg, r1, outb + F + col0, p.ldo, F - col0, lane);
                             } else {
+                                act_dispatch(p.act, [&](auto tag) {
+                                    constexpr int A = decltype(tag)::value;
 #pragma unroll
-                                for (int i = 0; i < 32; ++i) {
-                                    const float gm = i < nv ? __uint_as_float(v[i]) : 0.f;
-                                    gw += act_f(a[i], p.act) * gm;
-                                    r0[i] = gm * wr * act_grad(a[i], p.act);
-                                }
+                                    for (int i = 0; i < 32; ++i) {
+                                        const float gm = i < nv ? __uint_as_float(v[i]) : 0.f;
+                                        gw += act_t<A>(a[i]) * gm;
+                                        r0[i] = gm * wr * act_grad_t<A>(a[i]);
+                                    }
+                                });
                                 row_to_global(stg, r0, outb + col0, p.ldo, F - col0, lane);
                             }
                         }
@@ -542,6 +573,66 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                     constexpr int NCH = SW ? 4 : BN / 32;  // 32-column chunks per tile
                     constexpr int MY = NCH / 2;            // this warp's half
                     const int ncol = SW ? 128 : BN;
+                    if (compact && !p.save_a && p.tma_out) {
+                        // At most two tiles per CTA (no tile i+2 waits on this accumulator):
+                        // one chunk at a time in a rolled loop, so one chunk's instructions
+                        // serve every chunk.  With a single tile per CTA the unrolled drain
+                        // below is bound by cold instruction fetch, not by its math (~1.7 us
+                        // per 32-column chunk, OCC_GEMM_TIMELINE on the C1 layer).
+#pragma unroll 1
+                        for (int cc = 0; cc < MY; ++cc) {
+                            const int c = hsel * MY + cc;
+                            uint32_t av[32], bv[32];
+                            tmem_ld32(tbase + c * 32, av);
+                            if constexpr (SW) tmem_ld32(tbase + 128 + c * 32, bv);
+                            tmem_ld_wait();
+                            const bool tlm = warp == 2 && lane == 0 && tile == cid;
+                            if (tlm && cc == 1) tl_mark(p, 10);  // c1 in registers
+                            if (cc == MY - 1) {  // every column of this warp is in registers
+                                tc_fence_before();
+                                __syncwarp();
+                                if (lane == 0) mbar_arrive_cluster(smem_u32(&tempty[acc]) & kPeerBitMask);
+                            }
+                            const int col0 = nb * ncol + c * 32;
+                            if (col0 >= p.N) continue;
+                            float h[32];
+                            if constexpr (SW) {
+#pragma unroll
+                                for (int i = 0; i < 32; ++i)
+                                    h[i] = silu(__uint_as_float(av[i])) * __uint_as_float(bv[i]) * wr;
+                            } else {
+                                act_dispatch(p.act, [&](auto tag) {
+#pragma unroll
+                                    for (int i = 0; i < 32; ++i)
+                                        h[i] = act_t<decltype(tag)::value>(__uint_as_float(av[i])) * wr;
+                                });
+                            }
+                            uint8_t* stg = sC + ((warp - 2) * STG_PER_WARP + stg_n % STG_PER_WARP) * STG_BYTES;
+                            if (tlm && cc < 2) tl_mark(p, 8 + 3 * cc);  // c0 / c1 math done (8, 11)
+                            if (lane == 0) bulk_wait_read<STG_PER_WARP - 1>();
+                            __syncwarp();
+#pragma unroll
+                            for (int u = 0; u < 4; ++u) {
+                                uint4 o;
+                                o.x = pack_bf16(h[8 * u + 0], h[8 * u + 1]);
+                                o.y = pack_bf16(h[8 * u + 2], h[8 * u + 3]);
+                                o.z = pack_bf16(h[8 * u + 4], h[8 * u + 5]);
+                                o.w = pack_bf16(h[8 * u + 6], h[8 * u + 7]);
+                                *reinterpret_cast<uint4*>(stg + lane * 64 + ((u ^ ((lane >> 1) & 3)) << 4)) = o;
+                            }
+                            if (tlm && cc < 2) tl_mark(p, 12 + 2 * cc);  // staged (12, 14)
+                            fence_proxy_async();
+                            __syncwarp();
+                            if (tlm && cc < 2) tl_mark(p, 13 + 2 * cc);  // fenced (13, 15)
+                            if (lane == 0) {
+                                tma_store_2d(&tmC, stg, col0, (int)(row - lane));
+                                bulk_commit();
+                            }
+                            if (tlm && cc == 0) tl_mark(p, 9);  // first store issued
+                            ++stg_n;
+                        }
+                        released = true;
+                    } else {
                     // all of this warp's accumulator columns to registers first, then
                     // release the TMEM buffer: the MMAs of tile i+2 no longer wait for
                     // this tile's math and stores (short-K GEMMs were epilogue-bound)
@@ -593,8 +684,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                                 __syncwarp();
                                 row_to_global(stg, fa, p.save_a + (row - lane) * p.N + col0, p.N, p.N - col0, lane);
                             }
+                            act_dispatch(p.act, [&](auto tag) {
 #pragma unroll
-                            for (int i = 0; i < 32; ++i) h[i] = act_f(__uint_as_float(v[cc][i]), p.act) * wr;
+                                for (int i = 0; i < 32; ++i)
+                                    h[i] = act_t<decltype(tag)::value>(__uint_as_float(v[cc][i])) * wr;
+                            });
                         }
                         if (col0 < p.N) {
                             if (p.tma_out) {
@@ -602,8 +696,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                                 // (64-byte swizzle: 16-byte chunk u of row r at u ^ ((r >> 1) & 3)),
                                 // one TMA store per block
                                 uint8_t* stg = sC + ((warp - 2) * STG_PER_WARP + stg_n % STG_PER_WARP) * STG_BYTES;
+                                if (warp == 2 && lane == 0 && tile == cid) tl_mark(p, 8 + 2 * cc);  // chunk math done
                                 if (lane == 0) bulk_wait_read<STG_PER_WARP - 1>();
                                 __syncwarp();
+                                if (warp == 2 && lane == 0 && tile == cid) tl_mark(p, 9 + 2 * cc);  // staging free
 #pragma unroll
                                 for (int u = 0; u < 4; ++u) {
                                     uint4 o;
@@ -626,6 +722,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                             }
                         }
                     }
+                    }  // !compact
                 }
             }
             if (!released) {
@@ -729,8 +826,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     const uint32_t rank = cluster_ctarank();
     const int NB = SW ? (p.N + 127) / 128 : (p.N + BN - 1) / BN;  // 256-row B blocks
     const int NBW = (NB + 1) / 2;  // super-tiles along N (an odd NB leaves a last single-block super-tile)
-    for (int i = threadIdx.x; i <= p.ngroups; i += blockDim.x) s_gmb[i] = p.grp_mb[i];
-    for (int i = threadIdx.x; i < p.ngroups; i += blockDim.x) s_gw[i] = p.grp_w[i];
+    pdl_trigger();
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
@@ -748,6 +844,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    pdl_wait();  // group tables and operands come from the previous kernels
+    for (int i = threadIdx.x; i <= p.ngroups; i += blockDim.x) s_gmb[i] = p.grp_mb[i];
+    for (int i = threadIdx.x; i < p.ngroups; i += blockDim.x) s_gw[i] = p.grp_w[i];
+    __syncthreads();
     const int KB = (p.K + BK - 1) / BK;
     const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
     const int S = s_gmb[p.ngroups] * NBW;        // super-tiles
@@ -870,24 +970,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                                                  silu(__uint_as_float(v[2 * i + 1])) * __uint_as_float(g[2 * i + 1]) * wr);
                     }
                 } else {
+                    act_dispatch(p.act, [&](auto tag) {
+                        constexpr int A = decltype(tag)::value;
 #pragma unroll
-                    for (int c = 0; c < NCH; c += W_LDC) {
-                        uint32_t v[W_LDC][32];
+                        for (int c = 0; c < NCH; c += W_LDC) {
+                            uint32_t v[W_LDC][32];
 #pragma unroll
-                        for (int cc = 0; cc < W_LDC; ++cc) tmem_ld32(tbase + (c + cc) * 32, v[cc]);
-                        tmem_ld_wait();
-                        if (c == NCH - W_LDC) {
-                            tc_fence_before();
-                            __syncwarp();
-                            if (lane == 0) mbar_arrive_cluster(smem_u32(&tempty[0]) & kPeerBitMask);
+                            for (int cc = 0; cc < W_LDC; ++cc) tmem_ld32(tbase + (c + cc) * 32, v[cc]);
+                            tmem_ld_wait();
+                            if (c == NCH - W_LDC) {
+                                tc_fence_before();
+                                __syncwarp();
+                                if (lane == 0) mbar_arrive_cluster(smem_u32(&tempty[0]) & kPeerBitMask);
+                            }
+#pragma unroll
+                            for (int cc = 0; cc < W_LDC; ++cc)
+#pragma unroll
+                                for (int i = 0; i < 16; ++i)
+                                    pk[c + cc][i] = pack_bf16(act_t<A>(__uint_as_float(v[cc][2 * i])) * wr,
+                                                              act_t<A>(__uint_as_float(v[cc][2 * i + 1])) * wr);
                         }
-#pragma unroll
-                        for (int cc = 0; cc < W_LDC; ++cc)
-#pragma unroll
-                            for (int i = 0; i < 16; ++i)
-                                pk[c + cc][i] = pack_bf16(act_f(__uint_as_float(v[cc][2 * i]), p.act) * wr,
-                                                          act_f(__uint_as_float(v[cc][2 * i + 1]), p.act) * wr);
-                    }
+                    });
                 }
 #pragma unroll
                 for (int c = 0; c < NCH; ++c) {
@@ -941,10 +1044,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                         }
                     }
                     float h[32];
+                    if constexpr (SW) {
 #pragma unroll
-                    for (int i = 0; i < 32; ++i)
-                        h[i] = SW ? silu(__uint_as_float(v[cc][i])) * __uint_as_float(g[cc][i]) * wr
-                                  : act_f(__uint_as_float(v[cc][i]), p.act) * wr;
+                        for (int i = 0; i < 32; ++i) h[i] = silu(__uint_as_float(v[cc][i])) * __uint_as_float(g[cc][i]) * wr;
+                    } else {
+                        act_dispatch(p.act, [&](auto tag) {
+#pragma unroll
+                            for (int i = 0; i < 32; ++i)
+                                h[i] = act_t<decltype(tag)::value>(__uint_as_float(v[cc][i])) * wr;
+                        });
+                    }
                     if (col0 >= p.N) continue;
                     if (p.tma_out) {
                         if (lane == 0) bulk_wait_read<0>();
@@ -1005,18 +1114,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     const uint32_t rank = cluster_ctarank();
     const int NBW = (p.N + 2 * BN - 1) / (2 * BN);
     const int MT = (p.M + 2 * BM - 1) / (2 * BM);
-    if (threadIdx.x == 0) {
-        int run = 0;
-        for (int g = 0; g < p.ngroups; ++g) {
-            s_tb[g] = run;
-            const int rows = p.grp_cnt[g];
-            s_kb0[g] = p.seg_base[g] / BK;
-            s_kbn[g] = (rows + BK - 1) / BK;
-            if (rows > 0) run += MT * NBW;
-        }
-        s_tb[p.ngroups] = run;
-    }
-    for (int i = threadIdx.x; i < p.ngroups; i += blockDim.x) s_gw[i] = p.grp_w[i];
+    pdl_trigger();
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmA);
         tma_prefetch_desc(&tmB);
@@ -1033,6 +1131,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     cluster_sync();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    pdl_wait();  // group tables and operands come from the previous kernels
+    if (threadIdx.x == 0) {
+        int run = 0;
+        for (int g = 0; g < p.ngroups; ++g) {
+            s_tb[g] = run;
+            const int rows = p.grp_cnt[g];
+            s_kb0[g] = p.seg_base[g] / BK;
+            s_kbn[g] = (rows + BK - 1) / BK;
+            if (rows > 0) run += MT * NBW;
+        }
+        s_tb[p.ngroups] = run;
+    }
+    for (int i = threadIdx.x; i < p.ngroups; i += blockDim.x) s_gw[i] = p.grp_w[i];
+    __syncthreads();
     const int num_tiles = s_tb[p.ngroups];
     const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
 
@@ -1152,7 +1264,7 @@ void launch_wide(int grid, const CUtensorMap& ta, const CUtensorMap& tb, const C
                  cudaStream_t st) {
     const int smem = W_SMEM_BYTES + 1024;
     cudaFuncSetAttribute(wide_gemm_kernel<EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    wide_gemm_kernel<EPI><<<grid, THREADS, smem, st>>>(ta, tb, tc, p);
+    launch_pdl(wide_gemm_kernel<EPI>, grid, THREADS, smem, st, ta, tb, tc, p);
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -1176,7 +1288,7 @@ void launch_one(int grid, const CUtensorMap& ta, const CUtensorMap& tb, const CU
                 cudaStream_t st) {
     const int smem = SMEM_BYTES + 1024;
     cudaFuncSetAttribute(grouped_gemm_kernel<EPI, WGRAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    grouped_gemm_kernel<EPI, WGRAD><<<grid, THREADS, smem, st>>>(ta, tb, tc, p);
+    launch_pdl(grouped_gemm_kernel<EPI, WGRAD>, grid, THREADS, smem, st, ta, tb, tc, p);
 }
 
 }  // namespace
@@ -1225,8 +1337,8 @@ void launch_grouped_gemm(EpiMode mode, const GemmArgs& a, int num_sms, cudaStrea
     static const bool tl_on = getenv("OCC_GEMM_TIMELINE") != nullptr;
     static unsigned long long* tl_buf = nullptr;
     if (tl_on) {
-        if (!tl_buf) cudaMalloc(&tl_buf, sizeof(unsigned long long) * 8 * 1024);
-        cudaMemsetAsync(tl_buf, 0, sizeof(unsigned long long) * 8 * 1024, st);
+        if (!tl_buf) cudaMalloc(&tl_buf, sizeof(unsigned long long) * 16 * 1024);
+        cudaMemsetAsync(tl_buf, 0, sizeof(unsigned long long) * 16 * 1024, st);
         p.tl = tl_buf;
     }
     static const bool dbg_on = getenv("OCC_GEMM_DEBUG") != nullptr;
@@ -1292,7 +1404,7 @@ void launch_grouped_gemm(EpiMode mode, const GemmArgs& a, int num_sms, cudaStrea
             if (wide_env != 0 && ((a.N + BN - 1) / BN) % 2 == 0) {
                 const int smem = W_STAGES * (A_BYTES + W_B2) + 256 + 1024;
                 cudaFuncSetAttribute(wide_wgrad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-                wide_wgrad_kernel<<<grid, THREADS, smem, st>>>(ta, tb, p);
+                launch_pdl(wide_wgrad_kernel, grid, THREADS, smem, st, ta, tb, p);
             } else {
                 launch_one<EPI_F32, true>(grid, ta, tb, tc, p, st);
             }
@@ -1300,25 +1412,31 @@ void launch_grouped_gemm(EpiMode mode, const GemmArgs& a, int num_sms, cudaStrea
         }
     }
     if (tl_on) {  // per-CTA timeline (narrow kernel; diagnostics only)
-        unsigned long long h[8 * 1024];
+        static unsigned long long h[16 * 1024];
         cudaStreamSynchronize(st);
-        cudaMemcpy(h, tl_buf, sizeof(unsigned long long) * 8 * grid, cudaMemcpyDeviceToHost);
+        cudaMemcpy(h, tl_buf, sizeof(unsigned long long) * 16 * grid, cudaMemcpyDeviceToHost);
         unsigned long long t0 = ~0ull;
         for (int c = 0; c < grid; ++c)
-            if (h[c * 8] && h[c * 8] < t0) t0 = h[c * 8];
-        double mx[8] = {0, 0, 0, 0, 0, 0, 0, 0}, mn[8] = {1e30, 1e30, 1e30, 1e30, 1e30, 1e30, 1e30, 1e30};
-        for (int c = 0; c < grid; ++c)
-            for (int i = 0; i < 8; ++i)
-                if (h[c * 8 + i]) {
-                    const double v = (h[c * 8 + i] - t0) / 1e3;
-                    mx[i] = std::max(mx[i], v);
-                    mn[i] = std::min(mn[i], v);
-                }
-        fprintf(stderr, "[gemm tl] mode=%d K=%d N=%d grid=%d us from first CTA start (min..max over CTAs): start %.1f..%.1f "
-                "setup %.1f..%.1f acc-ready %.1f..%.1f in-regs %.1f..%.1f first-store %.1f..%.1f epi-issued %.1f..%.1f "
-                "stores-done %.1f..%.1f exit %.1f..%.1f\n",
-                (int)mode, a.K, a.N, grid, mn[0], mx[0], mn[1], mx[1], mn[2], mx[2], mn[6], mx[6], mn[7], mx[7], mn[3],
-                mx[3], mn[4], mx[4], mn[5], mx[5]);
+            if (h[c * 16] && h[c * 16] < t0) t0 = h[c * 16];
+        // (compact epilogue marks: 8 c0 math, 12 c0 staged, 13 c0 fenced, 9 c0 stored, 10 c1 loaded,
+        //  11 c1 math, 14 c1 staged, 15 c1 fenced; unrolled epilogue: 6 in-regs, 7 first store)
+        static const char* names[16] = {"start", "setup", "acc-ready", "epi-issued", "stores-done", "exit", "in-regs",
+                                        "first-store", "c0-math", "c0-stored", "c1-loaded", "c1-math", "c0-staged",
+                                        "c0-fenced", "c1-staged", "c1-fenced"};
+        fprintf(stderr, "[gemm tl] mode=%d K=%d N=%d grid=%d us from first CTA start (min/median/max over CTAs):", (int)mode,
+                a.K, a.N, grid);
+        static const int order[16] = {0, 1, 2, 6, 7, 8, 12, 13, 9, 10, 11, 14, 15, 3, 4, 5};
+        for (int oi = 0; oi < 16; ++oi) {
+            const int i = order[oi];
+            double v[1024];
+            int nv = 0;
+            for (int c = 0; c < grid; ++c)
+                if (h[c * 16 + i]) v[nv++] = (h[c * 16 + i] - t0) / 1e3;
+            if (!nv) continue;
+            std::sort(v, v + nv);
+            fprintf(stderr, " %s %.1f/%.1f/%.1f", names[i], v[0], v[nv / 2], v[nv - 1]);
+        }
+        fprintf(stderr, "\n");
     }
     if (dbg_on) {  // stall-cycle breakdown, averaged over CTAs (diagnostics only)
         unsigned long long h[4 * 1024];

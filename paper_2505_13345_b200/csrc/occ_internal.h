@@ -15,6 +15,31 @@ constexpr int kBM = 256;       // GEMM pair-tile rows (Epd segments are padded t
 extern long long g_launches;
 inline void count_launch(int n = 1) { g_launches += n; }
 
+// Programmatic dependent launch (PDL) for the layer's chain of kernels: the
+// next kernel is launched while its predecessor drains, runs its prologue
+// (barrier init, TMEM allocation, descriptor prefetch) and blocks in
+// griddepcontrol.wait (pdl_wait in occ_common.cuh) until the predecessor's
+// memory is visible.  Only kernels that call pdl_wait() before touching
+// dependent data may be launched this way.  OCC_PDL=0 turns it off.
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    if (pdl_enabled()) {
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+    }
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // ---- generic stable bucketed rank ("warp-ballot / scan compaction") ----
 // Items i < n carry group g_i in [0,G) and a bucket mask m_i (bits < B).
 // rank(i, b) = #{i' < i : g_i' = g_i, b in m_i'}; grank(i) = #{i' < i : g_i' = g_i}.
@@ -291,6 +316,7 @@ struct FusedPlanArgs {
     long long* stats;
     int32_t* err;
     int scatter = 1;         // copy the Epd A rows in the kernel (else the caller runs launch_scatter_rows)
+    int zero_stats = 0;      // stats[0..7] zeroed in the kernel (no memset node before it)
     unsigned long long* dbg = nullptr;  // OCC_PLAN_DEBUG phase timeline
 };
 bool fused_plan_supported(int nd, int E, int k);

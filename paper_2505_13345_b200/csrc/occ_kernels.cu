@@ -16,6 +16,13 @@
 namespace occ {
 
 long long g_launches = 0;
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("OCC_PDL");
+        return !e || atoi(e) != 0;
+    }();
+    return on;
+}
 
 namespace {
 
@@ -444,6 +451,8 @@ __global__ void init_epd_kernel(int Q, int32_t* src, float* w) {
 __global__ void __launch_bounds__(256) scatter_rows_kernel(int R_max, const int* R_total, int P, int D,
                                                            const __nv_bfloat16* src, const int32_t* src_rows,
                                                            const int32_t* row_epd, __nv_bfloat16* dst) {
+    pdl_trigger();
+    pdl_wait();  // launched with PDL: inputs come from the previous kernel
     // one warp per (row, 2 KB slice): 4 uint4 per lane in flight
     constexpr int kSlice = 128;  // uint4 per slice
     const int nvec = D / 8;
@@ -483,6 +492,8 @@ __global__ void __launch_bounds__(256) scatter_rows_kernel(int R_max, const int*
 
 // Zero the padding rows of every Epd segment (rows cnt..roundup(cnt, kBM)).
 __global__ void __launch_bounds__(256) zero_pad_rows_kernel(int NG, ComputeOffsets o, int D, __nv_bfloat16* dst) {
+    pdl_trigger();
+    pdl_wait();  // launched with PDL: inputs come from the previous kernel
     const int g = blockIdx.x;
     if (g >= NG) return;
     const int cnt = o.cnt[g];
@@ -782,6 +793,8 @@ __global__ void __launch_bounds__(256) combine_fused_kernel(int n, int nd, int k
                                                             const uint64_t* mask, const int32_t* tok_row,
                                                             const int32_t* row_epd, const __nv_bfloat16* Y,
                                                             const __nv_bfloat16* ys, __nv_bfloat16* out) {
+    pdl_trigger();
+    pdl_wait();  // launched with PDL: inputs come from the previous kernel
     __shared__ int s_q[8][kMaxTopK];
     const int wib = threadIdx.x >> 5;
     const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -1642,11 +1655,11 @@ void launch_scatter_rows(int R_max, const int* R_total, int P, int D, const __nv
                          __nv_bfloat16* dst, cudaStream_t st) {
     if (!R_max) return;
     const long warps = (long)R_max * ((D / 8 + 127) / 128);
-    scatter_rows_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, st>>>(R_max, R_total, P, D, src, src_rows, row_epd,
-                                                                     dst);
+    launch_pdl(scatter_rows_kernel, dim3((unsigned)((warps + 7) / 8)), dim3(256), 0, st, R_max, R_total, P, D, src,
+               src_rows, row_epd, dst);
     // up to kBM - 1 padding rows per segment: spread each over enough blocks
     const int ny = std::max(1, std::min(64, (int)((long)(kBM - 1) * D / 8 / (256 * 16))));
-    zero_pad_rows_kernel<<<dim3(NG, ny), 256, 0, st>>>(NG, o, D, dst);
+    launch_pdl(zero_pad_rows_kernel, dim3(NG, ny), dim3(256), 0, st, NG, o, D, dst);
     count_launch(2);
 }
 
@@ -1730,11 +1743,14 @@ void launch_combine_fused(int n, int nd, int k, int P, int dedup, int D, const u
     if (!n) return;
     const dim3 grid((n + 7) / 8);
     if (k <= 2)
-        combine_fused_kernel<2><<<grid, 256, 0, st>>>(n, nd, k, P, dedup, D, mask, tok_row, row_epd, Y, ys, out);
+        launch_pdl(combine_fused_kernel<2>, grid, dim3(256), 0, st, n, nd, k, P, dedup, D, mask, tok_row, row_epd, Y,
+                   ys, out);
     else if (k <= 4)
-        combine_fused_kernel<4><<<grid, 256, 0, st>>>(n, nd, k, P, dedup, D, mask, tok_row, row_epd, Y, ys, out);
+        launch_pdl(combine_fused_kernel<4>, grid, dim3(256), 0, st, n, nd, k, P, dedup, D, mask, tok_row, row_epd, Y,
+                   ys, out);
     else
-        combine_fused_kernel<8><<<grid, 256, 0, st>>>(n, nd, k, P, dedup, D, mask, tok_row, row_epd, Y, ys, out);
+        launch_pdl(combine_fused_kernel<8>, grid, dim3(256), 0, st, n, nd, k, P, dedup, D, mask, tok_row, row_epd, Y,
+                   ys, out);
     count_launch();
 }
 

@@ -52,9 +52,10 @@ namespace {
 
 constexpr int kThreads = 256;  // 8 warps per block
 constexpr int kWarps = kThreads / 32;
+constexpr long kSmallCounts = 4096;  // count-matrix size below which the scan phase is skipped
 
 struct Tables {  // phase C results, in shared memory
-    int *C, *off_sd, *inoff, *in_base, *ntok, *tok_base, *cnt, *seg_base, *ebase, *padpre, *dev, *slot;
+    int *C, *off_sd, *inoff, *in_base, *ntok, *tok_base, *cnt, *seg_base, *ebase, *padpre, *dev, *slot, *pre;
 };
 
 __device__ __forceinline__ int token_src(const FusedPlanArgs& a, int t) {
@@ -159,6 +160,8 @@ __device__ __forceinline__ void phase_mark(const FusedPlanArgs& a, int i) {
 }
 
 __global__ void __launch_bounds__(kThreads) fused_plan_kernel(FusedPlanArgs a) {
+    pdl_trigger();
+    pdl_wait();  // routing comes from the router kernel (PDL launch)
     phase_mark(a, 0);
     extern __shared__ int smem[];
     cg::grid_group grid = cg::this_grid();
@@ -184,6 +187,7 @@ __global__ void __launch_bounds__(kThreads) fused_plan_kernel(FusedPlanArgs a) {
         T.dev = p, p += E;
         T.slot = p, p += E;
         T.ebase = p, p += nd * E; // [nd][E]
+        T.pre = p, p += K;        // small mode: this block's chunk prefix per key
     }
     // global warp index, spread so consecutive work items land on different SMs
     // (blocks are placed round-robin over the SMs)
@@ -195,6 +199,11 @@ __global__ void __launch_bounds__(kThreads) fused_plan_kernel(FusedPlanArgs a) {
     __syncthreads();
 
     // ---------------------------------------------------------------- A --
+    if (a.zero_stats && blockIdx.x == 0 && threadIdx.x < 8) a.stats[threadIdx.x] = 0;  // atomics start after the barrier
+    // small count matrices (K x nchunks <= kSmallCounts): no scan phase; every
+    // block sums the matrix itself (totals and its own chunk's prefix), which
+    // saves a grid-wide barrier and a dependent phase on small batches
+    const bool small = (long)K * nchunks <= kSmallCounts && nchunks <= (int)gridDim.x;
     for (int c = blockIdx.x; c < nchunks; c += gridDim.x) {
         for (int i = threadIdx.x; i < kWarps * K; i += kThreads) wcnt[i] = 0;
         __syncthreads();
@@ -211,6 +220,36 @@ __global__ void __launch_bounds__(kThreads) fused_plan_kernel(FusedPlanArgs a) {
     }
     phase_mark(a, 1);
     grid.sync();
+    int* tot = wcnt;  // the K totals, staged (phase C)
+    if (small) {
+        // one chunk per block at most: totals and this block's exclusive prefix in one pass
+        // one warp per key: lanes stride over the chunks (coalesced, all loads
+        // in flight together), shuffle reductions
+        int* pre = T.pre;
+        const int mine = blockIdx.x;
+        for (int key = warp; key < K; key += kWarps) {
+            const int* row = a.chunk_cnt + (long)key * nchunks;
+            int t = 0, b = 0;
+#pragma unroll 4
+            for (int c = lane; c < nchunks; c += 32) {
+                const int v = __ldcg(row + c);
+                b += c < mine ? v : 0;
+                t += v;
+            }
+            for (int o = 16; o; o >>= 1) {
+                t += __shfl_xor_sync(kFull, t, o);
+                b += __shfl_xor_sync(kFull, b, o);
+            }
+            if (lane == 0) {
+                tot[key] = t;
+                pre[key] = b;
+            }
+        }
+        if (blockIdx.x == 0)
+            for (int key = threadIdx.x; key < K; key += kThreads) a.totals[key] = tot[key];
+        phase_mark(a, 2);
+        __syncthreads();
+    } else {
     // ---------------------------------------------------------------- B --
     // one block per key: each thread scans a contiguous run of chunks (loads
     // independent, in flight together), block exclusive scan of the run sums
@@ -246,10 +285,10 @@ __global__ void __launch_bounds__(kThreads) fused_plan_kernel(FusedPlanArgs a) {
     }
     phase_mark(a, 2);
     grid.sync();
-    // ---------------------------------------------------------------- C --
-    int* tot = wcnt;  // the K totals, staged
     for (int i = threadIdx.x; i < K; i += kThreads) tot[i] = a.totals[i];
     __syncthreads();
+    }
+    // ---------------------------------------------------------------- C --
     for (int i = threadIdx.x; i < nd * nd; i += kThreads) T.C[i] = tot[(i / nd) * (nd + 1) + i % nd];
     for (int e = threadIdx.x; e < E; e += kThreads) {  // group counts from the expert keys
         int c = 0;
@@ -357,6 +396,7 @@ __global__ void __launch_bounds__(kThreads) fused_plan_kernel(FusedPlanArgs a) {
     }
     phase_mark(a, 3);
     __syncthreads();  // (the staged totals in wcnt are dead from here)
+
     // ---------------------------------------------------------------- D --
     long long st_naive = 0, st_span = 0, st_intra = 0, st_inter = 0;
     for (int c = blockIdx.x; c < nchunks; c += gridDim.x) {
@@ -367,7 +407,7 @@ __global__ void __launch_bounds__(kThreads) fused_plan_kernel(FusedPlanArgs a) {
         entry_counts(a, x, wcnt + warp * K, lane, md, mg, me);
         __syncthreads();
         for (int key = threadIdx.x; key < K; key += kThreads) {  // exclusive bases per warp
-            int run = a.chunk_cnt[(long)key * nchunks + c];
+            int run = small ? T.pre[key] : a.chunk_cnt[(long)key * nchunks + c];
             for (int w = 0; w < kWarps; ++w) {
                 const int v = wcnt[w * K + key];
                 wcnt[w * K + key] = run;
@@ -509,7 +549,7 @@ __global__ void __launch_bounds__(kThreads) fused_plan_kernel(FusedPlanArgs a) {
 
 size_t fused_smem(int nd, int E, int k) {
     const int K = nd * (nd + 1) + nd * E;
-    const int tabs = 3 * nd * nd + (nd + 1) + 2 * nd + 5 * E + 1 + nd * E;
+    const int tabs = 3 * nd * nd + (nd + 1) + 2 * nd + 5 * E + 1 + nd * E + K;
     (void)k;
     return sizeof(int) * ((size_t)kWarps * K + tabs);
 }
@@ -542,7 +582,9 @@ bool launch_fused_plan(const FusedPlanArgs& a, int num_sms, cudaStream_t st) {
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_plan_kernel, kThreads, smem) != cudaSuccess ||
         per_sm < 1)
         return false;
-    const int blocks = num_sms * std::min(per_sm, 4);
+    int blocks = num_sms * std::min(per_sm, 4);
+    static const int blocks_env = getenv("OCC_PLAN_BLOCKS") ? atoi(getenv("OCC_PLAN_BLOCKS")) : 0;  // sweeps (profiles/)
+    if (blocks_env > 0) blocks = std::min(blocks_env, num_sms * per_sm);
     FusedPlanArgs args = a;
     static const bool dbg_on = getenv("OCC_PLAN_DEBUG") != nullptr;  // phase timeline (diagnostics only)
     static unsigned long long* dbg = nullptr;
@@ -552,9 +594,29 @@ bool launch_fused_plan(const FusedPlanArgs& a, int num_sms, cudaStream_t st) {
         cudaMemsetAsync(dbg, 0xFF, sizeof(unsigned long long), st);
         args.dbg = dbg;
     }
-    void* params[] = {&args};
-    if (cudaLaunchCooperativeKernel((const void*)fused_plan_kernel, blocks, kThreads, params, smem, st) != cudaSuccess)
-        return false;
+    // cooperative (grid-wide barriers) and, when allowed, programmatic: the
+    // kernel's blocks become resident while the router drains
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    if (cudaLaunchKernelEx(&cfg, fused_plan_kernel, args) != cudaSuccess) {
+        cudaGetLastError();
+        if (cfg.numAttrs == 1) return false;
+        cfg.numAttrs = 1;  // this driver refuses cooperative + programmatic: plain cooperative launch
+        if (cudaLaunchKernelEx(&cfg, fused_plan_kernel, args) != cudaSuccess) {
+            cudaGetLastError();
+            return false;
+        }
+    }
     count_launch();
     if (dbg_on) {
         unsigned long long h[8];

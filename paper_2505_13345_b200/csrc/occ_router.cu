@@ -52,8 +52,7 @@ __global__ void __launch_bounds__(RTHREADS, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     __shared__ uint8_t s_dev[256];  // expert -> device (pruning)
-    if (p.prune)
-        for (int i = threadIdx.x; i < p.e; i += blockDim.x) s_dev[i] = (uint8_t)p.dev_of[i];
+    pdl_trigger();
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&tmX);
         tma_prefetch_desc(&tmG);
@@ -69,6 +68,9 @@ __global__ void __launch_bounds__(RTHREADS, 1)
     }
     constexpr int TCOLS = 2 * NPMAX <= 32 ? 32 : (2 * NPMAX <= 64 ? 64 : (2 * NPMAX <= 128 ? 128 : (2 * NPMAX <= 256 ? 256 : 512)));
     if (warp == 1) tmem_alloc<TCOLS>(tmem_slot);
+    pdl_wait();  // x (and the tables) may come from the previous kernel in the stream
+    if (p.prune)
+        for (int i = threadIdx.x; i < p.e; i += blockDim.x) s_dev[i] = (uint8_t)p.dev_of[i];
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -284,7 +286,7 @@ void launch_router_np(const CUtensorMap& tx, const CUtensorMap& tg, const Router
     const int grid = tiles < num_sms ? tiles : num_sms;
     const int smem = rstages<NPMAX>() * (R_A_BYTES + p.np * RK * 2) + 256 + 1024;
     cudaFuncSetAttribute(router_tc_kernel<NPMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    router_tc_kernel<NPMAX><<<grid, RTHREADS, smem, st>>>(tx, tg, p);
+    launch_pdl(router_tc_kernel<NPMAX>, grid, RTHREADS, smem, st, tx, tg, p);
 }
 
 }  // namespace

@@ -8,7 +8,7 @@ HERE=$(cd "$(dirname "$0")" && pwd)
 CSRC=$HERE/../paper_2505_13345_b200/csrc
 NAME=$1; shift
 OUT=$HERE/variants; mkdir -p $OUT/$NAME
-NCCL=/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl
+NCCL=$(python3 -c "import nvidia.nccl as m; print(list(m.__path__)[0])")
 FL="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC,-O2 --expt-relaxed-constexpr -I$NCCL/include"
 nvcc $FL "$@" -c $CSRC/occ_gemm.cu -o $OUT/$NAME/occ_gemm.o
 OBJS=$(ls $CSRC/build/*.o | grep -v occ_gemm.o)
