@@ -293,6 +293,16 @@ constexpr int kPackVec = 8;  // 16-byte vectors per lane in flight in the pack k
 __device__ __forceinline__ void pack_token(const PackArgs& a, int t, int lane) {
     const int nvec = a.D / 8;
     const uint4* src = reinterpret_cast<const uint4*>(a.x + (long)t * a.D);
+    // the row's first slice is in flight while the destination rows resolve
+    // (mask -> tok_row is a dependent chain of two loads)
+    uint4 buf[kPackVec];
+    if (a.dst_x) {
+#pragma unroll
+        for (int u = 0; u < kPackVec; ++u) {
+            const int v = u * 32 + lane;
+            if (v < nvec) buf[u] = __ldg(src + v);
+        }
+    }
     int rows[kMaxDev];
     int nrows = 0;
     if (a.dedup) {
@@ -308,11 +318,12 @@ __device__ __forceinline__ void pack_token(const PackArgs& a, int t, int lane) {
     }
     // the whole row in flight (16 x 16 B per lane covers D = 4096 in one round trip)
     for (int v0 = 0; a.dst_x && v0 < nvec; v0 += kPackVec * 32) {
-        uint4 buf[kPackVec];
+        if (v0) {
 #pragma unroll
-        for (int u = 0; u < kPackVec; ++u) {
-            const int v = v0 + u * 32 + lane;
-            if (v < nvec) buf[u] = __ldg(src + v);
+            for (int u = 0; u < kPackVec; ++u) {
+                const int v = v0 + u * 32 + lane;
+                if (v < nvec) buf[u] = __ldg(src + v);
+            }
         }
         for (int q = 0; q < nrows; ++q) {
             uint4* dst = reinterpret_cast<uint4*>(a.dst_x + (long)rows[q] * a.D);
@@ -509,66 +520,102 @@ __global__ void __launch_bounds__(256) zero_pad_rows_kernel(int NG, ComputeOffse
 // merge_matmul's per-row sum over local experts (pipeline.cpp:263-281),
 // done after the grouped GEMM: ascending placement-list order, fp32.
 
-// Sum of nq bf16 rows (indices in shared memory, summed in list order, fp32)
-// + an optional extra row, rounded to bf16: KU 16-byte row vectors in flight.
-template <int KU>
-__device__ __forceinline__ void sum_rows_ordered(const __nv_bfloat16* Y, const int* qs, int nq, int D, int lane,
-                                                 const __nv_bfloat16* extra, __nv_bfloat16* dst) {
-    // two 16-byte vectors of the row per lane per pass: 2 x KU row loads in flight
+#ifndef OCC_CMB_VEC
+#define OCC_CMB_VEC 8  // row vectors in flight per lane in the ordered row sums (KU rows x OCC_CMB_VEC / KU)
+#endif
+// Streaming 16-byte store (evict-first): the combine / return outputs are
+// written once and not re-read by this layer (profiles/probes/hbm_pattern_probe.cu:
+// 2-rows-in / 1-row-out at 5.6 TB/s with plain stores, 6.0 TB/s with .cs).
+__device__ __forceinline__ void st_stream(void* p, uint4 v) {
+    asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+__device__ __forceinline__ void add_bf16x8(float* a, const uint4& u) {
+    const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        const float2 f = __bfloat1622float2(hh[e]);
+        a[2 * e] += f.x;
+        a[2 * e + 1] += f.y;
+    }
+}
+
+// Ordered sum of nq bf16 rows Y[qs[0..nq)] (+ an optional extra row), fp32,
+// rounded to bf16.  GROUPS: bit i of `opens` starts a new group at entry i;
+// each group's partial sum is rounded to bf16 (the payload the multi-GPU
+// return would carry) before it is added, so one-GPU results equal the
+// exchanged path bit for bit.  Per element the summation order is the list
+// order in every configuration.  A lane keeps V 16-byte vectors of each of KU
+// rows in flight (KU x V loads per round trip; V x 512 B per warp and row).
+template <int KU, int V, bool GROUPS>
+__device__ __forceinline__ void sum_rows_v(const __nv_bfloat16* Y, const int* qs, int nq, uint64_t opens, int D,
+                                           int lane, const __nv_bfloat16* extra, __nv_bfloat16* dst) {
     const int nv = D / 8;
-    for (int v = lane; v < nv; v += 64) {
-        const bool two = v + 32 < nv;
-        float acc[2][8];
+    for (int v0 = 0; v0 < nv; v0 += 32 * V) {
+        float acc[V][8], grp[GROUPS ? V : 1][8];
 #pragma unroll
-        for (int h = 0; h < 2; ++h)
+        for (int w = 0; w < V; ++w)
 #pragma unroll
-            for (int e = 0; e < 8; ++e) acc[h][e] = 0.f;
+            for (int e = 0; e < 8; ++e) {
+                acc[w][e] = 0.f;
+                if constexpr (GROUPS) grp[w][e] = 0.f;
+            }
         for (int i0 = 0; i0 < nq; i0 += KU) {
-            uint4 u[2][KU];
+            uint4 u[KU][V];
 #pragma unroll
             for (int j = 0; j < KU; ++j)
                 if (i0 + j < nq) {
-                    const uint4* r = reinterpret_cast<const uint4*>(Y + (long)qs[i0 + j] * D);
-                    u[0][j] = __ldg(r + v);
-                    if (two) u[1][j] = __ldg(r + v + 32);
+                    const uint4* r = reinterpret_cast<const uint4*>(Y + (long)qs[i0 + j] * D) + v0 + lane;
+#pragma unroll
+                    for (int w = 0; w < V; ++w)
+                        if (v0 + lane + 32 * w < nv) u[j][w] = __ldg(r + 32 * w);
                 }
 #pragma unroll
             for (int j = 0; j < KU; ++j) {
                 if (i0 + j >= nq) break;
+                if constexpr (GROUPS) {
+                    if (i0 + j && i0 + j < 64 && ((opens >> (i0 + j)) & 1)) {
 #pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&u[h][j]);
+                        for (int w = 0; w < V; ++w)
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const float2 f = __bfloat1622float2(hh[e]);
-                        acc[h][2 * e] += f.x;
-                        acc[h][2 * e + 1] += f.y;
+                            for (int e = 0; e < 8; ++e) {
+                                acc[w][e] += __bfloat162float(__float2bfloat16(grp[w][e]));
+                                grp[w][e] = 0.f;
+                            }
                     }
+#pragma unroll
+                    for (int w = 0; w < V; ++w) add_bf16x8(grp[w], u[j][w]);
+                } else {
+#pragma unroll
+                    for (int w = 0; w < V; ++w) add_bf16x8(acc[w], u[j][w]);
                 }
             }
         }
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            if (h == 1 && !two) break;
-            const int vv = v + 32 * h;
-            if (extra) {
-                const uint4 w = __ldg(reinterpret_cast<const uint4*>(extra) + vv);
-                const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&w);
+        for (int w = 0; w < V; ++w) {
+            const int vv = v0 + lane + 32 * w;
+            if (vv >= nv) break;
+            if constexpr (GROUPS) {
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const float2 f = __bfloat1622float2(hh[e]);
-                    acc[h][2 * e] += f.x;
-                    acc[h][2 * e + 1] += f.y;
-                }
+                for (int e = 0; e < 8; ++e) acc[w][e] += __bfloat162float(__float2bfloat16(grp[w][e]));
             }
+            if (extra) add_bf16x8(acc[w], __ldg(reinterpret_cast<const uint4*>(extra) + vv));
             uint4 o;
-            o.x = pack_bf16(acc[h][0], acc[h][1]);
-            o.y = pack_bf16(acc[h][2], acc[h][3]);
-            o.z = pack_bf16(acc[h][4], acc[h][5]);
-            o.w = pack_bf16(acc[h][6], acc[h][7]);
-            reinterpret_cast<uint4*>(dst)[vv] = o;
+            o.x = pack_bf16(acc[w][0], acc[w][1]);
+            o.y = pack_bf16(acc[w][2], acc[w][3]);
+            o.z = pack_bf16(acc[w][4], acc[w][5]);
+            o.w = pack_bf16(acc[w][6], acc[w][7]);
+            st_stream(reinterpret_cast<uint4*>(dst) + vv, o);
         }
     }
+}
+
+// Sum of nq bf16 rows (indices in shared memory, summed in list order, fp32)
+// + an optional extra row, rounded to bf16: KU rows x (8 / KU) vectors in flight.
+template <int KU>
+__device__ __forceinline__ void sum_rows_ordered(const __nv_bfloat16* Y, const int* qs, int nq, int D, int lane,
+                                                 const __nv_bfloat16* extra, __nv_bfloat16* dst) {
+    sum_rows_v<KU, (KU >= 8 ? 1 : OCC_CMB_VEC / KU), false>(Y, qs, nq, 0, D, lane, extra, dst);
 }
 
 // Append the non-negative entries of idx[0..cnt) (lane-parallel, order kept)
@@ -788,7 +835,11 @@ __global__ void one_source_totals_kernel(int nd, int r, int* totals) {
 // The token's row list is built warp-parallel (lane p reads row_epd[r, p],
 // ballot-compacted into shared memory); KU product rows are in flight per
 // 16-byte vector (KU = 2 / 4 / 8 picked from k at launch).
-template <int KU>
+// GROUPED = false when every row of a token is one group with nothing added
+// after it (one device, no shared experts): bf16(bf16(sum)) == bf16(sum), so
+// the plain ordered sum gives the same bits with half the accumulators (more
+// warps resident, more row loads in flight).
+template <int KU, bool GROUPED>
 __global__ void __launch_bounds__(256) combine_fused_kernel(int n, int nd, int k, int P, int dedup, int D,
                                                             const uint64_t* mask, const int32_t* tok_row,
                                                             const int32_t* row_epd, const __nv_bfloat16* Y,
@@ -828,52 +879,10 @@ __global__ void __launch_bounds__(256) combine_fused_kernel(int n, int nd, int k
     }
     nq = nq < kMaxTopK ? nq : kMaxTopK;
     __syncwarp();
-    const int nv = D / 8;
-    for (int v = lane; v < nv; v += 32) {
-        float acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, dev[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        for (int i0 = 0; i0 < nq; i0 += KU) {
-            uint4 u[KU];
-#pragma unroll
-            for (int j = 0; j < KU; ++j)
-                if (i0 + j < nq) u[j] = __ldg(reinterpret_cast<const uint4*>(Y + (long)qs[i0 + j] * D) + v);
-#pragma unroll
-            for (int j = 0; j < KU; ++j) {
-                if (i0 + j >= nq) break;
-                if (i0 + j && ((newdev >> (i0 + j)) & 1)) {
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) {
-                        acc[e] += __bfloat162float(__float2bfloat16(dev[e]));
-                        dev[e] = 0.f;
-                    }
-                }
-                const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&u[j]);
-#pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    const float2 f = __bfloat1622float2(hh[e]);
-                    dev[2 * e] += f.x;
-                    dev[2 * e + 1] += f.y;
-                }
-            }
-        }
-#pragma unroll
-        for (int e = 0; e < 8; ++e) acc[e] += __bfloat162float(__float2bfloat16(dev[e]));
-        if (ys) {  // shared experts (source device), added last
-            const uint4 w = __ldg(reinterpret_cast<const uint4*>(ys + (long)t * D) + v);
-            const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&w);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const float2 f = __bfloat1622float2(hh[e]);
-                acc[2 * e] += f.x;
-                acc[2 * e + 1] += f.y;
-            }
-        }
-        uint4 o;
-        o.x = pack_bf16(acc[0], acc[1]);
-        o.y = pack_bf16(acc[2], acc[3]);
-        o.z = pack_bf16(acc[4], acc[5]);
-        o.w = pack_bf16(acc[6], acc[7]);
-        reinterpret_cast<uint4*>(out + (long)t * D)[v] = o;
-    }
+    // devices in ascending order, each device's rows rounded to the bf16 return
+    // payload, the shared-expert row last
+    sum_rows_v<KU, (KU >= 8 ? 1 : OCC_CMB_VEC / KU), GROUPED>(Y, qs, nq, newdev, D, lane,
+                                                             ys ? ys + (long)t * D : nullptr, out + (long)t * D);
 }
 
 // ------------------------------------------------- peer-memory exchange ---
@@ -904,6 +913,12 @@ __device__ __forceinline__ void peer_pack_token(const PackArgs& a, int me, const
                                                 const int* inoff, void* const* peer_tab, int t, int lane) {
     const int nvec = a.D / 8;
     const uint4* src = reinterpret_cast<const uint4*>(a.x + (long)t * a.D);
+    uint4 buf[kPackVec];  // the row's first slice in flight while the destination rows resolve
+#pragma unroll
+    for (int u = 0; u < kPackVec; ++u) {
+        const int v = u * 32 + lane;
+        if (v < nvec) buf[u] = __ldg(src + v);
+    }
     int nrow = 0, dsts[kMaxTopK], rows[kMaxTopK], jsel[kMaxTopK];
     if (a.dedup) {  // one row per destination device
         uint64_t m = a.mask[t];
@@ -926,11 +941,12 @@ __device__ __forceinline__ void peer_pack_token(const PackArgs& a, int me, const
     // x row: read once, the whole row in flight (16 16-byte vectors per lane),
     // stored to every destination inbox row (NVLink peer stores)
     for (int v0 = 0; v0 < nvec; v0 += kPackVec * 32) {
-        uint4 buf[kPackVec];
+        if (v0) {
 #pragma unroll
-        for (int u = 0; u < kPackVec; ++u) {
-            const int v = v0 + u * 32 + lane;
-            if (v < nvec) buf[u] = __ldg(src + v);
+            for (int u = 0; u < kPackVec; ++u) {
+                const int v = v0 + u * 32 + lane;
+                if (v < nvec) buf[u] = __ldg(src + v);
+            }
         }
         for (int q = 0; q < nrow; ++q) {
             uint4* dst = reinterpret_cast<uint4*>(
@@ -1742,15 +1758,13 @@ void launch_combine_fused(int n, int nd, int k, int P, int dedup, int D, const u
                           const __nv_bfloat16* ys, __nv_bfloat16* out, cudaStream_t st) {
     if (!n) return;
     const dim3 grid((n + 7) / 8);
-    if (k <= 2)
-        launch_pdl(combine_fused_kernel<2>, grid, dim3(256), 0, st, n, nd, k, P, dedup, D, mask, tok_row, row_epd, Y,
-                   ys, out);
-    else if (k <= 4)
-        launch_pdl(combine_fused_kernel<4>, grid, dim3(256), 0, st, n, nd, k, P, dedup, D, mask, tok_row, row_epd, Y,
-                   ys, out);
-    else
-        launch_pdl(combine_fused_kernel<8>, grid, dim3(256), 0, st, n, nd, k, P, dedup, D, mask, tok_row, row_epd, Y,
-                   ys, out);
+    const bool grouped = !(nd == 1 && dedup && !ys);
+#define OCC_CF(KU, G) \
+    launch_pdl(combine_fused_kernel<KU, G>, grid, dim3(256), 0, st, n, nd, k, P, dedup, D, mask, tok_row, row_epd, Y, ys, out)
+    if (k <= 2) grouped ? OCC_CF(2, true) : OCC_CF(2, false);
+    else if (k <= 4) grouped ? OCC_CF(4, true) : OCC_CF(4, false);
+    else grouped ? OCC_CF(8, true) : OCC_CF(8, false);
+#undef OCC_CF
     count_launch();
 }
 
