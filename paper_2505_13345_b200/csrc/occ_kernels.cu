@@ -547,7 +547,10 @@ __device__ __forceinline__ void add_bf16x8(float* a, const uint4& u) {
 // exchanged path bit for bit.  Per element the summation order is the list
 // order in every configuration.  A lane keeps V 16-byte vectors of each of KU
 // rows in flight (KU x V loads per round trip; V x 512 B per warp and row).
-template <int KU, int V, bool GROUPS>
+// ROUND_FIRST (one group, then the extra row): the rows' sum is rounded to
+// bf16 before the extra row is added -- GROUPS with a single group, without
+// the second accumulator.
+template <int KU, int V, bool GROUPS, bool ROUND_FIRST = false>
 __device__ __forceinline__ void sum_rows_v(const __nv_bfloat16* Y, const int* qs, int nq, uint64_t opens, int D,
                                            int lane, const __nv_bfloat16* extra, __nv_bfloat16* dst) {
     const int nv = D / 8;
@@ -598,6 +601,10 @@ __device__ __forceinline__ void sum_rows_v(const __nv_bfloat16* Y, const int* qs
             if constexpr (GROUPS) {
 #pragma unroll
                 for (int e = 0; e < 8; ++e) acc[w][e] += __bfloat162float(__float2bfloat16(grp[w][e]));
+            }
+            if constexpr (ROUND_FIRST) {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) acc[w][e] = __bfloat162float(__float2bfloat16(acc[w][e]));
             }
             if (extra) add_bf16x8(acc[w], __ldg(reinterpret_cast<const uint4*>(extra) + vv));
             uint4 o;
@@ -835,10 +842,11 @@ __global__ void one_source_totals_kernel(int nd, int r, int* totals) {
 // The token's row list is built warp-parallel (lane p reads row_epd[r, p],
 // ballot-compacted into shared memory); KU product rows are in flight per
 // 16-byte vector (KU = 2 / 4 / 8 picked from k at launch).
-// GROUPED = false when every row of a token is one group with nothing added
-// after it (one device, no shared experts): bf16(bf16(sum)) == bf16(sum), so
-// the plain ordered sum gives the same bits with half the accumulators (more
-// warps resident, more row loads in flight).
+// GROUPED = 0 (one device): every row of a token is one group, so the plain
+// ordered sum gives the same bits with half the accumulators (more warps
+// resident, more row loads in flight) -- bf16(bf16(sum)) == bf16(sum), and
+// with shared experts the sum is rounded before their row is added
+// (ROUND_FIRST), exactly what the one-group grouped sum does.
 template <int KU, bool GROUPED>
 __global__ void __launch_bounds__(256) combine_fused_kernel(int n, int nd, int k, int P, int dedup, int D,
                                                             const uint64_t* mask, const int32_t* tok_row,
@@ -881,8 +889,9 @@ __global__ void __launch_bounds__(256) combine_fused_kernel(int n, int nd, int k
     __syncwarp();
     // devices in ascending order, each device's rows rounded to the bf16 return
     // payload, the shared-expert row last
-    sum_rows_v<KU, (KU >= 8 ? 1 : OCC_CMB_VEC / KU), GROUPED>(Y, qs, nq, newdev, D, lane,
-                                                             ys ? ys + (long)t * D : nullptr, out + (long)t * D);
+    sum_rows_v<KU, (KU >= 8 ? 1 : OCC_CMB_VEC / KU), GROUPED, !GROUPED>(Y, qs, nq, newdev, D, lane,
+                                                                       ys ? ys + (long)t * D : nullptr,
+                                                                       out + (long)t * D);
 }
 
 // ------------------------------------------------- peer-memory exchange ---
@@ -1758,7 +1767,7 @@ void launch_combine_fused(int n, int nd, int k, int P, int dedup, int D, const u
                           const __nv_bfloat16* ys, __nv_bfloat16* out, cudaStream_t st) {
     if (!n) return;
     const dim3 grid((n + 7) / 8);
-    const bool grouped = !(nd == 1 && dedup && !ys);
+    const bool grouped = !(nd == 1 && dedup);
 #define OCC_CF(KU, G) \
     launch_pdl(combine_fused_kernel<KU, G>, grid, dim3(256), 0, st, n, nd, k, P, dedup, D, mask, tok_row, row_epd, Y, ys, out)
     if (k <= 2) grouped ? OCC_CF(2, true) : OCC_CF(2, false);
