@@ -188,6 +188,9 @@ struct occ_handle {
     // the multi-kernel chain (occ_set_plan_kernels(h, 0) / OCC_FUSED_PLAN=0)
     int fused_plan = 1;
     DevBuf<int> fp_ws;
+    // dynamic tile schedulers of the grouped GEMMs: 2 ints (next tile, pairs
+    // done) per launch site, zeroed once, left zeroed by every launch
+    DevBuf<int> gsched;
     DispatchOffsets dofs{};
     ComputeOffsets cofs{};
     int* d_tok_base = nullptr;
@@ -606,6 +609,10 @@ occ_status upload_tables(occ_handle* h) {
     CUDA_TRY(cudaMemcpy(h->d_dev_of.p, h->dev_of.data(), sizeof(int32_t) * h->E, cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(h->d_slot_of.p, h->slot_of.data(), sizeof(int32_t) * h->E, cudaMemcpyHostToDevice));
     CUDA_TRY(cudaMemcpy(h->d_widx.p, widx.data(), sizeof(int32_t) * widx.size(), cudaMemcpyHostToDevice));
+    if (!h->gsched.p) {
+        CUDA_TRY(h->gsched.ensure(2 * kSchedSlots));
+        CUDA_TRY(cudaMemset(h->gsched.p, 0, sizeof(int) * 2 * kSchedSlots));
+    }
     return OCC_OK;
 }
 
@@ -747,6 +754,7 @@ void launch_gemm1(occ_handle* h, int ngroups, cudaStream_t st, bool gathered, co
     }
     g.band = h->D >= 4096 ? (1 << 20) : 8;  // see launch_gemm2
     g.max_tiles = (int)h->max_mblk * (h->gated ? h->F / 128 : (h->F + 255) / 256);
+    g.sched = h->gsched.p + 2 * SCHED_GEMM1;
     launch_grouped_gemm(h->gated ? EPI_SWIGLU_BF16 : EPI_ACT_BF16, g, h->num_sms, st);
 }
 
@@ -768,6 +776,7 @@ void launch_gemm2(occ_handle* h, int ngroups, cudaStream_t st, const int* widx =
     g.ldo = h->D;
     g.act = OCC_ACT_IDENTITY;
     g.max_tiles = (int)h->max_mblk * ((h->D + 255) / 256);
+    g.sched = h->gsched.p + 2 * SCHED_GEMM2;
     launch_grouped_gemm(EPI_ACT_BF16, g, h->num_sms, st);
 }
 
@@ -814,6 +823,7 @@ occ_status run_shared(occ_handle* h, const __nv_bfloat16* x, int n, cudaStream_t
     g.ldo = Fs;
     g.act = h->cfg.activation;
     g.max_tiles = nmb * (h->gated ? Fs / 128 : (Fs + 255) / 256);
+    g.sched = h->gsched.p + 2 * SCHED_SHARED1;
     launch_grouped_gemm(h->gated ? EPI_SWIGLU_BF16 : EPI_ACT_BF16, g, h->num_sms, st);
     GemmArgs g2;
     g2.tmap_a = h->tmAS2.bytes;
@@ -830,6 +840,7 @@ occ_status run_shared(occ_handle* h, const __nv_bfloat16* x, int n, cudaStream_t
     g2.ldo = D;
     g2.act = OCC_ACT_IDENTITY;
     g2.max_tiles = nmb * ((D + 255) / 256);
+    g2.sched = h->gsched.p + 2 * SCHED_SHARED2;
     launch_grouped_gemm(EPI_ACT_BF16, g2, h->num_sms, st);
     return OCC_OK;
 }
@@ -1289,6 +1300,7 @@ occ_status occ_destroy(occ_handle* h) {
     for (auto* b : {&h->w13s, &h->w2s, &h->sgate, &h->hs, &h->ys}) b->release();
     h->sw.release();
     h->sh_grp.release();
+    h->gsched.release();
     if (h->s_aux) cudaStreamDestroy(h->s_aux);
     if (h->ev_fork) cudaEventDestroy(h->ev_fork);
     if (h->ev_join) cudaEventDestroy(h->ev_join);
@@ -2007,6 +2019,7 @@ static void bwd_gemms(occ_handle* h, int NG, const int* widx, float* g_w1, float
     g.gw_part = h->gw_part.p;
     g.band = D >= 4096 ? (1 << 20) : 8;  // band from K, as in the forward (-3% at OLMoE)
     g.max_tiles = (int)h->max_mblk * ((F + 255) / 256);
+    g.sched = h->gsched.p + 2 * SCHED_BWD0;
     launch_grouped_gemm(h->gated ? EPI_BWD_SWIGLU : EPI_BWD_ACT, g, h->num_sms, st);
     // scatter adjoint (data): g_x per Epd row = g_pre [w1 | w3]^T, fp32
     // accumulate, bf16 rows (the forward's product buffer is free by now)
@@ -2025,6 +2038,7 @@ static void bwd_gemms(occ_handle* h, int NG, const int* widx, float* g_w1, float
     d1.ldo = D;
     d1.act = OCC_ACT_IDENTITY;
     d1.max_tiles = (int)h->max_mblk * ((D + 255) / 256);
+    d1.sched = h->gsched.p + 2 * (SCHED_BWD0 + 1);
     launch_grouped_gemm(EPI_ACT_BF16, d1, h->num_sms, st);
     // merge adjoint (weights): g_w2[e] = mod_e^T g_y_e (backward.cpp:84-93)
     GemmArgs w2;
@@ -2040,6 +2054,7 @@ static void bwd_gemms(occ_handle* h, int NG, const int* widx, float* g_w1, float
     w2.ldo = D;
     w2.out_estride = (long)F * D;
     w2.max_tiles = NG * ((F + 255) / 256) * ((D + 255) / 256);
+    w2.sched = h->gsched.p + 2 * (SCHED_BWD0 + 2);
     launch_grouped_gemm(EPI_WGRAD, w2, h->num_sms, st);
     // scatter adjoint (weights): [g_w1 | g_w3][e] = x_e^T g_pre_e (backward.cpp:123-133)
     GemmArgs w1;
@@ -2057,6 +2072,7 @@ static void bwd_gemms(occ_handle* h, int NG, const int* widx, float* g_w1, float
     w1.ldo = F;
     w1.out_estride = (long)D * F;
     w1.max_tiles = NG * ((D + 255) / 256) * ((kw + 255) / 256);
+    w1.sched = h->gsched.p + 2 * (SCHED_BWD0 + 3);
     launch_grouped_gemm(EPI_WGRAD, w1, h->num_sms, st);
 }
 

@@ -99,9 +99,64 @@ struct Params {
     unsigned long long* dbg;  // OCC_GEMM_DEBUG: per-CTA stall cycles [cta][4]
     unsigned long long* tl;   // OCC_GEMM_TIMELINE: globaltimer per CTA at 8 points [cta][8]
     int tail_split;           // wide kernel: split the tail wave's super-tiles into halves
+    int hint;                 // L2 policies: 1 B loads evict_first, 2 C stores evict_first, 4 A loads evict_last
+    int* sched;               // dynamic tile scheduler [next tile, pairs done]; null = static cid + i * ncl
     const int* a_rows;   // non-null: A row q of the padded Epd layout is row a_rows[q] of tmA
                          // (tile::gather4, box 64 x 1; -1 = zero padding row)
 };
+
+// Tile scheduling.  Static: pair c runs tiles c, c + ncl, c + 2 ncl, ...
+// Dynamic (p.sched): the first tile is still c, every further one is taken
+// from a global counter in launch order, so the pairs that share an operand
+// (the 16 m-tiles of one B block, the n-blocks of one A m-tile) start it
+// within a fraction of a tile of each other however the pairs' speeds drift
+// over ~100 waves -- with the static walk they drift apart by more than the
+// ~80 MB the L2 holds between two reads (profiles/r02_gemm_l2.md).  The
+// leader's producer thread is the scheduler: it publishes each tile index
+// into a 4-deep ring in BOTH CTAs' shared memory (st.shared::cluster +
+// release arrive); the consumers (peer producer, MMA issuer, 16 epilogue
+// warps) hand slots back on the leader's `empty` barrier.  The last pair to
+// finish re-zeroes the counter for the next launch.
+constexpr int TQN = 4;
+constexpr int TQ_CONSUMERS = 2 + 2 * 8;  // peer producer + MMA issuer + epilogue warps of both CTAs
+struct TileQueue {
+    int* tile;        // [TQN] this CTA's copy of the published indices
+    uint64_t* full;   // [TQN] this CTA: index published
+    uint64_t* empty;  // [TQN] leader: slot consumed by every consumer
+    int cid, ncl;
+    bool dyn;
+    // i-th tile of this pair (every lane of a consuming warp calls it)
+    __device__ __forceinline__ int get(int i) const {
+        if (!dyn) return cid + i * ncl;
+        const int s = i % TQN;
+        mbar_wait_acq_cluster(&full[s], (i / TQN) & 1);
+        return ld_shared_s32(&tile[s]);
+    }
+    // one thread per consuming warp, after every lane's get(i)
+    __device__ __forceinline__ void release(int i, uint32_t rank) const {
+        if (!dyn) return;
+        const int s = i % TQN;
+        mbar_arrive_release_cluster(rank == 0 ? smem_u32(&empty[s]) : mapa_rank(&empty[s], 0));
+    }
+    // scheduler (leader producer thread): publish the i-th tile to both CTAs
+    __device__ __forceinline__ void publish(int i, int t) const {
+        const int s = i % TQN;
+        mbar_wait_acq_cluster(&empty[s], ((i / TQN) & 1) ^ 1);
+        tile[s] = t;
+        st_cluster_s32(mapa_rank(&tile[s], 1), t);
+        mbar_arrive_release_cluster(smem_u32(&full[s]));
+        mbar_arrive_release_cluster(mapa_rank(&full[s], 1));
+    }
+};
+// end of kernel (after the final cluster sync): the last pair re-zeroes the counter
+__device__ __forceinline__ void sched_done(int* sched, int ncl) {
+    __threadfence();
+    if (atomicAdd(sched + 1, 1) == ncl - 1) {
+        atomicExch(sched, 0);
+        atomicExch(sched + 1, 0);
+        __threadfence();
+    }
+}
 
 // Forward / data-gradient tiles: expert group by group, bands of `band`
 // m-tiles walked n-block-major (resident CTAs share B n-blocks, a band's A
@@ -264,6 +319,11 @@ __device__ __forceinline__ void tl_mark(const Params& p, int i) {
     p.tl[blockIdx.x * 16 + i] = t;
 }
 
+__device__ __forceinline__ void store_c(const CUtensorMap* tmC, const void* stg, int x, int y, int hint) {
+    if (hint & 2) tma_store_2d_hint(tmC, stg, x, y, l2_policy_evict_first());
+    else tma_store_2d(tmC, stg, x, y);
+}
+
 template <int EPI, bool WGRAD>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     grouped_gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -277,9 +337,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     uint64_t* empty = full + STAGES;
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* tq_full = tempty + 2;
+    uint64_t* tq_empty = tq_full + TQN;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tq_empty + TQN);
     __shared__ int s_gmb[MAX_GROUPS + 1];  // forward: m-tile prefix; wgrad: tile prefix
     __shared__ int s_gw[MAX_GROUPS];
+    __shared__ int s_tq[TQN];
     __shared__ int s_kb0[MAX_GROUPS];      // wgrad: first K block / K block count per group
     __shared__ int s_kbn[MAX_GROUPS];
 
@@ -300,6 +363,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
             mbar_init(&tempty[a], 2 * EPI_WARPS);  // leader: epilogue warps of both CTAs
+        }
+        for (int s = 0; s < TQN; ++s) {
+            mbar_init(&tq_full[s], 1);
+            mbar_init(&tq_empty[s], TQ_CONSUMERS);
         }
         fence_barrier_init();
     }
@@ -335,6 +402,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     const int KB_fwd = (p.K + BK - 1) / BK;
     const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
     const bool compact = num_tiles <= 2 * ncl;  // <= 2 tiles per CTA: rolled epilogue (see there)
+    const TileQueue tq{s_tq, tq_full, tq_empty, cid, ncl, p.sched != nullptr};
 
     if (warp == 0 && !WGRAD && p.a_rows) {
         // ------------------------------------------------ TMA producer, gathered A rows:
@@ -342,7 +410,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         // straight from the inbox / token rows: no Epd copy of the activations)
         int stage = 0;
         uint32_t phase = 0;
-        for (int tile = cid; tile < num_tiles; tile += ncl) {
+        int next = cid;
+        for (int i = 0;; ++i) {
+            int tile = 0;
+            if (tq.dyn && rank == 0) {
+                if (lane == 0) {
+                    tq.publish(i, next);
+                    tile = next;
+                    if (tile < num_tiles) next = ncl + atomicAdd(p.sched, 1);
+                }
+                tile = __shfl_sync(0xffffffffu, tile, 0);
+            } else {
+                tile = tq.get(i);
+                __syncwarp();
+                if (lane == 0) tq.release(i, rank);
+            }
+            if (tile >= num_tiles) break;
             int mb, nb, wi;
             tile_coords(tile, s_gmb, s_gw, p.ngroups, NB, p.band, mb, nb, wi);
             const int q0 = mb * 2 * BM + rank * BM;
@@ -366,7 +449,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int tile = cid; tile < num_tiles; tile += ncl) {
+            int next = cid;
+            for (int i = 0;; ++i) {
+                int tile;
+                if (tq.dyn && rank == 0) {
+                    tile = next;
+                    tq.publish(i, tile);
+                    if (tile < num_tiles) next = ncl + atomicAdd(p.sched, 1);
+                } else {
+                    tile = tq.get(i);
+                    tq.release(i, rank);
+                }
+                if (tile >= num_tiles) break;
                 int kb0 = 0, KB = KB_fwd, ax = 0, ay = 0, bx = 0, by = 0;
                 if constexpr (WGRAD) {
                     int g, mt, nt;
@@ -396,8 +490,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                         tma_load_2d_cg2(b_dst, &tmB, lbar, bx, k);
                         tma_load_2d_cg2(b_dst + B_BYTES / 2, &tmB, lbar, bx + 64, k);
                     } else {
-                        tma_load_2d_cg2(a_dst, &tmA, lbar, kb * BK, ay);
-                        tma_load_2d_cg2(b_dst, &tmB, lbar, kb * BK, by);
+                        if (p.hint & 4) tma_load_2d_cg2_hint(a_dst, &tmA, lbar, kb * BK, ay, l2_policy_evict_last());
+                        else tma_load_2d_cg2(a_dst, &tmA, lbar, kb * BK, ay);
+                        if (p.hint & 1) tma_load_2d_cg2_hint(b_dst, &tmB, lbar, kb * BK, by, l2_policy_evict_first());
+                        else tma_load_2d_cg2(b_dst, &tmB, lbar, kb * BK, by);
                     }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
@@ -411,7 +507,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             uint32_t phase = 0;
             int acc = 0;
             uint32_t acc_phase = 0;
-            for (int tile = cid; tile < num_tiles; tile += ncl) {
+            for (int i = 0;; ++i) {
+                const int tile = tq.get(i);
+                __syncwarp();
+                if (lane == 0) tq.release(i, rank);
+                if (tile >= num_tiles) break;
                 int KB = KB_fwd;
                 if constexpr (WGRAD) {
                     int g, mt, nt;
@@ -454,7 +554,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         uint32_t stg_n = 0;      // TMA-store staging buffer counter
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int tile = cid; tile < num_tiles; tile += ncl) {
+        for (int i = 0;; ++i) {
+            const int tile = tq.get(i);
+            __syncwarp();
+            if (lane == 0) tq.release(i, rank);
+            if (tile >= num_tiles) break;
             // backward epilogue inputs (pre-activations) of this tile's first
             // chunk are fetched before waiting for the accumulator, so their
             // latency hides under the tile's MMAs
@@ -637,7 +741,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                             __syncwarp();
                             if (tlm && cc < 2) tl_mark(p, 13 + 2 * cc);  // fenced (13, 15)
                             if (lane == 0) {
-                                tma_store_2d(&tmC, stg, col0, (int)(row - lane));
+                                store_c(&tmC, stg, col0, (int)(row - lane), p.hint);
                                 bulk_commit();
                             }
                             if (tlm && cc == 0) tl_mark(p, 9);  // first store issued
@@ -724,7 +828,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                                 fence_proxy_async();
                                 __syncwarp();
                                 if (lane == 0) {
-                                    tma_store_2d(&tmC, stg, col0, (int)(row - lane));
+                                    store_c(&tmC, stg, col0, (int)(row - lane), p.hint);
                                     bulk_commit();
                                 }
                                 if (warp == 2 && lane == 0 && tile == cid && cc == 0) tl_mark(p, 7);  // first store
@@ -755,6 +859,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         tc_fence_after();
         tmem_dealloc_cg2<512>(tmem_base);
     }
+    if (tq.dyn && rank == 0 && threadIdx.x == 0) sched_done(p.sched, ncl);
 }
 
 // ---------------------------------------------------------------------------
@@ -830,9 +935,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     uint64_t* empty = full + W_STAGES;
     uint64_t* tfull = empty + W_STAGES;
     uint64_t* tempty = tfull + 1;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+    uint64_t* tq_full = tempty + 1;
+    uint64_t* tq_empty = tq_full + TQN;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tq_empty + TQN);
     __shared__ int s_gmb[MAX_GROUPS + 1];
     __shared__ int s_gw[MAX_GROUPS];
+    __shared__ int s_tq[TQN];
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
@@ -849,6 +957,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         }
         mbar_init(&tfull[0], 1);
         mbar_init(&tempty[0], 2 * EPI_WARPS);
+        for (int s = 0; s < TQN; ++s) {
+            mbar_init(&tq_full[s], 1);
+            mbar_init(&tq_empty[s], TQ_CONSUMERS);
+        }
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc_cg2<512>(tmem_slot);
@@ -867,12 +979,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     // tail super-tiles issued as halves (odd block counts end in single-block tiles already)
     const int split = p.tail_split && !(NB & 1) && 2 * tail <= ncl ? tail : 0;
     const int num_tiles = S + split;
+    const TileQueue tq{s_tq, tq_full, tq_empty, cid, ncl, p.sched != nullptr};
 
     if (warp == 0) {
         if (lane == 0) {  // -------------------------------------------- TMA producer
+            const uint64_t pol_b = l2_policy_evict_first(), pol_a = l2_policy_evict_last();
             int stage = 0;
             uint32_t phase = 0;
-            for (int tile = cid; tile < num_tiles; tile += ncl) {
+            int next = cid;  // scheduler: the tile index taken for this pair's next tile
+            for (int i = 0;; ++i) {
+                int tile;
+                if (tq.dyn && rank == 0) {
+                    tile = next;
+                    tq.publish(i, tile);
+                    if (tile < num_tiles) next = ncl + atomicAdd(p.sched, 1);  // used next iteration
+                } else {
+                    tile = tq.get(i);
+                    tq.release(i, rank);
+                }
+                if (tile >= num_tiles) break;
                 const WTile wt = wide_decode(tile, S, split, s_gmb, s_gw, p.ngroups, NBW, NB, p.band);
                 if (!wt.valid) continue;
                 const int ay = wt.mb * 2 * BM + rank * BM;
@@ -885,9 +1010,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                     const uint32_t lbar = smem_u32(&full[stage]) & kPeerBitMask;
                     if (rank == 0) mbar_arrive_expect_tx(&full[stage], 2 * (A_BYTES + (two ? W_B2 : B_BYTES)));
                     uint8_t* b_dst = sB + stage * W_B2;
-                    tma_load_2d_cg2(sA + stage * A_BYTES, &tmA, lbar, kb * BK, ay);
-                    tma_load_2d_cg2(b_dst, &tmB, lbar, kb * BK, by0);
-                    if (two) tma_load_2d_cg2(b_dst + B_BYTES, &tmB, lbar, kb * BK, by0 + BN);
+                    if (p.hint & 4) tma_load_2d_cg2_hint(sA + stage * A_BYTES, &tmA, lbar, kb * BK, ay, pol_a);
+                    else tma_load_2d_cg2(sA + stage * A_BYTES, &tmA, lbar, kb * BK, ay);
+                    if (p.hint & 1) {
+                        tma_load_2d_cg2_hint(b_dst, &tmB, lbar, kb * BK, by0, pol_b);
+                        if (two) tma_load_2d_cg2_hint(b_dst + B_BYTES, &tmB, lbar, kb * BK, by0 + BN, pol_b);
+                    } else {
+                        tma_load_2d_cg2(b_dst, &tmB, lbar, kb * BK, by0);
+                        if (two) tma_load_2d_cg2(b_dst + B_BYTES, &tmB, lbar, kb * BK, by0 + BN);
+                    }
                     if (++stage == W_STAGES) { stage = 0; phase ^= 1; }
                 }
             }
@@ -897,7 +1028,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             constexpr uint32_t IDESC = idesc_bf16_f32(2 * BM, BN);
             int stage = 0;
             uint32_t phase = 0, acc_phase = 0;
-            for (int tile = cid; tile < num_tiles; tile += ncl) {
+            for (int i = 0;; ++i) {
+                const int tile = tq.get(i);
+                __syncwarp();
+                if (lane == 0) tq.release(i, rank);
+                if (tile >= num_tiles) break;
                 const WTile wt = wide_decode(tile, S, split, s_gmb, s_gw, p.ngroups, NBW, NB, p.band);
                 if (!wt.valid) continue;
                 const bool two = wt.two;
@@ -938,7 +1073,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         uint32_t acc_phase = 0;
         constexpr int NCH = SW ? 4 : BN / 32;  // output chunks of 32 columns per accumulator
         constexpr int HALF = NCH / 2;          // chunks per drain round (128 registers)
-        for (int tile = cid; tile < num_tiles; tile += ncl) {
+        for (int i = 0;; ++i) {
+            const int tile = tq.get(i);
+            __syncwarp();
+            if (lane == 0) tq.release(i, rank);
+            if (tile >= num_tiles) break;
             const WTile wt = wide_decode(tile, S, split, s_gmb, s_gw, p.ngroups, NBW, NB, p.band);
             if (!wt.valid) continue;
             const int mb = wt.mb;
@@ -1017,7 +1156,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                     fence_proxy_async();
                     __syncwarp();
                     if (lane == 0) {
-                        tma_store_2d(&tmC, stg, col0, (int)(row - lane));
+                        store_c(&tmC, stg, col0, (int)(row - lane), p.hint);
                         bulk_commit();
                     }
                 }
@@ -1082,7 +1221,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                         fence_proxy_async();
                         __syncwarp();
                         if (lane == 0) {
-                            tma_store_2d(&tmC, stg, col0, (int)(row - lane));
+                            store_c(&tmC, stg, col0, (int)(row - lane), p.hint);
                             bulk_commit();
                         }
                     } else {
@@ -1100,6 +1239,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         tc_fence_after();
         tmem_dealloc_cg2<512>(tmem_base);
     }
+    if (tq.dyn && rank == 0 && threadIdx.x == 0) sched_done(p.sched, ncl);
 }
 
 // Weight-gradient GEMMs with the same 256 x 512 super-tiles: per expert
@@ -1117,11 +1257,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     uint64_t* empty = full + W_STAGES;
     uint64_t* tfull = empty + W_STAGES;
     uint64_t* tempty = tfull + 1;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+    uint64_t* tq_full = tempty + 1;
+    uint64_t* tq_empty = tq_full + TQN;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tq_empty + TQN);
     __shared__ int s_tb[MAX_GROUPS + 1];  // super-tile prefix per group
     __shared__ int s_gw[MAX_GROUPS];
     __shared__ int s_kb0[MAX_GROUPS];
     __shared__ int s_kbn[MAX_GROUPS];
+    __shared__ int s_tq[TQN];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_ctarank();
     const int NBW = (p.N + 2 * BN - 1) / (2 * BN);
@@ -1136,6 +1279,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         }
         mbar_init(&tfull[0], 1);
         mbar_init(&tempty[0], 2 * EPI_WARPS);
+        for (int s = 0; s < TQN; ++s) {
+            mbar_init(&tq_full[s], 1);
+            mbar_init(&tq_empty[s], TQ_CONSUMERS);
+        }
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc_cg2<512>(tmem_slot);
@@ -1159,12 +1306,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     __syncthreads();
     const int num_tiles = s_tb[p.ngroups];
     const int cid = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+    const TileQueue tq{s_tq, tq_full, tq_empty, cid, ncl, p.sched != nullptr};
 
     if (warp == 0) {
         if (lane == 0) {  // -------------------------------------------- TMA producer
             int stage = 0;
             uint32_t phase = 0;
-            for (int tile = cid; tile < num_tiles; tile += ncl) {
+            int next = cid;
+            for (int i = 0;; ++i) {
+                int tile;
+                if (tq.dyn && rank == 0) {
+                    tile = next;
+                    tq.publish(i, tile);
+                    if (tile < num_tiles) next = ncl + atomicAdd(p.sched, 1);
+                } else {
+                    tile = tq.get(i);
+                    tq.release(i, rank);
+                }
+                if (tile >= num_tiles) break;
                 int g, mt, ntw;
                 wtile_coords(tile, s_tb, p.ngroups, NBW, g, mt, ntw);
                 const int ax = mt * 2 * BM + rank * BM;
@@ -1191,7 +1350,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
             constexpr uint32_t IDESC = idesc_mn(2 * BM, BN);
             int stage = 0;
             uint32_t phase = 0, acc_phase = 0;
-            for (int tile = cid; tile < num_tiles; tile += ncl) {
+            for (int i = 0;; ++i) {
+                const int tile = tq.get(i);
+                __syncwarp();
+                if (lane == 0) tq.release(i, rank);
+                if (tile >= num_tiles) break;
                 int g, mt, ntw;
                 wtile_coords(tile, s_tb, p.ngroups, NBW, g, mt, ntw);
                 mbar_wait(&tempty[0], acc_phase ^ 1);
@@ -1222,7 +1385,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     } else {  // ------------------------------------------------------------ epilogue
         const int q = warp & 3, t = (warp - 2) >> 2;
         uint32_t acc_phase = 0;
-        for (int tile = cid; tile < num_tiles; tile += ncl) {
+        for (int i = 0;; ++i) {
+            const int tile = tq.get(i);
+            __syncwarp();
+            if (lane == 0) tq.release(i, rank);
+            if (tile >= num_tiles) break;
             int g, mt, ntw;
             wtile_coords(tile, s_tb, p.ngroups, NBW, g, mt, ntw);
             mbar_wait(&tfull[0], acc_phase);
@@ -1269,6 +1436,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
         tc_fence_after();
         tmem_dealloc_cg2<512>(tmem_base);
     }
+    if (tq.dyn && rank == 0 && threadIdx.x == 0) sched_done(p.sched, ncl);
 }
 
 template <int EPI>
@@ -1315,10 +1483,17 @@ bool make_tmap_2d(void* tmap, const void* base, uint64_t inner, uint64_t outer, 
     cuuint64_t strides[1] = {(pitch_elems ? pitch_elems : inner) * 2};
     cuuint32_t box[2] = {box_inner, box_outer};
     cuuint32_t estr[2] = {1, 1};
+    static const int promo_env = [] {  // L2 promotion experiments (profiles/), not a product knob
+        const char* e = getenv("OCC_TMAP_PROMO");
+        return e ? atoi(e) : 3;
+    }();
+    static const CUtensorMapL2promotion promos[4] = {CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_64B,
+                                                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B};
     return enc(reinterpret_cast<CUtensorMap*>(tmap), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base),
                dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
-               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+               promos[promo_env & 3], CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 void launch_grouped_gemm(EpiMode mode, const GemmArgs& a, int num_sms, cudaStream_t st) {
@@ -1389,6 +1564,10 @@ void launch_grouped_gemm(EpiMode mode, const GemmArgs& a, int num_sms, cudaStrea
     static const int wide_env = getenv("OCC_GEMM_WIDE") ? atoi(getenv("OCC_GEMM_WIDE")) : 1;
     static const int tail_env = getenv("OCC_GEMM_TAILSPLIT") ? atoi(getenv("OCC_GEMM_TAILSPLIT")) : 1;
     p.tail_split = tail_env;
+    static const int hint_env = getenv("OCC_GEMM_HINT") ? atoi(getenv("OCC_GEMM_HINT")) : 0;
+    p.hint = hint_env;
+    static const int dyn_env = getenv("OCC_GEMM_DYN") ? atoi(getenv("OCC_GEMM_DYN")) : 1;
+    p.sched = dyn_env ? a.sched : nullptr;
     bool wide = false;
     if ((mode == EPI_ACT_BF16 || mode == EPI_SWIGLU_BF16) && !a.a_rows) {
         const int nbk = mode == EPI_SWIGLU_BF16 ? (a.N + 127) / 128 : (a.N + BN - 1) / BN;

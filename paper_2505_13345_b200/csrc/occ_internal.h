@@ -361,7 +361,10 @@ struct GemmArgs {
     const __nv_bfloat16* pre_b = nullptr;
     float* gw_part = nullptr;      // backward: routing-weight gradient partial per (row, n-tile)
     int max_tiles = 0;             // static upper bound (grid sizing)
+    int* sched = nullptr;          // dynamic tile scheduler slot (2 zeroed ints; null = static schedule)
 };
+// Scheduler slots per handle (launch sites that can run concurrently get their own).
+enum SchedSlot { SCHED_GEMM1 = 0, SCHED_GEMM2, SCHED_SHARED1, SCHED_SHARED2, SCHED_BWD0, kSchedSlots = 16 };
 void launch_grouped_gemm(EpiMode mode, const GemmArgs& a, int num_sms, cudaStream_t st);
 bool make_tmap_2d(void* tmap, const void* base, uint64_t inner, uint64_t outer, uint32_t box_inner,
                   uint32_t box_outer, int swizzle_bytes = 128, uint64_t pitch_elems = 0);
