@@ -15,7 +15,7 @@ def main(path, skip=0):
         if len(r) <= vi:
             continue
         v = float(r[vi].replace(",", ""))
-        v *= {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(r[ui], 1.0)
+        v *= {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(r[ui], 1.0)
         k = r[ki].split("(")[0].replace("(anonymous namespace)::", "").replace("occ::", "")
         a = agg.setdefault(k, [0, 0.0])
         a[0] += 1
