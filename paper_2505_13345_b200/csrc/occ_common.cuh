@@ -157,6 +157,33 @@ OCC_DEV uint32_t mapa_rank(const void* p, uint32_t rank) {
 OCC_DEV void st_cluster_s32(uint32_t addr, int v) {
     asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
 }
+// Asynchronous store into a cluster CTA's shared memory that completes 4
+// bytes of the transaction count of that CTA's barrier `bar_cluster`: the
+// waiter sees the value once the phase completes (as with a TMA load).
+OCC_DEV void st_async_s32(uint32_t addr, int v, uint32_t bar_cluster) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.s32 [%0], %1, [%2];" ::"r"(addr), "r"(v),
+                 "r"(bar_cluster)
+                 : "memory");
+}
+OCC_DEV void mbar_arrive_expect_tx_cluster(uint32_t bar_cluster, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cluster.b64 _, [%0], %1;" ::"r"(bar_cluster), "r"(bytes)
+                 : "memory");
+}
+// 16-byte shared-memory accesses through the shared window (LDS/STS): a
+// pointer derived from the realigned dynamic smem base loses its address
+// space and would otherwise compile to generic LD/ST (ncu: the backward
+// epilogue's transposes stalled on long-scoreboard generic loads).
+OCC_DEV void sts128(const void* p, uint4 v) {
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(smem_u32(p)), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+OCC_DEV uint4 lds128(const void* p) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(smem_u32(p))
+                 : "memory");
+    return v;
+}
 OCC_DEV int ld_shared_s32(const int* p) {
     int v;
     asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");

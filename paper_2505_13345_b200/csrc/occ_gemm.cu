@@ -113,10 +113,12 @@ struct Params {
 // over ~100 waves -- with the static walk they drift apart by more than the
 // ~80 MB the L2 holds between two reads (profiles/r02_gemm_l2.md).  The
 // leader's producer thread is the scheduler: it publishes each tile index
-// into a 4-deep ring in BOTH CTAs' shared memory (st.shared::cluster +
-// release arrive); the consumers (peer producer, MMA issuer, 16 epilogue
-// warps) hand slots back on the leader's `empty` barrier.  The last pair to
-// finish re-zeroes the counter for the next launch.
+// into a 4-deep ring in both CTAs' shared memory -- locally a store + arrive,
+// into the peer with st.async completing the transaction count of the peer's
+// barrier (the TMA-load contract: no cluster-scope fence, which cost a GPU
+// membar per consumer warp per tile); the consumers (peer producer, MMA
+// issuer, 16 epilogue warps) hand slots back on the leader's `empty`
+// barrier.  The last pair to finish re-zeroes the counter for the next launch.
 constexpr int TQN = 4;
 constexpr int TQ_CONSUMERS = 2 + 2 * 8;  // peer producer + MMA issuer + epilogue warps of both CTAs
 struct TileQueue {
@@ -129,23 +131,26 @@ struct TileQueue {
     __device__ __forceinline__ int get(int i) const {
         if (!dyn) return cid + i * ncl;
         const int s = i % TQN;
-        mbar_wait_acq_cluster(&full[s], (i / TQN) & 1);
+        mbar_wait(&full[s], (i / TQN) & 1);
         return ld_shared_s32(&tile[s]);
     }
-    // one thread per consuming warp, after every lane's get(i)
+    // one thread per consuming warp, after every lane's get(i) (the index is
+    // in registers: the slot may be rewritten)
     __device__ __forceinline__ void release(int i, uint32_t rank) const {
         if (!dyn) return;
         const int s = i % TQN;
-        mbar_arrive_release_cluster(rank == 0 ? smem_u32(&empty[s]) : mapa_rank(&empty[s], 0));
+        if (rank == 0) mbar_arrive(&empty[s]);
+        else mbar_arrive_cluster(mapa_rank(&empty[s], 0));
     }
     // scheduler (leader producer thread): publish the i-th tile to both CTAs
     __device__ __forceinline__ void publish(int i, int t) const {
         const int s = i % TQN;
-        mbar_wait_acq_cluster(&empty[s], ((i / TQN) & 1) ^ 1);
+        mbar_wait(&empty[s], ((i / TQN) & 1) ^ 1);
         tile[s] = t;
-        st_cluster_s32(mapa_rank(&tile[s], 1), t);
-        mbar_arrive_release_cluster(smem_u32(&full[s]));
-        mbar_arrive_release_cluster(mapa_rank(&full[s], 1));
+        mbar_arrive(&full[s]);
+        const uint32_t rbar = mapa_rank(&full[s], 1);
+        mbar_arrive_expect_tx_cluster(rbar, 4);
+        st_async_s32(mapa_rank(&tile[s], 1), t, rbar);
     }
 };
 // end of kernel (after the final cluster sync): the last pair re-zeroes the counter
@@ -276,10 +281,10 @@ __device__ __forceinline__ void load_block_coalesced(const __nv_bfloat16* base, 
 // coalesced registers -> this lane's row (4 x 16 B)
 __device__ __forceinline__ void block_to_row(uint8_t* stg, const uint4 (&R)[4], int lane, uint4 (&row)[4]) {
 #pragma unroll
-    for (int u = 0; u < 4; ++u) *reinterpret_cast<uint4*>(stg + stg_off(u * 8 + (lane >> 2), lane & 3)) = R[u];
+    for (int u = 0; u < 4; ++u) sts128(stg + stg_off(u * 8 + (lane >> 2), lane & 3), R[u]);
     __syncwarp();
 #pragma unroll
-    for (int c = 0; c < 4; ++c) row[c] = *reinterpret_cast<const uint4*>(stg + stg_off(lane, c));
+    for (int c = 0; c < 4; ++c) row[c] = lds128(stg + stg_off(lane, c));
     __syncwarp();
 }
 // this lane's row (32 floats -> bf16) -> coalesced global stores
@@ -292,7 +297,7 @@ __device__ __forceinline__ void row_to_global(uint8_t* stg, const float (&h)[32]
         o.y = pack_bf16(h[8 * c + 2], h[8 * c + 3]);
         o.z = pack_bf16(h[8 * c + 4], h[8 * c + 5]);
         o.w = pack_bf16(h[8 * c + 6], h[8 * c + 7]);
-        *reinterpret_cast<uint4*>(stg + stg_off(lane, c)) = o;
+        sts128(stg + stg_off(lane, c), o);
     }
     __syncwarp();
     const int c = lane & 3;
@@ -300,7 +305,7 @@ __device__ __forceinline__ void row_to_global(uint8_t* stg, const float (&h)[32]
     for (int u = 0; u < 4; ++u)
         if (c * 8 < ncols)
             reinterpret_cast<uint4*>(base + (long)(u * 8 + (lane >> 2)) * ld)[c] =
-                *reinterpret_cast<const uint4*>(stg + stg_off(u * 8 + (lane >> 2), c));
+                lds128(stg + stg_off(u * 8 + (lane >> 2), c));
     __syncwarp();
 }
 // pre-activation block(s) of one chunk: rows rowbase..+31, columns col0..+31
@@ -734,7 +739,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                                 o.y = pack_bf16(h[8 * u + 2], h[8 * u + 3]);
                                 o.z = pack_bf16(h[8 * u + 4], h[8 * u + 5]);
                                 o.w = pack_bf16(h[8 * u + 6], h[8 * u + 7]);
-                                *reinterpret_cast<uint4*>(stg + lane * 64 + ((u ^ ((lane >> 1) & 3)) << 4)) = o;
+                                sts128(stg + lane * 64 + ((u ^ ((lane >> 1) & 3)) << 4), o);
                             }
                             if (tlm && cc < 2) tl_mark(p, 12 + 2 * cc);  // staged (12, 14)
                             fence_proxy_async();
@@ -823,7 +828,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                                     o.y = pack_bf16(h[8 * u + 2], h[8 * u + 3]);
                                     o.z = pack_bf16(h[8 * u + 4], h[8 * u + 5]);
                                     o.w = pack_bf16(h[8 * u + 6], h[8 * u + 7]);
-                                    *reinterpret_cast<uint4*>(stg + lane * 64 + ((u ^ ((lane >> 1) & 3)) << 4)) = o;
+                                    sts128(stg + lane * 64 + ((u ^ ((lane >> 1) & 3)) << 4), o);
                                 }
                                 fence_proxy_async();
                                 __syncwarp();
@@ -1151,8 +1156,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                     __syncwarp();
 #pragma unroll
                     for (int u = 0; u < 4; ++u)
-                        *reinterpret_cast<uint4*>(stg + lane * 64 + ((u ^ ((lane >> 1) & 3)) << 4)) =
-                            make_uint4(pk[c][4 * u], pk[c][4 * u + 1], pk[c][4 * u + 2], pk[c][4 * u + 3]);
+                        sts128(stg + lane * 64 + ((u ^ ((lane >> 1) & 3)) << 4),
+                               make_uint4(pk[c][4 * u], pk[c][4 * u + 1], pk[c][4 * u + 2], pk[c][4 * u + 3]));
                     fence_proxy_async();
                     __syncwarp();
                     if (lane == 0) {
@@ -1216,7 +1221,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                             o.y = pack_bf16(h[8 * u + 2], h[8 * u + 3]);
                             o.z = pack_bf16(h[8 * u + 4], h[8 * u + 5]);
                             o.w = pack_bf16(h[8 * u + 6], h[8 * u + 7]);
-                            *reinterpret_cast<uint4*>(stg + lane * 64 + ((u ^ ((lane >> 1) & 3)) << 4)) = o;
+                            sts128(stg + lane * 64 + ((u ^ ((lane >> 1) & 3)) << 4), o);
                         }
                         fence_proxy_async();
                         __syncwarp();
