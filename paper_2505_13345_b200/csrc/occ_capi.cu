@@ -2396,11 +2396,28 @@ occ_status occ_comm_init_loopback(occ_handle* h, long group_key) {
     return OCC_OK;
 }
 
+// CUDA 12 loads kernels lazily by default (CUDA_MODULE_LOADING); a first
+// launch then synchronises with the kernels running in the context.
+static bool lazy_module_loading() {
+    typedef CUresult (*GetModeFn)(CUmoduleLoadingMode*);
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuModuleGetLoadingMode", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !fn)
+        return false;
+    CUmoduleLoadingMode mode = CU_MODULE_EAGER_LOADING;
+    return reinterpret_cast<GetModeFn>(fn)(&mode) == CUDA_SUCCESS && mode == CU_MODULE_LAZY_LOADING;
+}
+
 occ_status occ_comm_enable_peer(occ_handle* h, int max_tokens_per_rank) {
     if (!h) return fail(OCC_ERR_ARG, "null handle");
     if (h->world == 1) return OCC_OK;
     if (!h->tp) return fail(OCC_ERR_STATE, "peer exchange: call occ_comm_init / occ_comm_init_loopback first");
     if (max_tokens_per_rank < 1) return fail(OCC_ERR_CONFIG, "peer exchange: max_tokens_per_rank must be >= 1");
+    if (std::string(h->tp->name()) == "loopback" && lazy_module_loading())
+        return fail(OCC_ERR_STATE,
+                    "peer exchange between ranks of one process needs CUDA_MODULE_LOADING=EAGER (set before CUDA "
+                    "starts): a lazily loaded kernel's first launch waits for the other ranks' spinning arrival waits");
     const int nd = h->nd, k = h->k, P = h->P;
     const size_t per_dev = h->cfg.dedup ? 1 : (size_t)std::min(k, P);   // rows per (token, device)
     const size_t R_cap = (size_t)max_tokens_per_rank * nd * per_dev;

@@ -184,6 +184,7 @@ OCC_DEV uint4 lds128(const void* p) {
                  : "memory");
     return v;
 }
+OCC_DEV void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
 OCC_DEV int ld_shared_s32(const int* p) {
     int v;
     asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");

@@ -572,7 +572,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 int mb0, nb0, wi0;
                 tile_coords(tile, s_gmb, s_gw, p.ngroups, NB, p.band, mb0, nb0, wi0);
                 const long rowbase0 = (long)mb0 * 2 * BM + rank * BM + q * 32;
-                load_pre_chunk<EPI>(p, rowbase0, nb0 * BN + hsel * (BN / 64) * 32, lane, pa_cur, pb_cur);
+                const int colh = nb0 * BN + hsel * (BN / 64) * 32;
+                load_pre_chunk<EPI>(p, rowbase0, colh, lane, pa_cur, pb_cur);
+                // the later chunks' inputs into L2 now (one register-free prefetch per
+                // 128-byte line of this lane's row): their loads, one chunk ahead of
+                // the math, then hit L2 instead of waiting on DRAM (ncu: the
+                // transposes' staging stores stalled on those loads)
+#ifndef OCC_NO_BWD_PF
+                if (colh < p.N) {
+                    const __nv_bfloat16* ra = p.pre_a + (rowbase0 + lane) * p.N + colh;
+                    const __nv_bfloat16* rb = EPI == EPI_BWD_SWIGLU ? p.pre_b + (rowbase0 + lane) * p.N + colh : nullptr;
+#pragma unroll
+                    for (int l = 0; l < (BN / 2) * 2 / 128; ++l)
+                        if (colh + l * 64 < p.N) {
+                            prefetch_l2(ra + l * 64);
+                            if (rb) prefetch_l2(rb + l * 64);
+                        }
+                }
+#endif
             }
             { const long long t0 = p.dbg ? clock64() : 0;
             mbar_wait(&tfull[acc], acc_phase);

@@ -3,6 +3,7 @@
 // index (BRIM1), gather, intra-device partial combine, combine, the
 // co-activation histogram and the routers.  Citations are to
 // /root/reference/proj/<file>:<line>.
+#include <cstdio>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -1018,6 +1019,8 @@ __global__ void peer_wait_kernel(const unsigned long long* flags, int nd, int ba
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
         if ((long long)(t1 - t0) > timeout_ns) {
             atomicExch(err, 7);
+            printf("occ peer wait: timeout on flag slot %d (phase base %d): saw %llu, want %llu\n", base + s, base, v,
+                   seq);
             break;
         }
         __nanosleep(256);

@@ -13,6 +13,8 @@ around whole forwards).  Under ncu, which serialises the ranks' kernels, run
 after 0.2 s (the forward's values are garbage, the kernels' traffic is real)."""
 import os
 import sys
+
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")  # peer mode between threads (tests/conftest.py)
 import threading
 
 import numpy as np

@@ -12,6 +12,14 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 # CUDA context exists).  One process per GPU -- the product setting -- uses
 # two or three streams and is unaffected.
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+# ...and every kernel loaded when the context is created: with lazy loading
+# (the CUDA 12 default) the first launch of a kernel waits for the kernels
+# already running in the context, so one rank's first launch of, say, the
+# arrival-signal kernel stalls behind another rank's spinning arrival wait
+# until the wait times out (threads in one process only; separate processes
+# have separate contexts).  The library refuses peer mode between ranks of one
+# process under lazy loading (occ_comm_enable_peer).
+os.environ.setdefault("CUDA_MODULE_LOADING", "EAGER")
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 

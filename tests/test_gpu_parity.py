@@ -760,6 +760,25 @@ def test_multi_rank_forward_loopback(nd, ne, k, act, dedup, shared, peer, mb):
         assert r0.per_device_token_counts == [rep.per_device_rows[d] for d in range(nd)]
 
 
+def test_loopback_peer_refused_under_lazy_loading():
+    """Ranks as threads of one process share one context: with lazy kernel
+    loading a rank's first launch of a kernel waits for another rank's
+    spinning arrival wait, so the loopback peer exchange would stall until
+    the wait's timeout.  occ_comm_enable_peer refuses it with a StateError
+    that names CUDA_MODULE_LOADING=EAGER (checked in a fresh process)."""
+    import os
+    import subprocess
+    import sys
+    code = ("import paper_2505_13345_b200 as occ\n"
+            "l = occ.ExpertParallelLayer(occ.MoEConfig(8, 2, 2, 128, 256), world_size=2, rank=0)\n"
+            "l.comm_init_loopback(12345)\n"
+            "try:\n    l.comm_enable_peer(16)\nexcept occ.StateError as e:\n    print('REFUSED', e)\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CUDA_MODULE_LOADING="LAZY")
+    out = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=300)
+    assert "REFUSED" in out.stdout and "CUDA_MODULE_LOADING=EAGER" in out.stdout, out.stdout + out.stderr
+
+
 # ------------------------------------------------------------------ backward --
 
 @pytest.mark.parametrize("nd,ne,k,act,dedup,peer", [(2, 8, 2, "silu", True, False), (4, 16, 4, "relu", True, False),
