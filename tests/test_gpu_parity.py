@@ -1139,6 +1139,26 @@ def test_wide_tile_forced_odd_blocks():
         assert float(l.split(" err ")[1].split()[0]) <= 1e-2, l
 
 
+def test_dynamic_tile_schedule_bit_identical():
+    """The dynamic tile scheduler (launch-order tile counter) only changes
+    which CTA pair runs a tile, never a tile's math: forward, shared-expert
+    and backward outputs of wide / narrow / weight-gradient GEMMs over many
+    waves are bit-identical to the static walk (OCC_GEMM_DYN=0), each in a
+    fresh process (the switch is read once)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    dig = []
+    for dyn in ("0", "1"):
+        r = subprocess.run([sys.executable, os.path.join(root, "profiles", "probes", "sched_digest.py")],
+                           env=dict(os.environ, OCC_GEMM_DYN=dyn), capture_output=True, text=True, timeout=600,
+                           cwd=root)
+        assert r.returncode == 0, r.stderr[-2000:]
+        dig.append([l for l in r.stdout.splitlines() if l.startswith("digest")][0].split()[1])
+    assert dig[0] == dig[1], dig
+
+
 @pytest.mark.parametrize("ne,k,nd", [(256, 8, 4), (200, 64, 4), (130, 3, 5)])
 def test_wide_gate_router_matches_oracle_topk(ne, k, nd):
     """Gates wider than 128 experts take the logits + router_select path:
