@@ -620,6 +620,9 @@ occ_status upload_tables(occ_handle* h) {
 // == 1: R is the static dedup bound n * min(k, N_d) (n * k for the naive
 // path) and n_epd = n * k exactly; world_size > 1: R is the exact received
 // row count (known after the count exchange) and n_epd <= R * min(k, P).
+// Columns of the saved pre-activations: whole 32-column tiles (occ_gemm.cu).
+inline size_t pre_cols(int F) { return (size_t)(F + 31) / 32 * 32; }
+
 occ_status ensure_recv(occ_handle* h, size_t R, size_t epd_bound) {
     const int k = h->k, P = h->P, D = h->D, F = h->F;
     const int G = h->world == 1 ? h->nd : 1;
@@ -645,8 +648,8 @@ occ_status ensure_recv(occ_handle* h, size_t R, size_t epd_bound) {
             return fail(OCC_ERR_CUDA, "cuTensorMapEncodeTiled failed (inbox rows)");
     }
     if (h->training) {
-        CUDA_TRY(h->save_a.ensure(std::max(Q, h->Q_max) * F));
-        if (h->gated) CUDA_TRY(h->save_b.ensure(std::max(Q, h->Q_max) * F));
+        CUDA_TRY(h->save_a.ensure(std::max(Q, h->Q_max) * pre_cols(F)));
+        if (h->gated) CUDA_TRY(h->save_b.ensure(std::max(Q, h->Q_max) * pre_cols(F)));
     }
     if (Q > h->Q_max || !h->x_epd.p) {
         CUDA_TRY(h->epd_src.ensure(Q));
@@ -1169,8 +1172,8 @@ occ_status occ_expert_compute(occ_handle* h, int device, const void* in_x, const
     const size_t R = (size_t)std::max(rows, 1);
     if ((s = ensure_recv(h, R, R * std::min(h->k, h->P))) != OCC_OK) return s;
     if (h->training) {
-        CUDA_TRY(h->save_a.ensure(h->Q_max * h->F));
-        if (h->gated) CUDA_TRY(h->save_b.ensure(h->Q_max * h->F));
+        CUDA_TRY(h->save_a.ensure(h->Q_max * pre_cols(h->F)));
+        if (h->gated) CUDA_TRY(h->save_b.ensure(h->Q_max * pre_cols(h->F)));
     }
     h->have_train_state = false;
     if (rows == 0) return OCC_OK;
@@ -1812,8 +1815,8 @@ static occ_status forward_one(occ_handle* h, const void* x, const int32_t* ids, 
     occ_status s = ensure_ws(h, n);
     if (s != OCC_OK) return s;
     if (h->training) {
-        CUDA_TRY(h->save_a.ensure(h->Q_max * h->F));
-        if (h->gated) CUDA_TRY(h->save_b.ensure(h->Q_max * h->F));
+        CUDA_TRY(h->save_a.ensure(h->Q_max * pre_cols(h->F)));
+        if (h->gated) CUDA_TRY(h->save_b.ensure(h->Q_max * pre_cols(h->F)));
     }
     h->last_n = n;
     h->have_forward = true;

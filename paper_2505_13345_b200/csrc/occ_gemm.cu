@@ -262,31 +262,14 @@ __device__ __forceinline__ void unpack_bf16x32(const uint4 (&w)[4], float (&f)[3
     }
 }
 
-// Backward epilogue I/O, warp-cooperative and coalesced: a warp's 32 rows x
-// 32 columns bf16 block is moved as 4 instructions of 8 rows x 64 B (instead
-// of 32 row-scattered 16 B accesses per instruction), and transposed through
-// the warp's 2 KB smem staging buffer (64-byte swizzle, conflict-free both
-// ways) to/from the one-row-per-thread layout of tcgen05.ld 32x32b.
-// Lane L, step u covers row u*8 + L/4, 16-byte chunk L%4.
+// Backward epilogue outputs, warp-cooperative and coalesced: a warp's 32 rows
+// x 32 columns bf16 block leaves the one-row-per-thread layout of tcgen05.ld
+// 32x32b through the warp's 2 KB smem staging buffer (64-byte swizzle,
+// conflict-free both ways) as 4 stores of 8 rows x 64 B (instead of 32
+// row-scattered 16 B accesses per instruction).  Lane L, step u covers row
+// u*8 + L/4, 16-byte chunk L%4.
 __device__ __forceinline__ uint32_t stg_off(int r, int c) { return r * 64 + ((c ^ ((r >> 1) & 3)) << 4); }
 
-__device__ __forceinline__ void load_block_coalesced(const __nv_bfloat16* base, long ld, int ncols, int lane,
-                                                     uint4 (&R)[4]) {
-    const int c = lane & 3;
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-        R[u] = c * 8 < ncols ? __ldg(reinterpret_cast<const uint4*>(base + (long)(u * 8 + (lane >> 2)) * ld) + c)
-                             : make_uint4(0, 0, 0, 0);
-}
-// coalesced registers -> this lane's row (4 x 16 B)
-__device__ __forceinline__ void block_to_row(uint8_t* stg, const uint4 (&R)[4], int lane, uint4 (&row)[4]) {
-#pragma unroll
-    for (int u = 0; u < 4; ++u) sts128(stg + stg_off(u * 8 + (lane >> 2), lane & 3), R[u]);
-    __syncwarp();
-#pragma unroll
-    for (int c = 0; c < 4; ++c) row[c] = lds128(stg + stg_off(lane, c));
-    __syncwarp();
-}
 // this lane's row (32 floats -> bf16) -> coalesced global stores
 __device__ __forceinline__ void row_to_global(uint8_t* stg, const float (&h)[32], __nv_bfloat16* base, long ld,
                                               int ncols, int lane) {
@@ -308,13 +291,39 @@ __device__ __forceinline__ void row_to_global(uint8_t* stg, const float (&h)[32]
                 lds128(stg + stg_off(u * 8 + (lane >> 2), c));
     __syncwarp();
 }
-// pre-activation block(s) of one chunk: rows rowbase..+31, columns col0..+31
+// Saved pre-activations (training forward -> backward epilogue, internal to
+// the library) are stored in 32-row x 32-column tiles, lane-major: element
+// (r, c) of tile (R, C) at ((R * CT + C) * 4 + c / 8) * 256 + (r % 32) * 8 + c % 8,
+// CT = ceil(N / 32) tiles per 32-row band.  The epilogue lane that owns row r
+// (tcgen05.ld 32x32b: one row per lane) then writes -- forward -- and reads --
+// backward -- its 32 values of a chunk as 4 x 16 bytes with every warp access
+// one contiguous 512-byte run: no shared-memory transposes (which were ~1/4 of
+// the backward epilogue's instructions).
+__device__ __forceinline__ long pre_tile(long rowbase, int col0, int N) {
+    return ((rowbase >> 5) * ((N + 31) >> 5) + (col0 >> 5)) * 1024;
+}
+__device__ __forceinline__ void store_pre_tiled(__nv_bfloat16* base, long rowbase, int col0, int N, int lane,
+                                                const float (&h)[32]) {
+    uint4* t = reinterpret_cast<uint4*>(base + pre_tile(rowbase, col0, N)) + lane;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+        t[u * 32] = make_uint4(pack_bf16(h[8 * u + 0], h[8 * u + 1]), pack_bf16(h[8 * u + 2], h[8 * u + 3]),
+                               pack_bf16(h[8 * u + 4], h[8 * u + 5]), pack_bf16(h[8 * u + 6], h[8 * u + 7]));
+}
+// this lane's row of a chunk's pre-activations (rows rowbase..+31, columns col0..+31)
 template <int EPI>
 __device__ __forceinline__ void load_pre_chunk(const Params& p, long rowbase, int col0, int lane, uint4 (&A)[4],
                                                uint4 (&B)[4]) {
     if (col0 >= p.N) return;
-    load_block_coalesced(p.pre_a + rowbase * p.N + col0, p.N, p.N - col0, lane, A);
-    if constexpr (EPI == EPI_BWD_SWIGLU) load_block_coalesced(p.pre_b + rowbase * p.N + col0, p.N, p.N - col0, lane, B);
+    const long t = pre_tile(rowbase, col0, p.N);
+    const uint4* ta = reinterpret_cast<const uint4*>(p.pre_a + t) + lane;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) A[u] = __ldg(ta + u * 32);
+    if constexpr (EPI == EPI_BWD_SWIGLU) {
+        const uint4* tb = reinterpret_cast<const uint4*>(p.pre_b + t) + lane;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) B[u] = __ldg(tb + u * 32);
+    }
 }
 
 __device__ __forceinline__ void tl_mark(const Params& p, int i) {
@@ -579,15 +588,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                 // the math, then hit L2 instead of waiting on DRAM (ncu: the
                 // transposes' staging stores stalled on those loads)
 #ifndef OCC_NO_BWD_PF
-                if (colh < p.N) {
-                    const __nv_bfloat16* ra = p.pre_a + (rowbase0 + lane) * p.N + colh;
-                    const __nv_bfloat16* rb = EPI == EPI_BWD_SWIGLU ? p.pre_b + (rowbase0 + lane) * p.N + colh : nullptr;
-#pragma unroll
-                    for (int l = 0; l < (BN / 2) * 2 / 128; ++l)
-                        if (colh + l * 64 < p.N) {
-                            prefetch_l2(ra + l * 64);
-                            if (rb) prefetch_l2(rb + l * 64);
-                        }
+                if (colh < p.N) {  // this warp's chunks: consecutive 2 KB tiles, 128 B per lane each
+                    const long t0 = pre_tile(rowbase0, colh, p.N);
+                    const int ntiles = min(BN / 64, (p.N - colh + 31) / 32);
+                    for (int tt = 0; tt < ntiles; ++tt) {
+                        prefetch_l2(p.pre_a + t0 + tt * 1024 + lane * 64);
+                        if constexpr (EPI == EPI_BWD_SWIGLU) prefetch_l2(p.pre_b + t0 + tt * 1024 + lane * 64);
+                    }
                 }
 #endif
             }
@@ -664,14 +671,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                         if (col0 < F) {  // warp-uniform
                             const int nv = F - col0 < 32 ? F - col0 : 32;
                             float a[32], r0[32];
-                            uint4 rowa[4];
-                            block_to_row(stg, pa_cur, lane, rowa);
-                            unpack_bf16x32(rowa, a);
+                            unpack_bf16x32(pa_cur, a);
                             if constexpr (EPI == EPI_BWD_SWIGLU) {
                                 float b[32], r1[32];
-                                uint4 rowb[4];
-                                block_to_row(stg, pb_cur, lane, rowb);
-                                unpack_bf16x32(rowb, b);
+                                unpack_bf16x32(pb_cur, b);
 #pragma unroll
                                 for (int i = 0; i < 32; ++i) {
                                     const float gm = i < nv ? __uint_as_float(v[i]) : 0.f;
@@ -802,12 +805,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                                 }
                                 // coalesced through the warp's staging buffer (free once
                                 // the previous TMA store has read it)
-                                uint8_t* stg = sC + ((warp - 2) * STG_PER_WARP + stg_n % STG_PER_WARP) * STG_BYTES;
-                                if (lane == 0) bulk_wait_read<STG_PER_WARP - 1>();
-                                __syncwarp();
-                                const long rb = row - lane;
-                                row_to_global(stg, fa, p.save_a + rb * p.N + col0, p.N, p.N - col0, lane);
-                                row_to_global(stg, fb, p.save_b + rb * p.N + col0, p.N, p.N - col0, lane);
+                                store_pre_tiled(p.save_a, row - lane, col0, p.N, lane, fa);
+                                store_pre_tiled(p.save_b, row - lane, col0, p.N, lane, fb);
                             }
 #pragma unroll
                             for (int i = 0; i < 32; ++i)
@@ -817,10 +816,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                                 float fa[32];
 #pragma unroll
                                 for (int i = 0; i < 32; ++i) fa[i] = __uint_as_float(v[cc][i]);
-                                uint8_t* stg = sC + ((warp - 2) * STG_PER_WARP + stg_n % STG_PER_WARP) * STG_BYTES;
-                                if (lane == 0) bulk_wait_read<STG_PER_WARP - 1>();
-                                __syncwarp();
-                                row_to_global(stg, fa, p.save_a + (row - lane) * p.N + col0, p.N, p.N - col0, lane);
+                                store_pre_tiled(p.save_a, row - lane, col0, p.N, lane, fa);
                             }
                             act_dispatch(p.act, [&](auto tag) {
 #pragma unroll
@@ -1203,17 +1199,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 #pragma unroll
                 for (int cc = 0; cc < HALF; ++cc) {
                     const int col0 = nb * ncol + (round * HALF + cc) * 32;
-                    if (p.save_a && col0 < p.N) {  // training: keep a = x w1 (and b = x w3), coalesced
+                    if (p.save_a && col0 < p.N) {  // training: keep a = x w1 (and b = x w3), tiled
                         float fa[32];
-                        if (lane == 0) bulk_wait_read<0>();
-                        __syncwarp();
 #pragma unroll
                         for (int i = 0; i < 32; ++i) fa[i] = __uint_as_float(v[cc][i]);
-                        row_to_global(stg, fa, p.save_a + (row - lane) * p.N + col0, p.N, p.N - col0, lane);
+                        store_pre_tiled(p.save_a, row - lane, col0, p.N, lane, fa);
                         if constexpr (SW) {
 #pragma unroll
                             for (int i = 0; i < 32; ++i) fa[i] = __uint_as_float(g[cc][i]);
-                            row_to_global(stg, fa, p.save_b + (row - lane) * p.N + col0, p.N, p.N - col0, lane);
+                            store_pre_tiled(p.save_b, row - lane, col0, p.N, lane, fa);
                         }
                     }
                     float h[32];
