@@ -213,7 +213,7 @@ struct occ_handle {
     // per-row routing-weight gradients (sent / received)
     DevBuf<__nv_bfloat16> g_in, g_ysrc;
     DevBuf<float> ret_gw, y_gw;
-    TmapBox tmG_k, tmW2o, tmP_k, tmW1o, tmH_mn, tmG_mn, tmX_mn, tmP_mn;
+    TmapBox tmG_k, tmW2o, tmP_k, tmW1o, tmH_mn, tmG_mn, tmX_mn, tmP_mn, tmP_out;
     int bwd_tmaps_q = -1;
     // host-buffer pipeline (occ_forward_host)
     cudaStream_t s_in = nullptr, s_out = nullptr, s_cap = nullptr;
@@ -1951,6 +1951,7 @@ static occ_status ensure_bwd(occ_handle* h) {
     if (h->bwd_tmaps_q != (int)Q) {
         if (!make_tmap_2d(h->tmG_k.bytes, h->g_epd.p, D, Q, 64, 128) ||
             !make_tmap_2d(h->tmP_k.bytes, h->gpre.p, kw, Q, 64, 128) ||
+            !make_tmap_out(h->tmP_out.bytes, h->gpre.p, kw, Q) ||
             !make_tmap_2d(h->tmH_mn.bytes, h->hbuf.p, F, Q, 64, 64) ||
             !make_tmap_2d(h->tmG_mn.bytes, h->g_epd.p, D, Q, 64, 64) ||
             !make_tmap_2d(h->tmX_mn.bytes, h->x_epd.p, D, Q, 64, 64) ||
@@ -2009,6 +2010,7 @@ static void bwd_gemms(occ_handle* h, int NG, const int* widx, float* g_w1, float
     // adjoints and the routing-weight partials fused in the epilogue
     GemmArgs g;
     g.tmap_a = h->tmG_k.bytes;
+    g.tmap_c = h->tmP_out.bytes;  // g_a | g_b leave through smem + TMA stores
     g.tmap_b = h->tmW2o.bytes;
     g.K = D;
     g.N = F;

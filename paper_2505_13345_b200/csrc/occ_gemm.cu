@@ -337,6 +337,25 @@ __device__ __forceinline__ void store_c(const CUtensorMap* tmC, const void* stg,
     if (hint & 2) tma_store_2d_hint(tmC, stg, x, y, l2_policy_evict_first());
     else tma_store_2d(tmC, stg, x, y);
 }
+// This lane's row of a 32 x 32 bf16 block (rows y..y+31, columns x..x+31)
+// out through the warp's 2 KB staging buffer (64-byte swizzle) and one TMA
+// store; waits for the buffer's previous store to have read it.
+__device__ __forceinline__ void row_to_tma(const CUtensorMap* tmC, uint8_t* stg, const float (&h)[32], int x, int y,
+                                           int lane) {
+    if (lane == 0) bulk_wait_read<0>();
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+        sts128(stg + lane * 64 + ((u ^ ((lane >> 1) & 3)) << 4),
+               make_uint4(pack_bf16(h[8 * u + 0], h[8 * u + 1]), pack_bf16(h[8 * u + 2], h[8 * u + 3]),
+                          pack_bf16(h[8 * u + 4], h[8 * u + 5]), pack_bf16(h[8 * u + 6], h[8 * u + 7])));
+    fence_proxy_async();
+    __syncwarp();
+    if (lane == 0) {
+        tma_store_2d(tmC, stg, x, y);
+        bulk_commit();
+    }
+}
 
 template <int EPI, bool WGRAD>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
@@ -685,8 +704,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                                     r0[i] = gh * b[i] * s * (1.0f + a[i] * (1.0f - s));
                                     r1[i] = gh * sa;
                                 }
-                                row_to_global(stg, r0, outb + col0, p.ldo, F - col0, lane);
-                                row_to_global(stg, r1, outb + F + col0, p.ldo, F - col0, lane);
+                                if (p.tma_out) {  // (SwiGLU: F % 128 == 0, whole blocks)
+                                    row_to_tma(&tmC, stg, r0, col0, (int)rowbase, lane);
+                                    row_to_tma(&tmC, stg, r1, F + col0, (int)rowbase, lane);
+                                } else {
+                                    row_to_global(stg, r0, outb + col0, p.ldo, F - col0, lane);
+                                    row_to_global(stg, r1, outb + F + col0, p.ldo, F - col0, lane);
+                                }
                             } else {
                                 act_dispatch(p.act, [&](auto tag) {
                                     constexpr int A = decltype(tag)::value;
@@ -697,7 +721,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
                                         r0[i] = gm * wr * act_grad_t<A>(a[i]);
                                     }
                                 });
-                                row_to_global(stg, r0, outb + col0, p.ldo, F - col0, lane);
+                                // (the map's width is F: a partial last block is clipped)
+                                if (p.tma_out) row_to_tma(&tmC, stg, r0, col0, (int)rowbase, lane);
+                                else row_to_global(stg, r0, outb + col0, p.ldo, F - col0, lane);
                             }
                         }
 #pragma unroll
@@ -1560,7 +1586,8 @@ void launch_grouped_gemm(EpiMode mode, const GemmArgs& a, int num_sms, cudaStrea
     const CUtensorMap& ta = *reinterpret_cast<const CUtensorMap*>(a.tmap_a);
     const CUtensorMap& tb = *reinterpret_cast<const CUtensorMap*>(a.tmap_b);
     static const int tma_store_env = getenv("OCC_GEMM_TMASTORE") ? atoi(getenv("OCC_GEMM_TMASTORE")) : 1;
-    p.tma_out = tma_store_env && a.tmap_c != nullptr && (mode == EPI_ACT_BF16 || mode == EPI_SWIGLU_BF16);
+    p.tma_out = tma_store_env && a.tmap_c != nullptr &&
+                (mode == EPI_ACT_BF16 || mode == EPI_SWIGLU_BF16 || mode == EPI_BWD_ACT || mode == EPI_BWD_SWIGLU);
     const CUtensorMap& tc = p.tma_out ? *reinterpret_cast<const CUtensorMap*>(a.tmap_c) : ta;
     static const int band_override = [] {  // raster experiments (profiles/), not a product knob
         const char* e = getenv("OCC_GEMM_BAND");
