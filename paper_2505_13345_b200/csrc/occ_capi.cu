@@ -1829,6 +1829,21 @@ static occ_status forward_one(occ_handle* h, const void* x, const int32_t* ids, 
     // CommReport counters itself: no memset nodes between route and plan)
     if (!h->in_ep) CUDA_TRY(cudaMemsetAsync(h->err.p, 0, sizeof(int32_t), st));
     if (!h->in_ep) h->ev_recorded = 0;
+    // shared experts (every token, at its source; no exchange) on a second
+    // stream from the start: their dense GEMMs fill the SMs the index chain and
+    // the scatter leave idle and the routed GEMMs' tail waves (the dynamic tile
+    // schedulers of both take tiles as CTAs free up); joined before the combine.
+    // Profiling keeps them in line so the stage times stay separable.
+    static const int shared_async_env = getenv("OCC_SHARED_ASYNC") ? atoi(getenv("OCC_SHARED_ASYNC")) : 1;
+    const bool shared = h->n_shared > 0;
+    const bool shared_async = shared && shared_async_env && !h->profiling && h->s_aux && h->ev_fork && h->ev_join;
+    if (shared_async) {
+        CUDA_TRY(cudaEventRecord(h->ev_fork, st));
+        CUDA_TRY(cudaStreamWaitEvent(h->s_aux, h->ev_fork, 0));
+        s = run_shared(h, reinterpret_cast<const __nv_bfloat16*>(x), n, h->s_aux);
+        if (s != OCC_OK) return s;
+        CUDA_TRY(cudaEventRecord(h->ev_join, h->s_aux));
+    }
     mark(h, ST_PLAN, st);
     const bool gathered = h->gather_a && !h->training;
     bool fused = h->fused_plan && dedup && !h->gather_a && h->fp_ws.p && fused_plan_supported(nd, h->E, k);
@@ -1898,9 +1913,7 @@ static occ_status forward_one(occ_handle* h, const void* x, const int32_t* ids, 
     mark(h, ST_GEMM2, st);
     // 5. grouped GEMM-2 (per-expert products, fp32)
     launch_gemm2(h, G * P, st);
-    // shared experts (every token, at its source; no exchange)
-    const bool shared = h->n_shared > 0;
-    if (shared) {
+    if (shared && !shared_async) {
         mark(h, ST_SHARED, st);
         s = run_shared(h, reinterpret_cast<const __nv_bfloat16*>(x), n, st);
         if (s != OCC_OK) return s;
@@ -1908,6 +1921,7 @@ static occ_status forward_one(occ_handle* h, const void* x, const int32_t* ids, 
     // 6+7. intra-device partial combine (placement order) -> bf16 return
     // payload -> combine over devices ascending, fused on one GPU
     mark(h, ST_COMBINE, st);
+    if (shared_async) CUDA_TRY(cudaStreamWaitEvent(st, h->ev_join, 0));
     launch_combine_fused(n, nd, k, P, dedup, D, h->mask.p, h->tok_row.p, h->row_epd.p, h->y16.p,
                          shared ? h->ys.p : nullptr, reinterpret_cast<__nv_bfloat16*>(out), st);
     mark(h, kStages, st);
