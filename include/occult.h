@@ -22,7 +22,9 @@
  * EP devices on one GPU exactly as the reference simulates them in one
  * process (pipeline.cpp:393-466); with world_size == N_d each rank is one
  * EP device and the two exchanges run over NCCL.  Handles are not
- * thread-safe.
+ * thread-safe, and one handle's work must be ordered on one stream at a time
+ * (its workspaces -- including the grouped GEMMs' tile counters -- are
+ * reused by every call; use one handle per concurrent stream).
  */
 #ifndef OCCULT_H
 #define OCCULT_H
